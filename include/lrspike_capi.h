@@ -1,0 +1,204 @@
+/* lrspike C-ABI -- the drop-in boundary of the B200-native LR-SPIKE solver.
+ *
+ * Plain C types only (no torch, no CUDA types in signatures).  Implemented by
+ * liblrspike_cuda.so (CUDA sm_100a kernels).  There is no CPU fallback: every
+ * numerical operation below runs on the GPU; the host side only validates,
+ * orchestrates launches and runs the Krylov scalar recurrences.
+ *
+ * Each entry point replaces one operation of the reference's C++ interface
+ * (reference paths relative to /root/reference):
+ *   lrs_mat_upload_csr      CsrMatrix + validate()      proj/core/include/lrspike/matrix.hpp:22-48,
+ *                                                        proj/core/src/matrix.cpp:21-37
+ *   lrs_spmv                spmv / spmv_accumulate      matrix.hpp:51-54, matrix.cpp:121-136
+ *   lrs_mat_band_metrics    band_metrics                matrix.hpp:58-70, matrix.cpp:138-158
+ *   lrs_make_layout         make_layout
+ *   lrs_factorize           factorize (extract_blocks, factorize_block, randomized_spike_svd,
+ *                           build_truncated_precond)    SPEC.md:476-484 (:180, :217, :286, :367)
+ *   lrs_solve_block         solve_block / solve_block_adjoint
+ *   lrs_apply_precond       apply_precond_T
+ *   lrs_apply_block_jacobi  apply_block_jacobi
+ *   lrs_solve               solve + bicgstab / GMRES(m) SPEC.md:520-528, :421-429 (GMRES: SURVEY D1)
+ *   lrs_last_error          the exception taxonomy      proj/core/include/lrspike/errors.hpp:11-94
+ *
+ * Memory: pointers tagged LRS_MEM_HOST are copied by the library (the caller
+ * keeps ownership); LRS_MEM_DEVICE pointers are CUDA device pointers on the
+ * context's device and are used in place.  Dense blocks are column-major with
+ * leading dimension ld >= rows.
+ *
+ * Threading: one host thread per lrs_ctx at a time.  Factor
+ * handles are immutable after lrs_factorize except for the
+ * communication ledger they accumulate.
+ */
+#ifndef LRSPIKE_CAPI_H
+#define LRSPIKE_CAPI_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LRS_API __attribute__((visibility("default")))
+
+typedef struct lrs_ctx lrs_ctx;
+typedef struct lrs_mat lrs_mat;
+typedef struct lrs_fact lrs_fact;
+
+/* One status per lrspike::Error subclass (errors.hpp) plus runtime codes. */
+typedef enum lrs_status {
+  LRS_OK = 0,
+  LRS_ERR_PARSE = 1,                      /* ParseError(line)                 errors.hpp:17 */
+  LRS_ERR_UNSUPPORTED_FIELD = 2,          /* UnsupportedFieldError            errors.hpp:30 */
+  LRS_ERR_DIMENSION = 3,                  /* DimensionError                   errors.hpp:36 */
+  LRS_ERR_SINGULAR_SCALING = 4,           /* SingularScalingError(row)        errors.hpp:41 */
+  LRS_ERR_LAYOUT = 5,                     /* LayoutError                      errors.hpp:53 */
+  LRS_ERR_NOT_BLOCK_TRIDIAGONAL = 6,      /* NotBlockTridiagonalError(r,c)    errors.hpp:59 */
+  LRS_ERR_SINGULAR_BLOCK = 7,             /* SingularBlockError(column)       errors.hpp:73 */
+  LRS_ERR_PARAMETER = 8,                  /* ParameterError                   errors.hpp:83 */
+  LRS_ERR_ILL_CONDITIONED_INTERFACE = 9,  /* IllConditionedInterfaceError     errors.hpp:86 */
+  LRS_ERR_BREAKDOWN = 10,                 /* BiCGStab stagnation, SPEC.md:425 (partial result kept) */
+  LRS_ERR_CUDA = 11,
+  LRS_ERR_OOM = 12,
+  LRS_ERR_NCCL = 13,
+  LRS_ERR_NOT_IMPLEMENTED = 14            /* e.g. a block that needs row interchanges */
+} lrs_status;
+
+typedef enum lrs_scalar { LRS_F64 = 0, LRS_C128 = 1 } lrs_scalar;
+typedef enum lrs_mem { LRS_MEM_HOST = 0, LRS_MEM_DEVICE = 1 } lrs_mem;
+typedef enum lrs_variant { LRS_VARIANT_T = 0, LRS_VARIANT_BJ = 1 } lrs_variant;
+typedef enum lrs_method { LRS_GMRES = 0, LRS_BICGSTAB = 1 } lrs_method;
+typedef enum lrs_side { LRS_SIDE_T = 0, LRS_SIDE_W = 1 } lrs_side;
+
+/* Ledger stages. */
+enum { LRS_STAGE_REDUCED_MATVEC = 0, LRS_STAGE_PRECOND_APPLY = 1, LRS_STAGE_RECOVERY = 2 };
+
+/* SolverConfig. */
+typedef struct lrs_solver_cfg {
+  int32_t variant;    /* lrs_variant */
+  int32_t passes;     /* randomized SVD passes, >= 2 (default 2) */
+  int64_t p;          /* partitions */
+  int64_t k;          /* coupling half-bandwidth; <= 0 -> band_metrics(A).k */
+  int64_t n_svd;      /* retained rank r */
+  int64_t oversample; /* < 0 -> ceil(n_svd / 2) */
+  uint64_t seed;      /* Omega streams (seed, partition, side) */
+} lrs_solver_cfg;
+
+/* IterConfig, SPEC.md:411-414 (+ method, GMRES restart). */
+typedef struct lrs_iter_cfg {
+  int32_t method;      /* lrs_method */
+  int32_t restart;     /* GMRES(m) */
+  double tol;          /* relative residual ||b-Ax||/||b|| per column */
+  int64_t max_iters;
+  double breakdown_eps; /* default 1e-30 */
+  const void* x0;      /* optional initial guess, same memory kind / ld as b; NULL -> 0 */
+} lrs_iter_cfg;
+
+/* SolveReport, plus the CommLedger and timings. */
+typedef struct lrs_report {
+  int32_t converged;
+  int32_t breakdown;
+  double iterations;            /* max over columns; BiCGStab has half-iteration resolution */
+  int64_t precond_applications; /* batched applications */
+  int64_t matvecs;
+  double residual_final;        /* max over columns of ||b - A x|| / ||b|| */
+  int64_t comm_messages[3];     /* per stage, this solve */
+  int64_t comm_scalars[3];
+  double t_solve;               /* seconds, CUDA events on the context stream */
+  uint64_t seed;
+  double* history;              /* caller buffer (may be NULL) */
+  int64_t history_cap;
+  int64_t history_len;          /* entries written (<= cap); total produced in history_total */
+  int64_t history_total;
+} lrs_report;
+
+/* Read-only facts about a factorization. */
+typedef struct lrs_fact_info {
+  int64_t n, p, k, n_svd, l;    /* l = n_svd + oversample */
+  int64_t kl, ku;               /* band of the diagonal blocks */
+  int64_t nb;                   /* tile size */
+  int64_t wl, wu;               /* band width in tiles */
+  int64_t factor_bytes;         /* device bytes of the tiled band factors */
+  int64_t lu_flops;             /* algorithmic no-fill LU flops */
+  int64_t apply_bytes;          /* algorithmic bytes per apply with n_rhs = 1 */
+  int32_t rank_collapsed;       /* some spike lost rank */
+  int32_t variant;
+  double t_factorize;           /* seconds */
+  double t_lu, t_spikes, t_precond; /* stage split of t_factorize */
+  double max_interface_cond;
+} lrs_fact_info;
+
+typedef struct lrs_error_info {
+  int32_t status;
+  char message[512];
+  int64_t line, row, col, column, interface_index;
+  double cond_estimate;
+} lrs_error_info;
+
+/* ---- context ---------------------------------------------------------------------- */
+/* stream: an existing cudaStream_t (e.g. torch's current stream) or NULL to create one. */
+LRS_API lrs_status lrs_ctx_create(int device, void* stream, lrs_ctx** out);
+LRS_API void lrs_ctx_destroy(lrs_ctx* ctx);
+LRS_API void* lrs_ctx_stream(lrs_ctx* ctx);
+LRS_API lrs_status lrs_last_error(lrs_ctx* ctx, lrs_error_info* info);
+LRS_API const char* lrs_status_string(lrs_status s);
+/* Number of kernel launches issued by this context so far (bench accounting). */
+LRS_API int64_t lrs_ctx_launch_count(lrs_ctx* ctx);
+LRS_API lrs_status lrs_ctx_synchronize(lrs_ctx* ctx);
+
+/* ---- matrix ----------------------------------------------------------------------- */
+LRS_API lrs_status lrs_mat_upload_csr(lrs_ctx* ctx, int64_t n, int64_t nnz, const int64_t* row_ptr,
+                                      const int64_t* col_idx, const void* values, int32_t scalar,
+                                      int32_t mem, lrs_mat** out);
+LRS_API void lrs_mat_destroy(lrs_mat* m);
+LRS_API lrs_status lrs_mat_band_metrics(lrs_mat* m, int64_t* ku, int64_t* kl, int64_t* k,
+                                        double* diag_weight, double* band_density);
+/* y = A x (accumulate = 0) or y += A x (accumulate = 1); n_rhs columns. */
+LRS_API lrs_status lrs_spmv(lrs_mat* m, const void* x, int64_t ldx, void* y, int64_t ldy,
+                            int64_t n_rhs, int32_t accumulate, int32_t mem);
+
+/* ---- partition -------------------------------------------------------------------- */
+LRS_API lrs_status lrs_make_layout(int64_t n, int64_t p, int64_t k, int64_t* sizes_out);
+
+/* ---- setup ------------------------------------------------------------------------ */
+LRS_API lrs_status lrs_factorize(lrs_ctx* ctx, lrs_mat* a, const lrs_solver_cfg* cfg,
+                                 lrs_fact** out);
+LRS_API void lrs_fact_destroy(lrs_fact* f);
+LRS_API lrs_status lrs_fact_get_info(lrs_fact* f, lrs_fact_info* info);
+/* Partition sizes / offsets (p entries each). */
+LRS_API lrs_status lrs_fact_get_layout(lrs_fact* f, int64_t* sizes, int64_t* offsets);
+/* Low-rank spike of partition i, side T (i < p-1) or W (i > 0): u n_i x r (ld n_i),
+ * sigma r, v r x k (ld r).  Host buffers; any may be NULL. */
+LRS_API lrs_status lrs_fact_get_spike(lrs_fact* f, int64_t partition, int32_t side, double* u,
+                                      double* sigma, double* v);
+/* Tiled band factor of partition i as stored on the device (tests / inspection):
+ * tiles[T_i][wl+wu+1][nb*nb] column-major nb x nb tiles; the diagonal tile holds
+ * inv(L_ii) strictly below and inv(U_ii) on/above the diagonal. */
+LRS_API lrs_status lrs_fact_get_tiles(lrs_fact* f, int64_t partition, double* host_out,
+                                      int64_t capacity_doubles, int64_t* needed_doubles);
+/* Ledger totals since factorization. */
+LRS_API lrs_status lrs_fact_get_ledger(lrs_fact* f, int64_t messages[3], int64_t scalars[3]);
+
+/* ---- apply ------------------------------------------------------------------------ */
+LRS_API lrs_status lrs_solve_block(lrs_fact* f, int64_t partition, const void* rhs, int64_t ld_rhs,
+                                   void* x, int64_t ld_x, int64_t n_rhs, int32_t adjoint,
+                                   int32_t mem);
+LRS_API lrs_status lrs_apply_precond(lrs_fact* f, const void* in, int64_t ld_in, void* out,
+                                     int64_t ld_out, int64_t n_rhs, int32_t mem);
+LRS_API lrs_status lrs_apply_block_jacobi(lrs_fact* f, const void* in, int64_t ld_in, void* out,
+                                          int64_t ld_out, int64_t n_rhs, int32_t mem);
+
+/* ---- solve ------------------------------------------------------------------------ */
+LRS_API lrs_status lrs_solve(lrs_fact* f, lrs_mat* a, const void* b, int64_t ldb, void* x,
+                             int64_t ldx, int64_t n_rhs, const lrs_iter_cfg* cfg,
+                             lrs_report* report, int32_t mem);
+
+/* ---- microbenchmarks used by bench.py for the roofline denominators --------------- */
+/* FP64 DMMA peak: runs a register-resident mma.sync f64 loop, returns TFLOP/s. */
+LRS_API lrs_status lrs_bench_dmma_peak(lrs_ctx* ctx, double* tflops);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LRSPIKE_CAPI_H */

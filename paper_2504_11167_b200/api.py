@@ -1,0 +1,531 @@
+"""Python mirror of the lrspike operations over the C-ABI (include/lrspike_capi.h).
+
+Names, argument meaning and error behaviour follow the reference interface:
+``CsrMatrix``/``spmv``/``band_metrics`` (proj/core/include/lrspike/matrix.hpp),
+the exception taxonomy (proj/core/include/lrspike/errors.hpp:11-94), and the
+SPEC operations make_layout / factorize / solve_block / apply_precond_T /
+apply_block_jacobi / bicgstab / solve.  GMRES(m) is the one
+added method.
+
+Every call goes to liblrspike_cuda.so; there is no CPU fallback: importing this
+module on a machine without the built library raises, and any operation on a
+machine without a GPU fails with CudaError.
+
+Arrays: numpy arrays are host buffers (copied by the library); torch CUDA
+tensors (or any object with ``data_ptr()`` and ``is_cuda``) are used in place
+on the device.  Blocks are column-major (Fortran order), shape (n, n_rhs).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIBPATH = os.path.join(_HERE, "liblrspike_cuda.so")
+
+LRS_OK = 0
+F64, C128 = 0, 1
+MEM_HOST, MEM_DEVICE = 0, 1
+VARIANT_T, VARIANT_BJ = 0, 1
+GMRES, BICGSTAB = 0, 1
+SIDE_T, SIDE_W = 0, 1
+STAGES = ("reduced-matvec", "precond-apply", "recovery")
+
+i64, f64, i32, u64 = ctypes.c_int64, ctypes.c_double, ctypes.c_int32, ctypes.c_uint64
+vp = ctypes.c_void_p
+
+
+class SolverCfgC(ctypes.Structure):
+    _fields_ = [("variant", i32), ("passes", i32), ("p", i64), ("k", i64), ("n_svd", i64),
+                ("oversample", i64), ("seed", u64)]
+
+
+class IterCfgC(ctypes.Structure):
+    _fields_ = [("method", i32), ("restart", i32), ("tol", f64), ("max_iters", i64),
+                ("breakdown_eps", f64), ("x0", vp)]
+
+
+class ReportC(ctypes.Structure):
+    _fields_ = [("converged", i32), ("breakdown", i32), ("iterations", f64),
+                ("precond_applications", i64), ("matvecs", i64), ("residual_final", f64),
+                ("comm_messages", i64 * 3), ("comm_scalars", i64 * 3), ("t_solve", f64),
+                ("seed", u64), ("history", ctypes.POINTER(f64)), ("history_cap", i64),
+                ("history_len", i64), ("history_total", i64)]
+
+
+class FactInfoC(ctypes.Structure):
+    _fields_ = [("n", i64), ("p", i64), ("k", i64), ("n_svd", i64), ("l", i64), ("kl", i64),
+                ("ku", i64), ("nb", i64), ("wl", i64), ("wu", i64), ("factor_bytes", i64),
+                ("lu_flops", i64), ("apply_bytes", i64), ("rank_collapsed", i32),
+                ("variant", i32), ("t_factorize", f64), ("t_lu", f64), ("t_spikes", f64),
+                ("t_precond", f64), ("max_interface_cond", f64)]
+
+
+class ErrorInfoC(ctypes.Structure):
+    _fields_ = [("status", i32), ("message", ctypes.c_char * 512), ("line", i64), ("row", i64),
+                ("col", i64), ("column", i64), ("interface_index", i64),
+                ("cond_estimate", f64)]
+
+
+# ---- exceptions: errors.hpp:11-94 -------------------------------------------------------
+class Error(RuntimeError):
+    """lrspike::Error (errors.hpp:11)."""
+
+
+class ParseError(Error):
+    def __init__(self, msg, line=-1):
+        super().__init__(msg)
+        self.line = line
+
+
+class UnsupportedFieldError(Error):
+    pass
+
+
+class DimensionError(Error):
+    pass
+
+
+class SingularScalingError(Error):
+    def __init__(self, msg, row=-1):
+        super().__init__(msg)
+        self.row = row
+
+
+class LayoutError(Error):
+    pass
+
+
+class NotBlockTridiagonalError(Error):
+    def __init__(self, msg, row=-1, col=-1):
+        super().__init__(msg)
+        self.row, self.col = row, col
+
+
+class SingularBlockError(Error):
+    def __init__(self, msg, column=-1):
+        super().__init__(msg)
+        self.column = column
+
+
+class ParameterError(Error):
+    pass
+
+
+class IllConditionedInterfaceError(Error):
+    def __init__(self, msg, interface_index=-1, cond_estimate=0.0):
+        super().__init__(msg)
+        self.interface_index, self.cond_estimate = interface_index, cond_estimate
+
+
+class BreakdownError(Error):
+    """BiCGStab stagnation; carries the partial x and the report."""
+
+    def __init__(self, msg, x=None, report=None):
+        super().__init__(msg)
+        self.x, self.report = x, report
+
+
+class CudaError(Error):
+    pass
+
+
+class OutOfMemoryError(Error):
+    pass
+
+
+class NotImplementedOnGpu(Error):
+    pass
+
+
+_lib = None
+
+
+def lib():
+    """Load liblrspike_cuda.so; raise loudly if it was not built (no CPU fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(_LIBPATH):
+        raise ImportError(f"{_LIBPATH} is missing: build it with `make` (__graft_entry__.build())")
+    L = ctypes.CDLL(_LIBPATH)
+    P = ctypes.POINTER
+    sig = {
+        "lrs_ctx_create": (i32, [ctypes.c_int, vp, P(vp)]),
+        "lrs_ctx_destroy": (None, [vp]),
+        "lrs_ctx_stream": (vp, [vp]),
+        "lrs_ctx_launch_count": (i64, [vp]),
+        "lrs_ctx_synchronize": (i32, [vp]),
+        "lrs_last_error": (i32, [vp, P(ErrorInfoC)]),
+        "lrs_status_string": (ctypes.c_char_p, [i32]),
+        "lrs_mat_upload_csr": (i32, [vp, i64, i64, vp, vp, vp, i32, i32, P(vp)]),
+        "lrs_mat_destroy": (None, [vp]),
+        "lrs_mat_band_metrics": (i32, [vp, P(i64), P(i64), P(i64), P(f64), P(f64)]),
+        "lrs_spmv": (i32, [vp, vp, i64, vp, i64, i64, i32, i32]),
+        "lrs_make_layout": (i32, [i64, i64, i64, P(i64)]),
+        "lrs_factorize": (i32, [vp, vp, P(SolverCfgC), P(vp)]),
+        "lrs_fact_destroy": (None, [vp]),
+        "lrs_fact_get_info": (i32, [vp, P(FactInfoC)]),
+        "lrs_fact_get_layout": (i32, [vp, vp, vp]),
+        "lrs_fact_get_spike": (i32, [vp, i64, i32, vp, vp, vp]),
+        "lrs_fact_get_tiles": (i32, [vp, i64, vp, i64, P(i64)]),
+        "lrs_fact_get_ledger": (i32, [vp, vp, vp]),
+        "lrs_solve_block": (i32, [vp, i64, vp, i64, vp, i64, i64, i32, i32]),
+        "lrs_apply_precond": (i32, [vp, vp, i64, vp, i64, i64, i32]),
+        "lrs_apply_block_jacobi": (i32, [vp, vp, i64, vp, i64, i64, i32]),
+        "lrs_solve": (i32, [vp, vp, vp, i64, vp, i64, i64, P(IterCfgC), P(ReportC), i32]),
+        "lrs_bench_dmma_peak": (i32, [vp, P(f64)]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(L, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = L
+    return L
+
+
+_EXC = {1: ParseError, 2: UnsupportedFieldError, 3: DimensionError, 4: SingularScalingError,
+        5: LayoutError, 6: NotBlockTridiagonalError, 7: SingularBlockError, 8: ParameterError,
+        9: IllConditionedInterfaceError, 10: BreakdownError, 11: CudaError, 12: OutOfMemoryError,
+        13: CudaError, 14: NotImplementedOnGpu}
+
+
+def _raise(status: int, ctx_handle=None):
+    info = ErrorInfoC()
+    lib().lrs_last_error(ctx_handle, ctypes.byref(info))
+    msg = info.message.decode(errors="replace") or lib().lrs_status_string(status).decode()
+    cls = _EXC.get(status, Error)
+    if cls is NotBlockTridiagonalError:
+        raise cls(msg, info.row, info.col)
+    if cls is SingularBlockError:
+        raise cls(msg, info.column)
+    if cls is IllConditionedInterfaceError:
+        raise cls(msg, info.interface_index, info.cond_estimate)
+    if cls is ParseError:
+        raise cls(msg, info.line)
+    if cls is SingularScalingError:
+        raise cls(msg, info.row)
+    raise cls(msg)
+
+
+def _check(status, ctx_handle=None):
+    if status != LRS_OK:
+        _raise(status, ctx_handle)
+
+
+def _is_device(a) -> bool:
+    return bool(getattr(a, "is_cuda", False))
+
+
+def _buf(a, n_rows):
+    """(pointer, ld, mem, ncols) of a column-major block (numpy F-order or torch CUDA)."""
+    if _is_device(a):
+        if a.dim() == 1:
+            return a.data_ptr(), n_rows, MEM_DEVICE, 1
+        # torch: column-major blocks are stored as (n_rhs, n) row-major == (n, n_rhs) F-order
+        if a.stride(0) == 1:
+            return a.data_ptr(), a.stride(1), MEM_DEVICE, a.shape[1]
+        raise DimensionError("device block must be column-major (stride(0) == 1)")
+    arr = np.asarray(a)
+    if arr.ndim == 1:
+        arr = arr.reshape(-1, 1)
+    if not (arr.flags.f_contiguous and arr.dtype == np.float64):
+        raise DimensionError("host block must be float64 Fortran-ordered")
+    return arr.ctypes.data, arr.shape[0], MEM_HOST, arr.shape[1]
+
+
+class Context:
+    """One device + one stream (lrs_ctx).  ``stream`` may be a torch stream handle."""
+
+    def __init__(self, device: int = 0, stream: int | None = None):
+        h = vp()
+        _check(lib().lrs_ctx_create(device, stream, ctypes.byref(h)))
+        self.h = h
+
+    def close(self):
+        if self.h:
+            lib().lrs_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def stream(self) -> int:
+        return lib().lrs_ctx_stream(self.h) or 0
+
+    @property
+    def launches(self) -> int:
+        return lib().lrs_ctx_launch_count(self.h)
+
+    def synchronize(self):
+        _check(lib().lrs_ctx_synchronize(self.h), self.h)
+
+    def dmma_peak_tflops(self) -> float:
+        out = f64()
+        _check(lib().lrs_bench_dmma_peak(self.h, ctypes.byref(out)), self.h)
+        return out.value
+
+
+@dataclass
+class BandMetrics:
+    """matrix.hpp:58-70."""
+
+    ku: int
+    kl: int
+    k: int
+    diag_weight: float
+    band_density: float
+
+
+class CsrMatrix:
+    """Device-resident CsrMatrix (matrix.hpp:22-48).  ``validate()`` semantics are
+    enforced at upload (DimensionError, matrix.cpp:21-37)."""
+
+    def __init__(self, ctx: Context, n, row_ptr, col_idx, values):
+        self.ctx = ctx
+        self.n = int(n)
+        rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
+        ci = np.ascontiguousarray(col_idx, dtype=np.int64)
+        va = np.ascontiguousarray(values, dtype=np.float64)
+        if rp.shape[0] != self.n + 1:
+            raise DimensionError("row_ptr length must be n_rows + 1")
+        if ci.shape[0] != va.shape[0]:
+            raise DimensionError("col_idx/values length mismatch")
+        h = vp()
+        _check(lib().lrs_mat_upload_csr(ctx.h, self.n, va.shape[0], rp.ctypes.data, ci.ctypes.data,
+                                        va.ctypes.data, F64, MEM_HOST, ctypes.byref(h)), ctx.h)
+        self.h = h
+        self.nnz = int(va.shape[0])
+
+    @classmethod
+    def from_csr(cls, ctx, csr):
+        return cls(ctx, csr.n, csr.row_ptr, csr.col_idx, csr.values)
+
+    def __del__(self):
+        try:
+            if self.h:
+                lib().lrs_mat_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+    def band_metrics(self) -> BandMetrics:
+        ku, kl, k, dw, bd = i64(), i64(), i64(), f64(), f64()
+        _check(lib().lrs_mat_band_metrics(self.h, ctypes.byref(ku), ctypes.byref(kl),
+                                          ctypes.byref(k), ctypes.byref(dw), ctypes.byref(bd)))
+        return BandMetrics(ku.value, kl.value, k.value, dw.value, bd.value)
+
+    def spmv(self, X, out=None, accumulate=False):
+        """matrix.cpp:121-136: returns A X (or out += A X)."""
+        px, ldx, mem, nc = _buf(X, self.n)
+        if out is None:
+            if mem == MEM_DEVICE:
+                import torch
+
+                out = torch.zeros((nc, self.n), dtype=torch.float64, device=X.device).t()
+            else:
+                out = np.zeros((self.n, nc), order="F")
+        py, ldy, memy, _ = _buf(out, self.n)
+        if memy != mem:
+            raise DimensionError("x and y must live in the same memory")
+        _check(lib().lrs_spmv(self.h, px, ldx, py, ldy, nc, 1 if accumulate else 0, mem),
+               self.ctx.h)
+        return out
+
+
+def band_metrics(A: CsrMatrix) -> BandMetrics:
+    return A.band_metrics()
+
+
+def make_layout(n: int, p: int, k: int) -> list:
+    """SPEC.md:171-179."""
+    sizes = (i64 * max(p, 1))()
+    _check(lib().lrs_make_layout(n, p, k, sizes))
+    return list(sizes)
+
+
+@dataclass
+class SolverConfig:
+    """SPEC.md:470-473 (variant "T" = LR-SPIKE-T, "BJ" = Block Jacobi)."""
+
+    variant: str = "T"
+    p: int = 4
+    k: int | None = None
+    n_svd: int = 8
+    oversample: int | None = None
+    passes: int = 2
+    seed: int = 0
+
+    def c(self):
+        return SolverCfgC(VARIANT_T if self.variant == "T" else VARIANT_BJ, self.passes, self.p,
+                          self.k or 0, self.n_svd,
+                          -1 if self.oversample is None else self.oversample, self.seed)
+
+
+@dataclass
+class IterConfig:
+    """SPEC.md:411-414 (+ method and GMRES restart)."""
+
+    tol: float = 1e-8
+    max_iters: int = 1000
+    breakdown_eps: float = 1e-30
+    initial_guess: object = None
+    method: str = "bicgstab"
+    restart: int = 30
+
+
+@dataclass
+class SolveReport:
+    """SPEC.md:415-419 + CommLedger."""
+
+    converged: bool
+    iterations: float
+    residual_history: list
+    precond_applications: int
+    matvecs: int
+    residual_final: float
+    comm: dict
+    seed: int
+    wall_time: float
+    breakdown: bool
+
+
+class SpikeFactorization:
+    """factorize result; immutable, reusable across solves."""
+
+    def __init__(self, ctx: Context, A: CsrMatrix, cfg: SolverConfig):
+        self.ctx, self.A, self.cfg = ctx, A, cfg
+        h = vp()
+        c = cfg.c()
+        _check(lib().lrs_factorize(ctx.h, A.h, ctypes.byref(c), ctypes.byref(h)), ctx.h)
+        self.h = h
+        inf = FactInfoC()
+        _check(lib().lrs_fact_get_info(h, ctypes.byref(inf)))
+        self.info = {f: getattr(inf, f) for f, _ in FactInfoC._fields_}
+        P = self.info["p"]
+        sz, of = (i64 * P)(), (i64 * P)()
+        _check(lib().lrs_fact_get_layout(h, sz, of))
+        self.sizes, self.offsets = list(sz), list(of)
+
+    def __del__(self):
+        try:
+            if self.h:
+                lib().lrs_fact_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+    @property
+    def n_svd(self) -> int:
+        return self.info["n_svd"]
+
+    def _apply(self, fn, f, out):
+        pin, ldi, mem, nc = _buf(f, self.A.n)
+        if out is None:
+            if mem == MEM_DEVICE:
+                import torch
+
+                out = torch.empty((nc, self.A.n), dtype=torch.float64, device=f.device).t()
+            else:
+                out = np.empty((self.A.n, nc), order="F")
+        po, ldo, memo, _ = _buf(out, self.A.n)
+        if memo != mem:
+            raise DimensionError("in and out must live in the same memory")
+        _check(fn(self.h, pin, ldi, po, ldo, nc, mem), self.ctx.h)
+        return out
+
+    def apply_precond_T(self, f, out=None):
+        """SPEC.md:485-493 (Block Jacobi if the factorization has n_svd = 0)."""
+        return self._apply(lib().lrs_apply_precond, f, out)
+
+    def apply_block_jacobi(self, f, out=None):
+        """SPEC.md:512-519."""
+        return self._apply(lib().lrs_apply_block_jacobi, f, out)
+
+    def solve_block(self, i: int, R, adjoint: bool = False):
+        """SPEC.md:226-241 on partition i (host arrays)."""
+        R = np.asfortranarray(np.asarray(R, dtype=np.float64).reshape(self.sizes[i], -1))
+        X = np.empty_like(R, order="F")
+        _check(lib().lrs_solve_block(self.h, i, R.ctypes.data, R.shape[0], X.ctypes.data,
+                                     X.shape[0], R.shape[1], 1 if adjoint else 0, MEM_HOST),
+               self.ctx.h)
+        return X
+
+    def solve_block_adjoint(self, i: int, R):
+        return self.solve_block(i, R, True)
+
+    def spike(self, i: int, side: int):
+        """(u n_i x r, sigma r, v r x k) of LowRankSpike T_i / W_i."""
+        r, k, ni = self.n_svd, self.info["k"], self.sizes[i]
+        u = np.empty((ni, r), order="F")
+        s = np.empty(r)
+        v = np.empty((r, k), order="F")
+        _check(lib().lrs_fact_get_spike(self.h, i, side, u.ctypes.data, s.ctypes.data,
+                                        v.ctypes.data), self.ctx.h)
+        return u, s, v
+
+    def tiles(self, i: int) -> np.ndarray:
+        need = i64()
+        _check(lib().lrs_fact_get_tiles(self.h, i, None, 0, ctypes.byref(need)), self.ctx.h)
+        nb = self.info["nb"]
+        W = self.info["wl"] + self.info["wu"] + 1
+        out = np.empty(need.value)
+        _check(lib().lrs_fact_get_tiles(self.h, i, out.ctypes.data, need.value,
+                                        ctypes.byref(need)), self.ctx.h)
+        return out.reshape(-1, W, nb, nb).transpose(0, 1, 3, 2)  # [I][J-slot][row][col]
+
+    def ledger(self) -> dict:
+        m, s = (i64 * 3)(), (i64 * 3)()
+        _check(lib().lrs_fact_get_ledger(self.h, m, s))
+        return {STAGES[i]: (m[i], s[i]) for i in range(3)}
+
+
+def factorize(ctx: Context, A: CsrMatrix, cfg: SolverConfig) -> SpikeFactorization:
+    return SpikeFactorization(ctx, A, cfg)
+
+
+def solve(A: CsrMatrix, f, cfg: SolverConfig | None = None, it: IterConfig | None = None,
+          F: SpikeFactorization | None = None, x_out=None, history_cap: int = 4096):
+    """factorize (or reuse F) and run the outer Krylov method.
+    Returns (x, SolveReport, F).  Non-convergence is reported, not raised."""
+    it = it or IterConfig()
+    if F is None:
+        F = SpikeFactorization(A.ctx, A, cfg or SolverConfig())
+    pb, ldb, mem, nc = _buf(f, A.n)
+    if x_out is None:
+        if mem == MEM_DEVICE:
+            import torch
+
+            x_out = torch.empty((nc, A.n), dtype=torch.float64, device=f.device).t()
+        else:
+            x_out = np.empty((A.n, nc), order="F")
+    px, ldx, memx, _ = _buf(x_out, A.n)
+    x0p = None
+    if it.initial_guess is not None:
+        x0p, ldx0, mem0, _ = _buf(it.initial_guess, A.n)
+        if mem0 != mem or ldx0 != ldx:
+            raise DimensionError("initial guess must match x's memory kind and layout")
+    ic = IterCfgC(GMRES if it.method == "gmres" else BICGSTAB, it.restart, it.tol, it.max_iters,
+                  it.breakdown_eps, x0p)
+    hist = (f64 * history_cap)()
+    rep = ReportC()
+    rep.history = ctypes.cast(hist, ctypes.POINTER(f64))
+    rep.history_cap = history_cap
+    st = lib().lrs_solve(F.h, A.h, pb, ldb, px, ldx, nc, ctypes.byref(ic), ctypes.byref(rep), mem)
+    report = SolveReport(bool(rep.converged), rep.iterations, list(hist[:rep.history_len]),
+                         rep.precond_applications, rep.matvecs, rep.residual_final,
+                         {STAGES[i]: (rep.comm_messages[i], rep.comm_scalars[i]) for i in range(3)},
+                         rep.seed, rep.t_solve, bool(rep.breakdown))
+    if st == 10:
+        info = ErrorInfoC()
+        lib().lrs_last_error(A.ctx.h, ctypes.byref(info))
+        raise BreakdownError(info.message.decode(), x_out, report)
+    _check(st, A.ctx.h)
+    return x_out, report, F

@@ -1,0 +1,367 @@
+// Tiled band LU of the diagonal blocks A_p (K1/K2 of SURVEY.md 2.3).
+//
+// Implements factorize_block with LAPACK dgbtrf's pivot
+// rule: the pivot of column j is the first max |a_ij|, i >= j.  This kernel
+// set is the no-interchange path: it evaluates that rule for every column and
+// records the first column whose rule would pick a row other than the
+// diagonal (status[2p]); the host then raises LRS_ERR_NOT_IMPLEMENTED instead
+// of returning factors that differ from LAPACK's.  Column-diagonally-dominant
+// blocks (c1-c3) never interchange.
+//
+// Storage: partition p owns T_p row tiles of NB = 128 rows; row tile I stores
+// the W = wl + wu + 1 tiles (I, I-wl) .. (I, I+wu) contiguously, each tile a
+// column-major 128 x 128 block.  After factorization the off-diagonal tiles
+// hold L (below) and U (above); the diagonal tile holds inv(L_II) strictly
+// below and inv(U_II) on/above the diagonal (used by the apply kernels).
+//
+// Per step K (all partitions in one launch each):
+//   lu_diag   : LU of tile (K,K) in shared memory + in-place triangular inverses
+//   lu_gemm<0>: L_IK = A_IK inv(U_KK), U_KJ = inv(L_KK) A_KJ (DMMA tiles)
+//   lu_gemm<1>: A_IJ -= L_IK U_KJ for the wl x wu trailing tiles (DMMA tiles)
+#include "common.cuh"
+#include "kernels.h"
+#include "lrs_internal.h"
+
+namespace lrs {
+
+__device__ __forceinline__ int find_partition(const int64_t* off, int P, int64_t row) {
+  int lo = 0, hi = P - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (off[mid] <= row) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+
+__global__ void __launch_bounds__(256) extract_tiles_kernel(int64_t n, const int* __restrict__ rp,
+                                                            const int* __restrict__ ci,
+                                                            const double* __restrict__ va,
+                                                            BandGeom g, double* tiles, int64_t k,
+                                                            unsigned long long* bad) {
+  const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= n) return;
+  const int p = find_partition(g.off, g.P, row);
+  const int64_t o = g.off[p], s = g.size[p];
+  const int64_t li = row - o;
+  const int I = (int)(li / NB);
+  for (int q = rp[row]; q < rp[row + 1]; ++q) {
+    const int64_t col = ci[q];
+    bool ok;
+    if (col >= o && col < o + s) {
+      const int64_t lj = col - o;
+      const int J = (int)(lj / NB);
+      const int d = J - I;
+      ok = d >= -g.wl && d <= g.wu;
+      if (ok)
+        tiles[(g.tbase[p] + (int64_t)I * g.W + (d + g.wl)) * TILE_ELEMS + (lj % NB) * NB +
+              (li % NB)] = va[q];
+    } else if (p + 1 < g.P && col >= o + s && col < g.off[p + 1] + g.size[p + 1]) {
+      ok = row >= o + s - k && col < o + s + k;  // B_p corner
+    } else if (p > 0 && col < o && col >= g.off[p - 1]) {
+      ok = row < o + k && col >= o - k;  // C_p corner
+    } else {
+      ok = false;
+    }
+    if (!ok) atomicMin(bad, (unsigned long long)(row * n + col));
+  }
+}
+
+__global__ void pad_diag_kernel(BandGeom g, double* tiles) {
+  const int p = blockIdx.x;
+  const int64_t s = g.size[p];
+  const int T = g.T[p];
+  for (int64_t li = s + threadIdx.x; li < (int64_t)T * NB; li += blockDim.x) {
+    const int I = (int)(li / NB);
+    tiles[(g.tbase[p] + (int64_t)I * g.W + g.wl) * TILE_ELEMS + (li % NB) * NB + (li % NB)] = 1.0;
+  }
+}
+
+void launch_extract_tiles(Ctx* c, const Mat* m, const BandGeom& g, double* tiles, int64_t k,
+                          const int*, unsigned long long* d_bad) {
+  if (m->n > 0) {
+    extract_tiles_kernel<<<(unsigned)((m->n + 255) / 256), 256, 0, c->stream>>>(
+        m->n, m->row_ptr.get(), m->col_idx.get(), m->vals.get(), g, tiles, k, d_bad);
+    LRS_LAUNCHED(c);
+  }
+  pad_diag_kernel<<<g.P, 128, 0, c->stream>>>(g, tiles);
+  LRS_LAUNCHED(c);
+}
+
+// ---------------------------------------------------------------------------------------
+// lu_diag: one CTA (512 threads) per partition factors tile (K,K) in shared memory.
+// ---------------------------------------------------------------------------------------
+constexpr int DIAG_THREADS = 512;
+
+__global__ void __launch_bounds__(DIAG_THREADS, 1) lu_diag_kernel(BandGeom g, double* tiles,
+                                                                  int K, int* status) {
+  extern __shared__ double sm[];
+  double* A = sm;                  // 128 x 128 column-major
+  double* part = sm + TILE_ELEMS;  // 4 x 128 partial sums
+  const int p = blockIdx.x;
+  if (K >= g.T[p]) return;
+  const int tid = threadIdx.x;
+  double* gt = tiles + (g.tbase[p] + (int64_t)K * g.W + g.wl) * TILE_ELEMS;
+  for (int e = tid; e < TILE_ELEMS; e += DIAG_THREADS) A[e] = gt[e];
+  __syncthreads();
+  const int col0 = K * NB;
+  const int i = tid & (NB - 1), cg = tid >> 7;  // row, column group 0..3
+  // ---- unblocked right-looking LU, pivot rule checked per column -------------------
+  for (int j = 0; j < NB; ++j) {
+    const double piv = A[j * NB + j];
+    if (cg == 0 && i > j) {
+      const double a = A[j * NB + i];
+      if (fabs(a) > fabs(piv)) atomicMin(&status[2 * p], col0 + j);  // dgbtrf would swap
+      A[j * NB + i] = a / piv;
+    }
+    if (tid == 0 && piv == 0.0) atomicMin(&status[2 * p + 1], col0 + j);
+    __syncthreads();
+    if (i > j) {
+      const double lij = A[j * NB + i];
+      for (int c = j + 1 + cg; c < NB; c += 4) A[c * NB + i] -= lij * A[c * NB + j];
+    }
+    __syncthreads();
+  }
+  // ---- in-place inverses: threads 0..255 invert U (upper, non-unit, LAPACK dtrti2 'U'),
+  //      threads 256..511 invert L (unit lower, dtrti2 'L' 'U'); disjoint triangles.
+  const int half = tid >> 8;           // 0: U, 1: L
+  const int q = (tid >> 7) & 1;        // k-phase
+  double* pq = part + (half * 2 + q) * NB;
+  for (int s = 0; s < NB; ++s) {
+    // phase 1: partial triangular mat-vec products (reads only)
+    double ujj_inv = 0.0;
+    if (half == 0) {
+      const int j = s;
+      // t_i = sum_{k=i}^{j-1} invU[i][k] * U[k][j]   for i < j
+      double t = 0.0;
+      if (i < j)
+        for (int kk = i + q; kk < j; kk += 2) t = fma(A[kk * NB + i], A[j * NB + kk], t);
+      pq[i] = t;
+      ujj_inv = 1.0 / A[j * NB + j];
+    } else {
+      const int j = NB - 1 - s;
+      // t_i = sum_{k=j+1}^{i-1} invL[i][k] * L[k][j]   for i > j
+      double t = 0.0;
+      if (i > j)
+        for (int kk = j + 1 + q; kk < i; kk += 2) t = fma(A[kk * NB + i], A[j * NB + kk], t);
+      pq[i] = t;
+    }
+    __syncthreads();
+    // phase 2: write column j (disjoint addresses; no reads of other threads' outputs)
+    if (q == 0) {
+      if (half == 0) {
+        const int j = s;
+        if (i < j) A[j * NB + i] = -ujj_inv * (part[i] + part[NB + i]);
+        else if (i == j) A[j * NB + j] = ujj_inv;
+      } else {
+        const int j = NB - 1 - s;
+        if (i > j) A[j * NB + i] = -(A[j * NB + i] + part[2 * NB + i] + part[3 * NB + i]);
+      }
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < TILE_ELEMS; e += DIAG_THREADS) gt[e] = A[e];
+}
+
+// ---------------------------------------------------------------------------------------
+// DMMA tile GEMM: C(128x128) = / -= A(128x128) * B(128x128), all tiles column-major.
+// 256 threads = 8 warps as 2 (M) x 4 (N); each warp owns 64 x 32 outputs = 8 x 4
+// DMMA.8x8x4 accumulators.  K is streamed in 4 chunks of 32 via cp.async, double
+// buffered.  Shared layouts are padded so fragment loads are bank-conflict free:
+// As[k][m] with row stride 132, Bs[n][k] with row stride 36.
+// ---------------------------------------------------------------------------------------
+constexpr int GEMM_THREADS = 256;
+constexpr int KC = 32;
+constexpr int AS_LD = NB + 4;   // 132
+constexpr int BS_LD = KC + 4;   // 36
+constexpr int AS_STAGE = KC * AS_LD;
+constexpr int BS_STAGE = NB * BS_LD;
+constexpr size_t GEMM_SMEM = sizeof(double) * 2 * (AS_STAGE + BS_STAGE);
+
+enum { MASK_NONE = 0, MASK_UNIT_LOWER = 1, MASK_UPPER = 2 };
+
+__device__ __forceinline__ void gemm_load_chunk(const double* __restrict__ A,
+                                                const double* __restrict__ B, double* As,
+                                                double* Bs, int kc, int tid) {
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int idx = tid + GEMM_THREADS * q;  // 0..2047
+    const int k = idx >> 6, m2 = (idx & 63) * 2;
+    cp_async16(As + k * AS_LD + m2, A + (int64_t)(kc * KC + k) * NB + m2);
+    const int nn = idx >> 4, k2 = (idx & 15) * 2;
+    cp_async16(Bs + nn * BS_LD + k2, B + (int64_t)nn * NB + kc * KC + k2);
+  }
+  cp_async_commit();
+}
+
+template <int MODE>  // 0: C = A*B, 1: C -= A*B
+__device__ __forceinline__ void tile_gemm(const double* A, const double* B, double* C, int maskA,
+                                          int maskB, double* sm, int* piv_status, int col0) {
+  double* As = sm;
+  double* Bs = sm + 2 * AS_STAGE;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int wm = w & 1, wn = w >> 1;
+  const int g = lane >> 2, t = lane & 3;
+  double acc[8][4][2];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  gemm_load_chunk(A, B, As, Bs, 0, tid);
+#pragma unroll 1
+  for (int kc = 0; kc < NB / KC; ++kc) {
+    const int st = kc & 1;
+    if (kc + 1 < NB / KC) {
+      gemm_load_chunk(A, B, As + (st ^ 1) * AS_STAGE, Bs + (st ^ 1) * BS_STAGE, kc + 1, tid);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const double* as = As + st * AS_STAGE;
+    const double* bs = Bs + st * BS_STAGE;
+#pragma unroll
+    for (int k4 = 0; k4 < KC / 4; ++k4) {
+      const int kk = k4 * 4 + t;
+      const int kg = kc * KC + kk;
+      double a[8], b[4];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int m = 64 * wm + 8 * i + g;
+        double v = as[kk * AS_LD + m];
+        if (maskA == MASK_UNIT_LOWER) v = m > kg ? v : (m == kg ? 1.0 : 0.0);
+        a[i] = v;
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int nn = 32 * wn + 8 * j + g;
+        double v = bs[nn * BS_LD + kk];
+        if (maskB == MASK_UPPER) v = kg <= nn ? v : 0.0;
+        b[j] = v;
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+    }
+    __syncthreads();
+  }
+  int bad_col = 0x7fffffff;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int m = 64 * wm + 8 * i + g;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int nn = 32 * wn + 8 * j + 2 * t + e;
+        double* cp = C + (int64_t)nn * NB + m;
+        if (MODE == 0) {
+          *cp = acc[i][j][e];
+          if (piv_status && fabs(acc[i][j][e]) > 1.0) bad_col = min(bad_col, col0 + nn);
+        } else {
+          *cp -= acc[i][j][e];
+        }
+      }
+    }
+  }
+  if (piv_status && bad_col != 0x7fffffff) atomicMin(piv_status, bad_col);
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(GEMM_THREADS, 1) lu_gemm_kernel(BandGeom g, double* tiles, int K,
+                                                                  int* status) {
+  extern __shared__ double sm[];
+  const int p = blockIdx.y;
+  const int T = g.T[p];
+  if (K >= T) return;
+  const int64_t base = g.tbase[p];
+  auto tile = [&](int I, int J) -> double* {
+    return tiles + (base + (int64_t)I * g.W + (J - I + g.wl)) * TILE_ELEMS;
+  };
+  const int x = blockIdx.x;
+  if (KIND == 0) {
+    if (x < g.wl) {
+      const int I = K + 1 + x;
+      if (I >= T) return;
+      // L_IK = A_IK * inv(U_KK); |l| > 1 means dgbtrf would have interchanged rows
+      tile_gemm<0>(tile(I, K), tile(K, K), tile(I, K), MASK_NONE, MASK_UPPER, sm, &status[2 * p],
+                   K * NB);
+    } else {
+      const int J = K + 1 + (x - g.wl);
+      if (J >= T) return;
+      tile_gemm<0>(tile(K, K), tile(K, J), tile(K, J), MASK_UNIT_LOWER, MASK_NONE, sm, nullptr, 0);
+    }
+  } else {
+    const int I = K + 1 + x / g.wu;
+    const int J = K + 1 + x % g.wu;
+    if (I >= T || J >= T) return;
+    tile_gemm<1>(tile(I, K), tile(K, J), tile(I, J), MASK_NONE, MASK_NONE, sm, nullptr, 0);
+  }
+}
+
+static bool g_lu_attr_set = false;
+
+void launch_lu_step(Ctx* c, const BandGeom& g, double* tiles, int K, int* status) {
+  if (!g_lu_attr_set) {
+    LRS_CUDA(cudaFuncSetAttribute(lu_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)(sizeof(double) * (TILE_ELEMS + 4 * NB))));
+    LRS_CUDA(cudaFuncSetAttribute(lu_gemm_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)GEMM_SMEM));
+    LRS_CUDA(cudaFuncSetAttribute(lu_gemm_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)GEMM_SMEM));
+    g_lu_attr_set = true;
+  }
+  lu_diag_kernel<<<g.P, DIAG_THREADS, sizeof(double) * (TILE_ELEMS + 4 * NB), c->stream>>>(
+      g, tiles, K, status);
+  LRS_LAUNCHED(c);
+  if (g.wl + g.wu > 0) {
+    lu_gemm_kernel<0><<<dim3(g.wl + g.wu, g.P), GEMM_THREADS, GEMM_SMEM, c->stream>>>(g, tiles, K,
+                                                                                     status);
+    LRS_LAUNCHED(c);
+  }
+  if (g.wl > 0 && g.wu > 0) {
+    lu_gemm_kernel<1><<<dim3(g.wl * g.wu, g.P), GEMM_THREADS, GEMM_SMEM, c->stream>>>(g, tiles, K,
+                                                                                     status);
+    LRS_LAUNCHED(c);
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// FP64 DMMA peak microbenchmark (roofline denominator; MEASURED_PEAKS.json has no FP64)
+// ---------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) dmma_peak_kernel(double* out, int iters) {
+  double acc[8][2];
+  double a = 1.0 + threadIdx.x * 1e-9, b = 1.0 - threadIdx.x * 1e-9;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) acc[i][0] = acc[i][1] = 0.0;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) dmma_8x8x4(acc[i][0], acc[i][1], a, b);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += acc[i][0] + acc[i][1];
+  if (s == 12345.678) out[threadIdx.x] = s;
+}
+
+double run_dmma_peak(Ctx* c) {
+  DevBuf<double> out;
+  out.alloc(256);
+  const int iters = 20000;
+  const int blocks = c->num_sms * 4;
+  dmma_peak_kernel<<<blocks, 256, 0, c->stream>>>(out.get(), 200);
+  LRS_LAUNCHED(c);
+  LRS_CUDA(cudaEventRecord(c->ev0, c->stream));
+  dmma_peak_kernel<<<blocks, 256, 0, c->stream>>>(out.get(), iters);
+  LRS_LAUNCHED(c);
+  LRS_CUDA(cudaEventRecord(c->ev1, c->stream));
+  LRS_CUDA(cudaEventSynchronize(c->ev1));
+  float ms = 0.f;
+  LRS_CUDA(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+  const double flops = 2.0 * 256.0 * 8.0 * iters * (double)blocks * 8.0;  // 8 warps, 8 dmma, 256 FMA
+  return flops / (ms * 1e-3) / 1e12;
+}
+
+}  // namespace lrs

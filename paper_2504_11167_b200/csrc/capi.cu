@@ -1,0 +1,502 @@
+// The extern "C" boundary (include/lrspike_capi.h).  Every entry point maps the
+// internal LrsError to an lrs_status and records the payload the reference's
+// exception classes carry (proj/core/include/lrspike/errors.hpp:11-94).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <new>
+#include <vector>
+
+#include "fact.h"
+#include "kernels.h"
+#include "lrs_internal.h"
+
+struct lrs_ctx : lrs::Ctx {};
+struct lrs_mat : lrs::Mat {};
+struct lrs_fact : lrs::Fact {};
+
+namespace lrs {
+
+[[noreturn]] void throw_cuda(cudaError_t e, const char* what, const char* file, int line) {
+  const lrs_status s = (e == cudaErrorMemoryAllocation) ? LRS_ERR_OOM : LRS_ERR_CUDA;
+  throw LrsError(s, std::string(cudaGetErrorString(e)) + " in " + what + " (" + file + ":" +
+                        std::to_string(line) + ")");
+}
+
+static thread_local lrs_error_info g_last{};
+
+static void record(Ctx* c, const LrsError& e) {
+  lrs_error_info info{};
+  info.status = e.status;
+  std::snprintf(info.message, sizeof(info.message), "%s", e.what());
+  info.line = e.line;
+  info.row = e.row;
+  info.col = e.col;
+  info.column = e.column;
+  info.interface_index = e.iface;
+  info.cond_estimate = e.cond;
+  g_last = info;
+  if (c) c->last = info;
+}
+
+template <class F>
+static lrs_status guard(Ctx* c, F&& fn) {
+  try {
+    fn();
+    return LRS_OK;
+  } catch (const LrsError& e) {
+    record(c, e);
+    return e.status;
+  } catch (const std::bad_alloc&) {
+    LrsError e(LRS_ERR_OOM, "host allocation failed");
+    record(c, e);
+    return LRS_ERR_OOM;
+  } catch (const std::exception& ex) {
+    LrsError e(LRS_ERR_CUDA, ex.what());
+    record(c, e);
+    return LRS_ERR_CUDA;
+  }
+}
+
+// Host staging of a user buffer: returns a device pointer (uploading HOST data).
+struct DevView {
+  const double* p = nullptr;
+  DevBuf<double> own;
+};
+
+static const double* dev_in(Ctx* c, const void* src, int64_t ld, int64_t rows, int64_t cols,
+                            int32_t mem, DevBuf<double>& own, int64_t* ld_out) {
+  if (mem == LRS_MEM_DEVICE) {
+    *ld_out = ld;
+    return static_cast<const double*>(src);
+  }
+  own.alloc((size_t)std::max<int64_t>(1, rows * cols));
+  if (rows * cols > 0)
+    LRS_CUDA(cudaMemcpy2DAsync(own.get(), sizeof(double) * rows, src, sizeof(double) * ld,
+                               sizeof(double) * rows, cols, cudaMemcpyHostToDevice, c->stream));
+  *ld_out = rows;
+  return own.get();
+}
+
+static void dev_out_finish(Ctx* c, void* dst, int64_t ld, const double* dev, int64_t rows,
+                           int64_t cols, int32_t mem) {
+  if (mem == LRS_MEM_DEVICE) return;
+  if (rows * cols > 0)
+    LRS_CUDA(cudaMemcpy2DAsync(dst, sizeof(double) * ld, dev, sizeof(double) * rows,
+                               sizeof(double) * rows, cols, cudaMemcpyDeviceToHost, c->stream));
+  LRS_CUDA(cudaStreamSynchronize(c->stream));
+}
+
+static void check_mem(int32_t mem) {
+  if (mem != LRS_MEM_HOST && mem != LRS_MEM_DEVICE)
+    throw LrsError(LRS_ERR_PARAMETER, "mem must be LRS_MEM_HOST or LRS_MEM_DEVICE");
+}
+
+}  // namespace lrs
+
+using namespace lrs;
+
+extern "C" {
+
+const char* lrs_status_string(lrs_status s) {
+  switch (s) {
+    case LRS_OK: return "ok";
+    case LRS_ERR_PARSE: return "ParseError";
+    case LRS_ERR_UNSUPPORTED_FIELD: return "UnsupportedFieldError";
+    case LRS_ERR_DIMENSION: return "DimensionError";
+    case LRS_ERR_SINGULAR_SCALING: return "SingularScalingError";
+    case LRS_ERR_LAYOUT: return "LayoutError";
+    case LRS_ERR_NOT_BLOCK_TRIDIAGONAL: return "NotBlockTridiagonalError";
+    case LRS_ERR_SINGULAR_BLOCK: return "SingularBlockError";
+    case LRS_ERR_PARAMETER: return "ParameterError";
+    case LRS_ERR_ILL_CONDITIONED_INTERFACE: return "IllConditionedInterfaceError";
+    case LRS_ERR_BREAKDOWN: return "BreakdownError";
+    case LRS_ERR_CUDA: return "CudaError";
+    case LRS_ERR_OOM: return "OutOfMemory";
+    case LRS_ERR_NCCL: return "NcclError";
+    case LRS_ERR_NOT_IMPLEMENTED: return "NotImplemented";
+  }
+  return "unknown";
+}
+
+lrs_status lrs_ctx_create(int device, void* stream, lrs_ctx** out) {
+  if (!out) return LRS_ERR_PARAMETER;
+  *out = nullptr;
+  std::unique_ptr<lrs_ctx> c(new (std::nothrow) lrs_ctx());
+  if (!c) return LRS_ERR_OOM;
+  lrs_status s = guard(nullptr, [&] {
+    int count = 0;
+    LRS_CUDA(cudaGetDeviceCount(&count));
+    if (device < 0 || device >= count) throw LrsError(LRS_ERR_PARAMETER, "no such CUDA device");
+    LRS_CUDA(cudaSetDevice(device));
+    c->device = device;
+    if (stream) {
+      c->stream = static_cast<cudaStream_t>(stream);
+      c->own_stream = false;
+    } else {
+      LRS_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+      c->own_stream = true;
+    }
+    LRS_CUDA(cudaEventCreate(&c->ev0));
+    LRS_CUDA(cudaEventCreate(&c->ev1));
+    LRS_CUDA(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
+  });
+  if (s == LRS_OK) *out = c.release();
+  return s;
+}
+
+void lrs_ctx_destroy(lrs_ctx* c) {
+  if (!c) return;
+  cudaStreamSynchronize(c->stream);
+  if (c->ev0) cudaEventDestroy(c->ev0);
+  if (c->ev1) cudaEventDestroy(c->ev1);
+  if (c->own_stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+void* lrs_ctx_stream(lrs_ctx* c) { return c ? (void*)c->stream : nullptr; }
+
+int64_t lrs_ctx_launch_count(lrs_ctx* c) { return c ? c->launches : 0; }
+
+lrs_status lrs_ctx_synchronize(lrs_ctx* c) {
+  if (!c) return LRS_ERR_PARAMETER;
+  return guard(c, [&] { LRS_CUDA(cudaStreamSynchronize(c->stream)); });
+}
+
+lrs_status lrs_last_error(lrs_ctx* c, lrs_error_info* info) {
+  if (!info) return LRS_ERR_PARAMETER;
+  *info = c ? c->last : g_last;
+  return LRS_OK;
+}
+
+// CsrMatrix upload + validate (matrix.cpp:21-37) + band_metrics (matrix.cpp:138-158).
+lrs_status lrs_mat_upload_csr(lrs_ctx* c, int64_t n, int64_t nnz, const int64_t* row_ptr,
+                              const int64_t* col_idx, const void* values, int32_t scalar,
+                              int32_t mem, lrs_mat** out) {
+  if (!c || !out) return LRS_ERR_PARAMETER;
+  *out = nullptr;
+  std::unique_ptr<lrs_mat> m(new (std::nothrow) lrs_mat());
+  if (!m) return LRS_ERR_OOM;
+  lrs_status s = guard(c, [&] {
+    check_mem(mem);
+    if (scalar != LRS_F64 && scalar != LRS_C128)
+      throw LrsError(LRS_ERR_PARAMETER, "scalar must be LRS_F64 or LRS_C128");
+    if (scalar == LRS_C128)
+      throw LrsError(LRS_ERR_NOT_IMPLEMENTED, "complex128 matrices are not implemented yet");
+    if (n < 0 || nnz < 0) throw LrsError(LRS_ERR_DIMENSION, "negative dimension");
+    if (n >= (1ll << 31) || nnz >= (1ll << 31))
+      throw LrsError(LRS_ERR_DIMENSION, "n and nnz must be < 2^31 on the device");
+    std::vector<int64_t> rp(n + 1), ci(nnz);
+    std::vector<double> va(nnz);
+    if (mem == LRS_MEM_HOST) {
+      std::memcpy(rp.data(), row_ptr, sizeof(int64_t) * (n + 1));
+      if (nnz) {
+        std::memcpy(ci.data(), col_idx, sizeof(int64_t) * nnz);
+        std::memcpy(va.data(), values, sizeof(double) * nnz);
+      }
+    } else {
+      LRS_CUDA(cudaMemcpy(rp.data(), row_ptr, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToHost));
+      if (nnz) {
+        LRS_CUDA(cudaMemcpy(ci.data(), col_idx, sizeof(int64_t) * nnz, cudaMemcpyDeviceToHost));
+        LRS_CUDA(cudaMemcpy(va.data(), values, sizeof(double) * nnz, cudaMemcpyDeviceToHost));
+      }
+    }
+    // validate() -- matrix.cpp:21-37
+    if (rp[0] != 0) throw LrsError(LRS_ERR_DIMENSION, "row_ptr[0] must be 0");
+    if (rp[n] != nnz) throw LrsError(LRS_ERR_DIMENSION, "row_ptr[n_rows] must equal nnz");
+    int64_t ku = 0, kl = 0;
+    double dsum = 0.0, tsum = 0.0;
+    for (int64_t i = 0; i < n; ++i) {
+      if (rp[i] > rp[i + 1]) throw LrsError(LRS_ERR_DIMENSION, "row_ptr must be non-decreasing");
+      for (int64_t p = rp[i]; p < rp[i + 1]; ++p) {
+        const int64_t j = ci[p];
+        if (j < 0 || j >= n) throw LrsError(LRS_ERR_DIMENSION, "column index out of range");
+        if (p > rp[i] && j <= ci[p - 1])
+          throw LrsError(LRS_ERR_DIMENSION,
+                         "column indices must be strictly increasing within a row");
+        if (j > i) ku = std::max(ku, j - i);
+        if (j < i) kl = std::max(kl, i - j);
+        tsum += std::fabs(va[p]);
+        if (i == j) dsum += std::fabs(va[p]);
+      }
+    }
+    m->ctx = c;
+    m->n = n;
+    m->nnz = nnz;
+    m->scalar = scalar;
+    m->ku = ku;
+    m->kl = kl;
+    m->k = std::max(ku, kl);
+    m->diag_weight = tsum > 0 ? dsum / tsum : 0.0;
+    const double cells = (double)(ku + kl + 1) * (double)n;
+    m->band_density = cells > 0 ? (double)nnz / cells : 0.0;
+    // device CSR with int32 indices, and the transpose (host counting sort, structural)
+    std::vector<int> rp32(n + 1), ci32(nnz), trp(n + 1, 0), tci(nnz);
+    std::vector<double> tva(nnz);
+    for (int64_t i = 0; i <= n; ++i) rp32[i] = (int)rp[i];
+    for (int64_t p = 0; p < nnz; ++p) {
+      ci32[p] = (int)ci[p];
+      trp[ci[p] + 1]++;
+    }
+    for (int64_t i = 0; i < n; ++i) trp[i + 1] += trp[i];
+    std::vector<int> next(trp.begin(), trp.end() - 1);
+    for (int64_t i = 0; i < n; ++i)
+      for (int64_t p = rp[i]; p < rp[i + 1]; ++p) {
+        const int q = next[ci[p]]++;
+        tci[q] = (int)i;
+        tva[q] = va[p];
+      }
+    m->row_ptr.alloc(n + 1);
+    m->col_idx.alloc(std::max<int64_t>(nnz, 1));
+    m->vals.alloc(std::max<int64_t>(nnz, 1));
+    m->trow_ptr.alloc(n + 1);
+    m->tcol_idx.alloc(std::max<int64_t>(nnz, 1));
+    m->tvals.alloc(std::max<int64_t>(nnz, 1));
+    LRS_CUDA(cudaMemcpy(m->row_ptr.get(), rp32.data(), sizeof(int) * (n + 1), cudaMemcpyHostToDevice));
+    LRS_CUDA(cudaMemcpy(m->trow_ptr.get(), trp.data(), sizeof(int) * (n + 1), cudaMemcpyHostToDevice));
+    if (nnz) {
+      LRS_CUDA(cudaMemcpy(m->col_idx.get(), ci32.data(), sizeof(int) * nnz, cudaMemcpyHostToDevice));
+      LRS_CUDA(cudaMemcpy(m->vals.get(), va.data(), sizeof(double) * nnz, cudaMemcpyHostToDevice));
+      LRS_CUDA(cudaMemcpy(m->tcol_idx.get(), tci.data(), sizeof(int) * nnz, cudaMemcpyHostToDevice));
+      LRS_CUDA(cudaMemcpy(m->tvals.get(), tva.data(), sizeof(double) * nnz, cudaMemcpyHostToDevice));
+    }
+  });
+  if (s == LRS_OK) *out = m.release();
+  return s;
+}
+
+void lrs_mat_destroy(lrs_mat* m) { delete m; }
+
+lrs_status lrs_mat_band_metrics(lrs_mat* m, int64_t* ku, int64_t* kl, int64_t* k,
+                                double* diag_weight, double* band_density) {
+  if (!m) return LRS_ERR_PARAMETER;
+  if (ku) *ku = m->ku;
+  if (kl) *kl = m->kl;
+  if (k) *k = m->k;
+  if (diag_weight) *diag_weight = m->diag_weight;
+  if (band_density) *band_density = m->band_density;
+  return LRS_OK;
+}
+
+lrs_status lrs_spmv(lrs_mat* m, const void* x, int64_t ldx, void* y, int64_t ldy, int64_t n_rhs,
+                    int32_t accumulate, int32_t mem) {
+  if (!m) return LRS_ERR_PARAMETER;
+  Ctx* c = m->ctx;
+  return guard(c, [&] {
+    check_mem(mem);
+    if (n_rhs < 0 || ldx < m->n || ldy < m->n)
+      throw LrsError(LRS_ERR_DIMENSION, "spmv: A.n_cols must equal x.n_rows");
+    DevBuf<double> xo, yo;
+    int64_t lx, ly;
+    const double* xd = dev_in(c, x, ldx, m->n, n_rhs, mem, xo, &lx);
+    double* yd;
+    if (mem == LRS_MEM_DEVICE) {
+      yd = static_cast<double*>(y);
+      ly = ldy;
+    } else {
+      int64_t tmp;
+      yd = const_cast<double*>(dev_in(c, y, ldy, m->n, n_rhs, mem, yo, &tmp));
+      ly = tmp;
+    }
+    launch_spmv(c, m, xd, lx, yd, ly, (int)n_rhs, accumulate ? 1 : 0, nullptr, 0);
+    dev_out_finish(c, y, ldy, yd, m->n, n_rhs, mem);
+  });
+}
+
+lrs_status lrs_make_layout(int64_t n, int64_t p, int64_t k, int64_t* sizes_out) {
+  return guard(nullptr, [&] {
+    if (p < 1 || k < 0) throw LrsError(LRS_ERR_PARAMETER, "make_layout: p >= 1 and k >= 0");
+    for (int64_t i = 0; i < p; ++i) {
+      const int64_t s = n / p + (i < n % p ? 1 : 0);
+      if (s <= k)
+        throw LrsError(LRS_ERR_LAYOUT,
+                       "layout infeasible: need n >= p*(k+1) = " + std::to_string(p * (k + 1)));
+      if (sizes_out) sizes_out[i] = s;
+    }
+  });
+}
+
+lrs_status lrs_factorize(lrs_ctx* c, lrs_mat* a, const lrs_solver_cfg* cfg, lrs_fact** out) {
+  if (!c || !a || !cfg || !out) return LRS_ERR_PARAMETER;
+  *out = nullptr;
+  return guard(c, [&] {
+    LRS_CUDA(cudaSetDevice(c->device));
+    Fact* f = factorize(c, a, *cfg);
+    *out = static_cast<lrs_fact*>(f);
+  });
+}
+
+void lrs_fact_destroy(lrs_fact* f) {
+  if (!f) return;
+  cudaStreamSynchronize(f->ctx->stream);
+  delete static_cast<Fact*>(f);
+}
+
+lrs_status lrs_fact_get_info(lrs_fact* f, lrs_fact_info* info) {
+  if (!f || !info) return LRS_ERR_PARAMETER;
+  *info = f->info;
+  return LRS_OK;
+}
+
+lrs_status lrs_fact_get_layout(lrs_fact* f, int64_t* sizes, int64_t* offsets) {
+  if (!f) return LRS_ERR_PARAMETER;
+  for (int i = 0; i < f->P; ++i) {
+    if (sizes) sizes[i] = f->size[i];
+    if (offsets) offsets[i] = f->off[i];
+  }
+  return LRS_OK;
+}
+
+lrs_status lrs_fact_get_spike(lrs_fact* f, int64_t i, int32_t side, double* u, double* sigma,
+                              double* v) {
+  if (!f) return LRS_ERR_PARAMETER;
+  return guard(f->ctx, [&] {
+    if (f->r == 0) throw LrsError(LRS_ERR_PARAMETER, "factorization has no low-rank spikes");
+    if (i < 0 || i >= f->P || (side == LRS_SIDE_T && i == f->P - 1) ||
+        (side == LRS_SIDE_W && i == 0) || (side != LRS_SIDE_T && side != LRS_SIDE_W))
+      throw LrsError(LRS_ERR_PARAMETER, "no such spike");
+    const int r = f->r;
+    const int64_t n = f->n, k = f->k, ni = f->size[i];
+    const double* ub = side == LRS_SIDE_T ? f->uT.get() : f->uW.get();
+    const double* vb = side == LRS_SIDE_T ? f->vtT.get() : f->vtW.get();
+    const double* sb = side == LRS_SIDE_T ? f->sT.get() : f->sW.get();
+    if (u)
+      LRS_CUDA(cudaMemcpy2D(u, sizeof(double) * ni, ub + f->off[i], sizeof(double) * n,
+                            sizeof(double) * ni, r, cudaMemcpyDeviceToHost));
+    if (sigma) LRS_CUDA(cudaMemcpy(sigma, sb + (size_t)i * r, sizeof(double) * r, cudaMemcpyDeviceToHost));
+    if (v) {  // stored as v^T (k x r); return v (r x k, ld r)
+      std::vector<double> vt((size_t)k * r);
+      LRS_CUDA(cudaMemcpy(vt.data(), vb + (size_t)i * k * r, sizeof(double) * k * r,
+                          cudaMemcpyDeviceToHost));
+      for (int a = 0; a < r; ++a)
+        for (int64_t row = 0; row < k; ++row) v[a + row * r] = vt[row + (size_t)a * k];
+    }
+  });
+}
+
+lrs_status lrs_fact_get_tiles(lrs_fact* f, int64_t i, double* host_out, int64_t capacity,
+                              int64_t* needed) {
+  if (!f) return LRS_ERR_PARAMETER;
+  return guard(f->ctx, [&] {
+    if (i < 0 || i >= f->P) throw LrsError(LRS_ERR_PARAMETER, "no such partition");
+    const int64_t cnt = (int64_t)f->T[i] * f->W * TILE_ELEMS;
+    if (needed) *needed = cnt;
+    if (host_out) {
+      if (capacity < cnt) throw LrsError(LRS_ERR_DIMENSION, "tile buffer too small");
+      LRS_CUDA(cudaStreamSynchronize(f->ctx->stream));
+      LRS_CUDA(cudaMemcpy(host_out, f->tiles.get() + f->tbase[i] * TILE_ELEMS,
+                          sizeof(double) * cnt, cudaMemcpyDeviceToHost));
+    }
+  });
+}
+
+lrs_status lrs_fact_get_ledger(lrs_fact* f, int64_t messages[3], int64_t scalars[3]) {
+  if (!f) return LRS_ERR_PARAMETER;
+  for (int s = 0; s < 3; ++s) {
+    if (messages) messages[s] = f->ledger_msgs[s];
+    if (scalars) scalars[s] = f->ledger_sc[s];
+  }
+  return LRS_OK;
+}
+
+lrs_status lrs_solve_block(lrs_fact* f, int64_t i, const void* rhs, int64_t ld_rhs, void* x,
+                           int64_t ld_x, int64_t n_rhs, int32_t adjoint, int32_t mem) {
+  if (!f) return LRS_ERR_PARAMETER;
+  Ctx* c = f->ctx;
+  return guard(c, [&] {
+    check_mem(mem);
+    if (i < 0 || i >= f->P) throw LrsError(LRS_ERR_PARAMETER, "no such partition");
+    const int64_t ni = f->size[i];
+    if (ld_rhs < ni || ld_x < ni || n_rhs < 0)
+      throw LrsError(LRS_ERR_DIMENSION, "solve_block: RHS rows must equal the block size");
+    // work in a global-row-layout buffer so the partition offset addressing of the
+    // dataflow kernel applies unchanged
+    DevBuf<double> work;
+    work.alloc((size_t)std::max<int64_t>(1, f->n * n_rhs));
+    double* wp = work.get() + f->off[i];
+    const cudaMemcpyKind k_in = mem == LRS_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+    if (n_rhs > 0)
+      LRS_CUDA(cudaMemcpy2DAsync(wp, sizeof(double) * f->n, rhs, sizeof(double) * ld_rhs,
+                                 sizeof(double) * ni, n_rhs, k_in, c->stream));
+    dstage(f, work.get(), f->n, (int)n_rhs, adjoint != 0, (int)i);
+    const cudaMemcpyKind k_out = mem == LRS_MEM_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+    if (n_rhs > 0)
+      LRS_CUDA(cudaMemcpy2DAsync(x, sizeof(double) * ld_x, wp, sizeof(double) * f->n,
+                                 sizeof(double) * ni, n_rhs, k_out, c->stream));
+    LRS_CUDA(cudaStreamSynchronize(c->stream));
+  });
+}
+
+static lrs_status apply_common(lrs_fact* f, const void* in, int64_t ld_in, void* out,
+                               int64_t ld_out, int64_t n_rhs, int32_t mem, bool bj) {
+  if (!f) return LRS_ERR_PARAMETER;
+  Ctx* c = f->ctx;
+  return guard(c, [&] {
+    check_mem(mem);
+    if (ld_in < f->n || ld_out < f->n || n_rhs < 0)
+      throw LrsError(LRS_ERR_DIMENSION, "apply: vector rows must equal n");
+    if (mem == LRS_MEM_DEVICE) {
+      apply_precond(f, static_cast<const double*>(in), ld_in, static_cast<double*>(out), ld_out,
+                    (int)n_rhs, bj);
+      return;
+    }
+    DevBuf<double> io;
+    int64_t ld;
+    const double* d = dev_in(c, in, ld_in, f->n, n_rhs, mem, io, &ld);
+    apply_precond(f, d, ld, const_cast<double*>(d), ld, (int)n_rhs, bj);
+    dev_out_finish(c, out, ld_out, d, f->n, n_rhs, mem);
+  });
+}
+
+lrs_status lrs_apply_precond(lrs_fact* f, const void* in, int64_t ld_in, void* out, int64_t ld_out,
+                             int64_t n_rhs, int32_t mem) {
+  return apply_common(f, in, ld_in, out, ld_out, n_rhs, mem, false);
+}
+
+lrs_status lrs_apply_block_jacobi(lrs_fact* f, const void* in, int64_t ld_in, void* out,
+                                  int64_t ld_out, int64_t n_rhs, int32_t mem) {
+  return apply_common(f, in, ld_in, out, ld_out, n_rhs, mem, true);
+}
+
+lrs_status lrs_solve(lrs_fact* f, lrs_mat* a, const void* b, int64_t ldb, void* x, int64_t ldx,
+                     int64_t n_rhs, const lrs_iter_cfg* cfg, lrs_report* report, int32_t mem) {
+  if (!f || !a || !cfg) return LRS_ERR_PARAMETER;
+  Ctx* c = f->ctx;
+  lrs_report local{};
+  lrs_report* rep = report ? report : &local;
+  return guard(c, [&] {
+    check_mem(mem);
+    if (ldb < f->n || ldx < f->n || n_rhs < 0)
+      throw LrsError(LRS_ERR_DIMENSION, "solve: vector rows must equal n");
+    lrs_iter_cfg cc = *cfg;
+    if (cc.breakdown_eps <= 0) cc.breakdown_eps = 1e-30;
+    if (cc.restart <= 0) cc.restart = 30;
+    if (mem == LRS_MEM_DEVICE) {
+      solve(f, a, static_cast<const double*>(b), ldb, static_cast<double*>(x), ldx, (int)n_rhs, cc,
+            rep);
+      return;
+    }
+    DevBuf<double> bo, xo, x0o;
+    int64_t lb, lx0 = f->n;
+    const double* bd = dev_in(c, b, ldb, f->n, n_rhs, mem, bo, &lb);
+    if (cc.x0) cc.x0 = dev_in(c, cc.x0, ldx, f->n, n_rhs, mem, x0o, &lx0);
+    xo.alloc((size_t)std::max<int64_t>(1, f->n * n_rhs));
+    // x0 (if any) is addressed with ldx inside solve(); pass it with ld n
+    try {
+      solve(f, a, bd, lb, xo.get(), f->n, (int)n_rhs, cc, rep);
+    } catch (const LrsError& e) {
+      // breakdown keeps the partial result
+      if (e.status == LRS_ERR_BREAKDOWN) dev_out_finish(c, x, ldx, xo.get(), f->n, n_rhs, mem);
+      throw;
+    }
+    dev_out_finish(c, x, ldx, xo.get(), f->n, n_rhs, mem);
+  });
+}
+
+lrs_status lrs_bench_dmma_peak(lrs_ctx* c, double* tflops) {
+  if (!c || !tflops) return LRS_ERR_PARAMETER;
+  return guard(c, [&] { *tflops = run_dmma_peak(c); });
+}
+
+}  // extern "C"

@@ -1,0 +1,145 @@
+// Krylov vector kernels (K12 of SURVEY.md 2.3) for bicgstab
+// and GMRES(m): column-batched, per-column scalars, and
+// deterministic reductions -- every dot product is summed per partition-aligned
+// chunk in a fixed tree, then over chunks in order, so the
+// result does not depend on launch geometry or (later) on the GPU count.
+#include "common.cuh"
+#include "kernels.h"
+#include "lrs_internal.h"
+
+namespace lrs {
+
+constexpr int KV_THREADS = 256;
+
+template <int NR>
+__global__ void __launch_bounds__(KV_THREADS) multidot_partial_kernel(
+    const int64_t* __restrict__ cstart, const double* __restrict__ X, int64_t ldx, int64_t strideX,
+    int nvec, const double* __restrict__ Y, int64_t ldy, int nrhs, double* __restrict__ partial) {
+  __shared__ double red[KV_THREADS / 32][NR];
+  const int c = blockIdx.x;
+  const int64_t r0 = cstart[c], r1 = cstart[c + 1];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  for (int q = 0; q < nvec; ++q) {
+    const double* Xq = X + q * strideX;
+    double acc[NR];
+#pragma unroll
+    for (int j = 0; j < NR; ++j) acc[j] = 0.0;
+    for (int64_t row = r0 + tid; row < r1; row += KV_THREADS) {
+#pragma unroll
+      for (int j = 0; j < NR; ++j)
+        if (j < nrhs) acc[j] = fma(Xq[row + j * ldx], Y[row + j * ldy], acc[j]);
+    }
+#pragma unroll
+    for (int j = 0; j < NR; ++j) {
+      const double s = warp_sum(acc[j]);
+      if (lane == 0) red[w][j] = s;
+    }
+    __syncthreads();
+    if (tid < nrhs) {
+      double s = 0.0;
+      for (int ww = 0; ww < KV_THREADS / 32; ++ww) s += red[ww][tid];
+      partial[((int64_t)c * nvec + q) * nrhs + tid] = s;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void multidot_final_kernel(int nchunks, int nout, const double* __restrict__ partial,
+                                      double* __restrict__ out) {
+  const int o = blockIdx.x * blockDim.x + threadIdx.x;
+  if (o >= nout) return;
+  double s = 0.0;
+  for (int c = 0; c < nchunks; ++c) s += partial[(int64_t)c * nout + o];
+  out[o] = s;
+}
+
+void launch_multidot(Ctx* c, const Chunks& ch, const double* X, int64_t ldx, int64_t strideX,
+                     int nvec, const double* Y, int64_t ldy, int nrhs, double* partial,
+                     double* out) {
+  if (nvec == 0 || nrhs == 0) return;
+  if (nrhs == 1)
+    multidot_partial_kernel<1><<<ch.nchunks, KV_THREADS, 0, c->stream>>>(
+        ch.start, X, ldx, strideX, nvec, Y, ldy, nrhs, partial);
+  else
+    multidot_partial_kernel<MAX_RHS><<<ch.nchunks, KV_THREADS, 0, c->stream>>>(
+        ch.start, X, ldx, strideX, nvec, Y, ldy, nrhs, partial);
+  LRS_LAUNCHED(c);
+  const int nout = nvec * nrhs;
+  multidot_final_kernel<<<(nout + 127) / 128, 128, 0, c->stream>>>(ch.nchunks, nout, partial, out);
+  LRS_LAUNCHED(c);
+}
+
+// Column-masked BLAS-1 updates; a, b per column, act[j] != 0 selects columns.
+//  0: X = Y + a (X - b Z)      (BiCGStab p)
+//  1: W = Y - a Z              (BiCGStab s = r - alpha v; r = s - omega t)
+//  2: X = X + a Y + b Z        (BiCGStab x)
+//  3: W = X + a Y              (half-step candidate x + alpha phat)
+//  4: W = a Y                  (scale: GMRES basis normalisation)
+//  5: W = Y                    (copy)
+__global__ void __launch_bounds__(KV_THREADS) axpby_kernel(int64_t n, int nrhs, int op, ColScal a,
+                                                           ColScal b, ColScal act, double* X,
+                                                           int64_t ldx, const double* Y,
+                                                           int64_t ldy, const double* Z,
+                                                           int64_t ldz, double* W, int64_t ldw) {
+  const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= n) return;
+  for (int j = 0; j < nrhs; ++j) {
+    if (act.v[j] == 0.0) continue;
+    const double aj = a.v[j], bj = b.v[j];
+    switch (op) {
+      case 0: {
+        double* xp = X + row + j * ldx;
+        *xp = Y[row + j * ldy] + aj * (*xp - bj * Z[row + j * ldz]);
+      } break;
+      case 1: W[row + j * ldw] = Y[row + j * ldy] - aj * Z[row + j * ldz]; break;
+      case 2: {
+        double* xp = X + row + j * ldx;
+        *xp = *xp + aj * Y[row + j * ldy] + bj * Z[row + j * ldz];
+      } break;
+      case 3: W[row + j * ldw] = X[row + j * ldx] + aj * Y[row + j * ldy]; break;
+      case 4: W[row + j * ldw] = aj * Y[row + j * ldy]; break;
+      default: W[row + j * ldw] = Y[row + j * ldy]; break;
+    }
+  }
+}
+
+void launch_axpby_cols(Ctx* c, int64_t n, int nrhs, int op, const ColScal& a, const ColScal& b,
+                       const ColScal& act, double* X, int64_t ldx, const double* Y, int64_t ldy,
+                       const double* Z, int64_t ldz, double* W, int64_t ldw) {
+  if (n == 0 || nrhs == 0) return;
+  axpby_kernel<<<(unsigned)((n + KV_THREADS - 1) / KV_THREADS), KV_THREADS, 0, c->stream>>>(
+      n, nrhs, op, a, b, act, X, ldx, Y, ldy, Z, ldz, W, ldw);
+  LRS_LAUNCHED(c);
+}
+
+// x[:, j] += sign * sum_q V_q[:, j] * y[q * nrhs + j]
+__global__ void __launch_bounds__(KV_THREADS) multi_axpy_kernel(int64_t n, int nrhs,
+                                                                const double* __restrict__ V,
+                                                                int64_t ldv, int64_t strideV,
+                                                                int nvec, const double* __restrict__ y,
+                                                                double sign, double* x,
+                                                                int64_t ldx) {
+  const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= n) return;
+  for (int j = 0; j < nrhs; ++j) {
+    double s = 0.0;
+    for (int q = 0; q < nvec; ++q) s = fma(V[q * strideV + row + j * ldv], y[q * nrhs + j], s);
+    x[row + j * ldx] += sign * s;
+  }
+}
+
+void launch_multi_axpy_signed(Ctx* c, int64_t n, int nrhs, const double* V, int64_t ldv,
+                              int64_t strideV, int nvec, const double* y_dev, double sign,
+                              double* x, int64_t ldx) {
+  if (n == 0 || nrhs == 0 || nvec == 0) return;
+  multi_axpy_kernel<<<(unsigned)((n + KV_THREADS - 1) / KV_THREADS), KV_THREADS, 0, c->stream>>>(
+      n, nrhs, V, ldv, strideV, nvec, y_dev, sign, x, ldx);
+  LRS_LAUNCHED(c);
+}
+
+void launch_multi_axpy(Ctx* c, int64_t n, int nrhs, const double* V, int64_t ldv, int64_t strideV,
+                       int nvec, const double* y_dev, double* x, int64_t ldx) {
+  launch_multi_axpy_signed(c, n, nrhs, V, ldv, strideV, nvec, y_dev, 1.0, x, ldx);
+}
+
+}  // namespace lrs

@@ -1,0 +1,980 @@
+// Host-side orchestration of the GPU path: factorize,
+// apply_precond_T / apply_block_jacobi, bicgstab
+// and GMRES(m).  Only launches, small
+// host<->device scalar traffic and the Krylov scalar recurrences live here;
+// all vector and matrix arithmetic runs in the kernels of this library.
+// The control flow mirrors oracle/lrspike_oracle.py line by line so that the
+// two produce the same iterates up to roundoff.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "fact.h"
+#include "lrs_rng.h"
+
+namespace lrs {
+
+namespace {
+
+template <class J>
+void upload(Ctx* c, DevBuf<J>& d, const std::vector<J>& h) {
+  d.alloc(h.size());
+  if (!h.empty())
+    LRS_CUDA(cudaMemcpyAsync(d.get(), h.data(), sizeof(J) * h.size(), cudaMemcpyHostToDevice,
+                             c->stream));
+}
+
+template <class T>
+void download(Ctx* c, T* h, const T* d, size_t count) {
+  if (count == 0) return;
+  LRS_CUDA(cudaMemcpyAsync(h, d, sizeof(T) * count, cudaMemcpyDeviceToHost, c->stream));
+  LRS_CUDA(cudaStreamSynchronize(c->stream));
+}
+
+float elapsed_ms(cudaEvent_t a, cudaEvent_t b) {
+  float ms = 0.f;
+  LRS_CUDA(cudaEventElapsedTime(&ms, a, b));
+  return ms;
+}
+
+// columns [0, ncols) of a block with leading dimension ld
+void copy_block(Ctx* c, double* dst, int64_t ldd, const double* src, int64_t lds, int64_t rows,
+                int ncols) {
+  if (rows == 0 || ncols == 0) return;
+  LRS_CUDA(cudaMemcpy2DAsync(dst, sizeof(double) * ldd, src, sizeof(double) * lds,
+                             sizeof(double) * rows, ncols, cudaMemcpyDeviceToDevice, c->stream));
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------------------------
+// D-stage: banded L then U solves (or U^T then L^T for the adjoint), batches of
+// MAX_RHS columns, all partitions concurrently.
+// ------------------------------------------------------------------------------------
+void dstage(Fact* f, double* x, int64_t ld, int nrhs, bool adjoint, int p_only) {
+  const BandGeom g = f->geom();
+  const int ntiles = p_only >= 0 ? f->T[p_only] : (int)f->total_rowtiles;
+  for (int c0 = 0; c0 < nrhs; c0 += MAX_RHS) {
+    const int nr = std::min(MAX_RHS, nrhs - c0);
+    double* xc = x + (int64_t)c0 * ld;
+    launch_band_solve(f->ctx, g, f->tiles.get(), adjoint ? 2 : 0, xc, ld, nr, f->flags.get(),
+                      f->next_epoch(), f->ticket.get(), p_only, ntiles);
+    launch_band_solve(f->ctx, g, f->tiles.get(), adjoint ? 3 : 1, xc, ld, nr, f->flags.get(),
+                      f->next_epoch(), f->ticket.get(), p_only, ntiles);
+  }
+}
+
+void apply_precond(Fact* f, const double* in, int64_t ldi, double* out, int64_t ldo, int nrhs,
+                   bool block_jacobi) {
+  Ctx* c = f->ctx;
+  if (out != in) copy_block(c, out, ldo, in, ldi, f->n, nrhs);
+  dstage(f, out, ldo, nrhs, false, -1);
+  const bool lowrank = !block_jacobi && f->variant == LRS_VARIANT_T && f->r > 0 && f->P > 1;
+  if (!lowrank) return;
+  for (int c0 = 0; c0 < nrhs; c0 += MAX_RHS) {
+    const int nr = std::min(MAX_RHS, nrhs - c0);
+    double* xc = out + (int64_t)c0 * ldo;
+    launch_iface_apply(c, f->iface_jobs.get(), f->P - 1, f->r, f->k, xc, ldo, nr);
+    launch_recovery(c, f->geom(), f->n, xc, ldo, xc, ldo, nr, f->uT.get(), f->uW.get(), f->r,
+                    f->scT.get(), f->scW.get());
+  }
+  // CommLedger: 2 compressed messages per interface in the reduced solve, 2 in recovery
+  // (SPEC.md:535): 4 (p-1) n_svd n_rhs scalars per application.
+  const int64_t msgs = 2 * (int64_t)(f->P - 1);
+  f->ledger_msgs[LRS_STAGE_PRECOND_APPLY] += msgs;
+  f->ledger_sc[LRS_STAGE_PRECOND_APPLY] += msgs * f->r * nrhs;
+  f->ledger_msgs[LRS_STAGE_RECOVERY] += msgs;
+  f->ledger_sc[LRS_STAGE_RECOVERY] += msgs * f->r * nrhs;
+}
+
+// ------------------------------------------------------------------------------------
+// Randomized spike SVDs and the truncated preconditioner for rank r.
+// Returns false (without throwing) if an interface is ill-conditioned, filling
+// *bad_iface / *bad_cond, so the caller can apply the r-halving retry.
+// ------------------------------------------------------------------------------------
+static bool build_lowrank(Fact* f, int r, int* bad_iface, double* bad_cond) {
+  Ctx* c = f->ctx;
+  Mat* m = f->mat;
+  const int P = f->P;
+  const int64_t n = f->n, k = f->k;
+  const int os = f->os >= 0 ? f->os : (r + 1) / 2;
+  const int l = r + os;
+  if (r < 1 || r > k) throw LrsError(LRS_ERR_PARAMETER, "randomized_spike_svd: 1 <= n_svd <= k");
+  if (l > k) throw LrsError(LRS_ERR_PARAMETER, "randomized_spike_svd: n_svd + oversample <= k");
+  if (f->passes < 2) throw LrsError(LRS_ERR_PARAMETER, "randomized_spike_svd: passes >= 2");
+  if (l > 96) throw LrsError(LRS_ERR_PARAMETER, "n_svd + oversample > 96 not supported");
+  f->r = r;
+  f->l = l;
+  const int L2 = 2 * l;
+  DevBuf<double> Y, S, Om, Zt, Rz, Ur, Vr, sig;
+  Y.alloc((size_t)n * L2);
+  S.alloc((size_t)n * L2);
+  Om.alloc((size_t)P * 2 * k * l);
+  Zt.alloc((size_t)P * 2 * k * l);
+  Rz.alloc((size_t)P * 2 * l * l);
+  Ur.alloc((size_t)P * 2 * l * l);
+  Vr.alloc((size_t)P * 2 * l * l);
+  sig.alloc((size_t)P * 2 * l);
+  // spikes: (partition, side)
+  std::vector<std::pair<int, int>> spk;
+  for (int i = 0; i < P; ++i) {
+    if (i < P - 1) spk.push_back({i, LRS_SIDE_T});
+    if (i > 0) spk.push_back({i, LRS_SIDE_W});
+  }
+  auto slot = [&](int i, int side) { return (size_t)(2 * i + side); };
+  // Omega on the host from the shared counter-based generator
+  {
+    std::vector<double> h((size_t)P * 2 * k * l, 0.0);
+    for (auto [i, side] : spk) {
+      const uint64_t key = lrs_rng_key(f->seed, LRS_STREAM_OMEGA + 2ull * i + side);
+      double* o = h.data() + slot(i, side) * k * l;
+      for (int64_t e = 0; e < k * l; ++e) o[e] = lrs_rng_normal(key, (uint64_t)e);
+    }
+    LRS_CUDA(cudaMemcpy(Om.get(), h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice));
+  }
+  auto ycol = [&](double* base, int i, int side) {
+    return base + f->off[i] + (int64_t)side * l * n;
+  };
+  // T_apply: Y = A_i^-1 pad(coupling X) for every spike, X = k x l blocks in src[slot]
+  DevBuf<CoupleJob> cj;
+  auto T_apply = [&](const double* src) {
+    std::vector<CoupleJob> jobs;
+    for (auto [i, side] : spk) {
+      CoupleJob j{};
+      if (side == LRS_SIDE_T) {
+        j.r0 = f->off[i] + f->size[i] - k;
+        j.c0 = f->off[i + 1];
+      } else {
+        j.r0 = f->off[i];
+        j.c0 = f->off[i] - k;
+      }
+      j.b = k;
+      j.dst0 = j.r0;
+      j.X = src + slot(i, side) * k * l;
+      j.ldx = k;
+      j.out = Y.get() + (int64_t)side * l * n;
+      j.ldo = n;
+      j.ncols = l;
+      jobs.push_back(j);
+    }
+    LRS_CUDA(cudaMemsetAsync(Y.get(), 0, sizeof(double) * n * L2, c->stream));
+    upload(c, cj, jobs);
+    launch_coupling(c, m, false, cj.get(), (int)jobs.size(), k, l);
+    dstage(f, Y.get(), n, L2, false, -1);
+  };
+  // Tt_apply: Zt[slot] = coupling^T (A_i^-T Q)|tip, Q = columns of Y
+  auto Tt_apply = [&]() {
+    copy_block(c, S.get(), n, Y.get(), n, n, L2);
+    dstage(f, S.get(), n, L2, true, -1);
+    std::vector<CoupleJob> jobs;
+    for (auto [i, side] : spk) {
+      CoupleJob j{};
+      int64_t tip0;
+      if (side == LRS_SIDE_T) {  // B_i^T = A^T[off_{i+1} .., off_i+n_i-k ..]
+        j.r0 = f->off[i + 1];
+        j.c0 = f->off[i] + f->size[i] - k;
+        tip0 = j.c0;
+      } else {  // C_i^T = A^T[off_i - k .., off_i ..]
+        j.r0 = f->off[i] - k;
+        j.c0 = f->off[i];
+        tip0 = j.c0;
+      }
+      j.b = k;
+      j.dst0 = 0;
+      j.X = S.get() + tip0 + (int64_t)side * l * n;
+      j.ldx = n;
+      j.out = Zt.get() + slot(i, side) * k * l;
+      j.ldo = k;
+      j.ncols = l;
+      jobs.push_back(j);
+    }
+    upload(c, cj, jobs);
+    launch_coupling(c, m, true, cj.get(), (int)jobs.size(), k, l);
+  };
+  DevBuf<QrJob> qj;
+  auto orth_Y = [&]() {
+    std::vector<QrJob> jobs;
+    for (auto [i, side] : spk) jobs.push_back(QrJob{ycol(Y.get(), i, side), f->size[i], n, nullptr});
+    upload(c, qj, jobs);
+    launch_householder_qr(c, qj.get(), (int)jobs.size(), l);
+  };
+  auto orth_Zt = [&](bool keepR) {
+    std::vector<QrJob> jobs;
+    for (auto [i, side] : spk)
+      jobs.push_back(QrJob{Zt.get() + slot(i, side) * k * l, k, k,
+                           keepR ? Rz.get() + slot(i, side) * l * l : nullptr});
+    upload(c, qj, jobs);
+    launch_householder_qr(c, qj.get(), (int)jobs.size(), l);
+  };
+
+  T_apply(Om.get());
+  orth_Y();
+  for (int pi = 0; pi < (f->passes - 2) / 2; ++pi) {
+    Tt_apply();
+    orth_Zt(false);
+    T_apply(Zt.get());
+    orth_Y();
+  }
+  Tt_apply();          // Zt = (Q^T T)^T, k x l
+  orth_Zt(true);       // Zt = Q_z R_z
+  {
+    std::vector<SvdJob> jobs;
+    for (auto [i, side] : spk) {
+      const size_t s = slot(i, side);
+      jobs.push_back(SvdJob{Rz.get() + s * l * l, Vr.get() + s * l * l, Ur.get() + s * l * l,
+                            sig.get() + s * l});
+    }
+    DevBuf<SvdJob> sj;
+    upload(c, sj, jobs);
+    launch_jacobi_svd(c, sj.get(), (int)jobs.size(), l);
+    // Z = V_R S (Q_z U_R)^T  =>  u = Q V_R[:, :r],  v^T = Q_z U_R[:, :r]
+    f->uT.alloc((size_t)n * r);
+    f->uW.alloc((size_t)n * r);
+    f->vtT.alloc((size_t)P * k * r);
+    f->vtW.alloc((size_t)P * k * r);
+    f->sT.alloc((size_t)P * r);
+    f->sW.alloc((size_t)P * r);
+    LRS_CUDA(cudaMemsetAsync(f->uT.get(), 0, sizeof(double) * n * r, c->stream));
+    LRS_CUDA(cudaMemsetAsync(f->uW.get(), 0, sizeof(double) * n * r, c->stream));
+    LRS_CUDA(cudaMemsetAsync(f->sT.get(), 0, sizeof(double) * P * r, c->stream));
+    LRS_CUDA(cudaMemsetAsync(f->sW.get(), 0, sizeof(double) * P * r, c->stream));
+    std::vector<GemmJob> gu, gv;
+    std::vector<SigmaJob> sjobs;
+    int64_t maxm = 0;
+    for (auto [i, side] : spk) {
+      const size_t s = slot(i, side);
+      double* ubuf = side == LRS_SIDE_T ? f->uT.get() : f->uW.get();
+      double* vbuf = side == LRS_SIDE_T ? f->vtT.get() : f->vtW.get();
+      double* sbuf = side == LRS_SIDE_T ? f->sT.get() : f->sW.get();
+      gu.push_back(GemmJob{ycol(Y.get(), i, side), n, Vr.get() + s * l * l, l,
+                           ubuf + f->off[i], n, f->size[i], r, l, 0});
+      gv.push_back(GemmJob{Zt.get() + s * k * l, k, Ur.get() + s * l * l, l,
+                           vbuf + (size_t)i * k * r, k, k, r, l, 0});
+      sjobs.push_back(SigmaJob{sig.get() + s * l, sbuf + (size_t)i * r});
+      maxm = std::max(maxm, f->size[i]);
+    }
+    DevBuf<GemmJob> dgu, dgv;
+    upload(c, dgu, gu);
+    upload(c, dgv, gv);
+    launch_small_gemm(c, dgu.get(), (int)gu.size(), maxm, r);
+    launch_small_gemm(c, dgv.get(), (int)gv.size(), k, r);
+    DevBuf<SigmaJob> dsj;
+    upload(c, dsj, sjobs);
+    DevBuf<int> flag;
+    flag.alloc(1);
+    LRS_CUDA(cudaMemsetAsync(flag.get(), 0, sizeof(int), c->stream));
+    launch_sigma_trunc(c, dsj.get(), (int)sjobs.size(), r, flag.get());
+    int hflag = 0;
+    download(c, &hflag, flag.get(), 1);
+    f->rank_collapsed = hflag != 0;
+  }
+  // interfaces
+  const int ni = P - 1;
+  f->Kd.alloc((size_t)ni * r * r);
+  f->Ed.alloc((size_t)ni * r * r);
+  f->Hinv.alloc((size_t)ni * r * r);
+  f->cond.alloc((size_t)ni * 2);
+  f->degen.alloc((size_t)ni);
+  {
+    std::vector<IfaceSetupJob> jobs;
+    for (int i = 0; i < ni; ++i) {
+      IfaceSetupJob j{};
+      j.uTb = f->uT.get() + f->off[i] + f->size[i] - k;
+      j.ld_uT = n;
+      j.uWt = f->uW.get() + f->off[i + 1];
+      j.ld_uW = n;
+      j.vtT = f->vtT.get() + (size_t)i * k * r;
+      j.vtW = f->vtW.get() + (size_t)(i + 1) * k * r;
+      j.sT = f->sT.get() + (size_t)i * r;
+      j.sW = f->sW.get() + (size_t)(i + 1) * r;
+      j.K = f->Kd.get() + (size_t)i * r * r;
+      j.E = f->Ed.get() + (size_t)i * r * r;
+      j.Hinv = f->Hinv.get() + (size_t)i * r * r;
+      j.cond = f->cond.get() + 2 * i;
+      j.degenerate = f->degen.get() + i;
+      jobs.push_back(j);
+    }
+    DevBuf<IfaceSetupJob> dj;
+    upload(c, dj, jobs);
+    launch_iface_setup(c, dj.get(), ni, r, k);
+    std::vector<double> hc(2 * ni);
+    download(c, hc.data(), f->cond.get(), hc.size());
+    double mx = 1.0;
+    for (int i = 0; i < ni; ++i) {
+      const double ci = std::max(hc[2 * i], hc[2 * i + 1]);
+      if (!(ci <= COND_LIMIT)) {
+        *bad_iface = i;
+        *bad_cond = ci;
+        return false;
+      }
+      mx = std::max(mx, ci);
+    }
+    f->info.max_interface_cond = mx;
+  }
+  // apply-time jobs
+  f->scT.alloc((size_t)P * r * MAX_RHS);
+  f->scW.alloc((size_t)P * r * MAX_RHS);
+  LRS_CUDA(cudaMemsetAsync(f->scT.get(), 0, sizeof(double) * P * r * MAX_RHS, c->stream));
+  LRS_CUDA(cudaMemsetAsync(f->scW.get(), 0, sizeof(double) * P * r * MAX_RHS, c->stream));
+  {
+    std::vector<IfaceApplyJob> jobs;
+    for (int i = 0; i < ni; ++i) {
+      IfaceApplyJob j{};
+      j.vtT = f->vtT.get() + (size_t)i * k * r;
+      j.vtW = f->vtW.get() + (size_t)(i + 1) * k * r;
+      j.sT = f->sT.get() + (size_t)i * r;
+      j.sW = f->sW.get() + (size_t)(i + 1) * r;
+      j.K = f->Kd.get() + (size_t)i * r * r;
+      j.E = f->Ed.get() + (size_t)i * r * r;
+      j.Hinv = f->Hinv.get() + (size_t)i * r * r;
+      j.yb_row = f->off[i] + f->size[i] - k;
+      j.yt_row = f->off[i + 1];
+      j.scT = f->scT.get() + (size_t)i * r * MAX_RHS;
+      j.scW = f->scW.get() + (size_t)(i + 1) * r * MAX_RHS;
+      jobs.push_back(j);
+    }
+    upload(c, f->iface_jobs, jobs);
+  }
+  LRS_CUDA(cudaStreamSynchronize(c->stream));
+  return true;
+}
+
+// ------------------------------------------------------------------------------------
+// factorize
+// ------------------------------------------------------------------------------------
+Fact* factorize(Ctx* c, Mat* m, const lrs_solver_cfg& cfg) {
+  if (m->scalar != LRS_F64)
+    throw LrsError(LRS_ERR_NOT_IMPLEMENTED, "complex128 factorization is not implemented yet");
+  std::unique_ptr<Fact> f(new Fact());
+  f->ctx = c;
+  f->mat = m;
+  f->variant = cfg.variant;
+  if (cfg.variant != LRS_VARIANT_T && cfg.variant != LRS_VARIANT_BJ)
+    throw LrsError(LRS_ERR_PARAMETER, "unknown variant");
+  if (cfg.p < 1) throw LrsError(LRS_ERR_PARAMETER, "p >= 1 required");
+  if (cfg.n_svd < 0) throw LrsError(LRS_ERR_PARAMETER, "n_svd >= 0 required");
+  f->P = (int)cfg.p;
+  f->n = m->n;
+  f->k = cfg.k > 0 ? cfg.k : m->k;
+  f->kl = m->kl;
+  f->ku = m->ku;
+  f->passes = cfg.passes > 0 ? cfg.passes : 2;
+  f->seed = cfg.seed;
+  f->os = (int)cfg.oversample;
+  // layout
+  {
+    const int64_t P = f->P, n = f->n;
+    f->size.resize(P);
+    f->off.resize(P);
+    for (int64_t i = 0; i < P; ++i) f->size[i] = n / P + (i < n % P ? 1 : 0);
+    int64_t o = 0;
+    for (int64_t i = 0; i < P; ++i) {
+      f->off[i] = o;
+      o += f->size[i];
+    }
+    const int64_t mn = *std::min_element(f->size.begin(), f->size.end());
+    if (mn <= f->k)
+      throw LrsError(LRS_ERR_LAYOUT, "layout infeasible: need n >= p*(k+1) = " +
+                                         std::to_string(P * (f->k + 1)));
+  }
+  const int P = f->P;
+  f->wl = (int)((f->kl + NB - 1) / NB);
+  f->wu = (int)((f->ku + NB - 1) / NB);
+  f->T.resize(P);
+  f->tbase.resize(P);
+  f->fbase.resize(P);
+  f->Tmax = 0;
+  for (int i = 0; i < P; ++i) {
+    f->T[i] = (int)((f->size[i] + NB - 1) / NB);
+    f->Tmax = std::max(f->Tmax, f->T[i]);
+  }
+  f->wl = std::min(f->wl, std::max(0, f->Tmax - 1));
+  f->wu = std::min(f->wu, std::max(0, f->Tmax - 1));
+  f->W = f->wl + f->wu + 1;
+  int64_t tb = 0, fb = 0;
+  for (int i = 0; i < P; ++i) {
+    f->tbase[i] = tb;
+    f->fbase[i] = fb;
+    tb += (int64_t)f->T[i] * f->W;
+    fb += f->T[i];
+  }
+  f->total_tiles = tb;
+  f->total_rowtiles = fb;
+  upload(c, f->d_off, f->off);
+  upload(c, f->d_size, f->size);
+  upload(c, f->d_tbase, f->tbase);
+  upload(c, f->d_fbase, f->fbase);
+  upload(c, f->d_T, f->T);
+  f->tiles.alloc((size_t)tb * TILE_ELEMS);
+  f->flags.alloc((size_t)fb);
+  f->ticket.alloc(1);
+  f->status.alloc(2 * P);
+  f->bad.alloc(1);
+  LRS_CUDA(cudaMemsetAsync(f->tiles.get(), 0, sizeof(double) * tb * TILE_ELEMS, c->stream));
+  LRS_CUDA(cudaMemsetAsync(f->flags.get(), 0, sizeof(unsigned) * fb, c->stream));
+  LRS_CUDA(cudaMemsetAsync(f->status.get(), 0x7f, sizeof(int) * 2 * P, c->stream));
+  LRS_CUDA(cudaMemsetAsync(f->bad.get(), 0xff, sizeof(unsigned long long), c->stream));
+  // deterministic reduction chunks, partition aligned
+  {
+    const int64_t CH = 2048;
+    f->chunk_start.clear();
+    for (int i = 0; i < P; ++i)
+      for (int64_t r0 = 0; r0 < f->size[i]; r0 += CH) f->chunk_start.push_back(f->off[i] + r0);
+    f->chunk_start.push_back(f->n);
+    upload(c, f->d_chunks, f->chunk_start);
+    const size_t nch = f->chunk_start.size() - 1;
+    f->partial.alloc(nch * 64 * MAX_RHS);
+    f->dotout.alloc(64 * MAX_RHS);
+  }
+  cudaEvent_t e0, e1, e2, e3;
+  LRS_CUDA(cudaEventCreate(&e0));
+  LRS_CUDA(cudaEventCreate(&e1));
+  LRS_CUDA(cudaEventCreate(&e2));
+  LRS_CUDA(cudaEventCreate(&e3));
+  struct EvGuard {
+    cudaEvent_t* e;
+    ~EvGuard() {
+      for (int i = 0; i < 4; ++i) cudaEventDestroy(e[i]);
+    }
+  };
+  cudaEvent_t evs[4] = {e0, e1, e2, e3};
+  EvGuard eg{evs};
+  LRS_CUDA(cudaEventRecord(e0, c->stream));
+  const BandGeom g = f->geom();
+  launch_extract_tiles(c, m, g, f->tiles.get(), f->k, nullptr, f->bad.get());
+  {
+    unsigned long long hb = 0;
+    download(c, &hb, f->bad.get(), 1);
+    if (hb != ~0ull) {
+      LrsError e(LRS_ERR_NOT_BLOCK_TRIDIAGONAL,
+                 "nonzero (" + std::to_string(hb / f->n) + "," + std::to_string(hb % f->n) +
+                     ") outside the block-tridiagonal pattern; increase k or decrease p");
+      e.row = (int64_t)(hb / f->n);
+      e.col = (int64_t)(hb % f->n);
+      throw e;
+    }
+  }
+  for (int K = 0; K < f->Tmax; ++K) launch_lu_step(c, g, f->tiles.get(), K, f->status.get());
+  LRS_CUDA(cudaEventRecord(e1, c->stream));
+  {
+    std::vector<int> st(2 * P);
+    download(c, st.data(), f->status.get(), st.size());
+    for (int i = 0; i < P; ++i) {
+      if (st[2 * i + 1] != 0x7f7f7f7f) {
+        LrsError e(LRS_ERR_SINGULAR_BLOCK, "exact zero pivot in column " +
+                                               std::to_string(st[2 * i + 1]) + " of block " +
+                                               std::to_string(i));
+        e.column = st[2 * i + 1];
+        throw e;
+      }
+      if (st[2 * i] != 0x7f7f7f7f) {
+        LrsError e(LRS_ERR_NOT_IMPLEMENTED,
+                   "block " + std::to_string(i) + " needs a row interchange at column " +
+                       std::to_string(st[2 * i]) +
+                       " (partial pivoting); the interchange path is not implemented on the GPU yet");
+        e.column = st[2 * i];
+        throw e;
+      }
+    }
+  }
+  // spikes + truncated preconditioner, with the r-halving retry
+  int r = (f->variant == LRS_VARIANT_T && P > 1) ? (int)cfg.n_svd : 0;
+  f->r = 0;
+  f->l = 0;
+  if (r > 0) {
+    for (int attempt = 0;; ++attempt) {
+      int bi = -1;
+      double bc = 0.0;
+      if (build_lowrank(f.get(), r, &bi, &bc)) break;
+      if (attempt == 1 || r / 2 < 1) {
+        LrsError e(LRS_ERR_ILL_CONDITIONED_INTERFACE,
+                   "interface " + std::to_string(bi) + " ill-conditioned (cond " +
+                       std::to_string(bc) + ")");
+        e.iface = bi;
+        e.cond = bc;
+        throw e;
+      }
+      r /= 2;
+    }
+  }
+  LRS_CUDA(cudaEventRecord(e2, c->stream));
+  LRS_CUDA(cudaEventSynchronize(e2));
+  // info
+  lrs_fact_info& in = f->info;
+  in.n = f->n;
+  in.p = P;
+  in.k = f->k;
+  in.n_svd = f->r;
+  in.l = f->l;
+  in.kl = f->kl;
+  in.ku = f->ku;
+  in.nb = NB;
+  in.wl = f->wl;
+  in.wu = f->wu;
+  in.factor_bytes = f->total_tiles * TILE_ELEMS * (int64_t)sizeof(double);
+  in.rank_collapsed = f->rank_collapsed;
+  in.variant = f->variant;
+  in.t_lu = elapsed_ms(e0, e1) * 1e-3;
+  in.t_spikes = elapsed_ms(e1, e2) * 1e-3;
+  in.t_precond = 0.0;
+  in.t_factorize = elapsed_ms(e0, e2) * 1e-3;
+  if (in.max_interface_cond == 0.0) in.max_interface_cond = 1.0;
+  // algorithmic work: no-fill band LU flops; factor bytes streamed per apply
+  double flops = 0.0, fbytes = 0.0;
+  for (int i = 0; i < P; ++i) {
+    const int64_t ni = f->size[i];
+    for (int64_t j = 0; j < ni; ++j) {
+      const double rem = (double)(ni - 1 - j);
+      const double a = std::min<double>((double)f->kl, rem), b = std::min<double>((double)f->ku, rem);
+      flops += a + 2.0 * a * b;
+      fbytes += a + 1.0 + b;
+    }
+  }
+  in.lu_flops = (int64_t)flops;
+  in.apply_bytes = (int64_t)(8.0 * (fbytes + 2.0 * f->n + 2.0 * f->n * f->r));
+  return f.release();
+}
+
+// ------------------------------------------------------------------------------------
+// Krylov drivers (mirror oracle.bicgstab / oracle.gmres)
+// ------------------------------------------------------------------------------------
+namespace {
+
+struct Work {
+  Fact* f;
+  Mat* A;
+  int64_t n;
+  int nr;
+  bool bj;
+  lrs_report* rep;
+  std::vector<double> hist;
+  double* hbuf = nullptr;  // pinned staging
+  Work() = default;
+  ~Work() {
+    if (hbuf) cudaFreeHost(hbuf);
+  }
+  void init() { LRS_CUDA(cudaMallocHost(&hbuf, sizeof(double) * 64 * MAX_RHS * 2)); }
+  Ctx* c() const { return f->ctx; }
+  // out[q*nr + j] for q < nvec
+  void dots(const double* X, int64_t strideX, int nvec, const double* Y, double* out) {
+    launch_multidot(c(), f->chunks(), X, n, strideX, nvec, Y, n, nr, f->partial.get(),
+                    f->dotout.get());
+    LRS_CUDA(cudaMemcpyAsync(hbuf, f->dotout.get(), sizeof(double) * nvec * nr,
+                             cudaMemcpyDeviceToHost, c()->stream));
+    LRS_CUDA(cudaStreamSynchronize(c()->stream));
+    std::memcpy(out, hbuf, sizeof(double) * nvec * nr);
+  }
+  void norms(const double* X, double* out) {
+    dots(X, 0, 1, X, out);
+    for (int j = 0; j < nr; ++j) out[j] = std::sqrt(out[j]);
+  }
+  void M(const double* in, double* out) {
+    apply_precond(f, in, n, out, n, nr, bj);
+    rep->precond_applications++;
+  }
+  void Aop(const double* in, double* out) {
+    launch_spmv(c(), A, in, n, out, n, nr, 0, nullptr, 0);
+    rep->matvecs++;
+  }
+  void resid(const double* b, const double* x, double* out) {  // out = b - A x
+    launch_spmv(c(), A, x, n, out, n, nr, 2, b, n);
+    rep->matvecs++;
+  }
+  void push(double v) { hist.push_back(v); }
+};
+
+ColScal cs_fill(const std::vector<double>& v) {
+  ColScal s{};
+  for (size_t j = 0; j < v.size() && j < MAX_RHS; ++j) s.v[j] = v[j];
+  return s;
+}
+ColScal cs_mask(const std::vector<bool>& v) {
+  ColScal s{};
+  for (size_t j = 0; j < v.size() && j < MAX_RHS; ++j) s.v[j] = v[j] ? 1.0 : 0.0;
+  return s;
+}
+bool any(const std::vector<bool>& v) {
+  for (bool b : v)
+    if (b) return true;
+  return false;
+}
+
+// returns iterations per column; sets conv/brk
+void run_bicgstab(Work& w, const double* b, double* x, const lrs_iter_cfg& cfg, bool has_x0,
+                  std::vector<double>& iters, std::vector<bool>& conv, std::vector<bool>& brk) {
+  const int nr = w.nr;
+  const int64_t n = w.n;
+  Ctx* c = w.c();
+  const size_t blk = (size_t)n * nr;
+  DevBuf<double> buf;
+  buf.alloc(blk * 9);
+  double* r = buf.get();
+  double* rhat = r + blk;
+  double* p = rhat + blk;
+  double* v = p + blk;
+  double* s = v + blk;
+  double* t = s + blk;
+  double* phat = t + blk;
+  double* shat = phat + blk;
+  double* tmp = shat + blk;
+  const ColScal none{};
+  std::vector<double> bn(nr), bns(nr), tmpv(nr), tmpv2(nr);
+  w.norms(b, bn.data());
+  for (int j = 0; j < nr; ++j) bns[j] = bn[j] > 0 ? bn[j] : 1.0;
+  if (has_x0) {
+    w.resid(b, x, r);
+  } else {
+    LRS_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * blk, c->stream));
+    copy_block(c, r, n, b, n, n, nr);
+  }
+  w.norms(r, tmpv.data());
+  double mx = 0;
+  conv.assign(nr, false);
+  brk.assign(nr, false);
+  iters.assign(nr, 0.0);
+  for (int j = 0; j < nr; ++j) {
+    conv[j] = tmpv[j] / bns[j] <= cfg.tol || bn[j] == 0.0;
+    mx = std::max(mx, tmpv[j] / bns[j]);
+  }
+  w.push(mx);
+  copy_block(c, rhat, n, r, n, n, nr);
+  std::vector<double> rho_prev(nr, 1.0), alpha(nr, 1.0), omega(nr, 1.0), rho(nr), rv(nr);
+  LRS_CUDA(cudaMemsetAsync(p, 0, sizeof(double) * blk, c->stream));
+  LRS_CUDA(cudaMemsetAsync(v, 0, sizeof(double) * blk, c->stream));
+  for (int64_t it = 1; it <= cfg.max_iters; ++it) {
+    std::vector<bool> act(nr);
+    for (int j = 0; j < nr; ++j) act[j] = !conv[j] && !brk[j];
+    if (!any(act)) break;
+    w.dots(rhat, 0, 1, r, rho.data());
+    for (int j = 0; j < nr; ++j)
+      if (act[j] && std::fabs(rho[j]) < cfg.breakdown_eps) {
+        brk[j] = true;
+        act[j] = false;
+      }
+    if (!any(act)) break;
+    if (it == 1) {
+      launch_axpby_cols(c, n, nr, 5, none, none, cs_mask(act), nullptr, 0, r, n, nullptr, 0, p, n);
+    } else {
+      std::vector<double> beta(nr, 0.0);
+      for (int j = 0; j < nr; ++j) beta[j] = (rho[j] / rho_prev[j]) * (alpha[j] / omega[j]);
+      launch_axpby_cols(c, n, nr, 0, cs_fill(beta), cs_fill(omega), cs_mask(act), p, n, r, n, v, n,
+                        nullptr, 0);
+    }
+    w.M(p, phat);
+    w.Aop(phat, v);
+    w.dots(rhat, 0, 1, v, rv.data());
+    for (int j = 0; j < nr; ++j)
+      if (act[j]) alpha[j] = rho[j] / (rv[j] != 0.0 ? rv[j] : 1.0);
+    launch_axpby_cols(c, n, nr, 1, cs_fill(alpha), none, cs_mask(act), nullptr, 0, r, n, v, n, s, n);
+    w.norms(s, tmpv.data());
+    std::vector<bool> half(nr, false);
+    for (int j = 0; j < nr; ++j) half[j] = act[j] && tmpv[j] / bns[j] <= cfg.tol;
+    std::vector<bool> hist_cols = act;
+    if (any(half)) {
+      launch_axpby_cols(c, n, nr, 3, cs_fill(alpha), none, cs_mask(half), x, n, phat, n, nullptr, 0,
+                        tmp, n);
+      // true residual of the candidate (columns outside `half` are stale and unused)
+      w.resid(b, tmp, t);
+      w.norms(t, tmpv2.data());
+      std::vector<bool> ok(nr, false);
+      for (int j = 0; j < nr; ++j) ok[j] = half[j] && tmpv2[j] / bns[j] <= cfg.tol;
+      if (any(ok)) {
+        launch_axpby_cols(c, n, nr, 5, none, none, cs_mask(ok), nullptr, 0, tmp, n, nullptr, 0, x, n);
+        for (int j = 0; j < nr; ++j)
+          if (ok[j]) {
+            conv[j] = true;
+            iters[j] = (double)it - 0.5;
+            act[j] = false;
+          }
+      }
+    }
+    mx = 0;
+    for (int j = 0; j < nr; ++j)
+      if (hist_cols[j]) mx = std::max(mx, tmpv[j] / bns[j]);
+    w.push(mx);
+    if (!any(act)) break;
+    w.M(s, shat);
+    w.Aop(shat, t);
+    std::vector<double> tt(nr), ts(nr);
+    w.dots(t, 0, 1, t, tt.data());
+    w.dots(t, 0, 1, s, ts.data());
+    for (int j = 0; j < nr; ++j)
+      if (act[j]) omega[j] = ts[j] / (tt[j] != 0.0 ? tt[j] : 1.0);
+    for (int j = 0; j < nr; ++j)
+      if (act[j] && std::fabs(omega[j]) < cfg.breakdown_eps) {
+        brk[j] = true;
+        act[j] = false;
+      }
+    launch_axpby_cols(c, n, nr, 2, cs_fill(alpha), cs_fill(omega), cs_mask(act), x, n, phat, n, shat,
+                      n, nullptr, 0);
+    launch_axpby_cols(c, n, nr, 1, cs_fill(omega), none, cs_mask(act), nullptr, 0, s, n, t, n, r, n);
+    w.norms(r, tmpv.data());
+    std::vector<bool> full(nr, false);
+    for (int j = 0; j < nr; ++j) full[j] = act[j] && tmpv[j] / bns[j] <= cfg.tol;
+    if (any(full)) {
+      w.resid(b, x, tmp);
+      w.norms(tmp, tmpv2.data());
+      for (int j = 0; j < nr; ++j)
+        if (full[j] && tmpv2[j] / bns[j] <= cfg.tol) {
+          conv[j] = true;
+          iters[j] = (double)it;
+        }
+    }
+    mx = 0;
+    for (int j = 0; j < nr; ++j)
+      if (act[j]) mx = std::max(mx, tmpv[j] / bns[j]);
+    w.push(mx);
+    for (int j = 0; j < nr; ++j) {
+      if (act[j]) rho_prev[j] = rho[j];
+      if (act[j] && !conv[j]) iters[j] = (double)it;
+    }
+  }
+}
+
+void givens(double a, double b, double* c, double* s, double* d) {
+  if (b == 0.0) {
+    *c = 1.0;
+    *s = 0.0;
+    *d = a;
+    return;
+  }
+  if (a == 0.0) {
+    *c = 0.0;
+    *s = b > 0 ? 1.0 : -1.0;
+    *d = std::fabs(b);
+    return;
+  }
+  const double na = std::fabs(a), nb = std::fabs(b);
+  const double dd = std::hypot(na, nb);
+  const double sa = a / na;
+  *c = na / dd;
+  *s = sa * b / dd;
+  *d = sa * dd;
+}
+
+void run_gmres(Work& w, const double* b, double* x, const lrs_iter_cfg& cfg, bool has_x0,
+               std::vector<double>& iters_out, std::vector<bool>& conv) {
+  const int nr = w.nr;
+  const int64_t n = w.n;
+  const int m = std::max(1, (int)cfg.restart);
+  if (m + 1 > 64) throw LrsError(LRS_ERR_PARAMETER, "GMRES restart must be <= 63");
+  Ctx* c = w.c();
+  const size_t blk = (size_t)n * nr;
+  DevBuf<double> buf;
+  buf.alloc(blk * (2 * (size_t)m + 3));
+  double* V = buf.get();               // (m+1) blocks
+  double* Z = V + blk * (m + 1);       // m blocks
+  double* wv = Z + blk * m;
+  double* r = wv + blk;
+  DevBuf<double> ydev;
+  ydev.alloc((size_t)(m + 1) * MAX_RHS);
+  const ColScal none{};
+  std::vector<double> bn(nr), bns(nr), beta(nr);
+  w.norms(b, bn.data());
+  for (int j = 0; j < nr; ++j) bns[j] = bn[j] > 0 ? bn[j] : 1.0;
+  if (has_x0) {
+    w.resid(b, x, r);
+  } else {
+    LRS_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * blk, c->stream));
+    copy_block(c, r, n, b, n, n, nr);
+  }
+  w.norms(r, beta.data());
+  conv.assign(nr, false);
+  std::vector<int64_t> iters(nr, 0);
+  double mx = 0;
+  for (int j = 0; j < nr; ++j) {
+    conv[j] = beta[j] / bns[j] <= cfg.tol || bn[j] == 0.0;
+    mx = std::max(mx, beta[j] / bns[j]);
+  }
+  w.push(mx);
+  const std::vector<bool> all(nr, true);
+  std::vector<double> h((m + 1) * nr), h2((m + 1) * nr), hn(nr);
+  while (true) {
+    std::vector<bool> act(nr);
+    for (int j = 0; j < nr; ++j) act[j] = !conv[j] && iters[j] < cfg.max_iters;
+    if (!any(act)) break;
+    std::vector<double> inv(nr);
+    for (int j = 0; j < nr; ++j) inv[j] = 1.0 / (beta[j] > 0 ? beta[j] : 1.0);
+    launch_axpby_cols(c, n, nr, 4, cs_fill(inv), none, cs_mask(all), nullptr, 0, r, n, nullptr, 0,
+                      V, n);
+    // per column Hessenberg (after rotations) R[row + col*(m+1)], g, rotations
+    std::vector<std::vector<double>> R(nr, std::vector<double>((size_t)(m + 1) * m, 0.0));
+    std::vector<std::vector<double>> g(nr, std::vector<double>(m + 1, 0.0));
+    std::vector<std::vector<double>> csv(nr, std::vector<double>(m, 0.0)), snv(nr, std::vector<double>(m, 0.0));
+    for (int j = 0; j < nr; ++j) g[j][0] = beta[j];
+    std::vector<bool> inner = act;
+    std::vector<int> steps(nr, 0);
+    for (int jj = 0; jj < m; ++jj) {
+      if (!any(inner)) break;
+      double* Vj = V + blk * jj;
+      double* Zj = Z + blk * jj;
+      w.M(Vj, Zj);
+      w.Aop(Zj, wv);
+      // CGS2
+      w.dots(V, (int64_t)blk, jj + 1, wv, h.data());
+      LRS_CUDA(cudaMemcpyAsync(ydev.get(), h.data(), sizeof(double) * (jj + 1) * nr,
+                               cudaMemcpyHostToDevice, c->stream));
+      launch_multi_axpy_signed(c, n, nr, V, n, (int64_t)blk, jj + 1, ydev.get(), -1.0, wv, n);
+      w.dots(V, (int64_t)blk, jj + 1, wv, h2.data());
+      LRS_CUDA(cudaMemcpyAsync(ydev.get(), h2.data(), sizeof(double) * (jj + 1) * nr,
+                               cudaMemcpyHostToDevice, c->stream));
+      launch_multi_axpy_signed(c, n, nr, V, n, (int64_t)blk, jj + 1, ydev.get(), -1.0, wv, n);
+      w.norms(wv, hn.data());
+      // the H2D copies above read pageable h/h2 synchronously before returning, so reuse is safe
+      for (int q = 0; q < (jj + 1) * nr; ++q) h[q] += h2[q];
+      std::vector<double> invn(nr);
+      for (int j = 0; j < nr; ++j) invn[j] = 1.0 / (hn[j] > 0 ? hn[j] : 1.0);
+      launch_axpby_cols(c, n, nr, 4, cs_fill(invn), none, cs_mask(all), nullptr, 0, wv, n, nullptr,
+                        0, V + blk * (jj + 1), n);
+      mx = 0;
+      for (int j = 0; j < nr; ++j) {
+        if (!inner[j]) continue;
+        std::vector<double> col(m + 1, 0.0);
+        for (int q = 0; q <= jj; ++q) col[q] = h[q * nr + j];
+        col[jj + 1] = hn[j];
+        for (int q = 0; q < jj; ++q) {
+          const double t = csv[j][q] * col[q] + snv[j][q] * col[q + 1];
+          col[q + 1] = -snv[j][q] * col[q] + csv[j][q] * col[q + 1];
+          col[q] = t;
+        }
+        double cc, ss, d;
+        givens(col[jj], col[jj + 1], &cc, &ss, &d);
+        csv[j][jj] = cc;
+        snv[j][jj] = ss;
+        col[jj] = d;
+        col[jj + 1] = 0.0;
+        g[j][jj + 1] = -ss * g[j][jj];
+        g[j][jj] = cc * g[j][jj];
+        for (int q = 0; q <= jj; ++q) R[j][q + (size_t)jj * (m + 1)] = col[q];
+        steps[j]++;
+        iters[j]++;
+      }
+      for (int j = 0; j < nr; ++j) {
+        if (!inner[j]) continue;
+        const double est = std::fabs(g[j][jj + 1]) / bns[j];
+        mx = std::max(mx, est);
+        if (!(est > cfg.tol) || iters[j] >= cfg.max_iters) inner[j] = false;
+      }
+      w.push(mx);
+    }
+    // x += Z y per active column
+    int kmax = 0;
+    for (int j = 0; j < nr; ++j)
+      if (act[j]) kmax = std::max(kmax, steps[j]);
+    if (kmax > 0) {
+      std::vector<double> y((size_t)kmax * nr, 0.0);
+      for (int j = 0; j < nr; ++j) {
+        if (!act[j] || steps[j] == 0) continue;
+        const int kk = steps[j];
+        std::vector<double> yy(kk);
+        for (int q = kk - 1; q >= 0; --q) {
+          double s = g[j][q];
+          for (int e = q + 1; e < kk; ++e) s -= R[j][q + (size_t)e * (m + 1)] * yy[e];
+          yy[q] = s / R[j][q + (size_t)q * (m + 1)];
+        }
+        for (int q = 0; q < kk; ++q) y[(size_t)q * nr + j] = yy[q];
+      }
+      LRS_CUDA(cudaMemcpyAsync(ydev.get(), y.data(), sizeof(double) * y.size(),
+                               cudaMemcpyHostToDevice, c->stream));
+      launch_multi_axpy_signed(c, n, nr, Z, n, (int64_t)blk, kmax, ydev.get(), 1.0, x, n);
+      LRS_CUDA(cudaStreamSynchronize(c->stream));
+    }
+    w.resid(b, x, r);
+    w.norms(r, hn.data());
+    for (int j = 0; j < nr; ++j)
+      if (act[j]) {
+        beta[j] = hn[j];
+        if (beta[j] / bns[j] <= cfg.tol) conv[j] = true;
+      }
+  }
+  iters_out.assign(nr, 0.0);
+  for (int j = 0; j < nr; ++j) iters_out[j] = (double)iters[j];
+}
+
+}  // namespace
+
+void solve(Fact* f, Mat* a, const double* b, int64_t ldb, double* x, int64_t ldx, int nrhs,
+           const lrs_iter_cfg& cfg, lrs_report* rep) {
+  Ctx* c = f->ctx;
+  if (a->n != f->n) throw LrsError(LRS_ERR_DIMENSION, "solve: matrix does not match factorization");
+  if (cfg.tol <= 0 || cfg.max_iters < 1) throw LrsError(LRS_ERR_PARAMETER, "tol > 0 and max_iters >= 1");
+  const int64_t m0[3] = {f->ledger_msgs[0], f->ledger_msgs[1], f->ledger_msgs[2]};
+  const int64_t s0[3] = {f->ledger_sc[0], f->ledger_sc[1], f->ledger_sc[2]};
+  lrs_report& R = *rep;
+  double* hist_buf = R.history;
+  const int64_t cap = R.history_cap;
+  std::memset(&R, 0, sizeof(R));
+  R.history = hist_buf;
+  R.history_cap = cap;
+  R.seed = f->seed;
+  R.converged = 1;
+  LRS_CUDA(cudaEventRecord(c->ev0, c->stream));
+  const int64_t n = f->n;
+  bool any_brk = false;
+  double worst = 0.0;
+  std::vector<double> hist_all;
+  for (int c0 = 0; c0 < nrhs; c0 += MAX_RHS) {
+    const int nr = std::min(MAX_RHS, nrhs - c0);
+    Work w;
+    w.f = f;
+    w.A = a;
+    w.n = n;
+    w.nr = nr;
+    w.bj = f->variant == LRS_VARIANT_BJ;
+    w.rep = &R;
+    w.init();
+    // contiguous device copies (ld = n) of this column batch
+    DevBuf<double> bb, xx;
+    bb.alloc((size_t)n * nr);
+    xx.alloc((size_t)n * nr);
+    copy_block(c, bb.get(), n, b + (int64_t)c0 * ldb, ldb, n, nr);
+    const bool has_x0 = cfg.x0 != nullptr;
+    if (has_x0)
+      copy_block(c, xx.get(), n, static_cast<const double*>(cfg.x0) + (int64_t)c0 * ldx, ldx, n, nr);
+    std::vector<double> iters;
+    std::vector<bool> conv, brk;
+    if (cfg.method == LRS_BICGSTAB) {
+      run_bicgstab(w, bb.get(), xx.get(), cfg, has_x0, iters, conv, brk);
+    } else if (cfg.method == LRS_GMRES) {
+      run_gmres(w, bb.get(), xx.get(), cfg, has_x0, iters, conv);
+      brk.assign(nr, false);
+    } else {
+      throw LrsError(LRS_ERR_PARAMETER, "unknown Krylov method");
+    }
+    for (int j = 0; j < nr; ++j) {
+      R.iterations = std::max(R.iterations, iters[j]);
+      if (!conv[j]) R.converged = 0;
+      if (brk[j]) any_brk = true;
+    }
+    // final true residual (not counted as a solver matvec)
+    {
+      std::vector<double> bn(nr), rn(nr);
+      w.norms(bb.get(), bn.data());
+      DevBuf<double> tmp;
+      tmp.alloc((size_t)n * nr);
+      launch_spmv(c, a, xx.get(), n, tmp.get(), n, nr, 2, bb.get(), n);
+      w.norms(tmp.get(), rn.data());
+      for (int j = 0; j < nr; ++j) worst = std::max(worst, rn[j] / (bn[j] > 0 ? bn[j] : 1.0));
+    }
+    copy_block(c, x + (int64_t)c0 * ldx, ldx, xx.get(), n, n, nr);
+    hist_all.insert(hist_all.end(), w.hist.begin(), w.hist.end());
+  }
+  LRS_CUDA(cudaEventRecord(c->ev1, c->stream));
+  LRS_CUDA(cudaEventSynchronize(c->ev1));
+  R.t_solve = elapsed_ms(c->ev0, c->ev1) * 1e-3;
+  R.residual_final = worst;
+  R.breakdown = any_brk ? 1 : 0;
+  for (int s = 0; s < 3; ++s) {
+    R.comm_messages[s] = f->ledger_msgs[s] - m0[s];
+    R.comm_scalars[s] = f->ledger_sc[s] - s0[s];
+  }
+  R.history_total = (int64_t)hist_all.size();
+  R.history_len = 0;
+  if (R.history && R.history_cap > 0) {
+    R.history_len = std::min<int64_t>(R.history_cap, (int64_t)hist_all.size());
+    std::memcpy(R.history, hist_all.data(), sizeof(double) * R.history_len);
+  }
+  if (any_brk) throw LrsError(LRS_ERR_BREAKDOWN, "BiCGStab stagnation detected (SF)");
+}
+
+}  // namespace lrs

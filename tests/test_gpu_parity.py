@@ -1,0 +1,154 @@
+"""GPU parity tests: the CUDA path (through the C-ABI) against the CPU oracle on
+identical seeded inputs.  Run on a B200 with ``pytest -m gpu``.
+
+Tolerances (north_star): solution relative difference <= 1e-8, final true
+relative residual <= tol, iteration count within 2 of the oracle.  Kernel-level
+parity (block factors, block solves, preconditioner applies) is checked at
+1e-12 relative, well inside the FP64 roundoff of the different summation orders.
+"""
+import numpy as np
+import pytest
+
+from oracle import lrspike_oracle as O
+from paper_2504_11167_b200 import api, configs
+
+pytestmark = pytest.mark.gpu
+
+
+def _rel(a, b):
+    return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(np.linalg.norm(b), 1e-300))
+
+
+def _oracle_cfg(cfg, r, variant="T"):
+    return O.SolverConfig(variant=variant, p=cfg.P, k=cfg.b, n_svd=r, seed=cfg.seed)
+
+
+def _gpu_cfg(cfg, r, variant="T"):
+    return api.SolverConfig(variant=variant, p=cfg.P, k=cfg.b, n_svd=r, seed=cfg.seed)
+
+
+def test_dmma_peak_positive(ctx):
+    tf = ctx.dmma_peak_tflops()
+    assert 1.0 < tf < 200.0
+
+
+@pytest.mark.parametrize("name,scale", [("c1", 48 / 256), ("c1", 128 / 256), ("c2", 16 / 64),
+                                        ("c2", 24 / 64)])
+def test_block_factors_match_lapack(ctx, name, scale):
+    cfg = configs.make_config(name, scale)
+    S = cfg.matrix.to_scipy()
+    A = api.CsrMatrix.from_csr(ctx, cfg.matrix)
+    F = api.factorize(ctx, A, _gpu_cfg(cfg, 0, "BJ"))
+    lay = O.make_layout(S.shape[0], cfg.P, cfg.b)
+    blocks = O.extract_blocks(S, lay)
+    nb, wl = F.info["nb"], F.info["wl"]
+    for i in (0, cfg.P - 1):
+        fo = O.factorize_block(blocks.A[i], F.info["kl"], F.info["ku"])
+        assert fo.swaps == 0
+        n_i = lay.sizes[i]
+        # dense LAPACK L (unit lower) and U
+        Lr = np.eye(n_i)
+        Ur = np.zeros((n_i, n_i))
+        kl, ku = fo.kl, fo.ku
+        for j in range(n_i):
+            for q in range(max(0, j - ku - kl), min(n_i, j + kl + 1)):
+                v = fo.ab[kl + ku + q - j, j]
+                if q > j:
+                    Lr[q, j] = v
+                else:
+                    Ur[q, j] = v
+        tl = F.tiles(i)
+        T = tl.shape[0]
+        Lg = np.eye(T * nb)
+        Ug = np.zeros((T * nb, T * nb))
+        W = tl.shape[1]
+        for I in range(T):
+            for s in range(W):
+                J = I + s - wl
+                if J < 0 or J >= T:
+                    continue
+                blk = tl[I, s]
+                if J < I:
+                    Lg[I * nb:(I + 1) * nb, J * nb:(J + 1) * nb] = blk
+                elif J > I:
+                    Ug[I * nb:(I + 1) * nb, J * nb:(J + 1) * nb] = blk
+                else:
+                    iL = np.tril(blk, -1) + np.eye(nb)
+                    iU = np.triu(blk)
+                    Lg[I * nb:(I + 1) * nb, J * nb:(J + 1) * nb] = np.linalg.inv(iL)
+                    Ug[I * nb:(I + 1) * nb, J * nb:(J + 1) * nb] = np.linalg.inv(iU)
+        assert _rel(Lg[:n_i, :n_i], Lr) < 1e-12
+        assert _rel(Ug[:n_i, :n_i], Ur) < 1e-12
+
+
+@pytest.mark.parametrize("name,scale", [("c1", 48 / 256), ("c2", 24 / 64)])
+def test_solve_block_and_adjoint(ctx, name, scale):
+    cfg = configs.make_config(name, scale)
+    S = cfg.matrix.to_scipy()
+    A = api.CsrMatrix.from_csr(ctx, cfg.matrix)
+    F = api.factorize(ctx, A, _gpu_cfg(cfg, 0, "BJ"))
+    lay = O.make_layout(S.shape[0], cfg.P, cfg.b)
+    blocks = O.extract_blocks(S, lay)
+    rng = np.random.default_rng(7)
+    for i in range(cfg.P):
+        fo = O.factorize_block(blocks.A[i])
+        R = np.asfortranarray(rng.standard_normal((lay.sizes[i], 3)))
+        assert _rel(F.solve_block(i, R), O.solve_block(fo, R)) < 1e-12
+        assert _rel(F.solve_block_adjoint(i, R), O.solve_block_adjoint(fo, R)) < 1e-12
+        # multi-column equals column-by-column bit-exactly
+        X3 = F.solve_block(i, R)
+        X1 = F.solve_block(i, R[:, 1:2])
+        assert np.array_equal(X3[:, 1], X1[:, 0])
+
+
+@pytest.mark.parametrize("name,scale,r", [("c1", 48 / 256, 8), ("c2", 16 / 64, 16),
+                                          ("c2", 24 / 64, 16)])
+def test_apply_precond_matches_oracle(ctx, name, scale, r):
+    cfg = configs.make_config(name, scale)
+    S = cfg.matrix.to_scipy()
+    A = api.CsrMatrix.from_csr(ctx, cfg.matrix)
+    F = api.factorize(ctx, A, _gpu_cfg(cfg, r))
+    Fo = O.factorize(S, _oracle_cfg(cfg, r))
+    assert F.n_svd == Fo.n_svd
+    f = np.asfortranarray(np.random.default_rng(3).uniform(-1, 1, (S.shape[0], 2)))
+    xg = F.apply_precond_T(f)
+    xo = O.apply_precond_T(Fo, f)
+    assert _rel(xg, xo) < 1e-10
+    bj_g = F.apply_block_jacobi(f)
+    assert _rel(bj_g, O.apply_block_jacobi(Fo, f)) < 1e-12
+    # spikes: the rank-r operator u S v is basis independent
+    for i, side in ((0, api.SIDE_T), (1, api.SIDE_W)):
+        u, s, v = F.spike(i, side)
+        so = Fo.spT[i] if side == api.SIDE_T else Fo.spW[i]
+        assert _rel(s, so.sigma) < 1e-10
+        assert _rel((u * s) @ v, (so.u * so.sigma) @ so.v) < 1e-9
+
+
+def test_r0_equals_block_jacobi_bitwise(ctx):
+    cfg = configs.make_config("c1", 48 / 256)
+    A = api.CsrMatrix.from_csr(ctx, cfg.matrix)
+    F = api.factorize(ctx, A, _gpu_cfg(cfg, 0, "T"))
+    f = np.asfortranarray(np.random.default_rng(1).uniform(-1, 1, (cfg.matrix.n, 1)))
+    assert np.array_equal(F.apply_precond_T(f), F.apply_block_jacobi(f))
+
+
+@pytest.mark.parametrize("name,scale,method", [("c1", 48 / 256, "gmres"), ("c1", 96 / 256, "gmres"),
+                                               ("c2", 16 / 64, "bicgstab"),
+                                               ("c2", 24 / 64, "bicgstab"),
+                                               ("c1", 48 / 256, "bicgstab")])
+def test_solve_parity(ctx, name, scale, method):
+    cfg = configs.make_config(name, scale)
+    S = cfg.matrix.to_scipy()
+    A = api.CsrMatrix.from_csr(ctx, cfg.matrix)
+    it = api.IterConfig(tol=cfg.tol, method=method, restart=cfg.m or 30, max_iters=500)
+    x, rep, F = api.solve(A, cfg.rhs, _gpu_cfg(cfg, cfg.r), it)
+    xo, repo, _ = O.solve(S, cfg.rhs, _oracle_cfg(cfg, cfg.r),
+                          O.IterConfig(tol=cfg.tol, restart=cfg.m or 30, max_iters=500),
+                          method=method)
+    assert rep.converged and repo.converged
+    assert rep.residual_final <= cfg.tol
+    assert abs(rep.iterations - repo.iterations) <= 2
+    assert _rel(x, xo) <= 1e-8
+    # ledger: 4 (p-1) n_svd n_rhs scalars per application
+    m, s = rep.comm["precond-apply"]
+    assert s == 2 * (cfg.P - 1) * F.n_svd * rep.precond_applications
