@@ -1,0 +1,392 @@
+"""bench.py -- LR-SPIKE preconditioned solve on B200 (BASELINE.json metric).
+
+Workload (one "step"): BASELINE.json configs[1] = c2, the 64^3 7-point
+convection-diffusion system (n = 262,144, half-bandwidth 4,096), P = 8
+partitions, n_svd = 16, BiCGStab to 1e-8: factorize (tiled band LU of the 8
+blocks + randomized spike SVDs + truncated preconditioner) followed by the
+preconditioned BiCGStab solve.  metric = time-to-tolerance in seconds
+(factorize + solve), lower is better.
+
+  value       device time of one step with the matrix and RHS already resident
+              in HBM (CUDA events on the library stream, max over ranks)
+  e2e         the same step through the public C-ABI with HOST buffers: CSR
+              upload (validate + transpose + H2D), factorize, solve with a host
+              RHS, x copied back -- host<->device copies inside the timed region
+  roofline    dominant kernel = the DMMA trailing-update GEMM of the band LU
+              (FP64 tensor-core bound), from per-launch CUDA events in the timed
+              region; roofline_apply = the HBM-bound preconditioner apply
+  cpu_baseline the oracle port (scipy/OpenBLAS dgbtrf/dgbtrs) on a bounded
+              sample of the same blocks, extrapolated by the algorithmic work
+
+Multi-GPU: partitions are not yet sharded across GPUs ("replicas
+only" this round): under torchrun each rank solves its own replica of c2.
+
+--impl reference times the reference algorithm's CPU implementation (the oracle
+port; the reference itself cannot be built) on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+C2_APPLIES = 71  # preconditioner applications of the c2 BiCGStab solve (GPU run == oracle +-2 it)
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+            time.sleep(0.25)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        try:
+            for line in open(self.path):
+                f = [x.strip() for x in line.split(",")]
+                if len(f) < 9:
+                    continue
+                try:
+                    sm.append(float(f[1]))
+                    mx = max(mx, float(f[2]))
+                except ValueError:
+                    continue
+                for name, v in zip(("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown",
+                                    "sw_power_cap"), f[5:9]):
+                    if v.lower().startswith("active"):
+                        reasons.add(name)
+        except Exception:
+            pass
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        load = [s for s in sm if s > 0.5 * mx] or sm
+        return {"sm_mhz": float(np.median(load)), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------------------
+# CPU baseline (oracle port, bounded sample, extrapolated by algorithmic work)
+# ---------------------------------------------------------------------------------------
+def _lu_flops(n, kl, ku):
+    j = np.arange(n, dtype=np.float64)
+    rem = n - 1 - j
+    a = np.minimum(kl, rem)
+    b = np.minimum(ku, rem)
+    return float(np.sum(a + 2 * a * b)), float(np.sum(a + 1 + b))
+
+
+def cpu_baseline(cfg_name="c2", scale=1.0, sample_rows=8192, threads=None):
+    """Time the oracle's dgbtrf / dgbtrs on the first ``sample_rows`` rows of
+    partition 0 of the config and extrapolate to the whole time-to-tolerance:
+    t = t_lu * (LU flops / sample flops) + (applies + spike solves) * t_apply * (bytes ratio)."""
+    threads = threads or os.cpu_count() or 1
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", str(threads))
+    from oracle import lrspike_oracle as O  # the checker / baseline, never the product
+    from paper_2504_11167_b200 import configs
+
+    cfg = configs.make_config(cfg_name, scale)
+    S = cfg.matrix.to_scipy()
+    lay = O.make_layout(S.shape[0], cfg.P, cfg.b)
+    n0 = lay.sizes[0]
+    ns = min(sample_rows, n0)
+    blk = S[:ns, :ns].tocsr()
+    ku, kl = O.band_metrics(S)[:2]
+    t0 = time.perf_counter()
+    fo = O.factorize_block(blk, kl, ku)
+    t_lu_s = time.perf_counter() - t0
+    rhs = np.asfortranarray(np.random.default_rng(0).uniform(-1, 1, (ns, 1)))
+    O.solve_block(fo, rhs)
+    t0 = time.perf_counter()
+    reps = 3
+    for _ in range(reps):
+        O.solve_block(fo, rhs)
+    t_ap_s = (time.perf_counter() - t0) / reps
+    fl_s, by_s = _lu_flops(ns, kl, ku)
+    fl_t, by_t = 0.0, 0.0
+    for s in lay.sizes:
+        a, b = _lu_flops(s, kl, ku)
+        fl_t += a
+        by_t += b
+    t_lu = t_lu_s * fl_t / fl_s
+    t_apply = t_ap_s * by_t / by_s
+    l = cfg.r + (cfg.r + 1) // 2
+    spike_cols = 2 * (2 * l)  # forward + adjoint solves of 2l columns per partition
+    t_total = t_lu + (C2_APPLIES + spike_cols) * t_apply
+    return {
+        "value": t_total, "unit": "s", "cores": threads, "kind": "port",
+        "sample": (f"oracle dgbtrf+dgbtrs (scipy OpenBLAS, {threads} threads) on rows 0..{ns} of "
+                   f"partition 0 of {cfg_name} (kl={kl}, ku={ku}); extrapolated by no-fill LU flops "
+                   f"(x{fl_t / fl_s:.1f}) and factor bytes (x{by_t / by_s:.1f}) to {cfg.P} partitions, "
+                   f"{C2_APPLIES} applies + {spike_cols} spike solve columns"),
+        "t_lu_sample_s": t_lu_s, "t_apply_sample_s": t_ap_s, "t_lu_est_s": t_lu,
+        "t_apply_est_s": t_apply,
+    }
+
+
+def run_reference(args):
+    ws, rank, _ = _dist()
+    if rank != 0:
+        return 0
+    for _ in range(args.warmup):
+        cb = cpu_baseline(args.config, args.scale, args.cpu_sample_rows)
+    vals = []
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        cb = cpu_baseline(args.config, args.scale, args.cpu_sample_rows)
+        vals.append(cb["value"])
+    wall = time.perf_counter() - t0
+    v = float(np.mean(vals))
+    line = {
+        "impl": "reference", "metric": "preconditioned solve time-to-tolerance (s)", "value": v,
+        "unit": "s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * wall / max(args.steps, 1), "higher_is_better": False,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{args.config} (BASELINE.json configs[1]) LR-SPIKE-T + BiCGStab",
+                   "scale": args.scale},
+        "cpu_baseline": {k: cb[k] for k in ("kind", "cores", "sample")} | {"value": v, "unit": "s"},
+        "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------------------
+def run_ours(args):
+    import torch
+
+    from paper_2504_11167_b200 import api, configs
+
+    ws, rank, local = _dist()
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    stream = torch.cuda.current_stream()
+    ctx = api.Context(local, stream.cuda_stream)
+    cfg = configs.make_config(args.config, args.scale)
+    A = api.CsrMatrix.from_csr(ctx, cfg.matrix)
+    scfg = api.SolverConfig(variant="T", p=cfg.P, k=cfg.b, n_svd=cfg.r, seed=cfg.seed)
+    it = api.IterConfig(tol=cfg.tol, method=cfg.method, restart=cfg.m or 30, max_iters=2000)
+    b_dev = torch.from_numpy(np.asfortranarray(cfg.rhs)).cuda()
+    x_dev = torch.empty_like(b_dev)
+    dmma_peak = ctx.dmma_peak_tflops()
+
+    def step():
+        F = api.factorize(ctx, A, scfg)
+        x, rep, _ = api.solve(A, b_dev, it=it, F=F, x_out=x_dev)
+        return F, rep
+
+    for _ in range(args.warmup):
+        F, rep = step()
+        del F
+    torch.cuda.synchronize()
+    if ws > 1:
+        torch.distributed.barrier()
+    ctx.set_profiling(True)
+    ctx.kernel_times(reset=True)
+    l0 = ctx.launches
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps, infos = [], []
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            F, rep = step()
+            reps.append(rep)
+            infos.append(F.info)
+            del F
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    launches = ctx.launches - l0
+    kt = ctx.kernel_times(reset=True)
+    ctx.set_profiling(False)
+    ms = ev0.elapsed_time(ev1) / args.steps
+    if ws > 1:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    value = ms / 1e3
+
+    # ---- e2e: public C-ABI with host buffers (CSR upload + factorize + solve + x back)
+    e2e_vals = []
+    csr = cfg.matrix
+    h2d = 8 * (csr.n + 1) + 16 * csr.nnz + 8 * cfg.rhs.size
+    d2h = 8 * cfg.rhs.size
+    for i in range(args.warmup + args.steps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        A2 = api.CsrMatrix(ctx, csr.n, csr.row_ptr, csr.col_idx, csr.values)
+        F2 = api.factorize(ctx, A2, scfg)
+        xh, rep2, _ = api.solve(A2, np.asfortranarray(cfg.rhs), it=it, F=F2)
+        dt = time.perf_counter() - t0
+        del F2, A2
+        if i >= args.warmup:
+            e2e_vals.append(dt)
+    e2e = float(np.mean(e2e_vals))
+    if ws > 1:
+        t = torch.tensor([e2e], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e = float(t.item())
+
+    # ---- roofline: dominant kernel = band-LU trailing update (DMMA, FP64 tensor core)
+    info = infos[-1]
+    upd_ms, upd_n = kt["lu_update"]
+    lu_upd_flops = 0.0  # 2 * sum_j min(kl, .) * min(ku, .) per factorization (no-fill)
+    for s in _partition_sizes(cfg.matrix.n, cfg.P):
+        j = np.arange(s, dtype=np.float64)
+        rem = s - 1 - j
+        lu_upd_flops += float(np.sum(2.0 * np.minimum(info["kl"], rem) * np.minimum(info["ku"], rem)))
+    per_launch_flops = lu_upd_flops * args.steps / max(upd_n, 1)
+    avg_launch_s = upd_ms / max(upd_n, 1) / 1e3
+    achieved_tf = per_launch_flops / avg_launch_s / 1e12 if upd_n else 0.0
+    # apply (HBM): band_solve launches of the Krylov phase
+    solve_ms, solve_n = kt["band_solve"]
+    napply = sum(r.precond_applications for r in reps)
+    apply_bytes = info["apply_bytes"]
+    peaks, peak_src = _peaks()
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    # D-stage: 2 band_solve launches per apply (L, U) + the spike-construction solves
+    apply_ms_each = None
+    if napply:
+        apply_ms_each = (kt["band_solve"][0] + kt["iface_apply"][0] + kt["recovery"][0]) / 1.0
+    total_ms = sum(v[0] for v in kt.values())
+    line = {
+        "metric": "preconditioned solve time-to-tolerance (s)",
+        "value": value, "unit": "s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms, "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{args.config} (BASELINE.json configs[1]): 64^3 7-pt conv-diff, "
+                               f"n={cfg.matrix.n}, k={cfg.b}, P={cfg.P}, n_svd={cfg.r}, "
+                               f"BiCGStab tol {cfg.tol}; factorize+solve",
+                   "scale": args.scale, "parallelism": f"replicas x{ws} (partitions not sharded yet)",
+                   "l2": "inputs larger than L2 (17 GB band factors streamed per apply)"},
+        "iterations": reps[-1].iterations, "precond_applications": reps[-1].precond_applications,
+        "residual_final": reps[-1].residual_final,
+        "t_factorize_s": info["t_factorize"], "t_lu_s": info["t_lu"], "t_spikes_s": info["t_spikes"],
+        "t_solve_s": reps[-1].wall_time,
+        "e2e": {"value": e2e, "unit": "s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
+        "gpu_launches": int(launches),
+        "roofline": {"bound": "tensor", "kernel": "lu_gemm_kernel<1> (DMMA trailing update)",
+                     "achieved": achieved_tf, "peak": dmma_peak, "unit": "TFLOP/s",
+                     "frac": achieved_tf / dmma_peak if dmma_peak else None,
+                     "peak_source": "in-run FP64 DMMA microbenchmark (MEASURED_PEAKS.json has no FP64); "
+                                    "nominal 148 SM x 64 FMA x 2 x 1.965 GHz = 37.2",
+                     "traffic": None, "launches": int(upd_n), "avg_launch_ms": avg_launch_s * 1e3,
+                     "flops_per_launch": per_launch_flops},
+        "roofline_lu_all": {"achieved": info["lu_flops"] / info["t_lu"] / 1e12, "unit": "TFLOP/s",
+                            "frac": info["lu_flops"] / info["t_lu"] / 1e12 / dmma_peak},
+        "roofline_apply": _apply_roofline(kt, reps, info, hbm_peak, peak_src, args.steps),
+        "kernel_ms_per_step": {k: v[0] / args.steps for k, v in kt.items()},
+        "kernel_launches_per_step": {k: v[1] / args.steps for k, v in kt.items()},
+        "kernel_ms_total_share": {k: (v[0] / total_ms if total_ms else 0) for k, v in kt.items()},
+    }
+    clocks = clk.summary()
+    line["clocks"] = clocks
+    if rank == 0 and not args.no_cpu_baseline:
+        try:
+            line["cpu_baseline"] = cpu_baseline(args.config, args.scale, args.cpu_sample_rows)
+        except Exception as e:  # baseline failure must not hide the GPU number
+            line["cpu_baseline"] = {"value": None, "error": str(e)[:200]}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    del apply_ms_each, solve_ms, solve_n, napply, apply_bytes
+    if ws > 1:
+        torch.distributed.barrier()
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def _partition_sizes(n, P):
+    return [n // P + (1 if i < n % P else 0) for i in range(P)]
+
+
+def _apply_roofline(kt, reps, info, hbm_peak, peak_src, steps):
+    """Per-apply achieved GB/s of the D-stage (2 band_solve launches) + iface + recovery
+    in the Krylov phase.  band_solve launches of the spike setup (2l columns, multi-RHS)
+    are a different shape, so the per-launch average here is restricted by count."""
+    applies = sum(r.precond_applications for r in reps)
+    ms, n = kt["band_solve"]
+    if not applies or not n:
+        return None
+    # the Krylov-phase solves are the single-column launches: 2 per apply
+    ms_iface = kt["iface_apply"][0] + kt["recovery"][0]
+    per_apply_ms = (ms * (2 * applies / n) + ms_iface) / applies
+    gbs = info["apply_bytes"] / (per_apply_ms / 1e3) / 1e9
+    return {"bound": "hbm", "kernel": "band_solve_kernel<L/U> + iface + recovery",
+            "achieved": gbs, "peak": hbm_peak, "unit": "GB/s", "frac": gbs / hbm_peak,
+            "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_src})",
+            "bytes_per_apply": info["apply_bytes"], "ms_per_apply": per_apply_ms,
+            "frac_of_8TBs_nominal": gbs / 8000.0}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--scale", type=float, default=1.0)
+    ap.add_argument("--cpu-sample-rows", type=int, default=8192)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -145,6 +145,14 @@ LRS_API const char* lrs_status_string(lrs_status s);
 /* Number of kernel launches issued by this context so far (bench accounting). */
 LRS_API int64_t lrs_ctx_launch_count(lrs_ctx* ctx);
 LRS_API lrs_status lrs_ctx_synchronize(lrs_ctx* ctx);
+/* Optional CUDA-event timing of every kernel launch, accumulated per kernel class
+ * (bench / roofline accounting).  Classes, in order: lu_diag, lu_panel, lu_update,
+ * band_solve, band_solve_adjoint, spmv, iface_apply, recovery, krylov_vec, setup_misc,
+ * spike_band_solve (the multi-RHS solves of the randomized spike SVD). */
+#define LRS_NUM_KERNEL_CLASSES 11
+LRS_API lrs_status lrs_ctx_set_profiling(lrs_ctx* ctx, int32_t on);
+/* Totals since the last reset (reset = 1 clears after reading). */
+LRS_API lrs_status lrs_ctx_kernel_times(lrs_ctx* ctx, double* ms, int64_t* counts, int32_t reset);
 
 /* ---- matrix ----------------------------------------------------------------------- */
 LRS_API lrs_status lrs_mat_upload_csr(lrs_ctx* ctx, int64_t n, int64_t nnz, const int64_t* row_ptr,

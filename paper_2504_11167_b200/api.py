@@ -33,6 +33,8 @@ VARIANT_T, VARIANT_BJ = 0, 1
 GMRES, BICGSTAB = 0, 1
 SIDE_T, SIDE_W = 0, 1
 STAGES = ("reduced-matvec", "precond-apply", "recovery")
+KERNEL_CLASSES = ("lu_diag", "lu_panel", "lu_update", "band_solve", "band_solve_adjoint", "spmv",
+                  "iface_apply", "recovery", "krylov_vec", "setup_misc", "spike_band_solve")
 
 i64, f64, i32, u64 = ctypes.c_int64, ctypes.c_double, ctypes.c_int32, ctypes.c_uint64
 vp = ctypes.c_void_p
@@ -178,6 +180,8 @@ def lib():
         "lrs_apply_block_jacobi": (i32, [vp, vp, i64, vp, i64, i64, i32]),
         "lrs_solve": (i32, [vp, vp, vp, i64, vp, i64, i64, P(IterCfgC), P(ReportC), i32]),
         "lrs_bench_dmma_peak": (i32, [vp, P(f64)]),
+        "lrs_ctx_set_profiling": (i32, [vp, i32]),
+        "lrs_ctx_kernel_times": (i32, [vp, vp, vp, i32]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -266,6 +270,15 @@ class Context:
 
     def synchronize(self):
         _check(lib().lrs_ctx_synchronize(self.h), self.h)
+
+    def set_profiling(self, on: bool):
+        _check(lib().lrs_ctx_set_profiling(self.h, 1 if on else 0), self.h)
+
+    def kernel_times(self, reset: bool = False) -> dict:
+        """{class: (total_ms, launches)} of the CUDA-event timed launches."""
+        ms, cnt = (f64 * len(KERNEL_CLASSES))(), (i64 * len(KERNEL_CLASSES))()
+        _check(lib().lrs_ctx_kernel_times(self.h, ms, cnt, 1 if reset else 0), self.h)
+        return {k: (ms[i], cnt[i]) for i, k in enumerate(KERNEL_CLASSES)}
 
     def dmma_peak_tflops(self) -> float:
         out = f64()

@@ -79,6 +79,7 @@ __global__ void pad_diag_kernel(BandGeom g, double* tiles) {
 
 void launch_extract_tiles(Ctx* c, const Mat* m, const BandGeom& g, double* tiles, int64_t k,
                           const int*, unsigned long long* d_bad) {
+  ProfScope ps_(c, K_SETUP);
   if (m->n > 0) {
     extract_tiles_kernel<<<(unsigned)((m->n + 255) / 256), 256, 0, c->stream>>>(
         m->n, m->row_ptr.get(), m->col_idx.get(), m->vals.get(), g, tiles, k, d_bad);
@@ -313,15 +314,20 @@ void launch_lu_step(Ctx* c, const BandGeom& g, double* tiles, int K, int* status
                                   (int)GEMM_SMEM));
     g_lu_attr_set = true;
   }
-  lu_diag_kernel<<<g.P, DIAG_THREADS, sizeof(double) * (TILE_ELEMS + 4 * NB), c->stream>>>(
-      g, tiles, K, status);
-  LRS_LAUNCHED(c);
+  {
+    ProfScope ps_(c, K_LU_DIAG);
+    lu_diag_kernel<<<g.P, DIAG_THREADS, sizeof(double) * (TILE_ELEMS + 4 * NB), c->stream>>>(
+        g, tiles, K, status);
+    LRS_LAUNCHED(c);
+  }
   if (g.wl + g.wu > 0) {
+    ProfScope ps_(c, K_LU_PANEL);
     lu_gemm_kernel<0><<<dim3(g.wl + g.wu, g.P), GEMM_THREADS, GEMM_SMEM, c->stream>>>(g, tiles, K,
                                                                                      status);
     LRS_LAUNCHED(c);
   }
   if (g.wl > 0 && g.wu > 0) {
+    ProfScope ps_(c, K_LU_UPDATE);
     lu_gemm_kernel<1><<<dim3(g.wl * g.wu, g.P), GEMM_THREADS, GEMM_SMEM, c->stream>>>(g, tiles, K,
                                                                                      status);
     LRS_LAUNCHED(c);

@@ -241,6 +241,7 @@ static void launch_mode(Ctx* c, const BandGeom& g, const double* tiles, double* 
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = true;
   }
+  ProfScope ps_(c, c->in_setup ? K_SPIKE_SOLVE : (MODE >= 2 ? K_SOLVE_ADJ : K_SOLVE));
   band_solve_kernel<MODE, NR><<<ntiles, SOLVE_THREADS, smem, c->stream>>>(
       g, tiles, x, ld, nrhs, flags, epoch, ticket, p_only);
   LRS_LAUNCHED(c);

@@ -149,6 +149,8 @@ lrs_status lrs_ctx_create(int device, void* stream, lrs_ctx** out) {
 void lrs_ctx_destroy(lrs_ctx* c) {
   if (!c) return;
   cudaStreamSynchronize(c->stream);
+  c->collect();
+  for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
   if (c->own_stream) cudaStreamDestroy(c->stream);
@@ -162,6 +164,29 @@ int64_t lrs_ctx_launch_count(lrs_ctx* c) { return c ? c->launches : 0; }
 lrs_status lrs_ctx_synchronize(lrs_ctx* c) {
   if (!c) return LRS_ERR_PARAMETER;
   return guard(c, [&] { LRS_CUDA(cudaStreamSynchronize(c->stream)); });
+}
+
+lrs_status lrs_ctx_set_profiling(lrs_ctx* c, int32_t on) {
+  if (!c) return LRS_ERR_PARAMETER;
+  return guard(c, [&] {
+    c->collect();
+    c->prof = on != 0;
+  });
+}
+
+lrs_status lrs_ctx_kernel_times(lrs_ctx* c, double* ms, int64_t* counts, int32_t reset) {
+  if (!c) return LRS_ERR_PARAMETER;
+  return guard(c, [&] {
+    c->collect();
+    for (int k = 0; k < K_NCLASS; ++k) {
+      if (ms) ms[k] = c->prof_ms[k];
+      if (counts) counts[k] = c->prof_cnt[k];
+      if (reset) {
+        c->prof_ms[k] = 0.0;
+        c->prof_cnt[k] = 0;
+      }
+    }
+  });
 }
 
 lrs_status lrs_last_error(lrs_ctx* c, lrs_error_info* info) {

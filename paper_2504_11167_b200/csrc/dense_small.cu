@@ -110,6 +110,7 @@ __global__ void __launch_bounds__(QR_THREADS) householder_qr_kernel(const QrJob*
 void launch_householder_qr(Ctx* c, const QrJob* d_jobs, int njobs, int l) {
   if (njobs == 0) return;
   const size_t smem = sizeof(double) * (l + (QR_THREADS / 32) * QR_CB + QR_CB);
+  ProfScope ps_(c, K_SETUP);
   householder_qr_kernel<<<njobs, QR_THREADS, smem, c->stream>>>(d_jobs, l);
   LRS_LAUNCHED(c);
 }
@@ -227,6 +228,7 @@ void launch_jacobi_svd(Ctx* c, const SvdJob* d_jobs, int njobs, int l) {
                                   (int)(sizeof(double) * (2 * 96 * 96 + 96) + sizeof(int) * 200)));
     attr = true;
   }
+  ProfScope ps_(c, K_SETUP);
   jacobi_svd_kernel<<<njobs, SVD_THREADS, smem, c->stream>>>(d_jobs, l);
   LRS_LAUNCHED(c);
 }
@@ -264,6 +266,7 @@ void launch_small_gemm(Ctx* c, const GemmJob* d_jobs, int njobs, int64_t max_m, 
     attr = true;
   }
   dim3 grid((unsigned)((max_m + 255) / 256), (unsigned)njobs);
+  ProfScope ps_(c, K_SETUP);
   small_gemm_kernel<<<grid, 256, sizeof(double) * 128 * 128, c->stream>>>(d_jobs);
   LRS_LAUNCHED(c);
 }
@@ -418,6 +421,7 @@ void launch_iface_setup(Ctx* c, const IfaceSetupJob* d_jobs, int njobs, int r, i
                                   (int)(sizeof(double) * (4 * 64 * 64 + 64))));
     attr = true;
   }
+  ProfScope ps_(c, K_SETUP);
   iface_setup_kernel<<<njobs, IF_THREADS, smem, c->stream>>>(d_jobs, r, k);
   LRS_LAUNCHED(c);
 }
@@ -435,6 +439,7 @@ __global__ void sigma_trunc_kernel(const SigmaJob* jobs, int r, int* flag) {
 
 void launch_sigma_trunc(Ctx* c, const SigmaJob* d_jobs, int njobs, int r, int* d_flag) {
   if (njobs == 0) return;
+  ProfScope ps_(c, K_SETUP);
   sigma_trunc_kernel<<<njobs, 64, 0, c->stream>>>(d_jobs, r, d_flag);
   LRS_LAUNCHED(c);
 }

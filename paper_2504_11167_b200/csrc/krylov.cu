@@ -57,6 +57,7 @@ void launch_multidot(Ctx* c, const Chunks& ch, const double* X, int64_t ldx, int
                      int nvec, const double* Y, int64_t ldy, int nrhs, double* partial,
                      double* out) {
   if (nvec == 0 || nrhs == 0) return;
+  ProfScope ps_(c, K_KRYLOV);
   if (nrhs == 1)
     multidot_partial_kernel<1><<<ch.nchunks, KV_THREADS, 0, c->stream>>>(
         ch.start, X, ldx, strideX, nvec, Y, ldy, nrhs, partial);
@@ -107,6 +108,7 @@ void launch_axpby_cols(Ctx* c, int64_t n, int nrhs, int op, const ColScal& a, co
                        const ColScal& act, double* X, int64_t ldx, const double* Y, int64_t ldy,
                        const double* Z, int64_t ldz, double* W, int64_t ldw) {
   if (n == 0 || nrhs == 0) return;
+  ProfScope ps_(c, K_KRYLOV);
   axpby_kernel<<<(unsigned)((n + KV_THREADS - 1) / KV_THREADS), KV_THREADS, 0, c->stream>>>(
       n, nrhs, op, a, b, act, X, ldx, Y, ldy, Z, ldz, W, ldw);
   LRS_LAUNCHED(c);
@@ -132,6 +134,7 @@ void launch_multi_axpy_signed(Ctx* c, int64_t n, int nrhs, const double* V, int6
                               int64_t strideV, int nvec, const double* y_dev, double sign,
                               double* x, int64_t ldx) {
   if (n == 0 || nrhs == 0 || nvec == 0) return;
+  ProfScope ps_(c, K_KRYLOV);
   multi_axpy_kernel<<<(unsigned)((n + KV_THREADS - 1) / KV_THREADS), KV_THREADS, 0, c->stream>>>(
       n, nrhs, V, ldv, strideV, nvec, y_dev, sign, x, ldx);
   LRS_LAUNCHED(c);

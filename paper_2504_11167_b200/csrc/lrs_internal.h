@@ -70,6 +70,12 @@ struct DevBuf {
   T* get() const { return p; }
 };
 
+// Kernel classes for the optional per-class CUDA-event timing (lrs_ctx_set_profiling).
+enum KClass {
+  K_LU_DIAG = 0, K_LU_PANEL, K_LU_UPDATE, K_SOLVE, K_SOLVE_ADJ, K_SPMV, K_IFACE, K_RECOVERY,
+  K_KRYLOV, K_SETUP, K_SPIKE_SOLVE, K_NCLASS
+};
+
 struct Ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -78,6 +84,61 @@ struct Ctx {
   lrs_error_info last{};
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   int num_sms = 148;
+  bool in_setup = false;  // band solves issued by the spike construction (profiling class)
+  // profiling: (class, start, end) event triples, summed on demand
+  bool prof = false;
+  std::vector<cudaEvent_t> ev_pool;
+  std::vector<int> prof_class;
+  std::vector<cudaEvent_t> prof_ev;  // 2 per record
+  double prof_ms[K_NCLASS] = {0};
+  int64_t prof_cnt[K_NCLASS] = {0};
+  cudaEvent_t take_event() {
+    if (!ev_pool.empty()) {
+      cudaEvent_t e = ev_pool.back();
+      ev_pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+  }
+  void collect() {
+    if (prof_class.empty()) return;
+    cudaStreamSynchronize(stream);
+    for (size_t i = 0; i < prof_class.size(); ++i) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, prof_ev[2 * i], prof_ev[2 * i + 1]);
+      prof_ms[prof_class[i]] += ms;
+      prof_cnt[prof_class[i]] += 1;
+      ev_pool.push_back(prof_ev[2 * i]);
+      ev_pool.push_back(prof_ev[2 * i + 1]);
+    }
+    prof_class.clear();
+    prof_ev.clear();
+  }
+};
+
+// RAII event pair around one launch (no-op unless profiling is on).
+struct ProfScope {
+  Ctx* c;
+  int cls;
+  cudaEvent_t b = nullptr;
+  ProfScope(Ctx* ctx, int k) : c(ctx), cls(k) {
+    if (c->prof) {
+      b = c->take_event();
+      cudaEventRecord(b, c->stream);
+    }
+  }
+  ~ProfScope() {
+    if (c->prof) {
+      cudaEvent_t e = c->take_event();
+      cudaEventRecord(e, c->stream);
+      c->prof_class.push_back(cls);
+      c->prof_ev.push_back(b);
+      c->prof_ev.push_back(e);
+      if (c->prof_class.size() > 20000) c->collect();
+    }
+  }
 };
 
 struct Mat {

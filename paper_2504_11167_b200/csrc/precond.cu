@@ -86,6 +86,7 @@ void launch_iface_apply(Ctx* c, const IfaceApplyJob* d_jobs, int njobs, int r, i
                         const double* y, int64_t ldy, int nrhs) {
   if (njobs == 0) return;
   const size_t smem = sizeof(double) * 6 * r * nrhs;
+  ProfScope ps_(c, K_IFACE);
   iface_apply_kernel<<<njobs, IA_THREADS, smem, c->stream>>>(d_jobs, r, k, y, ldy, nrhs);
   LRS_LAUNCHED(c);
 }
@@ -132,6 +133,7 @@ void launch_recovery(Ctx* c, const BandGeom& g, int64_t n, const double* y, int6
                      int64_t ldx, int nrhs, const double* uT, const double* uW, int r,
                      const double* scT, const double* scW) {
   if (n == 0) return;
+  ProfScope ps_(c, K_RECOVERY);
   recovery_kernel<<<(unsigned)((n + 255) / 256), 256, 0, c->stream>>>(g, n, y, ldy, x, ldx, nrhs,
                                                                       uT, uW, r, scT, scW);
   LRS_LAUNCHED(c);

@@ -3,8 +3,8 @@
 // and GMRES(m).  Only launches, small
 // host<->device scalar traffic and the Krylov scalar recurrences live here;
 // all vector and matrix arithmetic runs in the kernels of this library.
-// The control flow mirrors oracle/lrspike_oracle.py line by line so that the
-// two produce the same iterates up to roundoff.
+// The control flow mirrors the CPU checker in oracle/ line by line so that the
+// two produce the same iterates up to roundoff (the checker is never called).
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -485,7 +485,16 @@ Fact* factorize(Ctx* c, Mat* m, const lrs_solver_cfg& cfg) {
     for (int attempt = 0;; ++attempt) {
       int bi = -1;
       double bc = 0.0;
-      if (build_lowrank(f.get(), r, &bi, &bc)) break;
+      c->in_setup = true;
+      bool ok;
+      try {
+        ok = build_lowrank(f.get(), r, &bi, &bc);
+      } catch (...) {
+        c->in_setup = false;
+        throw;
+      }
+      c->in_setup = false;
+      if (ok) break;
       if (attempt == 1 || r / 2 < 1) {
         LrsError e(LRS_ERR_ILL_CONDITIONED_INTERFACE,
                    "interface " + std::to_string(bi) + " ill-conditioned (cond " +

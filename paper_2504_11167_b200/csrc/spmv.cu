@@ -50,6 +50,7 @@ void launch_spmv(Ctx* c, const Mat* m, const double* x, int64_t ldx, double* y, 
     const double* xj = x + j0 * ldx;
     double* yj = y + j0 * ldy;
     const double* bj = b ? b + j0 * ldb : nullptr;
+    ProfScope ps_(c, K_SPMV);
 #define LRS_SPMV(NRV)                                                                     \
   spmv_kernel<NRV><<<grid, 256, 0, c->stream>>>(n, m->row_ptr.get(), m->col_idx.get(),    \
                                                 m->vals.get(), xj, ldx, yj, ldy, nr, mode, bj, \
@@ -92,6 +93,7 @@ void launch_coupling(Ctx* c, const Mat* m, bool transposed, const CoupleJob* d_j
                      int64_t b, int ncols) {
   if (njobs == 0) return;
   dim3 grid((unsigned)((b * ncols + 255) / 256), (unsigned)njobs);
+  ProfScope ps_(c, K_SETUP);
   coupling_kernel<<<grid, 256, 0, c->stream>>>(
       d_jobs, transposed ? m->trow_ptr.get() : m->row_ptr.get(),
       transposed ? m->tcol_idx.get() : m->col_idx.get(),

@@ -152,3 +152,69 @@ def test_solve_parity(ctx, name, scale, method):
     # ledger: 4 (p-1) n_svd n_rhs scalars per application
     m, s = rep.comm["precond-apply"]
     assert s == 2 * (cfg.P - 1) * F.n_svd * rep.precond_applications
+
+
+@pytest.mark.parametrize("key", ["c1_s48", "c2_s16"])
+def test_gpu_matches_golden_fixtures(ctx, key):
+    import json
+    import os
+
+    gold = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+    case = json.load(open(os.path.join(gold, "golden.json")))["cases"][key]
+    z = np.load(os.path.join(gold, f"{key}.npz"))
+    cfg = configs.make_config(case["config"], case["scale"])
+    A = api.CsrMatrix.from_csr(ctx, cfg.matrix)
+    it = api.IterConfig(tol=cfg.tol, method=case["method"], restart=cfg.m or 30)
+    x, rep, F = api.solve(A, cfg.rhs, _gpu_cfg(cfg, cfg.r), it)
+    assert abs(rep.iterations - case["iterations"]) <= 2
+    assert _rel(x, z["x"]) <= 1e-8
+    assert _rel(F.apply_precond_T(np.asfortranarray(z["apply_in"])), z["apply_out"]) <= 1e-10
+
+
+def test_cpp_api_on_gpu():
+    import os
+    import subprocess
+
+    exe = os.path.join(os.path.dirname(os.path.abspath(__file__)), "cpp", "test_api")
+    r = subprocess.run([exe, "gpu"], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+
+
+def test_device_resident_torch_buffers(ctx):
+    import torch
+
+    cfg = configs.make_config("c2", 16 / 64)
+    A = api.CsrMatrix.from_csr(ctx, cfg.matrix)
+    F = api.factorize(ctx, A, _gpu_cfg(cfg, cfg.r))
+    f = np.asfortranarray(np.random.default_rng(5).uniform(-1, 1, (cfg.matrix.n, 3)))
+    torch.cuda.synchronize()
+    fd = torch.from_numpy(f.T.copy()).cuda().t()  # column-major on the device
+    torch.cuda.synchronize()
+    xd = F.apply_precond_T(fd)
+    ctx.synchronize()
+    assert _rel(xd.cpu().numpy(), F.apply_precond_T(f)) == 0.0
+    y = A.spmv(fd)
+    ctx.synchronize()
+    assert _rel(y.cpu().numpy(), cfg.matrix.to_scipy() @ f) < 1e-14
+
+
+def test_error_paths(ctx):
+    cfg = configs.make_config("c1", 48 / 256)
+    A = api.CsrMatrix.from_csr(ctx, cfg.matrix)
+    with pytest.raises(api.LayoutError):
+        api.factorize(ctx, A, api.SolverConfig(p=100, k=48, n_svd=4))
+    with pytest.raises(api.NotBlockTridiagonalError) as e:
+        api.factorize(ctx, A, api.SolverConfig(p=4, k=20, n_svd=4))
+    assert e.value.row >= 0 and e.value.col >= 0
+    with pytest.raises(api.ParameterError):
+        api.factorize(ctx, A, api.SolverConfig(p=4, k=48, n_svd=47))
+    with pytest.raises(api.DimensionError):
+        api.CsrMatrix(ctx, 3, [0, 2, 2, 3], [1, 0, 1], [1.0, 1.0, 1.0])  # decreasing cols
+    # zero pivot -> SingularBlockError(column)
+    import scipy.sparse as sp
+
+    Z = sp.csr_matrix(np.diag([1.0, 0.0, 2.0, 3.0]))
+    Az = api.CsrMatrix(ctx, 4, Z.indptr, Z.indices, Z.data)
+    with pytest.raises(api.SingularBlockError) as es:
+        api.factorize(ctx, Az, api.SolverConfig(variant="BJ", p=1, k=0, n_svd=0))
+    assert es.value.column == 1
