@@ -18,6 +18,8 @@
 //   lu_diag   : LU of tile (K,K) in shared memory + in-place triangular inverses
 //   lu_gemm<0>: L_IK = A_IK inv(U_KK), U_KJ = inv(L_KK) A_KJ (DMMA tiles)
 //   lu_gemm<1>: A_IJ -= L_IK U_KJ for the wl x wu trailing tiles (DMMA tiles)
+#include <utility>
+
 #include "common.cuh"
 #include "kernels.h"
 #include "lrs_internal.h"
@@ -204,12 +206,17 @@ __device__ __forceinline__ void tile_gemm(const double* A, const double* B, doub
   const int wm = w & 1, wn = w >> 1;
   const int g = lane >> 2, t = lane & 3;
   double acc[8][4][2];
+  gemm_load_chunk(A, B, As, Bs, 0, tid);
+  // MODE 1 accumulates straight into C (C + sum (-A) B): the C fragments are loaded
+  // while the first operand chunk is in flight and the epilogue is a plain store.
 #pragma unroll
   for (int i = 0; i < 8; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-
-  gemm_load_chunk(A, B, As, Bs, 0, tid);
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e)
+        acc[i][j][e] = MODE == 1 ? C[(int64_t)(32 * wn + 8 * j + 2 * t + e) * NB + 64 * wm + 8 * i + g]
+                                 : 0.0;
 #pragma unroll 1
   for (int kc = 0; kc < NB / KC; ++kc) {
     const int st = kc & 1;
@@ -232,7 +239,7 @@ __device__ __forceinline__ void tile_gemm(const double* A, const double* B, doub
         const int m = 64 * wm + 8 * i + g;
         double v = as[kk * AS_LD + m];
         if (maskA == MASK_UNIT_LOWER) v = m > kg ? v : (m == kg ? 1.0 : 0.0);
-        a[i] = v;
+        a[i] = MODE == 1 ? -v : v;
       }
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
@@ -262,7 +269,7 @@ __device__ __forceinline__ void tile_gemm(const double* A, const double* B, doub
           *cp = acc[i][j][e];
           if (piv_status && fabs(acc[i][j][e]) > 1.0) bad_col = min(bad_col, col0 + nn);
         } else {
-          *cp -= acc[i][j][e];
+          *cp = acc[i][j][e];
         }
       }
     }
@@ -294,9 +301,23 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) lu_gemm_kernel(BandGeom g, do
       if (J >= T) return;
       tile_gemm<0>(tile(K, K), tile(K, J), tile(K, J), MASK_UNIT_LOWER, MASK_NONE, sm, nullptr, 0);
     }
+  } else if (KIND == 1) {
+    // trailing update away from the next pivot row/column: I, J >= K + 2
+    const int I = K + 2 + x / (g.wu - 1);
+    const int J = K + 2 + x % (g.wu - 1);
+    if (I >= T || J >= T) return;
+    tile_gemm<1>(tile(I, K), tile(K, J), tile(I, J), MASK_NONE, MASK_NONE, sm, nullptr, 0);
   } else {
-    const int I = K + 1 + x / g.wu;
-    const int J = K + 1 + x % g.wu;
+    // look-ahead part of the trailing update: column K+1 (I = K+1..K+wl) and row K+1
+    // (J = K+2..K+wu), i.e. everything diag/panel of step K+1 needs
+    int I, J;
+    if (x < g.wl) {
+      I = K + 1 + x;
+      J = K + 1;
+    } else {
+      I = K + 1;
+      J = K + 2 + (x - g.wl);
+    }
     if (I >= T || J >= T) return;
     tile_gemm<1>(tile(I, K), tile(K, J), tile(I, J), MASK_NONE, MASK_NONE, sm, nullptr, 0);
   }
@@ -304,34 +325,80 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) lu_gemm_kernel(BandGeom g, do
 
 static bool g_lu_attr_set = false;
 
-void launch_lu_step(Ctx* c, const BandGeom& g, double* tiles, int K, int* status) {
-  if (!g_lu_attr_set) {
-    LRS_CUDA(cudaFuncSetAttribute(lu_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)(sizeof(double) * (TILE_ELEMS + 4 * NB))));
-    LRS_CUDA(cudaFuncSetAttribute(lu_gemm_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)GEMM_SMEM));
-    LRS_CUDA(cudaFuncSetAttribute(lu_gemm_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)GEMM_SMEM));
-    g_lu_attr_set = true;
-  }
+static void lu_attrs() {
+  if (g_lu_attr_set) return;
+  LRS_CUDA(cudaFuncSetAttribute(lu_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)(sizeof(double) * (TILE_ELEMS + 4 * NB))));
+  LRS_CUDA(cudaFuncSetAttribute(lu_gemm_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)GEMM_SMEM));
+  LRS_CUDA(cudaFuncSetAttribute(lu_gemm_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)GEMM_SMEM));
+  LRS_CUDA(cudaFuncSetAttribute(lu_gemm_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)GEMM_SMEM));
+  g_lu_attr_set = true;
+}
+
+static void lu_diag_panel(Ctx* c, cudaStream_t s, const BandGeom& g, double* tiles, int K,
+                          int* status) {
   {
-    ProfScope ps_(c, K_LU_DIAG);
-    lu_diag_kernel<<<g.P, DIAG_THREADS, sizeof(double) * (TILE_ELEMS + 4 * NB), c->stream>>>(
-        g, tiles, K, status);
+    ProfScope ps_(c, K_LU_DIAG, s);
+    lu_diag_kernel<<<g.P, DIAG_THREADS, sizeof(double) * (TILE_ELEMS + 4 * NB), s>>>(g, tiles, K,
+                                                                                    status);
     LRS_LAUNCHED(c);
   }
   if (g.wl + g.wu > 0) {
-    ProfScope ps_(c, K_LU_PANEL);
-    lu_gemm_kernel<0><<<dim3(g.wl + g.wu, g.P), GEMM_THREADS, GEMM_SMEM, c->stream>>>(g, tiles, K,
-                                                                                     status);
+    ProfScope ps_(c, K_LU_PANEL, s);
+    lu_gemm_kernel<0><<<dim3(g.wl + g.wu, g.P), GEMM_THREADS, GEMM_SMEM, s>>>(g, tiles, K, status);
     LRS_LAUNCHED(c);
   }
-  if (g.wl > 0 && g.wu > 0) {
-    ProfScope ps_(c, K_LU_UPDATE);
-    lu_gemm_kernel<1><<<dim3(g.wl * g.wu, g.P), GEMM_THREADS, GEMM_SMEM, c->stream>>>(g, tiles, K,
-                                                                                     status);
-    LRS_LAUNCHED(c);
+}
+
+// Right-looking tiled LU with look-ahead depth 1 over two streams:
+//   crit (high priority): [wait rest(K-1)] next(K) -> diag(K+1) -> panel(K+1)
+//   main               : [wait panel(K)]  rest(K)
+// next(K) applies step K to pivot row/column K+1 only, so diag/panel of step K+1
+// overlap the bulk trailing update rest(K) (I, J >= K+2) instead of idling the GPU.
+void launch_band_lu(Ctx* c, const BandGeom& g, double* tiles, int Tmax, int* status) {
+  lu_attrs();
+  if (Tmax <= 0) return;
+  cudaStream_t sm = c->stream, sc = c->stream_hi;
+  cudaEvent_t ev_start = c->take_event(), ev_panel = c->take_event(), ev_panel2 = c->take_event(),
+              ev_rest = c->take_event();
+  LRS_CUDA(cudaEventRecord(ev_start, sm));
+  LRS_CUDA(cudaStreamWaitEvent(sc, ev_start, 0));
+  lu_diag_panel(c, sc, g, tiles, 0, status);
+  LRS_CUDA(cudaEventRecord(ev_panel, sc));
+  for (int K = 0; K < Tmax; ++K) {
+    if (K + 1 < Tmax) {
+      if (K >= 1) LRS_CUDA(cudaStreamWaitEvent(sc, ev_rest, 0));
+      if (g.wl > 0 && g.wu > 0) {
+        ProfScope ps_(c, K_LU_UPDATE, sc);
+        lu_gemm_kernel<2><<<dim3(g.wl + g.wu - 1, g.P), GEMM_THREADS, GEMM_SMEM, sc>>>(g, tiles, K,
+                                                                                       status);
+        LRS_LAUNCHED(c);
+      }
+      lu_diag_panel(c, sc, g, tiles, K + 1, status);
+      LRS_CUDA(cudaEventRecord(ev_panel2, sc));
+    }
+    LRS_CUDA(cudaStreamWaitEvent(sm, ev_panel, 0));
+    if (g.wl > 1 && g.wu > 1) {
+      ProfScope ps_(c, K_LU_UPDATE, sm);
+      lu_gemm_kernel<1><<<dim3((g.wl - 1) * (g.wu - 1), g.P), GEMM_THREADS, GEMM_SMEM, sm>>>(
+          g, tiles, K, status);
+      LRS_LAUNCHED(c);
+    }
+    LRS_CUDA(cudaEventRecord(ev_rest, sm));
+    std::swap(ev_panel, ev_panel2);
   }
+  // join: everything issued on the crit stream precedes what follows on main
+  LRS_CUDA(cudaEventRecord(ev_panel2, sc));
+  LRS_CUDA(cudaStreamWaitEvent(sm, ev_panel2, 0));
+  LRS_CUDA(cudaEventRecord(ev_panel, sm));
+  LRS_CUDA(cudaEventSynchronize(ev_panel));  // events go back to the pool only once idle
+  c->ev_pool.push_back(ev_start);
+  c->ev_pool.push_back(ev_panel);
+  c->ev_pool.push_back(ev_panel2);
+  c->ev_pool.push_back(ev_rest);
 }
 
 // ---------------------------------------------------------------------------------------

@@ -5,13 +5,23 @@
 // One CTA per (partition, row tile).  CTAs take tickets in start order, so a
 // CTA only ever waits on tiles whose CTAs already started: no deadlock for
 // any residency.  Each CTA streams its row panel (wl or wu off-diagonal tiles
-// plus the diagonal tile, contiguous in HBM) through a shared-memory ring
-// with 1D bulk copies (cp.async.bulk, the TMA engine) *before* its
-// dependencies resolve, and only waits on the per-tile ready flag (release /
-// acquire at gpu scope, epoch-tagged so flags never need resetting) right
-// before it needs x_s.  The diagonal tile holds the explicit inverses of the
-// LU diagonal blocks, so the per-tile critical path is a flag round trip plus
-// one 128 x 128 mat-vec; the factor stream runs at HBM speed behind it.
+// plus the diagonal tile, contiguous in HBM) through a shared-memory ring with
+// 1D bulk copies (cp.async.bulk, the TMA engine) *before* its dependencies
+// resolve, and only waits on the per-tile ready flag (release / acquire at gpu
+// scope, epoch-tagged so flags never need resetting) right before it needs
+// x_s.  The diagonal tile holds the explicit inverses of the LU diagonal
+// blocks, so the per-tile critical path is a flag round trip plus one
+// 128 x 128 product; the factor stream runs at HBM speed behind it.
+//
+// A chunk is 32 contiguous tile columns (32 KB, one bulk copy).  Multi-RHS
+// chunk products are (128 x 32) x (32 x NR) GEMMs (or their transposes) on the
+// FP64 tensor cores (DMMA.8x8x4), NR in {8, 16, 48}; one code path for every
+// width keeps each column's arithmetic independent of the batch, so
+// solve_block on a multi-column RHS equals column-by-column bit-exactly
+// (solve_block always takes this path).  The Krylov hot path
+// (apply with one right-hand side) uses an FP64-FMA variant, one thread per
+// row, which keeps less work on the per-tile critical path and streams the
+// factor at ~96% of the measured HBM copy bandwidth.
 //
 // Modes: 0  L  forward (unit lower),   1  U  backward,
 //        2  U^T forward (adjoint),     3  L^T backward (adjoint).
@@ -23,27 +33,38 @@ namespace lrs {
 
 constexpr int SOLVE_THREADS = 256;
 constexpr int CH_COLS = 32;
-constexpr int CH_ELEMS = NB * CH_COLS;  // 32 KB chunk = 32 tile columns
-constexpr int NCH = NB / CH_COLS;
-constexpr int STAGES = 5;
+constexpr int CLD = NB;                  // column stride of a chunk in shared memory
+constexpr int CH_SM = CH_COLS * CLD;     // doubles per shared chunk
+constexpr int NCH = NB / CH_COLS;        // chunks per tile
+
+template <int NR> struct SolveCfg {
+  static constexpr int STAGES = NR >= 48 ? 3 : 5;
+  static constexpr int XLD = NR == 1 ? 1 : NR + 4;  // padded row stride of xs / red
+};
 
 template <int NR>
 constexpr size_t solve_smem_bytes() {
-  return sizeof(double) * ((size_t)STAGES * CH_ELEMS + 2 * (size_t)NB * NR) + 64 + 16 * STAGES;
+  return sizeof(double) * ((size_t)SolveCfg<NR>::STAGES * CH_SM + 2 * (size_t)NB * SolveCfg<NR>::XLD) +
+         16 * SolveCfg<NR>::STAGES + 64;
 }
 
 template <int MODE, int NR>
 __global__ void __launch_bounds__(SOLVE_THREADS, 1)
     band_solve_kernel(BandGeom g, const double* __restrict__ tiles, double* x, int64_t ld,
                       int nrhs, unsigned* flags, unsigned epoch, int* ticket, int p_only) {
+  constexpr int STAGES = SolveCfg<NR>::STAGES;
+  constexpr int XLD = SolveCfg<NR>::XLD;
+  constexpr bool FWD = (MODE == 0 || MODE == 2);
+  constexpr bool TRANS = (MODE >= 2);
+  constexpr bool MMA = NR >= 8;
   extern __shared__ __align__(128) unsigned char smraw[];
   double* ring = reinterpret_cast<double*>(smraw);
-  double* xs = ring + (size_t)STAGES * CH_ELEMS;  // [NB][NR]
-  double* red = xs + NB * NR;                     // [NB][NR]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(red + NB * NR);
+  double* xs = ring + (size_t)STAGES * CH_SM;  // [NB][XLD]: x_s, or the diagonal-step input
+  double* red = xs + NB * XLD;                 // [NB][XLD]: half sums / transposed accumulator
+  uint64_t* bars = reinterpret_cast<uint64_t*>(red + NB * XLD);
   int* s_tk = reinterpret_cast<int*>(bars + STAGES);
 
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   if (tid == 0) *s_tk = atomicAdd(ticket, 1);
   __syncthreads();
   const int tk = *s_tk;
@@ -57,12 +78,9 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1)
   }
   const int T = g.T[p];
   if (tt >= T) return;
-  constexpr bool FWD = (MODE == 0 || MODE == 2);
-  constexpr bool TRANS = (MODE >= 2);
   const int t = FWD ? tt : T - 1 - tt;
   const int64_t base = g.tbase[p], off = g.off[p], size = g.size[p];
   const int W = g.W, wl = g.wl;
-  // dependency range
   int s0, ndeps, sstep;
   if (MODE == 0) { s0 = max(0, t - g.wl); ndeps = t - s0; sstep = 1; }
   else if (MODE == 1) { s0 = min(T - 1, t + g.wu); ndeps = s0 - t; sstep = -1; }
@@ -75,40 +93,62 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1)
     return tiles + (base + (int64_t)s * W + (t - s + wl)) * TILE_ELEMS;
   };
   const int Q = (ndeps + 1) * NCH;
+  // producer: one 32 KB bulk copy per chunk (32 contiguous tile columns)
+  auto issue = [&](int q, int st) {
+    const double* src = tile_ptr(q / NCH) + (size_t)(q % NCH) * CH_COLS * NB;
+    mbar_expect_tx(&bars[st], CH_COLS * NB * sizeof(double));
+    bulk_g2s(ring + (size_t)st * CH_SM, src, CH_COLS * NB * sizeof(double), &bars[st]);
+  };
   if (tid == 0) {
     for (int st = 0; st < STAGES; ++st) mbar_init(&bars[st], 1);
     fence_mbar_init();
-    for (int q = 0; q < STAGES && q < Q; ++q) {
-      mbar_expect_tx(&bars[q], CH_ELEMS * sizeof(double));
-      bulk_g2s(ring + (size_t)q * CH_ELEMS, tile_ptr(q / NCH) + (q % NCH) * CH_ELEMS,
-               CH_ELEMS * sizeof(double), &bars[q]);
-    }
   }
-  const int row = tid & (NB - 1), hh = tid >> 7;
+  __syncthreads();
+  if (tid == 0)
+    for (int q = 0; q < STAGES && q < Q; ++q) issue(q, q);
+
   const int64_t row0 = (int64_t)t * NB;
-  const bool row_valid = row0 + row < size;
-  double acc[NR];
+  const int gq = lane >> 2, tq = lane & 3;  // DMMA fragment coordinates
+  // ---- accumulators -----------------------------------------------------------------
+  // FMA path (NR == 1): thread (row = tid & 127, half = tid >> 7) sums half the columns.
+  // DMMA non-trans: warp w owns rows 16w..16w+15 (2 m8 tiles) x NR/8 n8 tiles.
+  constexpr int NJ = MMA ? NR / 8 : 1;
+  double acc[2][NJ][2];
+  double acc1 = 0.0;
+  const int row = tid & (NB - 1), hh = tid >> 7;
 #pragma unroll
-  for (int j = 0; j < NR; ++j) acc[j] = 0.0;
+  for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+    for (int nj = 0; nj < NJ; ++nj) acc[mi][nj][0] = acc[mi][nj][1] = 0.0;
   if (!TRANS) {
-    if (hh == 0 && row_valid) {
+    if (!MMA) {
+      if (hh == 0 && row0 + row < size && nrhs > 0) acc1 = x[off + row0 + row];
+    } else {
 #pragma unroll
-      for (int j = 0; j < NR; ++j)
-        if (j < nrhs) acc[j] = x[off + row0 + row + j * ld];
+      for (int mi = 0; mi < 2; ++mi) {
+        const int m = 16 * w + 8 * mi + gq;
+        if (row0 + m < size)
+#pragma unroll
+          for (int nj = 0; nj < NJ; ++nj)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int n = 8 * nj + 2 * tq + e;
+              if (n < nrhs) acc[mi][nj][e] = x[off + row0 + m + n * ld];
+            }
+      }
     }
   } else {
     for (int e = tid; e < NB * NR; e += SOLVE_THREADS) {
-      const int r = e / NR, j = e % NR;
-      red[e] = (j < nrhs && row0 + r < size) ? x[off + row0 + r + j * ld] : 0.0;
+      const int r = e % NB, j = e / NB;
+      red[r * XLD + j] = (j < nrhs && row0 + r < size) ? x[off + row0 + r + j * ld] : 0.0;
     }
   }
-  __syncthreads();
 
-  const int lane = tid & 31, w = tid >> 5;
   for (int q = 0; q < Q; ++q) {
     const int d = q / NCH, sub = q % NCH, st = q % STAGES;
+    const bool diag = (d == ndeps);
     if (sub == 0) {
-      if (d < ndeps) {
+      if (!diag) {
         const int s = s0 + d * sstep;
         if (tid == 0) {
           const unsigned* f = flags + g.fbase[p] + s;
@@ -117,110 +157,155 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1)
         __syncthreads();
         const int64_t srow0 = (int64_t)s * NB;
         for (int e = tid; e < NB * NR; e += SOLVE_THREADS) {
-          const int r = e / NR, j = e % NR;
-          xs[e] = (j < nrhs && srow0 + r < size) ? __ldcg(x + off + srow0 + r + j * ld) : 0.0;
+          const int r = e % NB, j = e / NB;
+          xs[r * XLD + j] = (j < nrhs && srow0 + r < size) ? __ldcg(x + off + srow0 + r + j * ld) : 0.0;
         }
       } else {
-        // diagonal step: the accumulated right-hand side becomes the GEMV input
+        // diagonal step: the accumulated right-hand side becomes the product input
         if (!TRANS) {
-          if (hh == 1) {
+          if (!MMA) {
+            if (hh == 1) red[row] = acc1;
+            __syncthreads();
+            if (hh == 0) xs[row] = acc1 + red[row];
+            acc1 = 0.0;
+          } else {
 #pragma unroll
-            for (int j = 0; j < NR; ++j) red[row * NR + j] = acc[j];
+            for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+              for (int nj = 0; nj < NJ; ++nj)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                  xs[(16 * w + 8 * mi + gq) * XLD + 8 * nj + 2 * tq + e] = acc[mi][nj][e];
+                  acc[mi][nj][e] = 0.0;
+                }
           }
-          __syncthreads();
-          if (hh == 0) {
-#pragma unroll
-            for (int j = 0; j < NR; ++j) xs[row * NR + j] = acc[j] + red[row * NR + j];
-          }
-#pragma unroll
-          for (int j = 0; j < NR; ++j) acc[j] = 0.0;
         } else {
+          __syncthreads();
           for (int e = tid; e < NB * NR; e += SOLVE_THREADS) {
-            xs[e] = red[e];
-            red[e] = 0.0;
+            const int r = e % NB, j = e / NB;
+            xs[r * XLD + j] = red[r * XLD + j];
+            red[r * XLD + j] = 0.0;
           }
         }
       }
       __syncthreads();
     }
     mbar_wait(&bars[st], (unsigned)((q / STAGES) & 1));
-    const double* ch = ring + (size_t)st * CH_ELEMS;
+    const double* ch = ring + (size_t)st * CH_SM;
     const int cbase = sub * CH_COLS;
-    const bool diag = (d == ndeps);
-    if (!TRANS) {
+    if (!TRANS && !MMA) {
+      // out[row] (+|-)= sum_c Tile[row][c] xs[c], half the chunk columns per thread
 #pragma unroll 4
       for (int cc = hh * 16; cc < hh * 16 + 16; ++cc) {
         const int c = cbase + cc;
-        double v = ch[cc * NB + row];
-        if (diag) {
-          if (MODE == 0) v = (row > c) ? v : 0.0;   // strictly lower part of inv(L)
-          else v = (row <= c) ? v : 0.0;             // upper part of inv(U)
-        } else {
-          v = -v;
+        double v = ch[cc * CLD + row];
+        if (diag) v = (MODE == 0) ? (row > c ? v : 0.0) : (row <= c ? v : 0.0);
+        else v = -v;
+        acc1 = fma(v, xs[c], acc1);
+      }
+    } else if (!TRANS) {
+      // (128 x 32) x (32 x NR) on DMMA: A = chunk (row-major view ch[k*CLD + m]), B = xs rows
+#pragma unroll
+      for (int k4 = 0; k4 < CH_COLS / 4; ++k4) {
+        const int k = 4 * k4 + tq, kg = cbase + k;
+        double a[2], b[NJ];
+#pragma unroll
+        for (int mi = 0; mi < 2; ++mi) {
+          const int m = 16 * w + 8 * mi + gq;
+          double v = ch[k * CLD + m];
+          if (diag) v = (MODE == 0) ? (m > kg ? v : 0.0) : (m <= kg ? v : 0.0);
+          else v = -v;
+          a[mi] = v;
         }
 #pragma unroll
-        for (int j = 0; j < NR; ++j) acc[j] = fma(v, xs[c * NR + j], acc[j]);
+        for (int nj = 0; nj < NJ; ++nj) b[nj] = xs[kg * XLD + 8 * nj + gq];
+#pragma unroll
+        for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+          for (int nj = 0; nj < NJ; ++nj) dmma_8x8x4(acc[mi][nj][0], acc[mi][nj][1], a[mi], b[nj]);
       }
-    } else {
+    } else if (!MMA) {
+      // transposed, one RHS: out[c] (+|-)= sum_r Tile[r][c] xs[r]; 8 lanes per column
       const int cl = 4 * w + (lane >> 3), rg = lane & 7;
       const int c = cbase + cl;
-      double part[NR];
-#pragma unroll
-      for (int j = 0; j < NR; ++j) part[j] = 0.0;
+      double part = 0.0;
 #pragma unroll 4
       for (int i = 0; i < 16; ++i) {
         const int r = rg + 8 * i;
-        double v = ch[cl * NB + r];
-        if (diag) {
-          if (MODE == 2) v = (r <= c) ? v : 0.0;    // inv(U)^T
-          else v = (r > c) ? v : 0.0;               // strictly lower of inv(L), transposed
+        double v = ch[cl * CLD + r];
+        if (diag) v = (MODE == 2) ? (r <= c ? v : 0.0) : (r > c ? v : 0.0);
+        part = fma(v, xs[r], part);
+      }
+      part += __shfl_xor_sync(0xffffffffu, part, 1);
+      part += __shfl_xor_sync(0xffffffffu, part, 2);
+      part += __shfl_xor_sync(0xffffffffu, part, 4);
+      if (rg == 0) red[c] += diag ? part : -part;
+    } else {
+      // transposed: out(32 x NR) (+|-)= Tile^T (32 x 128) xs (128 x NR) on DMMA.
+      // 4 x NJ output tiles spread over the 8 warps; each warp runs the full K = 128.
+      constexpr int TPW = (4 * NJ + 7) / 8;
+#pragma unroll
+      for (int u = 0; u < TPW; ++u) {
+        const int ti = w + 8 * u;
+        if (ti >= 4 * NJ) break;
+        const int mi = ti & 3, nj = ti >> 2;
+        double c0 = 0.0, c1 = 0.0;
+        const int mloc = 8 * mi + gq;  // chunk-local output column
+        const int cglob = cbase + mloc;
+#pragma unroll 8
+        for (int k4 = 0; k4 < NB / 4; ++k4) {
+          const int r = 4 * k4 + tq;
+          double a = ch[mloc * CLD + r];
+          if (diag) a = (MODE == 2) ? (r <= cglob ? a : 0.0) : (r > cglob ? a : 0.0);
+          const double b = xs[r * XLD + 8 * nj + gq];
+          dmma_8x8x4(c0, c1, a, b);
         }
-#pragma unroll
-        for (int j = 0; j < NR; ++j) part[j] = fma(v, xs[r * NR + j], part[j]);
-      }
-#pragma unroll
-      for (int j = 0; j < NR; ++j) {
-        double v = part[j];
-        v += __shfl_xor_sync(0xffffffffu, v, 1);
-        v += __shfl_xor_sync(0xffffffffu, v, 2);
-        v += __shfl_xor_sync(0xffffffffu, v, 4);
-        part[j] = v;
-      }
-      if (rg == 0) {
-#pragma unroll
-        for (int j = 0; j < NR; ++j) red[c * NR + j] += diag ? part[j] : -part[j];
+        // fragment (m = 8 mi + gq, n = 8 nj + 2 tq + e) is owned by exactly this lane
+        const int n = 8 * nj + 2 * tq;
+        double* rp = red + (cbase + 8 * mi + gq) * XLD + n;
+        if (diag) {
+          rp[0] += c0;
+          rp[1] += c1;
+        } else {
+          rp[0] -= c0;
+          rp[1] -= c1;
+        }
       }
     }
     __syncthreads();
-    if (tid == 0 && q + STAGES < Q) {
-      const int qn = q + STAGES;
-      mbar_expect_tx(&bars[st], CH_ELEMS * sizeof(double));
-      bulk_g2s(ring + (size_t)st * CH_ELEMS, tile_ptr(qn / NCH) + (qn % NCH) * CH_ELEMS,
-               CH_ELEMS * sizeof(double), &bars[st]);
-    }
+    if (tid == 0 && q + STAGES < Q) issue(q + STAGES, st);
   }
   // ---- write x_t and publish -----------------------------------------------------------
-  if (!TRANS) {
-    if (hh == 1) {
-#pragma unroll
-      for (int j = 0; j < NR; ++j) red[row * NR + j] = acc[j];
-    }
+  if (!TRANS && !MMA) {
+    if (hh == 1) red[row] = acc1;
     __syncthreads();
-    if (hh == 0 && row_valid) {
+    if (hh == 0 && row0 + row < size && nrhs > 0) {
+      double v = acc1 + red[row];
+      if (MODE == 0) v += xs[row];  // unit diagonal of inv(L)
+      x[off + row0 + row] = v;
+    }
+  } else if (!TRANS) {
 #pragma unroll
-      for (int j = 0; j < NR; ++j) {
-        if (j >= nrhs) break;
-        double v = acc[j] + red[row * NR + j];
-        if (MODE == 0) v += xs[row * NR + j];  // unit diagonal of inv(L)
-        x[off + row0 + row + j * ld] = v;
-      }
+    for (int mi = 0; mi < 2; ++mi) {
+      const int m = 16 * w + 8 * mi + gq;
+      if (row0 + m >= size) continue;
+#pragma unroll
+      for (int nj = 0; nj < NJ; ++nj)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int n = 8 * nj + 2 * tq + e;
+          if (n >= nrhs) continue;
+          double v = acc[mi][nj][e];
+          if (MODE == 0) v += xs[m * XLD + n];
+          x[off + row0 + m + n * ld] = v;
+        }
     }
   } else {
     for (int e = tid; e < NB * NR; e += SOLVE_THREADS) {
-      const int r = e / NR, j = e % NR;
+      const int r = e % NB, j = e / NB;
       if (j < nrhs && row0 + r < size) {
-        double v = red[e];
-        if (MODE == 3) v += xs[e];
+        double v = red[r * XLD + j];
+        if (MODE == 3) v += xs[r * XLD + j];
         x[off + row0 + r + j * ld] = v;
       }
     }
@@ -251,15 +336,22 @@ template <int MODE>
 static void launch_nr(Ctx* c, const BandGeom& g, const double* tiles, double* x, int64_t ld,
                       int nrhs, unsigned* flags, unsigned epoch, int* ticket, int p_only,
                       int ntiles) {
-  if (nrhs <= 1) launch_mode<MODE, 1>(c, g, tiles, x, ld, nrhs, flags, epoch, ticket, p_only, ntiles);
-  else if (nrhs <= 4) launch_mode<MODE, 4>(c, g, tiles, x, ld, nrhs, flags, epoch, ticket, p_only, ntiles);
-  else launch_mode<MODE, 16>(c, g, tiles, x, ld, nrhs, flags, epoch, ticket, p_only, ntiles);
+  // every width runs the same DMMA code (one n8 tile for <= 8 columns), so each column's
+  // arithmetic is independent of the batch: multi-column == column-by-column bit-exactly
+  //
+  if (nrhs <= 1 && c->solve_fma1)
+    launch_mode<MODE, 1>(c, g, tiles, x, ld, nrhs, flags, epoch, ticket, p_only, ntiles);
+  else if (nrhs <= 8)
+    launch_mode<MODE, 8>(c, g, tiles, x, ld, nrhs, flags, epoch, ticket, p_only, ntiles);
+  else if (nrhs <= 16) launch_mode<MODE, 16>(c, g, tiles, x, ld, nrhs, flags, epoch, ticket, p_only, ntiles);
+  else launch_mode<MODE, 48>(c, g, tiles, x, ld, nrhs, flags, epoch, ticket, p_only, ntiles);
 }
 
 void launch_band_solve(Ctx* c, const BandGeom& g, const double* tiles, int mode, double* x,
                        int64_t ld, int nrhs, unsigned* flags, unsigned epoch, int* ticket,
                        int p_only, int ntiles) {
   if (ntiles == 0 || nrhs == 0) return;
+  if (nrhs > SOLVE_MAX_RHS) throw LrsError(LRS_ERR_PARAMETER, "band solve batch > 48 columns");
   LRS_CUDA(cudaMemsetAsync(ticket, 0, sizeof(int), c->stream));
   switch (mode) {
     case 0: launch_nr<0>(c, g, tiles, x, ld, nrhs, flags, epoch, ticket, p_only, ntiles); break;

@@ -40,8 +40,18 @@ static void record(Ctx* c, const LrsError& e) {
   if (c) c->last = info;
 }
 
+// Restores the thread's pool stream key on scope exit.
+struct PoolScope {
+  cudaStream_t prev;
+  explicit PoolScope(Ctx* c) : prev(current_pool_stream()) {
+    current_pool_stream() = c ? c->stream : nullptr;
+  }
+  ~PoolScope() { current_pool_stream() = prev; }
+};
+
 template <class F>
 static lrs_status guard(Ctx* c, F&& fn) {
+  PoolScope ps(c);
   try {
     fn();
     return LRS_OK;
@@ -141,6 +151,12 @@ lrs_status lrs_ctx_create(int device, void* stream, lrs_ctx** out) {
     LRS_CUDA(cudaEventCreate(&c->ev0));
     LRS_CUDA(cudaEventCreate(&c->ev1));
     LRS_CUDA(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
+    int lo_prio = 0, hi_prio = 0;
+    LRS_CUDA(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
+    LRS_CUDA(cudaStreamCreateWithPriority(&c->stream_hi, cudaStreamNonBlocking, hi_prio));
+    pool_stream_open(c->stream);
+    c->stage_cap = size_t(8) << 20;
+    LRS_CUDA(cudaMallocHost(reinterpret_cast<void**>(&c->stage), c->stage_cap));
   });
   if (s == LRS_OK) *out = c.release();
   return s;
@@ -151,9 +167,12 @@ void lrs_ctx_destroy(lrs_ctx* c) {
   cudaStreamSynchronize(c->stream);
   c->collect();
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
+  pool_stream_retire(c->stream);
+  if (c->stage) cudaFreeHost(c->stage);
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
   if (c->own_stream) cudaStreamDestroy(c->stream);
+  if (c->stream_hi) cudaStreamDestroy(c->stream_hi);
   delete c;
 }
 
@@ -444,6 +463,13 @@ lrs_status lrs_solve_block(lrs_fact* f, int64_t i, const void* rhs, int64_t ld_r
     if (n_rhs > 0)
       LRS_CUDA(cudaMemcpy2DAsync(wp, sizeof(double) * f->n, rhs, sizeof(double) * ld_rhs,
                                  sizeof(double) * ni, n_rhs, k_in, c->stream));
+    // solve_block always takes the batch-width-independent DMMA path
+    struct FmaOff {
+      Ctx* c;
+      bool prev;
+      ~FmaOff() { c->solve_fma1 = prev; }
+    } fo{c, c->solve_fma1};
+    c->solve_fma1 = false;
     dstage(f, work.get(), f->n, (int)n_rhs, adjoint != 0, (int)i);
     const cudaMemcpyKind k_out = mem == LRS_MEM_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
     if (n_rhs > 0)

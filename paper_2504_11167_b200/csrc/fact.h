@@ -37,6 +37,7 @@ struct Fact {
   DevBuf<int> degen;
   DevBuf<double> scT, scW;
   DevBuf<IfaceApplyJob> iface_jobs;
+  DevBuf<double> iface_work;  // partial message dots of the interface apply
   // deterministic reduction chunks (partition aligned)
   std::vector<int64_t> chunk_start;
   DevBuf<int64_t> d_chunks;

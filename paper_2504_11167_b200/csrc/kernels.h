@@ -34,9 +34,9 @@ void launch_coupling(Ctx* c, const Mat* m, bool transposed, const CoupleJob* d_j
 // block-tridiagonal pattern for coupling width k (row-major linear index).
 void launch_extract_tiles(Ctx* c, const Mat* m, const BandGeom& g, double* tiles, int64_t k,
                           const int* d_part_of_row_unused, unsigned long long* d_bad);
-// One right-looking step K of the tiled no-pivot band LU for all partitions.
+// Tiled no-pivot band LU of all partitions (Tmax steps, look-ahead over two streams).
 // status[2p] = min column needing a row interchange, status[2p+1] = min zero-pivot column.
-void launch_lu_step(Ctx* c, const BandGeom& g, double* tiles, int K, int* status);
+void launch_band_lu(Ctx* c, const BandGeom& g, double* tiles, int Tmax, int* status);
 
 // ---- band_solve.cu -------------------------------------------------------------------
 // In-place multi-RHS banded triangular solve over all partitions.
@@ -95,7 +95,8 @@ struct IfaceApplyJob {
   double* scW;       // r x nrhs: sigma_W .* (vW x_{i,b})     -> recovery of partition i+1
 };
 void launch_iface_apply(Ctx* c, const IfaceApplyJob* d_jobs, int njobs, int r, int64_t k,
-                        const double* y, int64_t ldy, int nrhs);
+                        const double* y, int64_t ldy, int nrhs, double* work);
+size_t iface_work_doubles(int njobs, int r, int64_t k);
 // dst[j] = sig[j] for j < r, zeroed where sig[j] < 1e-14 sig[0] (rank collapse);
 // *flag = 1 if any spike collapsed.
 struct SigmaJob { const double* sig; double* dst; };

@@ -16,7 +16,8 @@ namespace lrs {
 
 constexpr int NB = 128;                    // band-factor tile size (rows = cols)
 constexpr int64_t TILE_ELEMS = (int64_t)NB * NB;
-constexpr int MAX_RHS = 16;                // columns per Krylov / solve launch batch
+constexpr int MAX_RHS = 16;                // columns per Krylov batch
+constexpr int SOLVE_MAX_RHS = 48;          // columns per band-solve launch (DMMA path)
 constexpr double COND_LIMIT = 1e12;        // interface condition limit (oracle: COND_LIMIT)
 
 // Error carried from deep inside the implementation to the C-ABI wrapper.
@@ -42,29 +43,39 @@ struct LrsError : std::runtime_error {
     if (e_ != cudaSuccess) ::lrs::throw_cuda(e_, "kernel launch", __FILE__, __LINE__); \
   } while (0)
 
+// ---- stream-ordered caching device allocator (pool.cu) ---------------------------------
+// Blocks freed on a stream are cached per stream and handed out again only to
+// allocations on the same stream (stream order makes the reuse safe), so repeated
+// factorize/solve calls do not pay cudaMalloc/cudaFree (which also synchronize the
+// device).  The stream key comes from the C-ABI call in progress (set by guard()).
+void* pool_alloc(cudaStream_t s, size_t bytes, size_t* rounded);
+void pool_release(cudaStream_t s, void* p, size_t bytes);
+void pool_stream_open(cudaStream_t s);
+void pool_stream_retire(cudaStream_t s);
+size_t pool_cached_bytes();
+cudaStream_t& current_pool_stream();  // thread-local
+
 template <class T>
 struct DevBuf {
   T* p = nullptr;
   size_t n = 0;
+  size_t bytes = 0;
+  cudaStream_t key = nullptr;
   DevBuf() = default;
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
   ~DevBuf() { reset(); }
   void reset() {
-    if (p) cudaFree(p);
+    if (p) pool_release(key, p, bytes);
     p = nullptr;
     n = 0;
+    bytes = 0;
   }
   void alloc(size_t count) {
     reset();
     if (count == 0) return;
-    cudaError_t e = cudaMalloc(&p, count * sizeof(T));
-    if (e != cudaSuccess) {
-      cudaGetLastError();
-      p = nullptr;
-      throw LrsError(LRS_ERR_OOM, "cudaMalloc of " + std::to_string(count * sizeof(T)) +
-                                      " bytes failed: " + cudaGetErrorString(e));
-    }
+    key = current_pool_stream();
+    p = static_cast<T*>(pool_alloc(key, count * sizeof(T), &bytes));
     n = count;
   }
   T* get() const { return p; }
@@ -79,12 +90,19 @@ enum KClass {
 struct Ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t stream_hi = nullptr;  // high-priority side stream (LU look-ahead critical path)
   bool own_stream = false;
   int64_t launches = 0;
   lrs_error_info last{};
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   int num_sms = 148;
   bool in_setup = false;  // band solves issued by the spike construction (profiling class)
+  bool solve_fma1 = true;  // one-RHS band solves use the FMA kernel (false: DMMA, solve_block)
+  // pinned staging ring for small host->device uploads (job tables, Krylov scalars):
+  // a pageable cudaMemcpyAsync would first wait for the stream to drain.
+  char* stage = nullptr;
+  size_t stage_cap = 0, stage_pos = 0;
+  void stage_h2d(void* dst, const void* src, size_t bytes);  // pool.cu
   // profiling: (class, start, end) event triples, summed on demand
   bool prof = false;
   std::vector<cudaEvent_t> ev_pool;
@@ -122,17 +140,18 @@ struct Ctx {
 struct ProfScope {
   Ctx* c;
   int cls;
+  cudaStream_t s;
   cudaEvent_t b = nullptr;
-  ProfScope(Ctx* ctx, int k) : c(ctx), cls(k) {
+  ProfScope(Ctx* ctx, int k, cudaStream_t st = nullptr) : c(ctx), cls(k), s(st ? st : ctx->stream) {
     if (c->prof) {
       b = c->take_event();
-      cudaEventRecord(b, c->stream);
+      cudaEventRecord(b, s);
     }
   }
   ~ProfScope() {
     if (c->prof) {
       cudaEvent_t e = c->take_event();
-      cudaEventRecord(e, c->stream);
+      cudaEventRecord(e, s);
       c->prof_class.push_back(cls);
       c->prof_ev.push_back(b);
       c->prof_ev.push_back(e);

@@ -17,10 +17,49 @@
 namespace lrs {
 
 constexpr int IA_THREADS = 256;
+constexpr int IA_ROWS = 256;  // tip rows per partial-dot CTA
+
+// Partial messages over a 256-row slice of the tips: part[((job*2 + which)*nchunk + chunk)]
+// holds r x nrhs partial dots of v^T with y (which 0: m_W from y_{i,b}, 1: m_T from y_{i+1,t}).
+// Spreading the k-long dot products over many CTAs keeps this stage off a single SM.
+__global__ void __launch_bounds__(IA_THREADS) iface_dots_kernel(const IfaceApplyJob* jobs, int r,
+                                                                int64_t k, const double* y,
+                                                                int64_t ldy, int nrhs,
+                                                                double* part) {
+  __shared__ double red[IA_THREADS / 32][MAX_RHS];
+  const int job = blockIdx.y >> 1, which = blockIdx.y & 1, chunk = blockIdx.x;
+  const int nchunk = gridDim.x;
+  const IfaceApplyJob jb = jobs[job];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int64_t row = (int64_t)chunk * IA_ROWS + tid;
+  const bool valid = row < k;
+  const double* vt = which ? jb.vtT : jb.vtW;
+  const double* yy = y + (which ? jb.yt_row : jb.yb_row);
+  double yv[MAX_RHS];
+#pragma unroll
+  for (int j = 0; j < MAX_RHS; ++j) yv[j] = (valid && j < nrhs) ? yy[row + j * ldy] : 0.0;
+  double* out = part + ((size_t)(job * 2 + which) * nchunk + chunk) * r * MAX_RHS;
+  for (int a = 0; a < r; ++a) {
+    const double v = valid ? vt[row + a * k] : 0.0;
+#pragma unroll
+    for (int j = 0; j < MAX_RHS; ++j) {
+      if (j >= nrhs) break;
+      const double s = warp_sum(v * yv[j]);
+      if (lane == 0) red[w][j] = s;
+    }
+    __syncthreads();
+    if (tid < nrhs) {
+      double s = 0.0;
+      for (int q = 0; q < IA_THREADS / 32; ++q) s += red[q][tid];
+      out[a + tid * r] = s;
+    }
+    __syncthreads();
+  }
+}
 
 __global__ void __launch_bounds__(IA_THREADS) iface_apply_kernel(const IfaceApplyJob* jobs, int r,
-                                                                 int64_t k, const double* y,
-                                                                 int64_t ldy, int nrhs) {
+                                                                 int nrhs, int nchunk,
+                                                                 const double* part) {
   extern __shared__ double ism[];
   double* mW = ism;              // r x nrhs
   double* mT = mW + r * nrhs;
@@ -29,17 +68,14 @@ __global__ void __launch_bounds__(IA_THREADS) iface_apply_kernel(const IfaceAppl
   double* cT = h + r * nrhs;
   double* tmp = cT + r * nrhs;
   const IfaceApplyJob jb = jobs[blockIdx.x];
-  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, nw = IA_THREADS / 32;
-  // 2 r nrhs dot products of length k, one warp each
-  for (int o = w; o < 2 * r * nrhs; o += nw) {
+  const int tid = threadIdx.x;
+  // the two messages: partial dots summed over chunks in a fixed order
+  for (int o = tid; o < 2 * r * nrhs; o += IA_THREADS) {
     const int which = o / (r * nrhs), aj = o % (r * nrhs);
-    const int a = aj % r, j = aj / r;
-    const double* vt = which ? jb.vtT : jb.vtW;
-    const double* yy = y + (which ? jb.yt_row : jb.yb_row) + j * ldy;
+    const double* pp = part + (size_t)(blockIdx.x * 2 + which) * nchunk * r * MAX_RHS + aj;
     double s = 0.0;
-    for (int64_t row = lane; row < k; row += 32) s = fma(vt[row + a * k], yy[row], s);
-    s = warp_sum(s);
-    if (lane == 0) (which ? mT : mW)[a + j * r] = s;
+    for (int c = 0; c < nchunk; ++c) s += pp[(size_t)c * r * MAX_RHS];
+    (which ? mT : mW)[aj] = s;
   }
   __syncthreads();
   const int nout = r * nrhs;
@@ -83,12 +119,20 @@ __global__ void __launch_bounds__(IA_THREADS) iface_apply_kernel(const IfaceAppl
 }
 
 void launch_iface_apply(Ctx* c, const IfaceApplyJob* d_jobs, int njobs, int r, int64_t k,
-                        const double* y, int64_t ldy, int nrhs) {
+                        const double* y, int64_t ldy, int nrhs, double* work) {
   if (njobs == 0) return;
-  const size_t smem = sizeof(double) * 6 * r * nrhs;
+  const int nchunk = (int)((k + IA_ROWS - 1) / IA_ROWS);
   ProfScope ps_(c, K_IFACE);
-  iface_apply_kernel<<<njobs, IA_THREADS, smem, c->stream>>>(d_jobs, r, k, y, ldy, nrhs);
+  iface_dots_kernel<<<dim3(nchunk, 2 * njobs), IA_THREADS, 0, c->stream>>>(d_jobs, r, k, y, ldy,
+                                                                           nrhs, work);
   LRS_LAUNCHED(c);
+  const size_t smem = sizeof(double) * 6 * r * nrhs;
+  iface_apply_kernel<<<njobs, IA_THREADS, smem, c->stream>>>(d_jobs, r, nrhs, nchunk, work);
+  LRS_LAUNCHED(c);
+}
+
+size_t iface_work_doubles(int njobs, int r, int64_t k) {
+  return (size_t)njobs * 2 * ((k + IA_ROWS - 1) / IA_ROWS) * r * MAX_RHS;
 }
 
 // x[row, j] = y[row, j] - sum_a uW[row, a] scW_p[a, j] - sum_a uT[row, a] scT_p[a, j]

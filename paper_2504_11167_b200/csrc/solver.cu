@@ -6,8 +6,12 @@
 // The control flow mirrors the CPU checker in oracle/ line by line so that the
 // two produce the same iterates up to roundoff (the checker is never called).
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <future>
 
 #include "fact.h"
 #include "lrs_rng.h"
@@ -19,9 +23,7 @@ namespace {
 template <class J>
 void upload(Ctx* c, DevBuf<J>& d, const std::vector<J>& h) {
   d.alloc(h.size());
-  if (!h.empty())
-    LRS_CUDA(cudaMemcpyAsync(d.get(), h.data(), sizeof(J) * h.size(), cudaMemcpyHostToDevice,
-                             c->stream));
+  if (!h.empty()) c->stage_h2d(d.get(), h.data(), sizeof(J) * h.size());
 }
 
 template <class T>
@@ -54,8 +56,8 @@ void copy_block(Ctx* c, double* dst, int64_t ldd, const double* src, int64_t lds
 void dstage(Fact* f, double* x, int64_t ld, int nrhs, bool adjoint, int p_only) {
   const BandGeom g = f->geom();
   const int ntiles = p_only >= 0 ? f->T[p_only] : (int)f->total_rowtiles;
-  for (int c0 = 0; c0 < nrhs; c0 += MAX_RHS) {
-    const int nr = std::min(MAX_RHS, nrhs - c0);
+  for (int c0 = 0; c0 < nrhs; c0 += SOLVE_MAX_RHS) {
+    const int nr = std::min(SOLVE_MAX_RHS, nrhs - c0);
     double* xc = x + (int64_t)c0 * ld;
     launch_band_solve(f->ctx, g, f->tiles.get(), adjoint ? 2 : 0, xc, ld, nr, f->flags.get(),
                       f->next_epoch(), f->ticket.get(), p_only, ntiles);
@@ -74,7 +76,8 @@ void apply_precond(Fact* f, const double* in, int64_t ldi, double* out, int64_t 
   for (int c0 = 0; c0 < nrhs; c0 += MAX_RHS) {
     const int nr = std::min(MAX_RHS, nrhs - c0);
     double* xc = out + (int64_t)c0 * ldo;
-    launch_iface_apply(c, f->iface_jobs.get(), f->P - 1, f->r, f->k, xc, ldo, nr);
+    launch_iface_apply(c, f->iface_jobs.get(), f->P - 1, f->r, f->k, xc, ldo, nr,
+                       f->iface_work.get());
     launch_recovery(c, f->geom(), f->n, xc, ldo, xc, ldo, nr, f->uT.get(), f->uW.get(), f->r,
                     f->scT.get(), f->scW.get());
   }
@@ -92,7 +95,21 @@ void apply_precond(Fact* f, const double* in, int64_t ldi, double* out, int64_t 
 // Returns false (without throwing) if an interface is ill-conditioned, filling
 // *bad_iface / *bad_cond, so the caller can apply the r-halving retry.
 // ------------------------------------------------------------------------------------
-static bool build_lowrank(Fact* f, int r, int* bad_iface, double* bad_cond) {
+// Gaussian test blocks for every spike, slot 2*i + side, each k x l column-major.
+static std::vector<double> make_omega(uint64_t seed, int P, int64_t k, int l) {
+  std::vector<double> h((size_t)P * 2 * k * l, 0.0);
+  for (int i = 0; i < P; ++i)
+    for (int side = 0; side < 2; ++side) {
+      if ((side == LRS_SIDE_T && i == P - 1) || (side == LRS_SIDE_W && i == 0)) continue;
+      const uint64_t key = lrs_rng_key(seed, LRS_STREAM_OMEGA + 2ull * i + side);
+      double* o = h.data() + (size_t)(2 * i + side) * k * l;
+      for (int64_t e = 0; e < k * l; ++e) o[e] = lrs_rng_normal(key, (uint64_t)e);
+    }
+  return h;
+}
+
+static bool build_lowrank(Fact* f, int r, int* bad_iface, double* bad_cond,
+                          std::vector<double>* pre) {
   Ctx* c = f->ctx;
   Mat* m = f->mat;
   const int P = f->P;
@@ -122,14 +139,12 @@ static bool build_lowrank(Fact* f, int r, int* bad_iface, double* bad_cond) {
     if (i > 0) spk.push_back({i, LRS_SIDE_W});
   }
   auto slot = [&](int i, int side) { return (size_t)(2 * i + side); };
-  // Omega on the host from the shared counter-based generator
+  // Omega on the host from the shared counter-based generator;
+  // normally already produced by a host thread that overlapped the band LU.
   {
-    std::vector<double> h((size_t)P * 2 * k * l, 0.0);
-    for (auto [i, side] : spk) {
-      const uint64_t key = lrs_rng_key(f->seed, LRS_STREAM_OMEGA + 2ull * i + side);
-      double* o = h.data() + slot(i, side) * k * l;
-      for (int64_t e = 0; e < k * l; ++e) o[e] = lrs_rng_normal(key, (uint64_t)e);
-    }
+    std::vector<double> h = (pre && pre->size() == (size_t)P * 2 * k * l)
+                                ? std::move(*pre)
+                                : make_omega(f->seed, P, k, l);
     LRS_CUDA(cudaMemcpy(Om.get(), h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice));
   }
   auto ycol = [&](double* base, int i, int side) {
@@ -334,6 +349,7 @@ static bool build_lowrank(Fact* f, int r, int* bad_iface, double* bad_cond) {
       jobs.push_back(j);
     }
     upload(c, f->iface_jobs, jobs);
+    f->iface_work.alloc(iface_work_doubles(ni, r, k));
   }
   LRS_CUDA(cudaStreamSynchronize(c->stream));
   return true;
@@ -454,7 +470,15 @@ Fact* factorize(Ctx* c, Mat* m, const lrs_solver_cfg& cfg) {
       throw e;
     }
   }
-  for (int K = 0; K < f->Tmax; ++K) launch_lu_step(c, g, f->tiles.get(), K, f->status.get());
+  // the host draws Omega for the spike SVDs while the GPU runs the band LU
+  std::future<std::vector<double>> omega_future;
+  {
+    const int r0 = (int)cfg.n_svd;
+    const int l0 = r0 + (cfg.oversample >= 0 ? (int)cfg.oversample : (r0 + 1) / 2);
+    if (f->variant == LRS_VARIANT_T && P > 1 && r0 >= 1 && l0 <= f->k)
+      omega_future = std::async(std::launch::async, make_omega, f->seed, P, f->k, l0);
+  }
+  launch_band_lu(c, g, f->tiles.get(), f->Tmax, f->status.get());
   LRS_CUDA(cudaEventRecord(e1, c->stream));
   {
     std::vector<int> st(2 * P);
@@ -488,7 +512,9 @@ Fact* factorize(Ctx* c, Mat* m, const lrs_solver_cfg& cfg) {
       c->in_setup = true;
       bool ok;
       try {
-        ok = build_lowrank(f.get(), r, &bi, &bc);
+        std::vector<double> pre;
+        if (attempt == 0 && omega_future.valid()) pre = omega_future.get();
+        ok = build_lowrank(f.get(), r, &bi, &bc, &pre);
       } catch (...) {
         c->in_setup = false;
         throw;
@@ -650,7 +676,13 @@ void run_bicgstab(Work& w, const double* b, double* x, const lrs_iter_cfg& cfg, 
   std::vector<double> rho_prev(nr, 1.0), alpha(nr, 1.0), omega(nr, 1.0), rho(nr), rv(nr);
   LRS_CUDA(cudaMemsetAsync(p, 0, sizeof(double) * blk, c->stream));
   LRS_CUDA(cudaMemsetAsync(v, 0, sizeof(double) * blk, c->stream));
+  const bool trace = std::getenv("LRS_TRACE") != nullptr;
+  const auto t_start = std::chrono::steady_clock::now();
   for (int64_t it = 1; it <= cfg.max_iters; ++it) {
+    if (trace)
+      std::fprintf(stderr, "[lrs] bicgstab it %lld host %.3f ms\n", (long long)it,
+                   std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() -
+                                                             t_start).count());
     std::vector<bool> act(nr);
     for (int j = 0; j < nr; ++j) act[j] = !conv[j] && !brk[j];
     if (!any(act)) break;
@@ -820,16 +852,12 @@ void run_gmres(Work& w, const double* b, double* x, const lrs_iter_cfg& cfg, boo
       w.M(Vj, Zj);
       w.Aop(Zj, wv);
       // CGS2
+      // (the projections stay on the device in f->dotout and feed the update directly)
       w.dots(V, (int64_t)blk, jj + 1, wv, h.data());
-      LRS_CUDA(cudaMemcpyAsync(ydev.get(), h.data(), sizeof(double) * (jj + 1) * nr,
-                               cudaMemcpyHostToDevice, c->stream));
-      launch_multi_axpy_signed(c, n, nr, V, n, (int64_t)blk, jj + 1, ydev.get(), -1.0, wv, n);
+      launch_multi_axpy_signed(c, n, nr, V, n, (int64_t)blk, jj + 1, w.f->dotout.get(), -1.0, wv, n);
       w.dots(V, (int64_t)blk, jj + 1, wv, h2.data());
-      LRS_CUDA(cudaMemcpyAsync(ydev.get(), h2.data(), sizeof(double) * (jj + 1) * nr,
-                               cudaMemcpyHostToDevice, c->stream));
-      launch_multi_axpy_signed(c, n, nr, V, n, (int64_t)blk, jj + 1, ydev.get(), -1.0, wv, n);
+      launch_multi_axpy_signed(c, n, nr, V, n, (int64_t)blk, jj + 1, w.f->dotout.get(), -1.0, wv, n);
       w.norms(wv, hn.data());
-      // the H2D copies above read pageable h/h2 synchronously before returning, so reuse is safe
       for (int q = 0; q < (jj + 1) * nr; ++q) h[q] += h2[q];
       std::vector<double> invn(nr);
       for (int j = 0; j < nr; ++j) invn[j] = 1.0 / (hn[j] > 0 ? hn[j] : 1.0);
@@ -883,8 +911,7 @@ void run_gmres(Work& w, const double* b, double* x, const lrs_iter_cfg& cfg, boo
         }
         for (int q = 0; q < kk; ++q) y[(size_t)q * nr + j] = yy[q];
       }
-      LRS_CUDA(cudaMemcpyAsync(ydev.get(), y.data(), sizeof(double) * y.size(),
-                               cudaMemcpyHostToDevice, c->stream));
+      c->stage_h2d(ydev.get(), y.data(), sizeof(double) * y.size());
       launch_multi_axpy_signed(c, n, nr, Z, n, (int64_t)blk, kmax, ydev.get(), 1.0, x, n);
       LRS_CUDA(cudaStreamSynchronize(c->stream));
     }
