@@ -181,7 +181,7 @@ constexpr int AS_STAGE = KC * AS_LD;
 constexpr int BS_STAGE = NB * BS_LD;
 constexpr size_t GEMM_SMEM = sizeof(double) * 2 * (AS_STAGE + BS_STAGE);
 
-enum { MASK_NONE = 0, MASK_UNIT_LOWER = 1, MASK_UPPER = 2 };
+constexpr int MASK_NONE = 0, MASK_UNIT_LOWER = 1, MASK_UPPER = 2;
 
 __device__ __forceinline__ void gemm_load_chunk(const double* __restrict__ A,
                                                 const double* __restrict__ B, double* As,
@@ -197,9 +197,9 @@ __device__ __forceinline__ void gemm_load_chunk(const double* __restrict__ A,
   cp_async_commit();
 }
 
-template <int MODE>  // 0: C = A*B, 1: C -= A*B
-__device__ __forceinline__ void tile_gemm(const double* A, const double* B, double* C, int maskA,
-                                          int maskB, double* sm, int* piv_status, int col0) {
+template <int MODE, int maskA, int maskB>  // MODE 0: C = A*B, 1: C -= A*B
+__device__ __forceinline__ void tile_gemm(const double* A, const double* B, double* C, double* sm,
+                                          int* piv_status, int col0) {
   double* As = sm;
   double* Bs = sm + 2 * AS_STAGE;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
@@ -294,19 +294,19 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) lu_gemm_kernel(BandGeom g, do
       const int I = K + 1 + x;
       if (I >= T) return;
       // L_IK = A_IK * inv(U_KK); |l| > 1 means dgbtrf would have interchanged rows
-      tile_gemm<0>(tile(I, K), tile(K, K), tile(I, K), MASK_NONE, MASK_UPPER, sm, &status[2 * p],
+      tile_gemm<0, MASK_NONE, MASK_UPPER>(tile(I, K), tile(K, K), tile(I, K), sm, &status[2 * p],
                    K * NB);
     } else {
       const int J = K + 1 + (x - g.wl);
       if (J >= T) return;
-      tile_gemm<0>(tile(K, K), tile(K, J), tile(K, J), MASK_UNIT_LOWER, MASK_NONE, sm, nullptr, 0);
+      tile_gemm<0, MASK_UNIT_LOWER, MASK_NONE>(tile(K, K), tile(K, J), tile(K, J), sm, nullptr, 0);
     }
   } else if (KIND == 1) {
     // trailing update away from the next pivot row/column: I, J >= K + 2
     const int I = K + 2 + x / (g.wu - 1);
     const int J = K + 2 + x % (g.wu - 1);
     if (I >= T || J >= T) return;
-    tile_gemm<1>(tile(I, K), tile(K, J), tile(I, J), MASK_NONE, MASK_NONE, sm, nullptr, 0);
+    tile_gemm<1, MASK_NONE, MASK_NONE>(tile(I, K), tile(K, J), tile(I, J), sm, nullptr, 0);
   } else {
     // look-ahead part of the trailing update: column K+1 (I = K+1..K+wl) and row K+1
     // (J = K+2..K+wu), i.e. everything diag/panel of step K+1 needs
@@ -319,7 +319,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) lu_gemm_kernel(BandGeom g, do
       J = K + 2 + (x - g.wl);
     }
     if (I >= T || J >= T) return;
-    tile_gemm<1>(tile(I, K), tile(K, J), tile(I, J), MASK_NONE, MASK_NONE, sm, nullptr, 0);
+    tile_gemm<1, MASK_NONE, MASK_NONE>(tile(I, K), tile(K, J), tile(I, J), sm, nullptr, 0);
   }
 }
 

@@ -155,7 +155,7 @@ struct ProfScope {
       c->prof_class.push_back(cls);
       c->prof_ev.push_back(b);
       c->prof_ev.push_back(e);
-      if (c->prof_class.size() > 20000) c->collect();
+      if (c->prof_class.size() > (size_t(1) << 22)) c->collect();
     }
   }
 };

@@ -1,0 +1,79 @@
+"""Summarise an ncu report (``--set full``) or a launch-list CSV for profiles/.
+
+  python scripts/ncu_summary.py report.ncu-rep [kernel-substring]
+  python scripts/ncu_summary.py launches.csv
+"""
+import collections
+import csv
+import io
+import subprocess
+import sys
+
+METRICS = [
+    "gpu__time_duration.sum",
+    "dram__bytes_read.sum",
+    "dram__bytes_write.sum",
+    "dram__throughput.avg.pct_of_peak_sustained_elapsed",
+    "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+    "sm__inst_executed_pipe_tensor_subpipe_dmma.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
+    "sm__warps_active.avg.pct_of_peak_sustained_active",
+    "launch__registers_per_thread",
+    "launch__grid_size",
+    "launch__shared_mem_per_block_dynamic",
+    "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum",
+    "lts__t_bytes.sum",
+    "smsp__average_warp_latency_issue_stalled_barrier.ratio",
+    "smsp__average_warp_latency_issue_stalled_long_scoreboard.ratio",
+    "smsp__average_warp_latency_issue_stalled_math_pipe_throttle.ratio",
+    "smsp__average_warp_latency_issue_stalled_mio_throttle.ratio",
+    "smsp__average_warp_latency_issue_stalled_short_scoreboard.ratio",
+    "smsp__average_warp_latency_issue_stalled_wait.ratio",
+    "smsp__average_warp_latency_issue_stalled_tex_throttle.ratio",
+    "smsp__average_warp_latency_issue_stalled_dispatch_stall.ratio",
+]
+
+
+def report(path, sub=None):
+    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
+                         text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    hdr, units = rows[0], rows[1]
+    ki = hdr.index("Kernel Name")
+    for r in rows[2:]:
+        if sub and sub not in r[ki]:
+            continue
+        print(f"== {r[ki][:90]}")
+        for m in METRICS:
+            if m in hdr:
+                i = hdr.index(m)
+                print(f"  {m:78s} {r[i]:>14s} {units[i]}")
+
+
+def launches(path):
+    rows = list(csv.reader(open(path)))
+    h = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
+    hdr = rows[h]
+    ki, vi, ui = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
+    agg = collections.OrderedDict()
+    scale = {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "second": 1e3}
+    for r in rows[h + 1:]:
+        if len(r) <= vi:
+            continue
+        name = r[ki].split("(")[0]
+        a = agg.setdefault(name, [0, 0.0])
+        a[0] += 1
+        a[1] += float(r[vi].replace(",", "")) * scale.get(r[ui], 1e-6)
+    tot = sum(a[1] for a in agg.values())
+    print(f"{'kernel':60s} {'launches':>8s} {'ms':>10s} {'share':>6s}")
+    for k, (n, ms) in sorted(agg.items(), key=lambda x: -x[1][1]):
+        print(f"{k[:60]:60s} {n:8d} {ms:10.3f} {100 * ms / tot:5.1f}%")
+    print(f"{'total':60s} {sum(a[0] for a in agg.values()):8d} {tot:10.3f}")
+
+
+if __name__ == "__main__":
+    p = sys.argv[1]
+    if p.endswith(".csv"):
+        launches(p)
+    else:
+        report(p, sys.argv[2] if len(sys.argv) > 2 else None)
