@@ -24,7 +24,7 @@ from dataclasses import dataclass
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_LIBPATH = os.path.join(_HERE, "liblrspike_cuda.so")
+_LIBPATH = os.environ.get("LRS_LIB") or os.path.join(_HERE, "liblrspike_cuda.so")
 
 LRS_OK = 0
 F64, C128 = 0, 1

@@ -179,7 +179,12 @@ constexpr int AS_LD = NB + 4;   // 132
 constexpr int BS_LD = KC + 4;   // 36
 constexpr int AS_STAGE = KC * AS_LD;
 constexpr int BS_STAGE = NB * BS_LD;
-constexpr size_t GEMM_SMEM = sizeof(double) * 2 * (AS_STAGE + BS_STAGE);
+#ifndef LRS_GEMM_STAGES
+#define LRS_GEMM_STAGES 2  // measured: 2 stages 0.328 s vs 3 stages 0.363 s (c2 LU)
+#endif
+constexpr int GEMM_STAGES = LRS_GEMM_STAGES;
+static_assert(GEMM_STAGES >= 2 && GEMM_STAGES <= 3, "pipeline depth");
+constexpr size_t GEMM_SMEM = sizeof(double) * GEMM_STAGES * (AS_STAGE + BS_STAGE);
 
 constexpr int MASK_NONE = 0, MASK_UNIT_LOWER = 1, MASK_UPPER = 2;
 
@@ -197,81 +202,91 @@ __device__ __forceinline__ void gemm_load_chunk(const double* __restrict__ A,
   cp_async_commit();
 }
 
+// The DMMA computes the transposed product C^T = B^T A^T: the B tile supplies the
+// "A" fragments and the A tile the "B" fragments, so each lane's accumulator pair
+// (c0, c1) is C[m][n], C[m+1][n] -- adjacent in the column-major tile -- and the C
+// tile moves as 16-byte vectors.  Three cp.async stages (212 KB of shared memory).
 template <int MODE, int maskA, int maskB>  // MODE 0: C = A*B, 1: C -= A*B
 __device__ __forceinline__ void tile_gemm(const double* A, const double* B, double* C, double* sm,
                                           int* piv_status, int col0) {
   double* As = sm;
-  double* Bs = sm + 2 * AS_STAGE;
+  double* Bs = sm + GEMM_STAGES * AS_STAGE;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int wm = w & 1, wn = w >> 1;
   const int g = lane >> 2, t = lane & 3;
-  double acc[8][4][2];
-  gemm_load_chunk(A, B, As, Bs, 0, tid);
-  // MODE 1 accumulates straight into C (C + sum (-A) B): the C fragments are loaded
-  // while the first operand chunk is in flight and the epilogue is a plain store.
+  constexpr int NK = NB / KC;
+  double acc[4][8][2];  // [n tile j][m tile i][pair]: C[m0 + 2t + e][n0 + g]
+  constexpr int DIST = GEMM_STAGES - 1;  // prefetch distance in chunks
 #pragma unroll
-  for (int i = 0; i < 8; ++i)
+  for (int s = 0; s < DIST; ++s) gemm_load_chunk(A, B, As + s * AS_STAGE, Bs + s * BS_STAGE, s, tid);
+  // MODE 1 accumulates straight into C (C + sum (-A) B): the C fragments load while
+  // the first operand chunks are in flight and the epilogue is a plain store.
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
+  for (int j = 0; j < 4; ++j)
 #pragma unroll
-      for (int e = 0; e < 2; ++e)
-        acc[i][j][e] = MODE == 1 ? C[(int64_t)(32 * wn + 8 * j + 2 * t + e) * NB + 64 * wm + 8 * i + g]
-                                 : 0.0;
-#pragma unroll 1
-  for (int kc = 0; kc < NB / KC; ++kc) {
-    const int st = kc & 1;
-    if (kc + 1 < NB / KC) {
-      gemm_load_chunk(A, B, As + (st ^ 1) * AS_STAGE, Bs + (st ^ 1) * BS_STAGE, kc + 1, tid);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
+    for (int i = 0; i < 8; ++i) {
+      if (MODE == 1) {
+        const double2 v = *reinterpret_cast<const double2*>(
+            C + (int64_t)(32 * wn + 8 * j + g) * NB + 64 * wm + 8 * i + 2 * t);
+        acc[j][i][0] = v.x;
+        acc[j][i][1] = v.y;
+      } else {
+        acc[j][i][0] = acc[j][i][1] = 0.0;
+      }
     }
+#pragma unroll 1
+  for (int kc = 0; kc < NK; ++kc) {
+    if (kc + DIST < NK) {
+      const int s2 = (kc + DIST) % GEMM_STAGES;
+      gemm_load_chunk(A, B, As + s2 * AS_STAGE, Bs + s2 * BS_STAGE, kc + DIST, tid);
+    }
+    // chunk kc has landed once at most min(DIST, NK-1-kc) younger groups are pending
+    const int pend = min(DIST, NK - 1 - kc);
+    if (pend >= 2) cp_async_wait<2>();
+    else if (pend == 1) cp_async_wait<1>();
+    else cp_async_wait<0>();
     __syncthreads();
+    const int st = kc % GEMM_STAGES;
     const double* as = As + st * AS_STAGE;
     const double* bs = Bs + st * BS_STAGE;
 #pragma unroll
     for (int k4 = 0; k4 < KC / 4; ++k4) {
       const int kk = k4 * 4 + t;
       const int kg = kc * KC + kk;
-      double a[8], b[4];
+      double fa[8], fb[4];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
+      for (int i = 0; i < 8; ++i) {  // A[m][k], m = 64 wm + 8 i + g
         const int m = 64 * wm + 8 * i + g;
         double v = as[kk * AS_LD + m];
         if (maskA == MASK_UNIT_LOWER) v = m > kg ? v : (m == kg ? 1.0 : 0.0);
-        a[i] = MODE == 1 ? -v : v;
+        fa[i] = MODE == 1 ? -v : v;
       }
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
+      for (int j = 0; j < 4; ++j) {  // B[k][n], n = 32 wn + 8 j + g
         const int nn = 32 * wn + 8 * j + g;
         double v = bs[nn * BS_LD + kk];
         if (maskB == MASK_UPPER) v = kg <= nn ? v : 0.0;
-        b[j] = v;
+        fb[j] = v;
       }
 #pragma unroll
-      for (int i = 0; i < 8; ++i)
+      for (int j = 0; j < 4; ++j)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+        for (int i = 0; i < 8; ++i) dmma_8x8x4(acc[j][i][0], acc[j][i][1], fb[j], fa[i]);
     }
     __syncthreads();
   }
   int bad_col = 0x7fffffff;
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const int m = 64 * wm + 8 * i + g;
+  for (int j = 0; j < 4; ++j) {
+    const int nn = 32 * wn + 8 * j + g;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int nn = 32 * wn + 8 * j + 2 * t + e;
-        double* cp = C + (int64_t)nn * NB + m;
-        if (MODE == 0) {
-          *cp = acc[i][j][e];
-          if (piv_status && fabs(acc[i][j][e]) > 1.0) bad_col = min(bad_col, col0 + nn);
-        } else {
-          *cp = acc[i][j][e];
-        }
-      }
+    for (int i = 0; i < 8; ++i) {
+      double2 v;
+      v.x = acc[j][i][0];
+      v.y = acc[j][i][1];
+      *reinterpret_cast<double2*>(C + (int64_t)nn * NB + 64 * wm + 8 * i + 2 * t) = v;
+      if (MODE == 0 && piv_status && (fabs(v.x) > 1.0 || fabs(v.y) > 1.0))
+        bad_col = min(bad_col, col0 + nn);
     }
   }
   if (piv_status && bad_col != 0x7fffffff) atomicMin(piv_status, bad_col);
