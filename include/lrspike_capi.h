@@ -201,6 +201,32 @@ LRS_API lrs_status lrs_solve(lrs_fact* f, lrs_mat* a, const void* b, int64_t ldb
                              int64_t ldx, int64_t n_rhs, const lrs_iter_cfg* cfg,
                              lrs_report* report, int32_t mem);
 
+/* ---- multi-GPU: one process per GPU, partitions sharded across the ranks ------------ */
+/* Host callbacks for the exchanges of a sharded factorization.
+ * Buffers are device pointers (doubles) on the caller's GPU.  The library synchronizes
+ * its stream before every call and a callback must complete before it returns; every
+ * rank makes the same sequence of calls.
+ *   allgather: recv[q*count .. (q+1)*count) = send of rank q, for every rank q.
+ *   sendrecv : send `scount` doubles to rank `dest` and receive `rcount` doubles from
+ *              rank `source` (dest / source < 0: nothing to send / receive).
+ * Return 0 on success. */
+typedef struct lrs_comm {
+  int32_t rank, size;
+  void* user;
+  int32_t (*allgather)(void* user, const double* send, double* recv, int64_t count);
+  int32_t (*sendrecv)(void* user, const double* send, int64_t scount, int32_t dest, double* recv,
+                      int64_t rcount, int32_t source);
+} lrs_comm;
+
+/* Partitions [*p_lo, *p_hi) and rows [*row_lo, *row_hi) owned by `rank` (host only). */
+LRS_API lrs_status lrs_shard_plan(int64_t n, int64_t p, int32_t size, int32_t rank, int64_t* p_lo,
+                                  int64_t* p_hi, int64_t* row_lo, int64_t* row_hi);
+/* Factorize this rank's shard: every rank passes the full matrix and the same config.
+ * Applies and solves on the returned handle are collective; vectors are full-length,
+ * each rank reads and writes its own rows [row_lo, row_hi) (other rows are scratch). */
+LRS_API lrs_status lrs_factorize_dist(lrs_ctx* ctx, lrs_mat* a, const lrs_solver_cfg* cfg,
+                                      const lrs_comm* comm, lrs_fact** out);
+
 /* ---- microbenchmarks used by bench.py for the roofline denominators --------------- */
 /* FP64 DMMA peak: runs a register-resident mma.sync f64 loop, returns TFLOP/s. */
 LRS_API lrs_status lrs_bench_dmma_peak(lrs_ctx* ctx, double* tflops);

@@ -40,10 +40,12 @@ __global__ void __launch_bounds__(256) extract_tiles_kernel(int64_t n, const int
                                                             const int* __restrict__ ci,
                                                             const double* __restrict__ va,
                                                             BandGeom g, double* tiles, int64_t k,
+                                                            int64_t row_lo, int64_t row_hi,
                                                             unsigned long long* bad) {
-  const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (row >= n) return;
+  const int64_t row = row_lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= row_hi) return;
   const int p = find_partition(g.off, g.P, row);
+  const int pg = g.p0 + p;  // global partition of this row
   const int64_t o = g.off[p], s = g.size[p];
   const int64_t li = row - o;
   const int I = (int)(li / NB);
@@ -58,9 +60,9 @@ __global__ void __launch_bounds__(256) extract_tiles_kernel(int64_t n, const int
       if (ok)
         tiles[(g.tbase[p] + (int64_t)I * g.W + (d + g.wl)) * TILE_ELEMS + (lj % NB) * NB +
               (li % NB)] = va[q];
-    } else if (p + 1 < g.P && col >= o + s && col < g.off[p + 1] + g.size[p + 1]) {
+    } else if (pg + 1 < g.Pg && col >= o + s && col < g.goff[pg + 2]) {
       ok = row >= o + s - k && col < o + s + k;  // B_p corner
-    } else if (p > 0 && col < o && col >= g.off[p - 1]) {
+    } else if (pg > 0 && col < o && col >= g.goff[pg - 1]) {
       ok = row < o + k && col >= o - k;  // C_p corner
     } else {
       ok = false;
@@ -80,11 +82,12 @@ __global__ void pad_diag_kernel(BandGeom g, double* tiles) {
 }
 
 void launch_extract_tiles(Ctx* c, const Mat* m, const BandGeom& g, double* tiles, int64_t k,
-                          const int*, unsigned long long* d_bad) {
+                          int64_t row_lo, int64_t row_hi, unsigned long long* d_bad) {
   ProfScope ps_(c, K_SETUP);
-  if (m->n > 0) {
-    extract_tiles_kernel<<<(unsigned)((m->n + 255) / 256), 256, 0, c->stream>>>(
-        m->n, m->row_ptr.get(), m->col_idx.get(), m->vals.get(), g, tiles, k, d_bad);
+  if (row_hi > row_lo) {
+    extract_tiles_kernel<<<(unsigned)((row_hi - row_lo + 255) / 256), 256, 0, c->stream>>>(
+        m->n, m->row_ptr.get(), m->col_idx.get(), m->vals.get(), g, tiles, k, row_lo, row_hi,
+        d_bad);
     LRS_LAUNCHED(c);
   }
   pad_diag_kernel<<<g.P, 128, 0, c->stream>>>(g, tiles);

@@ -366,8 +366,34 @@ lrs_status lrs_factorize(lrs_ctx* c, lrs_mat* a, const lrs_solver_cfg* cfg, lrs_
   *out = nullptr;
   return guard(c, [&] {
     LRS_CUDA(cudaSetDevice(c->device));
-    Fact* f = factorize(c, a, *cfg);
+    Fact* f = factorize(c, a, *cfg, nullptr);
     *out = static_cast<lrs_fact*>(f);
+  });
+}
+
+lrs_status lrs_factorize_dist(lrs_ctx* c, lrs_mat* a, const lrs_solver_cfg* cfg,
+                              const lrs_comm* comm, lrs_fact** out) {
+  if (!c || !a || !cfg || !comm || !out) return LRS_ERR_PARAMETER;
+  *out = nullptr;
+  return guard(c, [&] {
+    LRS_CUDA(cudaSetDevice(c->device));
+    Fact* f = factorize(c, a, *cfg, comm);
+    *out = static_cast<lrs_fact*>(f);
+  });
+}
+
+lrs_status lrs_shard_plan(int64_t n, int64_t p, int32_t size, int32_t rank, int64_t* p_lo,
+                          int64_t* p_hi, int64_t* row_lo, int64_t* row_hi) {
+  return guard(nullptr, [&] {
+    if (p < 1 || size < 1 || rank < 0 || rank >= size || p < size || n < p)
+      throw LrsError(LRS_ERR_PARAMETER, "shard plan needs p >= size >= 1, 0 <= rank < size");
+    int64_t a, b;
+    shard_plan(p, size, rank, &a, &b);
+    auto off = [&](int64_t i) { return i * (n / p) + std::min<int64_t>(i, n % p); };
+    if (p_lo) *p_lo = a;
+    if (p_hi) *p_hi = b;
+    if (row_lo) *row_lo = off(a);
+    if (row_hi) *row_hi = off(b);
   });
 }
 
@@ -385,9 +411,9 @@ lrs_status lrs_fact_get_info(lrs_fact* f, lrs_fact_info* info) {
 
 lrs_status lrs_fact_get_layout(lrs_fact* f, int64_t* sizes, int64_t* offsets) {
   if (!f) return LRS_ERR_PARAMETER;
-  for (int i = 0; i < f->P; ++i) {
-    if (sizes) sizes[i] = f->size[i];
-    if (offsets) offsets[i] = f->off[i];
+  for (int i = 0; i < f->Pg; ++i) {  // the global layout (all partitions)
+    if (sizes) sizes[i] = f->goff[i + 1] - f->goff[i];
+    if (offsets) offsets[i] = f->goff[i];
   }
   return LRS_OK;
 }
@@ -397,16 +423,16 @@ lrs_status lrs_fact_get_spike(lrs_fact* f, int64_t i, int32_t side, double* u, d
   if (!f) return LRS_ERR_PARAMETER;
   return guard(f->ctx, [&] {
     if (f->r == 0) throw LrsError(LRS_ERR_PARAMETER, "factorization has no low-rank spikes");
-    if (i < 0 || i >= f->P || (side == LRS_SIDE_T && i == f->P - 1) ||
+    if (i < f->p0 || i >= f->p0 + f->P || (side == LRS_SIDE_T && i == f->Pg - 1) ||
         (side == LRS_SIDE_W && i == 0) || (side != LRS_SIDE_T && side != LRS_SIDE_W))
-      throw LrsError(LRS_ERR_PARAMETER, "no such spike");
+      throw LrsError(LRS_ERR_PARAMETER, "no such spike on this GPU");
     const int r = f->r;
-    const int64_t n = f->n, k = f->k, ni = f->size[i];
+    const int64_t n = f->n, k = f->k, ni = f->size[i - f->p0];
     const double* ub = side == LRS_SIDE_T ? f->uT.get() : f->uW.get();
     const double* vb = side == LRS_SIDE_T ? f->vtT.get() : f->vtW.get();
     const double* sb = side == LRS_SIDE_T ? f->sT.get() : f->sW.get();
     if (u)
-      LRS_CUDA(cudaMemcpy2D(u, sizeof(double) * ni, ub + f->off[i], sizeof(double) * n,
+      LRS_CUDA(cudaMemcpy2D(u, sizeof(double) * ni, ub + f->goff[i], sizeof(double) * n,
                             sizeof(double) * ni, r, cudaMemcpyDeviceToHost));
     if (sigma) LRS_CUDA(cudaMemcpy(sigma, sb + (size_t)i * r, sizeof(double) * r, cudaMemcpyDeviceToHost));
     if (v) {  // stored as v^T (k x r); return v (r x k, ld r)
@@ -423,13 +449,15 @@ lrs_status lrs_fact_get_tiles(lrs_fact* f, int64_t i, double* host_out, int64_t 
                               int64_t* needed) {
   if (!f) return LRS_ERR_PARAMETER;
   return guard(f->ctx, [&] {
-    if (i < 0 || i >= f->P) throw LrsError(LRS_ERR_PARAMETER, "no such partition");
-    const int64_t cnt = (int64_t)f->T[i] * f->W * TILE_ELEMS;
+    if (i < f->p0 || i >= f->p0 + f->P)
+      throw LrsError(LRS_ERR_PARAMETER, "partition not on this GPU");
+    const int li = (int)(i - f->p0);
+    const int64_t cnt = (int64_t)f->T[li] * f->W * TILE_ELEMS;
     if (needed) *needed = cnt;
     if (host_out) {
       if (capacity < cnt) throw LrsError(LRS_ERR_DIMENSION, "tile buffer too small");
       LRS_CUDA(cudaStreamSynchronize(f->ctx->stream));
-      LRS_CUDA(cudaMemcpy(host_out, f->tiles.get() + f->tbase[i] * TILE_ELEMS,
+      LRS_CUDA(cudaMemcpy(host_out, f->tiles.get() + f->tbase[li] * TILE_ELEMS,
                           sizeof(double) * cnt, cudaMemcpyDeviceToHost));
     }
   });
@@ -450,15 +478,17 @@ lrs_status lrs_solve_block(lrs_fact* f, int64_t i, const void* rhs, int64_t ld_r
   Ctx* c = f->ctx;
   return guard(c, [&] {
     check_mem(mem);
-    if (i < 0 || i >= f->P) throw LrsError(LRS_ERR_PARAMETER, "no such partition");
-    const int64_t ni = f->size[i];
+    if (i < f->p0 || i >= f->p0 + f->P)
+      throw LrsError(LRS_ERR_PARAMETER, "partition not on this GPU");
+    const int li = (int)(i - f->p0);
+    const int64_t ni = f->size[li];
     if (ld_rhs < ni || ld_x < ni || n_rhs < 0)
       throw LrsError(LRS_ERR_DIMENSION, "solve_block: RHS rows must equal the block size");
     // work in a global-row-layout buffer so the partition offset addressing of the
     // dataflow kernel applies unchanged
     DevBuf<double> work;
     work.alloc((size_t)std::max<int64_t>(1, f->n * n_rhs));
-    double* wp = work.get() + f->off[i];
+    double* wp = work.get() + f->off[li];
     const cudaMemcpyKind k_in = mem == LRS_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
     if (n_rhs > 0)
       LRS_CUDA(cudaMemcpy2DAsync(wp, sizeof(double) * f->n, rhs, sizeof(double) * ld_rhs,
@@ -470,7 +500,7 @@ lrs_status lrs_solve_block(lrs_fact* f, int64_t i, const void* rhs, int64_t ld_r
       ~FmaOff() { c->solve_fma1 = prev; }
     } fo{c, c->solve_fma1};
     c->solve_fma1 = false;
-    dstage(f, work.get(), f->n, (int)n_rhs, adjoint != 0, (int)i);
+    dstage(f, work.get(), f->n, (int)n_rhs, adjoint != 0, li);
     const cudaMemcpyKind k_out = mem == LRS_MEM_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
     if (n_rhs > 0)
       LRS_CUDA(cudaMemcpy2DAsync(x, sizeof(double) * ld_x, wp, sizeof(double) * f->n,

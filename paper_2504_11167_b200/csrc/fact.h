@@ -9,21 +9,26 @@
 
 namespace lrs {
 
-struct IfaceApplyJobDev;  // device job layout lives in precond.cu via IfaceApplyJob
-
+// A factorization owns a contiguous block of the P partitions: all of them on one GPU,
+// or [p0, p0 + P) of Pg when sharded across GPUs (lrs_factorize_dist).  Vectors are
+// full-length (global row indexing) on every GPU; each GPU reads and writes only its rows
+// [row_lo, row_hi) plus the halo rows it receives from its neighbours.
 struct Fact {
   Ctx* ctx = nullptr;
   Mat* mat = nullptr;
   int variant = LRS_VARIANT_T;
-  int P = 1;
+  int P = 1;                   // local partitions
+  int Pg = 1, p0 = 0;          // global partitions, global index of local partition 0
+  int64_t row_lo = 0, row_hi = 0;
   int64_t n = 0, k = 0, kl = 0, ku = 0;
   int r = 0, os = 0, l = 0, passes = 2;
   uint64_t seed = 0;
   int wl = 0, wu = 0, W = 1, Tmax = 0;
-  std::vector<int64_t> off, size, tbase, fbase;
+  std::vector<int64_t> off, size, tbase, fbase;  // local partitions (global row offsets)
+  std::vector<int64_t> goff;                     // global partition offsets [Pg + 1]
   std::vector<int> T;
   int64_t total_tiles = 0, total_rowtiles = 0;
-  DevBuf<int64_t> d_off, d_size, d_tbase, d_fbase;
+  DevBuf<int64_t> d_off, d_size, d_tbase, d_fbase, d_goff;
   DevBuf<int> d_T;
   DevBuf<double> tiles;
   DevBuf<unsigned> flags;
@@ -31,18 +36,30 @@ struct Fact {
   unsigned epoch = 0;
   DevBuf<int> status;
   DevBuf<unsigned long long> bad;
-  // low-rank spikes (global row layout n x r, ld n) and interface data
+  // low-rank spikes: u as n x r (global rows, ld n); v^T, sigma in GLOBAL partition slots
   DevBuf<double> uT, uW, vtT, vtW, sT, sW;
+  // interfaces with at least one local side (jobs in global interface order)
+  int ni = 0, iface0 = 0;      // number of jobs, global index of the first
   DevBuf<double> Kd, Ed, Hinv, cond;
   DevBuf<int> degen;
-  DevBuf<double> scT, scW;
+  DevBuf<double> scT, scW;     // per global partition, r x MAX_RHS
   DevBuf<IfaceApplyJob> iface_jobs;
-  DevBuf<double> iface_work;  // partial message dots of the interface apply
-  // deterministic reduction chunks (partition aligned)
+  DevBuf<double> iface_work, iface_msg;
+  int job_left = -1, job_right = -1;  // jobs of the cross-GPU interfaces (or -1)
+  // deterministic reductions (partition-aligned chunks, partition-ordered sums)
   std::vector<int64_t> chunk_start;
+  std::vector<int> part_first;
   DevBuf<int64_t> d_chunks;
-  DevBuf<double> partial, dotout;
-  // apply workspace
+  DevBuf<int> d_part_first;
+  DevBuf<double> partial, persum, gather, dotout;
+  std::vector<int> rank_pl;    // local partition count of every rank
+  DevBuf<int> d_rank_pl;
+  int pl_max = 1;
+  // multi-GPU
+  bool dist = false;
+  lrs_comm comm{};
+  DevBuf<double> xch;          // staging for neighbour exchanges
+  // ledger, info
   int64_t ledger_msgs[3] = {0, 0, 0}, ledger_sc[3] = {0, 0, 0};
   lrs_fact_info info{};
   bool rank_collapsed = false;
@@ -58,16 +75,26 @@ struct Fact {
     g.wl = wl;
     g.wu = wu;
     g.W = W;
+    g.goff = d_goff.get();
+    g.p0 = p0;
+    g.Pg = Pg;
     return g;
   }
-  Chunks chunks() const { return Chunks{d_chunks.get(), (int)chunk_start.size() - 1}; }
+  Chunks chunks() const {
+    return Chunks{d_chunks.get(), d_part_first.get(), (int)chunk_start.size() - 1, P};
+  }
   unsigned next_epoch() { return ++epoch; }
+  int rank() const { return dist ? comm.rank : 0; }
+  int nranks() const { return dist ? comm.size : 1; }
 };
 
-Fact* factorize(Ctx* c, Mat* m, const lrs_solver_cfg& cfg);
-// D-stage solve (all partitions, or one partition if p_only >= 0), in place on x (ld, nrhs cols).
+// Contiguous balanced blocks of partitions per rank: [p_lo, p_hi) of rank `rank`.
+void shard_plan(int64_t P, int size, int rank, int64_t* p_lo, int64_t* p_hi);
+
+Fact* factorize(Ctx* c, Mat* m, const lrs_solver_cfg& cfg, const lrs_comm* comm);
+// D-stage solve (local partitions, or local partition p_only >= 0), in place on x.
 void dstage(Fact* f, double* x, int64_t ld, int nrhs, bool adjoint, int p_only);
-// M^-1 applied to in -> out (device, ld_in / ld_out), variant T or Block Jacobi.
+// M^-1 applied to in -> out on the local rows, variant T or Block Jacobi.
 void apply_precond(Fact* f, const double* in, int64_t ldi, double* out, int64_t ldo, int nrhs,
                    bool block_jacobi);
 void solve(Fact* f, Mat* a, const double* b, int64_t ldb, double* x, int64_t ldx, int nrhs,

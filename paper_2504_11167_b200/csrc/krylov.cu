@@ -44,18 +44,32 @@ __global__ void __launch_bounds__(KV_THREADS) multidot_partial_kernel(
   }
 }
 
-__global__ void multidot_final_kernel(int nchunks, int nout, const double* __restrict__ partial,
-                                      double* __restrict__ out) {
+// persum[p][o] = sum of the chunk partials of local partition p, in chunk order
+__global__ void multidot_partition_kernel(const int* __restrict__ part_first, int Pl, int nout,
+                                          const double* __restrict__ partial,
+                                          double* __restrict__ persum) {
+  const int o = blockIdx.x * blockDim.x + threadIdx.x, p = blockIdx.y;
+  if (o >= nout || p >= Pl) return;
+  double s = 0.0;
+  for (int c = part_first[p]; c < part_first[p + 1]; ++c) s += partial[(int64_t)c * nout + o];
+  persum[(int64_t)p * nout + o] = s;
+}
+
+// out[o] = sum over ranks r, partitions p < counts[r] (global partition order)
+__global__ void partition_total_kernel(const double* __restrict__ blocks,
+                                       const int* __restrict__ counts, int nranks, int pmax,
+                                       int nout, double* __restrict__ out) {
   const int o = blockIdx.x * blockDim.x + threadIdx.x;
   if (o >= nout) return;
   double s = 0.0;
-  for (int c = 0; c < nchunks; ++c) s += partial[(int64_t)c * nout + o];
+  for (int rk = 0; rk < nranks; ++rk)
+    for (int p = 0; p < counts[rk]; ++p) s += blocks[((int64_t)rk * pmax + p) * nout + o];
   out[o] = s;
 }
 
-void launch_multidot(Ctx* c, const Chunks& ch, const double* X, int64_t ldx, int64_t strideX,
-                     int nvec, const double* Y, int64_t ldy, int nrhs, double* partial,
-                     double* out) {
+void launch_multidot_partition(Ctx* c, const Chunks& ch, const double* X, int64_t ldx,
+                               int64_t strideX, int nvec, const double* Y, int64_t ldy, int nrhs,
+                               double* partial, double* persum) {
   if (nvec == 0 || nrhs == 0) return;
   ProfScope ps_(c, K_KRYLOV);
   if (nrhs == 1)
@@ -66,7 +80,17 @@ void launch_multidot(Ctx* c, const Chunks& ch, const double* X, int64_t ldx, int
         ch.start, X, ldx, strideX, nvec, Y, ldy, nrhs, partial);
   LRS_LAUNCHED(c);
   const int nout = nvec * nrhs;
-  multidot_final_kernel<<<(nout + 127) / 128, 128, 0, c->stream>>>(ch.nchunks, nout, partial, out);
+  multidot_partition_kernel<<<dim3((nout + 127) / 128, ch.Pl), 128, 0, c->stream>>>(
+      ch.part_first, ch.Pl, nout, partial, persum);
+  LRS_LAUNCHED(c);
+}
+
+void launch_partition_total(Ctx* c, const double* blocks, const int* counts, int nranks,
+                            int pmax, int nout, double* out) {
+  if (nout == 0) return;
+  ProfScope ps_(c, K_KRYLOV);
+  partition_total_kernel<<<(nout + 127) / 128, 128, 0, c->stream>>>(blocks, counts, nranks, pmax,
+                                                                     nout, out);
   LRS_LAUNCHED(c);
 }
 

@@ -179,8 +179,10 @@ struct Fact;  // defined in fact.h
 // ------------------------------------------------------------------------------------
 
 // spmv.cu
+// rows [row_lo, row_hi) of y (+)= A x; mode: 0 y = A x, 1 y += A x, 2 y = b - A x.
+// x, y, b are full-length (global row indexing).
 void launch_spmv(Ctx* c, const Mat* m, const double* x, int64_t ldx, double* y, int64_t ldy,
-                 int nrhs, int mode, const double* b, int64_t ldb);
-// mode: 0 y = A x, 1 y += A x, 2 y = b - A x
+                 int nrhs, int mode, const double* b, int64_t ldb, int64_t row_lo = 0,
+                 int64_t row_hi = -1);
 
 }  // namespace lrs

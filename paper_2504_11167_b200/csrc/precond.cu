@@ -10,6 +10,12 @@
 // algebra of the oracle's literal W1-W3 + recovery with the reduced-solution
 // tips eliminated (x_{i,b} = g_{i,b} - uTb S_T cT), so no b x n_rhs tip is
 // ever formed; results agree with the oracle to roundoff.
+//
+// Multi-GPU: each side of a cross-GPU interface computes only its own message
+// (m_W on the GPU of partition i, m_T on the GPU of partition i+1); the two
+// r x n_rhs messages are exchanged (C1), after which both GPUs run the same
+// deterministic r x r algebra and each keeps the half its recovery needs -- so
+// the C2 messages never cross the link.
 #include "common.cuh"
 #include "kernels.h"
 #include "lrs_internal.h"
@@ -19,9 +25,8 @@ namespace lrs {
 constexpr int IA_THREADS = 256;
 constexpr int IA_ROWS = 256;  // tip rows per partial-dot CTA
 
-// Partial messages over a 256-row slice of the tips: part[((job*2 + which)*nchunk + chunk)]
-// holds r x nrhs partial dots of v^T with y (which 0: m_W from y_{i,b}, 1: m_T from y_{i+1,t}).
-// Spreading the k-long dot products over many CTAs keeps this stage off a single SM.
+// part[((job*2 + which)*nchunk + chunk)] = r x nrhs partial dots of v^T with y over a
+// 256-row slice (which 0: m_W from y_{i,b}, 1: m_T from y_{i+1,t}); only local sides.
 __global__ void __launch_bounds__(IA_THREADS) iface_dots_kernel(const IfaceApplyJob* jobs, int r,
                                                                 int64_t k, const double* y,
                                                                 int64_t ldy, int nrhs,
@@ -30,6 +35,7 @@ __global__ void __launch_bounds__(IA_THREADS) iface_dots_kernel(const IfaceApply
   const int job = blockIdx.y >> 1, which = blockIdx.y & 1, chunk = blockIdx.x;
   const int nchunk = gridDim.x;
   const IfaceApplyJob jb = jobs[job];
+  if (which == 0 ? !jb.has_left : !jb.has_right) return;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int64_t row = (int64_t)chunk * IA_ROWS + tid;
   const bool valid = row < k;
@@ -57,9 +63,22 @@ __global__ void __launch_bounds__(IA_THREADS) iface_dots_kernel(const IfaceApply
   }
 }
 
-__global__ void __launch_bounds__(IA_THREADS) iface_apply_kernel(const IfaceApplyJob* jobs, int r,
-                                                                 int nrhs, int nchunk,
-                                                                 const double* part) {
+// msg[which] = sum over chunks (fixed order) of the local partial messages
+__global__ void iface_reduce_kernel(const IfaceApplyJob* jobs, int r, int nrhs, int nchunk,
+                                    const double* part) {
+  const IfaceApplyJob jb = jobs[blockIdx.x];
+  for (int o = threadIdx.x; o < 2 * r * nrhs; o += blockDim.x) {
+    const int which = o / (r * nrhs), aj = o % (r * nrhs);
+    if (which == 0 ? !jb.has_left : !jb.has_right) continue;
+    const double* pp = part + (size_t)(blockIdx.x * 2 + which) * nchunk * r * MAX_RHS + aj;
+    double s = 0.0;
+    for (int c = 0; c < nchunk; ++c) s += pp[(size_t)c * r * MAX_RHS];
+    jb.msg[which * r * MAX_RHS + aj] = s;
+  }
+}
+
+__global__ void __launch_bounds__(IA_THREADS) iface_solve_kernel(const IfaceApplyJob* jobs, int r,
+                                                                 int nrhs) {
   extern __shared__ double ism[];
   double* mW = ism;              // r x nrhs
   double* mT = mW + r * nrhs;
@@ -69,13 +88,9 @@ __global__ void __launch_bounds__(IA_THREADS) iface_apply_kernel(const IfaceAppl
   double* tmp = cT + r * nrhs;
   const IfaceApplyJob jb = jobs[blockIdx.x];
   const int tid = threadIdx.x;
-  // the two messages: partial dots summed over chunks in a fixed order
-  for (int o = tid; o < 2 * r * nrhs; o += IA_THREADS) {
-    const int which = o / (r * nrhs), aj = o % (r * nrhs);
-    const double* pp = part + (size_t)(blockIdx.x * 2 + which) * nchunk * r * MAX_RHS + aj;
-    double s = 0.0;
-    for (int c = 0; c < nchunk; ++c) s += pp[(size_t)c * r * MAX_RHS];
-    (which ? mT : mW)[aj] = s;
+  for (int o = tid; o < r * nrhs; o += IA_THREADS) {
+    mW[o] = jb.msg[o];
+    mT[o] = jb.msg[r * MAX_RHS + o];
   }
   __syncthreads();
   const int nout = r * nrhs;
@@ -113,21 +128,28 @@ __global__ void __launch_bounds__(IA_THREADS) iface_apply_kernel(const IfaceAppl
   __syncthreads();
   for (int e = tid; e < nout; e += IA_THREADS) {
     const int a = e % r;
-    jb.scT[e] = jb.sT[a] * cT[e];
-    jb.scW[e] = jb.sW[a] * tmp[e];
+    if (jb.has_left) jb.scT[e] = jb.sT[a] * cT[e];
+    if (jb.has_right) jb.scW[e] = jb.sW[a] * tmp[e];
   }
 }
 
-void launch_iface_apply(Ctx* c, const IfaceApplyJob* d_jobs, int njobs, int r, int64_t k,
-                        const double* y, int64_t ldy, int nrhs, double* work) {
+void launch_iface_messages(Ctx* c, const IfaceApplyJob* d_jobs, int njobs, int r, int64_t k,
+                           const double* y, int64_t ldy, int nrhs, double* work) {
   if (njobs == 0) return;
   const int nchunk = (int)((k + IA_ROWS - 1) / IA_ROWS);
   ProfScope ps_(c, K_IFACE);
   iface_dots_kernel<<<dim3(nchunk, 2 * njobs), IA_THREADS, 0, c->stream>>>(d_jobs, r, k, y, ldy,
                                                                            nrhs, work);
   LRS_LAUNCHED(c);
+  iface_reduce_kernel<<<njobs, 128, 0, c->stream>>>(d_jobs, r, nrhs, nchunk, work);
+  LRS_LAUNCHED(c);
+}
+
+void launch_iface_solve(Ctx* c, const IfaceApplyJob* d_jobs, int njobs, int r, int nrhs) {
+  if (njobs == 0) return;
+  ProfScope ps_(c, K_IFACE);
   const size_t smem = sizeof(double) * 6 * r * nrhs;
-  iface_apply_kernel<<<njobs, IA_THREADS, smem, c->stream>>>(d_jobs, r, nrhs, nchunk, work);
+  iface_solve_kernel<<<njobs, IA_THREADS, smem, c->stream>>>(d_jobs, r, nrhs);
   LRS_LAUNCHED(c);
 }
 
@@ -136,35 +158,36 @@ size_t iface_work_doubles(int njobs, int r, int64_t k) {
 }
 
 // x[row, j] = y[row, j] - sum_a uW[row, a] scW_p[a, j] - sum_a uT[row, a] scT_p[a, j]
-// scT / scW: per partition r x MAX_RHS blocks (scT of the last partition and scW of the
-// first are never read).
-__global__ void __launch_bounds__(256) recovery_kernel(BandGeom g, int64_t n, const double* y,
+// for the local rows; scT / scW: one r x MAX_RHS block per GLOBAL partition (scT of the
+// last partition and scW of the first are never read).
+__global__ void __launch_bounds__(256) recovery_kernel(BandGeom g, int64_t n, int64_t row_lo,
+                                                       int64_t row_hi, const double* y,
                                                        int64_t ldy, double* x, int64_t ldx,
                                                        int nrhs, const double* __restrict__ uT,
                                                        const double* __restrict__ uW, int r,
                                                        const double* __restrict__ scT,
                                                        const double* __restrict__ scW) {
-  const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (row >= n) return;
+  const int64_t row = row_lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= row_hi) return;
   int lo = 0, hi = g.P - 1;
   while (lo < hi) {
     const int mid = (lo + hi + 1) >> 1;
     if (g.off[mid] <= row) lo = mid;
     else hi = mid - 1;
   }
-  const int p = lo;
-  const bool hasW = p > 0, hasT = p < g.P - 1;
+  const int pg = g.p0 + lo;
+  const bool hasW = pg > 0, hasT = pg < g.Pg - 1;
   double acc[MAX_RHS];
   for (int j = 0; j < nrhs; ++j) acc[j] = y[row + j * ldy];
   if (hasW) {
-    const double* sc = scW + (int64_t)p * r * MAX_RHS;
+    const double* sc = scW + (int64_t)pg * r * MAX_RHS;
     for (int a = 0; a < r; ++a) {
       const double u = uW[row + a * n];
       for (int j = 0; j < nrhs; ++j) acc[j] -= u * sc[a + j * r];
     }
   }
   if (hasT) {
-    const double* sc = scT + (int64_t)p * r * MAX_RHS;
+    const double* sc = scT + (int64_t)pg * r * MAX_RHS;
     for (int a = 0; a < r; ++a) {
       const double u = uT[row + a * n];
       for (int j = 0; j < nrhs; ++j) acc[j] -= u * sc[a + j * r];
@@ -173,13 +196,14 @@ __global__ void __launch_bounds__(256) recovery_kernel(BandGeom g, int64_t n, co
   for (int j = 0; j < nrhs; ++j) x[row + j * ldx] = acc[j];
 }
 
-void launch_recovery(Ctx* c, const BandGeom& g, int64_t n, const double* y, int64_t ldy, double* x,
-                     int64_t ldx, int nrhs, const double* uT, const double* uW, int r,
-                     const double* scT, const double* scW) {
-  if (n == 0) return;
+void launch_recovery(Ctx* c, const BandGeom& g, int64_t n, int64_t row_lo, int64_t row_hi,
+                     const double* y, int64_t ldy, double* x, int64_t ldx, int nrhs,
+                     const double* uT, const double* uW, int r, const double* scT,
+                     const double* scW) {
+  if (row_hi <= row_lo) return;
   ProfScope ps_(c, K_RECOVERY);
-  recovery_kernel<<<(unsigned)((n + 255) / 256), 256, 0, c->stream>>>(g, n, y, ldy, x, ldx, nrhs,
-                                                                      uT, uW, r, scT, scW);
+  recovery_kernel<<<(unsigned)((row_hi - row_lo + 255) / 256), 256, 0, c->stream>>>(
+      g, n, row_lo, row_hi, y, ldy, x, ldx, nrhs, uT, uW, r, scT, scW);
   LRS_LAUNCHED(c);
 }
 

@@ -5,6 +5,13 @@
 // all vector and matrix arithmetic runs in the kernels of this library.
 // The control flow mirrors the CPU checker in oracle/ line by line so that the
 // two produce the same iterates up to roundoff (the checker is never called).
+//
+// Sharding: a factorization owns partitions [p0, p0 + P) of Pg (all of them on one
+// GPU).  Cross-GPU traffic is exactly the SURVEY.md 2.4 set: the two rank-r interface
+// messages per apply (C1; C2 is computed on both sides, see precond.cu), the b-row
+// SpMV halos (C3), the per-partition dot partials (C4, all-gathered and summed in
+// global partition order, so every GPU count gives bit-identical iterates) and the
+// spike tips of the cross interfaces at setup (C5).
 #include <algorithm>
 #include <chrono>
 #include <cmath>
@@ -42,16 +49,77 @@ float elapsed_ms(cudaEvent_t a, cudaEvent_t b) {
 // columns [0, ncols) of a block with leading dimension ld
 void copy_block(Ctx* c, double* dst, int64_t ldd, const double* src, int64_t lds, int64_t rows,
                 int ncols) {
-  if (rows == 0 || ncols == 0) return;
+  if (rows <= 0 || ncols == 0) return;
   LRS_CUDA(cudaMemcpy2DAsync(dst, sizeof(double) * ldd, src, sizeof(double) * lds,
                              sizeof(double) * rows, ncols, cudaMemcpyDeviceToDevice, c->stream));
 }
 
+// ---- communication (no-ops on a single GPU) ---------------------------------------------
+void comm_rc(int32_t rc, const char* what) {
+  if (rc != 0) throw LrsError(LRS_ERR_NCCL, std::string("communication callback failed: ") + what);
+}
+
+// Two-phase neighbour exchange of `count` doubles: to_next -> rank+1 (received there in
+// from_prev), then to_prev -> rank-1 (received in from_next).
+void neighbor_exchange(Fact* f, const double* to_next, double* from_prev, const double* to_prev,
+                       double* from_next, int64_t count) {
+  if (!f->dist || count == 0) return;
+  LRS_CUDA(cudaStreamSynchronize(f->ctx->stream));
+  const int r = f->comm.rank, G = f->comm.size;
+  const int next = r + 1 < G ? r + 1 : -1, prev = r > 0 ? r - 1 : -1;
+  comm_rc(f->comm.sendrecv(f->comm.user, to_next, next >= 0 ? count : 0, next, from_prev,
+                           prev >= 0 ? count : 0, prev),
+          "sendrecv");
+  comm_rc(f->comm.sendrecv(f->comm.user, to_prev, prev >= 0 ? count : 0, prev, from_next,
+                           next >= 0 ? count : 0, next),
+          "sendrecv");
+}
+
+// All-gather of a small host vector (every rank contributes v.size() doubles).
+std::vector<double> allgather_host(Fact* f, const std::vector<double>& v) {
+  if (!f->dist) return v;
+  const int G = f->comm.size;
+  DevBuf<double> d;
+  d.alloc(v.size() * (G + 1));
+  LRS_CUDA(cudaMemcpy(d.get(), v.data(), sizeof(double) * v.size(), cudaMemcpyHostToDevice));
+  comm_rc(f->comm.allgather(f->comm.user, d.get(), d.get() + v.size(), (int64_t)v.size()),
+          "allgather");
+  std::vector<double> out(v.size() * G);
+  LRS_CUDA(cudaMemcpy(out.data(), d.get() + v.size(), sizeof(double) * out.size(),
+                      cudaMemcpyDeviceToHost));
+  return out;
+}
+
+// SpMV halo (C3): rows [row_lo - hb, row_lo) and [row_hi, row_hi + hb) of the
+// full-length block x from the neighbours, hb = the band half-width of A.
+void halo_exchange(Fact* f, double* x, int64_t ld, int nrhs) {
+  if (!f->dist) return;
+  const int64_t hb = std::min<int64_t>(f->mat->k, f->row_hi - f->row_lo);
+  if (hb == 0 || nrhs == 0) return;
+  Ctx* c = f->ctx;
+  const int64_t cnt = hb * nrhs;
+  double* s_next = f->xch.get();
+  double* s_prev = s_next + cnt;
+  double* r_prev = s_prev + cnt;
+  double* r_next = r_prev + cnt;
+  copy_block(c, s_next, hb, x + f->row_hi - hb, ld, hb, nrhs);
+  copy_block(c, s_prev, hb, x + f->row_lo, ld, hb, nrhs);
+  neighbor_exchange(f, s_next, r_prev, s_prev, r_next, cnt);
+  const int rk = f->comm.rank;
+  if (rk > 0) copy_block(c, x + f->row_lo - hb, ld, r_prev, hb, hb, nrhs);
+  if (rk + 1 < f->comm.size) copy_block(c, x + f->row_hi, ld, r_next, hb, hb, nrhs);
+}
+
 }  // namespace
+
+void shard_plan(int64_t P, int size, int rank, int64_t* p_lo, int64_t* p_hi) {
+  *p_lo = (int64_t)rank * P / size;
+  *p_hi = (int64_t)(rank + 1) * P / size;
+}
 
 // ------------------------------------------------------------------------------------
 // D-stage: banded L then U solves (or U^T then L^T for the adjoint), batches of
-// MAX_RHS columns, all partitions concurrently.
+// SOLVE_MAX_RHS columns, all local partitions concurrently.
 // ------------------------------------------------------------------------------------
 void dstage(Fact* f, double* x, int64_t ld, int nrhs, bool adjoint, int p_only) {
   const BandGeom g = f->geom();
@@ -69,38 +137,56 @@ void dstage(Fact* f, double* x, int64_t ld, int nrhs, bool adjoint, int p_only) 
 void apply_precond(Fact* f, const double* in, int64_t ldi, double* out, int64_t ldo, int nrhs,
                    bool block_jacobi) {
   Ctx* c = f->ctx;
-  if (out != in) copy_block(c, out, ldo, in, ldi, f->n, nrhs);
+  const int64_t nl = f->row_hi - f->row_lo;
+  if (out != in) copy_block(c, out + f->row_lo, ldo, in + f->row_lo, ldi, nl, nrhs);
   dstage(f, out, ldo, nrhs, false, -1);
-  const bool lowrank = !block_jacobi && f->variant == LRS_VARIANT_T && f->r > 0 && f->P > 1;
+  const bool lowrank = !block_jacobi && f->variant == LRS_VARIANT_T && f->r > 0 && f->Pg > 1;
   if (!lowrank) return;
+  const int r = f->r;
   for (int c0 = 0; c0 < nrhs; c0 += MAX_RHS) {
     const int nr = std::min(MAX_RHS, nrhs - c0);
     double* xc = out + (int64_t)c0 * ldo;
-    launch_iface_apply(c, f->iface_jobs.get(), f->P - 1, f->r, f->k, xc, ldo, nr,
-                       f->iface_work.get());
-    launch_recovery(c, f->geom(), f->n, xc, ldo, xc, ldo, nr, f->uT.get(), f->uW.get(), f->r,
-                    f->scT.get(), f->scW.get());
+    launch_iface_messages(c, f->iface_jobs.get(), f->ni, r, f->k, xc, ldo, nr,
+                          f->iface_work.get());
+    if (f->dist) {
+      // C1 across the GPU boundaries: m_W (computed left) goes right, m_T goes left
+      const int64_t blk = (int64_t)r * MAX_RHS;
+      double* mbase = f->iface_msg.get();
+      const double* to_next = f->job_right >= 0 ? mbase + (2 * f->job_right + 0) * blk : mbase;
+      double* from_prev = f->job_left >= 0 ? mbase + (2 * f->job_left + 0) * blk : mbase;
+      const double* to_prev = f->job_left >= 0 ? mbase + (2 * f->job_left + 1) * blk : mbase;
+      double* from_next = f->job_right >= 0 ? mbase + (2 * f->job_right + 1) * blk : mbase;
+      neighbor_exchange(f, to_next, from_prev, to_prev, from_next, blk);
+    }
+    launch_iface_solve(c, f->iface_jobs.get(), f->ni, r, nr);
+    launch_recovery(c, f->geom(), f->n, f->row_lo, f->row_hi, xc, ldo, xc, ldo, nr, f->uT.get(),
+                    f->uW.get(), r, f->scT.get(), f->scW.get());
   }
-  // CommLedger: 2 compressed messages per interface in the reduced solve, 2 in recovery
-  // (SPEC.md:535): 4 (p-1) n_svd n_rhs scalars per application.
-  const int64_t msgs = 2 * (int64_t)(f->P - 1);
+  // CommLedger: 2 compressed messages per local-side interface in the
+  // reduced solve and 2 in the recovery, r n_rhs scalars each -- 4 (p-1) r n_rhs per
+  // application summed over the GPUs (every interface is counted by the GPU of its
+  // left partition).
+  int64_t owned = 0;
+  for (int i = f->iface0; i < f->iface0 + f->ni; ++i)
+    if (i >= f->p0 && i < f->p0 + f->P) ++owned;
+  const int64_t msgs = 2 * owned;
   f->ledger_msgs[LRS_STAGE_PRECOND_APPLY] += msgs;
-  f->ledger_sc[LRS_STAGE_PRECOND_APPLY] += msgs * f->r * nrhs;
+  f->ledger_sc[LRS_STAGE_PRECOND_APPLY] += msgs * r * nrhs;
   f->ledger_msgs[LRS_STAGE_RECOVERY] += msgs;
-  f->ledger_sc[LRS_STAGE_RECOVERY] += msgs * f->r * nrhs;
+  f->ledger_sc[LRS_STAGE_RECOVERY] += msgs * r * nrhs;
 }
 
 // ------------------------------------------------------------------------------------
 // Randomized spike SVDs and the truncated preconditioner for rank r.
-// Returns false (without throwing) if an interface is ill-conditioned, filling
-// *bad_iface / *bad_cond, so the caller can apply the r-halving retry.
+// Returns false (without throwing) if an interface is ill-conditioned on ANY rank,
+// filling *bad_iface / *bad_cond, so the caller can apply the r-halving retry.
 // ------------------------------------------------------------------------------------
-// Gaussian test blocks for every spike, slot 2*i + side, each k x l column-major.
-static std::vector<double> make_omega(uint64_t seed, int P, int64_t k, int l) {
-  std::vector<double> h((size_t)P * 2 * k * l, 0.0);
-  for (int i = 0; i < P; ++i)
+// Gaussian test blocks of the spikes of partitions [plo, phi): slot 2*i + side, k x l each.
+static std::vector<double> make_omega(uint64_t seed, int Pg, int plo, int phi, int64_t k, int l) {
+  std::vector<double> h((size_t)Pg * 2 * k * l, 0.0);
+  for (int i = plo; i < phi; ++i)
     for (int side = 0; side < 2; ++side) {
-      if ((side == LRS_SIDE_T && i == P - 1) || (side == LRS_SIDE_W && i == 0)) continue;
+      if ((side == LRS_SIDE_T && i == Pg - 1) || (side == LRS_SIDE_W && i == 0)) continue;
       const uint64_t key = lrs_rng_key(seed, LRS_STREAM_OMEGA + 2ull * i + side);
       double* o = h.data() + (size_t)(2 * i + side) * k * l;
       for (int64_t e = 0; e < k * l; ++e) o[e] = lrs_rng_normal(key, (uint64_t)e);
@@ -112,7 +198,7 @@ static bool build_lowrank(Fact* f, int r, int* bad_iface, double* bad_cond,
                           std::vector<double>* pre) {
   Ctx* c = f->ctx;
   Mat* m = f->mat;
-  const int P = f->P;
+  const int Pg = f->Pg, p0 = f->p0, P = f->P;
   const int64_t n = f->n, k = f->k;
   const int os = f->os >= 0 ? f->os : (r + 1) / 2;
   const int l = r + os;
@@ -126,30 +212,30 @@ static bool build_lowrank(Fact* f, int r, int* bad_iface, double* bad_cond,
   DevBuf<double> Y, S, Om, Zt, Rz, Ur, Vr, sig;
   Y.alloc((size_t)n * L2);
   S.alloc((size_t)n * L2);
-  Om.alloc((size_t)P * 2 * k * l);
-  Zt.alloc((size_t)P * 2 * k * l);
-  Rz.alloc((size_t)P * 2 * l * l);
-  Ur.alloc((size_t)P * 2 * l * l);
-  Vr.alloc((size_t)P * 2 * l * l);
-  sig.alloc((size_t)P * 2 * l);
-  // spikes: (partition, side)
+  Om.alloc((size_t)Pg * 2 * k * l);
+  Zt.alloc((size_t)Pg * 2 * k * l);
+  Rz.alloc((size_t)Pg * 2 * l * l);
+  Ur.alloc((size_t)Pg * 2 * l * l);
+  Vr.alloc((size_t)Pg * 2 * l * l);
+  sig.alloc((size_t)Pg * 2 * l);
+  // local spikes: (global partition, side); partition g = p0 + local index
   std::vector<std::pair<int, int>> spk;
-  for (int i = 0; i < P; ++i) {
-    if (i < P - 1) spk.push_back({i, LRS_SIDE_T});
+  for (int i = p0; i < p0 + P; ++i) {
+    if (i < Pg - 1) spk.push_back({i, LRS_SIDE_T});
     if (i > 0) spk.push_back({i, LRS_SIDE_W});
   }
   auto slot = [&](int i, int side) { return (size_t)(2 * i + side); };
-  // Omega on the host from the shared counter-based generator;
-  // normally already produced by a host thread that overlapped the band LU.
+  auto goff = [&](int i) { return f->goff[i]; };
+  auto gsize = [&](int i) { return f->goff[i + 1] - f->goff[i]; };
+  // Omega from the shared counter-based generator, normally drawn by a
+  // host thread while the band LU ran
   {
-    std::vector<double> h = (pre && pre->size() == (size_t)P * 2 * k * l)
+    std::vector<double> h = (pre && pre->size() == (size_t)Pg * 2 * k * l)
                                 ? std::move(*pre)
-                                : make_omega(f->seed, P, k, l);
+                                : make_omega(f->seed, Pg, p0, p0 + P, k, l);
     LRS_CUDA(cudaMemcpy(Om.get(), h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice));
   }
-  auto ycol = [&](double* base, int i, int side) {
-    return base + f->off[i] + (int64_t)side * l * n;
-  };
+  auto ycol = [&](double* base, int i, int side) { return base + goff(i) + (int64_t)side * l * n; };
   // T_apply: Y = A_i^-1 pad(coupling X) for every spike, X = k x l blocks in src[slot]
   DevBuf<CoupleJob> cj;
   auto T_apply = [&](const double* src) {
@@ -157,11 +243,11 @@ static bool build_lowrank(Fact* f, int r, int* bad_iface, double* bad_cond,
     for (auto [i, side] : spk) {
       CoupleJob j{};
       if (side == LRS_SIDE_T) {
-        j.r0 = f->off[i] + f->size[i] - k;
-        j.c0 = f->off[i + 1];
+        j.r0 = goff(i) + gsize(i) - k;
+        j.c0 = goff(i + 1);
       } else {
-        j.r0 = f->off[i];
-        j.c0 = f->off[i] - k;
+        j.r0 = goff(i);
+        j.c0 = goff(i) - k;
       }
       j.b = k;
       j.dst0 = j.r0;
@@ -184,19 +270,16 @@ static bool build_lowrank(Fact* f, int r, int* bad_iface, double* bad_cond,
     std::vector<CoupleJob> jobs;
     for (auto [i, side] : spk) {
       CoupleJob j{};
-      int64_t tip0;
       if (side == LRS_SIDE_T) {  // B_i^T = A^T[off_{i+1} .., off_i+n_i-k ..]
-        j.r0 = f->off[i + 1];
-        j.c0 = f->off[i] + f->size[i] - k;
-        tip0 = j.c0;
+        j.r0 = goff(i + 1);
+        j.c0 = goff(i) + gsize(i) - k;
       } else {  // C_i^T = A^T[off_i - k .., off_i ..]
-        j.r0 = f->off[i] - k;
-        j.c0 = f->off[i];
-        tip0 = j.c0;
+        j.r0 = goff(i) - k;
+        j.c0 = goff(i);
       }
       j.b = k;
       j.dst0 = 0;
-      j.X = S.get() + tip0 + (int64_t)side * l * n;
+      j.X = S.get() + j.c0 + (int64_t)side * l * n;
       j.ldx = n;
       j.out = Zt.get() + slot(i, side) * k * l;
       j.ldo = k;
@@ -209,7 +292,7 @@ static bool build_lowrank(Fact* f, int r, int* bad_iface, double* bad_cond,
   DevBuf<QrJob> qj;
   auto orth_Y = [&]() {
     std::vector<QrJob> jobs;
-    for (auto [i, side] : spk) jobs.push_back(QrJob{ycol(Y.get(), i, side), f->size[i], n, nullptr});
+    for (auto [i, side] : spk) jobs.push_back(QrJob{ycol(Y.get(), i, side), gsize(i), n, nullptr});
     upload(c, qj, jobs);
     launch_householder_qr(c, qj.get(), (int)jobs.size(), l);
   };
@@ -232,6 +315,18 @@ static bool build_lowrank(Fact* f, int r, int* bad_iface, double* bad_cond,
   }
   Tt_apply();          // Zt = (Q^T T)^T, k x l
   orth_Zt(true);       // Zt = Q_z R_z
+  f->uT.alloc((size_t)n * r);
+  f->uW.alloc((size_t)n * r);
+  f->vtT.alloc((size_t)Pg * k * r);
+  f->vtW.alloc((size_t)Pg * k * r);
+  f->sT.alloc((size_t)Pg * r);
+  f->sW.alloc((size_t)Pg * r);
+  LRS_CUDA(cudaMemsetAsync(f->uT.get(), 0, sizeof(double) * n * r, c->stream));
+  LRS_CUDA(cudaMemsetAsync(f->uW.get(), 0, sizeof(double) * n * r, c->stream));
+  LRS_CUDA(cudaMemsetAsync(f->vtT.get(), 0, sizeof(double) * Pg * k * r, c->stream));
+  LRS_CUDA(cudaMemsetAsync(f->vtW.get(), 0, sizeof(double) * Pg * k * r, c->stream));
+  LRS_CUDA(cudaMemsetAsync(f->sT.get(), 0, sizeof(double) * Pg * r, c->stream));
+  LRS_CUDA(cudaMemsetAsync(f->sW.get(), 0, sizeof(double) * Pg * r, c->stream));
   {
     std::vector<SvdJob> jobs;
     for (auto [i, side] : spk) {
@@ -243,16 +338,6 @@ static bool build_lowrank(Fact* f, int r, int* bad_iface, double* bad_cond,
     upload(c, sj, jobs);
     launch_jacobi_svd(c, sj.get(), (int)jobs.size(), l);
     // Z = V_R S (Q_z U_R)^T  =>  u = Q V_R[:, :r],  v^T = Q_z U_R[:, :r]
-    f->uT.alloc((size_t)n * r);
-    f->uW.alloc((size_t)n * r);
-    f->vtT.alloc((size_t)P * k * r);
-    f->vtW.alloc((size_t)P * k * r);
-    f->sT.alloc((size_t)P * r);
-    f->sW.alloc((size_t)P * r);
-    LRS_CUDA(cudaMemsetAsync(f->uT.get(), 0, sizeof(double) * n * r, c->stream));
-    LRS_CUDA(cudaMemsetAsync(f->uW.get(), 0, sizeof(double) * n * r, c->stream));
-    LRS_CUDA(cudaMemsetAsync(f->sT.get(), 0, sizeof(double) * P * r, c->stream));
-    LRS_CUDA(cudaMemsetAsync(f->sW.get(), 0, sizeof(double) * P * r, c->stream));
     std::vector<GemmJob> gu, gv;
     std::vector<SigmaJob> sjobs;
     int64_t maxm = 0;
@@ -261,12 +346,12 @@ static bool build_lowrank(Fact* f, int r, int* bad_iface, double* bad_cond,
       double* ubuf = side == LRS_SIDE_T ? f->uT.get() : f->uW.get();
       double* vbuf = side == LRS_SIDE_T ? f->vtT.get() : f->vtW.get();
       double* sbuf = side == LRS_SIDE_T ? f->sT.get() : f->sW.get();
-      gu.push_back(GemmJob{ycol(Y.get(), i, side), n, Vr.get() + s * l * l, l,
-                           ubuf + f->off[i], n, f->size[i], r, l, 0});
+      gu.push_back(GemmJob{ycol(Y.get(), i, side), n, Vr.get() + s * l * l, l, ubuf + goff(i), n,
+                           gsize(i), r, l, 0});
       gv.push_back(GemmJob{Zt.get() + s * k * l, k, Ur.get() + s * l * l, l,
                            vbuf + (size_t)i * k * r, k, k, r, l, 0});
       sjobs.push_back(SigmaJob{sig.get() + s * l, sbuf + (size_t)i * r});
-      maxm = std::max(maxm, f->size[i]);
+      maxm = std::max(maxm, gsize(i));
     }
     DevBuf<GemmJob> dgu, dgv;
     upload(c, dgu, gu);
@@ -283,30 +368,80 @@ static bool build_lowrank(Fact* f, int r, int* bad_iface, double* bad_cond,
     download(c, &hflag, flag.get(), 1);
     f->rank_collapsed = hflag != 0;
   }
-  // interfaces
-  const int ni = P - 1;
-  f->Kd.alloc((size_t)ni * r * r);
-  f->Ed.alloc((size_t)ni * r * r);
-  f->Hinv.alloc((size_t)ni * r * r);
-  f->cond.alloc((size_t)ni * 2);
-  f->degen.alloc((size_t)ni);
-  {
+  // C5: ship the T side of the last local partition right and the W side of the first
+  // local partition left: [u tip (k x r) | v^T (k x r) | sigma (r)]
+  if (f->dist) {
+    const int64_t cnt = 2 * k * r + r;
+    DevBuf<double> buf;
+    buf.alloc((size_t)cnt * 4);
+    double* s_next = buf.get();
+    double* r_prev = s_next + cnt;
+    double* s_prev = r_prev + cnt;
+    double* r_next = s_prev + cnt;
+    const int iR = p0 + P - 1;  // T side, to the right neighbour (if any)
+    if (iR < Pg - 1) {
+      copy_block(c, s_next, k, f->uT.get() + goff(iR + 1) - k, n, k, r);
+      LRS_CUDA(cudaMemcpyAsync(s_next + k * r, f->vtT.get() + (size_t)iR * k * r,
+                               sizeof(double) * k * r, cudaMemcpyDeviceToDevice, c->stream));
+      LRS_CUDA(cudaMemcpyAsync(s_next + 2 * k * r, f->sT.get() + (size_t)iR * r,
+                               sizeof(double) * r, cudaMemcpyDeviceToDevice, c->stream));
+    }
+    if (p0 > 0) {  // W side of partition p0, to the left neighbour
+      copy_block(c, s_prev, k, f->uW.get() + goff(p0), n, k, r);
+      LRS_CUDA(cudaMemcpyAsync(s_prev + k * r, f->vtW.get() + (size_t)p0 * k * r,
+                               sizeof(double) * k * r, cudaMemcpyDeviceToDevice, c->stream));
+      LRS_CUDA(cudaMemcpyAsync(s_prev + 2 * k * r, f->sW.get() + (size_t)p0 * r,
+                               sizeof(double) * r, cudaMemcpyDeviceToDevice, c->stream));
+    }
+    neighbor_exchange(f, s_next, r_prev, s_prev, r_next, cnt);
+    if (p0 > 0) {  // T side of partition p0 - 1
+      const int i = p0 - 1;
+      copy_block(c, f->uT.get() + goff(i + 1) - k, n, r_prev, k, k, r);
+      LRS_CUDA(cudaMemcpyAsync(f->vtT.get() + (size_t)i * k * r, r_prev + k * r,
+                               sizeof(double) * k * r, cudaMemcpyDeviceToDevice, c->stream));
+      LRS_CUDA(cudaMemcpyAsync(f->sT.get() + (size_t)i * r, r_prev + 2 * k * r,
+                               sizeof(double) * r, cudaMemcpyDeviceToDevice, c->stream));
+    }
+    if (iR < Pg - 1) {  // W side of partition iR + 1
+      const int i = iR + 1;
+      copy_block(c, f->uW.get() + goff(i), n, r_next, k, k, r);
+      LRS_CUDA(cudaMemcpyAsync(f->vtW.get() + (size_t)i * k * r, r_next + k * r,
+                               sizeof(double) * k * r, cudaMemcpyDeviceToDevice, c->stream));
+      LRS_CUDA(cudaMemcpyAsync(f->sW.get() + (size_t)i * r, r_next + 2 * k * r,
+                               sizeof(double) * r, cudaMemcpyDeviceToDevice, c->stream));
+    }
+  }
+  // interfaces with at least one local side: global i in [iface0, iface0 + ni)
+  f->iface0 = std::max(0, p0 - 1);
+  const int ilast = std::min(Pg - 2, p0 + P - 1);
+  const int ni = std::max(0, ilast - f->iface0 + 1);
+  f->ni = ni;
+  f->Kd.alloc((size_t)std::max(ni, 1) * r * r);
+  f->Ed.alloc((size_t)std::max(ni, 1) * r * r);
+  f->Hinv.alloc((size_t)std::max(ni, 1) * r * r);
+  f->cond.alloc((size_t)std::max(ni, 1) * 2);
+  f->degen.alloc((size_t)std::max(ni, 1));
+  double mx = 1.0;
+  int bad_i = -1;
+  double bad_c = 0.0;
+  if (ni > 0) {
     std::vector<IfaceSetupJob> jobs;
-    for (int i = 0; i < ni; ++i) {
+    for (int q = 0; q < ni; ++q) {
+      const int i = f->iface0 + q;
       IfaceSetupJob j{};
-      j.uTb = f->uT.get() + f->off[i] + f->size[i] - k;
+      j.uTb = f->uT.get() + goff(i) + gsize(i) - k;
       j.ld_uT = n;
-      j.uWt = f->uW.get() + f->off[i + 1];
+      j.uWt = f->uW.get() + goff(i + 1);
       j.ld_uW = n;
       j.vtT = f->vtT.get() + (size_t)i * k * r;
       j.vtW = f->vtW.get() + (size_t)(i + 1) * k * r;
       j.sT = f->sT.get() + (size_t)i * r;
       j.sW = f->sW.get() + (size_t)(i + 1) * r;
-      j.K = f->Kd.get() + (size_t)i * r * r;
-      j.E = f->Ed.get() + (size_t)i * r * r;
-      j.Hinv = f->Hinv.get() + (size_t)i * r * r;
-      j.cond = f->cond.get() + 2 * i;
-      j.degenerate = f->degen.get() + i;
+      j.K = f->Kd.get() + (size_t)q * r * r;
+      j.E = f->Ed.get() + (size_t)q * r * r;
+      j.Hinv = f->Hinv.get() + (size_t)q * r * r;
+      j.cond = f->cond.get() + 2 * q;
+      j.degenerate = f->degen.get() + q;
       jobs.push_back(j);
     }
     DevBuf<IfaceSetupJob> dj;
@@ -314,42 +449,69 @@ static bool build_lowrank(Fact* f, int r, int* bad_iface, double* bad_cond,
     launch_iface_setup(c, dj.get(), ni, r, k);
     std::vector<double> hc(2 * ni);
     download(c, hc.data(), f->cond.get(), hc.size());
-    double mx = 1.0;
-    for (int i = 0; i < ni; ++i) {
-      const double ci = std::max(hc[2 * i], hc[2 * i + 1]);
-      if (!(ci <= COND_LIMIT)) {
-        *bad_iface = i;
-        *bad_cond = ci;
-        return false;
+    for (int q = 0; q < ni; ++q) {
+      const double ci = std::max(hc[2 * q], hc[2 * q + 1]);
+      if (!(ci <= COND_LIMIT) && bad_i < 0) {
+        bad_i = f->iface0 + q;
+        bad_c = ci;
       }
-      mx = std::max(mx, ci);
+      if (ci <= COND_LIMIT) mx = std::max(mx, ci);
     }
-    f->info.max_interface_cond = mx;
   }
+  // every rank takes the same decision (first ill-conditioned interface in global order)
+  {
+    const std::vector<double> all = allgather_host(
+        f, {bad_i >= 0 ? (double)bad_i : -1.0, bad_c, mx, f->rank_collapsed ? 1.0 : 0.0});
+    bad_i = -1;
+    for (size_t q = 0; q < all.size(); q += 4) {
+      if (all[q] >= 0 && (bad_i < 0 || all[q] < bad_i)) {
+        bad_i = (int)all[q];
+        bad_c = all[q + 1];
+      }
+      mx = std::max(mx, all[q + 2]);
+      f->rank_collapsed = f->rank_collapsed || all[q + 3] != 0.0;
+    }
+  }
+  if (bad_i >= 0) {
+    *bad_iface = bad_i;
+    *bad_cond = bad_c;
+    return false;
+  }
+  f->info.max_interface_cond = mx;
   // apply-time jobs
-  f->scT.alloc((size_t)P * r * MAX_RHS);
-  f->scW.alloc((size_t)P * r * MAX_RHS);
-  LRS_CUDA(cudaMemsetAsync(f->scT.get(), 0, sizeof(double) * P * r * MAX_RHS, c->stream));
-  LRS_CUDA(cudaMemsetAsync(f->scW.get(), 0, sizeof(double) * P * r * MAX_RHS, c->stream));
+  f->scT.alloc((size_t)Pg * r * MAX_RHS);
+  f->scW.alloc((size_t)Pg * r * MAX_RHS);
+  f->iface_msg.alloc((size_t)std::max(ni, 1) * 2 * r * MAX_RHS);
+  LRS_CUDA(cudaMemsetAsync(f->scT.get(), 0, sizeof(double) * Pg * r * MAX_RHS, c->stream));
+  LRS_CUDA(cudaMemsetAsync(f->scW.get(), 0, sizeof(double) * Pg * r * MAX_RHS, c->stream));
+  LRS_CUDA(cudaMemsetAsync(f->iface_msg.get(), 0, sizeof(double) * std::max(ni, 1) * 2 * r * MAX_RHS,
+                           c->stream));
+  f->job_left = f->job_right = -1;
   {
     std::vector<IfaceApplyJob> jobs;
-    for (int i = 0; i < ni; ++i) {
+    for (int q = 0; q < ni; ++q) {
+      const int i = f->iface0 + q;
       IfaceApplyJob j{};
       j.vtT = f->vtT.get() + (size_t)i * k * r;
       j.vtW = f->vtW.get() + (size_t)(i + 1) * k * r;
       j.sT = f->sT.get() + (size_t)i * r;
       j.sW = f->sW.get() + (size_t)(i + 1) * r;
-      j.K = f->Kd.get() + (size_t)i * r * r;
-      j.E = f->Ed.get() + (size_t)i * r * r;
-      j.Hinv = f->Hinv.get() + (size_t)i * r * r;
-      j.yb_row = f->off[i] + f->size[i] - k;
-      j.yt_row = f->off[i + 1];
+      j.K = f->Kd.get() + (size_t)q * r * r;
+      j.E = f->Ed.get() + (size_t)q * r * r;
+      j.Hinv = f->Hinv.get() + (size_t)q * r * r;
+      j.yb_row = goff(i) + gsize(i) - k;
+      j.yt_row = goff(i + 1);
       j.scT = f->scT.get() + (size_t)i * r * MAX_RHS;
       j.scW = f->scW.get() + (size_t)(i + 1) * r * MAX_RHS;
+      j.msg = f->iface_msg.get() + (size_t)q * 2 * r * MAX_RHS;
+      j.has_left = (i >= p0 && i < p0 + P) ? 1 : 0;
+      j.has_right = (i + 1 >= p0 && i + 1 < p0 + P) ? 1 : 0;
+      if (!j.has_left) f->job_left = q;
+      if (!j.has_right) f->job_right = q;
       jobs.push_back(j);
     }
     upload(c, f->iface_jobs, jobs);
-    f->iface_work.alloc(iface_work_doubles(ni, r, k));
+    f->iface_work.alloc(iface_work_doubles(std::max(ni, 1), r, k));
   }
   LRS_CUDA(cudaStreamSynchronize(c->stream));
   return true;
@@ -358,7 +520,7 @@ static bool build_lowrank(Fact* f, int r, int* bad_iface, double* bad_cond,
 // ------------------------------------------------------------------------------------
 // factorize
 // ------------------------------------------------------------------------------------
-Fact* factorize(Ctx* c, Mat* m, const lrs_solver_cfg& cfg) {
+Fact* factorize(Ctx* c, Mat* m, const lrs_solver_cfg& cfg, const lrs_comm* comm) {
   if (m->scalar != LRS_F64)
     throw LrsError(LRS_ERR_NOT_IMPLEMENTED, "complex128 factorization is not implemented yet");
   std::unique_ptr<Fact> f(new Fact());
@@ -369,7 +531,17 @@ Fact* factorize(Ctx* c, Mat* m, const lrs_solver_cfg& cfg) {
     throw LrsError(LRS_ERR_PARAMETER, "unknown variant");
   if (cfg.p < 1) throw LrsError(LRS_ERR_PARAMETER, "p >= 1 required");
   if (cfg.n_svd < 0) throw LrsError(LRS_ERR_PARAMETER, "n_svd >= 0 required");
-  f->P = (int)cfg.p;
+  if (comm && comm->size > 1) {
+    if (!comm->allgather || !comm->sendrecv)
+      throw LrsError(LRS_ERR_PARAMETER, "lrs_comm needs allgather and sendrecv callbacks");
+    if (comm->rank < 0 || comm->rank >= comm->size)
+      throw LrsError(LRS_ERR_PARAMETER, "lrs_comm rank out of range");
+    if (cfg.p < comm->size) throw LrsError(LRS_ERR_PARAMETER, "p must be >= the number of GPUs");
+    f->dist = true;
+    f->comm = *comm;
+  }
+  const int G = f->nranks(), rank = f->rank();
+  f->Pg = (int)cfg.p;
   f->n = m->n;
   f->k = cfg.k > 0 ? cfg.k : m->k;
   f->kl = m->kl;
@@ -377,21 +549,39 @@ Fact* factorize(Ctx* c, Mat* m, const lrs_solver_cfg& cfg) {
   f->passes = cfg.passes > 0 ? cfg.passes : 2;
   f->seed = cfg.seed;
   f->os = (int)cfg.oversample;
-  // layout
+  // global layout and this rank's shard
   {
-    const int64_t P = f->P, n = f->n;
-    f->size.resize(P);
-    f->off.resize(P);
-    for (int64_t i = 0; i < P; ++i) f->size[i] = n / P + (i < n % P ? 1 : 0);
-    int64_t o = 0;
-    for (int64_t i = 0; i < P; ++i) {
-      f->off[i] = o;
-      o += f->size[i];
+    const int64_t Pg = f->Pg, n = f->n;
+    f->goff.assign(Pg + 1, 0);
+    int64_t mn = n;
+    for (int64_t i = 0; i < Pg; ++i) {
+      const int64_t s = n / Pg + (i < n % Pg ? 1 : 0);
+      f->goff[i + 1] = f->goff[i] + s;
+      mn = std::min(mn, s);
     }
-    const int64_t mn = *std::min_element(f->size.begin(), f->size.end());
     if (mn <= f->k)
       throw LrsError(LRS_ERR_LAYOUT, "layout infeasible: need n >= p*(k+1) = " +
-                                         std::to_string(P * (f->k + 1)));
+                                         std::to_string(Pg * (f->k + 1)));
+    int64_t plo, phi;
+    shard_plan(Pg, G, rank, &plo, &phi);
+    f->p0 = (int)plo;
+    f->P = (int)(phi - plo);
+    f->row_lo = f->goff[plo];
+    f->row_hi = f->goff[phi];
+    f->off.resize(f->P);
+    f->size.resize(f->P);
+    for (int i = 0; i < f->P; ++i) {
+      f->off[i] = f->goff[plo + i];
+      f->size[i] = f->goff[plo + i + 1] - f->goff[plo + i];
+    }
+    f->rank_pl.resize(G);
+    f->pl_max = 0;
+    for (int q = 0; q < G; ++q) {
+      int64_t a, b;
+      shard_plan(Pg, G, q, &a, &b);
+      f->rank_pl[q] = (int)(b - a);
+      f->pl_max = std::max(f->pl_max, f->rank_pl[q]);
+    }
   }
   const int P = f->P;
   f->wl = (int)((f->kl + NB - 1) / NB);
@@ -400,12 +590,16 @@ Fact* factorize(Ctx* c, Mat* m, const lrs_solver_cfg& cfg) {
   f->tbase.resize(P);
   f->fbase.resize(P);
   f->Tmax = 0;
+  int Tmax_all = 0;
+  for (int i = 0; i < f->Pg; ++i)
+    Tmax_all = std::max<int>(Tmax_all, (int)((f->goff[i + 1] - f->goff[i] + NB - 1) / NB));
   for (int i = 0; i < P; ++i) {
     f->T[i] = (int)((f->size[i] + NB - 1) / NB);
     f->Tmax = std::max(f->Tmax, f->T[i]);
   }
-  f->wl = std::min(f->wl, std::max(0, f->Tmax - 1));
-  f->wu = std::min(f->wu, std::max(0, f->Tmax - 1));
+  // band width in tiles from the global block sizes, identical on every rank
+  f->wl = std::min(f->wl, std::max(0, Tmax_all - 1));
+  f->wu = std::min(f->wu, std::max(0, Tmax_all - 1));
   f->W = f->wl + f->wu + 1;
   int64_t tb = 0, fb = 0;
   for (int i = 0; i < P; ++i) {
@@ -421,6 +615,8 @@ Fact* factorize(Ctx* c, Mat* m, const lrs_solver_cfg& cfg) {
   upload(c, f->d_tbase, f->tbase);
   upload(c, f->d_fbase, f->fbase);
   upload(c, f->d_T, f->T);
+  upload(c, f->d_goff, f->goff);
+  upload(c, f->d_rank_pl, f->rank_pl);
   f->tiles.alloc((size_t)tb * TILE_ELEMS);
   f->flags.alloc((size_t)fb);
   f->ticket.alloc(1);
@@ -434,13 +630,21 @@ Fact* factorize(Ctx* c, Mat* m, const lrs_solver_cfg& cfg) {
   {
     const int64_t CH = 2048;
     f->chunk_start.clear();
-    for (int i = 0; i < P; ++i)
+    f->part_first.assign(P + 1, 0);
+    for (int i = 0; i < P; ++i) {
+      f->part_first[i] = (int)f->chunk_start.size();
       for (int64_t r0 = 0; r0 < f->size[i]; r0 += CH) f->chunk_start.push_back(f->off[i] + r0);
-    f->chunk_start.push_back(f->n);
+    }
+    f->part_first[P] = (int)f->chunk_start.size();
+    f->chunk_start.push_back(f->row_hi);
     upload(c, f->d_chunks, f->chunk_start);
+    upload(c, f->d_part_first, f->part_first);
     const size_t nch = f->chunk_start.size() - 1;
     f->partial.alloc(nch * 64 * MAX_RHS);
+    f->persum.alloc((size_t)f->pl_max * 64 * MAX_RHS);
+    f->gather.alloc((size_t)G * f->pl_max * 64 * MAX_RHS);
     f->dotout.alloc(64 * MAX_RHS);
+    f->xch.alloc((size_t)4 * std::max<int64_t>(1, m->k) * MAX_RHS);
   }
   cudaEvent_t e0, e1, e2, e3;
   LRS_CUDA(cudaEventCreate(&e0));
@@ -457,16 +661,22 @@ Fact* factorize(Ctx* c, Mat* m, const lrs_solver_cfg& cfg) {
   EvGuard eg{evs};
   LRS_CUDA(cudaEventRecord(e0, c->stream));
   const BandGeom g = f->geom();
-  launch_extract_tiles(c, m, g, f->tiles.get(), f->k, nullptr, f->bad.get());
+  launch_extract_tiles(c, m, g, f->tiles.get(), f->k, f->row_lo, f->row_hi, f->bad.get());
   {
     unsigned long long hb = 0;
     download(c, &hb, f->bad.get(), 1);
-    if (hb != ~0ull) {
+    // agree on the first offending entry over all ranks (row-major order)
+    const std::vector<double> all = allgather_host(f.get(), {hb == ~0ull ? -1.0 : (double)hb});
+    double first = -1.0;
+    for (double v : all)
+      if (v >= 0 && (first < 0 || v < first)) first = v;
+    if (first >= 0) {
+      const unsigned long long hv = (unsigned long long)first;
       LrsError e(LRS_ERR_NOT_BLOCK_TRIDIAGONAL,
-                 "nonzero (" + std::to_string(hb / f->n) + "," + std::to_string(hb % f->n) +
+                 "nonzero (" + std::to_string(hv / f->n) + "," + std::to_string(hv % f->n) +
                      ") outside the block-tridiagonal pattern; increase k or decrease p");
-      e.row = (int64_t)(hb / f->n);
-      e.col = (int64_t)(hb % f->n);
+      e.row = (int64_t)(hv / f->n);
+      e.col = (int64_t)(hv % f->n);
       throw e;
     }
   }
@@ -475,34 +685,49 @@ Fact* factorize(Ctx* c, Mat* m, const lrs_solver_cfg& cfg) {
   {
     const int r0 = (int)cfg.n_svd;
     const int l0 = r0 + (cfg.oversample >= 0 ? (int)cfg.oversample : (r0 + 1) / 2);
-    if (f->variant == LRS_VARIANT_T && P > 1 && r0 >= 1 && l0 <= f->k)
-      omega_future = std::async(std::launch::async, make_omega, f->seed, P, f->k, l0);
+    if (f->variant == LRS_VARIANT_T && f->Pg > 1 && r0 >= 1 && l0 <= f->k)
+      omega_future = std::async(std::launch::async, make_omega, f->seed, f->Pg, f->p0,
+                                f->p0 + P, f->k, l0);
   }
   launch_band_lu(c, g, f->tiles.get(), f->Tmax, f->status.get());
   LRS_CUDA(cudaEventRecord(e1, c->stream));
   {
     std::vector<int> st(2 * P);
     download(c, st.data(), f->status.get(), st.size());
-    for (int i = 0; i < P; ++i) {
+    // (global block index, code: 1 zero pivot / 2 interchange, column) -- first in order
+    double blk = -1, code = 0, col = 0;
+    for (int i = 0; i < P && blk < 0; ++i) {
       if (st[2 * i + 1] != 0x7f7f7f7f) {
-        LrsError e(LRS_ERR_SINGULAR_BLOCK, "exact zero pivot in column " +
-                                               std::to_string(st[2 * i + 1]) + " of block " +
-                                               std::to_string(i));
-        e.column = st[2 * i + 1];
+        blk = f->p0 + i;
+        code = 1;
+        col = st[2 * i + 1];
+      } else if (st[2 * i] != 0x7f7f7f7f) {
+        blk = f->p0 + i;
+        code = 2;
+        col = st[2 * i];
+      }
+    }
+    const std::vector<double> all = allgather_host(f.get(), {blk, code, col});
+    for (size_t q = 0; q < all.size(); q += 3) {
+      if (all[q] < 0) continue;
+      const int b = (int)all[q];
+      const int64_t cc = (int64_t)all[q + 2];
+      if (all[q + 1] == 1) {
+        LrsError e(LRS_ERR_SINGULAR_BLOCK, "exact zero pivot in column " + std::to_string(cc) +
+                                               " of block " + std::to_string(b));
+        e.column = cc;
         throw e;
       }
-      if (st[2 * i] != 0x7f7f7f7f) {
-        LrsError e(LRS_ERR_NOT_IMPLEMENTED,
-                   "block " + std::to_string(i) + " needs a row interchange at column " +
-                       std::to_string(st[2 * i]) +
-                       " (partial pivoting); the interchange path is not implemented on the GPU yet");
-        e.column = st[2 * i];
-        throw e;
-      }
+      LrsError e(LRS_ERR_NOT_IMPLEMENTED,
+                 "block " + std::to_string(b) + " needs a row interchange at column " +
+                     std::to_string(cc) +
+                     " (partial pivoting); the interchange path is not implemented on the GPU yet");
+      e.column = cc;
+      throw e;
     }
   }
   // spikes + truncated preconditioner, with the r-halving retry
-  int r = (f->variant == LRS_VARIANT_T && P > 1) ? (int)cfg.n_svd : 0;
+  int r = (f->variant == LRS_VARIANT_T && f->Pg > 1) ? (int)cfg.n_svd : 0;
   f->r = 0;
   f->l = 0;
   if (r > 0) {
@@ -537,7 +762,7 @@ Fact* factorize(Ctx* c, Mat* m, const lrs_solver_cfg& cfg) {
   // info
   lrs_fact_info& in = f->info;
   in.n = f->n;
-  in.p = P;
+  in.p = f->Pg;
   in.k = f->k;
   in.n_svd = f->r;
   in.l = f->l;
@@ -554,7 +779,7 @@ Fact* factorize(Ctx* c, Mat* m, const lrs_solver_cfg& cfg) {
   in.t_precond = 0.0;
   in.t_factorize = elapsed_ms(e0, e2) * 1e-3;
   if (in.max_interface_cond == 0.0) in.max_interface_cond = 1.0;
-  // algorithmic work: no-fill band LU flops; factor bytes streamed per apply
+  // algorithmic work of THIS shard: no-fill band LU flops, apply bytes
   double flops = 0.0, fbytes = 0.0;
   for (int i = 0; i < P; ++i) {
     const int64_t ni = f->size[i];
@@ -565,20 +790,22 @@ Fact* factorize(Ctx* c, Mat* m, const lrs_solver_cfg& cfg) {
       fbytes += a + 1.0 + b;
     }
   }
+  const double nl = (double)(f->row_hi - f->row_lo);
   in.lu_flops = (int64_t)flops;
-  in.apply_bytes = (int64_t)(8.0 * (fbytes + 2.0 * f->n + 2.0 * f->n * f->r));
+  in.apply_bytes = (int64_t)(8.0 * (fbytes + 2.0 * nl + 2.0 * nl * f->r));
   return f.release();
 }
 
 // ------------------------------------------------------------------------------------
-// Krylov drivers (mirror oracle.bicgstab / oracle.gmres)
+// Krylov drivers (mirror the oracle's bicgstab / gmres); vector work on the local rows
 // ------------------------------------------------------------------------------------
 namespace {
 
 struct Work {
   Fact* f;
   Mat* A;
-  int64_t n;
+  int64_t n;       // full length (ld of every block)
+  int64_t lo, nl;  // local rows [lo, lo + nl)
   int nr;
   bool bj;
   lrs_report* rep;
@@ -590,14 +817,26 @@ struct Work {
   }
   void init() { LRS_CUDA(cudaMallocHost(&hbuf, sizeof(double) * 64 * MAX_RHS * 2)); }
   Ctx* c() const { return f->ctx; }
-  // out[q*nr + j] for q < nvec
+  // out[q*nr + j] = X_q[:, j] . Y[:, j] over ALL rows (partition-ordered, any GPU count)
   void dots(const double* X, int64_t strideX, int nvec, const double* Y, double* out) {
-    launch_multidot(c(), f->chunks(), X, n, strideX, nvec, Y, n, nr, f->partial.get(),
-                    f->dotout.get());
-    LRS_CUDA(cudaMemcpyAsync(hbuf, f->dotout.get(), sizeof(double) * nvec * nr,
-                             cudaMemcpyDeviceToHost, c()->stream));
+    const int nout = nvec * nr;
+    launch_multidot_partition(c(), f->chunks(), X, n, strideX, nvec, Y, n, nr, f->partial.get(),
+                              f->persum.get());
+    if (f->dist) {
+      LRS_CUDA(cudaStreamSynchronize(c()->stream));
+      comm_rc(f->comm.allgather(f->comm.user, f->persum.get(), f->gather.get(),
+                                (int64_t)f->pl_max * nout),
+              "allgather");
+      launch_partition_total(c(), f->gather.get(), f->d_rank_pl.get(), f->comm.size, f->pl_max,
+                             nout, f->dotout.get());
+    } else {
+      launch_partition_total(c(), f->persum.get(), f->d_rank_pl.get(), 1, f->P, nout,
+                             f->dotout.get());
+    }
+    LRS_CUDA(cudaMemcpyAsync(hbuf, f->dotout.get(), sizeof(double) * nout, cudaMemcpyDeviceToHost,
+                             c()->stream));
     LRS_CUDA(cudaStreamSynchronize(c()->stream));
-    std::memcpy(out, hbuf, sizeof(double) * nvec * nr);
+    std::memcpy(out, hbuf, sizeof(double) * nout);
   }
   void norms(const double* X, double* out) {
     dots(X, 0, 1, X, out);
@@ -607,13 +846,25 @@ struct Work {
     apply_precond(f, in, n, out, n, nr, bj);
     rep->precond_applications++;
   }
-  void Aop(const double* in, double* out) {
-    launch_spmv(c(), A, in, n, out, n, nr, 0, nullptr, 0);
+  void Aop(double* in, double* out) {
+    halo_exchange(f, in, n, nr);
+    launch_spmv(c(), A, in, n, out, n, nr, 0, nullptr, 0, lo, lo + nl);
     rep->matvecs++;
   }
-  void resid(const double* b, const double* x, double* out) {  // out = b - A x
-    launch_spmv(c(), A, x, n, out, n, nr, 2, b, n);
+  void resid(const double* b, double* x, double* out) {  // out = b - A x
+    halo_exchange(f, x, n, nr);
+    launch_spmv(c(), A, x, n, out, n, nr, 2, b, n, lo, lo + nl);
     rep->matvecs++;
+  }
+  void axpby(int op, const ColScal& a, const ColScal& b, const ColScal& act, double* X,
+             const double* Y, const double* Z, double* Wv) {
+    launch_axpby_cols(c(), nl, nr, op, a, b, act, X ? X + lo : nullptr, n, Y ? Y + lo : nullptr, n,
+                      Z ? Z + lo : nullptr, n, Wv ? Wv + lo : nullptr, n);
+  }
+  void copy(double* dst, const double* src) { copy_block(c(), dst + lo, n, src + lo, n, nl, nr); }
+  void zero(double* dst) {
+    for (int j = 0; j < nr; ++j)
+      LRS_CUDA(cudaMemsetAsync(dst + lo + (int64_t)j * n, 0, sizeof(double) * nl, c()->stream));
   }
   void push(double v) { hist.push_back(v); }
 };
@@ -634,12 +885,10 @@ bool any(const std::vector<bool>& v) {
   return false;
 }
 
-// returns iterations per column; sets conv/brk
 void run_bicgstab(Work& w, const double* b, double* x, const lrs_iter_cfg& cfg, bool has_x0,
                   std::vector<double>& iters, std::vector<bool>& conv, std::vector<bool>& brk) {
   const int nr = w.nr;
   const int64_t n = w.n;
-  Ctx* c = w.c();
   const size_t blk = (size_t)n * nr;
   DevBuf<double> buf;
   buf.alloc(blk * 9);
@@ -659,8 +908,8 @@ void run_bicgstab(Work& w, const double* b, double* x, const lrs_iter_cfg& cfg, 
   if (has_x0) {
     w.resid(b, x, r);
   } else {
-    LRS_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * blk, c->stream));
-    copy_block(c, r, n, b, n, n, nr);
+    w.zero(x);
+    w.copy(r, b);
   }
   w.norms(r, tmpv.data());
   double mx = 0;
@@ -672,10 +921,10 @@ void run_bicgstab(Work& w, const double* b, double* x, const lrs_iter_cfg& cfg, 
     mx = std::max(mx, tmpv[j] / bns[j]);
   }
   w.push(mx);
-  copy_block(c, rhat, n, r, n, n, nr);
+  w.copy(rhat, r);
   std::vector<double> rho_prev(nr, 1.0), alpha(nr, 1.0), omega(nr, 1.0), rho(nr), rv(nr);
-  LRS_CUDA(cudaMemsetAsync(p, 0, sizeof(double) * blk, c->stream));
-  LRS_CUDA(cudaMemsetAsync(v, 0, sizeof(double) * blk, c->stream));
+  w.zero(p);
+  w.zero(v);
   const bool trace = std::getenv("LRS_TRACE") != nullptr;
   const auto t_start = std::chrono::steady_clock::now();
   for (int64_t it = 1; it <= cfg.max_iters; ++it) {
@@ -694,33 +943,31 @@ void run_bicgstab(Work& w, const double* b, double* x, const lrs_iter_cfg& cfg, 
       }
     if (!any(act)) break;
     if (it == 1) {
-      launch_axpby_cols(c, n, nr, 5, none, none, cs_mask(act), nullptr, 0, r, n, nullptr, 0, p, n);
+      w.axpby(5, none, none, cs_mask(act), nullptr, r, nullptr, p);
     } else {
       std::vector<double> beta(nr, 0.0);
       for (int j = 0; j < nr; ++j) beta[j] = (rho[j] / rho_prev[j]) * (alpha[j] / omega[j]);
-      launch_axpby_cols(c, n, nr, 0, cs_fill(beta), cs_fill(omega), cs_mask(act), p, n, r, n, v, n,
-                        nullptr, 0);
+      w.axpby(0, cs_fill(beta), cs_fill(omega), cs_mask(act), p, r, v, nullptr);
     }
     w.M(p, phat);
     w.Aop(phat, v);
     w.dots(rhat, 0, 1, v, rv.data());
     for (int j = 0; j < nr; ++j)
       if (act[j]) alpha[j] = rho[j] / (rv[j] != 0.0 ? rv[j] : 1.0);
-    launch_axpby_cols(c, n, nr, 1, cs_fill(alpha), none, cs_mask(act), nullptr, 0, r, n, v, n, s, n);
+    w.axpby(1, cs_fill(alpha), none, cs_mask(act), nullptr, r, v, s);
     w.norms(s, tmpv.data());
     std::vector<bool> half(nr, false);
     for (int j = 0; j < nr; ++j) half[j] = act[j] && tmpv[j] / bns[j] <= cfg.tol;
     std::vector<bool> hist_cols = act;
     if (any(half)) {
-      launch_axpby_cols(c, n, nr, 3, cs_fill(alpha), none, cs_mask(half), x, n, phat, n, nullptr, 0,
-                        tmp, n);
+      w.axpby(3, cs_fill(alpha), none, cs_mask(half), x, phat, nullptr, tmp);
       // true residual of the candidate (columns outside `half` are stale and unused)
       w.resid(b, tmp, t);
       w.norms(t, tmpv2.data());
       std::vector<bool> ok(nr, false);
       for (int j = 0; j < nr; ++j) ok[j] = half[j] && tmpv2[j] / bns[j] <= cfg.tol;
       if (any(ok)) {
-        launch_axpby_cols(c, n, nr, 5, none, none, cs_mask(ok), nullptr, 0, tmp, n, nullptr, 0, x, n);
+        w.axpby(5, none, none, cs_mask(ok), nullptr, tmp, nullptr, x);
         for (int j = 0; j < nr; ++j)
           if (ok[j]) {
             conv[j] = true;
@@ -746,9 +993,8 @@ void run_bicgstab(Work& w, const double* b, double* x, const lrs_iter_cfg& cfg, 
         brk[j] = true;
         act[j] = false;
       }
-    launch_axpby_cols(c, n, nr, 2, cs_fill(alpha), cs_fill(omega), cs_mask(act), x, n, phat, n, shat,
-                      n, nullptr, 0);
-    launch_axpby_cols(c, n, nr, 1, cs_fill(omega), none, cs_mask(act), nullptr, 0, s, n, t, n, r, n);
+    w.axpby(2, cs_fill(alpha), cs_fill(omega), cs_mask(act), x, phat, shat, nullptr);
+    w.axpby(1, cs_fill(omega), none, cs_mask(act), nullptr, s, t, r);
     w.norms(r, tmpv.data());
     std::vector<bool> full(nr, false);
     for (int j = 0; j < nr; ++j) full[j] = act[j] && tmpv[j] / bns[j] <= cfg.tol;
@@ -816,8 +1062,8 @@ void run_gmres(Work& w, const double* b, double* x, const lrs_iter_cfg& cfg, boo
   if (has_x0) {
     w.resid(b, x, r);
   } else {
-    LRS_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * blk, c->stream));
-    copy_block(c, r, n, b, n, n, nr);
+    w.zero(x);
+    w.copy(r, b);
   }
   w.norms(r, beta.data());
   conv.assign(nr, false);
@@ -836,8 +1082,7 @@ void run_gmres(Work& w, const double* b, double* x, const lrs_iter_cfg& cfg, boo
     if (!any(act)) break;
     std::vector<double> inv(nr);
     for (int j = 0; j < nr; ++j) inv[j] = 1.0 / (beta[j] > 0 ? beta[j] : 1.0);
-    launch_axpby_cols(c, n, nr, 4, cs_fill(inv), none, cs_mask(all), nullptr, 0, r, n, nullptr, 0,
-                      V, n);
+    w.axpby(4, cs_fill(inv), none, cs_mask(all), nullptr, r, nullptr, V);
     // per column Hessenberg (after rotations) R[row + col*(m+1)], g, rotations
     std::vector<std::vector<double>> R(nr, std::vector<double>((size_t)(m + 1) * m, 0.0));
     std::vector<std::vector<double>> g(nr, std::vector<double>(m + 1, 0.0));
@@ -851,18 +1096,18 @@ void run_gmres(Work& w, const double* b, double* x, const lrs_iter_cfg& cfg, boo
       double* Zj = Z + blk * jj;
       w.M(Vj, Zj);
       w.Aop(Zj, wv);
-      // CGS2
-      // (the projections stay on the device in f->dotout and feed the update directly)
+      // CGS2 (the projections stay on the device in dotout and feed the update directly)
       w.dots(V, (int64_t)blk, jj + 1, wv, h.data());
-      launch_multi_axpy_signed(c, n, nr, V, n, (int64_t)blk, jj + 1, w.f->dotout.get(), -1.0, wv, n);
+      launch_multi_axpy_signed(c, w.nl, nr, V + w.lo, n, (int64_t)blk, jj + 1,
+                               w.f->dotout.get(), -1.0, wv + w.lo, n);
       w.dots(V, (int64_t)blk, jj + 1, wv, h2.data());
-      launch_multi_axpy_signed(c, n, nr, V, n, (int64_t)blk, jj + 1, w.f->dotout.get(), -1.0, wv, n);
+      launch_multi_axpy_signed(c, w.nl, nr, V + w.lo, n, (int64_t)blk, jj + 1,
+                               w.f->dotout.get(), -1.0, wv + w.lo, n);
       w.norms(wv, hn.data());
       for (int q = 0; q < (jj + 1) * nr; ++q) h[q] += h2[q];
       std::vector<double> invn(nr);
       for (int j = 0; j < nr; ++j) invn[j] = 1.0 / (hn[j] > 0 ? hn[j] : 1.0);
-      launch_axpby_cols(c, n, nr, 4, cs_fill(invn), none, cs_mask(all), nullptr, 0, wv, n, nullptr,
-                        0, V + blk * (jj + 1), n);
+      w.axpby(4, cs_fill(invn), none, cs_mask(all), nullptr, wv, nullptr, V + blk * (jj + 1));
       mx = 0;
       for (int j = 0; j < nr; ++j) {
         if (!inner[j]) continue;
@@ -912,7 +1157,8 @@ void run_gmres(Work& w, const double* b, double* x, const lrs_iter_cfg& cfg, boo
         for (int q = 0; q < kk; ++q) y[(size_t)q * nr + j] = yy[q];
       }
       c->stage_h2d(ydev.get(), y.data(), sizeof(double) * y.size());
-      launch_multi_axpy_signed(c, n, nr, Z, n, (int64_t)blk, kmax, ydev.get(), 1.0, x, n);
+      launch_multi_axpy_signed(c, w.nl, nr, Z + w.lo, n, (int64_t)blk, kmax, ydev.get(), 1.0,
+                               x + w.lo, n);
       LRS_CUDA(cudaStreamSynchronize(c->stream));
     }
     w.resid(b, x, r);
@@ -945,7 +1191,7 @@ void solve(Fact* f, Mat* a, const double* b, int64_t ldb, double* x, int64_t ldx
   R.seed = f->seed;
   R.converged = 1;
   LRS_CUDA(cudaEventRecord(c->ev0, c->stream));
-  const int64_t n = f->n;
+  const int64_t n = f->n, lo = f->row_lo, nl = f->row_hi - f->row_lo;
   bool any_brk = false;
   double worst = 0.0;
   std::vector<double> hist_all;
@@ -955,18 +1201,21 @@ void solve(Fact* f, Mat* a, const double* b, int64_t ldb, double* x, int64_t ldx
     w.f = f;
     w.A = a;
     w.n = n;
+    w.lo = lo;
+    w.nl = nl;
     w.nr = nr;
     w.bj = f->variant == LRS_VARIANT_BJ;
     w.rep = &R;
     w.init();
-    // contiguous device copies (ld = n) of this column batch
+    // full-length device copies (ld = n) of this column batch; local rows only
     DevBuf<double> bb, xx;
     bb.alloc((size_t)n * nr);
     xx.alloc((size_t)n * nr);
-    copy_block(c, bb.get(), n, b + (int64_t)c0 * ldb, ldb, n, nr);
+    copy_block(c, bb.get() + lo, n, b + (int64_t)c0 * ldb + lo, ldb, nl, nr);
     const bool has_x0 = cfg.x0 != nullptr;
     if (has_x0)
-      copy_block(c, xx.get(), n, static_cast<const double*>(cfg.x0) + (int64_t)c0 * ldx, ldx, n, nr);
+      copy_block(c, xx.get() + lo, n, static_cast<const double*>(cfg.x0) + (int64_t)c0 * ldx + lo,
+                 ldx, nl, nr);
     std::vector<double> iters;
     std::vector<bool> conv, brk;
     if (cfg.method == LRS_BICGSTAB) {
@@ -988,11 +1237,12 @@ void solve(Fact* f, Mat* a, const double* b, int64_t ldb, double* x, int64_t ldx
       w.norms(bb.get(), bn.data());
       DevBuf<double> tmp;
       tmp.alloc((size_t)n * nr);
-      launch_spmv(c, a, xx.get(), n, tmp.get(), n, nr, 2, bb.get(), n);
+      halo_exchange(f, xx.get(), n, nr);
+      launch_spmv(c, a, xx.get(), n, tmp.get(), n, nr, 2, bb.get(), n, lo, lo + nl);
       w.norms(tmp.get(), rn.data());
       for (int j = 0; j < nr; ++j) worst = std::max(worst, rn[j] / (bn[j] > 0 ? bn[j] : 1.0));
     }
-    copy_block(c, x + (int64_t)c0 * ldx, ldx, xx.get(), n, n, nr);
+    copy_block(c, x + (int64_t)c0 * ldx + lo, ldx, xx.get() + lo, n, nl, nr);
     hist_all.insert(hist_all.end(), w.hist.begin(), w.hist.end());
   }
   LRS_CUDA(cudaEventRecord(c->ev1, c->stream));

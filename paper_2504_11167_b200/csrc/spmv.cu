@@ -16,8 +16,8 @@ __global__ void __launch_bounds__(256) spmv_kernel(int64_t n, const int* __restr
                                                    const double* __restrict__ x, int64_t ldx,
                                                    double* __restrict__ y, int64_t ldy, int nrhs,
                                                    int mode, const double* __restrict__ b,
-                                                   int64_t ldb) {
-  const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+                                                   int64_t ldb, int64_t row_lo) {
+  const int64_t row = row_lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (row >= n) return;
   double acc[NR];
 #pragma unroll
@@ -41,12 +41,13 @@ __global__ void __launch_bounds__(256) spmv_kernel(int64_t n, const int* __restr
 }
 
 void launch_spmv(Ctx* c, const Mat* m, const double* x, int64_t ldx, double* y, int64_t ldy,
-                 int nrhs, int mode, const double* b, int64_t ldb) {
-  const int64_t n = m->n;
-  if (n == 0 || nrhs == 0) return;
+                 int nrhs, int mode, const double* b, int64_t ldb, int64_t row_lo,
+                 int64_t row_hi) {
+  const int64_t n = row_hi < 0 ? m->n : row_hi;  // rows [row_lo, n)
+  if (n <= row_lo || nrhs == 0) return;
   for (int j0 = 0; j0 < nrhs; j0 += MAX_RHS) {
     const int nr = nrhs - j0 < MAX_RHS ? nrhs - j0 : MAX_RHS;
-    dim3 grid((unsigned)((n + 255) / 256));
+    dim3 grid((unsigned)((n - row_lo + 255) / 256));
     const double* xj = x + j0 * ldx;
     double* yj = y + j0 * ldy;
     const double* bj = b ? b + j0 * ldb : nullptr;
@@ -54,7 +55,7 @@ void launch_spmv(Ctx* c, const Mat* m, const double* x, int64_t ldx, double* y, 
 #define LRS_SPMV(NRV)                                                                     \
   spmv_kernel<NRV><<<grid, 256, 0, c->stream>>>(n, m->row_ptr.get(), m->col_idx.get(),    \
                                                 m->vals.get(), xj, ldx, yj, ldy, nr, mode, bj, \
-                                                ldb)
+                                                ldb, row_lo)
     if (nr == 1) LRS_SPMV(1);
     else if (nr <= 2) LRS_SPMV(2);
     else if (nr <= 4) LRS_SPMV(4);
