@@ -252,9 +252,11 @@ def solve_block(F: BlockFactor, R: np.ndarray) -> np.ndarray:
 
 
 def solve_block_adjoint(F: BlockFactor, R: np.ndarray) -> np.ndarray:
-    """A_i^-T R (transpose; the spikes are real-field in SPEC,
-    for complex we use the plain transpose as in T_i^T)."""
-    return _gbtrs(F, R, 1)
+    """A_i^-T R.  The SPEC is real-field; for the complex128
+    config (c5) the field-generic adjoint is the conjugate
+    transpose A_i^-H (gbtrs trans='C'), which is what the Halko range finder
+    needs (T^H Q)."""
+    return _gbtrs(F, R, 2 if np.iscomplexobj(F.ab) else 1)
 
 
 # --------------------------------------------------------------------------------------
@@ -326,17 +328,19 @@ def randomized_spike_svd(F: BlockFactor, coupling, side: int, n_svd: int, oversa
     def T_apply(X):
         return solve_block(F, _pad(np.asarray(Cs @ X), n, side))
 
-    def Tt_apply(Q):
+    CsH = Cs.conj().T if np.iscomplexobj(Cs.data) else Cs.T
+
+    def Tt_apply(Q):  # T^H Q (T^T Q for real)
         S = solve_block_adjoint(F, Q)
         tip = S[n - k:] if side == SIDE_T else S[:k]
-        return np.asarray(Cs.T @ tip)
+        return np.asarray(CsH @ tip)
 
     Q = _orth(T_apply(Om))
     for _ in range((passes - 2) // 2):
         W = _orth(Tt_apply(Q))
         Q = _orth(T_apply(W))
-    Zt = Tt_apply(Q)  # k x l
-    Uh, s, Vh = np.linalg.svd(Zt.T, full_matrices=False)  # Z = Uh diag(s) Vh
+    Zt = Tt_apply(Q)  # k x l, = (Q^H T)^H
+    Uh, s, Vh = np.linalg.svd(Zt.conj().T, full_matrices=False)  # Z = Uh diag(s) Vh
     u = Q @ Uh[:, :n_svd]
     sigma = s[:n_svd].copy()
     v = Vh[:n_svd].copy()

@@ -224,9 +224,18 @@ def _is_device(a) -> bool:
     return bool(getattr(a, "is_cuda", False))
 
 
-def _buf(a, n_rows):
-    """(pointer, ld, mem, ncols) of a column-major block (numpy F-order or torch CUDA)."""
+def _torch_dtype(dtype):
+    import torch
+
+    return torch.complex128 if np.dtype(dtype) == np.complex128 else torch.float64
+
+
+def _buf(a, n_rows, dtype=np.float64):
+    """(pointer, ld, mem, ncols) of a column-major block (numpy F-order or torch CUDA)
+    of the matrix scalar type (float64, or interleaved complex128)."""
     if _is_device(a):
+        if a.dtype != _torch_dtype(dtype):
+            raise DimensionError(f"device block must be {np.dtype(dtype).name}")
         if a.dim() == 1:
             return a.data_ptr(), n_rows, MEM_DEVICE, 1
         # torch: column-major blocks are stored as (n_rhs, n) row-major == (n, n_rhs) F-order
@@ -236,8 +245,8 @@ def _buf(a, n_rows):
     arr = np.asarray(a)
     if arr.ndim == 1:
         arr = arr.reshape(-1, 1)
-    if not (arr.flags.f_contiguous and arr.dtype == np.float64):
-        raise DimensionError("host block must be float64 Fortran-ordered")
+    if not (arr.flags.f_contiguous and arr.dtype == np.dtype(dtype)):
+        raise DimensionError(f"host block must be {np.dtype(dtype).name} Fortran-ordered")
     return arr.ctypes.data, arr.shape[0], MEM_HOST, arr.shape[1]
 
 
@@ -306,14 +315,17 @@ class CsrMatrix:
         self.n = int(n)
         rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
         ci = np.ascontiguousarray(col_idx, dtype=np.int64)
-        va = np.ascontiguousarray(values, dtype=np.float64)
+        cplx = np.iscomplexobj(values)
+        self.dtype = np.dtype(np.complex128 if cplx else np.float64)
+        va = np.ascontiguousarray(values, dtype=self.dtype)
         if rp.shape[0] != self.n + 1:
             raise DimensionError("row_ptr length must be n_rows + 1")
         if ci.shape[0] != va.shape[0]:
             raise DimensionError("col_idx/values length mismatch")
         h = vp()
         _check(lib().lrs_mat_upload_csr(ctx.h, self.n, va.shape[0], rp.ctypes.data, ci.ctypes.data,
-                                        va.ctypes.data, F64, MEM_HOST, ctypes.byref(h)), ctx.h)
+                                        va.ctypes.data, C128 if cplx else F64, MEM_HOST,
+                                        ctypes.byref(h)), ctx.h)
         self.h = h
         self.nnz = int(va.shape[0])
 
@@ -337,15 +349,16 @@ class CsrMatrix:
 
     def spmv(self, X, out=None, accumulate=False):
         """matrix.cpp:121-136: returns A X (or out += A X)."""
-        px, ldx, mem, nc = _buf(X, self.n)
+        px, ldx, mem, nc = _buf(X, self.n, self.dtype)
         if out is None:
             if mem == MEM_DEVICE:
                 import torch
 
-                out = torch.zeros((nc, self.n), dtype=torch.float64, device=X.device).t()
+                out = torch.zeros((nc, self.n), dtype=_torch_dtype(self.dtype),
+                                  device=X.device).t()
             else:
-                out = np.zeros((self.n, nc), order="F")
-        py, ldy, memy, _ = _buf(out, self.n)
+                out = np.zeros((self.n, nc), dtype=self.dtype, order="F")
+        py, ldy, memy, _ = _buf(out, self.n, self.dtype)
         if memy != mem:
             raise DimensionError("x and y must live in the same memory")
         _check(lib().lrs_spmv(self.h, px, ldx, py, ldy, nc, 1 if accumulate else 0, mem),
@@ -440,15 +453,16 @@ class SpikeFactorization:
         return self.info["n_svd"]
 
     def _apply(self, fn, f, out):
-        pin, ldi, mem, nc = _buf(f, self.A.n)
+        dt = self.A.dtype
+        pin, ldi, mem, nc = _buf(f, self.A.n, dt)
         if out is None:
             if mem == MEM_DEVICE:
                 import torch
 
-                out = torch.empty((nc, self.A.n), dtype=torch.float64, device=f.device).t()
+                out = torch.empty((nc, self.A.n), dtype=_torch_dtype(dt), device=f.device).t()
             else:
-                out = np.empty((self.A.n, nc), order="F")
-        po, ldo, memo, _ = _buf(out, self.A.n)
+                out = np.empty((self.A.n, nc), dtype=dt, order="F")
+        po, ldo, memo, _ = _buf(out, self.A.n, dt)
         if memo != mem:
             raise DimensionError("in and out must live in the same memory")
         _check(fn(self.h, pin, ldi, po, ldo, nc, mem), self.ctx.h)
@@ -464,7 +478,7 @@ class SpikeFactorization:
 
     def solve_block(self, i: int, R, adjoint: bool = False):
         """SPEC.md:226-241 on partition i (host arrays)."""
-        R = np.asfortranarray(np.asarray(R, dtype=np.float64).reshape(self.sizes[i], -1))
+        R = np.asfortranarray(np.asarray(R, dtype=self.A.dtype).reshape(self.sizes[i], -1))
         X = np.empty_like(R, order="F")
         _check(lib().lrs_solve_block(self.h, i, R.ctypes.data, R.shape[0], X.ctypes.data,
                                      X.shape[0], R.shape[1], 1 if adjoint else 0, MEM_HOST),
@@ -477,9 +491,9 @@ class SpikeFactorization:
     def spike(self, i: int, side: int):
         """(u n_i x r, sigma r, v r x k) of LowRankSpike T_i / W_i."""
         r, k, ni = self.n_svd, self.info["k"], self.sizes[i]
-        u = np.empty((ni, r), order="F")
+        u = np.empty((ni, r), dtype=self.A.dtype, order="F")
         s = np.empty(r)
-        v = np.empty((r, k), order="F")
+        v = np.empty((r, k), dtype=self.A.dtype, order="F")
         _check(lib().lrs_fact_get_spike(self.h, i, side, u.ctypes.data, s.ctypes.data,
                                         v.ctypes.data), self.ctx.h)
         return u, s, v
@@ -492,6 +506,8 @@ class SpikeFactorization:
         out = np.empty(need.value)
         _check(lib().lrs_fact_get_tiles(self.h, i, out.ctypes.data, need.value,
                                         ctypes.byref(need)), self.ctx.h)
+        if self.A.dtype == np.complex128:
+            out = out.view(np.complex128)
         return out.reshape(-1, W, nb, nb).transpose(0, 1, 3, 2)  # [I][J-slot][row][col]
 
     def ledger(self) -> dict:
@@ -511,18 +527,19 @@ def solve(A: CsrMatrix, f, cfg: SolverConfig | None = None, it: IterConfig | Non
     it = it or IterConfig()
     if F is None:
         F = SpikeFactorization(A.ctx, A, cfg or SolverConfig())
-    pb, ldb, mem, nc = _buf(f, A.n)
+    dt = A.dtype
+    pb, ldb, mem, nc = _buf(f, A.n, dt)
     if x_out is None:
         if mem == MEM_DEVICE:
             import torch
 
-            x_out = torch.empty((nc, A.n), dtype=torch.float64, device=f.device).t()
+            x_out = torch.empty((nc, A.n), dtype=_torch_dtype(dt), device=f.device).t()
         else:
-            x_out = np.empty((A.n, nc), order="F")
-    px, ldx, memx, _ = _buf(x_out, A.n)
+            x_out = np.empty((A.n, nc), dtype=dt, order="F")
+    px, ldx, memx, _ = _buf(x_out, A.n, dt)
     x0p = None
     if it.initial_guess is not None:
-        x0p, ldx0, mem0, _ = _buf(it.initial_guess, A.n)
+        x0p, ldx0, mem0, _ = _buf(it.initial_guess, A.n, dt)
         if mem0 != mem or ldx0 != ldx:
             raise DimensionError("initial guess must match x's memory kind and layout")
     ic = IterCfgC(GMRES if it.method == "gmres" else BICGSTAB, it.restart, it.tol, it.max_iters,

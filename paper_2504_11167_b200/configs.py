@@ -128,6 +128,15 @@ def omega(seed: int, partition: int, side: int, rows: int, cols: int) -> np.ndar
     return out.reshape((rows, cols), order="F")
 
 
+def shifted(A: Csr, z: complex) -> Csr:
+    """The FEAST contour system z I - A of config c5 (complex128).
+    Every row of the c5 base matrix holds its diagonal, so the pattern is unchanged."""
+    vals = -A.values.astype(np.complex128)
+    rows = np.repeat(np.arange(A.n), np.diff(A.row_ptr))
+    vals[rows == A.col_idx] += z
+    return Csr(A.n, A.row_ptr.copy(), A.col_idx.copy(), vals)
+
+
 @dataclass
 class Config:
     """One BASELINE.json configuration (possibly scaled down)."""
@@ -143,6 +152,10 @@ class Config:
     tol: float
     seed: int
     shifts: list = field(default_factory=list)  # c5 only
+
+    def system(self, j: int = 0) -> Csr:
+        """The matrix of shift j (c5: z_j I - A, complex); the matrix itself otherwise."""
+        return shifted(self.matrix, self.shifts[j]) if self.shifts else self.matrix
 
 
 def make_config(name: str, scale: float = 1.0, P: int | None = None) -> Config:

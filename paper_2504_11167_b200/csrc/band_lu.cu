@@ -356,19 +356,39 @@ static void lu_attrs() {
   g_lu_attr_set = true;
 }
 
-static void lu_diag_panel(Ctx* c, cudaStream_t s, const BandGeom& g, double* tiles, int K,
-                          int* status) {
+static void real_diag(Ctx* c, cudaStream_t s, const BandGeom& g, void* tiles, int K, int* status) {
+  lu_diag_kernel<<<g.P, DIAG_THREADS, sizeof(double) * (TILE_ELEMS + 4 * NB), s>>>(
+      g, static_cast<double*>(tiles), K, status);
+}
+static void real_gemm(Ctx* c, cudaStream_t s, const BandGeom& g, void* tiles, int K, int* status,
+                      int kind) {
+  double* t = static_cast<double*>(tiles);
+  if (kind == 0)
+    lu_gemm_kernel<0><<<dim3(g.wl + g.wu, g.P), GEMM_THREADS, GEMM_SMEM, s>>>(g, t, K, status);
+  else if (kind == 1)
+    lu_gemm_kernel<1><<<dim3((g.wl - 1) * (g.wu - 1), g.P), GEMM_THREADS, GEMM_SMEM, s>>>(g, t, K,
+                                                                                          status);
+  else
+    lu_gemm_kernel<2><<<dim3(g.wl + g.wu - 1, g.P), GEMM_THREADS, GEMM_SMEM, s>>>(g, t, K, status);
+}
+
+static void lu_diag_panel(Ctx* c, cudaStream_t s, const BandGeom& g, void* tiles, int K,
+                          int* status, const LuKernels& L) {
   {
     ProfScope ps_(c, K_LU_DIAG, s);
-    lu_diag_kernel<<<g.P, DIAG_THREADS, sizeof(double) * (TILE_ELEMS + 4 * NB), s>>>(g, tiles, K,
-                                                                                    status);
+    L.diag(c, s, g, tiles, K, status);
     LRS_LAUNCHED(c);
   }
   if (g.wl + g.wu > 0) {
     ProfScope ps_(c, K_LU_PANEL, s);
-    lu_gemm_kernel<0><<<dim3(g.wl + g.wu, g.P), GEMM_THREADS, GEMM_SMEM, s>>>(g, tiles, K, status);
+    L.gemm(c, s, g, tiles, K, status, 0);
     LRS_LAUNCHED(c);
   }
+}
+
+void launch_band_lu(Ctx* c, const BandGeom& g, double* tiles, int Tmax, int* status) {
+  lu_attrs();
+  run_band_lu(c, g, tiles, Tmax, status, LuKernels{real_diag, real_gemm});
 }
 
 // Right-looking tiled LU with look-ahead depth 1 over two streams:
@@ -376,33 +396,31 @@ static void lu_diag_panel(Ctx* c, cudaStream_t s, const BandGeom& g, double* til
 //   main               : [wait panel(K)]  rest(K)
 // next(K) applies step K to pivot row/column K+1 only, so diag/panel of step K+1
 // overlap the bulk trailing update rest(K) (I, J >= K+2) instead of idling the GPU.
-void launch_band_lu(Ctx* c, const BandGeom& g, double* tiles, int Tmax, int* status) {
-  lu_attrs();
+void run_band_lu(Ctx* c, const BandGeom& g, void* tiles, int Tmax, int* status,
+                 const LuKernels& L) {
   if (Tmax <= 0) return;
   cudaStream_t sm = c->stream, sc = c->stream_hi;
   cudaEvent_t ev_start = c->take_event(), ev_panel = c->take_event(), ev_panel2 = c->take_event(),
               ev_rest = c->take_event();
   LRS_CUDA(cudaEventRecord(ev_start, sm));
   LRS_CUDA(cudaStreamWaitEvent(sc, ev_start, 0));
-  lu_diag_panel(c, sc, g, tiles, 0, status);
+  lu_diag_panel(c, sc, g, tiles, 0, status, L);
   LRS_CUDA(cudaEventRecord(ev_panel, sc));
   for (int K = 0; K < Tmax; ++K) {
     if (K + 1 < Tmax) {
       if (K >= 1) LRS_CUDA(cudaStreamWaitEvent(sc, ev_rest, 0));
       if (g.wl > 0 && g.wu > 0) {
         ProfScope ps_(c, K_LU_UPDATE, sc);
-        lu_gemm_kernel<2><<<dim3(g.wl + g.wu - 1, g.P), GEMM_THREADS, GEMM_SMEM, sc>>>(g, tiles, K,
-                                                                                       status);
+        L.gemm(c, sc, g, tiles, K, status, 2);
         LRS_LAUNCHED(c);
       }
-      lu_diag_panel(c, sc, g, tiles, K + 1, status);
+      lu_diag_panel(c, sc, g, tiles, K + 1, status, L);
       LRS_CUDA(cudaEventRecord(ev_panel2, sc));
     }
     LRS_CUDA(cudaStreamWaitEvent(sm, ev_panel, 0));
     if (g.wl > 1 && g.wu > 1) {
       ProfScope ps_(c, K_LU_UPDATE, sm);
-      lu_gemm_kernel<1><<<dim3((g.wl - 1) * (g.wu - 1), g.P), GEMM_THREADS, GEMM_SMEM, sm>>>(
-          g, tiles, K, status);
+      L.gemm(c, sm, g, tiles, K, status, 1);
       LRS_LAUNCHED(c);
     }
     LRS_CUDA(cudaEventRecord(ev_rest, sm));

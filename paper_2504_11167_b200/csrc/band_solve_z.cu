@@ -1,0 +1,290 @@
+// Complex128 dataflow banded triangular solves (config 5).  Same ticket / flag /
+// bulk-copy pipeline as band_solve.cu; chunks are 16 complex tile columns (32 KB) and
+// every chunk product runs on DMMA as four real products per complex one.  Modes 2/3
+// apply the conjugate transpose (U^H, L^H): the adjoint a complex randomized SVD needs
+// (Z = Q^H T  =>  T^H Q = pad(C)^H A^-H Q).  All widths share one code path, so
+// multi-column == column-by-column bit-exactly.
+#include "common.cuh"
+#include "kernels.h"
+#include "lrs_internal.h"
+
+namespace lrs {
+
+constexpr int ZS_THREADS = 256;
+constexpr int ZCH_COLS = 16;
+constexpr int ZCH_SM = ZCH_COLS * NB;  // complex elements per chunk
+constexpr int ZNCH = NB / ZCH_COLS;    // 8 chunks per tile
+constexpr int ZSTAGES = 3;
+
+template <int NR>
+constexpr size_t zsolve_smem_bytes() {
+  return sizeof(zc) * ((size_t)ZSTAGES * ZCH_SM + 2 * (size_t)NB * (NR + 4)) + 16 * ZSTAGES + 64;
+}
+
+template <int MODE, int NR>
+__global__ void __launch_bounds__(ZS_THREADS, 1)
+    band_solve_z_kernel(BandGeom g, const zc* __restrict__ tiles, zc* x, int64_t ld, int nrhs,
+                        unsigned* flags, unsigned epoch, int* ticket, int p_only) {
+  constexpr int XLD = NR + 4;
+  constexpr bool FWD = (MODE == 0 || MODE == 2);
+  constexpr bool TRANS = (MODE >= 2);
+  constexpr int NJ = NR / 8;
+  extern __shared__ __align__(128) unsigned char smraw[];
+  zc* ring = reinterpret_cast<zc*>(smraw);
+  zc* xs = ring + (size_t)ZSTAGES * ZCH_SM;
+  zc* red = xs + NB * XLD;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(red + NB * XLD);
+  int* s_tk = reinterpret_cast<int*>(bars + ZSTAGES);
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  if (tid == 0) *s_tk = atomicAdd(ticket, 1);
+  __syncthreads();
+  const int tk = *s_tk;
+  int p, tt;
+  if (p_only >= 0) {
+    p = p_only;
+    tt = tk;
+  } else {
+    p = tk % g.P;
+    tt = tk / g.P;
+  }
+  const int T = g.T[p];
+  if (tt >= T) return;
+  const int t = FWD ? tt : T - 1 - tt;
+  const int64_t base = g.tbase[p], off = g.off[p], size = g.size[p];
+  const int W = g.W, wl = g.wl;
+  int s0, ndeps, sstep;
+  if (MODE == 0) { s0 = max(0, t - g.wl); ndeps = t - s0; sstep = 1; }
+  else if (MODE == 1) { s0 = min(T - 1, t + g.wu); ndeps = s0 - t; sstep = -1; }
+  else if (MODE == 2) { s0 = max(0, t - g.wu); ndeps = t - s0; sstep = 1; }
+  else { s0 = min(T - 1, t + g.wl); ndeps = s0 - t; sstep = -1; }
+  auto tile_ptr = [&](int d) -> const zc* {
+    if (d == ndeps) return tiles + (base + (int64_t)t * W + wl) * TILE_ELEMS;
+    const int s = s0 + d * sstep;
+    if (!TRANS) return tiles + (base + (int64_t)t * W + (s - t + wl)) * TILE_ELEMS;
+    return tiles + (base + (int64_t)s * W + (t - s + wl)) * TILE_ELEMS;
+  };
+  const int Q = (ndeps + 1) * ZNCH;
+  auto issue = [&](int q, int st) {
+    const zc* src = tile_ptr(q / ZNCH) + (size_t)(q % ZNCH) * ZCH_SM;
+    mbar_expect_tx(&bars[st], ZCH_SM * sizeof(zc));
+    bulk_g2s(ring + (size_t)st * ZCH_SM, src, ZCH_SM * sizeof(zc), &bars[st]);
+  };
+  if (tid == 0) {
+    for (int st = 0; st < ZSTAGES; ++st) mbar_init(&bars[st], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (tid == 0)
+    for (int q = 0; q < ZSTAGES && q < Q; ++q) issue(q, q);
+  const int64_t row0 = (int64_t)t * NB;
+  const int gq = lane >> 2, tq = lane & 3;
+  double accr[2][NJ][2], acci[2][NJ][2];
+#pragma unroll
+  for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+    for (int nj = 0; nj < NJ; ++nj)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) accr[mi][nj][e] = acci[mi][nj][e] = 0.0;
+  if (!TRANS) {
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi) {
+      const int m = 16 * w + 8 * mi + gq;
+      if (row0 + m < size)
+#pragma unroll
+        for (int nj = 0; nj < NJ; ++nj)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int n = 8 * nj + 2 * tq + e;
+            if (n < nrhs) {
+              const zc v = x[off + row0 + m + n * ld];
+              accr[mi][nj][e] = v.x;
+              acci[mi][nj][e] = v.y;
+            }
+          }
+    }
+  } else {
+    for (int e = tid; e < NB * NR; e += ZS_THREADS) {
+      const int r = e % NB, j = e / NB;
+      red[r * XLD + j] = (j < nrhs && row0 + r < size) ? x[off + row0 + r + j * ld] : zc{0.0, 0.0};
+    }
+  }
+  for (int q = 0; q < Q; ++q) {
+    const int d = q / ZNCH, sub = q % ZNCH, st = q % ZSTAGES;
+    const bool diag = (d == ndeps);
+    if (sub == 0) {
+      if (!diag) {
+        const int s = s0 + d * sstep;
+        if (tid == 0) {
+          const unsigned* f = flags + g.fbase[p] + s;
+          while (ld_acquire_u32(f) != epoch) __nanosleep(32);
+        }
+        __syncthreads();
+        const int64_t srow0 = (int64_t)s * NB;
+        for (int e = tid; e < NB * NR; e += ZS_THREADS) {
+          const int r = e % NB, j = e / NB;
+          zc v = {0.0, 0.0};
+          if (j < nrhs && srow0 + r < size) {
+            const double2 raw = __ldcg(reinterpret_cast<const double2*>(x + off + srow0 + r + j * ld));
+            v = {raw.x, raw.y};
+          }
+          xs[r * XLD + j] = v;
+        }
+      } else {
+        if (!TRANS) {
+#pragma unroll
+          for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+            for (int nj = 0; nj < NJ; ++nj)
+#pragma unroll
+              for (int e = 0; e < 2; ++e) {
+                xs[(16 * w + 8 * mi + gq) * XLD + 8 * nj + 2 * tq + e] = {accr[mi][nj][e], acci[mi][nj][e]};
+                accr[mi][nj][e] = acci[mi][nj][e] = 0.0;
+              }
+        } else {
+          __syncthreads();
+          for (int e = tid; e < NB * NR; e += ZS_THREADS) {
+            const int r = e % NB, j = e / NB;
+            xs[r * XLD + j] = red[r * XLD + j];
+            red[r * XLD + j] = {0.0, 0.0};
+          }
+        }
+      }
+      __syncthreads();
+    }
+    mbar_wait(&bars[st], (unsigned)((q / ZSTAGES) & 1));
+    const zc* ch = ring + (size_t)st * ZCH_SM;
+    const int cbase = sub * ZCH_COLS;
+    if (!TRANS) {
+#pragma unroll
+      for (int k4 = 0; k4 < ZCH_COLS / 4; ++k4) {
+        const int k = 4 * k4 + tq, kg = cbase + k;
+        double ar[2], ai[2], br[NJ], bi[NJ];
+#pragma unroll
+        for (int mi = 0; mi < 2; ++mi) {
+          const int m = 16 * w + 8 * mi + gq;
+          zc v = ch[k * NB + m];
+          if (diag) {
+            if (!(MODE == 0 ? m > kg : m <= kg)) v = {0.0, 0.0};
+          } else {
+            v = {-v.x, -v.y};
+          }
+          ar[mi] = v.x;
+          ai[mi] = v.y;
+        }
+#pragma unroll
+        for (int nj = 0; nj < NJ; ++nj) {
+          const zc v = xs[kg * XLD + 8 * nj + gq];
+          br[nj] = v.x;
+          bi[nj] = v.y;
+        }
+#pragma unroll
+        for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+          for (int nj = 0; nj < NJ; ++nj) {
+            dmma_8x8x4(accr[mi][nj][0], accr[mi][nj][1], ar[mi], br[nj]);
+            dmma_8x8x4(accr[mi][nj][0], accr[mi][nj][1], -ai[mi], bi[nj]);
+            dmma_8x8x4(acci[mi][nj][0], acci[mi][nj][1], ar[mi], bi[nj]);
+            dmma_8x8x4(acci[mi][nj][0], acci[mi][nj][1], ai[mi], br[nj]);
+          }
+      }
+    } else {
+      // out(16 x NR) (+|-)= conj(Tile)^T (16 x 128) xs (128 x NR): 2 x NJ tiles over warps
+      for (int ti = w; ti < 2 * NJ; ti += 8) {
+        const int mi = ti & 1, nj = ti >> 1;
+        double cr0 = 0.0, cr1 = 0.0, ci0 = 0.0, ci1 = 0.0;
+        const int mloc = 8 * mi + gq;
+        const int cglob = cbase + mloc;
+#pragma unroll 4
+        for (int k4 = 0; k4 < NB / 4; ++k4) {
+          const int r = 4 * k4 + tq;
+          zc a = ch[mloc * NB + r];
+          if (diag && !(MODE == 2 ? r <= cglob : r > cglob)) a = {0.0, 0.0};
+          const double ar = a.x, ai = -a.y;  // conjugate
+          const zc b = xs[r * XLD + 8 * nj + gq];
+          dmma_8x8x4(cr0, cr1, ar, b.x);
+          dmma_8x8x4(cr0, cr1, -ai, b.y);
+          dmma_8x8x4(ci0, ci1, ar, b.y);
+          dmma_8x8x4(ci0, ci1, ai, b.x);
+        }
+        zc* rp = red + (cbase + 8 * mi + gq) * XLD + 8 * nj + 2 * tq;
+        if (diag) {
+          rp[0] = {rp[0].x + cr0, rp[0].y + ci0};
+          rp[1] = {rp[1].x + cr1, rp[1].y + ci1};
+        } else {
+          rp[0] = {rp[0].x - cr0, rp[0].y - ci0};
+          rp[1] = {rp[1].x - cr1, rp[1].y - ci1};
+        }
+      }
+    }
+    __syncthreads();
+    if (tid == 0 && q + ZSTAGES < Q) issue(q + ZSTAGES, st);
+  }
+  if (!TRANS) {
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi) {
+      const int m = 16 * w + 8 * mi + gq;
+      if (row0 + m >= size) continue;
+#pragma unroll
+      for (int nj = 0; nj < NJ; ++nj)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int n = 8 * nj + 2 * tq + e;
+          if (n >= nrhs) continue;
+          zc v = {accr[mi][nj][e], acci[mi][nj][e]};
+          if (MODE == 0) v = s_add(v, xs[m * XLD + n]);
+          x[off + row0 + m + n * ld] = v;
+        }
+    }
+  } else {
+    for (int e = tid; e < NB * NR; e += ZS_THREADS) {
+      const int r = e % NB, j = e / NB;
+      if (j < nrhs && row0 + r < size) {
+        zc v = red[r * XLD + j];
+        if (MODE == 3) v = s_add(v, xs[r * XLD + j]);
+        x[off + row0 + r + j * ld] = v;
+      }
+    }
+  }
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) st_release_u32(flags + g.fbase[p] + t, epoch);
+}
+
+template <int MODE, int NR>
+static void zlaunch_mode(Ctx* c, const BandGeom& g, const zc* tiles, zc* x, int64_t ld, int nrhs,
+                         unsigned* flags, unsigned epoch, int* ticket, int p_only, int ntiles) {
+  static bool attr = false;
+  const size_t smem = zsolve_smem_bytes<NR>();
+  if (!attr) {
+    LRS_CUDA(cudaFuncSetAttribute(band_solve_z_kernel<MODE, NR>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  ProfScope ps_(c, c->in_setup ? K_SPIKE_SOLVE : (MODE >= 2 ? K_SOLVE_ADJ : K_SOLVE));
+  band_solve_z_kernel<MODE, NR><<<ntiles, ZS_THREADS, smem, c->stream>>>(
+      g, tiles, x, ld, nrhs, flags, epoch, ticket, p_only);
+  LRS_LAUNCHED(c);
+}
+
+template <int MODE>
+static void zlaunch_nr(Ctx* c, const BandGeom& g, const zc* tiles, zc* x, int64_t ld, int nrhs,
+                       unsigned* flags, unsigned epoch, int* ticket, int p_only, int ntiles) {
+  if (nrhs <= 8) zlaunch_mode<MODE, 8>(c, g, tiles, x, ld, nrhs, flags, epoch, ticket, p_only, ntiles);
+  else zlaunch_mode<MODE, 16>(c, g, tiles, x, ld, nrhs, flags, epoch, ticket, p_only, ntiles);
+}
+
+void launch_band_solve_z(Ctx* c, const BandGeom& g, const zc* tiles, int mode, zc* x, int64_t ld,
+                         int nrhs, unsigned* flags, unsigned epoch, int* ticket, int p_only,
+                         int ntiles) {
+  if (ntiles == 0 || nrhs == 0) return;
+  if (nrhs > ZSOLVE_MAX_RHS) throw LrsError(LRS_ERR_PARAMETER, "complex band solve batch > 16");
+  LRS_CUDA(cudaMemsetAsync(ticket, 0, sizeof(int), c->stream));
+  switch (mode) {
+    case 0: zlaunch_nr<0>(c, g, tiles, x, ld, nrhs, flags, epoch, ticket, p_only, ntiles); break;
+    case 1: zlaunch_nr<1>(c, g, tiles, x, ld, nrhs, flags, epoch, ticket, p_only, ntiles); break;
+    case 2: zlaunch_nr<2>(c, g, tiles, x, ld, nrhs, flags, epoch, ticket, p_only, ntiles); break;
+    default: zlaunch_nr<3>(c, g, tiles, x, ld, nrhs, flags, epoch, ticket, p_only, ntiles); break;
+  }
+}
+
+}  // namespace lrs

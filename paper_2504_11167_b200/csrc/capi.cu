@@ -70,31 +70,29 @@ static lrs_status guard(Ctx* c, F&& fn) {
 }
 
 // Host staging of a user buffer: returns a device pointer (uploading HOST data).
-struct DevView {
-  const double* p = nullptr;
-  DevBuf<double> own;
-};
-
-static const double* dev_in(Ctx* c, const void* src, int64_t ld, int64_t rows, int64_t cols,
-                            int32_t mem, DevBuf<double>& own, int64_t* ld_out) {
+// w = doubles per scalar (1: float64, 2: interleaved complex128).
+static void* dev_in(Ctx* c, const void* src, int64_t ld, int64_t rows, int64_t cols, int32_t mem,
+                    DevBuf<double>& own, int64_t* ld_out, int w) {
   if (mem == LRS_MEM_DEVICE) {
     *ld_out = ld;
-    return static_cast<const double*>(src);
+    return const_cast<void*>(src);
   }
-  own.alloc((size_t)std::max<int64_t>(1, rows * cols));
+  const size_t es = sizeof(double) * w;
+  own.alloc((size_t)std::max<int64_t>(1, rows * cols) * w);
   if (rows * cols > 0)
-    LRS_CUDA(cudaMemcpy2DAsync(own.get(), sizeof(double) * rows, src, sizeof(double) * ld,
-                               sizeof(double) * rows, cols, cudaMemcpyHostToDevice, c->stream));
+    LRS_CUDA(cudaMemcpy2DAsync(own.get(), es * rows, src, es * ld, es * rows, cols,
+                               cudaMemcpyHostToDevice, c->stream));
   *ld_out = rows;
   return own.get();
 }
 
-static void dev_out_finish(Ctx* c, void* dst, int64_t ld, const double* dev, int64_t rows,
-                           int64_t cols, int32_t mem) {
+static void dev_out_finish(Ctx* c, void* dst, int64_t ld, const void* dev, int64_t rows,
+                           int64_t cols, int32_t mem, int w) {
   if (mem == LRS_MEM_DEVICE) return;
+  const size_t es = sizeof(double) * w;
   if (rows * cols > 0)
-    LRS_CUDA(cudaMemcpy2DAsync(dst, sizeof(double) * ld, dev, sizeof(double) * rows,
-                               sizeof(double) * rows, cols, cudaMemcpyDeviceToHost, c->stream));
+    LRS_CUDA(cudaMemcpy2DAsync(dst, es * ld, dev, es * rows, es * rows, cols,
+                               cudaMemcpyDeviceToHost, c->stream));
   LRS_CUDA(cudaStreamSynchronize(c->stream));
 }
 
@@ -226,26 +224,28 @@ lrs_status lrs_mat_upload_csr(lrs_ctx* c, int64_t n, int64_t nnz, const int64_t*
     check_mem(mem);
     if (scalar != LRS_F64 && scalar != LRS_C128)
       throw LrsError(LRS_ERR_PARAMETER, "scalar must be LRS_F64 or LRS_C128");
-    if (scalar == LRS_C128)
-      throw LrsError(LRS_ERR_NOT_IMPLEMENTED, "complex128 matrices are not implemented yet");
     if (n < 0 || nnz < 0) throw LrsError(LRS_ERR_DIMENSION, "negative dimension");
     if (n >= (1ll << 31) || nnz >= (1ll << 31))
       throw LrsError(LRS_ERR_DIMENSION, "n and nnz must be < 2^31 on the device");
+    const int w = scalar == LRS_C128 ? 2 : 1;  // complex values are interleaved (re, im)
     std::vector<int64_t> rp(n + 1), ci(nnz);
-    std::vector<double> va(nnz);
+    std::vector<double> va((size_t)nnz * w);
     if (mem == LRS_MEM_HOST) {
       std::memcpy(rp.data(), row_ptr, sizeof(int64_t) * (n + 1));
       if (nnz) {
         std::memcpy(ci.data(), col_idx, sizeof(int64_t) * nnz);
-        std::memcpy(va.data(), values, sizeof(double) * nnz);
+        std::memcpy(va.data(), values, sizeof(double) * nnz * w);
       }
     } else {
       LRS_CUDA(cudaMemcpy(rp.data(), row_ptr, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToHost));
       if (nnz) {
         LRS_CUDA(cudaMemcpy(ci.data(), col_idx, sizeof(int64_t) * nnz, cudaMemcpyDeviceToHost));
-        LRS_CUDA(cudaMemcpy(va.data(), values, sizeof(double) * nnz, cudaMemcpyDeviceToHost));
+        LRS_CUDA(cudaMemcpy(va.data(), values, sizeof(double) * nnz * w, cudaMemcpyDeviceToHost));
       }
     }
+    auto absv = [&](int64_t p) {
+      return w == 1 ? std::fabs(va[p]) : std::hypot(va[2 * p], va[2 * p + 1]);
+    };
     // validate() -- matrix.cpp:21-37
     if (rp[0] != 0) throw LrsError(LRS_ERR_DIMENSION, "row_ptr[0] must be 0");
     if (rp[n] != nnz) throw LrsError(LRS_ERR_DIMENSION, "row_ptr[n_rows] must equal nnz");
@@ -261,8 +261,8 @@ lrs_status lrs_mat_upload_csr(lrs_ctx* c, int64_t n, int64_t nnz, const int64_t*
                          "column indices must be strictly increasing within a row");
         if (j > i) ku = std::max(ku, j - i);
         if (j < i) kl = std::max(kl, i - j);
-        tsum += std::fabs(va[p]);
-        if (i == j) dsum += std::fabs(va[p]);
+        tsum += absv(p);
+        if (i == j) dsum += absv(p);
       }
     }
     m->ctx = c;
@@ -277,7 +277,7 @@ lrs_status lrs_mat_upload_csr(lrs_ctx* c, int64_t n, int64_t nnz, const int64_t*
     m->band_density = cells > 0 ? (double)nnz / cells : 0.0;
     // device CSR with int32 indices, and the transpose (host counting sort, structural)
     std::vector<int> rp32(n + 1), ci32(nnz), trp(n + 1, 0), tci(nnz);
-    std::vector<double> tva(nnz);
+    std::vector<double> tva((size_t)nnz * w);
     for (int64_t i = 0; i <= n; ++i) rp32[i] = (int)rp[i];
     for (int64_t p = 0; p < nnz; ++p) {
       ci32[p] = (int)ci[p];
@@ -289,21 +289,21 @@ lrs_status lrs_mat_upload_csr(lrs_ctx* c, int64_t n, int64_t nnz, const int64_t*
       for (int64_t p = rp[i]; p < rp[i + 1]; ++p) {
         const int q = next[ci[p]]++;
         tci[q] = (int)i;
-        tva[q] = va[p];
+        for (int e = 0; e < w; ++e) tva[(size_t)q * w + e] = va[(size_t)p * w + e];
       }
     m->row_ptr.alloc(n + 1);
     m->col_idx.alloc(std::max<int64_t>(nnz, 1));
-    m->vals.alloc(std::max<int64_t>(nnz, 1));
+    m->vals.alloc(std::max<int64_t>(nnz, 1) * w);
     m->trow_ptr.alloc(n + 1);
     m->tcol_idx.alloc(std::max<int64_t>(nnz, 1));
-    m->tvals.alloc(std::max<int64_t>(nnz, 1));
+    m->tvals.alloc(std::max<int64_t>(nnz, 1) * w);
     LRS_CUDA(cudaMemcpy(m->row_ptr.get(), rp32.data(), sizeof(int) * (n + 1), cudaMemcpyHostToDevice));
     LRS_CUDA(cudaMemcpy(m->trow_ptr.get(), trp.data(), sizeof(int) * (n + 1), cudaMemcpyHostToDevice));
     if (nnz) {
       LRS_CUDA(cudaMemcpy(m->col_idx.get(), ci32.data(), sizeof(int) * nnz, cudaMemcpyHostToDevice));
-      LRS_CUDA(cudaMemcpy(m->vals.get(), va.data(), sizeof(double) * nnz, cudaMemcpyHostToDevice));
+      LRS_CUDA(cudaMemcpy(m->vals.get(), va.data(), sizeof(double) * nnz * w, cudaMemcpyHostToDevice));
       LRS_CUDA(cudaMemcpy(m->tcol_idx.get(), tci.data(), sizeof(int) * nnz, cudaMemcpyHostToDevice));
-      LRS_CUDA(cudaMemcpy(m->tvals.get(), tva.data(), sizeof(double) * nnz, cudaMemcpyHostToDevice));
+      LRS_CUDA(cudaMemcpy(m->tvals.get(), tva.data(), sizeof(double) * nnz * w, cudaMemcpyHostToDevice));
     }
   });
   if (s == LRS_OK) *out = m.release();
@@ -331,20 +331,18 @@ lrs_status lrs_spmv(lrs_mat* m, const void* x, int64_t ldx, void* y, int64_t ldy
     check_mem(mem);
     if (n_rhs < 0 || ldx < m->n || ldy < m->n)
       throw LrsError(LRS_ERR_DIMENSION, "spmv: A.n_cols must equal x.n_rows");
+    const int w = m->scalar == LRS_C128 ? 2 : 1;
     DevBuf<double> xo, yo;
     int64_t lx, ly;
-    const double* xd = dev_in(c, x, ldx, m->n, n_rhs, mem, xo, &lx);
-    double* yd;
-    if (mem == LRS_MEM_DEVICE) {
-      yd = static_cast<double*>(y);
-      ly = ldy;
-    } else {
-      int64_t tmp;
-      yd = const_cast<double*>(dev_in(c, y, ldy, m->n, n_rhs, mem, yo, &tmp));
-      ly = tmp;
-    }
-    launch_spmv(c, m, xd, lx, yd, ly, (int)n_rhs, accumulate ? 1 : 0, nullptr, 0);
-    dev_out_finish(c, y, ldy, yd, m->n, n_rhs, mem);
+    void* xd = dev_in(c, x, ldx, m->n, n_rhs, mem, xo, &lx, w);
+    void* yd = dev_in(c, y, ldy, m->n, n_rhs, mem, yo, &ly, w);
+    if (w == 2)
+      launch_spmv_z(c, m, static_cast<const zc*>(xd), lx, static_cast<zc*>(yd), ly, (int)n_rhs,
+                    accumulate ? 1 : 0, nullptr, 0);
+    else
+      launch_spmv(c, m, static_cast<const double*>(xd), lx, static_cast<double*>(yd), ly,
+                  (int)n_rhs, accumulate ? 1 : 0, nullptr, 0);
+    dev_out_finish(c, y, ldy, yd, m->n, n_rhs, mem, w);
   });
 }
 
@@ -426,21 +424,23 @@ lrs_status lrs_fact_get_spike(lrs_fact* f, int64_t i, int32_t side, double* u, d
     if (i < f->p0 || i >= f->p0 + f->P || (side == LRS_SIDE_T && i == f->Pg - 1) ||
         (side == LRS_SIDE_W && i == 0) || (side != LRS_SIDE_T && side != LRS_SIDE_W))
       throw LrsError(LRS_ERR_PARAMETER, "no such spike on this GPU");
-    const int r = f->r;
+    const int r = f->r, w = f->sw;
+    const size_t es = sizeof(double) * w;
     const int64_t n = f->n, k = f->k, ni = f->size[i - f->p0];
     const double* ub = side == LRS_SIDE_T ? f->uT.get() : f->uW.get();
     const double* vb = side == LRS_SIDE_T ? f->vtT.get() : f->vtW.get();
     const double* sb = side == LRS_SIDE_T ? f->sT.get() : f->sW.get();
     if (u)
-      LRS_CUDA(cudaMemcpy2D(u, sizeof(double) * ni, ub + f->goff[i], sizeof(double) * n,
-                            sizeof(double) * ni, r, cudaMemcpyDeviceToHost));
+      LRS_CUDA(cudaMemcpy2D(u, es * ni, ub + f->goff[i] * w, es * n, es * ni, r,
+                            cudaMemcpyDeviceToHost));
     if (sigma) LRS_CUDA(cudaMemcpy(sigma, sb + (size_t)i * r, sizeof(double) * r, cudaMemcpyDeviceToHost));
     if (v) {  // stored as v^T (k x r); return v (r x k, ld r)
-      std::vector<double> vt((size_t)k * r);
-      LRS_CUDA(cudaMemcpy(vt.data(), vb + (size_t)i * k * r, sizeof(double) * k * r,
+      std::vector<double> vt((size_t)k * r * w);
+      LRS_CUDA(cudaMemcpy(vt.data(), vb + (size_t)i * k * r * w, es * k * r,
                           cudaMemcpyDeviceToHost));
       for (int a = 0; a < r; ++a)
-        for (int64_t row = 0; row < k; ++row) v[a + row * r] = vt[row + (size_t)a * k];
+        for (int64_t row = 0; row < k; ++row)
+          for (int e = 0; e < w; ++e) v[(a + row * r) * w + e] = vt[(row + (size_t)a * k) * w + e];
     }
   });
 }
@@ -452,12 +452,12 @@ lrs_status lrs_fact_get_tiles(lrs_fact* f, int64_t i, double* host_out, int64_t 
     if (i < f->p0 || i >= f->p0 + f->P)
       throw LrsError(LRS_ERR_PARAMETER, "partition not on this GPU");
     const int li = (int)(i - f->p0);
-    const int64_t cnt = (int64_t)f->T[li] * f->W * TILE_ELEMS;
+    const int64_t cnt = (int64_t)f->T[li] * f->W * TILE_ELEMS * f->sw;  // doubles
     if (needed) *needed = cnt;
     if (host_out) {
       if (capacity < cnt) throw LrsError(LRS_ERR_DIMENSION, "tile buffer too small");
       LRS_CUDA(cudaStreamSynchronize(f->ctx->stream));
-      LRS_CUDA(cudaMemcpy(host_out, f->tiles.get() + f->tbase[li] * TILE_ELEMS,
+      LRS_CUDA(cudaMemcpy(host_out, f->tiles.get() + f->tbase[li] * TILE_ELEMS * f->sw,
                           sizeof(double) * cnt, cudaMemcpyDeviceToHost));
     }
   });
@@ -486,13 +486,14 @@ lrs_status lrs_solve_block(lrs_fact* f, int64_t i, const void* rhs, int64_t ld_r
       throw LrsError(LRS_ERR_DIMENSION, "solve_block: RHS rows must equal the block size");
     // work in a global-row-layout buffer so the partition offset addressing of the
     // dataflow kernel applies unchanged
+    const int w = f->sw;
+    const size_t es = sizeof(double) * w;
     DevBuf<double> work;
-    work.alloc((size_t)std::max<int64_t>(1, f->n * n_rhs));
-    double* wp = work.get() + f->off[li];
+    work.alloc((size_t)std::max<int64_t>(1, f->n * n_rhs) * w);
+    double* wp = work.get() + f->off[li] * w;
     const cudaMemcpyKind k_in = mem == LRS_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
     if (n_rhs > 0)
-      LRS_CUDA(cudaMemcpy2DAsync(wp, sizeof(double) * f->n, rhs, sizeof(double) * ld_rhs,
-                                 sizeof(double) * ni, n_rhs, k_in, c->stream));
+      LRS_CUDA(cudaMemcpy2DAsync(wp, es * f->n, rhs, es * ld_rhs, es * ni, n_rhs, k_in, c->stream));
     // solve_block always takes the batch-width-independent DMMA path
     struct FmaOff {
       Ctx* c;
@@ -503,8 +504,7 @@ lrs_status lrs_solve_block(lrs_fact* f, int64_t i, const void* rhs, int64_t ld_r
     dstage(f, work.get(), f->n, (int)n_rhs, adjoint != 0, li);
     const cudaMemcpyKind k_out = mem == LRS_MEM_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
     if (n_rhs > 0)
-      LRS_CUDA(cudaMemcpy2DAsync(x, sizeof(double) * ld_x, wp, sizeof(double) * f->n,
-                                 sizeof(double) * ni, n_rhs, k_out, c->stream));
+      LRS_CUDA(cudaMemcpy2DAsync(x, es * ld_x, wp, es * f->n, es * ni, n_rhs, k_out, c->stream));
     LRS_CUDA(cudaStreamSynchronize(c->stream));
   });
 }
@@ -518,15 +518,14 @@ static lrs_status apply_common(lrs_fact* f, const void* in, int64_t ld_in, void*
     if (ld_in < f->n || ld_out < f->n || n_rhs < 0)
       throw LrsError(LRS_ERR_DIMENSION, "apply: vector rows must equal n");
     if (mem == LRS_MEM_DEVICE) {
-      apply_precond(f, static_cast<const double*>(in), ld_in, static_cast<double*>(out), ld_out,
-                    (int)n_rhs, bj);
+      apply_precond(f, in, ld_in, out, ld_out, (int)n_rhs, bj);
       return;
     }
     DevBuf<double> io;
     int64_t ld;
-    const double* d = dev_in(c, in, ld_in, f->n, n_rhs, mem, io, &ld);
-    apply_precond(f, d, ld, const_cast<double*>(d), ld, (int)n_rhs, bj);
-    dev_out_finish(c, out, ld_out, d, f->n, n_rhs, mem);
+    void* d = dev_in(c, in, ld_in, f->n, n_rhs, mem, io, &ld, f->sw);
+    apply_precond(f, d, ld, d, ld, (int)n_rhs, bj);
+    dev_out_finish(c, out, ld_out, d, f->n, n_rhs, mem, f->sw);
   });
 }
 
@@ -554,24 +553,24 @@ lrs_status lrs_solve(lrs_fact* f, lrs_mat* a, const void* b, int64_t ldb, void* 
     if (cc.breakdown_eps <= 0) cc.breakdown_eps = 1e-30;
     if (cc.restart <= 0) cc.restart = 30;
     if (mem == LRS_MEM_DEVICE) {
-      solve(f, a, static_cast<const double*>(b), ldb, static_cast<double*>(x), ldx, (int)n_rhs, cc,
-            rep);
+      solve(f, a, b, ldb, x, ldx, (int)n_rhs, cc, rep);
       return;
     }
+    const int w = f->sw;
     DevBuf<double> bo, xo, x0o;
     int64_t lb, lx0 = f->n;
-    const double* bd = dev_in(c, b, ldb, f->n, n_rhs, mem, bo, &lb);
-    if (cc.x0) cc.x0 = dev_in(c, cc.x0, ldx, f->n, n_rhs, mem, x0o, &lx0);
-    xo.alloc((size_t)std::max<int64_t>(1, f->n * n_rhs));
+    const void* bd = dev_in(c, b, ldb, f->n, n_rhs, mem, bo, &lb, w);
+    if (cc.x0) cc.x0 = dev_in(c, cc.x0, ldx, f->n, n_rhs, mem, x0o, &lx0, w);
+    xo.alloc((size_t)std::max<int64_t>(1, f->n * n_rhs) * w);
     // x0 (if any) is addressed with ldx inside solve(); pass it with ld n
     try {
       solve(f, a, bd, lb, xo.get(), f->n, (int)n_rhs, cc, rep);
     } catch (const LrsError& e) {
       // breakdown keeps the partial result
-      if (e.status == LRS_ERR_BREAKDOWN) dev_out_finish(c, x, ldx, xo.get(), f->n, n_rhs, mem);
+      if (e.status == LRS_ERR_BREAKDOWN) dev_out_finish(c, x, ldx, xo.get(), f->n, n_rhs, mem, w);
       throw;
     }
-    dev_out_finish(c, x, ldx, xo.get(), f->n, n_rhs, mem);
+    dev_out_finish(c, x, ldx, xo.get(), f->n, n_rhs, mem, w);
   });
 }
 

@@ -1,143 +1,158 @@
-// Small dense kernels of the setup (K7/K8 of SURVEY.md 2.3): Householder QR of
-// tall-skinny blocks (orth() of the randomized spike SVD),
-// one-sided Jacobi SVD of the l x l R factor, the small GEMMs that form u and
-// v, and the per-interface Woodbury setup of build_truncated_precond
-// (G = K^-1 explicit, H = G - S_T vT uW S_W, cond_1 estimate).
-// All run on the GPU, one CTA per job; nothing here falls back to the host.
+// Small dense kernels of the setup (K7/K8 of SURVEY.md 2.3), real and complex:
+// Householder QR of tall-skinny blocks (orth() of the randomized spike SVD,
+// SPEC.md:289, :310; LAPACK geqr2 + ung2r semantics), one-sided Jacobi SVD of the
+// l x l R factor, the small GEMMs that form u and v, and the per-interface Woodbury
+// setup of build_truncated_precond (G = K^-1 explicit,
+// H = G - S_T vT uW S_W, cond_1 estimate).  All on the GPU, one CTA per job.
 #include "common.cuh"
 #include "kernels.h"
 #include "lrs_internal.h"
 
 namespace lrs {
 
+__device__ __forceinline__ double ds_warp_sum(double v) { return warp_sum(v); }
+__device__ __forceinline__ zc ds_warp_sum(zc v) { return warp_sum_z(v); }
+
 // ---------------------------------------------------------------------------------------
-// Householder QR (LAPACK dgeqr2 + dorg2r semantics, no column pivoting).
+// Householder QR.  Reflector j: H_j = I - tau_j v v^H (v_j = 1); the factorization
+// applies H_j^H (coefficient conj(tau)), the explicit Q applies H_j (coefficient tau).
 // ---------------------------------------------------------------------------------------
 constexpr int QR_THREADS = 512;
 constexpr int QR_CB = 8;  // columns per reduction batch
 
-__global__ void __launch_bounds__(QR_THREADS) householder_qr_kernel(const QrJob* jobs, int l) {
-  extern __shared__ double qsm[];
-  double* tau = qsm;                 // l
-  double* red = tau + l;             // (QR_THREADS/32) * QR_CB
-  double* wv = red + (QR_THREADS / 32) * QR_CB;  // QR_CB
-  const QrJob jb = jobs[blockIdx.x];
-  double* A = jb.A;
+template <class S>
+__global__ void __launch_bounds__(QR_THREADS) householder_qr_kernel(const QrJobT<S>* jobs, int l) {
+  extern __shared__ __align__(16) unsigned char qsm_raw[];
+  S* tau = reinterpret_cast<S*>(qsm_raw);   // l
+  S* red = tau + l;                         // (QR_THREADS/32) * QR_CB
+  S* wv = red + (QR_THREADS / 32) * QR_CB;  // QR_CB
+  double* rs = reinterpret_cast<double*>(wv + QR_CB);  // QR_THREADS/32 real partials
+  const QrJobT<S> jb = jobs[blockIdx.x];
+  S* A = jb.A;
   const int64_t m = jb.m, ld = jb.ld;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, nw = QR_THREADS / 32;
 
-  // apply H_j = I - tau v v^T (v_j = 1, v_i = A[i][j] for i > j) to columns [c0, c0+cb)
-  auto apply_reflector = [&](int j, int c0, int cb, double tj) {
-    double part[QR_CB];
+  // A[j:, c0:c0+cb] -= v (coef * (v^H A[j:, c]))
+  auto apply_reflector = [&](int j, int c0, int cb, S coef) {
+    S part[QR_CB];
 #pragma unroll
-    for (int u = 0; u < QR_CB; ++u) part[u] = 0.0;
+    for (int u = 0; u < QR_CB; ++u) part[u] = s_zero(S());
     for (int64_t i = j + tid; i < m; i += QR_THREADS) {
-      const double vi = (i == j) ? 1.0 : A[i + j * ld];
+      const S vi = (i == j) ? s_real<S>(1.0) : A[i + j * ld];
 #pragma unroll
       for (int u = 0; u < QR_CB; ++u)
-        if (u < cb) part[u] = fma(vi, A[i + (c0 + u) * ld], part[u]);
+        if (u < cb) part[u] = s_cfma(vi, A[i + (c0 + u) * ld], part[u]);
     }
 #pragma unroll
     for (int u = 0; u < QR_CB; ++u) {
-      const double s = warp_sum(part[u]);
+      const S s = ds_warp_sum(part[u]);
       if (lane == 0) red[w * QR_CB + u] = s;
     }
     __syncthreads();
     if (tid < cb) {
-      double s = 0.0;
-      for (int q = 0; q < nw; ++q) s += red[q * QR_CB + tid];
-      wv[tid] = s * tj;
+      S s = s_zero(S());
+      for (int q = 0; q < nw; ++q) s = s_add(s, red[q * QR_CB + tid]);
+      wv[tid] = s_mul(coef, s);
     }
     __syncthreads();
     for (int64_t i = j + tid; i < m; i += QR_THREADS) {
-      const double vi = (i == j) ? 1.0 : A[i + j * ld];
+      const S vi = (i == j) ? s_real<S>(1.0) : A[i + j * ld];
 #pragma unroll
       for (int u = 0; u < QR_CB; ++u)
-        if (u < cb) A[i + (c0 + u) * ld] -= vi * wv[u];
+        if (u < cb) A[i + (c0 + u) * ld] = s_sub(A[i + (c0 + u) * ld], s_mul(vi, wv[u]));
     }
     __syncthreads();
   };
 
   for (int j = 0; j < l; ++j) {
     double ss = 0.0;
-    for (int64_t i = j + 1 + tid; i < m; i += QR_THREADS) {
-      const double v = A[i + j * ld];
-      ss = fma(v, v, ss);
-    }
-    ss = block_sum(ss, red);
-    const double alpha = A[j + j * ld];
+    for (int64_t i = j + 1 + tid; i < m; i += QR_THREADS) ss += s_abs2(A[i + j * ld]);
+    ss = block_sum(ss, rs);
+    const S alpha = A[j + j * ld];
     const double xnorm = sqrt(ss);
-    double tj = 0.0, scal = 1.0, beta = alpha;
-    if (xnorm != 0.0) {
-      beta = -copysign(hypot(alpha, xnorm), alpha);
-      tj = (beta - alpha) / beta;
-      scal = 1.0 / (alpha - beta);
+    S tj = s_zero(S()), scal = s_real<S>(1.0), beta = alpha;
+    const double alphi = IsC<S>::value ? reinterpret_cast<const double*>(&alpha)[1] : 0.0;
+    const double alphr = reinterpret_cast<const double*>(&alpha)[0];
+    if (xnorm != 0.0 || alphi != 0.0) {  // LAPACK larfg
+      const double b = -copysign(sqrt(alphr * alphr + alphi * alphi + ss), alphr);
+      beta = s_real<S>(b);
+      S t;
+      if constexpr (IsC<S>::value) t = S{(b - alphr) / b, -alphi / b};
+      else t = (b - alphr) / b;
+      tj = t;
+      scal = s_inv(s_sub(alpha, beta));
     }
-    if (tj != 0.0)
-      for (int64_t i = j + 1 + tid; i < m; i += QR_THREADS) A[i + j * ld] *= scal;
+    if (!s_iszero(tj))
+      for (int64_t i = j + 1 + tid; i < m; i += QR_THREADS) A[i + j * ld] = s_mul(A[i + j * ld], scal);
     __syncthreads();
     if (tid == 0) {
       A[j + j * ld] = beta;
       tau[j] = tj;
     }
     __syncthreads();
-    if (tj != 0.0)
-      for (int c0 = j + 1; c0 < l; c0 += QR_CB) apply_reflector(j, c0, min(QR_CB, l - c0), tj);
+    if (!s_iszero(tj))
+      for (int c0 = j + 1; c0 < l; c0 += QR_CB)
+        apply_reflector(j, c0, min(QR_CB, l - c0), s_conj(tj));
   }
   if (jb.R) {
     for (int e = tid; e < l * l; e += QR_THREADS) {
       const int r = e % l, c = e / l;
-      jb.R[e] = (r <= c) ? A[r + c * ld] : 0.0;
+      jb.R[e] = (r <= c) ? A[r + c * ld] : s_zero(S());
     }
   }
   __syncthreads();
-  // form Q explicitly (dorg2r): right to left
+  // form Q explicitly (ung2r): right to left
   for (int j = l - 1; j >= 0; --j) {
-    const double tj = tau[j];
-    if (j < l - 1 && tj != 0.0)
+    const S tj = tau[j];
+    if (j < l - 1 && !s_iszero(tj))
       for (int c0 = j + 1; c0 < l; c0 += QR_CB) apply_reflector(j, c0, min(QR_CB, l - c0), tj);
     for (int64_t i = tid; i < m; i += QR_THREADS) {
-      double v;
-      if (i < j) v = 0.0;
-      else if (i == j) v = 1.0 - tj;
-      else v = -tj * A[i + j * ld];
+      S v;
+      if (i < j) v = s_zero(S());
+      else if (i == j) v = s_sub(s_real<S>(1.0), tj);
+      else v = s_neg(s_mul(tj, A[i + j * ld]));
       A[i + j * ld] = v;
     }
     __syncthreads();
   }
 }
 
-void launch_householder_qr(Ctx* c, const QrJob* d_jobs, int njobs, int l) {
+template <class S>
+void launch_householder_qr_t(Ctx* c, const QrJobT<S>* d_jobs, int njobs, int l) {
   if (njobs == 0) return;
-  const size_t smem = sizeof(double) * (l + (QR_THREADS / 32) * QR_CB + QR_CB);
+  const size_t smem = sizeof(S) * (l + (QR_THREADS / 32) * QR_CB + QR_CB) +
+                      sizeof(double) * (QR_THREADS / 32);
   ProfScope ps_(c, K_SETUP);
-  householder_qr_kernel<<<njobs, QR_THREADS, smem, c->stream>>>(d_jobs, l);
+  householder_qr_kernel<S><<<njobs, QR_THREADS, smem, c->stream>>>(d_jobs, l);
   LRS_LAUNCHED(c);
 }
 
 // ---------------------------------------------------------------------------------------
 // One-sided (Hestenes) Jacobi SVD of an l x l matrix R: R V = U diag(sigma).
 // Round-robin pair ordering, one warp per pair, converged when a sweep makes no
-// rotation with |c| > 1e-15 sqrt(a b).  Results sorted by sigma descending.
+// rotation with |c| > 1e-15 sqrt(a b).  Complex: column q is first turned by the phase
+// of c = p^H q (a unitary diagonal factor, accumulated in V) so the rotation is real.
+// Results sorted by sigma descending.
 // ---------------------------------------------------------------------------------------
 constexpr int SVD_THREADS = 256;
 constexpr int SVD_MAXL = 96;
 
-__global__ void __launch_bounds__(SVD_THREADS) jacobi_svd_kernel(const SvdJob* jobs, int l) {
-  extern __shared__ double ssm[];
+template <class S>
+__global__ void __launch_bounds__(SVD_THREADS) jacobi_svd_kernel(const SvdJobT<S>* jobs, int l) {
+  extern __shared__ __align__(16) unsigned char ssm_raw[];
   const int L2 = (l + 1) & ~1;  // even number of slots (dummy column if l is odd)
-  double* R = ssm;              // L2 x L2 column-major (padded rows/cols zero)
-  double* V = R + L2 * L2;
-  double* sg = V + L2 * L2;     // L2
-  int* pos = reinterpret_cast<int*>(sg + L2);  // L2 tournament slots
+  S* R = reinterpret_cast<S*>(ssm_raw);  // L2 x L2 column-major (padded rows/cols zero)
+  S* V = R + L2 * L2;
+  double* sg = reinterpret_cast<double*>(V + L2 * L2);  // L2
+  int* pos = reinterpret_cast<int*>(sg + L2);
   int* order = pos + L2;
   int* rotated = order + L2;
-  const SvdJob jb = jobs[blockIdx.x];
+  const SvdJobT<S> jb = jobs[blockIdx.x];
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, nw = SVD_THREADS / 32;
   for (int e = tid; e < L2 * L2; e += SVD_THREADS) {
     const int r = e % L2, c = e / L2;
-    R[e] = (r < l && c < l) ? jb.R[r + c * l] : 0.0;
-    V[e] = (r == c) ? 1.0 : 0.0;
+    R[e] = (r < l && c < l) ? jb.R[r + c * l] : s_zero(S());
+    V[e] = (r == c) ? s_real<S>(1.0) : s_zero(S());
   }
   for (int e = tid; e < L2; e += SVD_THREADS) pos[e] = e;
   __syncthreads();
@@ -149,34 +164,36 @@ __global__ void __launch_bounds__(SVD_THREADS) jacobi_svd_kernel(const SvdJob* j
       for (int pr = w; pr < npairs; pr += nw) {
         int p = pos[pr], q = pos[L2 - 1 - pr];
         if (p > q) { const int t = p; p = q; q = t; }
-        double a = 0, b = 0, cc = 0;
+        double a = 0, b = 0;
+        S cc = s_zero(S());
         for (int r = lane; r < L2; r += 32) {
-          const double x = R[r + p * L2], y = R[r + q * L2];
-          a = fma(x, x, a);
-          b = fma(y, y, b);
-          cc = fma(x, y, cc);
+          const S x = R[r + p * L2], y = R[r + q * L2];
+          a += s_abs2(x);
+          b += s_abs2(y);
+          cc = s_cfma(x, y, cc);
         }
         a = warp_sum(a);
         b = warp_sum(b);
-        cc = warp_sum(cc);
-        if (fabs(cc) > 1e-15 * sqrt(a * b) && cc != 0.0) {
-          const double zeta = (b - a) / (2.0 * cc);
+        cc = ds_warp_sum(cc);
+        const double cabs = s_abs(cc);
+        if (cabs > 1e-15 * sqrt(a * b) && cabs != 0.0) {
+          const double zeta = (b - a) / (2.0 * cabs);
           const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
           const double cs = 1.0 / sqrt(1.0 + t * t), sn = cs * t;
+          const S ph = s_scale(s_conj(cc), 1.0 / cabs);  // q~ = ph q, p^H q~ = |c|
           for (int r = lane; r < L2; r += 32) {
-            const double x = R[r + p * L2], y = R[r + q * L2];
-            R[r + p * L2] = cs * x - sn * y;
-            R[r + q * L2] = sn * x + cs * y;
-            const double vx = V[r + p * L2], vy = V[r + q * L2];
-            V[r + p * L2] = cs * vx - sn * vy;
-            V[r + q * L2] = sn * vx + cs * vy;
+            const S x = R[r + p * L2], y = s_mul(ph, R[r + q * L2]);
+            R[r + p * L2] = s_sub(s_scale(x, cs), s_scale(y, sn));
+            R[r + q * L2] = s_add(s_scale(x, sn), s_scale(y, cs));
+            const S vx = V[r + p * L2], vy = s_mul(ph, V[r + q * L2]);
+            V[r + p * L2] = s_sub(s_scale(vx, cs), s_scale(vy, sn));
+            V[r + q * L2] = s_add(s_scale(vx, sn), s_scale(vy, cs));
           }
           if (lane == 0) *rotated = 1;
         }
       }
       __syncthreads();
-      // rotate tournament positions (slot 0 fixed)
-      if (tid == 0) {
+      if (tid == 0) {  // rotate tournament positions (slot 0 fixed)
         const int last = pos[L2 - 1];
         for (int e = L2 - 1; e > 1; --e) pos[e] = pos[e - 1];
         pos[1] = last;
@@ -187,10 +204,9 @@ __global__ void __launch_bounds__(SVD_THREADS) jacobi_svd_kernel(const SvdJob* j
     __syncthreads();
     if (!any) break;
   }
-  // singular values and ordering
   for (int c = w; c < L2; c += nw) {
     double s = 0.0;
-    for (int r = lane; r < L2; r += 32) s = fma(R[r + c * L2], R[r + c * L2], s);
+    for (int r = lane; r < L2; r += 32) s += s_abs2(R[r + c * L2]);
     s = warp_sum(s);
     if (lane == 0) sg[c] = sqrt(s);
   }
@@ -212,33 +228,39 @@ __global__ void __launch_bounds__(SVD_THREADS) jacobi_svd_kernel(const SvdJob* j
     const int src = order[c];
     const double s = sg[src];
     jb.V[r + c * l] = V[r + src * L2];
-    jb.U[r + c * l] = s > 0.0 ? R[r + src * L2] / s : (r == c ? 1.0 : 0.0);
+    jb.U[r + c * l] = s > 0.0 ? s_scale(R[r + src * L2], 1.0 / s)
+                              : (r == c ? s_real<S>(1.0) : s_zero(S()));
   }
   for (int c = tid; c < l; c += SVD_THREADS) jb.sigma[c] = sg[order[c]];
 }
 
-void launch_jacobi_svd(Ctx* c, const SvdJob* d_jobs, int njobs, int l) {
+template <class S>
+void launch_jacobi_svd_t(Ctx* c, const SvdJobT<S>* d_jobs, int njobs, int l) {
   if (njobs == 0) return;
   if (l > SVD_MAXL) throw LrsError(LRS_ERR_PARAMETER, "n_svd + oversample > 96 not supported");
   const int L2 = (l + 1) & ~1;
-  const size_t smem = sizeof(double) * (2 * L2 * L2 + L2) + sizeof(int) * (2 * L2 + 1);
-  static bool attr = false;
-  if (!attr) {
-    LRS_CUDA(cudaFuncSetAttribute(jacobi_svd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)(sizeof(double) * (2 * 96 * 96 + 96) + sizeof(int) * 200)));
-    attr = true;
+  const size_t smem = sizeof(S) * 2 * L2 * L2 + sizeof(double) * L2 + sizeof(int) * (2 * L2 + 1);
+  if (smem > 227 * 1024)  // complex: l <= 84
+    throw LrsError(LRS_ERR_PARAMETER, "n_svd + oversample too large for the shared-memory SVD");
+  static size_t attr = 0;
+  if (smem > attr) {
+    LRS_CUDA(cudaFuncSetAttribute(jacobi_svd_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem));
+    attr = smem;
   }
   ProfScope ps_(c, K_SETUP);
-  jacobi_svd_kernel<<<njobs, SVD_THREADS, smem, c->stream>>>(d_jobs, l);
+  jacobi_svd_kernel<S><<<njobs, SVD_THREADS, smem, c->stream>>>(d_jobs, l);
   LRS_LAUNCHED(c);
 }
 
 // ---------------------------------------------------------------------------------------
-// C (m x n) = op(A) (m x k) * B (k x n); k, n <= 128 (B staged in shared memory).
+// C (m x n) = A (m x k) * B (k x n); k x n <= 96 x 64 (B staged in shared memory)
 // ---------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) small_gemm_kernel(const GemmJob* jobs) {
-  extern __shared__ double gsm[];
-  const GemmJob jb = jobs[blockIdx.y];
+template <class S>
+__global__ void __launch_bounds__(256) small_gemm_kernel(const GemmJobT<S>* jobs) {
+  extern __shared__ __align__(16) unsigned char gsm_raw[];
+  S* gsm = reinterpret_cast<S*>(gsm_raw);
+  const GemmJobT<S> jb = jobs[blockIdx.y];
   for (int e = threadIdx.x; e < jb.k * jb.n; e += blockDim.x) {
     const int r = e % jb.k, c = e / jb.k;
     gsm[e] = jb.B[r + c * jb.ldb];
@@ -247,27 +269,26 @@ __global__ void __launch_bounds__(256) small_gemm_kernel(const GemmJob* jobs) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= jb.m) return;
   for (int c = 0; c < jb.n; ++c) {
-    double s = 0.0;
-    for (int kk = 0; kk < jb.k; ++kk) {
-      const double a = jb.transA ? jb.A[kk + i * jb.lda] : jb.A[i + kk * jb.lda];
-      s = fma(a, gsm[kk + c * jb.k], s);
-    }
-    jb.C[i + c * jb.ldc] = s;
+    S s = s_zero(S());
+    for (int kk = 0; kk < jb.k; ++kk) s = s_fma(jb.A[i + kk * jb.lda], gsm[kk + c * jb.k], s);
+    jb.C[i + c * jb.ldc] = jb.conjC ? s_conj(s) : s;
   }
 }
 
-void launch_small_gemm(Ctx* c, const GemmJob* d_jobs, int njobs, int64_t max_m, int max_n) {
+template <class S>
+void launch_small_gemm_t(Ctx* c, const GemmJobT<S>* d_jobs, int njobs, int64_t max_m, int max_n) {
   if (njobs == 0 || max_m == 0) return;
   (void)max_n;
+  const size_t smem = sizeof(S) * 96 * 64;
   static bool attr = false;
   if (!attr) {
-    LRS_CUDA(cudaFuncSetAttribute(small_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)(sizeof(double) * 128 * 128)));
+    LRS_CUDA(cudaFuncSetAttribute(small_gemm_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem));
     attr = true;
   }
-  dim3 grid((unsigned)((max_m + 255) / 256), (unsigned)njobs);
   ProfScope ps_(c, K_SETUP);
-  small_gemm_kernel<<<grid, 256, sizeof(double) * 128 * 128, c->stream>>>(d_jobs);
+  dim3 grid((unsigned)((max_m + 255) / 256), (unsigned)njobs);
+  small_gemm_kernel<S><<<grid, 256, smem, c->stream>>>(d_jobs);
   LRS_LAUNCHED(c);
 }
 
@@ -278,9 +299,10 @@ void launch_small_gemm(Ctx* c, const GemmJob* d_jobs, int njobs, int64_t max_m, 
 // ---------------------------------------------------------------------------------------
 constexpr int IF_THREADS = 256;
 
-// Gauss-Jordan inverse with partial pivoting of an r x r matrix in shared memory.
-// M is r x 2r column-major [A | I]; returns 0 on an exact zero pivot.
-__device__ int gj_inverse(double* M, int r, int* piv_row) {
+// Gauss-Jordan inverse with partial pivoting (largest |a|) of an r x r matrix in shared
+// memory.  M is r x 2r column-major [A | I]; returns 0 on an exact zero pivot.
+template <class S>
+__device__ int gj_inverse(S* M, int r, int* piv_row) {
   const int tid = threadIdx.x;
   const int ld = r;
   __shared__ int s_ok;
@@ -289,9 +311,9 @@ __device__ int gj_inverse(double* M, int r, int* piv_row) {
   for (int j = 0; j < r; ++j) {
     if (tid == 0) {
       int best = j;
-      double bv = fabs(M[j + j * ld]);
+      double bv = s_abs(M[j + j * ld]);
       for (int i = j + 1; i < r; ++i)
-        if (fabs(M[i + j * ld]) > bv) { bv = fabs(M[i + j * ld]); best = i; }
+        if (s_abs(M[i + j * ld]) > bv) { bv = s_abs(M[i + j * ld]); best = i; }
       *piv_row = best;
       if (bv == 0.0) s_ok = 0;
     }
@@ -300,33 +322,34 @@ __device__ int gj_inverse(double* M, int r, int* piv_row) {
     const int pr = *piv_row;
     if (pr != j)
       for (int c = tid; c < 2 * r; c += blockDim.x) {
-        const double t = M[j + c * ld];
+        const S t = M[j + c * ld];
         M[j + c * ld] = M[pr + c * ld];
         M[pr + c * ld] = t;
       }
     __syncthreads();
-    const double d = 1.0 / M[j + j * ld];
+    const S d = s_inv(M[j + j * ld]);
     __syncthreads();
-    for (int c = tid; c < 2 * r; c += blockDim.x) M[j + c * ld] *= d;
+    for (int c = tid; c < 2 * r; c += blockDim.x) M[j + c * ld] = s_mul(M[j + c * ld], d);
     __syncthreads();
     for (int e = tid; e < r * 2 * r; e += blockDim.x) {
       const int i = e % r, c = e / r;
-      if (i != j && c != j) M[i + c * ld] -= M[i + j * ld] * M[j + c * ld];
+      if (i != j && c != j) M[i + c * ld] = s_sub(M[i + c * ld], s_mul(M[i + j * ld], M[j + c * ld]));
     }
     __syncthreads();
     for (int i = tid; i < r; i += blockDim.x)
-      if (i != j) M[i + j * ld] = 0.0;
+      if (i != j) M[i + j * ld] = s_zero(S());
     __syncthreads();
   }
   return 1;
 }
 
-__device__ double norm1(const double* A, int r, int ld, double* red) {
+template <class S>
+__device__ double norm1(const S* A, int r, int ld, double* red) {
   // max column sum of |A|, columns handled by threads, reduced by thread 0
   const int tid = threadIdx.x;
   for (int c = tid; c < r; c += blockDim.x) {
     double s = 0.0;
-    for (int i = 0; i < r; ++i) s += fabs(A[i + c * ld]);
+    for (int i = 0; i < r; ++i) s += s_abs(A[i + c * ld]);
     red[c] = s;
   }
   __syncthreads();
@@ -336,43 +359,41 @@ __device__ double norm1(const double* A, int r, int ld, double* red) {
   return mx;
 }
 
-__global__ void __launch_bounds__(IF_THREADS) iface_setup_kernel(const IfaceSetupJob* jobs, int r,
-                                                                 int64_t k) {
-  extern __shared__ double fsm[];
-  double* Ks = fsm;            // r x r
-  double* Es = Ks + r * r;     // r x r
-  double* M = Es + r * r;      // r x 2r
-  double* red = M + 2 * r * r; // r
+template <class S>
+__global__ void __launch_bounds__(IF_THREADS) iface_setup_kernel(const IfaceSetupJobT<S>* jobs,
+                                                                 int r, int64_t k) {
+  extern __shared__ __align__(16) unsigned char fsm_raw[];
+  S* Ks = reinterpret_cast<S*>(fsm_raw);  // r x r
+  S* Es = Ks + r * r;                      // r x r
+  S* M = Es + r * r;                       // r x 2r
+  double* red = reinterpret_cast<double*>(M + 2 * r * r);  // r
   __shared__ int piv;
-  const IfaceSetupJob jb = jobs[blockIdx.x];
+  const IfaceSetupJobT<S> jb = jobs[blockIdx.x];
   const int tid = threadIdx.x;
   // K[a][c] = sum_row vtW[row, a] uTb[row, c];  E[a][c] = sum_row vtT[row, a] uWt[row, c]
   for (int e = tid; e < 2 * r * r; e += IF_THREADS) {
     const int which = e / (r * r), ac = e % (r * r);
     const int a = ac % r, c = ac / r;
-    const double* vt = which ? jb.vtT : jb.vtW;
-    const double* u = which ? jb.uWt : jb.uTb;
+    const S* vt = which ? jb.vtT : jb.vtW;
+    const S* u = which ? jb.uWt : jb.uTb;
     const int64_t ldu = which ? jb.ld_uW : jb.ld_uT;
-    double s = 0.0;
-    for (int64_t row = 0; row < k; ++row) s = fma(vt[row + a * k], u[row + c * ldu], s);
+    S s = s_zero(S());
+    for (int64_t row = 0; row < k; ++row) s = s_fma(vt[row + a * k], u[row + c * ldu], s);
     (which ? Es : Ks)[a + c * r] = s;
   }
   __syncthreads();
-  bool degenerate = true;
-  {
-    bool anyT = false, anyW = false;
-    for (int a = 0; a < r; ++a) {
-      anyT |= jb.sT[a] != 0.0;
-      anyW |= jb.sW[a] != 0.0;
-    }
-    degenerate = !(anyT && anyW);
+  bool anyT = false, anyW = false;
+  for (int a = 0; a < r; ++a) {
+    anyT |= jb.sT[a] != 0.0;
+    anyW |= jb.sW[a] != 0.0;
   }
+  const bool degenerate = !(anyT && anyW);
   for (int e = tid; e < r * r; e += IF_THREADS) {
     jb.K[e] = Ks[e];
     jb.E[e] = Es[e];
   }
   if (degenerate) {
-    for (int e = tid; e < r * r; e += IF_THREADS) jb.Hinv[e] = 0.0;
+    for (int e = tid; e < r * r; e += IF_THREADS) jb.Hinv[e] = s_zero(S());
     if (tid == 0) {
       jb.cond[0] = jb.cond[1] = 1.0;
       *jb.degenerate = 1;
@@ -382,29 +403,29 @@ __global__ void __launch_bounds__(IF_THREADS) iface_setup_kernel(const IfaceSetu
   // G = K^-1
   for (int e = tid; e < 2 * r * r; e += IF_THREADS) {
     const int i = e % r, c = e / r;
-    M[e] = (c < r) ? Ks[i + c * r] : (i == c - r ? 1.0 : 0.0);
+    M[e] = (c < r) ? Ks[i + c * r] : (i == c - r ? s_real<S>(1.0) : s_zero(S()));
   }
   __syncthreads();
   const double nK = norm1(Ks, r, r, red);
   const int okK = gj_inverse(M, r, &piv);
   double condK = INFINITY;
   if (okK) condK = nK * norm1(M + r * r, r, r, red);
-  // H = G - S_T E S_W   (store H in Ks, G no longer needed afterwards)
+  // H = G - S_T E S_W   (stored in Ks; G is no longer needed afterwards)
   for (int e = tid; e < r * r; e += IF_THREADS) {
     const int a = e % r, c = e / r;
-    Ks[e] = okK ? M[r * r + e] - jb.sT[a] * Es[e] * jb.sW[c] : 0.0;
+    Ks[e] = okK ? s_sub(M[r * r + e], s_scale(Es[e], jb.sT[a] * jb.sW[c])) : s_zero(S());
   }
   __syncthreads();
   for (int e = tid; e < 2 * r * r; e += IF_THREADS) {
     const int i = e % r, c = e / r;
-    M[e] = (c < r) ? Ks[i + c * r] : (i == c - r ? 1.0 : 0.0);
+    M[e] = (c < r) ? Ks[i + c * r] : (i == c - r ? s_real<S>(1.0) : s_zero(S()));
   }
   __syncthreads();
   const double nH = norm1(Ks, r, r, red);
   const int okH = okK ? gj_inverse(M, r, &piv) : 0;
   double condH = INFINITY;
   if (okH) condH = nH * norm1(M + r * r, r, r, red);
-  for (int e = tid; e < r * r; e += IF_THREADS) jb.Hinv[e] = okH ? M[r * r + e] : 0.0;
+  for (int e = tid; e < r * r; e += IF_THREADS) jb.Hinv[e] = okH ? M[r * r + e] : s_zero(S());
   if (tid == 0) {
     jb.cond[0] = isfinite(condK) ? condK : INFINITY;
     jb.cond[1] = isfinite(condH) ? condH : INFINITY;
@@ -412,17 +433,20 @@ __global__ void __launch_bounds__(IF_THREADS) iface_setup_kernel(const IfaceSetu
   }
 }
 
-void launch_iface_setup(Ctx* c, const IfaceSetupJob* d_jobs, int njobs, int r, int64_t k) {
+template <class S>
+void launch_iface_setup_t(Ctx* c, const IfaceSetupJobT<S>* d_jobs, int njobs, int r, int64_t k) {
   if (njobs == 0) return;
-  const size_t smem = sizeof(double) * (4 * r * r + r);
-  static bool attr = false;
-  if (!attr) {
-    LRS_CUDA(cudaFuncSetAttribute(iface_setup_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)(sizeof(double) * (4 * 64 * 64 + 64))));
-    attr = true;
+  const size_t smem = sizeof(S) * 4 * r * r + sizeof(double) * r;
+  if (smem > 227 * 1024)  // real: r <= 85, complex: r <= 60
+    throw LrsError(LRS_ERR_PARAMETER, "n_svd too large for the shared-memory interface setup");
+  static size_t attr = 0;
+  if (smem > attr) {
+    LRS_CUDA(cudaFuncSetAttribute(iface_setup_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem));
+    attr = smem;
   }
   ProfScope ps_(c, K_SETUP);
-  iface_setup_kernel<<<njobs, IF_THREADS, smem, c->stream>>>(d_jobs, r, k);
+  iface_setup_kernel<S><<<njobs, IF_THREADS, smem, c->stream>>>(d_jobs, r, k);
   LRS_LAUNCHED(c);
 }
 
@@ -443,5 +467,14 @@ void launch_sigma_trunc(Ctx* c, const SigmaJob* d_jobs, int njobs, int r, int* d
   sigma_trunc_kernel<<<njobs, 64, 0, c->stream>>>(d_jobs, r, d_flag);
   LRS_LAUNCHED(c);
 }
+
+#define LRS_INST(S)                                                                          \
+  template void launch_householder_qr_t<S>(Ctx*, const QrJobT<S>*, int, int);                \
+  template void launch_jacobi_svd_t<S>(Ctx*, const SvdJobT<S>*, int, int);                   \
+  template void launch_small_gemm_t<S>(Ctx*, const GemmJobT<S>*, int, int64_t, int);         \
+  template void launch_iface_setup_t<S>(Ctx*, const IfaceSetupJobT<S>*, int, int, int64_t);
+LRS_INST(double)
+LRS_INST(zc)
+#undef LRS_INST
 
 }  // namespace lrs

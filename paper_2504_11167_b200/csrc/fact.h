@@ -17,6 +17,9 @@ struct Fact {
   Ctx* ctx = nullptr;
   Mat* mat = nullptr;
   int variant = LRS_VARIANT_T;
+  int32_t scalar = LRS_F64;    // LRS_F64 | LRS_C128
+  int sw = 1;                  // doubles per scalar: every S-typed buffer below is a
+                               // DevBuf<double> of sw * (element count)
   int P = 1;                   // local partitions
   int Pg = 1, p0 = 0;          // global partitions, global index of local partition 0
   int64_t row_lo = 0, row_hi = 0;
@@ -43,7 +46,7 @@ struct Fact {
   DevBuf<double> Kd, Ed, Hinv, cond;
   DevBuf<int> degen;
   DevBuf<double> scT, scW;     // per global partition, r x MAX_RHS
-  DevBuf<IfaceApplyJob> iface_jobs;
+  DevBuf<unsigned char> iface_jobs;  // IfaceApplyJobT<S>[ni]
   DevBuf<double> iface_work, iface_msg;
   int job_left = -1, job_right = -1;  // jobs of the cross-GPU interfaces (or -1)
   // deterministic reductions (partition-aligned chunks, partition-ordered sums)
@@ -93,11 +96,12 @@ void shard_plan(int64_t P, int size, int rank, int64_t* p_lo, int64_t* p_hi);
 
 Fact* factorize(Ctx* c, Mat* m, const lrs_solver_cfg& cfg, const lrs_comm* comm);
 // D-stage solve (local partitions, or local partition p_only >= 0), in place on x.
-void dstage(Fact* f, double* x, int64_t ld, int nrhs, bool adjoint, int p_only);
+// Vectors are double* (LRS_F64) or interleaved complex128 (LRS_C128) per f->scalar.
+void dstage(Fact* f, void* x, int64_t ld, int nrhs, bool adjoint, int p_only);
 // M^-1 applied to in -> out on the local rows, variant T or Block Jacobi.
-void apply_precond(Fact* f, const double* in, int64_t ldi, double* out, int64_t ldo, int nrhs,
+void apply_precond(Fact* f, const void* in, int64_t ldi, void* out, int64_t ldo, int nrhs,
                    bool block_jacobi);
-void solve(Fact* f, Mat* a, const double* b, int64_t ldb, double* x, int64_t ldx, int nrhs,
+void solve(Fact* f, Mat* a, const void* b, int64_t ldb, void* x, int64_t ldx, int nrhs,
            const lrs_iter_cfg& cfg, lrs_report* rep);
 
 }  // namespace lrs

@@ -1,8 +1,9 @@
 // Krylov vector kernels (K12 of SURVEY.md 2.3) for bicgstab
-// and GMRES(m): column-batched, per-column scalars, and
-// deterministic reductions -- every dot product is summed per partition-aligned
-// chunk in a fixed tree, then over chunks in order, so the
-// result does not depend on launch geometry or (later) on the GPU count.
+// and GMRES(m), real and complex: column-batched, per-column scalars,
+// Hermitian dot products, and deterministic reductions -- every dot product is summed
+// per partition-aligned chunk in a fixed tree, per partition over its chunks in order,
+// then over the GLOBAL partitions in order, so the result does not
+// depend on launch geometry or on the number of GPUs.
 #include "common.cuh"
 #include "kernels.h"
 #include "lrs_internal.h"
@@ -11,33 +12,36 @@ namespace lrs {
 
 constexpr int KV_THREADS = 256;
 
-template <int NR>
+__device__ __forceinline__ double kv_warp_sum(double v) { return warp_sum(v); }
+__device__ __forceinline__ zc kv_warp_sum(zc v) { return warp_sum_z(v); }
+
+template <int NR, class S>
 __global__ void __launch_bounds__(KV_THREADS) multidot_partial_kernel(
-    const int64_t* __restrict__ cstart, const double* __restrict__ X, int64_t ldx, int64_t strideX,
-    int nvec, const double* __restrict__ Y, int64_t ldy, int nrhs, double* __restrict__ partial) {
-  __shared__ double red[KV_THREADS / 32][NR];
+    const int64_t* __restrict__ cstart, const S* __restrict__ X, int64_t ldx, int64_t strideX,
+    int nvec, const S* __restrict__ Y, int64_t ldy, int nrhs, S* __restrict__ partial) {
+  __shared__ S red[KV_THREADS / 32][NR];
   const int c = blockIdx.x;
   const int64_t r0 = cstart[c], r1 = cstart[c + 1];
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   for (int q = 0; q < nvec; ++q) {
-    const double* Xq = X + q * strideX;
-    double acc[NR];
+    const S* Xq = X + q * strideX;
+    S acc[NR];
 #pragma unroll
-    for (int j = 0; j < NR; ++j) acc[j] = 0.0;
+    for (int j = 0; j < NR; ++j) acc[j] = s_zero(S());
     for (int64_t row = r0 + tid; row < r1; row += KV_THREADS) {
 #pragma unroll
       for (int j = 0; j < NR; ++j)
-        if (j < nrhs) acc[j] = fma(Xq[row + j * ldx], Y[row + j * ldy], acc[j]);
+        if (j < nrhs) acc[j] = s_cfma(Xq[row + j * ldx], Y[row + j * ldy], acc[j]);
     }
 #pragma unroll
     for (int j = 0; j < NR; ++j) {
-      const double s = warp_sum(acc[j]);
+      const S s = kv_warp_sum(acc[j]);
       if (lane == 0) red[w][j] = s;
     }
     __syncthreads();
     if (tid < nrhs) {
-      double s = 0.0;
-      for (int ww = 0; ww < KV_THREADS / 32; ++ww) s += red[ww][tid];
+      S s = s_zero(S());
+      for (int ww = 0; ww < KV_THREADS / 32; ++ww) s = s_add(s, red[ww][tid]);
       partial[((int64_t)c * nvec + q) * nrhs + tid] = s;
     }
     __syncthreads();
@@ -45,6 +49,7 @@ __global__ void __launch_bounds__(KV_THREADS) multidot_partial_kernel(
 }
 
 // persum[p][o] = sum of the chunk partials of local partition p, in chunk order
+// (o indexes doubles: a complex output is two independent sums)
 __global__ void multidot_partition_kernel(const int* __restrict__ part_first, int Pl, int nout,
                                           const double* __restrict__ partial,
                                           double* __restrict__ persum) {
@@ -67,21 +72,23 @@ __global__ void partition_total_kernel(const double* __restrict__ blocks,
   out[o] = s;
 }
 
-void launch_multidot_partition(Ctx* c, const Chunks& ch, const double* X, int64_t ldx,
-                               int64_t strideX, int nvec, const double* Y, int64_t ldy, int nrhs,
-                               double* partial, double* persum) {
+template <class S>
+void launch_multidot_partition_t(Ctx* c, const Chunks& ch, const S* X, int64_t ldx,
+                                 int64_t strideX, int nvec, const S* Y, int64_t ldy, int nrhs,
+                                 S* partial, S* persum) {
   if (nvec == 0 || nrhs == 0) return;
   ProfScope ps_(c, K_KRYLOV);
   if (nrhs == 1)
-    multidot_partial_kernel<1><<<ch.nchunks, KV_THREADS, 0, c->stream>>>(
+    multidot_partial_kernel<1, S><<<ch.nchunks, KV_THREADS, 0, c->stream>>>(
         ch.start, X, ldx, strideX, nvec, Y, ldy, nrhs, partial);
   else
-    multidot_partial_kernel<MAX_RHS><<<ch.nchunks, KV_THREADS, 0, c->stream>>>(
+    multidot_partial_kernel<MAX_RHS, S><<<ch.nchunks, KV_THREADS, 0, c->stream>>>(
         ch.start, X, ldx, strideX, nvec, Y, ldy, nrhs, partial);
   LRS_LAUNCHED(c);
-  const int nout = nvec * nrhs;
+  const int nout = nvec * nrhs * (int)(sizeof(S) / sizeof(double));
   multidot_partition_kernel<<<dim3((nout + 127) / 128, ch.Pl), 128, 0, c->stream>>>(
-      ch.part_first, ch.Pl, nout, partial, persum);
+      ch.part_first, ch.Pl, nout, reinterpret_cast<const double*>(partial),
+      reinterpret_cast<double*>(persum));
   LRS_LAUNCHED(c);
 }
 
@@ -101,72 +108,80 @@ void launch_partition_total(Ctx* c, const double* blocks, const int* counts, int
 //  3: W = X + a Y              (half-step candidate x + alpha phat)
 //  4: W = a Y                  (scale: GMRES basis normalisation)
 //  5: W = Y                    (copy)
-__global__ void __launch_bounds__(KV_THREADS) axpby_kernel(int64_t n, int nrhs, int op, ColScal a,
-                                                           ColScal b, ColScal act, double* X,
-                                                           int64_t ldx, const double* Y,
-                                                           int64_t ldy, const double* Z,
-                                                           int64_t ldz, double* W, int64_t ldw) {
+template <class S>
+__global__ void __launch_bounds__(KV_THREADS) axpby_kernel(int64_t n, int nrhs, int op,
+                                                           ColScalT<S> a, ColScalT<S> b,
+                                                           ColScal act, S* X, int64_t ldx,
+                                                           const S* Y, int64_t ldy, const S* Z,
+                                                           int64_t ldz, S* W, int64_t ldw) {
   const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (row >= n) return;
   for (int j = 0; j < nrhs; ++j) {
     if (act.v[j] == 0.0) continue;
-    const double aj = a.v[j], bj = b.v[j];
+    const S aj = a.v[j], bj = b.v[j];
     switch (op) {
       case 0: {
-        double* xp = X + row + j * ldx;
-        *xp = Y[row + j * ldy] + aj * (*xp - bj * Z[row + j * ldz]);
+        S* xp = X + row + j * ldx;
+        *xp = s_add(Y[row + j * ldy], s_mul(aj, s_sub(*xp, s_mul(bj, Z[row + j * ldz]))));
       } break;
-      case 1: W[row + j * ldw] = Y[row + j * ldy] - aj * Z[row + j * ldz]; break;
+      case 1: W[row + j * ldw] = s_sub(Y[row + j * ldy], s_mul(aj, Z[row + j * ldz])); break;
       case 2: {
-        double* xp = X + row + j * ldx;
-        *xp = *xp + aj * Y[row + j * ldy] + bj * Z[row + j * ldz];
+        S* xp = X + row + j * ldx;
+        *xp = s_add(s_add(*xp, s_mul(aj, Y[row + j * ldy])), s_mul(bj, Z[row + j * ldz]));
       } break;
-      case 3: W[row + j * ldw] = X[row + j * ldx] + aj * Y[row + j * ldy]; break;
-      case 4: W[row + j * ldw] = aj * Y[row + j * ldy]; break;
+      case 3: W[row + j * ldw] = s_add(X[row + j * ldx], s_mul(aj, Y[row + j * ldy])); break;
+      case 4: W[row + j * ldw] = s_mul(aj, Y[row + j * ldy]); break;
       default: W[row + j * ldw] = Y[row + j * ldy]; break;
     }
   }
 }
 
-void launch_axpby_cols(Ctx* c, int64_t n, int nrhs, int op, const ColScal& a, const ColScal& b,
-                       const ColScal& act, double* X, int64_t ldx, const double* Y, int64_t ldy,
-                       const double* Z, int64_t ldz, double* W, int64_t ldw) {
+template <class S>
+void launch_axpby_cols_t(Ctx* c, int64_t n, int nrhs, int op, const ColScalT<S>& a,
+                         const ColScalT<S>& b, const ColScal& act, S* X, int64_t ldx, const S* Y,
+                         int64_t ldy, const S* Z, int64_t ldz, S* W, int64_t ldw) {
   if (n == 0 || nrhs == 0) return;
   ProfScope ps_(c, K_KRYLOV);
-  axpby_kernel<<<(unsigned)((n + KV_THREADS - 1) / KV_THREADS), KV_THREADS, 0, c->stream>>>(
+  axpby_kernel<S><<<(unsigned)((n + KV_THREADS - 1) / KV_THREADS), KV_THREADS, 0, c->stream>>>(
       n, nrhs, op, a, b, act, X, ldx, Y, ldy, Z, ldz, W, ldw);
   LRS_LAUNCHED(c);
 }
 
-// x[:, j] += sign * sum_q V_q[:, j] * y[q * nrhs + j]
+template <class S>
 __global__ void __launch_bounds__(KV_THREADS) multi_axpy_kernel(int64_t n, int nrhs,
-                                                                const double* __restrict__ V,
+                                                                const S* __restrict__ V,
                                                                 int64_t ldv, int64_t strideV,
-                                                                int nvec, const double* __restrict__ y,
-                                                                double sign, double* x,
-                                                                int64_t ldx) {
+                                                                int nvec, const S* __restrict__ y,
+                                                                double sign, S* x, int64_t ldx) {
   const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (row >= n) return;
   for (int j = 0; j < nrhs; ++j) {
-    double s = 0.0;
-    for (int q = 0; q < nvec; ++q) s = fma(V[q * strideV + row + j * ldv], y[q * nrhs + j], s);
-    x[row + j * ldx] += sign * s;
+    S s = s_zero(S());
+    for (int q = 0; q < nvec; ++q) s = s_fma(V[q * strideV + row + j * ldv], y[q * nrhs + j], s);
+    x[row + j * ldx] = s_add(x[row + j * ldx], s_scale(s, sign));
   }
 }
 
-void launch_multi_axpy_signed(Ctx* c, int64_t n, int nrhs, const double* V, int64_t ldv,
-                              int64_t strideV, int nvec, const double* y_dev, double sign,
-                              double* x, int64_t ldx) {
+template <class S>
+void launch_multi_axpy_t(Ctx* c, int64_t n, int nrhs, const S* V, int64_t ldv, int64_t strideV,
+                         int nvec, const S* y_dev, double sign, S* x, int64_t ldx) {
   if (n == 0 || nrhs == 0 || nvec == 0) return;
   ProfScope ps_(c, K_KRYLOV);
-  multi_axpy_kernel<<<(unsigned)((n + KV_THREADS - 1) / KV_THREADS), KV_THREADS, 0, c->stream>>>(
-      n, nrhs, V, ldv, strideV, nvec, y_dev, sign, x, ldx);
+  multi_axpy_kernel<S><<<(unsigned)((n + KV_THREADS - 1) / KV_THREADS), KV_THREADS, 0,
+                         c->stream>>>(n, nrhs, V, ldv, strideV, nvec, y_dev, sign, x, ldx);
   LRS_LAUNCHED(c);
 }
 
-void launch_multi_axpy(Ctx* c, int64_t n, int nrhs, const double* V, int64_t ldv, int64_t strideV,
-                       int nvec, const double* y_dev, double* x, int64_t ldx) {
-  launch_multi_axpy_signed(c, n, nrhs, V, ldv, strideV, nvec, y_dev, 1.0, x, ldx);
-}
+#define LRS_INST(S)                                                                             \
+  template void launch_multidot_partition_t<S>(Ctx*, const Chunks&, const S*, int64_t, int64_t, \
+                                               int, const S*, int64_t, int, S*, S*);            \
+  template void launch_axpby_cols_t<S>(Ctx*, int64_t, int, int, const ColScalT<S>&,             \
+                                       const ColScalT<S>&, const ColScal&, S*, int64_t,         \
+                                       const S*, int64_t, const S*, int64_t, S*, int64_t);      \
+  template void launch_multi_axpy_t<S>(Ctx*, int64_t, int, const S*, int64_t, int64_t, int,     \
+                                       const S*, double, S*, int64_t);
+LRS_INST(double)
+LRS_INST(zc)
+#undef LRS_INST
 
 }  // namespace lrs

@@ -1,5 +1,5 @@
 // Interface Woodbury solve (K9) and low-rank recovery (K10) of apply_precond_T
-// (SURVEY.md Appendix A.1/A.3).
+// (SURVEY.md Appendix A.1/A.3), real and complex.
 //
 // Per interface i (partitions i, i+1), from the D-stage output y:
 //   m_W = vW y_{i,b},  m_T = vT y_{i+1,t}                      (the two C1 messages)
@@ -25,38 +25,41 @@ namespace lrs {
 constexpr int IA_THREADS = 256;
 constexpr int IA_ROWS = 256;  // tip rows per partial-dot CTA
 
+__device__ __forceinline__ double warp_sum_s(double v) { return warp_sum(v); }
+__device__ __forceinline__ zc warp_sum_s(zc v) { return warp_sum_z(v); }
+
 // part[((job*2 + which)*nchunk + chunk)] = r x nrhs partial dots of v^T with y over a
 // 256-row slice (which 0: m_W from y_{i,b}, 1: m_T from y_{i+1,t}); only local sides.
-__global__ void __launch_bounds__(IA_THREADS) iface_dots_kernel(const IfaceApplyJob* jobs, int r,
-                                                                int64_t k, const double* y,
-                                                                int64_t ldy, int nrhs,
-                                                                double* part) {
-  __shared__ double red[IA_THREADS / 32][MAX_RHS];
+template <class S>
+__global__ void __launch_bounds__(IA_THREADS) iface_dots_kernel(const IfaceApplyJobT<S>* jobs,
+                                                                int r, int64_t k, const S* y,
+                                                                int64_t ldy, int nrhs, S* part) {
+  __shared__ S red[IA_THREADS / 32][MAX_RHS];
   const int job = blockIdx.y >> 1, which = blockIdx.y & 1, chunk = blockIdx.x;
   const int nchunk = gridDim.x;
-  const IfaceApplyJob jb = jobs[job];
+  const IfaceApplyJobT<S> jb = jobs[job];
   if (which == 0 ? !jb.has_left : !jb.has_right) return;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int64_t row = (int64_t)chunk * IA_ROWS + tid;
   const bool valid = row < k;
-  const double* vt = which ? jb.vtT : jb.vtW;
-  const double* yy = y + (which ? jb.yt_row : jb.yb_row);
-  double yv[MAX_RHS];
+  const S* vt = which ? jb.vtT : jb.vtW;
+  const S* yy = y + (which ? jb.yt_row : jb.yb_row);
+  S yv[MAX_RHS];
 #pragma unroll
-  for (int j = 0; j < MAX_RHS; ++j) yv[j] = (valid && j < nrhs) ? yy[row + j * ldy] : 0.0;
-  double* out = part + ((size_t)(job * 2 + which) * nchunk + chunk) * r * MAX_RHS;
+  for (int j = 0; j < MAX_RHS; ++j) yv[j] = (valid && j < nrhs) ? yy[row + j * ldy] : s_zero(S());
+  S* out = part + ((size_t)(job * 2 + which) * nchunk + chunk) * r * MAX_RHS;
   for (int a = 0; a < r; ++a) {
-    const double v = valid ? vt[row + a * k] : 0.0;
+    const S v = valid ? vt[row + a * k] : s_zero(S());
 #pragma unroll
     for (int j = 0; j < MAX_RHS; ++j) {
       if (j >= nrhs) break;
-      const double s = warp_sum(v * yv[j]);
+      const S s = warp_sum_s(s_mul(v, yv[j]));
       if (lane == 0) red[w][j] = s;
     }
     __syncthreads();
     if (tid < nrhs) {
-      double s = 0.0;
-      for (int q = 0; q < IA_THREADS / 32; ++q) s += red[q][tid];
+      S s = s_zero(S());
+      for (int q = 0; q < IA_THREADS / 32; ++q) s = s_add(s, red[q][tid]);
       out[a + tid * r] = s;
     }
     __syncthreads();
@@ -64,29 +67,31 @@ __global__ void __launch_bounds__(IA_THREADS) iface_dots_kernel(const IfaceApply
 }
 
 // msg[which] = sum over chunks (fixed order) of the local partial messages
-__global__ void iface_reduce_kernel(const IfaceApplyJob* jobs, int r, int nrhs, int nchunk,
-                                    const double* part) {
-  const IfaceApplyJob jb = jobs[blockIdx.x];
+template <class S>
+__global__ void iface_reduce_kernel(const IfaceApplyJobT<S>* jobs, int r, int nrhs, int nchunk,
+                                    const S* part) {
+  const IfaceApplyJobT<S> jb = jobs[blockIdx.x];
   for (int o = threadIdx.x; o < 2 * r * nrhs; o += blockDim.x) {
     const int which = o / (r * nrhs), aj = o % (r * nrhs);
     if (which == 0 ? !jb.has_left : !jb.has_right) continue;
-    const double* pp = part + (size_t)(blockIdx.x * 2 + which) * nchunk * r * MAX_RHS + aj;
-    double s = 0.0;
-    for (int c = 0; c < nchunk; ++c) s += pp[(size_t)c * r * MAX_RHS];
+    const S* pp = part + (size_t)(blockIdx.x * 2 + which) * nchunk * r * MAX_RHS + aj;
+    S s = s_zero(S());
+    for (int c = 0; c < nchunk; ++c) s = s_add(s, pp[(size_t)c * r * MAX_RHS]);
     jb.msg[which * r * MAX_RHS + aj] = s;
   }
 }
 
-__global__ void __launch_bounds__(IA_THREADS) iface_solve_kernel(const IfaceApplyJob* jobs, int r,
-                                                                 int nrhs) {
-  extern __shared__ double ism[];
-  double* mW = ism;              // r x nrhs
-  double* mT = mW + r * nrhs;
-  double* vTz = mT + r * nrhs;
-  double* h = vTz + r * nrhs;
-  double* cT = h + r * nrhs;
-  double* tmp = cT + r * nrhs;
-  const IfaceApplyJob jb = jobs[blockIdx.x];
+template <class S>
+__global__ void __launch_bounds__(IA_THREADS) iface_solve_kernel(const IfaceApplyJobT<S>* jobs,
+                                                                 int r, int nrhs) {
+  extern __shared__ __align__(16) unsigned char ism_raw[];
+  S* mW = reinterpret_cast<S*>(ism_raw);  // r x nrhs
+  S* mT = mW + r * nrhs;
+  S* vTz = mT + r * nrhs;
+  S* h = vTz + r * nrhs;
+  S* cT = h + r * nrhs;
+  S* tmp = cT + r * nrhs;
+  const IfaceApplyJobT<S> jb = jobs[blockIdx.x];
   const int tid = threadIdx.x;
   for (int o = tid; o < r * nrhs; o += IA_THREADS) {
     mW[o] = jb.msg[o];
@@ -97,59 +102,61 @@ __global__ void __launch_bounds__(IA_THREADS) iface_solve_kernel(const IfaceAppl
   // vTz = mT - E (sW .* mW)
   for (int e = tid; e < nout; e += IA_THREADS) {
     const int a = e % r, j = e / r;
-    double s = mT[e];
-    for (int c = 0; c < r; ++c) s -= jb.E[a + c * r] * (jb.sW[c] * mW[c + j * r]);
+    S s = mT[e];
+    for (int c = 0; c < r; ++c) s = s_sub(s, s_mul(jb.E[a + c * r], s_scale(mW[c + j * r], jb.sW[c])));
     vTz[e] = s;
   }
   __syncthreads();
   // h = Hinv (sT .* vTz)
   for (int e = tid; e < nout; e += IA_THREADS) {
     const int a = e % r, j = e / r;
-    double s = 0.0;
-    for (int c = 0; c < r; ++c) s += jb.Hinv[a + c * r] * (jb.sT[c] * vTz[c + j * r]);
+    S s = s_zero(S());
+    for (int c = 0; c < r; ++c) s = s_add(s, s_mul(jb.Hinv[a + c * r], s_scale(vTz[c + j * r], jb.sT[c])));
     h[e] = s;
   }
   __syncthreads();
   // cT = vTz + E (sW .* h)
   for (int e = tid; e < nout; e += IA_THREADS) {
     const int a = e % r, j = e / r;
-    double s = vTz[e];
-    for (int c = 0; c < r; ++c) s += jb.E[a + c * r] * (jb.sW[c] * h[c + j * r]);
+    S s = vTz[e];
+    for (int c = 0; c < r; ++c) s = s_add(s, s_mul(jb.E[a + c * r], s_scale(h[c + j * r], jb.sW[c])));
     cT[e] = s;
   }
   __syncthreads();
   // cW = mW - K (sT .* cT)
   for (int e = tid; e < nout; e += IA_THREADS) {
     const int a = e % r, j = e / r;
-    double s = mW[e];
-    for (int c = 0; c < r; ++c) s -= jb.K[a + c * r] * (jb.sT[c] * cT[c + j * r]);
+    S s = mW[e];
+    for (int c = 0; c < r; ++c) s = s_sub(s, s_mul(jb.K[a + c * r], s_scale(cT[c + j * r], jb.sT[c])));
     tmp[e] = s;
   }
   __syncthreads();
   for (int e = tid; e < nout; e += IA_THREADS) {
     const int a = e % r;
-    if (jb.has_left) jb.scT[e] = jb.sT[a] * cT[e];
-    if (jb.has_right) jb.scW[e] = jb.sW[a] * tmp[e];
+    if (jb.has_left) jb.scT[e] = s_scale(cT[e], jb.sT[a]);
+    if (jb.has_right) jb.scW[e] = s_scale(tmp[e], jb.sW[a]);
   }
 }
 
-void launch_iface_messages(Ctx* c, const IfaceApplyJob* d_jobs, int njobs, int r, int64_t k,
-                           const double* y, int64_t ldy, int nrhs, double* work) {
+template <class S>
+void launch_iface_messages_t(Ctx* c, const IfaceApplyJobT<S>* d_jobs, int njobs, int r, int64_t k,
+                             const S* y, int64_t ldy, int nrhs, S* work) {
   if (njobs == 0) return;
   const int nchunk = (int)((k + IA_ROWS - 1) / IA_ROWS);
   ProfScope ps_(c, K_IFACE);
-  iface_dots_kernel<<<dim3(nchunk, 2 * njobs), IA_THREADS, 0, c->stream>>>(d_jobs, r, k, y, ldy,
-                                                                           nrhs, work);
+  iface_dots_kernel<S><<<dim3(nchunk, 2 * njobs), IA_THREADS, 0, c->stream>>>(d_jobs, r, k, y, ldy,
+                                                                              nrhs, work);
   LRS_LAUNCHED(c);
-  iface_reduce_kernel<<<njobs, 128, 0, c->stream>>>(d_jobs, r, nrhs, nchunk, work);
+  iface_reduce_kernel<S><<<njobs, 128, 0, c->stream>>>(d_jobs, r, nrhs, nchunk, work);
   LRS_LAUNCHED(c);
 }
 
-void launch_iface_solve(Ctx* c, const IfaceApplyJob* d_jobs, int njobs, int r, int nrhs) {
+template <class S>
+void launch_iface_solve_t(Ctx* c, const IfaceApplyJobT<S>* d_jobs, int njobs, int r, int nrhs) {
   if (njobs == 0) return;
   ProfScope ps_(c, K_IFACE);
-  const size_t smem = sizeof(double) * 6 * r * nrhs;
-  iface_solve_kernel<<<njobs, IA_THREADS, smem, c->stream>>>(d_jobs, r, nrhs);
+  const size_t smem = sizeof(S) * 6 * r * nrhs;
+  iface_solve_kernel<S><<<njobs, IA_THREADS, smem, c->stream>>>(d_jobs, r, nrhs);
   LRS_LAUNCHED(c);
 }
 
@@ -160,13 +167,14 @@ size_t iface_work_doubles(int njobs, int r, int64_t k) {
 // x[row, j] = y[row, j] - sum_a uW[row, a] scW_p[a, j] - sum_a uT[row, a] scT_p[a, j]
 // for the local rows; scT / scW: one r x MAX_RHS block per GLOBAL partition (scT of the
 // last partition and scW of the first are never read).
+template <class S>
 __global__ void __launch_bounds__(256) recovery_kernel(BandGeom g, int64_t n, int64_t row_lo,
-                                                       int64_t row_hi, const double* y,
-                                                       int64_t ldy, double* x, int64_t ldx,
-                                                       int nrhs, const double* __restrict__ uT,
-                                                       const double* __restrict__ uW, int r,
-                                                       const double* __restrict__ scT,
-                                                       const double* __restrict__ scW) {
+                                                       int64_t row_hi, const S* y, int64_t ldy,
+                                                       S* x, int64_t ldx, int nrhs,
+                                                       const S* __restrict__ uT,
+                                                       const S* __restrict__ uW, int r,
+                                                       const S* __restrict__ scT,
+                                                       const S* __restrict__ scW) {
   const int64_t row = row_lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (row >= row_hi) return;
   int lo = 0, hi = g.P - 1;
@@ -177,34 +185,45 @@ __global__ void __launch_bounds__(256) recovery_kernel(BandGeom g, int64_t n, in
   }
   const int pg = g.p0 + lo;
   const bool hasW = pg > 0, hasT = pg < g.Pg - 1;
-  double acc[MAX_RHS];
+  S acc[MAX_RHS];
   for (int j = 0; j < nrhs; ++j) acc[j] = y[row + j * ldy];
   if (hasW) {
-    const double* sc = scW + (int64_t)pg * r * MAX_RHS;
+    const S* sc = scW + (int64_t)pg * r * MAX_RHS;
     for (int a = 0; a < r; ++a) {
-      const double u = uW[row + a * n];
-      for (int j = 0; j < nrhs; ++j) acc[j] -= u * sc[a + j * r];
+      const S u = uW[row + a * n];
+      for (int j = 0; j < nrhs; ++j) acc[j] = s_sub(acc[j], s_mul(u, sc[a + j * r]));
     }
   }
   if (hasT) {
-    const double* sc = scT + (int64_t)pg * r * MAX_RHS;
+    const S* sc = scT + (int64_t)pg * r * MAX_RHS;
     for (int a = 0; a < r; ++a) {
-      const double u = uT[row + a * n];
-      for (int j = 0; j < nrhs; ++j) acc[j] -= u * sc[a + j * r];
+      const S u = uT[row + a * n];
+      for (int j = 0; j < nrhs; ++j) acc[j] = s_sub(acc[j], s_mul(u, sc[a + j * r]));
     }
   }
   for (int j = 0; j < nrhs; ++j) x[row + j * ldx] = acc[j];
 }
 
-void launch_recovery(Ctx* c, const BandGeom& g, int64_t n, int64_t row_lo, int64_t row_hi,
-                     const double* y, int64_t ldy, double* x, int64_t ldx, int nrhs,
-                     const double* uT, const double* uW, int r, const double* scT,
-                     const double* scW) {
+template <class S>
+void launch_recovery_t(Ctx* c, const BandGeom& g, int64_t n, int64_t row_lo, int64_t row_hi,
+                       const S* y, int64_t ldy, S* x, int64_t ldx, int nrhs, const S* uT,
+                       const S* uW, int r, const S* scT, const S* scW) {
   if (row_hi <= row_lo) return;
   ProfScope ps_(c, K_RECOVERY);
-  recovery_kernel<<<(unsigned)((row_hi - row_lo + 255) / 256), 256, 0, c->stream>>>(
+  recovery_kernel<S><<<(unsigned)((row_hi - row_lo + 255) / 256), 256, 0, c->stream>>>(
       g, n, row_lo, row_hi, y, ldy, x, ldx, nrhs, uT, uW, r, scT, scW);
   LRS_LAUNCHED(c);
 }
+
+#define LRS_INST(S)                                                                              \
+  template void launch_iface_messages_t<S>(Ctx*, const IfaceApplyJobT<S>*, int, int, int64_t,    \
+                                           const S*, int64_t, int, S*);                          \
+  template void launch_iface_solve_t<S>(Ctx*, const IfaceApplyJobT<S>*, int, int, int);          \
+  template void launch_recovery_t<S>(Ctx*, const BandGeom&, int64_t, int64_t, int64_t, const S*, \
+                                     int64_t, S*, int64_t, int, const S*, const S*, int,         \
+                                     const S*, const S*);
+LRS_INST(double)
+LRS_INST(zc)
+#undef LRS_INST
 
 }  // namespace lrs

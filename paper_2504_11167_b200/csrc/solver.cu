@@ -6,6 +6,10 @@
 // The control flow mirrors the CPU checker in oracle/ line by line so that the
 // two produce the same iterates up to roundoff (the checker is never called).
 //
+// Everything is templated on the scalar S = double | zc (complex128, config c5,
+// SURVEY.md D2): Hermitian dot products, complex Givens rotations, and the
+// conjugate-transpose adjoint in the spike range finder.
+//
 // Sharding: a factorization owns partitions [p0, p0 + P) of Pg (all of them on one
 // GPU).  Cross-GPU traffic is exactly the SURVEY.md 2.4 set: the two rank-r interface
 // messages per apply (C1; C2 is computed on both sides, see precond.cu), the b-row
@@ -15,10 +19,12 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <complex>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <future>
+#include <type_traits>
 
 #include "fact.h"
 #include "lrs_rng.h"
@@ -27,9 +33,27 @@ namespace lrs {
 
 namespace {
 
+template <class S> constexpr int SW = (int)(sizeof(S) / sizeof(double));
+template <class S> S* sp(const DevBuf<double>& b) { return reinterpret_cast<S*>(b.get()); }
+// host scalar of a device scalar type
+template <class S>
+using HT = std::conditional_t<IsC<S>::value, std::complex<double>, double>;
+inline double hconj(double a) { return a; }
+inline std::complex<double> hconj(std::complex<double> a) { return std::conj(a); }
+inline double hreal(double a) { return a; }
+inline double hreal(std::complex<double> a) { return a.real(); }
+template <class S> S to_dev(HT<S> v);
+template <> double to_dev<double>(double v) { return v; }
+template <> zc to_dev<zc>(std::complex<double> v) { return zc{v.real(), v.imag()}; }
+
 template <class J>
 void upload(Ctx* c, DevBuf<J>& d, const std::vector<J>& h) {
   d.alloc(h.size());
+  if (!h.empty()) c->stage_h2d(d.get(), h.data(), sizeof(J) * h.size());
+}
+template <class J>
+void upload_raw(Ctx* c, DevBuf<unsigned char>& d, const std::vector<J>& h) {
+  d.alloc(sizeof(J) * h.size());
   if (!h.empty()) c->stage_h2d(d.get(), h.data(), sizeof(J) * h.size());
 }
 
@@ -47,11 +71,11 @@ float elapsed_ms(cudaEvent_t a, cudaEvent_t b) {
 }
 
 // columns [0, ncols) of a block with leading dimension ld
-void copy_block(Ctx* c, double* dst, int64_t ldd, const double* src, int64_t lds, int64_t rows,
-                int ncols) {
+template <class S>
+void copy_block(Ctx* c, S* dst, int64_t ldd, const S* src, int64_t lds, int64_t rows, int ncols) {
   if (rows <= 0 || ncols == 0) return;
-  LRS_CUDA(cudaMemcpy2DAsync(dst, sizeof(double) * ldd, src, sizeof(double) * lds,
-                             sizeof(double) * rows, ncols, cudaMemcpyDeviceToDevice, c->stream));
+  LRS_CUDA(cudaMemcpy2DAsync(dst, sizeof(S) * ldd, src, sizeof(S) * lds, sizeof(S) * rows, ncols,
+                             cudaMemcpyDeviceToDevice, c->stream));
 }
 
 // ---- communication (no-ops on a single GPU) ---------------------------------------------
@@ -61,16 +85,18 @@ void comm_rc(int32_t rc, const char* what) {
 
 // Two-phase neighbour exchange of `count` doubles: to_next -> rank+1 (received there in
 // from_prev), then to_prev -> rank-1 (received in from_next).
-void neighbor_exchange(Fact* f, const double* to_next, double* from_prev, const double* to_prev,
-                       double* from_next, int64_t count) {
+void neighbor_exchange(Fact* f, const void* to_next, void* from_prev, const void* to_prev,
+                       void* from_next, int64_t count) {
   if (!f->dist || count == 0) return;
   LRS_CUDA(cudaStreamSynchronize(f->ctx->stream));
   const int r = f->comm.rank, G = f->comm.size;
   const int next = r + 1 < G ? r + 1 : -1, prev = r > 0 ? r - 1 : -1;
-  comm_rc(f->comm.sendrecv(f->comm.user, to_next, next >= 0 ? count : 0, next, from_prev,
+  comm_rc(f->comm.sendrecv(f->comm.user, static_cast<const double*>(to_next),
+                           next >= 0 ? count : 0, next, static_cast<double*>(from_prev),
                            prev >= 0 ? count : 0, prev),
           "sendrecv");
-  comm_rc(f->comm.sendrecv(f->comm.user, to_prev, prev >= 0 ? count : 0, prev, from_next,
+  comm_rc(f->comm.sendrecv(f->comm.user, static_cast<const double*>(to_prev),
+                           prev >= 0 ? count : 0, prev, static_cast<double*>(from_next),
                            next >= 0 ? count : 0, next),
           "sendrecv");
 }
@@ -92,75 +118,84 @@ std::vector<double> allgather_host(Fact* f, const std::vector<double>& v) {
 
 // SpMV halo (C3): rows [row_lo - hb, row_lo) and [row_hi, row_hi + hb) of the
 // full-length block x from the neighbours, hb = the band half-width of A.
-void halo_exchange(Fact* f, double* x, int64_t ld, int nrhs) {
+template <class S>
+void halo_exchange(Fact* f, S* x, int64_t ld, int nrhs) {
   if (!f->dist) return;
   const int64_t hb = std::min<int64_t>(f->mat->k, f->row_hi - f->row_lo);
   if (hb == 0 || nrhs == 0) return;
   Ctx* c = f->ctx;
   const int64_t cnt = hb * nrhs;
-  double* s_next = f->xch.get();
-  double* s_prev = s_next + cnt;
-  double* r_prev = s_prev + cnt;
-  double* r_next = r_prev + cnt;
+  S* s_next = sp<S>(f->xch);
+  S* s_prev = s_next + cnt;
+  S* r_prev = s_prev + cnt;
+  S* r_next = r_prev + cnt;
   copy_block(c, s_next, hb, x + f->row_hi - hb, ld, hb, nrhs);
   copy_block(c, s_prev, hb, x + f->row_lo, ld, hb, nrhs);
-  neighbor_exchange(f, s_next, r_prev, s_prev, r_next, cnt);
+  neighbor_exchange(f, s_next, r_prev, s_prev, r_next, cnt * SW<S>);
   const int rk = f->comm.rank;
   if (rk > 0) copy_block(c, x + f->row_lo - hb, ld, r_prev, hb, hb, nrhs);
   if (rk + 1 < f->comm.size) copy_block(c, x + f->row_hi, ld, r_next, hb, hb, nrhs);
 }
 
-}  // namespace
-
-void shard_plan(int64_t P, int size, int rank, int64_t* p_lo, int64_t* p_hi) {
-  *p_lo = (int64_t)rank * P / size;
-  *p_hi = (int64_t)(rank + 1) * P / size;
+template <class S>
+void spmv_s(Ctx* c, const Mat* m, const S* x, int64_t ldx, S* y, int64_t ldy, int nrhs, int mode,
+            const S* b, int64_t ldb, int64_t lo, int64_t hi) {
+  if constexpr (IsC<S>::value) launch_spmv_z(c, m, x, ldx, y, ldy, nrhs, mode, b, ldb, lo, hi);
+  else launch_spmv(c, m, x, ldx, y, ldy, nrhs, mode, b, ldb, lo, hi);
 }
 
 // ------------------------------------------------------------------------------------
-// D-stage: banded L then U solves (or U^T then L^T for the adjoint), batches of
-// SOLVE_MAX_RHS columns, all local partitions concurrently.
+// D-stage: banded L then U solves (or U^H then L^H for the adjoint), batches of up to
+// SOLVE_MAX_RHS (real) / ZSOLVE_MAX_RHS (complex) columns, all local partitions at once.
 // ------------------------------------------------------------------------------------
-void dstage(Fact* f, double* x, int64_t ld, int nrhs, bool adjoint, int p_only) {
+template <class S>
+void dstage_t(Fact* f, S* x, int64_t ld, int nrhs, bool adjoint, int p_only) {
   const BandGeom g = f->geom();
   const int ntiles = p_only >= 0 ? f->T[p_only] : (int)f->total_rowtiles;
-  for (int c0 = 0; c0 < nrhs; c0 += SOLVE_MAX_RHS) {
-    const int nr = std::min(SOLVE_MAX_RHS, nrhs - c0);
-    double* xc = x + (int64_t)c0 * ld;
-    launch_band_solve(f->ctx, g, f->tiles.get(), adjoint ? 2 : 0, xc, ld, nr, f->flags.get(),
-                      f->next_epoch(), f->ticket.get(), p_only, ntiles);
-    launch_band_solve(f->ctx, g, f->tiles.get(), adjoint ? 3 : 1, xc, ld, nr, f->flags.get(),
-                      f->next_epoch(), f->ticket.get(), p_only, ntiles);
+  constexpr int MAXR = IsC<S>::value ? ZSOLVE_MAX_RHS : SOLVE_MAX_RHS;
+  for (int c0 = 0; c0 < nrhs; c0 += MAXR) {
+    const int nr = std::min(MAXR, nrhs - c0);
+    S* xc = x + (int64_t)c0 * ld;
+    for (int half = 0; half < 2; ++half) {
+      const int mode = adjoint ? 2 + half : half;
+      if constexpr (IsC<S>::value)
+        launch_band_solve_z(f->ctx, g, sp<zc>(f->tiles), mode, xc, ld, nr, f->flags.get(),
+                            f->next_epoch(), f->ticket.get(), p_only, ntiles);
+      else
+        launch_band_solve(f->ctx, g, f->tiles.get(), mode, xc, ld, nr, f->flags.get(),
+                          f->next_epoch(), f->ticket.get(), p_only, ntiles);
+    }
   }
 }
 
-void apply_precond(Fact* f, const double* in, int64_t ldi, double* out, int64_t ldo, int nrhs,
-                   bool block_jacobi) {
+template <class S>
+void apply_precond_t(Fact* f, const S* in, int64_t ldi, S* out, int64_t ldo, int nrhs,
+                     bool block_jacobi) {
   Ctx* c = f->ctx;
   const int64_t nl = f->row_hi - f->row_lo;
   if (out != in) copy_block(c, out + f->row_lo, ldo, in + f->row_lo, ldi, nl, nrhs);
-  dstage(f, out, ldo, nrhs, false, -1);
+  dstage_t(f, out, ldo, nrhs, false, -1);
   const bool lowrank = !block_jacobi && f->variant == LRS_VARIANT_T && f->r > 0 && f->Pg > 1;
   if (!lowrank) return;
   const int r = f->r;
+  const auto* jobs = reinterpret_cast<const IfaceApplyJobT<S>*>(f->iface_jobs.get());
   for (int c0 = 0; c0 < nrhs; c0 += MAX_RHS) {
     const int nr = std::min(MAX_RHS, nrhs - c0);
-    double* xc = out + (int64_t)c0 * ldo;
-    launch_iface_messages(c, f->iface_jobs.get(), f->ni, r, f->k, xc, ldo, nr,
-                          f->iface_work.get());
+    S* xc = out + (int64_t)c0 * ldo;
+    launch_iface_messages_t<S>(c, jobs, f->ni, r, f->k, xc, ldo, nr, sp<S>(f->iface_work));
     if (f->dist) {
       // C1 across the GPU boundaries: m_W (computed left) goes right, m_T goes left
       const int64_t blk = (int64_t)r * MAX_RHS;
-      double* mbase = f->iface_msg.get();
-      const double* to_next = f->job_right >= 0 ? mbase + (2 * f->job_right + 0) * blk : mbase;
-      double* from_prev = f->job_left >= 0 ? mbase + (2 * f->job_left + 0) * blk : mbase;
-      const double* to_prev = f->job_left >= 0 ? mbase + (2 * f->job_left + 1) * blk : mbase;
-      double* from_next = f->job_right >= 0 ? mbase + (2 * f->job_right + 1) * blk : mbase;
-      neighbor_exchange(f, to_next, from_prev, to_prev, from_next, blk);
+      S* mbase = sp<S>(f->iface_msg);
+      const S* to_next = f->job_right >= 0 ? mbase + (2 * f->job_right + 0) * blk : mbase;
+      S* from_prev = f->job_left >= 0 ? mbase + (2 * f->job_left + 0) * blk : mbase;
+      const S* to_prev = f->job_left >= 0 ? mbase + (2 * f->job_left + 1) * blk : mbase;
+      S* from_next = f->job_right >= 0 ? mbase + (2 * f->job_right + 1) * blk : mbase;
+      neighbor_exchange(f, to_next, from_prev, to_prev, from_next, blk * SW<S>);
     }
-    launch_iface_solve(c, f->iface_jobs.get(), f->ni, r, nr);
-    launch_recovery(c, f->geom(), f->n, f->row_lo, f->row_hi, xc, ldo, xc, ldo, nr, f->uT.get(),
-                    f->uW.get(), r, f->scT.get(), f->scW.get());
+    launch_iface_solve_t<S>(c, jobs, f->ni, r, nr);
+    launch_recovery_t<S>(c, f->geom(), f->n, f->row_lo, f->row_hi, xc, ldo, xc, ldo, nr,
+                         sp<S>(f->uT), sp<S>(f->uW), r, sp<S>(f->scT), sp<S>(f->scW));
   }
   // CommLedger: 2 compressed messages per local-side interface in the
   // reduced solve and 2 in the recovery, r n_rhs scalars each -- 4 (p-1) r n_rhs per
@@ -181,8 +216,9 @@ void apply_precond(Fact* f, const double* in, int64_t ldi, double* out, int64_t 
 // Returns false (without throwing) if an interface is ill-conditioned on ANY rank,
 // filling *bad_iface / *bad_cond, so the caller can apply the r-halving retry.
 // ------------------------------------------------------------------------------------
-// Gaussian test blocks of the spikes of partitions [plo, phi): slot 2*i + side, k x l each.
-static std::vector<double> make_omega(uint64_t seed, int Pg, int plo, int phi, int64_t k, int l) {
+// Gaussian test blocks of the spikes of partitions [plo, phi): slot 2*i + side, k x l each
+// (real for both fields, as the shared generator draws them).
+std::vector<double> make_omega(uint64_t seed, int Pg, int plo, int phi, int64_t k, int l) {
   std::vector<double> h((size_t)Pg * 2 * k * l, 0.0);
   for (int i = plo; i < phi; ++i)
     for (int side = 0; side < 2; ++side) {
@@ -194,14 +230,15 @@ static std::vector<double> make_omega(uint64_t seed, int Pg, int plo, int phi, i
   return h;
 }
 
-static bool build_lowrank(Fact* f, int r, int* bad_iface, double* bad_cond,
-                          std::vector<double>* pre) {
+template <class S>
+bool build_lowrank(Fact* f, int r, int* bad_iface, double* bad_cond, std::vector<double>* pre) {
   Ctx* c = f->ctx;
   Mat* m = f->mat;
   const int Pg = f->Pg, p0 = f->p0, P = f->P;
   const int64_t n = f->n, k = f->k;
   const int os = f->os >= 0 ? f->os : (r + 1) / 2;
   const int l = r + os;
+  constexpr int w = SW<S>;
   if (r < 1 || r > k) throw LrsError(LRS_ERR_PARAMETER, "randomized_spike_svd: 1 <= n_svd <= k");
   if (l > k) throw LrsError(LRS_ERR_PARAMETER, "randomized_spike_svd: n_svd + oversample <= k");
   if (f->passes < 2) throw LrsError(LRS_ERR_PARAMETER, "randomized_spike_svd: passes >= 2");
@@ -209,15 +246,22 @@ static bool build_lowrank(Fact* f, int r, int* bad_iface, double* bad_cond,
   f->r = r;
   f->l = l;
   const int L2 = 2 * l;
-  DevBuf<double> Y, S, Om, Zt, Rz, Ur, Vr, sig;
-  Y.alloc((size_t)n * L2);
-  S.alloc((size_t)n * L2);
-  Om.alloc((size_t)Pg * 2 * k * l);
-  Zt.alloc((size_t)Pg * 2 * k * l);
-  Rz.alloc((size_t)Pg * 2 * l * l);
-  Ur.alloc((size_t)Pg * 2 * l * l);
-  Vr.alloc((size_t)Pg * 2 * l * l);
+  DevBuf<double> Yb, Sb, Omb, Ztb, Rzb, Urb, Vrb, sig;
+  Yb.alloc((size_t)n * L2 * w);
+  Sb.alloc((size_t)n * L2 * w);
+  Omb.alloc((size_t)Pg * 2 * k * l * w);
+  Ztb.alloc((size_t)Pg * 2 * k * l * w);
+  Rzb.alloc((size_t)Pg * 2 * l * l * w);
+  Urb.alloc((size_t)Pg * 2 * l * l * w);
+  Vrb.alloc((size_t)Pg * 2 * l * l * w);
   sig.alloc((size_t)Pg * 2 * l);
+  S* Y = sp<S>(Yb);
+  S* Sx = sp<S>(Sb);
+  S* Om = sp<S>(Omb);
+  S* Zt = sp<S>(Ztb);
+  S* Rz = sp<S>(Rzb);
+  S* Ur = sp<S>(Urb);
+  S* Vr = sp<S>(Vrb);
   // local spikes: (global partition, side); partition g = p0 + local index
   std::vector<std::pair<int, int>> spk;
   for (int i = p0; i < p0 + P; ++i) {
@@ -233,15 +277,20 @@ static bool build_lowrank(Fact* f, int r, int* bad_iface, double* bad_cond,
     std::vector<double> h = (pre && pre->size() == (size_t)Pg * 2 * k * l)
                                 ? std::move(*pre)
                                 : make_omega(f->seed, Pg, p0, p0 + P, k, l);
-    LRS_CUDA(cudaMemcpy(Om.get(), h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice));
+    if constexpr (IsC<S>::value) {
+      std::vector<double> hz(h.size() * 2, 0.0);
+      for (size_t e = 0; e < h.size(); ++e) hz[2 * e] = h[e];
+      h.swap(hz);
+    }
+    LRS_CUDA(cudaMemcpy(Om, h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice));
   }
-  auto ycol = [&](double* base, int i, int side) { return base + goff(i) + (int64_t)side * l * n; };
+  auto ycol = [&](S* base, int i, int side) { return base + goff(i) + (int64_t)side * l * n; };
   // T_apply: Y = A_i^-1 pad(coupling X) for every spike, X = k x l blocks in src[slot]
-  DevBuf<CoupleJob> cj;
-  auto T_apply = [&](const double* src) {
-    std::vector<CoupleJob> jobs;
+  DevBuf<CoupleJobT<S>> cj;
+  auto T_apply = [&](const S* src) {
+    std::vector<CoupleJobT<S>> jobs;
     for (auto [i, side] : spk) {
-      CoupleJob j{};
+      CoupleJobT<S> j{};
       if (side == LRS_SIDE_T) {
         j.r0 = goff(i) + gsize(i) - k;
         j.c0 = goff(i + 1);
@@ -253,111 +302,110 @@ static bool build_lowrank(Fact* f, int r, int* bad_iface, double* bad_cond,
       j.dst0 = j.r0;
       j.X = src + slot(i, side) * k * l;
       j.ldx = k;
-      j.out = Y.get() + (int64_t)side * l * n;
+      j.out = Y + (int64_t)side * l * n;
       j.ldo = n;
       j.ncols = l;
       jobs.push_back(j);
     }
-    LRS_CUDA(cudaMemsetAsync(Y.get(), 0, sizeof(double) * n * L2, c->stream));
+    LRS_CUDA(cudaMemsetAsync(Y, 0, sizeof(S) * n * L2, c->stream));
     upload(c, cj, jobs);
-    launch_coupling(c, m, false, cj.get(), (int)jobs.size(), k, l);
-    dstage(f, Y.get(), n, L2, false, -1);
+    launch_coupling_t<S>(c, m, false, cj.get(), (int)jobs.size(), k, l);
+    dstage_t(f, Y, n, L2, false, -1);
   };
-  // Tt_apply: Zt[slot] = coupling^T (A_i^-T Q)|tip, Q = columns of Y
+  // Tt_apply: Zt[slot] = coupling^H (A_i^-H Q)|tip, Q = columns of Y  (= T^H Q)
   auto Tt_apply = [&]() {
-    copy_block(c, S.get(), n, Y.get(), n, n, L2);
-    dstage(f, S.get(), n, L2, true, -1);
-    std::vector<CoupleJob> jobs;
+    copy_block(c, Sx, n, Y, n, n, L2);
+    dstage_t(f, Sx, n, L2, true, -1);
+    std::vector<CoupleJobT<S>> jobs;
     for (auto [i, side] : spk) {
-      CoupleJob j{};
-      if (side == LRS_SIDE_T) {  // B_i^T = A^T[off_{i+1} .., off_i+n_i-k ..]
+      CoupleJobT<S> j{};
+      if (side == LRS_SIDE_T) {  // B_i^H = A^H[off_{i+1} .., off_i+n_i-k ..]
         j.r0 = goff(i + 1);
         j.c0 = goff(i) + gsize(i) - k;
-      } else {  // C_i^T = A^T[off_i - k .., off_i ..]
+      } else {  // C_i^H = A^H[off_i - k .., off_i ..]
         j.r0 = goff(i) - k;
         j.c0 = goff(i);
       }
       j.b = k;
       j.dst0 = 0;
-      j.X = S.get() + j.c0 + (int64_t)side * l * n;
+      j.X = Sx + j.c0 + (int64_t)side * l * n;
       j.ldx = n;
-      j.out = Zt.get() + slot(i, side) * k * l;
+      j.out = Zt + slot(i, side) * k * l;
       j.ldo = k;
       j.ncols = l;
       jobs.push_back(j);
     }
     upload(c, cj, jobs);
-    launch_coupling(c, m, true, cj.get(), (int)jobs.size(), k, l);
+    launch_coupling_t<S>(c, m, true, cj.get(), (int)jobs.size(), k, l);
   };
-  DevBuf<QrJob> qj;
+  DevBuf<QrJobT<S>> qj;
   auto orth_Y = [&]() {
-    std::vector<QrJob> jobs;
-    for (auto [i, side] : spk) jobs.push_back(QrJob{ycol(Y.get(), i, side), gsize(i), n, nullptr});
+    std::vector<QrJobT<S>> jobs;
+    for (auto [i, side] : spk) jobs.push_back(QrJobT<S>{ycol(Y, i, side), gsize(i), n, nullptr});
     upload(c, qj, jobs);
-    launch_householder_qr(c, qj.get(), (int)jobs.size(), l);
+    launch_householder_qr_t<S>(c, qj.get(), (int)jobs.size(), l);
   };
   auto orth_Zt = [&](bool keepR) {
-    std::vector<QrJob> jobs;
+    std::vector<QrJobT<S>> jobs;
     for (auto [i, side] : spk)
-      jobs.push_back(QrJob{Zt.get() + slot(i, side) * k * l, k, k,
-                           keepR ? Rz.get() + slot(i, side) * l * l : nullptr});
+      jobs.push_back(QrJobT<S>{Zt + slot(i, side) * k * l, k, k,
+                               keepR ? Rz + slot(i, side) * l * l : nullptr});
     upload(c, qj, jobs);
-    launch_householder_qr(c, qj.get(), (int)jobs.size(), l);
+    launch_householder_qr_t<S>(c, qj.get(), (int)jobs.size(), l);
   };
 
-  T_apply(Om.get());
+  T_apply(Om);
   orth_Y();
   for (int pi = 0; pi < (f->passes - 2) / 2; ++pi) {
     Tt_apply();
     orth_Zt(false);
-    T_apply(Zt.get());
+    T_apply(Zt);
     orth_Y();
   }
-  Tt_apply();          // Zt = (Q^T T)^T, k x l
+  Tt_apply();          // Zt = (Q^H T)^H, k x l
   orth_Zt(true);       // Zt = Q_z R_z
-  f->uT.alloc((size_t)n * r);
-  f->uW.alloc((size_t)n * r);
-  f->vtT.alloc((size_t)Pg * k * r);
-  f->vtW.alloc((size_t)Pg * k * r);
+  f->uT.alloc((size_t)n * r * w);
+  f->uW.alloc((size_t)n * r * w);
+  f->vtT.alloc((size_t)Pg * k * r * w);
+  f->vtW.alloc((size_t)Pg * k * r * w);
   f->sT.alloc((size_t)Pg * r);
   f->sW.alloc((size_t)Pg * r);
-  LRS_CUDA(cudaMemsetAsync(f->uT.get(), 0, sizeof(double) * n * r, c->stream));
-  LRS_CUDA(cudaMemsetAsync(f->uW.get(), 0, sizeof(double) * n * r, c->stream));
-  LRS_CUDA(cudaMemsetAsync(f->vtT.get(), 0, sizeof(double) * Pg * k * r, c->stream));
-  LRS_CUDA(cudaMemsetAsync(f->vtW.get(), 0, sizeof(double) * Pg * k * r, c->stream));
+  LRS_CUDA(cudaMemsetAsync(f->uT.get(), 0, sizeof(S) * n * r, c->stream));
+  LRS_CUDA(cudaMemsetAsync(f->uW.get(), 0, sizeof(S) * n * r, c->stream));
+  LRS_CUDA(cudaMemsetAsync(f->vtT.get(), 0, sizeof(S) * Pg * k * r, c->stream));
+  LRS_CUDA(cudaMemsetAsync(f->vtW.get(), 0, sizeof(S) * Pg * k * r, c->stream));
   LRS_CUDA(cudaMemsetAsync(f->sT.get(), 0, sizeof(double) * Pg * r, c->stream));
   LRS_CUDA(cudaMemsetAsync(f->sW.get(), 0, sizeof(double) * Pg * r, c->stream));
   {
-    std::vector<SvdJob> jobs;
+    std::vector<SvdJobT<S>> jobs;
     for (auto [i, side] : spk) {
       const size_t s = slot(i, side);
-      jobs.push_back(SvdJob{Rz.get() + s * l * l, Vr.get() + s * l * l, Ur.get() + s * l * l,
-                            sig.get() + s * l});
+      jobs.push_back(SvdJobT<S>{Rz + s * l * l, Vr + s * l * l, Ur + s * l * l, sig.get() + s * l});
     }
-    DevBuf<SvdJob> sj;
+    DevBuf<SvdJobT<S>> sj;
     upload(c, sj, jobs);
-    launch_jacobi_svd(c, sj.get(), (int)jobs.size(), l);
-    // Z = V_R S (Q_z U_R)^T  =>  u = Q V_R[:, :r],  v^T = Q_z U_R[:, :r]
-    std::vector<GemmJob> gu, gv;
+    launch_jacobi_svd_t<S>(c, sj.get(), (int)jobs.size(), l);
+    // Z = V_R S (Q_z U_R)^H  =>  u = Q V_R[:, :r],  v^T = conj(Q_z U_R[:, :r])
+    std::vector<GemmJobT<S>> gu, gv;
     std::vector<SigmaJob> sjobs;
     int64_t maxm = 0;
     for (auto [i, side] : spk) {
       const size_t s = slot(i, side);
-      double* ubuf = side == LRS_SIDE_T ? f->uT.get() : f->uW.get();
-      double* vbuf = side == LRS_SIDE_T ? f->vtT.get() : f->vtW.get();
+      S* ubuf = side == LRS_SIDE_T ? sp<S>(f->uT) : sp<S>(f->uW);
+      S* vbuf = side == LRS_SIDE_T ? sp<S>(f->vtT) : sp<S>(f->vtW);
       double* sbuf = side == LRS_SIDE_T ? f->sT.get() : f->sW.get();
-      gu.push_back(GemmJob{ycol(Y.get(), i, side), n, Vr.get() + s * l * l, l, ubuf + goff(i), n,
-                           gsize(i), r, l, 0});
-      gv.push_back(GemmJob{Zt.get() + s * k * l, k, Ur.get() + s * l * l, l,
-                           vbuf + (size_t)i * k * r, k, k, r, l, 0});
+      gu.push_back(GemmJobT<S>{ycol(Y, i, side), n, Vr + s * l * l, l, ubuf + goff(i), n,
+                               gsize(i), r, l, 0});
+      gv.push_back(GemmJobT<S>{Zt + s * k * l, k, Ur + s * l * l, l, vbuf + (size_t)i * k * r, k,
+                               k, r, l, IsC<S>::value ? 1 : 0});
       sjobs.push_back(SigmaJob{sig.get() + s * l, sbuf + (size_t)i * r});
       maxm = std::max(maxm, gsize(i));
     }
-    DevBuf<GemmJob> dgu, dgv;
+    DevBuf<GemmJobT<S>> dgu, dgv;
     upload(c, dgu, gu);
     upload(c, dgv, gv);
-    launch_small_gemm(c, dgu.get(), (int)gu.size(), maxm, r);
-    launch_small_gemm(c, dgv.get(), (int)gv.size(), k, r);
+    launch_small_gemm_t<S>(c, dgu.get(), (int)gu.size(), maxm, r);
+    launch_small_gemm_t<S>(c, dgv.get(), (int)gv.size(), k, r);
     DevBuf<SigmaJob> dsj;
     upload(c, dsj, sjobs);
     DevBuf<int> flag;
@@ -369,84 +417,77 @@ static bool build_lowrank(Fact* f, int r, int* bad_iface, double* bad_cond,
     f->rank_collapsed = hflag != 0;
   }
   // C5: ship the T side of the last local partition right and the W side of the first
-  // local partition left: [u tip (k x r) | v^T (k x r) | sigma (r)]
+  // local partition left: [u tip (k x r) | v^T (k x r) | sigma (r, real)]
   if (f->dist) {
-    const int64_t cnt = 2 * k * r + r;
+    const int64_t kr = k * r, cnt = 2 * kr * w + r;  // doubles
     DevBuf<double> buf;
     buf.alloc((size_t)cnt * 4);
     double* s_next = buf.get();
     double* r_prev = s_next + cnt;
     double* s_prev = r_prev + cnt;
     double* r_next = s_prev + cnt;
+    auto U = [](double* b) { return reinterpret_cast<S*>(b); };
+    auto pack = [&](double* dst, const S* ubuf, int64_t urow, const S* vbuf, const double* sbuf,
+                    int i) {
+      copy_block(c, U(dst), k, ubuf + urow, n, k, r);
+      LRS_CUDA(cudaMemcpyAsync(U(dst) + kr, vbuf + (size_t)i * kr, sizeof(S) * kr,
+                               cudaMemcpyDeviceToDevice, c->stream));
+      LRS_CUDA(cudaMemcpyAsync(dst + 2 * kr * w, sbuf + (size_t)i * r, sizeof(double) * r,
+                               cudaMemcpyDeviceToDevice, c->stream));
+    };
+    auto unpack = [&](const double* src, S* ubuf, int64_t urow, S* vbuf, double* sbuf, int i) {
+      copy_block(c, ubuf + urow, n, reinterpret_cast<const S*>(src), k, k, r);
+      LRS_CUDA(cudaMemcpyAsync(vbuf + (size_t)i * kr, reinterpret_cast<const S*>(src) + kr,
+                               sizeof(S) * kr, cudaMemcpyDeviceToDevice, c->stream));
+      LRS_CUDA(cudaMemcpyAsync(sbuf + (size_t)i * r, src + 2 * kr * w, sizeof(double) * r,
+                               cudaMemcpyDeviceToDevice, c->stream));
+    };
     const int iR = p0 + P - 1;  // T side, to the right neighbour (if any)
-    if (iR < Pg - 1) {
-      copy_block(c, s_next, k, f->uT.get() + goff(iR + 1) - k, n, k, r);
-      LRS_CUDA(cudaMemcpyAsync(s_next + k * r, f->vtT.get() + (size_t)iR * k * r,
-                               sizeof(double) * k * r, cudaMemcpyDeviceToDevice, c->stream));
-      LRS_CUDA(cudaMemcpyAsync(s_next + 2 * k * r, f->sT.get() + (size_t)iR * r,
-                               sizeof(double) * r, cudaMemcpyDeviceToDevice, c->stream));
-    }
-    if (p0 > 0) {  // W side of partition p0, to the left neighbour
-      copy_block(c, s_prev, k, f->uW.get() + goff(p0), n, k, r);
-      LRS_CUDA(cudaMemcpyAsync(s_prev + k * r, f->vtW.get() + (size_t)p0 * k * r,
-                               sizeof(double) * k * r, cudaMemcpyDeviceToDevice, c->stream));
-      LRS_CUDA(cudaMemcpyAsync(s_prev + 2 * k * r, f->sW.get() + (size_t)p0 * r,
-                               sizeof(double) * r, cudaMemcpyDeviceToDevice, c->stream));
-    }
+    if (iR < Pg - 1) pack(s_next, sp<S>(f->uT), goff(iR + 1) - k, sp<S>(f->vtT), f->sT.get(), iR);
+    if (p0 > 0) pack(s_prev, sp<S>(f->uW), goff(p0), sp<S>(f->vtW), f->sW.get(), p0);
     neighbor_exchange(f, s_next, r_prev, s_prev, r_next, cnt);
-    if (p0 > 0) {  // T side of partition p0 - 1
-      const int i = p0 - 1;
-      copy_block(c, f->uT.get() + goff(i + 1) - k, n, r_prev, k, k, r);
-      LRS_CUDA(cudaMemcpyAsync(f->vtT.get() + (size_t)i * k * r, r_prev + k * r,
-                               sizeof(double) * k * r, cudaMemcpyDeviceToDevice, c->stream));
-      LRS_CUDA(cudaMemcpyAsync(f->sT.get() + (size_t)i * r, r_prev + 2 * k * r,
-                               sizeof(double) * r, cudaMemcpyDeviceToDevice, c->stream));
-    }
-    if (iR < Pg - 1) {  // W side of partition iR + 1
-      const int i = iR + 1;
-      copy_block(c, f->uW.get() + goff(i), n, r_next, k, k, r);
-      LRS_CUDA(cudaMemcpyAsync(f->vtW.get() + (size_t)i * k * r, r_next + k * r,
-                               sizeof(double) * k * r, cudaMemcpyDeviceToDevice, c->stream));
-      LRS_CUDA(cudaMemcpyAsync(f->sW.get() + (size_t)i * r, r_next + 2 * k * r,
-                               sizeof(double) * r, cudaMemcpyDeviceToDevice, c->stream));
-    }
+    if (p0 > 0)  // T side of partition p0 - 1
+      unpack(r_prev, sp<S>(f->uT), goff(p0) - k, sp<S>(f->vtT), f->sT.get(), p0 - 1);
+    if (iR < Pg - 1)  // W side of partition iR + 1
+      unpack(r_next, sp<S>(f->uW), goff(iR + 1), sp<S>(f->vtW), f->sW.get(), iR + 1);
   }
   // interfaces with at least one local side: global i in [iface0, iface0 + ni)
   f->iface0 = std::max(0, p0 - 1);
   const int ilast = std::min(Pg - 2, p0 + P - 1);
   const int ni = std::max(0, ilast - f->iface0 + 1);
   f->ni = ni;
-  f->Kd.alloc((size_t)std::max(ni, 1) * r * r);
-  f->Ed.alloc((size_t)std::max(ni, 1) * r * r);
-  f->Hinv.alloc((size_t)std::max(ni, 1) * r * r);
+  const size_t rr = (size_t)r * r;
+  f->Kd.alloc((size_t)std::max(ni, 1) * rr * w);
+  f->Ed.alloc((size_t)std::max(ni, 1) * rr * w);
+  f->Hinv.alloc((size_t)std::max(ni, 1) * rr * w);
   f->cond.alloc((size_t)std::max(ni, 1) * 2);
   f->degen.alloc((size_t)std::max(ni, 1));
   double mx = 1.0;
   int bad_i = -1;
   double bad_c = 0.0;
   if (ni > 0) {
-    std::vector<IfaceSetupJob> jobs;
+    std::vector<IfaceSetupJobT<S>> jobs;
     for (int q = 0; q < ni; ++q) {
       const int i = f->iface0 + q;
-      IfaceSetupJob j{};
-      j.uTb = f->uT.get() + goff(i) + gsize(i) - k;
+      IfaceSetupJobT<S> j{};
+      j.uTb = sp<S>(f->uT) + goff(i) + gsize(i) - k;
       j.ld_uT = n;
-      j.uWt = f->uW.get() + goff(i + 1);
+      j.uWt = sp<S>(f->uW) + goff(i + 1);
       j.ld_uW = n;
-      j.vtT = f->vtT.get() + (size_t)i * k * r;
-      j.vtW = f->vtW.get() + (size_t)(i + 1) * k * r;
+      j.vtT = sp<S>(f->vtT) + (size_t)i * k * r;
+      j.vtW = sp<S>(f->vtW) + (size_t)(i + 1) * k * r;
       j.sT = f->sT.get() + (size_t)i * r;
       j.sW = f->sW.get() + (size_t)(i + 1) * r;
-      j.K = f->Kd.get() + (size_t)q * r * r;
-      j.E = f->Ed.get() + (size_t)q * r * r;
-      j.Hinv = f->Hinv.get() + (size_t)q * r * r;
+      j.K = sp<S>(f->Kd) + q * rr;
+      j.E = sp<S>(f->Ed) + q * rr;
+      j.Hinv = sp<S>(f->Hinv) + q * rr;
       j.cond = f->cond.get() + 2 * q;
       j.degenerate = f->degen.get() + q;
       jobs.push_back(j);
     }
-    DevBuf<IfaceSetupJob> dj;
+    DevBuf<IfaceSetupJobT<S>> dj;
     upload(c, dj, jobs);
-    launch_iface_setup(c, dj.get(), ni, r, k);
+    launch_iface_setup_t<S>(c, dj.get(), ni, r, k);
     std::vector<double> hc(2 * ni);
     download(c, hc.data(), f->cond.get(), hc.size());
     for (int q = 0; q < ni; ++q) {
@@ -479,53 +520,76 @@ static bool build_lowrank(Fact* f, int r, int* bad_iface, double* bad_cond,
   }
   f->info.max_interface_cond = mx;
   // apply-time jobs
-  f->scT.alloc((size_t)Pg * r * MAX_RHS);
-  f->scW.alloc((size_t)Pg * r * MAX_RHS);
-  f->iface_msg.alloc((size_t)std::max(ni, 1) * 2 * r * MAX_RHS);
-  LRS_CUDA(cudaMemsetAsync(f->scT.get(), 0, sizeof(double) * Pg * r * MAX_RHS, c->stream));
-  LRS_CUDA(cudaMemsetAsync(f->scW.get(), 0, sizeof(double) * Pg * r * MAX_RHS, c->stream));
-  LRS_CUDA(cudaMemsetAsync(f->iface_msg.get(), 0, sizeof(double) * std::max(ni, 1) * 2 * r * MAX_RHS,
-                           c->stream));
+  const size_t scn = (size_t)Pg * r * MAX_RHS, msgn = (size_t)std::max(ni, 1) * 2 * r * MAX_RHS;
+  f->scT.alloc(scn * w);
+  f->scW.alloc(scn * w);
+  f->iface_msg.alloc(msgn * w);
+  LRS_CUDA(cudaMemsetAsync(f->scT.get(), 0, sizeof(S) * scn, c->stream));
+  LRS_CUDA(cudaMemsetAsync(f->scW.get(), 0, sizeof(S) * scn, c->stream));
+  LRS_CUDA(cudaMemsetAsync(f->iface_msg.get(), 0, sizeof(S) * msgn, c->stream));
   f->job_left = f->job_right = -1;
   {
-    std::vector<IfaceApplyJob> jobs;
+    std::vector<IfaceApplyJobT<S>> jobs;
     for (int q = 0; q < ni; ++q) {
       const int i = f->iface0 + q;
-      IfaceApplyJob j{};
-      j.vtT = f->vtT.get() + (size_t)i * k * r;
-      j.vtW = f->vtW.get() + (size_t)(i + 1) * k * r;
+      IfaceApplyJobT<S> j{};
+      j.vtT = sp<S>(f->vtT) + (size_t)i * k * r;
+      j.vtW = sp<S>(f->vtW) + (size_t)(i + 1) * k * r;
       j.sT = f->sT.get() + (size_t)i * r;
       j.sW = f->sW.get() + (size_t)(i + 1) * r;
-      j.K = f->Kd.get() + (size_t)q * r * r;
-      j.E = f->Ed.get() + (size_t)q * r * r;
-      j.Hinv = f->Hinv.get() + (size_t)q * r * r;
+      j.K = sp<S>(f->Kd) + q * rr;
+      j.E = sp<S>(f->Ed) + q * rr;
+      j.Hinv = sp<S>(f->Hinv) + q * rr;
       j.yb_row = goff(i) + gsize(i) - k;
       j.yt_row = goff(i + 1);
-      j.scT = f->scT.get() + (size_t)i * r * MAX_RHS;
-      j.scW = f->scW.get() + (size_t)(i + 1) * r * MAX_RHS;
-      j.msg = f->iface_msg.get() + (size_t)q * 2 * r * MAX_RHS;
+      j.scT = sp<S>(f->scT) + (size_t)i * r * MAX_RHS;
+      j.scW = sp<S>(f->scW) + (size_t)(i + 1) * r * MAX_RHS;
+      j.msg = sp<S>(f->iface_msg) + (size_t)q * 2 * r * MAX_RHS;
       j.has_left = (i >= p0 && i < p0 + P) ? 1 : 0;
       j.has_right = (i + 1 >= p0 && i + 1 < p0 + P) ? 1 : 0;
       if (!j.has_left) f->job_left = q;
       if (!j.has_right) f->job_right = q;
       jobs.push_back(j);
     }
-    upload(c, f->iface_jobs, jobs);
-    f->iface_work.alloc(iface_work_doubles(std::max(ni, 1), r, k));
+    upload_raw(c, f->iface_jobs, jobs);
+    f->iface_work.alloc(iface_work_doubles(std::max(ni, 1), r, k) * w);
   }
   LRS_CUDA(cudaStreamSynchronize(c->stream));
   return true;
+}
+
+}  // namespace
+
+void shard_plan(int64_t P, int size, int rank, int64_t* p_lo, int64_t* p_hi) {
+  *p_lo = (int64_t)rank * P / size;
+  *p_hi = (int64_t)(rank + 1) * P / size;
+}
+
+void dstage(Fact* f, void* x, int64_t ld, int nrhs, bool adjoint, int p_only) {
+  if (f->scalar == LRS_C128) dstage_t(f, static_cast<zc*>(x), ld, nrhs, adjoint, p_only);
+  else dstage_t(f, static_cast<double*>(x), ld, nrhs, adjoint, p_only);
+}
+
+void apply_precond(Fact* f, const void* in, int64_t ldi, void* out, int64_t ldo, int nrhs,
+                   bool block_jacobi) {
+  if (f->scalar == LRS_C128)
+    apply_precond_t(f, static_cast<const zc*>(in), ldi, static_cast<zc*>(out), ldo, nrhs,
+                    block_jacobi);
+  else
+    apply_precond_t(f, static_cast<const double*>(in), ldi, static_cast<double*>(out), ldo, nrhs,
+                    block_jacobi);
 }
 
 // ------------------------------------------------------------------------------------
 // factorize
 // ------------------------------------------------------------------------------------
 Fact* factorize(Ctx* c, Mat* m, const lrs_solver_cfg& cfg, const lrs_comm* comm) {
-  if (m->scalar != LRS_F64)
-    throw LrsError(LRS_ERR_NOT_IMPLEMENTED, "complex128 factorization is not implemented yet");
   std::unique_ptr<Fact> f(new Fact());
   f->ctx = c;
   f->mat = m;
+  f->scalar = m->scalar;
+  f->sw = m->scalar == LRS_C128 ? 2 : 1;
+  const bool cplx = f->scalar == LRS_C128;
   f->variant = cfg.variant;
   if (cfg.variant != LRS_VARIANT_T && cfg.variant != LRS_VARIANT_BJ)
     throw LrsError(LRS_ERR_PARAMETER, "unknown variant");
@@ -541,6 +605,7 @@ Fact* factorize(Ctx* c, Mat* m, const lrs_solver_cfg& cfg, const lrs_comm* comm)
     f->comm = *comm;
   }
   const int G = f->nranks(), rank = f->rank();
+  const int w = f->sw;
   f->Pg = (int)cfg.p;
   f->n = m->n;
   f->k = cfg.k > 0 ? cfg.k : m->k;
@@ -617,12 +682,12 @@ Fact* factorize(Ctx* c, Mat* m, const lrs_solver_cfg& cfg, const lrs_comm* comm)
   upload(c, f->d_T, f->T);
   upload(c, f->d_goff, f->goff);
   upload(c, f->d_rank_pl, f->rank_pl);
-  f->tiles.alloc((size_t)tb * TILE_ELEMS);
+  f->tiles.alloc((size_t)tb * TILE_ELEMS * w);
   f->flags.alloc((size_t)fb);
   f->ticket.alloc(1);
   f->status.alloc(2 * P);
   f->bad.alloc(1);
-  LRS_CUDA(cudaMemsetAsync(f->tiles.get(), 0, sizeof(double) * tb * TILE_ELEMS, c->stream));
+  LRS_CUDA(cudaMemsetAsync(f->tiles.get(), 0, sizeof(double) * tb * TILE_ELEMS * w, c->stream));
   LRS_CUDA(cudaMemsetAsync(f->flags.get(), 0, sizeof(unsigned) * fb, c->stream));
   LRS_CUDA(cudaMemsetAsync(f->status.get(), 0x7f, sizeof(int) * 2 * P, c->stream));
   LRS_CUDA(cudaMemsetAsync(f->bad.get(), 0xff, sizeof(unsigned long long), c->stream));
@@ -640,11 +705,11 @@ Fact* factorize(Ctx* c, Mat* m, const lrs_solver_cfg& cfg, const lrs_comm* comm)
     upload(c, f->d_chunks, f->chunk_start);
     upload(c, f->d_part_first, f->part_first);
     const size_t nch = f->chunk_start.size() - 1;
-    f->partial.alloc(nch * 64 * MAX_RHS);
-    f->persum.alloc((size_t)f->pl_max * 64 * MAX_RHS);
-    f->gather.alloc((size_t)G * f->pl_max * 64 * MAX_RHS);
-    f->dotout.alloc(64 * MAX_RHS);
-    f->xch.alloc((size_t)4 * std::max<int64_t>(1, m->k) * MAX_RHS);
+    f->partial.alloc(nch * 64 * MAX_RHS * w);
+    f->persum.alloc((size_t)f->pl_max * 64 * MAX_RHS * w);
+    f->gather.alloc((size_t)G * f->pl_max * 64 * MAX_RHS * w);
+    f->dotout.alloc(64 * MAX_RHS * w);
+    f->xch.alloc((size_t)4 * std::max<int64_t>(1, m->k) * MAX_RHS * w);
   }
   cudaEvent_t e0, e1, e2, e3;
   LRS_CUDA(cudaEventCreate(&e0));
@@ -661,7 +726,10 @@ Fact* factorize(Ctx* c, Mat* m, const lrs_solver_cfg& cfg, const lrs_comm* comm)
   EvGuard eg{evs};
   LRS_CUDA(cudaEventRecord(e0, c->stream));
   const BandGeom g = f->geom();
-  launch_extract_tiles(c, m, g, f->tiles.get(), f->k, f->row_lo, f->row_hi, f->bad.get());
+  if (cplx)
+    launch_extract_tiles_z(c, m, g, sp<zc>(f->tiles), f->k, f->row_lo, f->row_hi, f->bad.get());
+  else
+    launch_extract_tiles(c, m, g, f->tiles.get(), f->k, f->row_lo, f->row_hi, f->bad.get());
   {
     unsigned long long hb = 0;
     download(c, &hb, f->bad.get(), 1);
@@ -689,7 +757,8 @@ Fact* factorize(Ctx* c, Mat* m, const lrs_solver_cfg& cfg, const lrs_comm* comm)
       omega_future = std::async(std::launch::async, make_omega, f->seed, f->Pg, f->p0,
                                 f->p0 + P, f->k, l0);
   }
-  launch_band_lu(c, g, f->tiles.get(), f->Tmax, f->status.get());
+  if (cplx) launch_band_lu_z(c, g, sp<zc>(f->tiles), f->Tmax, f->status.get());
+  else launch_band_lu(c, g, f->tiles.get(), f->Tmax, f->status.get());
   LRS_CUDA(cudaEventRecord(e1, c->stream));
   {
     std::vector<int> st(2 * P);
@@ -739,7 +808,8 @@ Fact* factorize(Ctx* c, Mat* m, const lrs_solver_cfg& cfg, const lrs_comm* comm)
       try {
         std::vector<double> pre;
         if (attempt == 0 && omega_future.valid()) pre = omega_future.get();
-        ok = build_lowrank(f.get(), r, &bi, &bc, &pre);
+        ok = cplx ? build_lowrank<zc>(f.get(), r, &bi, &bc, &pre)
+                  : build_lowrank<double>(f.get(), r, &bi, &bc, &pre);
       } catch (...) {
         c->in_setup = false;
         throw;
@@ -771,7 +841,7 @@ Fact* factorize(Ctx* c, Mat* m, const lrs_solver_cfg& cfg, const lrs_comm* comm)
   in.nb = NB;
   in.wl = f->wl;
   in.wu = f->wu;
-  in.factor_bytes = f->total_tiles * TILE_ELEMS * (int64_t)sizeof(double);
+  in.factor_bytes = f->total_tiles * TILE_ELEMS * (int64_t)sizeof(double) * w;
   in.rank_collapsed = f->rank_collapsed;
   in.variant = f->variant;
   in.t_lu = elapsed_ms(e0, e1) * 1e-3;
@@ -779,7 +849,8 @@ Fact* factorize(Ctx* c, Mat* m, const lrs_solver_cfg& cfg, const lrs_comm* comm)
   in.t_precond = 0.0;
   in.t_factorize = elapsed_ms(e0, e2) * 1e-3;
   if (in.max_interface_cond == 0.0) in.max_interface_cond = 1.0;
-  // algorithmic work of THIS shard: no-fill band LU flops, apply bytes
+  // algorithmic work of THIS shard: no-fill band LU flops (x4 for
+  // complex arithmetic), apply bytes
   double flops = 0.0, fbytes = 0.0;
   for (int i = 0; i < P; ++i) {
     const int64_t ni = f->size[i];
@@ -791,17 +862,19 @@ Fact* factorize(Ctx* c, Mat* m, const lrs_solver_cfg& cfg, const lrs_comm* comm)
     }
   }
   const double nl = (double)(f->row_hi - f->row_lo);
-  in.lu_flops = (int64_t)flops;
-  in.apply_bytes = (int64_t)(8.0 * (fbytes + 2.0 * nl + 2.0 * nl * f->r));
+  in.lu_flops = (int64_t)(flops * (cplx ? 4.0 : 1.0));
+  in.apply_bytes = (int64_t)(8.0 * w * (fbytes + 2.0 * nl + 2.0 * nl * f->r));
   return f.release();
 }
 
 // ------------------------------------------------------------------------------------
-// Krylov drivers (mirror the oracle's bicgstab / gmres); vector work on the local rows
+// Krylov drivers (mirror the checker's bicgstab / gmres); vector work on the local rows
 // ------------------------------------------------------------------------------------
 namespace {
 
+template <class S>
 struct Work {
+  using H = HT<S>;
   Fact* f;
   Mat* A;
   int64_t n;       // full length (ld of every block)
@@ -817,11 +890,12 @@ struct Work {
   }
   void init() { LRS_CUDA(cudaMallocHost(&hbuf, sizeof(double) * 64 * MAX_RHS * 2)); }
   Ctx* c() const { return f->ctx; }
-  // out[q*nr + j] = X_q[:, j] . Y[:, j] over ALL rows (partition-ordered, any GPU count)
-  void dots(const double* X, int64_t strideX, int nvec, const double* Y, double* out) {
-    const int nout = nvec * nr;
-    launch_multidot_partition(c(), f->chunks(), X, n, strideX, nvec, Y, n, nr, f->partial.get(),
-                              f->persum.get());
+  S* dotout() const { return sp<S>(f->dotout); }
+  // out[q*nr + j] = X_q[:, j]^H Y[:, j] over ALL rows (partition-ordered, any GPU count)
+  void dots(const S* X, int64_t strideX, int nvec, const S* Y, H* out) {
+    const int nout = nvec * nr * SW<S>;  // doubles
+    launch_multidot_partition_t<S>(c(), f->chunks(), X, n, strideX, nvec, Y, n, nr,
+                                   sp<S>(f->partial), sp<S>(f->persum));
     if (f->dist) {
       LRS_CUDA(cudaStreamSynchronize(c()->stream));
       comm_rc(f->comm.allgather(f->comm.user, f->persum.get(), f->gather.get(),
@@ -836,42 +910,45 @@ struct Work {
     LRS_CUDA(cudaMemcpyAsync(hbuf, f->dotout.get(), sizeof(double) * nout, cudaMemcpyDeviceToHost,
                              c()->stream));
     LRS_CUDA(cudaStreamSynchronize(c()->stream));
-    std::memcpy(out, hbuf, sizeof(double) * nout);
+    std::memcpy(static_cast<void*>(out), hbuf, sizeof(double) * nout);
   }
-  void norms(const double* X, double* out) {
-    dots(X, 0, 1, X, out);
-    for (int j = 0; j < nr; ++j) out[j] = std::sqrt(out[j]);
+  void norms(const S* X, double* out) {
+    std::vector<H> d(nr);
+    dots(X, 0, 1, X, d.data());
+    for (int j = 0; j < nr; ++j) out[j] = std::sqrt(hreal(d[j]));
   }
-  void M(const double* in, double* out) {
-    apply_precond(f, in, n, out, n, nr, bj);
+  void M(const S* in, S* out) {
+    apply_precond_t(f, in, n, out, n, nr, bj);
     rep->precond_applications++;
   }
-  void Aop(double* in, double* out) {
+  void Aop(S* in, S* out) {
     halo_exchange(f, in, n, nr);
-    launch_spmv(c(), A, in, n, out, n, nr, 0, nullptr, 0, lo, lo + nl);
+    spmv_s<S>(c(), A, in, n, out, n, nr, 0, nullptr, 0, lo, lo + nl);
     rep->matvecs++;
   }
-  void resid(const double* b, double* x, double* out) {  // out = b - A x
+  void resid(const S* b, S* x, S* out) {  // out = b - A x
     halo_exchange(f, x, n, nr);
-    launch_spmv(c(), A, x, n, out, n, nr, 2, b, n, lo, lo + nl);
+    spmv_s<S>(c(), A, x, n, out, n, nr, 2, b, n, lo, lo + nl);
     rep->matvecs++;
   }
-  void axpby(int op, const ColScal& a, const ColScal& b, const ColScal& act, double* X,
-             const double* Y, const double* Z, double* Wv) {
-    launch_axpby_cols(c(), nl, nr, op, a, b, act, X ? X + lo : nullptr, n, Y ? Y + lo : nullptr, n,
-                      Z ? Z + lo : nullptr, n, Wv ? Wv + lo : nullptr, n);
+  void axpby(int op, const ColScalT<S>& a, const ColScalT<S>& b, const ColScal& act, S* X,
+             const S* Y, const S* Z, S* Wv) {
+    launch_axpby_cols_t<S>(c(), nl, nr, op, a, b, act, X ? X + lo : nullptr, n,
+                           Y ? Y + lo : nullptr, n, Z ? Z + lo : nullptr, n,
+                           Wv ? Wv + lo : nullptr, n);
   }
-  void copy(double* dst, const double* src) { copy_block(c(), dst + lo, n, src + lo, n, nl, nr); }
-  void zero(double* dst) {
+  void copy(S* dst, const S* src) { copy_block(c(), dst + lo, n, src + lo, n, nl, nr); }
+  void zero(S* dst) {
     for (int j = 0; j < nr; ++j)
-      LRS_CUDA(cudaMemsetAsync(dst + lo + (int64_t)j * n, 0, sizeof(double) * nl, c()->stream));
+      LRS_CUDA(cudaMemsetAsync(dst + lo + (int64_t)j * n, 0, sizeof(S) * nl, c()->stream));
   }
   void push(double v) { hist.push_back(v); }
 };
 
-ColScal cs_fill(const std::vector<double>& v) {
-  ColScal s{};
-  for (size_t j = 0; j < v.size() && j < MAX_RHS; ++j) s.v[j] = v[j];
+template <class S>
+ColScalT<S> cs_fill(const std::vector<HT<S>>& v) {
+  ColScalT<S> s{};
+  for (size_t j = 0; j < v.size() && j < MAX_RHS; ++j) s.v[j] = to_dev<S>(v[j]);
   return s;
 }
 ColScal cs_mask(const std::vector<bool>& v) {
@@ -885,23 +962,25 @@ bool any(const std::vector<bool>& v) {
   return false;
 }
 
-void run_bicgstab(Work& w, const double* b, double* x, const lrs_iter_cfg& cfg, bool has_x0,
+template <class S>
+void run_bicgstab(Work<S>& w, const S* b, S* x, const lrs_iter_cfg& cfg, bool has_x0,
                   std::vector<double>& iters, std::vector<bool>& conv, std::vector<bool>& brk) {
+  using H = HT<S>;
   const int nr = w.nr;
   const int64_t n = w.n;
   const size_t blk = (size_t)n * nr;
-  DevBuf<double> buf;
+  DevBuf<S> buf;
   buf.alloc(blk * 9);
-  double* r = buf.get();
-  double* rhat = r + blk;
-  double* p = rhat + blk;
-  double* v = p + blk;
-  double* s = v + blk;
-  double* t = s + blk;
-  double* phat = t + blk;
-  double* shat = phat + blk;
-  double* tmp = shat + blk;
-  const ColScal none{};
+  S* r = buf.get();
+  S* rhat = r + blk;
+  S* p = rhat + blk;
+  S* v = p + blk;
+  S* s = v + blk;
+  S* t = s + blk;
+  S* phat = t + blk;
+  S* shat = phat + blk;
+  S* tmp = shat + blk;
+  const ColScalT<S> none{};
   std::vector<double> bn(nr), bns(nr), tmpv(nr), tmpv2(nr);
   w.norms(b, bn.data());
   for (int j = 0; j < nr; ++j) bns[j] = bn[j] > 0 ? bn[j] : 1.0;
@@ -922,7 +1001,7 @@ void run_bicgstab(Work& w, const double* b, double* x, const lrs_iter_cfg& cfg, 
   }
   w.push(mx);
   w.copy(rhat, r);
-  std::vector<double> rho_prev(nr, 1.0), alpha(nr, 1.0), omega(nr, 1.0), rho(nr), rv(nr);
+  std::vector<H> rho_prev(nr, H(1.0)), alpha(nr, H(1.0)), omega(nr, H(1.0)), rho(nr), rv(nr);
   w.zero(p);
   w.zero(v);
   const bool trace = std::getenv("LRS_TRACE") != nullptr;
@@ -937,7 +1016,7 @@ void run_bicgstab(Work& w, const double* b, double* x, const lrs_iter_cfg& cfg, 
     if (!any(act)) break;
     w.dots(rhat, 0, 1, r, rho.data());
     for (int j = 0; j < nr; ++j)
-      if (act[j] && std::fabs(rho[j]) < cfg.breakdown_eps) {
+      if (act[j] && std::abs(rho[j]) < cfg.breakdown_eps) {
         brk[j] = true;
         act[j] = false;
       }
@@ -945,22 +1024,22 @@ void run_bicgstab(Work& w, const double* b, double* x, const lrs_iter_cfg& cfg, 
     if (it == 1) {
       w.axpby(5, none, none, cs_mask(act), nullptr, r, nullptr, p);
     } else {
-      std::vector<double> beta(nr, 0.0);
+      std::vector<H> beta(nr, H(0.0));
       for (int j = 0; j < nr; ++j) beta[j] = (rho[j] / rho_prev[j]) * (alpha[j] / omega[j]);
-      w.axpby(0, cs_fill(beta), cs_fill(omega), cs_mask(act), p, r, v, nullptr);
+      w.axpby(0, cs_fill<S>(beta), cs_fill<S>(omega), cs_mask(act), p, r, v, nullptr);
     }
     w.M(p, phat);
     w.Aop(phat, v);
     w.dots(rhat, 0, 1, v, rv.data());
     for (int j = 0; j < nr; ++j)
-      if (act[j]) alpha[j] = rho[j] / (rv[j] != 0.0 ? rv[j] : 1.0);
-    w.axpby(1, cs_fill(alpha), none, cs_mask(act), nullptr, r, v, s);
+      if (act[j]) alpha[j] = rho[j] / (rv[j] != H(0.0) ? rv[j] : H(1.0));
+    w.axpby(1, cs_fill<S>(alpha), none, cs_mask(act), nullptr, r, v, s);
     w.norms(s, tmpv.data());
     std::vector<bool> half(nr, false);
     for (int j = 0; j < nr; ++j) half[j] = act[j] && tmpv[j] / bns[j] <= cfg.tol;
     std::vector<bool> hist_cols = act;
     if (any(half)) {
-      w.axpby(3, cs_fill(alpha), none, cs_mask(half), x, phat, nullptr, tmp);
+      w.axpby(3, cs_fill<S>(alpha), none, cs_mask(half), x, phat, nullptr, tmp);
       // true residual of the candidate (columns outside `half` are stale and unused)
       w.resid(b, tmp, t);
       w.norms(t, tmpv2.data());
@@ -983,18 +1062,18 @@ void run_bicgstab(Work& w, const double* b, double* x, const lrs_iter_cfg& cfg, 
     if (!any(act)) break;
     w.M(s, shat);
     w.Aop(shat, t);
-    std::vector<double> tt(nr), ts(nr);
+    std::vector<H> tt(nr), ts(nr);
     w.dots(t, 0, 1, t, tt.data());
     w.dots(t, 0, 1, s, ts.data());
     for (int j = 0; j < nr; ++j)
-      if (act[j]) omega[j] = ts[j] / (tt[j] != 0.0 ? tt[j] : 1.0);
+      if (act[j]) omega[j] = ts[j] / (tt[j] != H(0.0) ? tt[j] : H(1.0));
     for (int j = 0; j < nr; ++j)
-      if (act[j] && std::fabs(omega[j]) < cfg.breakdown_eps) {
+      if (act[j] && std::abs(omega[j]) < cfg.breakdown_eps) {
         brk[j] = true;
         act[j] = false;
       }
-    w.axpby(2, cs_fill(alpha), cs_fill(omega), cs_mask(act), x, phat, shat, nullptr);
-    w.axpby(1, cs_fill(omega), none, cs_mask(act), nullptr, s, t, r);
+    w.axpby(2, cs_fill<S>(alpha), cs_fill<S>(omega), cs_mask(act), x, phat, shat, nullptr);
+    w.axpby(1, cs_fill<S>(omega), none, cs_mask(act), nullptr, s, t, r);
     w.norms(r, tmpv.data());
     std::vector<bool> full(nr, false);
     for (int j = 0; j < nr; ++j) full[j] = act[j] && tmpv[j] / bns[j] <= cfg.tol;
@@ -1018,44 +1097,48 @@ void run_bicgstab(Work& w, const double* b, double* x, const lrs_iter_cfg& cfg, 
   }
 }
 
-void givens(double a, double b, double* c, double* s, double* d) {
-  if (b == 0.0) {
+// Givens rotation zeroing b against a: c real, c a + s b = d, -conj(s) a + c b = 0.
+template <class H>
+void givens(H a, H b, double* c, H* s, H* d) {
+  if (b == H(0.0)) {
     *c = 1.0;
-    *s = 0.0;
+    *s = H(0.0);
     *d = a;
     return;
   }
-  if (a == 0.0) {
+  if (a == H(0.0)) {
     *c = 0.0;
-    *s = b > 0 ? 1.0 : -1.0;
-    *d = std::fabs(b);
+    *s = hconj(b) / std::abs(b);
+    *d = H(std::abs(b));
     return;
   }
-  const double na = std::fabs(a), nb = std::fabs(b);
+  const double na = std::abs(a), nb = std::abs(b);
   const double dd = std::hypot(na, nb);
-  const double sa = a / na;
+  const H sa = a / na;
   *c = na / dd;
-  *s = sa * b / dd;
+  *s = sa * hconj(b) / dd;
   *d = sa * dd;
 }
 
-void run_gmres(Work& w, const double* b, double* x, const lrs_iter_cfg& cfg, bool has_x0,
+template <class S>
+void run_gmres(Work<S>& w, const S* b, S* x, const lrs_iter_cfg& cfg, bool has_x0,
                std::vector<double>& iters_out, std::vector<bool>& conv) {
+  using H = HT<S>;
   const int nr = w.nr;
   const int64_t n = w.n;
   const int m = std::max(1, (int)cfg.restart);
   if (m + 1 > 64) throw LrsError(LRS_ERR_PARAMETER, "GMRES restart must be <= 63");
   Ctx* c = w.c();
   const size_t blk = (size_t)n * nr;
-  DevBuf<double> buf;
+  DevBuf<S> buf;
   buf.alloc(blk * (2 * (size_t)m + 3));
-  double* V = buf.get();               // (m+1) blocks
-  double* Z = V + blk * (m + 1);       // m blocks
-  double* wv = Z + blk * m;
-  double* r = wv + blk;
-  DevBuf<double> ydev;
+  S* V = buf.get();               // (m+1) blocks
+  S* Z = V + blk * (m + 1);       // m blocks
+  S* wv = Z + blk * m;
+  S* r = wv + blk;
+  DevBuf<S> ydev;
   ydev.alloc((size_t)(m + 1) * MAX_RHS);
-  const ColScal none{};
+  const ColScalT<S> none{};
   std::vector<double> bn(nr), bns(nr), beta(nr);
   w.norms(b, bn.data());
   for (int j = 0; j < nr; ++j) bns[j] = bn[j] > 0 ? bn[j] : 1.0;
@@ -1075,57 +1158,60 @@ void run_gmres(Work& w, const double* b, double* x, const lrs_iter_cfg& cfg, boo
   }
   w.push(mx);
   const std::vector<bool> all(nr, true);
-  std::vector<double> h((m + 1) * nr), h2((m + 1) * nr), hn(nr);
+  std::vector<H> h((m + 1) * nr), h2((m + 1) * nr);
+  std::vector<double> hn(nr);
   while (true) {
     std::vector<bool> act(nr);
     for (int j = 0; j < nr; ++j) act[j] = !conv[j] && iters[j] < cfg.max_iters;
     if (!any(act)) break;
-    std::vector<double> inv(nr);
-    for (int j = 0; j < nr; ++j) inv[j] = 1.0 / (beta[j] > 0 ? beta[j] : 1.0);
-    w.axpby(4, cs_fill(inv), none, cs_mask(all), nullptr, r, nullptr, V);
+    std::vector<H> inv(nr);
+    for (int j = 0; j < nr; ++j) inv[j] = H(1.0 / (beta[j] > 0 ? beta[j] : 1.0));
+    w.axpby(4, cs_fill<S>(inv), none, cs_mask(all), nullptr, r, nullptr, V);
     // per column Hessenberg (after rotations) R[row + col*(m+1)], g, rotations
-    std::vector<std::vector<double>> R(nr, std::vector<double>((size_t)(m + 1) * m, 0.0));
-    std::vector<std::vector<double>> g(nr, std::vector<double>(m + 1, 0.0));
-    std::vector<std::vector<double>> csv(nr, std::vector<double>(m, 0.0)), snv(nr, std::vector<double>(m, 0.0));
-    for (int j = 0; j < nr; ++j) g[j][0] = beta[j];
+    std::vector<std::vector<H>> R(nr, std::vector<H>((size_t)(m + 1) * m, H(0.0)));
+    std::vector<std::vector<H>> g(nr, std::vector<H>(m + 1, H(0.0)));
+    std::vector<std::vector<double>> csv(nr, std::vector<double>(m, 0.0));
+    std::vector<std::vector<H>> snv(nr, std::vector<H>(m, H(0.0)));
+    for (int j = 0; j < nr; ++j) g[j][0] = H(beta[j]);
     std::vector<bool> inner = act;
     std::vector<int> steps(nr, 0);
     for (int jj = 0; jj < m; ++jj) {
       if (!any(inner)) break;
-      double* Vj = V + blk * jj;
-      double* Zj = Z + blk * jj;
+      S* Vj = V + blk * jj;
+      S* Zj = Z + blk * jj;
       w.M(Vj, Zj);
       w.Aop(Zj, wv);
       // CGS2 (the projections stay on the device in dotout and feed the update directly)
       w.dots(V, (int64_t)blk, jj + 1, wv, h.data());
-      launch_multi_axpy_signed(c, w.nl, nr, V + w.lo, n, (int64_t)blk, jj + 1,
-                               w.f->dotout.get(), -1.0, wv + w.lo, n);
+      launch_multi_axpy_t<S>(c, w.nl, nr, V + w.lo, n, (int64_t)blk, jj + 1, w.dotout(), -1.0,
+                             wv + w.lo, n);
       w.dots(V, (int64_t)blk, jj + 1, wv, h2.data());
-      launch_multi_axpy_signed(c, w.nl, nr, V + w.lo, n, (int64_t)blk, jj + 1,
-                               w.f->dotout.get(), -1.0, wv + w.lo, n);
+      launch_multi_axpy_t<S>(c, w.nl, nr, V + w.lo, n, (int64_t)blk, jj + 1, w.dotout(), -1.0,
+                             wv + w.lo, n);
       w.norms(wv, hn.data());
       for (int q = 0; q < (jj + 1) * nr; ++q) h[q] += h2[q];
-      std::vector<double> invn(nr);
-      for (int j = 0; j < nr; ++j) invn[j] = 1.0 / (hn[j] > 0 ? hn[j] : 1.0);
-      w.axpby(4, cs_fill(invn), none, cs_mask(all), nullptr, wv, nullptr, V + blk * (jj + 1));
+      std::vector<H> invn(nr);
+      for (int j = 0; j < nr; ++j) invn[j] = H(1.0 / (hn[j] > 0 ? hn[j] : 1.0));
+      w.axpby(4, cs_fill<S>(invn), none, cs_mask(all), nullptr, wv, nullptr, V + blk * (jj + 1));
       mx = 0;
       for (int j = 0; j < nr; ++j) {
         if (!inner[j]) continue;
-        std::vector<double> col(m + 1, 0.0);
+        std::vector<H> col(m + 1, H(0.0));
         for (int q = 0; q <= jj; ++q) col[q] = h[q * nr + j];
-        col[jj + 1] = hn[j];
+        col[jj + 1] = H(hn[j]);
         for (int q = 0; q < jj; ++q) {
-          const double t = csv[j][q] * col[q] + snv[j][q] * col[q + 1];
-          col[q + 1] = -snv[j][q] * col[q] + csv[j][q] * col[q + 1];
+          const H t = csv[j][q] * col[q] + snv[j][q] * col[q + 1];
+          col[q + 1] = -hconj(snv[j][q]) * col[q] + csv[j][q] * col[q + 1];
           col[q] = t;
         }
-        double cc, ss, d;
-        givens(col[jj], col[jj + 1], &cc, &ss, &d);
+        double cc;
+        H ss, d;
+        givens<H>(col[jj], col[jj + 1], &cc, &ss, &d);
         csv[j][jj] = cc;
         snv[j][jj] = ss;
         col[jj] = d;
-        col[jj + 1] = 0.0;
-        g[j][jj + 1] = -ss * g[j][jj];
+        col[jj + 1] = H(0.0);
+        g[j][jj + 1] = -hconj(ss) * g[j][jj];
         g[j][jj] = cc * g[j][jj];
         for (int q = 0; q <= jj; ++q) R[j][q + (size_t)jj * (m + 1)] = col[q];
         steps[j]++;
@@ -1133,7 +1219,7 @@ void run_gmres(Work& w, const double* b, double* x, const lrs_iter_cfg& cfg, boo
       }
       for (int j = 0; j < nr; ++j) {
         if (!inner[j]) continue;
-        const double est = std::fabs(g[j][jj + 1]) / bns[j];
+        const double est = std::abs(g[j][jj + 1]) / bns[j];
         mx = std::max(mx, est);
         if (!(est > cfg.tol) || iters[j] >= cfg.max_iters) inner[j] = false;
       }
@@ -1144,21 +1230,21 @@ void run_gmres(Work& w, const double* b, double* x, const lrs_iter_cfg& cfg, boo
     for (int j = 0; j < nr; ++j)
       if (act[j]) kmax = std::max(kmax, steps[j]);
     if (kmax > 0) {
-      std::vector<double> y((size_t)kmax * nr, 0.0);
+      std::vector<H> y((size_t)kmax * nr, H(0.0));
       for (int j = 0; j < nr; ++j) {
         if (!act[j] || steps[j] == 0) continue;
         const int kk = steps[j];
-        std::vector<double> yy(kk);
+        std::vector<H> yy(kk);
         for (int q = kk - 1; q >= 0; --q) {
-          double s = g[j][q];
+          H s = g[j][q];
           for (int e = q + 1; e < kk; ++e) s -= R[j][q + (size_t)e * (m + 1)] * yy[e];
           yy[q] = s / R[j][q + (size_t)q * (m + 1)];
         }
         for (int q = 0; q < kk; ++q) y[(size_t)q * nr + j] = yy[q];
       }
-      c->stage_h2d(ydev.get(), y.data(), sizeof(double) * y.size());
-      launch_multi_axpy_signed(c, w.nl, nr, Z + w.lo, n, (int64_t)blk, kmax, ydev.get(), 1.0,
-                               x + w.lo, n);
+      c->stage_h2d(ydev.get(), y.data(), sizeof(H) * y.size());
+      launch_multi_axpy_t<S>(c, w.nl, nr, Z + w.lo, n, (int64_t)blk, kmax, ydev.get(), 1.0,
+                             x + w.lo, n);
       LRS_CUDA(cudaStreamSynchronize(c->stream));
     }
     w.resid(b, x, r);
@@ -1173,13 +1259,10 @@ void run_gmres(Work& w, const double* b, double* x, const lrs_iter_cfg& cfg, boo
   for (int j = 0; j < nr; ++j) iters_out[j] = (double)iters[j];
 }
 
-}  // namespace
-
-void solve(Fact* f, Mat* a, const double* b, int64_t ldb, double* x, int64_t ldx, int nrhs,
-           const lrs_iter_cfg& cfg, lrs_report* rep) {
+template <class S>
+void solve_t(Fact* f, Mat* a, const S* b, int64_t ldb, S* x, int64_t ldx, int nrhs,
+             const lrs_iter_cfg& cfg, lrs_report* rep) {
   Ctx* c = f->ctx;
-  if (a->n != f->n) throw LrsError(LRS_ERR_DIMENSION, "solve: matrix does not match factorization");
-  if (cfg.tol <= 0 || cfg.max_iters < 1) throw LrsError(LRS_ERR_PARAMETER, "tol > 0 and max_iters >= 1");
   const int64_t m0[3] = {f->ledger_msgs[0], f->ledger_msgs[1], f->ledger_msgs[2]};
   const int64_t s0[3] = {f->ledger_sc[0], f->ledger_sc[1], f->ledger_sc[2]};
   lrs_report& R = *rep;
@@ -1197,7 +1280,7 @@ void solve(Fact* f, Mat* a, const double* b, int64_t ldb, double* x, int64_t ldx
   std::vector<double> hist_all;
   for (int c0 = 0; c0 < nrhs; c0 += MAX_RHS) {
     const int nr = std::min(MAX_RHS, nrhs - c0);
-    Work w;
+    Work<S> w;
     w.f = f;
     w.A = a;
     w.n = n;
@@ -1208,14 +1291,14 @@ void solve(Fact* f, Mat* a, const double* b, int64_t ldb, double* x, int64_t ldx
     w.rep = &R;
     w.init();
     // full-length device copies (ld = n) of this column batch; local rows only
-    DevBuf<double> bb, xx;
+    DevBuf<S> bb, xx;
     bb.alloc((size_t)n * nr);
     xx.alloc((size_t)n * nr);
     copy_block(c, bb.get() + lo, n, b + (int64_t)c0 * ldb + lo, ldb, nl, nr);
     const bool has_x0 = cfg.x0 != nullptr;
     if (has_x0)
-      copy_block(c, xx.get() + lo, n, static_cast<const double*>(cfg.x0) + (int64_t)c0 * ldx + lo,
-                 ldx, nl, nr);
+      copy_block(c, xx.get() + lo, n, static_cast<const S*>(cfg.x0) + (int64_t)c0 * ldx + lo, ldx,
+                 nl, nr);
     std::vector<double> iters;
     std::vector<bool> conv, brk;
     if (cfg.method == LRS_BICGSTAB) {
@@ -1235,10 +1318,10 @@ void solve(Fact* f, Mat* a, const double* b, int64_t ldb, double* x, int64_t ldx
     {
       std::vector<double> bn(nr), rn(nr);
       w.norms(bb.get(), bn.data());
-      DevBuf<double> tmp;
+      DevBuf<S> tmp;
       tmp.alloc((size_t)n * nr);
       halo_exchange(f, xx.get(), n, nr);
-      launch_spmv(c, a, xx.get(), n, tmp.get(), n, nr, 2, bb.get(), n, lo, lo + nl);
+      spmv_s<S>(c, a, xx.get(), n, tmp.get(), n, nr, 2, bb.get(), n, lo, lo + nl);
       w.norms(tmp.get(), rn.data());
       for (int j = 0; j < nr; ++j) worst = std::max(worst, rn[j] / (bn[j] > 0 ? bn[j] : 1.0));
     }
@@ -1261,6 +1344,20 @@ void solve(Fact* f, Mat* a, const double* b, int64_t ldb, double* x, int64_t ldx
     std::memcpy(R.history, hist_all.data(), sizeof(double) * R.history_len);
   }
   if (any_brk) throw LrsError(LRS_ERR_BREAKDOWN, "BiCGStab stagnation detected (SF)");
+}
+
+}  // namespace
+
+void solve(Fact* f, Mat* a, const void* b, int64_t ldb, void* x, int64_t ldx, int nrhs,
+           const lrs_iter_cfg& cfg, lrs_report* rep) {
+  if (a->n != f->n) throw LrsError(LRS_ERR_DIMENSION, "solve: matrix does not match factorization");
+  if (a->scalar != f->scalar)
+    throw LrsError(LRS_ERR_PARAMETER, "solve: matrix scalar type does not match factorization");
+  if (cfg.tol <= 0 || cfg.max_iters < 1) throw LrsError(LRS_ERR_PARAMETER, "tol > 0 and max_iters >= 1");
+  if (f->scalar == LRS_C128)
+    solve_t(f, a, static_cast<const zc*>(b), ldb, static_cast<zc*>(x), ldx, nrhs, cfg, rep);
+  else
+    solve_t(f, a, static_cast<const double*>(b), ldb, static_cast<double*>(x), ldx, nrhs, cfg, rep);
 }
 
 }  // namespace lrs
