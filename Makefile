@@ -49,3 +49,14 @@ clean:
 	rm -rf build $(PKG)/*.so tests/cpp/test_api
 
 .PHONY: all gen cuda api cpptest clean
+
+# Experiment builds: make variant V=<name> DEFS="-DLRS_GEMM_SPLIT=1" ->
+# build/var_<name>/liblrspike_cuda.so (select with LRS_LIB=...).
+VOBJ = $(patsubst $(PKG)/csrc/%.cu,build/var_$(V)/%.o,$(CU_SRC))
+build/var_$(V)/%.o: $(PKG)/csrc/%.cu $(CU_HDR)
+	@mkdir -p build/var_$(V)
+	$(NVCC) $(NVFLAGS) $(DEFS) -c -o $@ $< 2> build/var_$(V)/$*.ptxas.log || (cat build/var_$(V)/$*.ptxas.log; false)
+build/var_$(V)/liblrspike_cuda.so: $(VOBJ)
+	$(NVCC) $(ARCH) -shared -Xcompiler -fPIC -o $@ $(VOBJ) -lcudart
+variant: build/var_$(V)/liblrspike_cuda.so
+.PHONY: variant

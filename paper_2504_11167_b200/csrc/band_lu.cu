@@ -171,17 +171,26 @@ __global__ void __launch_bounds__(DIAG_THREADS, 1) lu_diag_kernel(BandGeom g, do
 
 // ---------------------------------------------------------------------------------------
 // DMMA tile GEMM: C(128x128) = / -= A(128x128) * B(128x128), all tiles column-major.
-// 256 threads = 8 warps as 2 (M) x 4 (N); each warp owns 64 x 32 outputs = 8 x 4
-// DMMA.8x8x4 accumulators.  K is streamed in 4 chunks of 32 via cp.async, double
-// buffered.  Shared layouts are padded so fragment loads are bank-conflict free:
-// As[k][m] with row stride 132, Bs[n][k] with row stride 36.
+// A tile update is split over GEMM_SPLIT CTAs by columns (CN = 128 / GEMM_SPLIT each);
+// every warp owns 64 x 32 outputs = 8 x 4 DMMA.8x8x4 accumulators, the warps of a CTA
+// laid out 2 (M) x (CN / 32) (N).  With GEMM_SPLIT = 2 two CTAs share an SM, so one's
+// C load / store overlaps the other's DMMA stream.  K is streamed in 4 chunks of 32 via
+// cp.async, double buffered.  Shared layouts are padded so fragment loads are bank-
+// conflict free: As[k][m] with row stride 132, Bs[n][k] with row stride 36.
 // ---------------------------------------------------------------------------------------
-constexpr int GEMM_THREADS = 256;
+#ifndef LRS_GEMM_SPLIT
+#define LRS_GEMM_SPLIT 2
+#endif
+constexpr int GEMM_SPLIT = LRS_GEMM_SPLIT;
+static_assert(GEMM_SPLIT == 1 || GEMM_SPLIT == 2, "column split");
+constexpr int GEMM_THREADS = 256 / GEMM_SPLIT;
+constexpr int GEMM_CN = NB / GEMM_SPLIT;     // tile columns per CTA
+constexpr int GEMM_WN = GEMM_CN / 32;        // warps along N
 constexpr int KC = 32;
 constexpr int AS_LD = NB + 4;   // 132
 constexpr int BS_LD = KC + 4;   // 36
 constexpr int AS_STAGE = KC * AS_LD;
-constexpr int BS_STAGE = NB * BS_LD;
+constexpr int BS_STAGE = GEMM_CN * BS_LD;
 #ifndef LRS_GEMM_STAGES
 #define LRS_GEMM_STAGES 2  // measured: 2 stages 0.328 s vs 3 stages 0.363 s (c2 LU)
 #endif
@@ -189,16 +198,26 @@ constexpr int GEMM_STAGES = LRS_GEMM_STAGES;
 static_assert(GEMM_STAGES >= 2 && GEMM_STAGES <= 3, "pipeline depth");
 constexpr size_t GEMM_SMEM = sizeof(double) * GEMM_STAGES * (AS_STAGE + BS_STAGE);
 
+#ifndef LRS_C_EPILOGUE
+#define LRS_C_EPILOGUE 1  // measured c2 LU 0.308 s vs 0.315 s with the C preload
+#endif
+
 constexpr int MASK_NONE = 0, MASK_UNIT_LOWER = 1, MASK_UPPER = 2;
 
 __device__ __forceinline__ void gemm_load_chunk(const double* __restrict__ A,
                                                 const double* __restrict__ B, double* As,
                                                 double* Bs, int kc, int tid) {
+  constexpr int QA = KC * NB / 2 / GEMM_THREADS;       // 16-byte copies per thread (A)
+  constexpr int QB = GEMM_CN * KC / 2 / GEMM_THREADS;  // (B)
 #pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    const int idx = tid + GEMM_THREADS * q;  // 0..2047
+  for (int q = 0; q < QA; ++q) {
+    const int idx = tid + GEMM_THREADS * q;
     const int k = idx >> 6, m2 = (idx & 63) * 2;
     cp_async16(As + k * AS_LD + m2, A + (int64_t)(kc * KC + k) * NB + m2);
+  }
+#pragma unroll
+  for (int q = 0; q < QB; ++q) {
+    const int idx = tid + GEMM_THREADS * q;
     const int nn = idx >> 4, k2 = (idx & 15) * 2;
     cp_async16(Bs + nn * BS_LD + k2, B + (int64_t)nn * NB + kc * KC + k2);
   }
@@ -208,31 +227,39 @@ __device__ __forceinline__ void gemm_load_chunk(const double* __restrict__ A,
 // The DMMA computes the transposed product C^T = B^T A^T: the B tile supplies the
 // "A" fragments and the A tile the "B" fragments, so each lane's accumulator pair
 // (c0, c1) is C[m][n], C[m+1][n] -- adjacent in the column-major tile -- and the C
-// tile moves as 16-byte vectors.  Three cp.async stages (212 KB of shared memory).
+// tile moves as 16-byte vectors.  MODE 1 accumulates -C + A B from the negated C and
+// stores the negation: bitwise the same as C - A B (round-to-nearest is sign
+// symmetric) without negating every A fragment.  h: the CTA's column block.
 template <int MODE, int maskA, int maskB>  // MODE 0: C = A*B, 1: C -= A*B
 __device__ __forceinline__ void tile_gemm(const double* A, const double* B, double* C, double* sm,
-                                          int* piv_status, int col0) {
+                                          int* piv_status, int col0, int h) {
   double* As = sm;
   double* Bs = sm + GEMM_STAGES * AS_STAGE;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int wm = w & 1, wn = w >> 1;
   const int g = lane >> 2, t = lane & 3;
+  const int n0 = h * GEMM_CN;
+  B += (int64_t)n0 * NB;
+  C += (int64_t)n0 * NB;
   constexpr int NK = NB / KC;
   double acc[4][8][2];  // [n tile j][m tile i][pair]: C[m0 + 2t + e][n0 + g]
   constexpr int DIST = GEMM_STAGES - 1;  // prefetch distance in chunks
 #pragma unroll
   for (int s = 0; s < DIST; ++s) gemm_load_chunk(A, B, As + s * AS_STAGE, Bs + s * BS_STAGE, s, tid);
-  // MODE 1 accumulates straight into C (C + sum (-A) B): the C fragments load while
-  // the first operand chunks are in flight and the epilogue is a plain store.
+  // MODE 1 (C_EPI = 0) accumulates straight into C: the C fragments load while the first
+  // operand chunks are in flight and the epilogue is a plain store.  C_EPI = 1: the TMA
+  // engine prefetches the C block into L2 now and the epilogue forms C - A B.
+  constexpr bool C_EPI = MODE == 1 && LRS_C_EPILOGUE;
+  if (C_EPI && tid == 0) bulk_prefetch_l2(C, sizeof(double) * NB * GEMM_CN);
 #pragma unroll
   for (int j = 0; j < 4; ++j)
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-      if (MODE == 1) {
+      if (MODE == 1 && !C_EPI) {
         const double2 v = *reinterpret_cast<const double2*>(
             C + (int64_t)(32 * wn + 8 * j + g) * NB + 64 * wm + 8 * i + 2 * t);
-        acc[j][i][0] = v.x;
-        acc[j][i][1] = v.y;
+        acc[j][i][0] = -v.x;
+        acc[j][i][1] = -v.y;
       } else {
         acc[j][i][0] = acc[j][i][1] = 0.0;
       }
@@ -262,13 +289,13 @@ __device__ __forceinline__ void tile_gemm(const double* A, const double* B, doub
         const int m = 64 * wm + 8 * i + g;
         double v = as[kk * AS_LD + m];
         if (maskA == MASK_UNIT_LOWER) v = m > kg ? v : (m == kg ? 1.0 : 0.0);
-        fa[i] = MODE == 1 ? -v : v;
+        fa[i] = v;
       }
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {  // B[k][n], n = 32 wn + 8 j + g
+      for (int j = 0; j < 4; ++j) {  // B[k][n], n = 32 wn + 8 j + g (tile column n0 + n)
         const int nn = 32 * wn + 8 * j + g;
         double v = bs[nn * BS_LD + kk];
-        if (maskB == MASK_UPPER) v = kg <= nn ? v : 0.0;
+        if (maskB == MASK_UPPER) v = kg <= n0 + nn ? v : 0.0;
         fb[j] = v;
       }
 #pragma unroll
@@ -285,19 +312,26 @@ __device__ __forceinline__ void tile_gemm(const double* A, const double* B, doub
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       double2 v;
-      v.x = acc[j][i][0];
-      v.y = acc[j][i][1];
-      *reinterpret_cast<double2*>(C + (int64_t)nn * NB + 64 * wm + 8 * i + 2 * t) = v;
+      double2* cp = reinterpret_cast<double2*>(C + (int64_t)nn * NB + 64 * wm + 8 * i + 2 * t);
+      if (C_EPI) {
+        v = *cp;
+        v.x -= acc[j][i][0];
+        v.y -= acc[j][i][1];
+      } else {
+        v.x = MODE == 1 ? -acc[j][i][0] : acc[j][i][0];
+        v.y = MODE == 1 ? -acc[j][i][1] : acc[j][i][1];
+      }
+      *cp = v;
       if (MODE == 0 && piv_status && (fabs(v.x) > 1.0 || fabs(v.y) > 1.0))
-        bad_col = min(bad_col, col0 + nn);
+        bad_col = min(bad_col, col0 + n0 + nn);
     }
   }
   if (piv_status && bad_col != 0x7fffffff) atomicMin(piv_status, bad_col);
 }
 
 template <int KIND>
-__global__ void __launch_bounds__(GEMM_THREADS, 1) lu_gemm_kernel(BandGeom g, double* tiles, int K,
-                                                                  int* status) {
+__global__ void __launch_bounds__(GEMM_THREADS, GEMM_SPLIT) lu_gemm_kernel(BandGeom g, double* tiles,
+                                                                           int K, int* status) {
   extern __shared__ double sm[];
   const int p = blockIdx.y;
   const int T = g.T[p];
@@ -306,25 +340,26 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) lu_gemm_kernel(BandGeom g, do
   auto tile = [&](int I, int J) -> double* {
     return tiles + (base + (int64_t)I * g.W + (J - I + g.wl)) * TILE_ELEMS;
   };
-  const int x = blockIdx.x;
+  const int x = blockIdx.x / GEMM_SPLIT, h = blockIdx.x % GEMM_SPLIT;
   if (KIND == 0) {
     if (x < g.wl) {
       const int I = K + 1 + x;
       if (I >= T) return;
       // L_IK = A_IK * inv(U_KK); |l| > 1 means dgbtrf would have interchanged rows
       tile_gemm<0, MASK_NONE, MASK_UPPER>(tile(I, K), tile(K, K), tile(I, K), sm, &status[2 * p],
-                   K * NB);
+                                          K * NB, h);
     } else {
       const int J = K + 1 + (x - g.wl);
       if (J >= T) return;
-      tile_gemm<0, MASK_UNIT_LOWER, MASK_NONE>(tile(K, K), tile(K, J), tile(K, J), sm, nullptr, 0);
+      tile_gemm<0, MASK_UNIT_LOWER, MASK_NONE>(tile(K, K), tile(K, J), tile(K, J), sm, nullptr, 0,
+                                               h);
     }
   } else if (KIND == 1) {
     // trailing update away from the next pivot row/column: I, J >= K + 2
     const int I = K + 2 + x / (g.wu - 1);
     const int J = K + 2 + x % (g.wu - 1);
     if (I >= T || J >= T) return;
-    tile_gemm<1, MASK_NONE, MASK_NONE>(tile(I, K), tile(K, J), tile(I, J), sm, nullptr, 0);
+    tile_gemm<1, MASK_NONE, MASK_NONE>(tile(I, K), tile(K, J), tile(I, J), sm, nullptr, 0, h);
   } else {
     // look-ahead part of the trailing update: column K+1 (I = K+1..K+wl) and row K+1
     // (J = K+2..K+wu), i.e. everything diag/panel of step K+1 needs
@@ -337,7 +372,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) lu_gemm_kernel(BandGeom g, do
       J = K + 2 + (x - g.wl);
     }
     if (I >= T || J >= T) return;
-    tile_gemm<1, MASK_NONE, MASK_NONE>(tile(I, K), tile(K, J), tile(I, J), sm, nullptr, 0);
+    tile_gemm<1, MASK_NONE, MASK_NONE>(tile(I, K), tile(K, J), tile(I, J), sm, nullptr, 0, h);
   }
 }
 
@@ -363,13 +398,15 @@ static void real_diag(Ctx* c, cudaStream_t s, const BandGeom& g, void* tiles, in
 static void real_gemm(Ctx* c, cudaStream_t s, const BandGeom& g, void* tiles, int K, int* status,
                       int kind) {
   double* t = static_cast<double*>(tiles);
+  constexpr int S = GEMM_SPLIT;
   if (kind == 0)
-    lu_gemm_kernel<0><<<dim3(g.wl + g.wu, g.P), GEMM_THREADS, GEMM_SMEM, s>>>(g, t, K, status);
+    lu_gemm_kernel<0><<<dim3(S * (g.wl + g.wu), g.P), GEMM_THREADS, GEMM_SMEM, s>>>(g, t, K, status);
   else if (kind == 1)
-    lu_gemm_kernel<1><<<dim3((g.wl - 1) * (g.wu - 1), g.P), GEMM_THREADS, GEMM_SMEM, s>>>(g, t, K,
-                                                                                          status);
+    lu_gemm_kernel<1><<<dim3(S * (g.wl - 1) * (g.wu - 1), g.P), GEMM_THREADS, GEMM_SMEM, s>>>(
+        g, t, K, status);
   else
-    lu_gemm_kernel<2><<<dim3(g.wl + g.wu - 1, g.P), GEMM_THREADS, GEMM_SMEM, s>>>(g, t, K, status);
+    lu_gemm_kernel<2><<<dim3(S * (g.wl + g.wu - 1), g.P), GEMM_THREADS, GEMM_SMEM, s>>>(g, t, K,
+                                                                                       status);
 }
 
 static void lu_diag_panel(Ctx* c, cudaStream_t s, const BandGeom& g, void* tiles, int K,

@@ -155,6 +155,7 @@ lrs_status lrs_ctx_create(int device, void* stream, lrs_ctx** out) {
     pool_stream_open(c->stream);
     c->stage_cap = size_t(8) << 20;
     LRS_CUDA(cudaMallocHost(reinterpret_cast<void**>(&c->stage), c->stage_cap));
+    LRS_CUDA(cudaMallocHost(reinterpret_cast<void**>(&c->dots_host), Ctx::DOTS_HOST_BYTES));
   });
   if (s == LRS_OK) *out = c.release();
   return s;
@@ -167,6 +168,7 @@ void lrs_ctx_destroy(lrs_ctx* c) {
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
   pool_stream_retire(c->stream);
   if (c->stage) cudaFreeHost(c->stage);
+  if (c->dots_host) cudaFreeHost(c->dots_host);
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
   if (c->own_stream) cudaStreamDestroy(c->stream);

@@ -883,12 +883,8 @@ struct Work {
   bool bj;
   lrs_report* rep;
   std::vector<double> hist;
-  double* hbuf = nullptr;  // pinned staging
-  Work() = default;
-  ~Work() {
-    if (hbuf) cudaFreeHost(hbuf);
-  }
-  void init() { LRS_CUDA(cudaMallocHost(&hbuf, sizeof(double) * 64 * MAX_RHS * 2)); }
+  double* hbuf = nullptr;  // pinned landing buffer of the dot products (Ctx-owned)
+  void init() { hbuf = f->ctx->dots_host; }
   Ctx* c() const { return f->ctx; }
   S* dotout() const { return sp<S>(f->dotout); }
   // out[q*nr + j] = X_q[:, j]^H Y[:, j] over ALL rows (partition-ordered, any GPU count)
