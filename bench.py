@@ -300,11 +300,11 @@ def run_ours(args):
     # ---- roofline: dominant kernel = band-LU trailing update (DMMA, FP64 tensor core)
     info = infos[-1]
     upd_ms, upd_n = kt["lu_update"]
-    lu_upd_flops = 0.0  # 2 * sum_j min(kl, .) * min(ku, .) per factorization (no-fill)
-    for s in _partition_sizes(cfg.matrix.n, cfg.P):
-        j = np.arange(s, dtype=np.float64)
-        rem = s - 1 - j
-        lu_upd_flops += float(np.sum(2.0 * np.minimum(info["kl"], rem) * np.minimum(info["ku"], rem)))
+    # algorithmic (no-fill) flops of the bulk trailing update lu_gemm<1>: for pivot column
+    # j (row tile K = j / 128) the rank-1 update of rows and columns >= 128 (K + 2); the
+    # look-ahead row/column K + 1 is critical-path work timed with the panel
+    lu_upd_flops = sum(_rest_update_flops(s, info["kl"], info["ku"], info["nb"])
+                       for s in _partition_sizes(cfg.matrix.n, cfg.P))
     per_launch_flops = lu_upd_flops * args.steps / max(upd_n, 1)
     avg_launch_s = upd_ms / max(upd_n, 1) / 1e3
     achieved_tf = per_launch_flops / avg_launch_s / 1e12 if upd_n else 0.0
@@ -365,6 +365,14 @@ def run_ours(args):
         torch.distributed.barrier()
         torch.distributed.destroy_process_group()
     return 0
+
+
+def _rest_update_flops(s, kl, ku, nb=128):
+    j = np.arange(s, dtype=np.int64)
+    lo = (j // nb + 2) * nb
+    ni = np.clip(np.minimum(j + kl, s - 1) - np.maximum(j + 1, lo) + 1, 0, None).astype(np.float64)
+    nc = np.clip(np.minimum(j + ku, s - 1) - np.maximum(j + 1, lo) + 1, 0, None).astype(np.float64)
+    return float(2.0 * np.sum(ni * nc))
 
 
 def _partition_sizes(n, P):

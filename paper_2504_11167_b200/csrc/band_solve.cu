@@ -15,10 +15,13 @@
 //
 // A chunk is 32 contiguous tile columns (32 KB, one bulk copy).  Multi-RHS
 // chunk products are (128 x 32) x (32 x NR) GEMMs (or their transposes) on the
-// FP64 tensor cores (DMMA.8x8x4), NR in {8, 16, 48}; one code path for every
+// FP64 tensor cores (DMMA.8x8x4), NR in {8, 16}; one code path for every
 // width keeps each column's arithmetic independent of the batch, so
 // solve_block on a multi-column RHS equals column-by-column bit-exactly
-// (solve_block always takes this path).  The Krylov hot path
+// (solve_block always takes this path).  Wider blocks (the 2l spike
+// columns of the setup) run as independent 16-column groups in the same launch,
+// each with its own ready flags: the per-tile critical path is a 16-column product,
+// and the groups of one row tile start together so their factor reads share L2.  The Krylov hot path
 // (apply with one right-hand side) uses an FP64-FMA variant, one thread per
 // row, which keeps less work on the per-tile critical path and streams the
 // factor at ~96% of the measured HBM copy bandwidth.
@@ -38,7 +41,7 @@ constexpr int CH_SM = CH_COLS * CLD;     // doubles per shared chunk
 constexpr int NCH = NB / CH_COLS;        // chunks per tile
 
 template <int NR> struct SolveCfg {
-  static constexpr int STAGES = NR >= 48 ? 3 : 5;
+  static constexpr int STAGES = 5;
   static constexpr int XLD = NR == 1 ? 1 : NR + 4;  // padded row stride of xs / red
 };
 
@@ -51,7 +54,8 @@ constexpr size_t solve_smem_bytes() {
 template <int MODE, int NR>
 __global__ void __launch_bounds__(SOLVE_THREADS, 1)
     band_solve_kernel(BandGeom g, const double* __restrict__ tiles, double* x, int64_t ld,
-                      int nrhs, unsigned* flags, unsigned epoch, int* ticket, int p_only) {
+                      int nrhs, unsigned* flags, unsigned epoch, int* ticket, int p_only,
+                      int ngroups, int64_t flag_stride) {
   constexpr int STAGES = SolveCfg<NR>::STAGES;
   constexpr int XLD = SolveCfg<NR>::XLD;
   constexpr bool FWD = (MODE == 0 || MODE == 2);
@@ -67,7 +71,12 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1)
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   if (tid == 0) *s_tk = atomicAdd(ticket, 1);
   __syncthreads();
-  const int tk = *s_tk;
+  const int tk0 = *s_tk;
+  // column group (adjacent tickets: the groups of one row tile start together)
+  const int grp = tk0 % ngroups, tk = tk0 / ngroups;
+  x += (int64_t)grp * NR * ld;
+  nrhs = min(NR, nrhs - grp * NR);
+  flags += grp * flag_stride;
   int p, tt;
   if (p_only >= 0) {
     p = p_only;
@@ -318,7 +327,8 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1)
 template <int MODE, int NR>
 static void launch_mode(Ctx* c, const BandGeom& g, const double* tiles, double* x, int64_t ld,
                         int nrhs, unsigned* flags, unsigned epoch, int* ticket, int p_only,
-                        int ntiles) {
+                        int ntiles, int64_t flag_stride) {
+  const int ngroups = (nrhs + NR - 1) / NR;
   static bool attr = false;
   const size_t smem = solve_smem_bytes<NR>();
   if (!attr) {
@@ -327,37 +337,37 @@ static void launch_mode(Ctx* c, const BandGeom& g, const double* tiles, double* 
     attr = true;
   }
   ProfScope ps_(c, c->in_setup ? K_SPIKE_SOLVE : (MODE >= 2 ? K_SOLVE_ADJ : K_SOLVE));
-  band_solve_kernel<MODE, NR><<<ntiles, SOLVE_THREADS, smem, c->stream>>>(
-      g, tiles, x, ld, nrhs, flags, epoch, ticket, p_only);
+  band_solve_kernel<MODE, NR><<<ntiles * ngroups, SOLVE_THREADS, smem, c->stream>>>(
+      g, tiles, x, ld, nrhs, flags, epoch, ticket, p_only, ngroups, flag_stride);
   LRS_LAUNCHED(c);
 }
 
 template <int MODE>
 static void launch_nr(Ctx* c, const BandGeom& g, const double* tiles, double* x, int64_t ld,
                       int nrhs, unsigned* flags, unsigned epoch, int* ticket, int p_only,
-                      int ntiles) {
-  // every width runs the same DMMA code (one n8 tile for <= 8 columns), so each column's
-  // arithmetic is independent of the batch: multi-column == column-by-column bit-exactly
-  //
+                      int ntiles, int64_t fs) {
+  // every width runs the same DMMA code (one n8 tile for <= 8 columns, 16-column groups
+  // beyond 16), so each column's arithmetic is independent of the batch: multi-column ==
+  // column-by-column bit-exactly
   if (nrhs <= 1 && c->solve_fma1)
-    launch_mode<MODE, 1>(c, g, tiles, x, ld, nrhs, flags, epoch, ticket, p_only, ntiles);
+    launch_mode<MODE, 1>(c, g, tiles, x, ld, nrhs, flags, epoch, ticket, p_only, ntiles, fs);
   else if (nrhs <= 8)
-    launch_mode<MODE, 8>(c, g, tiles, x, ld, nrhs, flags, epoch, ticket, p_only, ntiles);
-  else if (nrhs <= 16) launch_mode<MODE, 16>(c, g, tiles, x, ld, nrhs, flags, epoch, ticket, p_only, ntiles);
-  else launch_mode<MODE, 48>(c, g, tiles, x, ld, nrhs, flags, epoch, ticket, p_only, ntiles);
+    launch_mode<MODE, 8>(c, g, tiles, x, ld, nrhs, flags, epoch, ticket, p_only, ntiles, fs);
+  else
+    launch_mode<MODE, 16>(c, g, tiles, x, ld, nrhs, flags, epoch, ticket, p_only, ntiles, fs);
 }
 
 void launch_band_solve(Ctx* c, const BandGeom& g, const double* tiles, int mode, double* x,
                        int64_t ld, int nrhs, unsigned* flags, unsigned epoch, int* ticket,
-                       int p_only, int ntiles) {
+                       int p_only, int ntiles, int64_t fs) {
   if (ntiles == 0 || nrhs == 0) return;
   if (nrhs > SOLVE_MAX_RHS) throw LrsError(LRS_ERR_PARAMETER, "band solve batch > 48 columns");
   LRS_CUDA(cudaMemsetAsync(ticket, 0, sizeof(int), c->stream));
   switch (mode) {
-    case 0: launch_nr<0>(c, g, tiles, x, ld, nrhs, flags, epoch, ticket, p_only, ntiles); break;
-    case 1: launch_nr<1>(c, g, tiles, x, ld, nrhs, flags, epoch, ticket, p_only, ntiles); break;
-    case 2: launch_nr<2>(c, g, tiles, x, ld, nrhs, flags, epoch, ticket, p_only, ntiles); break;
-    default: launch_nr<3>(c, g, tiles, x, ld, nrhs, flags, epoch, ticket, p_only, ntiles); break;
+    case 0: launch_nr<0>(c, g, tiles, x, ld, nrhs, flags, epoch, ticket, p_only, ntiles, fs); break;
+    case 1: launch_nr<1>(c, g, tiles, x, ld, nrhs, flags, epoch, ticket, p_only, ntiles, fs); break;
+    case 2: launch_nr<2>(c, g, tiles, x, ld, nrhs, flags, epoch, ticket, p_only, ntiles, fs); break;
+    default: launch_nr<3>(c, g, tiles, x, ld, nrhs, flags, epoch, ticket, p_only, ntiles, fs); break;
   }
 }
 

@@ -24,7 +24,8 @@ constexpr size_t zsolve_smem_bytes() {
 template <int MODE, int NR>
 __global__ void __launch_bounds__(ZS_THREADS, 1)
     band_solve_z_kernel(BandGeom g, const zc* __restrict__ tiles, zc* x, int64_t ld, int nrhs,
-                        unsigned* flags, unsigned epoch, int* ticket, int p_only) {
+                        unsigned* flags, unsigned epoch, int* ticket, int p_only, int ngroups,
+                        int64_t flag_stride) {
   constexpr int XLD = NR + 4;
   constexpr bool FWD = (MODE == 0 || MODE == 2);
   constexpr bool TRANS = (MODE >= 2);
@@ -38,7 +39,12 @@ __global__ void __launch_bounds__(ZS_THREADS, 1)
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   if (tid == 0) *s_tk = atomicAdd(ticket, 1);
   __syncthreads();
-  const int tk = *s_tk;
+  const int tk0 = *s_tk;
+  // 16-column group (as in band_solve.cu)
+  const int grp = tk0 % ngroups, tk = tk0 / ngroups;
+  x += (int64_t)grp * NR * ld;
+  nrhs = min(NR, nrhs - grp * NR);
+  flags += grp * flag_stride;
   int p, tt;
   if (p_only >= 0) {
     p = p_only;
@@ -252,7 +258,9 @@ __global__ void __launch_bounds__(ZS_THREADS, 1)
 
 template <int MODE, int NR>
 static void zlaunch_mode(Ctx* c, const BandGeom& g, const zc* tiles, zc* x, int64_t ld, int nrhs,
-                         unsigned* flags, unsigned epoch, int* ticket, int p_only, int ntiles) {
+                         unsigned* flags, unsigned epoch, int* ticket, int p_only, int ntiles,
+                         int64_t fs) {
+  const int ngroups = (nrhs + NR - 1) / NR;
   static bool attr = false;
   const size_t smem = zsolve_smem_bytes<NR>();
   if (!attr) {
@@ -261,29 +269,32 @@ static void zlaunch_mode(Ctx* c, const BandGeom& g, const zc* tiles, zc* x, int6
     attr = true;
   }
   ProfScope ps_(c, c->in_setup ? K_SPIKE_SOLVE : (MODE >= 2 ? K_SOLVE_ADJ : K_SOLVE));
-  band_solve_z_kernel<MODE, NR><<<ntiles, ZS_THREADS, smem, c->stream>>>(
-      g, tiles, x, ld, nrhs, flags, epoch, ticket, p_only);
+  band_solve_z_kernel<MODE, NR><<<ntiles * ngroups, ZS_THREADS, smem, c->stream>>>(
+      g, tiles, x, ld, nrhs, flags, epoch, ticket, p_only, ngroups, fs);
   LRS_LAUNCHED(c);
 }
 
 template <int MODE>
 static void zlaunch_nr(Ctx* c, const BandGeom& g, const zc* tiles, zc* x, int64_t ld, int nrhs,
-                       unsigned* flags, unsigned epoch, int* ticket, int p_only, int ntiles) {
-  if (nrhs <= 8) zlaunch_mode<MODE, 8>(c, g, tiles, x, ld, nrhs, flags, epoch, ticket, p_only, ntiles);
-  else zlaunch_mode<MODE, 16>(c, g, tiles, x, ld, nrhs, flags, epoch, ticket, p_only, ntiles);
+                       unsigned* flags, unsigned epoch, int* ticket, int p_only, int ntiles,
+                       int64_t fs) {
+  if (nrhs <= 8)
+    zlaunch_mode<MODE, 8>(c, g, tiles, x, ld, nrhs, flags, epoch, ticket, p_only, ntiles, fs);
+  else
+    zlaunch_mode<MODE, 16>(c, g, tiles, x, ld, nrhs, flags, epoch, ticket, p_only, ntiles, fs);
 }
 
 void launch_band_solve_z(Ctx* c, const BandGeom& g, const zc* tiles, int mode, zc* x, int64_t ld,
                          int nrhs, unsigned* flags, unsigned epoch, int* ticket, int p_only,
-                         int ntiles) {
+                         int ntiles, int64_t fs) {
   if (ntiles == 0 || nrhs == 0) return;
-  if (nrhs > ZSOLVE_MAX_RHS) throw LrsError(LRS_ERR_PARAMETER, "complex band solve batch > 16");
+  if (nrhs > ZSOLVE_MAX_RHS) throw LrsError(LRS_ERR_PARAMETER, "complex band solve batch > 96");
   LRS_CUDA(cudaMemsetAsync(ticket, 0, sizeof(int), c->stream));
   switch (mode) {
-    case 0: zlaunch_nr<0>(c, g, tiles, x, ld, nrhs, flags, epoch, ticket, p_only, ntiles); break;
-    case 1: zlaunch_nr<1>(c, g, tiles, x, ld, nrhs, flags, epoch, ticket, p_only, ntiles); break;
-    case 2: zlaunch_nr<2>(c, g, tiles, x, ld, nrhs, flags, epoch, ticket, p_only, ntiles); break;
-    default: zlaunch_nr<3>(c, g, tiles, x, ld, nrhs, flags, epoch, ticket, p_only, ntiles); break;
+    case 0: zlaunch_nr<0>(c, g, tiles, x, ld, nrhs, flags, epoch, ticket, p_only, ntiles, fs); break;
+    case 1: zlaunch_nr<1>(c, g, tiles, x, ld, nrhs, flags, epoch, ticket, p_only, ntiles, fs); break;
+    case 2: zlaunch_nr<2>(c, g, tiles, x, ld, nrhs, flags, epoch, ticket, p_only, ntiles, fs); break;
+    default: zlaunch_nr<3>(c, g, tiles, x, ld, nrhs, flags, epoch, ticket, p_only, ntiles, fs); break;
   }
 }
 

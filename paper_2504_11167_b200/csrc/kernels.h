@@ -61,15 +61,16 @@ void launch_extract_tiles_z(Ctx* c, const Mat* m, const BandGeom& g, zc* tiles, 
 // ---- band_solve.cu -------------------------------------------------------------------
 // In-place multi-RHS banded triangular solve over all partitions.
 // mode 0: L (forward), 1: U (backward), 2: U^T (forward), 3: L^T (backward).
-// x is the global-row-layout block (n rows, ld), columns [0, nrhs) with nrhs <= MAX_RHS.
+// x is the global-row-layout block (n rows, ld), columns [0, nrhs), nrhs <= SOLVE_MAX_RHS.
+// flags: SOLVE_GROUPS x flag_stride ready flags (one set per 16-column group).
 void launch_band_solve(Ctx* c, const BandGeom& g, const double* tiles, int mode, double* x,
                        int64_t ld, int nrhs, unsigned* flags, unsigned epoch, int* ticket,
-                       int p_only, int ntiles);
-constexpr int ZSOLVE_MAX_RHS = 16;
+                       int p_only, int ntiles, int64_t flag_stride);
+constexpr int ZSOLVE_MAX_RHS = 16 * SOLVE_GROUPS;  // 96
 // complex: modes 2 / 3 are the conjugate transposes U^H, L^H
 void launch_band_solve_z(Ctx* c, const BandGeom& g, const zc* tiles, int mode, zc* x, int64_t ld,
                          int nrhs, unsigned* flags, unsigned epoch, int* ticket, int p_only,
-                         int ntiles);
+                         int ntiles, int64_t flag_stride);
 
 // ---- dense_small.cu (templated on the scalar S = double | zc) -------------------------
 template <class S>

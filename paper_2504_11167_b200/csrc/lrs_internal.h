@@ -18,6 +18,8 @@ constexpr int NB = 128;                    // band-factor tile size (rows = cols
 constexpr int64_t TILE_ELEMS = (int64_t)NB * NB;
 constexpr int MAX_RHS = 16;                // columns per Krylov batch
 constexpr int SOLVE_MAX_RHS = 48;          // columns per band-solve launch (DMMA path)
+constexpr int SOLVE_GROUPS = 6;            // 16-column groups per launch (ready-flag sets):
+                                           // 48 / 16 real, 96 / 16 complex (2 l <= 96)
 constexpr double COND_LIMIT = 1e12;        // interface condition limit (oracle: COND_LIMIT)
 
 // Error carried from deep inside the implementation to the C-ABI wrapper.

@@ -160,10 +160,10 @@ void dstage_t(Fact* f, S* x, int64_t ld, int nrhs, bool adjoint, int p_only) {
       const int mode = adjoint ? 2 + half : half;
       if constexpr (IsC<S>::value)
         launch_band_solve_z(f->ctx, g, sp<zc>(f->tiles), mode, xc, ld, nr, f->flags.get(),
-                            f->next_epoch(), f->ticket.get(), p_only, ntiles);
+                            f->next_epoch(), f->ticket.get(), p_only, ntiles, f->total_rowtiles);
       else
         launch_band_solve(f->ctx, g, f->tiles.get(), mode, xc, ld, nr, f->flags.get(),
-                          f->next_epoch(), f->ticket.get(), p_only, ntiles);
+                          f->next_epoch(), f->ticket.get(), p_only, ntiles, f->total_rowtiles);
     }
   }
 }
@@ -683,12 +683,12 @@ Fact* factorize(Ctx* c, Mat* m, const lrs_solver_cfg& cfg, const lrs_comm* comm)
   upload(c, f->d_goff, f->goff);
   upload(c, f->d_rank_pl, f->rank_pl);
   f->tiles.alloc((size_t)tb * TILE_ELEMS * w);
-  f->flags.alloc((size_t)fb);
+  f->flags.alloc((size_t)fb * SOLVE_GROUPS);
   f->ticket.alloc(1);
   f->status.alloc(2 * P);
   f->bad.alloc(1);
   LRS_CUDA(cudaMemsetAsync(f->tiles.get(), 0, sizeof(double) * tb * TILE_ELEMS * w, c->stream));
-  LRS_CUDA(cudaMemsetAsync(f->flags.get(), 0, sizeof(unsigned) * fb, c->stream));
+  LRS_CUDA(cudaMemsetAsync(f->flags.get(), 0, sizeof(unsigned) * fb * SOLVE_GROUPS, c->stream));
   LRS_CUDA(cudaMemsetAsync(f->status.get(), 0x7f, sizeof(int) * 2 * P, c->stream));
   LRS_CUDA(cudaMemsetAsync(f->bad.get(), 0xff, sizeof(unsigned long long), c->stream));
   // deterministic reduction chunks, partition aligned
