@@ -43,11 +43,14 @@ constexpr int NCH = NB / CH_COLS;        // chunks per tile
 template <int NR> struct SolveCfg {
   static constexpr int STAGES = 5;
   static constexpr int XLD = NR == 1 ? 1 : NR + 4;  // padded row stride of xs / red
+  static constexpr int PLD = NR + 1;                // K-quarter partials (adjoint DMMA)
+  static constexpr int PART = NR == 1 ? 0 : 4 * CH_COLS * PLD;
 };
 
 template <int NR>
 constexpr size_t solve_smem_bytes() {
-  return sizeof(double) * ((size_t)SolveCfg<NR>::STAGES * CH_SM + 2 * (size_t)NB * SolveCfg<NR>::XLD) +
+  return sizeof(double) * ((size_t)SolveCfg<NR>::STAGES * CH_SM + 2 * (size_t)NB * SolveCfg<NR>::XLD +
+                           SolveCfg<NR>::PART) +
          16 * SolveCfg<NR>::STAGES + 64;
 }
 
@@ -65,7 +68,8 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1)
   double* ring = reinterpret_cast<double*>(smraw);
   double* xs = ring + (size_t)STAGES * CH_SM;  // [NB][XLD]: x_s, or the diagonal-step input
   double* red = xs + NB * XLD;                 // [NB][XLD]: half sums / transposed accumulator
-  uint64_t* bars = reinterpret_cast<uint64_t*>(red + NB * XLD);
+  double* part = red + NB * XLD;               // [4][CH_COLS][PLD]: adjoint K-quarter partials
+  uint64_t* bars = reinterpret_cast<uint64_t*>(part + SolveCfg<NR>::PART);
   int* s_tk = reinterpret_cast<int*>(bars + STAGES);
 
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
@@ -251,34 +255,46 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1)
       if (rg == 0) red[c] += diag ? part : -part;
     } else {
       // transposed: out(32 x NR) (+|-)= Tile^T (32 x 128) xs (128 x NR) on DMMA.
-      // 4 x NJ output tiles spread over the 8 warps; each warp runs the full K = 128.
-      constexpr int TPW = (4 * NJ + 7) / 8;
+      // Warp w takes K-quarter kq = w & 3 (32 tile rows) of half the 4 x NJ output tiles,
+      // so each warp runs 4 NJ / 2 independent accumulator chains of 8 DMMAs; the four
+      // K-quarter partials are then summed in fixed order (the same for every NR, so
+      // multi-column stays bit-identical to column-by-column).
+      constexpr int PLD = SolveCfg<NR>::PLD;
+      constexpr int TPH = 2 * NJ;  // output tiles per warp
+      const int kq = w & 3, th = w >> 2;
+      double cacc[TPH][2];
 #pragma unroll
-      for (int u = 0; u < TPW; ++u) {
-        const int ti = w + 8 * u;
-        if (ti >= 4 * NJ) break;
-        const int mi = ti & 3, nj = ti >> 2;
-        double c0 = 0.0, c1 = 0.0;
-        const int mloc = 8 * mi + gq;  // chunk-local output column
-        const int cglob = cbase + mloc;
-#pragma unroll 8
-        for (int k4 = 0; k4 < NB / 4; ++k4) {
-          const int r = 4 * k4 + tq;
+      for (int u = 0; u < TPH; ++u) cacc[u][0] = cacc[u][1] = 0.0;
+#pragma unroll
+      for (int k4 = 0; k4 < CH_COLS / 4; ++k4) {
+        const int r = 32 * kq + 4 * k4 + tq;
+#pragma unroll
+        for (int u = 0; u < TPH; ++u) {
+          const int ti = th * TPH + u;
+          const int mi = ti & 3, nj = ti >> 2;
+          const int mloc = 8 * mi + gq;  // chunk-local output column
           double a = ch[mloc * CLD + r];
-          if (diag) a = (MODE == 2) ? (r <= cglob ? a : 0.0) : (r > cglob ? a : 0.0);
-          const double b = xs[r * XLD + 8 * nj + gq];
-          dmma_8x8x4(c0, c1, a, b);
+          if (diag) a = (MODE == 2) ? (r <= cbase + mloc ? a : 0.0) : (r > cbase + mloc ? a : 0.0);
+          dmma_8x8x4(cacc[u][0], cacc[u][1], a, xs[r * XLD + 8 * nj + gq]);
         }
+      }
+#pragma unroll
+      for (int u = 0; u < TPH; ++u) {
+        const int ti = th * TPH + u;
+        const int mi = ti & 3, nj = ti >> 2;
         // fragment (m = 8 mi + gq, n = 8 nj + 2 tq + e) is owned by exactly this lane
-        const int n = 8 * nj + 2 * tq;
-        double* rp = red + (cbase + 8 * mi + gq) * XLD + n;
-        if (diag) {
-          rp[0] += c0;
-          rp[1] += c1;
-        } else {
-          rp[0] -= c0;
-          rp[1] -= c1;
-        }
+        double* pp = part + (kq * CH_COLS + 8 * mi + gq) * PLD + 8 * nj + 2 * tq;
+        pp[0] = cacc[u][0];
+        pp[1] = cacc[u][1];
+      }
+      __syncthreads();
+      for (int e = tid; e < CH_COLS * NR; e += SOLVE_THREADS) {
+        const int mm = e / NR, nn = e % NR;
+        const double v = ((part[mm * PLD + nn] + part[(CH_COLS + mm) * PLD + nn]) +
+                          part[(2 * CH_COLS + mm) * PLD + nn]) +
+                         part[(3 * CH_COLS + mm) * PLD + nn];
+        double* rp = red + (cbase + mm) * XLD + nn;
+        *rp = diag ? *rp + v : *rp - v;
       }
     }
     __syncthreads();

@@ -17,8 +17,12 @@ constexpr int ZNCH = NB / ZCH_COLS;    // 8 chunks per tile
 constexpr int ZSTAGES = 3;
 
 template <int NR>
+constexpr int zpart_elems() { return 4 * ZCH_COLS * (NR + 1); }  // adjoint K-quarter partials
+
+template <int NR>
 constexpr size_t zsolve_smem_bytes() {
-  return sizeof(zc) * ((size_t)ZSTAGES * ZCH_SM + 2 * (size_t)NB * (NR + 4)) + 16 * ZSTAGES + 64;
+  return sizeof(zc) * ((size_t)ZSTAGES * ZCH_SM + 2 * (size_t)NB * (NR + 4) + zpart_elems<NR>()) +
+         16 * ZSTAGES + 64;
 }
 
 template <int MODE, int NR>
@@ -34,7 +38,8 @@ __global__ void __launch_bounds__(ZS_THREADS, 1)
   zc* ring = reinterpret_cast<zc*>(smraw);
   zc* xs = ring + (size_t)ZSTAGES * ZCH_SM;
   zc* red = xs + NB * XLD;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(red + NB * XLD);
+  zc* part = red + NB * XLD;  // [4][ZCH_COLS][NR + 1]: adjoint K-quarter partials
+  uint64_t* bars = reinterpret_cast<uint64_t*>(part + zpart_elems<NR>());
   int* s_tk = reinterpret_cast<int*>(bars + ZSTAGES);
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   if (tid == 0) *s_tk = atomicAdd(ticket, 1);
@@ -194,32 +199,48 @@ __global__ void __launch_bounds__(ZS_THREADS, 1)
           }
       }
     } else {
-      // out(16 x NR) (+|-)= conj(Tile)^T (16 x 128) xs (128 x NR): 2 x NJ tiles over warps
-      for (int ti = w; ti < 2 * NJ; ti += 8) {
-        const int mi = ti & 1, nj = ti >> 1;
-        double cr0 = 0.0, cr1 = 0.0, ci0 = 0.0, ci1 = 0.0;
-        const int mloc = 8 * mi + gq;
-        const int cglob = cbase + mloc;
-#pragma unroll 4
-        for (int k4 = 0; k4 < NB / 4; ++k4) {
-          const int r = 4 * k4 + tq;
+      // out(16 x NR) (+|-)= conj(Tile)^T (16 x 128) xs (128 x NR).  Warp w takes K-quarter
+      // kq = w & 3 (32 tile rows) of half the 2 x NJ output tiles (independent chains);
+      // the four partials are summed in fixed order (NR independent: bit-exact columns).
+      constexpr int PLD = NR + 1;
+      const int kq = w & 3, th = w >> 2;
+      double cr[NJ][2], ci[NJ][2];
+#pragma unroll
+      for (int u = 0; u < NJ; ++u) cr[u][0] = cr[u][1] = ci[u][0] = ci[u][1] = 0.0;
+#pragma unroll
+      for (int k4 = 0; k4 < 8; ++k4) {
+        const int r = 32 * kq + 4 * k4 + tq;
+#pragma unroll
+        for (int u = 0; u < NJ; ++u) {
+          const int ti = th * NJ + u;
+          const int mi = ti & 1, nj = ti >> 1;
+          const int mloc = 8 * mi + gq;
           zc a = ch[mloc * NB + r];
-          if (diag && !(MODE == 2 ? r <= cglob : r > cglob)) a = {0.0, 0.0};
+          if (diag && !(MODE == 2 ? r <= cbase + mloc : r > cbase + mloc)) a = {0.0, 0.0};
           const double ar = a.x, ai = -a.y;  // conjugate
           const zc b = xs[r * XLD + 8 * nj + gq];
-          dmma_8x8x4(cr0, cr1, ar, b.x);
-          dmma_8x8x4(cr0, cr1, -ai, b.y);
-          dmma_8x8x4(ci0, ci1, ar, b.y);
-          dmma_8x8x4(ci0, ci1, ai, b.x);
+          dmma_8x8x4(cr[u][0], cr[u][1], ar, b.x);
+          dmma_8x8x4(ci[u][0], ci[u][1], ar, b.y);
+          dmma_8x8x4(cr[u][0], cr[u][1], -ai, b.y);
+          dmma_8x8x4(ci[u][0], ci[u][1], ai, b.x);
         }
-        zc* rp = red + (cbase + 8 * mi + gq) * XLD + 8 * nj + 2 * tq;
-        if (diag) {
-          rp[0] = {rp[0].x + cr0, rp[0].y + ci0};
-          rp[1] = {rp[1].x + cr1, rp[1].y + ci1};
-        } else {
-          rp[0] = {rp[0].x - cr0, rp[0].y - ci0};
-          rp[1] = {rp[1].x - cr1, rp[1].y - ci1};
-        }
+      }
+#pragma unroll
+      for (int u = 0; u < NJ; ++u) {
+        const int ti = th * NJ + u;
+        const int mi = ti & 1, nj = ti >> 1;
+        zc* pp = part + (kq * ZCH_COLS + 8 * mi + gq) * PLD + 8 * nj + 2 * tq;
+        pp[0] = {cr[u][0], ci[u][0]};
+        pp[1] = {cr[u][1], ci[u][1]};
+      }
+      __syncthreads();
+      for (int e = tid; e < ZCH_COLS * NR; e += ZS_THREADS) {
+        const int mm = e / NR, nn = e % NR;
+        const zc v = s_add(s_add(s_add(part[mm * PLD + nn], part[(ZCH_COLS + mm) * PLD + nn]),
+                                 part[(2 * ZCH_COLS + mm) * PLD + nn]),
+                           part[(3 * ZCH_COLS + mm) * PLD + nn]);
+        zc* rp = red + (cbase + mm) * XLD + nn;
+        *rp = diag ? s_add(*rp, v) : s_sub(*rp, v);
       }
     }
     __syncthreads();

@@ -4,6 +4,8 @@
 // l x l R factor, the small GEMMs that form u and v, and the per-interface Woodbury
 // setup of build_truncated_precond (G = K^-1 explicit,
 // H = G - S_T vT uW S_W, cond_1 estimate).  All on the GPU, one CTA per job.
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 #include "kernels.h"
 #include "lrs_internal.h"
@@ -18,6 +20,7 @@ __device__ __forceinline__ zc ds_warp_sum(zc v) { return warp_sum_z(v); }
 // applies H_j^H (coefficient conj(tau)), the explicit Q applies H_j (coefficient tau).
 // ---------------------------------------------------------------------------------------
 constexpr int QR_THREADS = 512;
+constexpr int SVD_MAXL = 96;
 constexpr int QR_CB = 8;  // columns per reduction batch
 
 template <class S>
@@ -117,9 +120,149 @@ __global__ void __launch_bounds__(QR_THREADS) householder_qr_kernel(const QrJobT
   }
 }
 
+// Cluster variant: QRC CTAs per job (one thread-block cluster), each owning a contiguous
+// slice of the rows, so a spike's QR streams through QRC SMs instead of one.  Every column
+// reduction is a block reduction followed by a fixed-rank-order sum of the QRC block
+// partials read through distributed shared memory (deterministic, identical on every CTA
+// of the cluster).  Rank 0 owns rows 0..l-1 (requires ceil(m / QRC) >= l).
+constexpr int QRC = 8;
+
 template <class S>
-void launch_householder_qr_t(Ctx* c, const QrJobT<S>* d_jobs, int njobs, int l) {
+__global__ void __cluster_dims__(QRC, 1, 1) __launch_bounds__(QR_THREADS)
+    householder_qr_cluster_kernel(const QrJobT<S>* jobs, int l) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int crank = (int)cluster.block_rank();
+  constexpr int NW = QR_THREADS / 32;
+  __shared__ S wred[NW][QR_CB];
+  __shared__ S slot[2][QR_CB + 1];  // block partials (double buffered) + alpha broadcast
+  __shared__ S tot[QR_CB + 1];
+  __shared__ S tau[SVD_MAXL];
+  const QrJobT<S> jb = jobs[blockIdx.x / QRC];
+  S* A = jb.A;
+  const int64_t m = jb.m, ld = jb.ld;
+  const int64_t rows_per = (m + QRC - 1) / QRC;
+  const int64_t r0 = crank * rows_per, r1 = min(m, r0 + rows_per);
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  int par = 0;
+  // tot[u] = sum over the cluster of every thread's part[u], u < cb; tot[QR_CB] = the
+  // value rank 0 passed as bcast (when given)
+  auto cluster_sum = [&](const S* part, int cb, const S* bcast) {
+#pragma unroll
+    for (int u = 0; u < QR_CB; ++u)
+      if (u < cb) {
+        const S v = ds_warp_sum(part[u]);
+        if (lane == 0) wred[w][u] = v;
+      }
+    __syncthreads();
+    if (tid < cb) {
+      S v = s_zero(S());
+      for (int q = 0; q < NW; ++q) v = s_add(v, wred[q][tid]);
+      slot[par][tid] = v;
+    }
+    if (bcast && crank == 0 && tid == 0) slot[par][QR_CB] = *bcast;
+    cluster.sync();
+    if (tid < cb) {
+      S v = s_zero(S());
+      for (int rk = 0; rk < QRC; ++rk) v = s_add(v, *cluster.map_shared_rank(&slot[par][tid], rk));
+      tot[tid] = v;
+    }
+    if (bcast && tid == 0) tot[QR_CB] = *cluster.map_shared_rank(&slot[par][QR_CB], 0);
+    __syncthreads();
+    par ^= 1;
+  };
+  // A[j:, c0:c0+cb] -= v (coef * (v^H A[j:, c])) on this CTA's rows
+  auto apply_reflector = [&](int j, int c0, int cb, S coef) {
+    S part[QR_CB];
+#pragma unroll
+    for (int u = 0; u < QR_CB; ++u) part[u] = s_zero(S());
+    for (int64_t i = (r0 > (int64_t)j ? r0 : (int64_t)j) + tid; i < r1; i += QR_THREADS) {
+      const S vi = (i == j) ? s_real<S>(1.0) : A[i + j * ld];
+#pragma unroll
+      for (int u = 0; u < QR_CB; ++u)
+        if (u < cb) part[u] = s_cfma(vi, A[i + (c0 + u) * ld], part[u]);
+    }
+    cluster_sum(part, cb, nullptr);
+    S wv[QR_CB];
+#pragma unroll
+    for (int u = 0; u < QR_CB; ++u) wv[u] = u < cb ? s_mul(coef, tot[u]) : s_zero(S());
+    for (int64_t i = (r0 > (int64_t)j ? r0 : (int64_t)j) + tid; i < r1; i += QR_THREADS) {
+      const S vi = (i == j) ? s_real<S>(1.0) : A[i + j * ld];
+#pragma unroll
+      for (int u = 0; u < QR_CB; ++u)
+        if (u < cb) A[i + (c0 + u) * ld] = s_sub(A[i + (c0 + u) * ld], s_mul(vi, wv[u]));
+    }
+    __syncthreads();
+  };
+
+  for (int j = 0; j < l; ++j) {
+    S ss[QR_CB];
+    ss[0] = s_zero(S());
+    double acc = 0.0;
+    for (int64_t i = (r0 > (int64_t)(j + 1) ? r0 : (int64_t)(j + 1)) + tid; i < r1; i += QR_THREADS) acc += s_abs2(A[i + j * ld]);
+    ss[0] = s_real<S>(acc);
+    S alpha_own = s_zero(S());
+    if (crank == 0) alpha_own = A[j + j * ld];
+    cluster_sum(ss, 1, &alpha_own);
+    const double sq = reinterpret_cast<const double*>(&tot[0])[0];
+    const S alpha = tot[QR_CB];
+    const double xnorm = sqrt(sq);
+    const double alphr = reinterpret_cast<const double*>(&alpha)[0];
+    const double alphi = IsC<S>::value ? reinterpret_cast<const double*>(&alpha)[1] : 0.0;
+    S tj = s_zero(S()), scal = s_real<S>(1.0), beta = alpha;
+    if (xnorm != 0.0 || alphi != 0.0) {  // LAPACK larfg
+      const double b = -copysign(sqrt(alphr * alphr + alphi * alphi + sq), alphr);
+      beta = s_real<S>(b);
+      S t;
+      if constexpr (IsC<S>::value) t = S{(b - alphr) / b, -alphi / b};
+      else t = (b - alphr) / b;
+      tj = t;
+      scal = s_inv(s_sub(alpha, beta));
+    }
+    if (!s_iszero(tj))
+      for (int64_t i = (r0 > (int64_t)(j + 1) ? r0 : (int64_t)(j + 1)) + tid; i < r1; i += QR_THREADS)
+        A[i + j * ld] = s_mul(A[i + j * ld], scal);
+    __syncthreads();
+    if (tid == 0) {
+      if (crank == 0) A[j + j * ld] = beta;
+      tau[j] = tj;
+    }
+    __syncthreads();
+    if (!s_iszero(tj))
+      for (int c0 = j + 1; c0 < l; c0 += QR_CB) apply_reflector(j, c0, min(QR_CB, l - c0), s_conj(tj));
+  }
+  if (jb.R && crank == 0) {
+    for (int e = tid; e < l * l; e += QR_THREADS) {
+      const int r = e % l, c = e / l;
+      jb.R[e] = (r <= c) ? A[r + c * ld] : s_zero(S());
+    }
+  }
+  __syncthreads();
+  for (int j = l - 1; j >= 0; --j) {
+    const S tj = tau[j];
+    if (j < l - 1 && !s_iszero(tj))
+      for (int c0 = j + 1; c0 < l; c0 += QR_CB) apply_reflector(j, c0, min(QR_CB, l - c0), tj);
+    for (int64_t i = r0 + tid; i < r1; i += QR_THREADS) {
+      S v;
+      if (i < j) v = s_zero(S());
+      else if (i == j) v = s_sub(s_real<S>(1.0), tj);
+      else v = s_neg(s_mul(tj, A[i + j * ld]));
+      A[i + j * ld] = v;
+    }
+    __syncthreads();
+  }
+  cluster.sync();  // no CTA leaves while another may still read its shared memory
+}
+
+template <class S>
+void launch_householder_qr_t(Ctx* c, const QrJobT<S>* d_jobs, int njobs, int l, int64_t min_m) {
   if (njobs == 0) return;
+  if (l <= SVD_MAXL && (min_m + QRC - 1) / QRC >= l && min_m >= 2048) {
+    ProfScope ps_(c, K_SETUP);
+    householder_qr_cluster_kernel<S><<<njobs * QRC, QR_THREADS, 0, c->stream>>>(d_jobs, l);
+    LRS_LAUNCHED(c);
+    return;
+  }
   const size_t smem = sizeof(S) * (l + (QR_THREADS / 32) * QR_CB + QR_CB) +
                       sizeof(double) * (QR_THREADS / 32);
   ProfScope ps_(c, K_SETUP);
@@ -135,7 +278,6 @@ void launch_householder_qr_t(Ctx* c, const QrJobT<S>* d_jobs, int njobs, int l) 
 // Results sorted by sigma descending.
 // ---------------------------------------------------------------------------------------
 constexpr int SVD_THREADS = 256;
-constexpr int SVD_MAXL = 96;
 
 template <class S>
 __global__ void __launch_bounds__(SVD_THREADS) jacobi_svd_kernel(const SvdJobT<S>* jobs, int l) {
@@ -469,7 +611,7 @@ void launch_sigma_trunc(Ctx* c, const SigmaJob* d_jobs, int njobs, int r, int* d
 }
 
 #define LRS_INST(S)                                                                          \
-  template void launch_householder_qr_t<S>(Ctx*, const QrJobT<S>*, int, int);                \
+  template void launch_householder_qr_t<S>(Ctx*, const QrJobT<S>*, int, int, int64_t);       \
   template void launch_jacobi_svd_t<S>(Ctx*, const SvdJobT<S>*, int, int);                   \
   template void launch_small_gemm_t<S>(Ctx*, const GemmJobT<S>*, int, int64_t, int);         \
   template void launch_iface_setup_t<S>(Ctx*, const IfaceSetupJobT<S>*, int, int, int64_t);

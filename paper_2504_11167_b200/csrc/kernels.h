@@ -79,8 +79,9 @@ struct QrJobT {
   int64_t m, ld;
   S* R;          // l x l column-major output (may be null)
 };
+// min_m: the smallest m of the jobs (tall jobs run as 8-CTA clusters)
 template <class S>
-void launch_householder_qr_t(Ctx* c, const QrJobT<S>* d_jobs, int njobs, int l);
+void launch_householder_qr_t(Ctx* c, const QrJobT<S>* d_jobs, int njobs, int l, int64_t min_m);
 
 template <class S>
 struct SvdJobT {

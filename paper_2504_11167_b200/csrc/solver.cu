@@ -341,9 +341,13 @@ bool build_lowrank(Fact* f, int r, int* bad_iface, double* bad_cond, std::vector
   DevBuf<QrJobT<S>> qj;
   auto orth_Y = [&]() {
     std::vector<QrJobT<S>> jobs;
-    for (auto [i, side] : spk) jobs.push_back(QrJobT<S>{ycol(Y, i, side), gsize(i), n, nullptr});
+    int64_t mm = n;
+    for (auto [i, side] : spk) {
+      jobs.push_back(QrJobT<S>{ycol(Y, i, side), gsize(i), n, nullptr});
+      mm = std::min(mm, gsize(i));
+    }
     upload(c, qj, jobs);
-    launch_householder_qr_t<S>(c, qj.get(), (int)jobs.size(), l);
+    launch_householder_qr_t<S>(c, qj.get(), (int)jobs.size(), l, mm);
   };
   auto orth_Zt = [&](bool keepR) {
     std::vector<QrJobT<S>> jobs;
@@ -351,7 +355,7 @@ bool build_lowrank(Fact* f, int r, int* bad_iface, double* bad_cond, std::vector
       jobs.push_back(QrJobT<S>{Zt + slot(i, side) * k * l, k, k,
                                keepR ? Rz + slot(i, side) * l * l : nullptr});
     upload(c, qj, jobs);
-    launch_householder_qr_t<S>(c, qj.get(), (int)jobs.size(), l);
+    launch_householder_qr_t<S>(c, qj.get(), (int)jobs.size(), l, k);
   };
 
   T_apply(Om);
