@@ -33,7 +33,7 @@ struct PartitionLayout {
 PartitionLayout make_layout(index_t n, index_t p, index_t k);
 
 enum class Variant { LR_SPIKE_T, BLOCK_JACOBI };
-enum class Method { BICGSTAB, GMRES };
+enum class Method { BICGSTAB, GMRES, CG };  // CG: SPEC.md:430-436
 
 /// SPEC.md:411-414 (+ method / restart).
 struct IterConfig {

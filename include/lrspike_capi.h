@@ -67,7 +67,7 @@ typedef enum lrs_status {
 typedef enum lrs_scalar { LRS_F64 = 0, LRS_C128 = 1 } lrs_scalar;
 typedef enum lrs_mem { LRS_MEM_HOST = 0, LRS_MEM_DEVICE = 1 } lrs_mem;
 typedef enum lrs_variant { LRS_VARIANT_T = 0, LRS_VARIANT_BJ = 1 } lrs_variant;
-typedef enum lrs_method { LRS_GMRES = 0, LRS_BICGSTAB = 1 } lrs_method;
+typedef enum lrs_method { LRS_GMRES = 0, LRS_BICGSTAB = 1, LRS_CG = 2 } lrs_method;
 typedef enum lrs_side { LRS_SIDE_T = 0, LRS_SIDE_W = 1 } lrs_side;
 
 /* Ledger stages. */

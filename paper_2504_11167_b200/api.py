@@ -30,7 +30,8 @@ LRS_OK = 0
 F64, C128 = 0, 1
 MEM_HOST, MEM_DEVICE = 0, 1
 VARIANT_T, VARIANT_BJ = 0, 1
-GMRES, BICGSTAB = 0, 1
+GMRES, BICGSTAB, CG = 0, 1, 2
+_METHODS = {"gmres": GMRES, "bicgstab": BICGSTAB, "cg": CG}
 SIDE_T, SIDE_W = 0, 1
 STAGES = ("reduced-matvec", "precond-apply", "recovery")
 KERNEL_CLASSES = ("lu_diag", "lu_panel", "lu_update", "band_solve", "band_solve_adjoint", "spmv",
@@ -542,7 +543,9 @@ def solve(A: CsrMatrix, f, cfg: SolverConfig | None = None, it: IterConfig | Non
         x0p, ldx0, mem0, _ = _buf(it.initial_guess, A.n, dt)
         if mem0 != mem or ldx0 != ldx:
             raise DimensionError("initial guess must match x's memory kind and layout")
-    ic = IterCfgC(GMRES if it.method == "gmres" else BICGSTAB, it.restart, it.tol, it.max_iters,
+    if it.method not in _METHODS:
+        raise ParameterError(f"unknown Krylov method {it.method!r}")
+    ic = IterCfgC(_METHODS[it.method], it.restart, it.tol, it.max_iters,
                   it.breakdown_eps, x0p)
     hist = (f64 * history_cap)()
     rep = ReportC()

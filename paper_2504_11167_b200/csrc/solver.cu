@@ -1097,6 +1097,101 @@ void run_bicgstab(Work<S>& w, const S* b, S* x, const lrs_iter_cfg& cfg, bool ha
   }
 }
 
+// Preconditioned CG, mirroring the checker's cg: iterations in
+// BiCGStab half-iteration units (0.5 per CG step), true residual at claimed convergence.
+template <class S>
+void run_cg(Work<S>& w, const S* b, S* x, const lrs_iter_cfg& cfg, bool has_x0,
+            std::vector<double>& iters, std::vector<bool>& conv, std::vector<bool>& brk) {
+  using H = HT<S>;
+  const int nr = w.nr;
+  const int64_t n = w.n;
+  const size_t blk = (size_t)n * nr;
+  DevBuf<S> buf;
+  buf.alloc(blk * 5);
+  S* r = buf.get();
+  S* z = r + blk;
+  S* p = z + blk;
+  S* q = p + blk;
+  S* tmp = q + blk;
+  const ColScalT<S> none{};
+  std::vector<double> bn(nr), bns(nr), rres(nr), tr(nr);
+  w.norms(b, bn.data());
+  for (int j = 0; j < nr; ++j) bns[j] = bn[j] > 0 ? bn[j] : 1.0;
+  if (has_x0) {
+    w.resid(b, x, r);
+  } else {
+    w.zero(x);
+    w.copy(r, b);
+  }
+  w.norms(r, rres.data());
+  conv.assign(nr, false);
+  brk.assign(nr, false);
+  iters.assign(nr, 0.0);
+  double mx = 0;
+  for (int j = 0; j < nr; ++j) {
+    conv[j] = rres[j] / bns[j] <= cfg.tol || bn[j] == 0.0;
+    mx = std::max(mx, rres[j] / bns[j]);
+  }
+  w.push(mx);
+  w.M(r, z);
+  w.copy(p, z);
+  std::vector<H> rz(nr), pq(nr), rzn(nr);
+  w.dots(r, 0, 1, z, rz.data());
+  for (int64_t it = 1; it <= cfg.max_iters; ++it) {
+    std::vector<bool> act(nr);
+    for (int j = 0; j < nr; ++j) act[j] = !conv[j] && !brk[j];
+    if (!any(act)) break;
+    for (int j = 0; j < nr; ++j)
+      if (act[j] && std::abs(rz[j]) < cfg.breakdown_eps) {
+        brk[j] = true;
+        act[j] = false;
+      }
+    if (!any(act)) break;
+    w.Aop(p, q);
+    w.dots(p, 0, 1, q, pq.data());
+    for (int j = 0; j < nr; ++j)
+      if (act[j] && std::abs(pq[j]) < cfg.breakdown_eps) {
+        brk[j] = true;
+        act[j] = false;
+      }
+    if (!any(act)) break;
+    std::vector<H> alpha(nr, H(0.0));
+    for (int j = 0; j < nr; ++j)
+      if (act[j]) alpha[j] = rz[j] / (pq[j] != H(0.0) ? pq[j] : H(1.0));
+    w.axpby(2, cs_fill<S>(alpha), none, cs_mask(act), x, p, p, nullptr);  // x += alpha p
+    w.axpby(1, cs_fill<S>(alpha), none, cs_mask(act), nullptr, r, q, r);  // r -= alpha q
+    w.norms(r, rres.data());
+    std::vector<bool> full(nr, false);
+    for (int j = 0; j < nr; ++j) full[j] = act[j] && rres[j] / bns[j] <= cfg.tol;
+    if (any(full)) {
+      w.resid(b, x, tmp);
+      w.norms(tmp, tr.data());
+      for (int j = 0; j < nr; ++j)
+        if (full[j] && tr[j] / bns[j] <= cfg.tol) {
+          conv[j] = true;
+          iters[j] = 0.5 * (double)it;
+        }
+    }
+    mx = 0;
+    for (int j = 0; j < nr; ++j)
+      if (act[j]) mx = std::max(mx, rres[j] / bns[j]);
+    w.push(mx);
+    for (int j = 0; j < nr; ++j) {
+      act[j] = act[j] && !conv[j];
+      if (act[j]) iters[j] = 0.5 * (double)it;
+    }
+    if (!any(act)) break;
+    w.M(r, z);
+    w.dots(r, 0, 1, z, rzn.data());
+    std::vector<H> beta(nr, H(0.0));
+    for (int j = 0; j < nr; ++j)
+      if (act[j]) beta[j] = rzn[j] / (rz[j] != H(0.0) ? rz[j] : H(1.0));
+    w.axpby(0, cs_fill<S>(beta), none, cs_mask(act), p, z, p, nullptr);  // p = z + beta p
+    for (int j = 0; j < nr; ++j)
+      if (act[j]) rz[j] = rzn[j];
+  }
+}
+
 // Givens rotation zeroing b against a: c real, c a + s b = d, -conj(s) a + c b = 0.
 template <class H>
 void givens(H a, H b, double* c, H* s, H* d) {
@@ -1306,6 +1401,8 @@ void solve_t(Fact* f, Mat* a, const S* b, int64_t ldb, S* x, int64_t ldx, int nr
     } else if (cfg.method == LRS_GMRES) {
       run_gmres(w, bb.get(), xx.get(), cfg, has_x0, iters, conv);
       brk.assign(nr, false);
+    } else if (cfg.method == LRS_CG) {
+      run_cg(w, bb.get(), xx.get(), cfg, has_x0, iters, conv, brk);
     } else {
       throw LrsError(LRS_ERR_PARAMETER, "unknown Krylov method");
     }
@@ -1343,7 +1440,10 @@ void solve_t(Fact* f, Mat* a, const S* b, int64_t ldb, S* x, int64_t ldx, int nr
     R.history_len = std::min<int64_t>(R.history_cap, (int64_t)hist_all.size());
     std::memcpy(R.history, hist_all.data(), sizeof(double) * R.history_len);
   }
-  if (any_brk) throw LrsError(LRS_ERR_BREAKDOWN, "BiCGStab stagnation detected (SF)");
+  if (any_brk)
+    throw LrsError(LRS_ERR_BREAKDOWN, cfg.method == LRS_CG
+                                          ? "CG breakdown (|p^H A p| or |r^H z| below breakdown_eps)"
+                                          : "BiCGStab stagnation detected (SF)");
 }
 
 }  // namespace

@@ -301,7 +301,9 @@ std::pair<DenseBlock, SolveReport> solve(const CsrMatrix& a, const DenseBlock& r
   if (rhs.rows() != a.n_rows) throw DimensionError("solve: rhs rows must equal n");
   const IterConfig& it = cfg.outer;
   lrs_iter_cfg ic{};
-  ic.method = it.method == Method::GMRES ? LRS_GMRES : LRS_BICGSTAB;
+  ic.method = it.method == Method::GMRES ? LRS_GMRES
+              : it.method == Method::CG  ? LRS_CG
+                                         : LRS_BICGSTAB;
   ic.restart = it.restart;
   ic.tol = it.tol;
   ic.max_iters = it.max_iters;

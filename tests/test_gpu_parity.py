@@ -218,3 +218,20 @@ def test_error_paths(ctx):
     with pytest.raises(api.SingularBlockError) as es:
         api.factorize(ctx, Az, api.SolverConfig(variant="BJ", p=1, k=0, n_svd=0))
     assert es.value.column == 1
+
+
+@pytest.mark.parametrize("variant,r", [("BJ", 0), ("T", 8)])
+def test_cg_parity(ctx, variant, r):
+    """PCG on the SPD c1 system: GPU vs oracle."""
+    cfg = configs.make_config("c1", 64 / 256)
+    S = cfg.matrix.to_scipy()
+    A = api.CsrMatrix.from_csr(ctx, cfg.matrix)
+    it = api.IterConfig(tol=1e-9, method="cg", max_iters=800)
+    x, rep, F = api.solve(A, cfg.rhs, _gpu_cfg(cfg, r, variant), it)
+    xo, repo, _ = O.solve(S, cfg.rhs, _oracle_cfg(cfg, r, variant),
+                          O.IterConfig(tol=1e-9, max_iters=800), method="cg")
+    assert rep.converged and repo.converged
+    assert rep.residual_final <= 1e-9
+    assert abs(rep.iterations - repo.iterations) <= 2
+    assert _rel(x, xo) <= 1e-8
+    assert rep.precond_applications == 2 * rep.iterations
