@@ -487,15 +487,26 @@ def matvec_exact(tipsT: list, tipsW: list, xt: list, xb: list):
 
 @dataclass
 class SolverConfig:
-    """SPEC.md:470-473 (outer IterConfig is passed to solve separately)."""
+    """SPEC.md:470-473 (outer IterConfig is passed to solve separately).
 
-    variant: str = "T"  # "T" (LR-SPIKE-T) | "BJ" (Block Jacobi)
+    variant: "T" (LR-SPIKE-T), "I" (LR-SPIKE-I), "OTF" (LR-SPIKE-OTF), "BJ" (Block
+    Jacobi).  inner: the LR-SPIKE-I reduced solve (SPEC.md:472 names 1e-16 after the
+    paper's Table 3; a BiCGStab true residual cannot certify 1e-16 in FP64, so the
+    default here is 1e-12); otf_tol / otf_escalations: LR-SPIKE-OTF's reduced-system
+    tolerance and its escalation schedule (/100 per escalation, at most 4)."""
+
+    variant: str = "T"
     p: int = 4
     k: int | None = None  # None -> band_metrics(A).k
     n_svd: int = 8
     oversample: int | None = None  # None -> ceil(n_svd/2) (SPEC.md:311)
     passes: int = 2
     seed: int = 0
+    inner_tol: float = 1e-12
+    inner_max_iters: int = 200
+    otf_tol: float = 1e-8
+    otf_max_iters: int = 500
+    otf_escalations: int = 4
 
 
 @dataclass
@@ -509,6 +520,8 @@ class SpikeFactorization:
     n_svd: int
     ledger: CommLedger = field(default_factory=CommLedger)
     rank_collapsed: bool = False
+    inner_iterations: float = 0.0  # LR-SPIKE-I: inner half-iterations summed over applies
+    inner_solves: int = 0
 
 
 def factorize(A: sp.csr_matrix, cfg: SolverConfig) -> SpikeFactorization:
@@ -520,7 +533,9 @@ def factorize(A: sp.csr_matrix, cfg: SolverConfig) -> SpikeFactorization:
     lay = make_layout(A.shape[0], cfg.p, k)
     blocks = extract_blocks(A, lay)
     factors = [factorize_block(Ai) for Ai in blocks.A]
-    n_svd = cfg.n_svd if cfg.variant == "T" else 0
+    if cfg.variant not in ("T", "I", "OTF", "BJ"):
+        raise ParameterError(f"unknown variant {cfg.variant!r}")
+    n_svd = cfg.n_svd if cfg.variant in ("T", "I", "OTF") else 0
     for attempt in range(2):
         spT, spW, trunc, coll = _build_spikes(blocks, factors, cfg, n_svd, k)
         try:
@@ -570,6 +585,81 @@ def apply_precond_T(F: SpikeFactorization, f: np.ndarray) -> np.ndarray:
     top = [y[:k] for y in ys]
     bot = [y[-k:] for y in ys]
     xt, xb = apply_truncated_precond(F.trunc, top, bot, F.ledger)
+    return _lowrank_recovery(F, ys, xt, xb, f2.shape[1]).reshape(f.shape)
+
+
+def _pack(xt, xb):
+    """ReducedVector as one 2kp x n_rhs block: partition i's top tip
+    in rows [2ki, 2ki+k), its bottom tip in [2ki+k, 2k(i+1))."""
+    return np.concatenate([np.concatenate([t, b]) for t, b in zip(xt, xb)])
+
+
+def _unpack(v, p, k):
+    v = v.reshape(v.shape[0], -1)
+    return ([v[2 * k * i:2 * k * i + k] for i in range(p)],
+            [v[2 * k * i + k:2 * k * (i + 1)] for i in range(p)])
+
+
+def matvec_lowrank(F: SpikeFactorization, xt: list, xb: list, ledger=None):
+    """y_i = x_i + W~_i x_{i-1,b} + T~_i x_{i+1,t} with the low-rank
+    spikes: the owner of x_{i-1,b} sends the compressed message S_W v_W x_{i-1,b}
+    (r x n_rhs), the owner of x_{i+1,t} sends S_T v_T x_{i+1,t}; the receiver applies
+    its u tips (top k and bottom k rows).  W term first, then T term."""
+    p = len(xt)
+    k = F.blocks.layout.k
+    yt = [a.copy() for a in xt]
+    yb = [a.copy() for a in xb]
+    nr = xt[0].shape[1]
+    for i in range(p):
+        if i > 0:
+            s = F.spW[i]
+            m = s.sigma[:, None] * (s.v @ xb[i - 1])
+            yt[i] = yt[i] + s.u[:k] @ m
+            yb[i] = yb[i] + s.u[-k:] @ m
+            if ledger is not None:
+                ledger.record("reduced-matvec", 1, F.n_svd * nr)
+        if i < p - 1:
+            s = F.spT[i]
+            m = s.sigma[:, None] * (s.v @ xt[i + 1])
+            yt[i] = yt[i] + s.u[:k] @ m
+            yb[i] = yb[i] + s.u[-k:] @ m
+            if ledger is not None:
+                ledger.record("reduced-matvec", 1, F.n_svd * nr)
+    return yt, yb
+
+
+def _coupled_solve(F: SpikeFactorization, xt: list, xb: list, nr: int):
+    """z_i = A_i^-1 (pad_top(C_i x_{i-1,b}) + pad_bottom(B_i x_{i+1,t})) = W_i x_{i-1,b}
+    + T_i x_{i+1,t} with the exact spikes (padded solve_block)."""
+    lay = F.blocks.layout
+    k, p = lay.k, lay.p
+    zs = []
+    for i in range(p):
+        n_i = lay.sizes[i]
+        dt = np.result_type(xt[0].dtype, F.factors[i].dtype)
+        rhs = np.zeros((n_i, nr), dtype=dt)
+        if i > 0:
+            rhs[:k] += np.asarray(F.blocks.C[i] @ xb[i - 1])
+        if i < p - 1:
+            rhs[n_i - k:] += np.asarray(F.blocks.B[i] @ xt[i + 1])
+        zs.append(solve_block(F.factors[i], rhs))
+    return zs
+
+
+def matvec_otf(F: SpikeFactorization, xt: list, xb: list, ledger=None):
+    """the TRUE reduced matvec, tips of the exact spikes evaluated on
+    the fly (right to left: couplings, padded block solve, first/last k rows); the
+    messages are the uncompressed k x n_rhs neighbour tips."""
+    p = len(xt)
+    k = F.blocks.layout.k
+    nr = xt[0].shape[1]
+    zs = _coupled_solve(F, xt, xb, nr)
+    if ledger is not None and p > 1:
+        ledger.record("reduced-matvec", 2 * (p - 1), 2 * (p - 1) * k * nr)
+    return ([xt[i] + zs[i][:k] for i in range(p)], [xb[i] + zs[i][-k:] for i in range(p)])
+
+
+def _lowrank_recovery(F, ys, xt, xb, nr):
     p = len(ys)
     out = []
     for i, y in enumerate(ys):
@@ -577,13 +667,112 @@ def apply_precond_T(F: SpikeFactorization, f: np.ndarray) -> np.ndarray:
         if i > 0:
             s = F.spW[i]
             x -= s.u @ (s.sigma[:, None] * (s.v @ xb[i - 1]))
-            F.ledger.record("recovery", 1, F.n_svd * f2.shape[1])
+            F.ledger.record("recovery", 1, F.n_svd * nr)
         if i < p - 1:
             s = F.spT[i]
             x -= s.u @ (s.sigma[:, None] * (s.v @ xt[i + 1]))
-            F.ledger.record("recovery", 1, F.n_svd * f2.shape[1])
+            F.ledger.record("recovery", 1, F.n_svd * nr)
         out.append(x)
-    return np.concatenate(out).reshape(f.shape)
+    return np.concatenate(out)
+
+
+class PreconditionerFailureError(Error):
+    """LR-SPIKE-I inner reduced solve did not converge; carries the
+    inner SolveReport."""
+
+    def __init__(self, msg, report):
+        super().__init__(msg)
+        self.report = report
+
+
+def apply_precond_I(F: SpikeFactorization, f: np.ndarray) -> np.ndarray:
+    """D-stage; inner BiCGStab on the low-rank reduced system S~_r
+    (operator matvec_lowrank, preconditioner apply_truncated_precond, tolerance
+    cfg.inner_tol); recovery with the low-rank spikes as in apply_precond_T.  Inner
+    iterations are accumulated on F (reported with the outer solve)."""
+    if F.n_svd == 0 or F.trunc is None:
+        return apply_block_jacobi(F, f)
+    f2 = f.reshape(f.shape[0], -1)
+    lay = F.blocks.layout
+    k, p = lay.k, lay.p
+    ys = [solve_block(Fi, fi) for Fi, fi in zip(F.factors, _split(F, f2))]
+    g = _pack([y[:k] for y in ys], [y[-k:] for y in ys])
+    # the inner solve runs on the column-normalised reduced right-hand side (and scales
+    # back): the reduced system is linear, and the absolute breakdown threshold then
+    # does not fire on the tiny residuals an outer solve applies M to near convergence
+    gn = _cnorm(g)
+    gs = np.where(gn > 0, gn, 1.0)
+    A_r = lambda v: _pack(*matvec_lowrank(F, *_unpack(v, p, k), F.ledger))  # noqa: E731
+    M_r = lambda v: _pack(*apply_truncated_precond(F.trunc, *_unpack(v, p, k), F.ledger))  # noqa: E731
+    icfg = IterConfig(tol=F.cfg.inner_tol, max_iters=F.cfg.inner_max_iters)
+    try:
+        xr, rep = bicgstab(A_r, M_r, g / gs, icfg)
+        xr = xr * gs
+    except BreakdownError as e:
+        raise PreconditionerFailureError("LR-SPIKE-I inner solve broke down", e.report)
+    if not rep.converged:
+        raise PreconditionerFailureError("LR-SPIKE-I inner solve did not converge", rep)
+    F.inner_iterations += rep.iterations
+    F.inner_solves += 1
+    xt, xb = _unpack(xr, p, k)
+    return _lowrank_recovery(F, ys, xt, xb, f2.shape[1]).reshape(f.shape)
+
+
+def solve_otf(A: sp.csr_matrix, F: SpikeFactorization, f: np.ndarray, it: "IterConfig"):
+    """D-stage once; BiCGStab on the TRUE reduced system (matvec_otf)
+    preconditioned by apply_truncated_precond to cfg.otf_tol; exact recovery
+    x_i = y_i - A_i^-1 (pad_top(C_i x_{i-1,b}) + pad_bottom(B_i x_{i+1,t})); if the full
+    relative residual misses it.tol, the reduced tolerance is divided by 100 and the
+    reduced solve restarts warm from the previous x_r, at most cfg.otf_escalations
+    times; exhausted -> the last x with converged = False.  iterations = reduced
+    BiCGStab half-iterations summed over the escalations."""
+    f2 = np.asarray(f).reshape(f.shape[0], -1)
+    lay = F.blocks.layout
+    k, p = lay.k, lay.p
+    nr = f2.shape[1]
+    ys = [solve_block(Fi, fi) for Fi, fi in zip(F.factors, _split(F, f2))]
+    g = _pack([y[:k] for y in ys], [y[-k:] for y in ys])
+    rep = SolveReport()
+    rep.precond_applications = 1  # the D-stage
+    bn = _cnorm(f2)
+    bn_safe = np.where(bn > 0, bn, 1.0)
+    if F.n_svd == 0 or F.trunc is None or p == 1:
+        M_r = lambda v: v  # noqa: E731
+    else:
+        M_r = lambda v: _pack(*apply_truncated_precond(F.trunc, *_unpack(v, p, k), F.ledger))  # noqa: E731
+    A_r = lambda v: _pack(*matvec_otf(F, *_unpack(v, p, k), F.ledger))  # noqa: E731
+    if p == 1 or all(B.nnz == 0 for B in F.blocks.B) and all(C.nnz == 0 for C in F.blocks.C[1:]):
+        # no coupling: S_r = I, x = D^-1 f with zero reduced iterations (SPEC.md:509)
+        x = np.concatenate(ys)
+        rep.residual_final = float(np.max(_cnorm(f2 - A @ x) / bn_safe))
+        rep.converged = bool(rep.residual_final <= it.tol)
+        return x.reshape(np.asarray(f).shape), rep
+    tol = F.cfg.otf_tol
+    xr0 = None
+    x = None
+    total = 0.0
+    for esc in range(F.cfg.otf_escalations + 1):
+        rcfg = IterConfig(tol=tol, max_iters=F.cfg.otf_max_iters,
+                          breakdown_eps=it.breakdown_eps, initial_guess=xr0)
+        xr, rr = bicgstab(A_r, M_r, g, rcfg)
+        total += rr.iterations
+        rep.matvecs += rr.matvecs
+        rep.residual_history.extend(rr.residual_history)
+        xt, xb = _unpack(xr, p, k)
+        zs = _coupled_solve(F, xt, xb, nr)
+        if p > 1:
+            F.ledger.record("recovery", 2 * (p - 1), 2 * (p - 1) * k * nr)
+        x = np.concatenate([ys[i] - zs[i] for i in range(p)])
+        res = _cnorm(f2 - A @ x) / bn_safe
+        rep.matvecs += 1
+        if np.all(res <= it.tol):
+            rep.converged = True
+            break
+        tol /= 100.0
+        xr0 = xr
+    rep.iterations = total
+    rep.residual_final = float(np.max(_cnorm(f2 - A @ x) / bn_safe))
+    return x.reshape(np.asarray(f).shape), rep
 
 
 # --------------------------------------------------------------------------------------
@@ -614,6 +803,7 @@ class SolveReport:
     matvecs: int = 0
     residual_final: float = math.nan
     breakdown: bool = False
+    inner_iterations: float = 0.0  # LR-SPIKE-I inner half-iterations (summed)
 
 
 def _cnorm(X):
@@ -913,8 +1103,11 @@ def solve(A: sp.csr_matrix, f: np.ndarray, cfg: SolverConfig, it: IterConfig,
     A = sp.csr_matrix(A)
     if F is None:
         F = factorize(A, cfg)
-    M = (lambda v: apply_precond_T(F, v)) if cfg.variant == "T" else (
-        lambda v: apply_block_jacobi(F, v))
+    if cfg.variant == "OTF":
+        return (*solve_otf(A, F, f, it), F)
+    inner0 = F.inner_iterations
+    M = {"T": lambda v: apply_precond_T(F, v), "I": lambda v: apply_precond_I(F, v),
+         "BJ": lambda v: apply_block_jacobi(F, v)}[cfg.variant]
     Aop = lambda v: A @ v  # noqa: E731
     if method == "bicgstab":
         x, rep = bicgstab(Aop, M, f, it)
@@ -924,4 +1117,5 @@ def solve(A: sp.csr_matrix, f: np.ndarray, cfg: SolverConfig, it: IterConfig,
         x, rep = cg(Aop, M, f, it)
     else:
         raise ParameterError(method)
+    rep.inner_iterations = F.inner_iterations - inner0
     return x, rep, F
