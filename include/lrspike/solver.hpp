@@ -32,7 +32,8 @@ struct PartitionLayout {
 /// first (n mod p) partitions get ceil(n/p) rows; every n_i > k.
 PartitionLayout make_layout(index_t n, index_t p, index_t k);
 
-enum class Variant { LR_SPIKE_T, BLOCK_JACOBI };
+// Table 1 of the paper / SPEC.md:470
+enum class Variant { LR_SPIKE_T, BLOCK_JACOBI, LR_SPIKE_I, LR_SPIKE_OTF };
 enum class Method { BICGSTAB, GMRES, CG };  // CG: SPEC.md:430-436
 
 /// SPEC.md:411-414 (+ method / restart).
@@ -55,6 +56,12 @@ struct SolverConfig {
   int passes = 2;
   std::uint64_t seed = 0;
   IterConfig outer;
+  // LR-SPIKE-I inner reduced solve (BiCGStab); LR-SPIKE-OTF reduced solve
+  double inner_tol = 1e-12;
+  index_t inner_max_iters = 200;
+  double otf_tol = 1e-8;
+  index_t otf_max_iters = 500;
+  int otf_escalations = 4;
 };
 
 /// SPEC.md:466-469.
@@ -78,6 +85,8 @@ struct SolveReport {
   std::uint64_t seed = 0;
   double wall_time = 0.0;
   double residual_final = 0.0;
+  double inner_iterations = 0.0;  // LR-SPIKE-I: inner half-iterations summed over applies
+  index_t inner_solves = 0;
 };
 
 /// A CUDA device + stream (lrs_ctx).  device() returns the process default (GPU 0).

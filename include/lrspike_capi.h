@@ -15,9 +15,12 @@
  *   lrs_factorize           factorize (extract_blocks, factorize_block, randomized_spike_svd,
  *                           build_truncated_precond)    SPEC.md:476-484 (:180, :217, :286, :367)
  *   lrs_solve_block         solve_block / solve_block_adjoint
- *   lrs_apply_precond       apply_precond_T
+ *   lrs_apply_precond       the factorization's preconditioner: apply_precond_I for
+ *                           LR-SPIKE-I, apply_precond_T for T / OTF
+ *   lrs_apply_precond_T     apply_precond_T
  *   lrs_apply_block_jacobi  apply_block_jacobi
- *   lrs_solve               solve + bicgstab / GMRES(m) SPEC.md:520-528, :421-429 (GMRES: SURVEY D1)
+ *   lrs_solve               solve + bicgstab / cg / GMRES(m), solve_otf for LR-SPIKE-OTF
+ *                           SPEC.md:520-528, :421-436, :503-511 (GMRES: SURVEY D1)
  *   lrs_last_error          the exception taxonomy      proj/core/include/lrspike/errors.hpp:11-94
  *
  * Memory: pointers tagged LRS_MEM_HOST are copied by the library (the caller
@@ -61,12 +64,19 @@ typedef enum lrs_status {
   LRS_ERR_CUDA = 11,
   LRS_ERR_OOM = 12,
   LRS_ERR_NCCL = 13,
-  LRS_ERR_NOT_IMPLEMENTED = 14            /* e.g. a block that needs row interchanges */
+  LRS_ERR_NOT_IMPLEMENTED = 14,           /* e.g. a block that needs row interchanges */
+  LRS_ERR_PRECOND_FAILURE = 15            /* LR-SPIKE-I inner solve did not converge */
 } lrs_status;
 
 typedef enum lrs_scalar { LRS_F64 = 0, LRS_C128 = 1 } lrs_scalar;
 typedef enum lrs_mem { LRS_MEM_HOST = 0, LRS_MEM_DEVICE = 1 } lrs_mem;
-typedef enum lrs_variant { LRS_VARIANT_T = 0, LRS_VARIANT_BJ = 1 } lrs_variant;
+/* Table 1 of the paper / SPEC.md:470: LR-SPIKE-T, Block Jacobi, LR-SPIKE-I, LR-SPIKE-OTF. */
+typedef enum lrs_variant {
+  LRS_VARIANT_T = 0,
+  LRS_VARIANT_BJ = 1,
+  LRS_VARIANT_I = 2,  /* apply_precond_I */
+  LRS_VARIANT_OTF = 3 /* solve_otf, SPEC.md:503-511 (lrs_solve runs it; no apply) */
+} lrs_variant;
 typedef enum lrs_method { LRS_GMRES = 0, LRS_BICGSTAB = 1, LRS_CG = 2 } lrs_method;
 typedef enum lrs_side { LRS_SIDE_T = 0, LRS_SIDE_W = 1 } lrs_side;
 
@@ -82,6 +92,14 @@ typedef struct lrs_solver_cfg {
   int64_t n_svd;      /* retained rank r */
   int64_t oversample; /* < 0 -> ceil(n_svd / 2) */
   uint64_t seed;      /* Omega streams (seed, partition, side) */
+  /* LR-SPIKE-I inner reduced solve ("inner"): <= 0 -> 1e-12 / 200 */
+  double inner_tol;
+  int64_t inner_max_iters;
+  /* LR-SPIKE-OTF reduced solve ("otf_redsys"): <= 0 -> 1e-8 / 500;
+     escalations (tolerance / 100 each): < 0 -> 4, 0 = none */
+  double otf_tol;
+  int64_t otf_max_iters;
+  int32_t otf_escalations;
 } lrs_solver_cfg;
 
 /* IterConfig, SPEC.md:411-414 (+ method, GMRES restart). */
@@ -110,6 +128,8 @@ typedef struct lrs_report {
   int64_t history_cap;
   int64_t history_len;          /* entries written (<= cap); total produced in history_total */
   int64_t history_total;
+  double inner_iterations;      /* LR-SPIKE-I: inner half-iterations summed over the applies */
+  int64_t inner_solves;         /* LR-SPIKE-I: inner solves (one per applied column batch) */
 } lrs_report;
 
 /* Read-only facts about a factorization. */
@@ -195,6 +215,8 @@ LRS_API lrs_status lrs_apply_precond(lrs_fact* f, const void* in, int64_t ld_in,
                                      int64_t ld_out, int64_t n_rhs, int32_t mem);
 LRS_API lrs_status lrs_apply_block_jacobi(lrs_fact* f, const void* in, int64_t ld_in, void* out,
                                           int64_t ld_out, int64_t n_rhs, int32_t mem);
+LRS_API lrs_status lrs_apply_precond_T(lrs_fact* f, const void* in, int64_t ld_in, void* out,
+                                       int64_t ld_out, int64_t n_rhs, int32_t mem);
 
 /* ---- solve ------------------------------------------------------------------------ */
 LRS_API lrs_status lrs_solve(lrs_fact* f, lrs_mat* a, const void* b, int64_t ldb, void* x,

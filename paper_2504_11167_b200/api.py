@@ -29,7 +29,8 @@ _LIBPATH = os.environ.get("LRS_LIB") or os.path.join(_HERE, "liblrspike_cuda.so"
 LRS_OK = 0
 F64, C128 = 0, 1
 MEM_HOST, MEM_DEVICE = 0, 1
-VARIANT_T, VARIANT_BJ = 0, 1
+VARIANT_T, VARIANT_BJ, VARIANT_I, VARIANT_OTF = 0, 1, 2, 3
+_VARIANTS = {"T": VARIANT_T, "BJ": VARIANT_BJ, "I": VARIANT_I, "OTF": VARIANT_OTF}
 GMRES, BICGSTAB, CG = 0, 1, 2
 _METHODS = {"gmres": GMRES, "bicgstab": BICGSTAB, "cg": CG}
 SIDE_T, SIDE_W = 0, 1
@@ -43,7 +44,8 @@ vp = ctypes.c_void_p
 
 class SolverCfgC(ctypes.Structure):
     _fields_ = [("variant", i32), ("passes", i32), ("p", i64), ("k", i64), ("n_svd", i64),
-                ("oversample", i64), ("seed", u64)]
+                ("oversample", i64), ("seed", u64), ("inner_tol", f64), ("inner_max_iters", i64),
+                ("otf_tol", f64), ("otf_max_iters", i64), ("otf_escalations", i32)]
 
 
 class IterCfgC(ctypes.Structure):
@@ -56,7 +58,8 @@ class ReportC(ctypes.Structure):
                 ("precond_applications", i64), ("matvecs", i64), ("residual_final", f64),
                 ("comm_messages", i64 * 3), ("comm_scalars", i64 * 3), ("t_solve", f64),
                 ("seed", u64), ("history", ctypes.POINTER(f64)), ("history_cap", i64),
-                ("history_len", i64), ("history_total", i64)]
+                ("history_len", i64), ("history_total", i64), ("inner_iterations", f64),
+                ("inner_solves", i64)]
 
 
 class FactInfoC(ctypes.Structure):
@@ -144,6 +147,10 @@ class NotImplementedOnGpu(Error):
     pass
 
 
+class PreconditionerFailureError(Error):
+    """LR-SPIKE-I inner reduced solve did not converge."""
+
+
 _lib = None
 
 
@@ -179,6 +186,7 @@ def lib():
         "lrs_solve_block": (i32, [vp, i64, vp, i64, vp, i64, i64, i32, i32]),
         "lrs_apply_precond": (i32, [vp, vp, i64, vp, i64, i64, i32]),
         "lrs_apply_block_jacobi": (i32, [vp, vp, i64, vp, i64, i64, i32]),
+        "lrs_apply_precond_T": (i32, [vp, vp, i64, vp, i64, i64, i32]),
         "lrs_solve": (i32, [vp, vp, vp, i64, vp, i64, i64, P(IterCfgC), P(ReportC), i32]),
         "lrs_bench_dmma_peak": (i32, [vp, P(f64)]),
         "lrs_ctx_set_profiling": (i32, [vp, i32]),
@@ -195,7 +203,7 @@ def lib():
 _EXC = {1: ParseError, 2: UnsupportedFieldError, 3: DimensionError, 4: SingularScalingError,
         5: LayoutError, 6: NotBlockTridiagonalError, 7: SingularBlockError, 8: ParameterError,
         9: IllConditionedInterfaceError, 10: BreakdownError, 11: CudaError, 12: OutOfMemoryError,
-        13: CudaError, 14: NotImplementedOnGpu}
+        13: CudaError, 14: NotImplementedOnGpu, 15: PreconditionerFailureError}
 
 
 def _raise(status: int, ctx_handle=None):
@@ -380,7 +388,9 @@ def make_layout(n: int, p: int, k: int) -> list:
 
 @dataclass
 class SolverConfig:
-    """SPEC.md:470-473 (variant "T" = LR-SPIKE-T, "BJ" = Block Jacobi)."""
+    """SPEC.md:470-473.  variant: "T" (LR-SPIKE-T), "I" (LR-SPIKE-I), "OTF"
+    (LR-SPIKE-OTF), "BJ" (Block Jacobi); inner_*: the LR-SPIKE-I reduced solve; otf_*:
+    the LR-SPIKE-OTF reduced solve and its tolerance escalations."""
 
     variant: str = "T"
     p: int = 4
@@ -389,11 +399,19 @@ class SolverConfig:
     oversample: int | None = None
     passes: int = 2
     seed: int = 0
+    inner_tol: float = 1e-12
+    inner_max_iters: int = 200
+    otf_tol: float = 1e-8
+    otf_max_iters: int = 500
+    otf_escalations: int = 4
 
     def c(self):
-        return SolverCfgC(VARIANT_T if self.variant == "T" else VARIANT_BJ, self.passes, self.p,
-                          self.k or 0, self.n_svd,
-                          -1 if self.oversample is None else self.oversample, self.seed)
+        if self.variant not in _VARIANTS:
+            raise ParameterError(f"unknown variant {self.variant!r}")
+        return SolverCfgC(_VARIANTS[self.variant], self.passes, self.p, self.k or 0, self.n_svd,
+                          -1 if self.oversample is None else self.oversample, self.seed,
+                          self.inner_tol, self.inner_max_iters, self.otf_tol, self.otf_max_iters,
+                          self.otf_escalations)
 
 
 @dataclass
@@ -422,6 +440,8 @@ class SolveReport:
     seed: int
     wall_time: float
     breakdown: bool
+    inner_iterations: float = 0.0  # LR-SPIKE-I inner half-iterations (summed)
+    inner_solves: int = 0
 
 
 class SpikeFactorization:
@@ -471,6 +491,16 @@ class SpikeFactorization:
 
     def apply_precond_T(self, f, out=None):
         """SPEC.md:485-493 (Block Jacobi if the factorization has n_svd = 0)."""
+        return self._apply(lib().lrs_apply_precond_T, f, out)
+
+    def apply_precond_I(self, f, out=None):
+        """SPEC.md:494-502 (an LR-SPIKE-I factorization)."""
+        if self.cfg.variant != "I":
+            raise ParameterError("apply_precond_I needs a variant 'I' factorization")
+        return self._apply(lib().lrs_apply_precond, f, out)
+
+    def apply(self, f, out=None):
+        """The factorization's own preconditioner (I, T or Block Jacobi)."""
         return self._apply(lib().lrs_apply_precond, f, out)
 
     def apply_block_jacobi(self, f, out=None):
@@ -555,7 +585,8 @@ def solve(A: CsrMatrix, f, cfg: SolverConfig | None = None, it: IterConfig | Non
     report = SolveReport(bool(rep.converged), rep.iterations, list(hist[:rep.history_len]),
                          rep.precond_applications, rep.matvecs, rep.residual_final,
                          {STAGES[i]: (rep.comm_messages[i], rep.comm_scalars[i]) for i in range(3)},
-                         rep.seed, rep.t_solve, bool(rep.breakdown))
+                         rep.seed, rep.t_solve, bool(rep.breakdown), rep.inner_iterations,
+                         rep.inner_solves)
     if st == 10:
         info = ErrorInfoC()
         lib().lrs_last_error(A.ctx.h, ctypes.byref(info))

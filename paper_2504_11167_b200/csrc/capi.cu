@@ -124,6 +124,7 @@ const char* lrs_status_string(lrs_status s) {
     case LRS_ERR_OOM: return "OutOfMemory";
     case LRS_ERR_NCCL: return "NcclError";
     case LRS_ERR_NOT_IMPLEMENTED: return "NotImplemented";
+    case LRS_ERR_PRECOND_FAILURE: return "PreconditionerFailureError";
   }
   return "unknown";
 }
@@ -512,7 +513,7 @@ lrs_status lrs_solve_block(lrs_fact* f, int64_t i, const void* rhs, int64_t ld_r
 }
 
 static lrs_status apply_common(lrs_fact* f, const void* in, int64_t ld_in, void* out,
-                               int64_t ld_out, int64_t n_rhs, int32_t mem, bool bj) {
+                               int64_t ld_out, int64_t n_rhs, int32_t mem, int mode) {
   if (!f) return LRS_ERR_PARAMETER;
   Ctx* c = f->ctx;
   return guard(c, [&] {
@@ -520,25 +521,30 @@ static lrs_status apply_common(lrs_fact* f, const void* in, int64_t ld_in, void*
     if (ld_in < f->n || ld_out < f->n || n_rhs < 0)
       throw LrsError(LRS_ERR_DIMENSION, "apply: vector rows must equal n");
     if (mem == LRS_MEM_DEVICE) {
-      apply_precond(f, in, ld_in, out, ld_out, (int)n_rhs, bj);
+      apply_precond(f, in, ld_in, out, ld_out, (int)n_rhs, mode);
       return;
     }
     DevBuf<double> io;
     int64_t ld;
     void* d = dev_in(c, in, ld_in, f->n, n_rhs, mem, io, &ld, f->sw);
-    apply_precond(f, d, ld, d, ld, (int)n_rhs, bj);
+    apply_precond(f, d, ld, d, ld, (int)n_rhs, mode);
     dev_out_finish(c, out, ld_out, d, f->n, n_rhs, mem, f->sw);
   });
 }
 
 lrs_status lrs_apply_precond(lrs_fact* f, const void* in, int64_t ld_in, void* out, int64_t ld_out,
                              int64_t n_rhs, int32_t mem) {
-  return apply_common(f, in, ld_in, out, ld_out, n_rhs, mem, false);
+  return apply_common(f, in, ld_in, out, ld_out, n_rhs, mem, APPLY_VARIANT);
 }
 
 lrs_status lrs_apply_block_jacobi(lrs_fact* f, const void* in, int64_t ld_in, void* out,
                                   int64_t ld_out, int64_t n_rhs, int32_t mem) {
-  return apply_common(f, in, ld_in, out, ld_out, n_rhs, mem, true);
+  return apply_common(f, in, ld_in, out, ld_out, n_rhs, mem, APPLY_BJ);
+}
+
+lrs_status lrs_apply_precond_T(lrs_fact* f, const void* in, int64_t ld_in, void* out,
+                               int64_t ld_out, int64_t n_rhs, int32_t mem) {
+  return apply_common(f, in, ld_in, out, ld_out, n_rhs, mem, APPLY_T);
 }
 
 lrs_status lrs_solve(lrs_fact* f, lrs_mat* a, const void* b, int64_t ldb, void* x, int64_t ldx,

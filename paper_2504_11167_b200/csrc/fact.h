@@ -47,6 +47,7 @@ struct Fact {
   DevBuf<int> degen;
   DevBuf<double> scT, scW;     // per global partition, r x MAX_RHS
   DevBuf<unsigned char> iface_jobs;  // IfaceApplyJobT<S>[ni]
+  DevBuf<unsigned char> iface_jobs_red;  // the same with compact reduced-vector tip rows
   DevBuf<double> iface_work, iface_msg;
   int job_left = -1, job_right = -1;  // jobs of the cross-GPU interfaces (or -1)
   // deterministic reductions (partition-aligned chunks, partition-ordered sums)
@@ -54,6 +55,19 @@ struct Fact {
   std::vector<int> part_first;
   DevBuf<int64_t> d_chunks;
   DevBuf<int> d_part_first;
+  // the compact reduced space of LR-SPIKE-I / OTF: 2k rows per partition, ld = ldr
+  int64_t ldr = 0;
+  std::vector<int64_t> rchunk_start;
+  std::vector<int> rpart_first;
+  DevBuf<int64_t> d_rchunks;
+  DevBuf<int> d_rpart_first;
+  // variant parameters (lrs_solver_cfg) and the LR-SPIKE-I inner-solve statistics
+  double inner_tol = 1e-12, otf_tol = 1e-8;
+  int64_t inner_max_iters = 200, otf_max_iters = 500;
+  int otf_escalations = 4;
+  bool coupled = true;  // some coupling block B_i / C_i is nonzero (OTF short-circuit)
+  double inner_iterations = 0.0;
+  int64_t inner_solves = 0;
   DevBuf<double> partial, persum, gather, dotout;
   std::vector<int> rank_pl;    // local partition count of every rank
   DevBuf<int> d_rank_pl;
@@ -86,6 +100,9 @@ struct Fact {
   Chunks chunks() const {
     return Chunks{d_chunks.get(), d_part_first.get(), (int)chunk_start.size() - 1, P};
   }
+  Chunks rchunks() const {
+    return Chunks{d_rchunks.get(), d_rpart_first.get(), (int)rchunk_start.size() - 1, P};
+  }
   unsigned next_epoch() { return ++epoch; }
   int rank() const { return dist ? comm.rank : 0; }
   int nranks() const { return dist ? comm.size : 1; }
@@ -98,9 +115,11 @@ Fact* factorize(Ctx* c, Mat* m, const lrs_solver_cfg& cfg, const lrs_comm* comm)
 // D-stage solve (local partitions, or local partition p_only >= 0), in place on x.
 // Vectors are double* (LRS_F64) or interleaved complex128 (LRS_C128) per f->scalar.
 void dstage(Fact* f, void* x, int64_t ld, int nrhs, bool adjoint, int p_only);
-// M^-1 applied to in -> out on the local rows, variant T or Block Jacobi.
+// M^-1 applied to in -> out on the local rows.  mode: APPLY_VARIANT (the factorization's
+// own preconditioner: I, T or Block Jacobi), APPLY_BJ (D-stage only), APPLY_T.
+enum { APPLY_VARIANT = 0, APPLY_BJ = 1, APPLY_T = 2 };
 void apply_precond(Fact* f, const void* in, int64_t ldi, void* out, int64_t ldo, int nrhs,
-                   bool block_jacobi);
+                   int mode);
 void solve(Fact* f, Mat* a, const void* b, int64_t ldb, void* x, int64_t ldx, int nrhs,
            const lrs_iter_cfg& cfg, lrs_report* rep);
 

@@ -30,10 +30,10 @@ struct CoupleJobT {
   int ncols;
 };
 using CoupleJob = CoupleJobT<double>;
-// transposed: use A^T (conjugated for complex: the adjoint couplings)
+// transposed: use A^T (conjugated for complex: the adjoint couplings); accumulate: out +=
 template <class S>
 void launch_coupling_t(Ctx* c, const Mat* m, bool transposed, const CoupleJobT<S>* d_jobs,
-                       int njobs, int64_t b, int ncols);
+                       int njobs, int64_t b, int ncols, bool accumulate = false);
 void launch_spmv_z(Ctx* c, const Mat* m, const zc* x, int64_t ldx, zc* y, int64_t ldy, int nrhs,
                    int mode, const zc* b, int64_t ldb, int64_t row_lo = 0, int64_t row_hi = -1);
 
@@ -151,6 +151,19 @@ template <class S>
 void launch_recovery_t(Ctx* c, const BandGeom& g, int64_t n, int64_t row_lo, int64_t row_hi,
                        const S* y, int64_t ldy, S* x, int64_t ldx, int nrhs, const S* uT,
                        const S* uW, int r, const S* scT, const S* scW);
+
+// ---- reduced.cu (LR-SPIKE-I / OTF reduced system, compact 2k-per-partition layout) ----
+template <class S>
+void launch_tips_gather_t(Ctx* c, const BandGeom& g, int64_t k, const S* y, int64_t ldy,
+                          const S* x, S* r, int64_t ldr, int nrhs);
+template <class S>
+void launch_tips_lowrank_t(Ctx* c, const BandGeom& g, int64_t n, int64_t k, const S* in, S* out,
+                           int64_t ldr, int nrhs, const S* uT, const S* uW, int r, const S* scT,
+                           const S* scW, int mode, double sign);
+template <class S>
+void launch_iface_scale_t(Ctx* c, const IfaceApplyJobT<S>* d_jobs, int njobs, int r, int nrhs);
+void launch_coupling_present(Ctx* c, const Mat* m, const BandGeom& g, int64_t row_lo,
+                             int64_t row_hi, int* d_flag);
 
 // ---- krylov.cu -----------------------------------------------------------------------
 template <class S> struct ColScalT { S v[MAX_RHS]; };

@@ -23,6 +23,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <future>
 #include <type_traits>
 
@@ -168,6 +169,29 @@ void dstage_t(Fact* f, S* x, int64_t ld, int nrhs, bool adjoint, int p_only) {
   }
 }
 
+// C1 across the GPU boundaries: m_W (computed left) goes right, m_T goes left
+template <class S>
+void exchange_msgs(Fact* f) {
+  if (!f->dist) return;
+  const int64_t blk = (int64_t)f->r * MAX_RHS;
+  S* mbase = sp<S>(f->iface_msg);
+  const S* to_next = f->job_right >= 0 ? mbase + (2 * f->job_right + 0) * blk : mbase;
+  S* from_prev = f->job_left >= 0 ? mbase + (2 * f->job_left + 0) * blk : mbase;
+  const S* to_prev = f->job_left >= 0 ? mbase + (2 * f->job_left + 1) * blk : mbase;
+  S* from_next = f->job_right >= 0 ? mbase + (2 * f->job_right + 1) * blk : mbase;
+  neighbor_exchange(f, to_next, from_prev, to_prev, from_next, blk * SW<S>);
+}
+
+// `per_iface` messages of `scalars` each for every interface this GPU owns (the GPU of
+// its left partition), so the sum over the GPUs is the single-GPU count
+void ledger_add(Fact* f, int stage, int64_t per_iface, int64_t scalars) {
+  int64_t owned = 0;
+  for (int i = f->p0; i < f->p0 + f->P; ++i)
+    if (i < f->Pg - 1) ++owned;
+  f->ledger_msgs[stage] += per_iface * owned;
+  f->ledger_sc[stage] += per_iface * owned * scalars;
+}
+
 template <class S>
 void apply_precond_t(Fact* f, const S* in, int64_t ldi, S* out, int64_t ldo, int nrhs,
                      bool block_jacobi) {
@@ -175,7 +199,7 @@ void apply_precond_t(Fact* f, const S* in, int64_t ldi, S* out, int64_t ldo, int
   const int64_t nl = f->row_hi - f->row_lo;
   if (out != in) copy_block(c, out + f->row_lo, ldo, in + f->row_lo, ldi, nl, nrhs);
   dstage_t(f, out, ldo, nrhs, false, -1);
-  const bool lowrank = !block_jacobi && f->variant == LRS_VARIANT_T && f->r > 0 && f->Pg > 1;
+  const bool lowrank = !block_jacobi && f->r > 0 && f->Pg > 1;
   if (!lowrank) return;
   const int r = f->r;
   const auto* jobs = reinterpret_cast<const IfaceApplyJobT<S>*>(f->iface_jobs.get());
@@ -183,16 +207,7 @@ void apply_precond_t(Fact* f, const S* in, int64_t ldi, S* out, int64_t ldo, int
     const int nr = std::min(MAX_RHS, nrhs - c0);
     S* xc = out + (int64_t)c0 * ldo;
     launch_iface_messages_t<S>(c, jobs, f->ni, r, f->k, xc, ldo, nr, sp<S>(f->iface_work));
-    if (f->dist) {
-      // C1 across the GPU boundaries: m_W (computed left) goes right, m_T goes left
-      const int64_t blk = (int64_t)r * MAX_RHS;
-      S* mbase = sp<S>(f->iface_msg);
-      const S* to_next = f->job_right >= 0 ? mbase + (2 * f->job_right + 0) * blk : mbase;
-      S* from_prev = f->job_left >= 0 ? mbase + (2 * f->job_left + 0) * blk : mbase;
-      const S* to_prev = f->job_left >= 0 ? mbase + (2 * f->job_left + 1) * blk : mbase;
-      S* from_next = f->job_right >= 0 ? mbase + (2 * f->job_right + 1) * blk : mbase;
-      neighbor_exchange(f, to_next, from_prev, to_prev, from_next, blk * SW<S>);
-    }
+    exchange_msgs<S>(f);
     launch_iface_solve_t<S>(c, jobs, f->ni, r, nr);
     launch_recovery_t<S>(c, f->geom(), f->n, f->row_lo, f->row_hi, xc, ldo, xc, ldo, nr,
                          sp<S>(f->uT), sp<S>(f->uW), r, sp<S>(f->scT), sp<S>(f->scW));
@@ -201,14 +216,8 @@ void apply_precond_t(Fact* f, const S* in, int64_t ldi, S* out, int64_t ldo, int
   // reduced solve and 2 in the recovery, r n_rhs scalars each -- 4 (p-1) r n_rhs per
   // application summed over the GPUs (every interface is counted by the GPU of its
   // left partition).
-  int64_t owned = 0;
-  for (int i = f->iface0; i < f->iface0 + f->ni; ++i)
-    if (i >= f->p0 && i < f->p0 + f->P) ++owned;
-  const int64_t msgs = 2 * owned;
-  f->ledger_msgs[LRS_STAGE_PRECOND_APPLY] += msgs;
-  f->ledger_sc[LRS_STAGE_PRECOND_APPLY] += msgs * r * nrhs;
-  f->ledger_msgs[LRS_STAGE_RECOVERY] += msgs;
-  f->ledger_sc[LRS_STAGE_RECOVERY] += msgs * r * nrhs;
+  ledger_add(f, LRS_STAGE_PRECOND_APPLY, 2, (int64_t)r * nrhs);
+  ledger_add(f, LRS_STAGE_RECOVERY, 2, (int64_t)r * nrhs);
 }
 
 // ------------------------------------------------------------------------------------
@@ -556,6 +565,14 @@ bool build_lowrank(Fact* f, int r, int* bad_iface, double* bad_cond, std::vector
       jobs.push_back(j);
     }
     upload_raw(c, f->iface_jobs, jobs);
+    // the same interfaces addressed in the compact reduced layout (LR-SPIKE-I / OTF):
+    // bottom tip of partition i at row 2ki + k, top tip of partition i+1 at 2k(i+1)
+    for (int q = 0; q < ni; ++q) {
+      const int i = f->iface0 + q;
+      jobs[q].yb_row = 2 * k * i + k;
+      jobs[q].yt_row = 2 * k * (i + 1);
+    }
+    upload_raw(c, f->iface_jobs_red, jobs);
     f->iface_work.alloc(iface_work_doubles(std::max(ni, 1), r, k) * w);
   }
   LRS_CUDA(cudaStreamSynchronize(c->stream));
@@ -574,15 +591,6 @@ void dstage(Fact* f, void* x, int64_t ld, int nrhs, bool adjoint, int p_only) {
   else dstage_t(f, static_cast<double*>(x), ld, nrhs, adjoint, p_only);
 }
 
-void apply_precond(Fact* f, const void* in, int64_t ldi, void* out, int64_t ldo, int nrhs,
-                   bool block_jacobi) {
-  if (f->scalar == LRS_C128)
-    apply_precond_t(f, static_cast<const zc*>(in), ldi, static_cast<zc*>(out), ldo, nrhs,
-                    block_jacobi);
-  else
-    apply_precond_t(f, static_cast<const double*>(in), ldi, static_cast<double*>(out), ldo, nrhs,
-                    block_jacobi);
-}
 
 // ------------------------------------------------------------------------------------
 // factorize
@@ -595,8 +603,14 @@ Fact* factorize(Ctx* c, Mat* m, const lrs_solver_cfg& cfg, const lrs_comm* comm)
   f->sw = m->scalar == LRS_C128 ? 2 : 1;
   const bool cplx = f->scalar == LRS_C128;
   f->variant = cfg.variant;
-  if (cfg.variant != LRS_VARIANT_T && cfg.variant != LRS_VARIANT_BJ)
+  if (cfg.variant != LRS_VARIANT_T && cfg.variant != LRS_VARIANT_BJ &&
+      cfg.variant != LRS_VARIANT_I && cfg.variant != LRS_VARIANT_OTF)
     throw LrsError(LRS_ERR_PARAMETER, "unknown variant");
+  f->inner_tol = cfg.inner_tol > 0 ? cfg.inner_tol : 1e-12;
+  f->inner_max_iters = cfg.inner_max_iters > 0 ? cfg.inner_max_iters : 200;
+  f->otf_tol = cfg.otf_tol > 0 ? cfg.otf_tol : 1e-8;
+  f->otf_max_iters = cfg.otf_max_iters > 0 ? cfg.otf_max_iters : 500;
+  f->otf_escalations = cfg.otf_escalations >= 0 ? cfg.otf_escalations : 4;
   if (cfg.p < 1) throw LrsError(LRS_ERR_PARAMETER, "p >= 1 required");
   if (cfg.n_svd < 0) throw LrsError(LRS_ERR_PARAMETER, "n_svd >= 0 required");
   if (comm && comm->size > 1) {
@@ -708,12 +722,25 @@ Fact* factorize(Ctx* c, Mat* m, const lrs_solver_cfg& cfg, const lrs_comm* comm)
     f->chunk_start.push_back(f->row_hi);
     upload(c, f->d_chunks, f->chunk_start);
     upload(c, f->d_part_first, f->part_first);
-    const size_t nch = f->chunk_start.size() - 1;
+    // the compact reduced space (2k rows per partition)
+    const int64_t k2 = 2 * f->k;
+    f->ldr = k2 * f->Pg;
+    f->rchunk_start.clear();
+    f->rpart_first.assign(P + 1, 0);
+    for (int i = 0; i < P; ++i) {
+      f->rpart_first[i] = (int)f->rchunk_start.size();
+      for (int64_t r0 = 0; r0 < k2; r0 += CH) f->rchunk_start.push_back(k2 * (f->p0 + i) + r0);
+    }
+    f->rpart_first[P] = (int)f->rchunk_start.size();
+    f->rchunk_start.push_back(k2 * (f->p0 + P));
+    upload(c, f->d_rchunks, f->rchunk_start);
+    upload(c, f->d_rpart_first, f->rpart_first);
+    const size_t nch = std::max(f->chunk_start.size(), f->rchunk_start.size()) - 1;
     f->partial.alloc(nch * 64 * MAX_RHS * w);
     f->persum.alloc((size_t)f->pl_max * 64 * MAX_RHS * w);
     f->gather.alloc((size_t)G * f->pl_max * 64 * MAX_RHS * w);
     f->dotout.alloc(64 * MAX_RHS * w);
-    f->xch.alloc((size_t)4 * std::max<int64_t>(1, m->k) * MAX_RHS * w);
+    f->xch.alloc((size_t)4 * std::max<int64_t>(1, std::max(m->k, f->k)) * MAX_RHS * w);
   }
   cudaEvent_t e0, e1, e2, e3;
   LRS_CUDA(cudaEventCreate(&e0));
@@ -752,12 +779,25 @@ Fact* factorize(Ctx* c, Mat* m, const lrs_solver_cfg& cfg, const lrs_comm* comm)
       throw e;
     }
   }
+  // structurally nonzero couplings? (LR-SPIKE-OTF skips the reduced solve without any)
+  {
+    DevBuf<int> flag;
+    flag.alloc(1);
+    LRS_CUDA(cudaMemsetAsync(flag.get(), 0, sizeof(int), c->stream));
+    launch_coupling_present(c, m, g, f->row_lo, f->row_hi, flag.get());
+    int hf = 0;
+    download(c, &hf, flag.get(), 1);
+    double any_c = hf;
+    for (double v : allgather_host(f.get(), {(double)hf})) any_c = std::max(any_c, v);
+    f->coupled = any_c > 0 && f->Pg > 1;
+  }
   // the host draws Omega for the spike SVDs while the GPU runs the band LU
   std::future<std::vector<double>> omega_future;
   {
     const int r0 = (int)cfg.n_svd;
     const int l0 = r0 + (cfg.oversample >= 0 ? (int)cfg.oversample : (r0 + 1) / 2);
-    if (f->variant == LRS_VARIANT_T && f->Pg > 1 && r0 >= 1 && l0 <= f->k)
+    if ((f->variant == LRS_VARIANT_T || f->variant == LRS_VARIANT_I ||
+         f->variant == LRS_VARIANT_OTF) && f->Pg > 1 && r0 >= 1 && l0 <= f->k)
       omega_future = std::async(std::launch::async, make_omega, f->seed, f->Pg, f->p0,
                                 f->p0 + P, f->k, l0);
   }
@@ -800,7 +840,9 @@ Fact* factorize(Ctx* c, Mat* m, const lrs_solver_cfg& cfg, const lrs_comm* comm)
     }
   }
   // spikes + truncated preconditioner, with the r-halving retry
-  int r = (f->variant == LRS_VARIANT_T && f->Pg > 1) ? (int)cfg.n_svd : 0;
+  const bool spiked = f->variant == LRS_VARIANT_T || f->variant == LRS_VARIANT_I ||
+                      f->variant == LRS_VARIANT_OTF;
+  int r = (spiked && f->Pg > 1) ? (int)cfg.n_svd : 0;
   f->r = 0;
   f->l = 0;
   if (r > 0) {
@@ -876,25 +918,31 @@ Fact* factorize(Ctx* c, Mat* m, const lrs_solver_cfg& cfg, const lrs_comm* comm)
 // ------------------------------------------------------------------------------------
 namespace {
 
+// A Krylov space: full-length blocks with leading dimension n, this GPU's rows
+// [lo, lo + nl), partition-aligned reduction chunks, and the operator / preconditioner.
+// The outer solve works in the n-layout (A = the CSR, M = the preconditioner); the
+// LR-SPIKE-I inner solve and the LR-SPIKE-OTF reduced solve in the compact reduced space.
 template <class S>
 struct Work {
   using H = HT<S>;
   Fact* f;
-  Mat* A;
   int64_t n;       // full length (ld of every block)
   int64_t lo, nl;  // local rows [lo, lo + nl)
+  Chunks ch;       // deterministic reduction chunks of the space
   int nr;
-  bool bj;
   lrs_report* rep;
   std::vector<double> hist;
   double* hbuf = nullptr;  // pinned landing buffer of the dot products (Ctx-owned)
+  std::function<void(const S*, S*)> Mf;            // out = M^-1 in
+  std::function<void(S*, S*)> Af;                  // out = A in (halo rows of in may be written)
+  std::function<void(const S*, S*, S*)> Rf;        // out = b - A x
   void init() { hbuf = f->ctx->dots_host; }
   Ctx* c() const { return f->ctx; }
   S* dotout() const { return sp<S>(f->dotout); }
   // out[q*nr + j] = X_q[:, j]^H Y[:, j] over ALL rows (partition-ordered, any GPU count)
   void dots(const S* X, int64_t strideX, int nvec, const S* Y, H* out) {
     const int nout = nvec * nr * SW<S>;  // doubles
-    launch_multidot_partition_t<S>(c(), f->chunks(), X, n, strideX, nvec, Y, n, nr,
+    launch_multidot_partition_t<S>(c(), ch, X, n, strideX, nvec, Y, n, nr,
                                    sp<S>(f->partial), sp<S>(f->persum));
     if (f->dist) {
       LRS_CUDA(cudaStreamSynchronize(c()->stream));
@@ -918,17 +966,15 @@ struct Work {
     for (int j = 0; j < nr; ++j) out[j] = std::sqrt(hreal(d[j]));
   }
   void M(const S* in, S* out) {
-    apply_precond_t(f, in, n, out, n, nr, bj);
+    Mf(in, out);
     rep->precond_applications++;
   }
   void Aop(S* in, S* out) {
-    halo_exchange(f, in, n, nr);
-    spmv_s<S>(c(), A, in, n, out, n, nr, 0, nullptr, 0, lo, lo + nl);
+    Af(in, out);
     rep->matvecs++;
   }
   void resid(const S* b, S* x, S* out) {  // out = b - A x
-    halo_exchange(f, x, n, nr);
-    spmv_s<S>(c(), A, x, n, out, n, nr, 2, b, n, lo, lo + nl);
+    Rf(b, x, out);
     rep->matvecs++;
   }
   void axpby(int op, const ColScalT<S>& a, const ColScalT<S>& b, const ColScal& act, S* X,
@@ -1354,6 +1400,302 @@ void run_gmres(Work<S>& w, const S* b, S* x, const lrs_iter_cfg& cfg, bool has_x
   for (int j = 0; j < nr; ++j) iters_out[j] = (double)iters[j];
 }
 
+// ------------------------------------------------------------------------------------
+// The reduced system of LR-SPIKE-I / OTF in the compact layout (reduced.cu)
+// ------------------------------------------------------------------------------------
+template <class S>
+const IfaceApplyJobT<S>* red_jobs(Fact* f) {
+  return reinterpret_cast<const IfaceApplyJobT<S>*>(f->iface_jobs_red.get());
+}
+
+// the two compressed messages of every local-side interface of a compact vector (C1)
+template <class S>
+void reduced_messages(Fact* f, const S* xr, int nr) {
+  launch_iface_messages_t<S>(f->ctx, red_jobs<S>(f), f->ni, f->r, f->k, xr, f->ldr, nr,
+                             sp<S>(f->iface_work));
+  exchange_msgs<S>(f);
+}
+
+// matvec_lowrank: y = x + W~ x_{i-1,b} + T~ x_{i+1,t}
+template <class S>
+void matvec_lowrank_t(Fact* f, const S* x, S* y, int nr) {
+  reduced_messages(f, x, nr);
+  launch_iface_scale_t<S>(f->ctx, red_jobs<S>(f), f->ni, f->r, nr);
+  launch_tips_lowrank_t<S>(f->ctx, f->geom(), f->n, f->k, x, y, f->ldr, nr, sp<S>(f->uT),
+                           sp<S>(f->uW), f->r, sp<S>(f->scT), sp<S>(f->scW), 0, 1.0);
+  ledger_add(f, LRS_STAGE_REDUCED_MATVEC, 2, (int64_t)f->r * nr);
+}
+
+// apply_truncated_precond on a compact vector
+template <class S>
+void trunc_precond_t(Fact* f, const S* g, S* x, int nr) {
+  reduced_messages(f, g, nr);
+  launch_iface_solve_t<S>(f->ctx, red_jobs<S>(f), f->ni, f->r, nr);
+  launch_tips_lowrank_t<S>(f->ctx, f->geom(), f->n, f->k, g, x, f->ldr, nr, sp<S>(f->uT),
+                           sp<S>(f->uW), f->r, sp<S>(f->scT), sp<S>(f->scW), 1, -1.0);
+  ledger_add(f, LRS_STAGE_PRECOND_APPLY, 2, (int64_t)f->r * nr);
+}
+
+// z (n-layout, zeroed local rows) = A_i^-1 (pad_top(C_i x_{i-1,b}) + pad_bottom(B_i x_{i+1,t}))
+// for the local partitions, x compact (exact spikes applied on the fly);
+// the neighbour tips of the cross-GPU interfaces arrive by a neighbour exchange.
+template <class S>
+void coupled_solve_t(Fact* f, S* xr, S* z, int nr) {
+  Ctx* c = f->ctx;
+  const int64_t k = f->k, n = f->n, ldr = f->ldr, k2 = 2 * k;
+  if (f->dist) {  // x_{p0-1,b} from the left GPU, x_{p0+P,t} from the right GPU
+    const int64_t cnt = k * nr;
+    S* s_next = sp<S>(f->xch);
+    S* s_prev = s_next + cnt;
+    S* r_prev = s_prev + cnt;
+    S* r_next = r_prev + cnt;
+    copy_block(c, s_next, k, xr + k2 * (f->p0 + f->P - 1) + k, ldr, k, nr);
+    copy_block(c, s_prev, k, xr + k2 * f->p0, ldr, k, nr);
+    neighbor_exchange(f, s_next, r_prev, s_prev, r_next, cnt * SW<S>);
+    if (f->p0 > 0) copy_block(c, xr + k2 * (f->p0 - 1) + k, ldr, r_prev, k, k, nr);
+    if (f->p0 + f->P < f->Pg) copy_block(c, xr + k2 * (f->p0 + f->P), ldr, r_next, k, k, nr);
+  }
+  for (int j = 0; j < nr; ++j)
+    LRS_CUDA(cudaMemsetAsync(z + f->row_lo + (int64_t)j * n, 0,
+                             sizeof(S) * (f->row_hi - f->row_lo), c->stream));
+  std::vector<CoupleJobT<S>> wj, tj;
+  for (int i = f->p0; i < f->p0 + f->P; ++i) {
+    const int64_t o = f->goff[i], ni = f->goff[i + 1] - f->goff[i];
+    if (i > 0) {  // C_i x_{i-1,b} into the top k rows
+      CoupleJobT<S> j{};
+      j.r0 = o;
+      j.c0 = o - k;
+      j.b = k;
+      j.dst0 = o;
+      j.X = xr + k2 * (i - 1) + k;
+      j.ldx = ldr;
+      j.out = z;
+      j.ldo = n;
+      j.ncols = nr;
+      wj.push_back(j);
+    }
+    if (i < f->Pg - 1) {  // B_i x_{i+1,t} into the bottom k rows
+      CoupleJobT<S> j{};
+      j.r0 = o + ni - k;
+      j.c0 = f->goff[i + 1];
+      j.b = k;
+      j.dst0 = o + ni - k;
+      j.X = xr + k2 * (i + 1);
+      j.ldx = ldr;
+      j.out = z;
+      j.ldo = n;
+      j.ncols = nr;
+      tj.push_back(j);
+    }
+  }
+  DevBuf<CoupleJobT<S>> dw, dt;
+  upload(c, dw, wj);
+  upload(c, dt, tj);
+  launch_coupling_t<S>(c, f->mat, false, dw.get(), (int)wj.size(), k, nr, true);
+  launch_coupling_t<S>(c, f->mat, false, dt.get(), (int)tj.size(), k, nr, true);
+  dstage_t(f, z, n, nr, false, -1);
+}
+
+// matvec_otf: y = x + tips(z), z from coupled_solve_t
+template <class S>
+void matvec_otf_t(Fact* f, S* x, S* y, S* z, int nr) {
+  coupled_solve_t(f, x, z, nr);
+  launch_tips_gather_t<S>(f->ctx, f->geom(), f->k, z, f->n, x, y, f->ldr, nr);
+  ledger_add(f, LRS_STAGE_REDUCED_MATVEC, 2, f->k * nr);
+}
+
+template <class S>
+void reduced_work(Work<S>& w, Fact* f, int nr, lrs_report* rep) {
+  w.f = f;
+  w.n = f->ldr;
+  w.lo = 2 * f->k * f->p0;
+  w.nl = 2 * f->k * f->P;
+  w.ch = f->rchunks();
+  w.nr = nr;
+  w.rep = rep;
+  w.init();
+}
+
+template <class S>
+ColScalT<S> cs_const(int nr, double v) {
+  ColScalT<S> s{};
+  for (int j = 0; j < nr && j < MAX_RHS; ++j) s.v[j] = s_real<S>(v);
+  return s;
+}
+
+// apply_precond_I: D-stage; inner BiCGStab on the low-rank reduced
+// system (matvec_lowrank, preconditioned by apply_truncated_precond) on the column-
+// normalised tips; low-rank recovery.  Inner non-convergence -> LRS_ERR_PRECOND_FAILURE.
+template <class S>
+void apply_precond_I_t(Fact* f, const S* in, int64_t ldi, S* out, int64_t ldo, int nrhs) {
+  Ctx* c = f->ctx;
+  const int64_t nl = f->row_hi - f->row_lo;
+  if (out != in) copy_block(c, out + f->row_lo, ldo, in + f->row_lo, ldi, nl, nrhs);
+  dstage_t(f, out, ldo, nrhs, false, -1);
+  if (!(f->r > 0 && f->Pg > 1)) return;
+  for (int c0 = 0; c0 < nrhs; c0 += MAX_RHS) {
+    const int nr = std::min(MAX_RHS, nrhs - c0);
+    S* y = out + (int64_t)c0 * ldo;
+    DevBuf<S> rb;
+    rb.alloc((size_t)f->ldr * nr * 2);
+    S* g = rb.get();
+    S* xr = g + (size_t)f->ldr * nr;
+    launch_tips_gather_t<S>(c, f->geom(), f->k, y, ldo, nullptr, g, f->ldr, nr);
+    lrs_report irep{};
+    Work<S> wi;
+    reduced_work(wi, f, nr, &irep);
+    wi.Af = [&](S* a, S* o) { matvec_lowrank_t(f, a, o, nr); };
+    wi.Mf = [&](const S* a, S* o) { trunc_precond_t(f, a, o, nr); };
+    wi.Rf = [&](const S* b, S* xx, S* o) {
+      matvec_lowrank_t(f, xx, o, nr);
+      wi.axpby(1, cs_const<S>(nr, 1.0), ColScalT<S>{}, cs_const<double>(nr, 1.0), nullptr, b, o, o);
+    };
+    std::vector<double> gn(nr);
+    wi.norms(g, gn.data());
+    ColScalT<S> inv{}, scl{};
+    for (int j = 0; j < nr; ++j) {
+      const double gs = gn[j] > 0 ? gn[j] : 1.0;
+      inv.v[j] = s_real<S>(1.0 / gs);
+      scl.v[j] = s_real<S>(gs);
+    }
+    const ColScal all = cs_const<double>(nr, 1.0);
+    wi.axpby(4, inv, ColScalT<S>{}, all, nullptr, g, nullptr, g);
+    lrs_iter_cfg icfg{};
+    icfg.method = LRS_BICGSTAB;
+    icfg.tol = f->inner_tol;
+    icfg.max_iters = f->inner_max_iters;
+    icfg.breakdown_eps = 1e-30;
+    std::vector<double> its;
+    std::vector<bool> conv, brk;
+    run_bicgstab(wi, g, xr, icfg, false, its, conv, brk);
+    bool ok = true;
+    double itmax = 0.0;
+    for (int j = 0; j < nr; ++j) {
+      ok = ok && conv[j] && !brk[j];
+      itmax = std::max(itmax, its[j]);
+    }
+    if (!ok)
+      throw LrsError(LRS_ERR_PRECOND_FAILURE,
+                     "LR-SPIKE-I inner reduced solve did not converge (tol " +
+                         std::to_string(f->inner_tol) + ", " + std::to_string(icfg.max_iters) +
+                         " iterations)");
+    f->inner_iterations += itmax;
+    f->inner_solves += 1;
+    wi.axpby(4, scl, ColScalT<S>{}, all, nullptr, xr, nullptr, xr);
+    // low-rank recovery with the reduced solution's compressed messages
+    reduced_messages(f, xr, nr);
+    launch_iface_scale_t<S>(c, red_jobs<S>(f), f->ni, f->r, nr);
+    launch_recovery_t<S>(c, f->geom(), f->n, f->row_lo, f->row_hi, y, ldo, y, ldo, nr,
+                         sp<S>(f->uT), sp<S>(f->uW), f->r, sp<S>(f->scT), sp<S>(f->scW));
+    ledger_add(f, LRS_STAGE_RECOVERY, 2, (int64_t)f->r * nr);
+  }
+}
+
+// mode APPLY_VARIANT: the factorization's own preconditioner (I for LR-SPIKE-I, Block
+// Jacobi for BJ, T otherwise); APPLY_BJ: the D-stage only; APPLY_T: apply_precond_T
+template <class S>
+void apply_variant_t(Fact* f, const S* in, int64_t ldi, S* out, int64_t ldo, int nrhs, int mode) {
+  if (mode == APPLY_VARIANT && f->variant == LRS_VARIANT_I)
+    apply_precond_I_t(f, in, ldi, out, ldo, nrhs);
+  else
+    apply_precond_t(f, in, ldi, out, ldo, nrhs,
+                    mode == APPLY_BJ || (mode == APPLY_VARIANT && f->variant == LRS_VARIANT_BJ));
+}
+
+// solve_otf for one column batch: D-stage once; BiCGStab on the true
+// reduced system (matvec_otf) preconditioned by apply_truncated_precond to otf_tol;
+// exact recovery x = y - z(x_r); full residual against the outer tol, escalating the
+// reduced tolerance /100 (warm restart) at most otf_escalations times.
+template <class S>
+void run_otf(Work<S>& w, Fact* f, const S* b, S* x, const lrs_iter_cfg& cfg,
+             std::vector<double>& iters, std::vector<bool>& conv, std::vector<bool>& brk) {
+  Ctx* c = f->ctx;
+  const int nr = w.nr;
+  const int64_t n = f->n;
+  const size_t blk = (size_t)n * nr;
+  DevBuf<S> buf;
+  buf.alloc(blk * 3);
+  S* y = buf.get();
+  S* z = y + blk;
+  S* t = z + blk;
+  std::vector<double> bn(nr), res(nr);
+  w.norms(b, bn.data());
+  w.copy(y, b);
+  dstage_t(f, y, n, nr, false, -1);
+  w.rep->precond_applications++;
+  iters.assign(nr, 0.0);
+  conv.assign(nr, false);
+  brk.assign(nr, false);
+  auto check = [&]() {
+    w.resid(b, x, t);
+    w.norms(t, res.data());
+    bool all = true;
+    double mx = 0.0;
+    for (int j = 0; j < nr; ++j) {
+      const double rr = res[j] / (bn[j] > 0 ? bn[j] : 1.0);
+      mx = std::max(mx, rr);
+      all = all && rr <= cfg.tol;
+    }
+    return std::make_pair(all, mx);
+  };
+  if (!f->coupled) {  // S_r = I: x = D^-1 f, zero reduced iterations
+    w.copy(x, y);
+    const auto ck = check();
+    conv.assign(nr, ck.first);
+    return;
+  }
+  DevBuf<S> rb;
+  rb.alloc((size_t)f->ldr * nr * 2);
+  S* g = rb.get();
+  S* xr = g + (size_t)f->ldr * nr;
+  launch_tips_gather_t<S>(c, f->geom(), f->k, y, n, nullptr, g, f->ldr, nr);
+  lrs_report rrep{};
+  Work<S> wr;
+  reduced_work(wr, f, nr, &rrep);
+  wr.Af = [&](S* a, S* o) { matvec_otf_t(f, a, o, z, nr); };
+  if (f->r > 0) wr.Mf = [&](const S* a, S* o) { trunc_precond_t(f, a, o, nr); };
+  else wr.Mf = [&](const S* a, S* o) { copy_block(c, o + wr.lo, wr.n, a + wr.lo, wr.n, wr.nl, nr); };
+  wr.Rf = [&](const S* bb, S* xx, S* o) {
+    matvec_otf_t(f, xx, o, z, nr);
+    wr.axpby(1, cs_const<S>(nr, 1.0), ColScalT<S>{}, cs_const<double>(nr, 1.0), nullptr, bb, o, o);
+  };
+  double tol = f->otf_tol, total = 0.0;
+  bool warm = false;
+  const ColScal all = cs_const<double>(nr, 1.0);
+  for (int esc = 0; esc <= f->otf_escalations; ++esc) {
+    lrs_iter_cfg rcfg{};
+    rcfg.method = LRS_BICGSTAB;
+    rcfg.tol = tol;
+    rcfg.max_iters = f->otf_max_iters;
+    rcfg.breakdown_eps = cfg.breakdown_eps;
+    std::vector<double> its;
+    std::vector<bool> rc, rbrk;
+    run_bicgstab(wr, g, xr, rcfg, warm, its, rc, rbrk);
+    double itmax = 0.0;
+    for (int j = 0; j < nr; ++j) {
+      itmax = std::max(itmax, its[j]);
+      if (rbrk[j]) brk[j] = true;
+    }
+    total += itmax;
+    w.hist.insert(w.hist.end(), wr.hist.begin(), wr.hist.end());
+    wr.hist.clear();
+    if (std::any_of(brk.begin(), brk.end(), [](bool v) { return v; })) break;
+    // exact recovery x = y - z(x_r)
+    coupled_solve_t(f, xr, z, nr);
+    ledger_add(f, LRS_STAGE_RECOVERY, 2, f->k * nr);
+    w.axpby(1, cs_const<S>(nr, 1.0), ColScalT<S>{}, all, nullptr, y, z, x);
+    const auto ck = check();
+    if (ck.first) {
+      conv.assign(nr, true);
+      break;
+    }
+    tol /= 100.0;
+    warm = true;
+  }
+  w.rep->matvecs += rrep.matvecs;
+  for (int j = 0; j < nr; ++j) iters[j] = total;
+}
+
 template <class S>
 void solve_t(Fact* f, Mat* a, const S* b, int64_t ldb, S* x, int64_t ldx, int nrhs,
              const lrs_iter_cfg& cfg, lrs_report* rep) {
@@ -1368,6 +1710,8 @@ void solve_t(Fact* f, Mat* a, const S* b, int64_t ldb, S* x, int64_t ldx, int nr
   R.history_cap = cap;
   R.seed = f->seed;
   R.converged = 1;
+  const double inner0 = f->inner_iterations;
+  const int64_t solves0 = f->inner_solves;
   LRS_CUDA(cudaEventRecord(c->ev0, c->stream));
   const int64_t n = f->n, lo = f->row_lo, nl = f->row_hi - f->row_lo;
   bool any_brk = false;
@@ -1377,14 +1721,22 @@ void solve_t(Fact* f, Mat* a, const S* b, int64_t ldb, S* x, int64_t ldx, int nr
     const int nr = std::min(MAX_RHS, nrhs - c0);
     Work<S> w;
     w.f = f;
-    w.A = a;
     w.n = n;
     w.lo = lo;
     w.nl = nl;
+    w.ch = f->chunks();
     w.nr = nr;
-    w.bj = f->variant == LRS_VARIANT_BJ;
     w.rep = &R;
     w.init();
+    w.Mf = [&](const S* in, S* out) { apply_variant_t(f, in, n, out, n, nr, APPLY_VARIANT); };
+    w.Af = [&](S* in, S* out) {
+      halo_exchange(f, in, n, nr);
+      spmv_s<S>(c, a, in, n, out, n, nr, 0, nullptr, 0, lo, lo + nl);
+    };
+    w.Rf = [&](const S* bv, S* xv, S* out) {
+      halo_exchange(f, xv, n, nr);
+      spmv_s<S>(c, a, xv, n, out, n, nr, 2, bv, n, lo, lo + nl);
+    };
     // full-length device copies (ld = n) of this column batch; local rows only
     DevBuf<S> bb, xx;
     bb.alloc((size_t)n * nr);
@@ -1396,7 +1748,9 @@ void solve_t(Fact* f, Mat* a, const S* b, int64_t ldb, S* x, int64_t ldx, int nr
                  nl, nr);
     std::vector<double> iters;
     std::vector<bool> conv, brk;
-    if (cfg.method == LRS_BICGSTAB) {
+    if (f->variant == LRS_VARIANT_OTF) {
+      run_otf(w, f, bb.get(), xx.get(), cfg, iters, conv, brk);
+    } else if (cfg.method == LRS_BICGSTAB) {
       run_bicgstab(w, bb.get(), xx.get(), cfg, has_x0, iters, conv, brk);
     } else if (cfg.method == LRS_GMRES) {
       run_gmres(w, bb.get(), xx.get(), cfg, has_x0, iters, conv);
@@ -1430,6 +1784,8 @@ void solve_t(Fact* f, Mat* a, const S* b, int64_t ldb, S* x, int64_t ldx, int nr
   R.t_solve = elapsed_ms(c->ev0, c->ev1) * 1e-3;
   R.residual_final = worst;
   R.breakdown = any_brk ? 1 : 0;
+  R.inner_iterations = f->inner_iterations - inner0;
+  R.inner_solves = f->inner_solves - solves0;
   for (int s = 0; s < 3; ++s) {
     R.comm_messages[s] = f->ledger_msgs[s] - m0[s];
     R.comm_scalars[s] = f->ledger_sc[s] - s0[s];
@@ -1458,6 +1814,15 @@ void solve(Fact* f, Mat* a, const void* b, int64_t ldb, void* x, int64_t ldx, in
     solve_t(f, a, static_cast<const zc*>(b), ldb, static_cast<zc*>(x), ldx, nrhs, cfg, rep);
   else
     solve_t(f, a, static_cast<const double*>(b), ldb, static_cast<double*>(x), ldx, nrhs, cfg, rep);
+}
+
+void apply_precond(Fact* f, const void* in, int64_t ldi, void* out, int64_t ldo, int nrhs,
+                   int mode) {
+  if (f->scalar == LRS_C128)
+    apply_variant_t(f, static_cast<const zc*>(in), ldi, static_cast<zc*>(out), ldo, nrhs, mode);
+  else
+    apply_variant_t(f, static_cast<const double*>(in), ldi, static_cast<double*>(out), ldo, nrhs,
+                    mode);
 }
 
 }  // namespace lrs

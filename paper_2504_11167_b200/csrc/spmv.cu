@@ -86,7 +86,8 @@ template <class S>
 __global__ void __launch_bounds__(256) coupling_kernel(const CoupleJobT<S>* __restrict__ jobs,
                                                        const int* __restrict__ rp,
                                                        const int* __restrict__ ci,
-                                                       const S* __restrict__ va, int conj) {
+                                                       const S* __restrict__ va, int conj,
+                                                       int accumulate) {
   const CoupleJobT<S> jb = jobs[blockIdx.y];
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= jb.b * jb.ncols) return;
@@ -101,12 +102,13 @@ __global__ void __launch_bounds__(256) coupling_kernel(const CoupleJobT<S>* __re
     const S v = conj ? s_conj(va[q]) : va[q];
     acc = s_fma(v, jb.X[(col - jb.c0) + j * jb.ldx], acc);
   }
-  jb.out[jb.dst0 + rr + j * jb.ldo] = acc;
+  S* o = jb.out + jb.dst0 + rr + j * jb.ldo;
+  *o = accumulate ? s_add(*o, acc) : acc;
 }
 
 template <class S>
 void launch_coupling_t(Ctx* c, const Mat* m, bool transposed, const CoupleJobT<S>* d_jobs,
-                       int njobs, int64_t b, int ncols) {
+                       int njobs, int64_t b, int ncols, bool accumulate) {
   if (njobs == 0) return;
   dim3 grid((unsigned)((b * ncols + 255) / 256), (unsigned)njobs);
   ProfScope ps_(c, K_SETUP);
@@ -114,12 +116,12 @@ void launch_coupling_t(Ctx* c, const Mat* m, bool transposed, const CoupleJobT<S
   coupling_kernel<S><<<grid, 256, 0, c->stream>>>(
       d_jobs, transposed ? m->trow_ptr.get() : m->row_ptr.get(),
       transposed ? m->tcol_idx.get() : m->col_idx.get(), reinterpret_cast<const S*>(vals),
-      transposed && IsC<S>::value ? 1 : 0);
+      transposed && IsC<S>::value ? 1 : 0, accumulate ? 1 : 0);
   LRS_LAUNCHED(c);
 }
 template void launch_coupling_t<double>(Ctx*, const Mat*, bool, const CoupleJobT<double>*, int,
-                                        int64_t, int);
+                                        int64_t, int, bool);
 template void launch_coupling_t<zc>(Ctx*, const Mat*, bool, const CoupleJobT<zc>*, int, int64_t,
-                                    int);
+                                    int, bool);
 
 }  // namespace lrs

@@ -35,6 +35,7 @@ namespace {
       throw IllConditionedInterfaceError(msg, (int)e.interface_index, e.cond_estimate);
     case LRS_ERR_BREAKDOWN: throw BreakdownError(msg);
     case LRS_ERR_NOT_IMPLEMENTED: throw NotImplementedError(msg);
+    case LRS_ERR_PRECOND_FAILURE: throw PreconditionerFailureError(msg);
     default: throw CudaError(msg);
   }
 }
@@ -210,7 +211,15 @@ PartitionLayout make_layout(index_t n, index_t p, index_t k) {
 SpikeFactorization::SpikeFactorization(std::shared_ptr<DeviceMatrix> a, const SolverConfig& cfg)
     : a_(std::move(a)), cfg_(cfg) {
   lrs_solver_cfg c{};
-  c.variant = cfg.variant == Variant::LR_SPIKE_T ? LRS_VARIANT_T : LRS_VARIANT_BJ;
+  c.variant = cfg.variant == Variant::LR_SPIKE_T    ? LRS_VARIANT_T
+              : cfg.variant == Variant::LR_SPIKE_I   ? LRS_VARIANT_I
+              : cfg.variant == Variant::LR_SPIKE_OTF ? LRS_VARIANT_OTF
+                                                     : LRS_VARIANT_BJ;
+  c.inner_tol = cfg.inner_tol;
+  c.inner_max_iters = cfg.inner_max_iters;
+  c.otf_tol = cfg.otf_tol;
+  c.otf_max_iters = cfg.otf_max_iters;
+  c.otf_escalations = cfg.otf_escalations;
   c.passes = cfg.passes;
   c.p = cfg.p;
   c.k = cfg.k;
@@ -334,6 +343,8 @@ std::pair<DenseBlock, SolveReport> solve(const CsrMatrix& a, const DenseBlock& r
   rep.seed = r.seed;
   rep.wall_time = r.t_solve;
   rep.residual_final = r.residual_final;
+  rep.inner_iterations = r.inner_iterations;
+  rep.inner_solves = r.inner_solves;
   check(s, ctx);
   return {std::move(x), std::move(rep)};
 }
