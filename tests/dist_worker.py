@@ -49,7 +49,7 @@ def cpu_comm_worker(rank, world, port, out_dir):
     dist.destroy_process_group()
 
 
-def gpu_solve_worker(rank, world, port, out_dir, name, scale, method, P):
+def gpu_solve_worker(rank, world, port, out_dir, name, scale, method, P, variant="T"):
     """One rank of a sharded factorize + solve on cuda:0 (ranks share the GPU; all
     cross-rank dependencies are host-synchronous gloo calls)."""
     dist = _init(rank, world, port)
@@ -63,7 +63,7 @@ def gpu_solve_worker(rank, world, port, out_dir, name, scale, method, P):
     cfg = configs.make_config(name, scale, P)
     ctx = api.Context(0)
     A = api.CsrMatrix.from_csr(ctx, cfg.matrix)
-    scfg = api.SolverConfig(variant="T", p=cfg.P, k=cfg.b, n_svd=cfg.r, seed=cfg.seed)
+    scfg = api.SolverConfig(variant=variant, p=cfg.P, k=cfg.b, n_svd=cfg.r, seed=cfg.seed)
     F = DistFactorization(ctx, A, scfg, comm)
     f = np.asfortranarray(configs.vector("uniform", 77, cfg.matrix.n))
     y = F.apply_precond_T(f)

@@ -27,15 +27,18 @@ def _port():
     return p
 
 
-@pytest.mark.parametrize("name,scale,method,P,world", [("c2", 16 / 64, "bicgstab", 8, 2),
-                                                      ("c2", 16 / 64, "bicgstab", 8, 3),
-                                                      ("c1", 64 / 256, "gmres", 4, 2)])
-def test_sharded_solve_matches_single_gpu(ctx, name, scale, method, P, world):
+@pytest.mark.parametrize("name,scale,method,P,world,variant",
+                         [("c2", 16 / 64, "bicgstab", 8, 2, "T"),
+                          ("c2", 16 / 64, "bicgstab", 8, 3, "T"),
+                          ("c1", 64 / 256, "gmres", 4, 2, "T"),
+                          ("c2", 16 / 64, "bicgstab", 8, 3, "I"),
+                          ("c1", 64 / 256, "gmres", 4, 2, "OTF")])
+def test_sharded_solve_matches_single_gpu(ctx, name, scale, method, P, world, variant):
     from paper_2504_11167_b200 import api, configs
 
     cfg = configs.make_config(name, scale, P)
     A = api.CsrMatrix.from_csr(ctx, cfg.matrix)
-    F = api.factorize(ctx, A, api.SolverConfig(variant="T", p=cfg.P, k=cfg.b, n_svd=cfg.r,
+    F = api.factorize(ctx, A, api.SolverConfig(variant=variant, p=cfg.P, k=cfg.b, n_svd=cfg.r,
                                                seed=cfg.seed))
     f = np.asfortranarray(configs.vector("uniform", 77, cfg.matrix.n))
     y1 = F.apply_precond_T(f)
@@ -43,7 +46,8 @@ def test_sharded_solve_matches_single_gpu(ctx, name, scale, method, P, world):
     x1, rep1, _ = api.solve(A, np.asfortranarray(cfg.rhs), it=it, F=F)
     with tempfile.TemporaryDirectory() as d:
         mp.spawn(dist_worker.gpu_solve_worker,
-                 args=(world, _port(), d, name, scale, method, P), nprocs=world, join=True)
+                 args=(world, _port(), d, name, scale, method, P, variant), nprocs=world,
+                 join=True)
         z = np.load(os.path.join(d, "dist.npz"))
     assert np.array_equal(z["y"], y1)  # the preconditioner apply, bit for bit
     assert float(z["iterations"]) == rep1.iterations
