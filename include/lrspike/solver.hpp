@@ -157,6 +157,8 @@ class SpikeFactorization {
 std::shared_ptr<SpikeFactorization> factorize(const CsrMatrix& a, const SolverConfig& cfg);
 /// SPEC.md:485-493.
 DenseBlock apply_precond_T(const SpikeFactorization& f, const DenseBlock& rhs);
+/// SPEC.md:494-502 (an LR_SPIKE_I factorization; inner BiCGStab on the reduced system).
+DenseBlock apply_precond_I(const SpikeFactorization& f, const DenseBlock& rhs);
 /// SPEC.md:512-519.
 DenseBlock apply_block_jacobi(const SpikeFactorization& f, const DenseBlock& rhs);
 /// factorize (or reuse f) and run the outer Krylov method.

@@ -283,24 +283,28 @@ std::shared_ptr<SpikeFactorization> factorize(const CsrMatrix& a, const SolverCo
   return std::make_shared<SpikeFactorization>(std::make_shared<DeviceMatrix>(a), cfg);
 }
 
-static DenseBlock apply_impl(const SpikeFactorization& f, const DenseBlock& rhs, bool bj) {
+using ApplyFn = lrs_status (*)(lrs_fact*, const void*, int64_t, void*, int64_t, int64_t, int32_t);
+
+static DenseBlock apply_impl(const SpikeFactorization& f, const DenseBlock& rhs, ApplyFn fn) {
   if (rhs.rows() != f.matrix()->n()) throw DimensionError("apply: vector rows must equal n");
   DenseBlock x(rhs.rows(), rhs.cols());
   lrs_ctx* ctx = f.matrix()->device().handle();
-  check(bj ? lrs_apply_block_jacobi(f.handle(), rhs.data(), rhs.rows(), x.data(), x.rows(),
-                                    rhs.cols(), LRS_MEM_HOST)
-           : lrs_apply_precond(f.handle(), rhs.data(), rhs.rows(), x.data(), x.rows(), rhs.cols(),
-                               LRS_MEM_HOST),
-        ctx);
+  check(fn(f.handle(), rhs.data(), rhs.rows(), x.data(), x.rows(), rhs.cols(), LRS_MEM_HOST), ctx);
   return x;
 }
 
 DenseBlock apply_precond_T(const SpikeFactorization& f, const DenseBlock& rhs) {
-  return apply_impl(f, rhs, false);
+  return apply_impl(f, rhs, lrs_apply_precond_T);
+}
+
+DenseBlock apply_precond_I(const SpikeFactorization& f, const DenseBlock& rhs) {
+  if (f.config().variant != Variant::LR_SPIKE_I)
+    throw ParameterError("apply_precond_I needs an LR_SPIKE_I factorization");
+  return apply_impl(f, rhs, lrs_apply_precond);
 }
 
 DenseBlock apply_block_jacobi(const SpikeFactorization& f, const DenseBlock& rhs) {
-  return apply_impl(f, rhs, true);
+  return apply_impl(f, rhs, lrs_apply_block_jacobi);
 }
 
 std::pair<DenseBlock, SolveReport> solve(const CsrMatrix& a, const DenseBlock& rhs,

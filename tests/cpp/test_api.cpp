@@ -171,6 +171,29 @@ static void gpu_tests() {
     bool same = true;
     for (index_t i = 0; i < A.n_rows; ++i) same &= x1(i, 0) == x2(i, 0);
     CHECK(same);
+    // LR-SPIKE-I (inner reduced BiCGStab) and LR-SPIKE-OTF (exact reduced system)
+    SolverConfig ci = cfg;
+    ci.variant = Variant::LR_SPIKE_I;
+    auto fi = factorize(A, ci);
+    auto xi = apply_precond_I(*fi, b);
+    CHECK(xi.rows() == A.n_rows);
+    auto si = solve(A, b, ci, fi);
+    CHECK(si.second.converged && resid(A, si.first, b) <= 1e-8);
+    CHECK(si.second.inner_solves == si.second.precond_applications);
+    CHECK(si.second.inner_iterations > 0);
+    CHECK(throws<ParameterError>([&] { apply_precond_I(*f, b); }));
+    SolverConfig co = cfg;
+    co.variant = Variant::LR_SPIKE_OTF;
+    auto so = solve(A, b, co);
+    CHECK(so.second.converged && resid(A, so.first, b) <= 1e-8);
+    CHECK(so.second.ledger.reduced_matvec.scalars % (2 * 3 * 40) == 0);
+    // CG with the (symmetric) Block Jacobi preconditioner on the SPD Laplacian
+    SolverConfig cg = cfg;
+    cg.variant = Variant::BLOCK_JACOBI;
+    cg.n_svd = 0;
+    cg.outer.method = Method::CG;
+    auto sc = solve(A, b, cg);
+    CHECK(sc.second.converged && resid(A, sc.first, b) <= 1e-8);
     // errors: layout infeasible, not block tridiagonal
     SolverConfig bad = cfg;
     bad.p = 400;
