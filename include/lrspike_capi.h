@@ -21,6 +21,7 @@
  *   lrs_apply_block_jacobi  apply_block_jacobi
  *   lrs_solve               solve + bicgstab / cg / GMRES(m), solve_otf for LR-SPIKE-OTF
  *                           SPEC.md:520-528, :421-436, :503-511 (GMRES: SURVEY D1)
+ *   lrs_krylov              bicgstab / cg / GMRES(m) on caller operators
  *   lrs_last_error          the exception taxonomy      proj/core/include/lrspike/errors.hpp:11-94
  *
  * Memory: pointers tagged LRS_MEM_HOST are copied by the library (the caller
@@ -222,6 +223,23 @@ LRS_API lrs_status lrs_apply_precond_T(lrs_fact* f, const void* in, int64_t ld_i
 LRS_API lrs_status lrs_solve(lrs_fact* f, lrs_mat* a, const void* b, int64_t ldb, void* x,
                              int64_t ldx, int64_t n_rhs, const lrs_iter_cfg* cfg,
                              lrs_report* report, int32_t mem);
+
+/* ---- Krylov drivers on caller operators --------------------------- */
+/* bicgstab / cg (and GMRES(m)) take abstract operator and preconditioner contracts: the
+ * callback computes out = Op(in) for an n x n_rhs column-major block with leading
+ * dimension ld (both DEVICE pointers on the context's device, in the scalar type of the
+ * call) and returns 0, or nonzero to abort.  The library synchronizes its stream before
+ * each call; the callback must finish its work (or order it on the context stream)
+ * before returning. */
+typedef struct lrs_operator {
+  void* user;
+  int32_t (*apply)(void* user, const void* in, void* out, int64_t ld, int64_t n_rhs);
+} lrs_operator;
+/* apply_M may be NULL (identity).  b, x: n x n_rhs blocks, mem HOST or DEVICE. */
+LRS_API lrs_status lrs_krylov(lrs_ctx* c, int64_t n, int32_t scalar, const lrs_operator* apply_A,
+                              const lrs_operator* apply_M, const void* b, int64_t ldb, void* x,
+                              int64_t ldx, int64_t n_rhs, const lrs_iter_cfg* cfg,
+                              lrs_report* report, int32_t mem);
 
 /* ---- multi-GPU: one process per GPU, partitions sharded across the ranks ------------ */
 /* Host callbacks for the exchanges of a sharded factorization.

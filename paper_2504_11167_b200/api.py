@@ -70,6 +70,13 @@ class FactInfoC(ctypes.Structure):
                 ("t_precond", f64), ("max_interface_cond", f64)]
 
 
+_OPFN = ctypes.CFUNCTYPE(i32, vp, vp, vp, i64, i64)
+
+
+class OperatorC(ctypes.Structure):
+    _fields_ = [("user", vp), ("apply", _OPFN)]
+
+
 class ErrorInfoC(ctypes.Structure):
     _fields_ = [("status", i32), ("message", ctypes.c_char * 512), ("line", i64), ("row", i64),
                 ("col", i64), ("column", i64), ("interface_index", i64),
@@ -189,6 +196,8 @@ def lib():
         "lrs_apply_precond_T": (i32, [vp, vp, i64, vp, i64, i64, i32]),
         "lrs_solve": (i32, [vp, vp, vp, i64, vp, i64, i64, P(IterCfgC), P(ReportC), i32]),
         "lrs_bench_dmma_peak": (i32, [vp, P(f64)]),
+        "lrs_krylov": (i32, [vp, i64, i32, P(OperatorC), P(OperatorC), vp, i64, vp, i64, i64,
+                             P(IterCfgC), P(ReportC), i32]),
         "lrs_ctx_set_profiling": (i32, [vp, i32]),
         "lrs_ctx_kernel_times": (i32, [vp, vp, vp, i32]),
     }
@@ -593,3 +602,82 @@ def solve(A: CsrMatrix, f, cfg: SolverConfig | None = None, it: IterConfig | Non
         raise BreakdownError(info.message.decode(), x_out, report)
     _check(st, A.ctx.h)
     return x_out, report, F
+
+
+class _DevBlock:
+    """Zero-copy column-major device block (n x n_rhs, leading dimension ld) for torch."""
+
+    def __init__(self, ptr, ld, nrhs, dtype):
+        self.__cuda_array_interface__ = {
+            "shape": (int(nrhs), int(ld)), "typestr": "<c16" if dtype == np.complex128 else "<f8",
+            "data": (int(ptr), False), "version": 3, "strides": None}
+
+
+def _operator(fn, n, dtype):
+    """Wrap fn(x, y) (torch CUDA column-major views, y written in place) as an lrs_operator."""
+    import torch
+
+    def cb(user, pin, pout, ld, nrhs):
+        try:
+            xin = torch.as_tensor(_DevBlock(pin, ld, nrhs, dtype), device="cuda")[:, :n].t()
+            yout = torch.as_tensor(_DevBlock(pout, ld, nrhs, dtype), device="cuda")[:, :n].t()
+            fn(xin, yout)
+            torch.cuda.synchronize()
+            return 0
+        except Exception:  # reported to the caller as a failed callback
+            import traceback
+
+            traceback.print_exc()
+            return 1
+
+    f = _OPFN(cb)
+    return OperatorC(None, f), f
+
+
+def krylov(ctx: Context, apply_A, b, it: IterConfig | None = None, apply_M=None, x_out=None,
+           history_cap: int = 4096):
+    """bicgstab / cg (it.method; "gmres" too) on caller operators.
+
+    apply_A(x, y) and apply_M(x, y) receive column-major torch CUDA views (n x n_rhs) of
+    the library's device blocks and must write y = Op(x) (e.g. ``A.spmv(x, y)`` or
+    ``F.apply_precond_T(x, y)``).  apply_M None = identity.  Returns (x, SolveReport)."""
+    it = it or IterConfig()
+    b_arr = b
+    dt = np.complex128 if (getattr(b, "dtype", None) in (np.complex128,) or
+                           str(getattr(b, "dtype", "")) == "torch.complex128") else np.float64
+    n = int(b.shape[0])
+    pb, ldb, mem, nc = _buf(b_arr, n, dt)
+    if x_out is None:
+        if mem == MEM_DEVICE:
+            import torch
+
+            x_out = torch.empty((nc, n), dtype=_torch_dtype(dt), device=b.device).t()
+        else:
+            x_out = np.empty((n, nc), dtype=dt, order="F")
+    px, ldx, _, _ = _buf(x_out, n, dt)
+    if it.method not in _METHODS:
+        raise ParameterError(f"unknown Krylov method {it.method!r}")
+    x0p = None
+    if it.initial_guess is not None:
+        x0p, _, _, _ = _buf(it.initial_guess, n, dt)
+    ic = IterCfgC(_METHODS[it.method], it.restart, it.tol, it.max_iters, it.breakdown_eps, x0p)
+    opA, keepA = _operator(apply_A, n, dt)
+    opM, keepM = (_operator(apply_M, n, dt) if apply_M is not None else (None, None))
+    hist = (f64 * history_cap)()
+    rep = ReportC()
+    rep.history = ctypes.cast(hist, ctypes.POINTER(f64))
+    rep.history_cap = history_cap
+    st = lib().lrs_krylov(ctx.h, n, C128 if dt == np.complex128 else F64, ctypes.byref(opA),
+                          ctypes.byref(opM) if opM is not None else None, pb, ldb, px, ldx, nc,
+                          ctypes.byref(ic), ctypes.byref(rep), mem)
+    del keepA, keepM
+    report = SolveReport(bool(rep.converged), rep.iterations, list(hist[:rep.history_len]),
+                         rep.precond_applications, rep.matvecs, rep.residual_final,
+                         {STAGES[i]: (0, 0) for i in range(3)}, 0, rep.t_solve,
+                         bool(rep.breakdown))
+    if st == 10:
+        info = ErrorInfoC()
+        lib().lrs_last_error(ctx.h, ctypes.byref(info))
+        raise BreakdownError(info.message.decode(), x_out, report)
+    _check(st, ctx.h)
+    return x_out, report

@@ -582,6 +582,41 @@ lrs_status lrs_solve(lrs_fact* f, lrs_mat* a, const void* b, int64_t ldb, void* 
   });
 }
 
+lrs_status lrs_krylov(lrs_ctx* c, int64_t n, int32_t scalar, const lrs_operator* apply_A,
+                      const lrs_operator* apply_M, const void* b, int64_t ldb, void* x,
+                      int64_t ldx, int64_t n_rhs, const lrs_iter_cfg* cfg, lrs_report* report,
+                      int32_t mem) {
+  if (!c || !apply_A || !cfg) return LRS_ERR_PARAMETER;
+  lrs_report local{};
+  lrs_report* rep = report ? report : &local;
+  return guard(c, [&] {
+    check_mem(mem);
+    if (scalar != LRS_F64 && scalar != LRS_C128)
+      throw LrsError(LRS_ERR_PARAMETER, "scalar must be LRS_F64 or LRS_C128");
+    if (ldb < n || ldx < n || n_rhs < 0) throw LrsError(LRS_ERR_DIMENSION, "krylov: ld >= n");
+    lrs_iter_cfg cc = *cfg;
+    if (cc.breakdown_eps <= 0) cc.breakdown_eps = 1e-30;
+    if (cc.restart <= 0) cc.restart = 30;
+    if (mem == LRS_MEM_DEVICE) {
+      krylov_ops(c, n, scalar, *apply_A, apply_M, b, ldb, x, ldx, (int)n_rhs, cc, rep);
+      return;
+    }
+    const int w = scalar == LRS_C128 ? 2 : 1;
+    DevBuf<double> bo, xo, x0o;
+    int64_t lb, lx0 = n;
+    const void* bd = dev_in(c, b, ldb, n, n_rhs, mem, bo, &lb, w);
+    if (cc.x0) cc.x0 = dev_in(c, cc.x0, ldx, n, n_rhs, mem, x0o, &lx0, w);
+    xo.alloc((size_t)std::max<int64_t>(1, n * n_rhs) * w);
+    try {
+      krylov_ops(c, n, scalar, *apply_A, apply_M, bd, lb, xo.get(), n, (int)n_rhs, cc, rep);
+    } catch (const LrsError& e) {
+      if (e.status == LRS_ERR_BREAKDOWN) dev_out_finish(c, x, ldx, xo.get(), n, n_rhs, mem, w);
+      throw;
+    }
+    dev_out_finish(c, x, ldx, xo.get(), n, n_rhs, mem, w);
+  });
+}
+
 lrs_status lrs_bench_dmma_peak(lrs_ctx* c, double* tflops) {
   if (!c || !tflops) return LRS_ERR_PARAMETER;
   return guard(c, [&] { *tflops = run_dmma_peak(c); });

@@ -122,5 +122,9 @@ void apply_precond(Fact* f, const void* in, int64_t ldi, void* out, int64_t ldo,
                    int mode);
 void solve(Fact* f, Mat* a, const void* b, int64_t ldb, void* x, int64_t ldx, int nrhs,
            const lrs_iter_cfg& cfg, lrs_report* rep);
+// BiCGStab / CG / GMRES(m) on caller operators (device buffers, ld = n)
+void krylov_ops(Ctx* c, int64_t n, int32_t scalar, const lrs_operator& A, const lrs_operator* M,
+                const void* b, int64_t ldb, void* x, int64_t ldx, int nrhs,
+                const lrs_iter_cfg& cfg, lrs_report* rep);
 
 }  // namespace lrs

@@ -1816,6 +1816,134 @@ void solve(Fact* f, Mat* a, const void* b, int64_t ldb, void* x, int64_t ldx, in
     solve_t(f, a, static_cast<const double*>(b), ldb, static_cast<double*>(x), ldx, nrhs, cfg, rep);
 }
 
+// ------------------------------------------------------------------------------------
+// Krylov drivers on caller-supplied operators (bicgstab / cg take
+// abstract operator and preconditioner contracts; GMRES(m) likewise).  The space is one
+// "partition" of n rows with the same deterministic chunked reductions.
+// ------------------------------------------------------------------------------------
+template <class S>
+void krylov_ops_t(Ctx* c, int64_t n, const lrs_operator& A, const lrs_operator* M, const S* b,
+                  int64_t ldb, S* x, int64_t ldx, int nrhs, const lrs_iter_cfg& cfg,
+                  lrs_report* rep) {
+  if (n < 1) throw LrsError(LRS_ERR_DIMENSION, "krylov: n >= 1 required");
+  if (!A.apply) throw LrsError(LRS_ERR_PARAMETER, "krylov: apply_A callback required");
+  if (cfg.tol <= 0 || cfg.max_iters < 1) throw LrsError(LRS_ERR_PARAMETER, "tol > 0 and max_iters >= 1");
+  constexpr int w = SW<S>;
+  Fact sp_;  // the reduction machinery of a one-partition space (no factors)
+  Fact* f = &sp_;
+  f->ctx = c;
+  f->scalar = IsC<S>::value ? LRS_C128 : LRS_F64;
+  f->sw = w;
+  f->P = f->Pg = 1;
+  f->n = n;
+  f->row_lo = 0;
+  f->row_hi = n;
+  f->rank_pl.assign(1, 1);
+  f->pl_max = 1;
+  upload(c, f->d_rank_pl, f->rank_pl);
+  const int64_t CH = 2048;
+  for (int64_t r0 = 0; r0 < n; r0 += CH) f->chunk_start.push_back(r0);
+  f->part_first = {0, (int)f->chunk_start.size()};
+  f->chunk_start.push_back(n);
+  upload(c, f->d_chunks, f->chunk_start);
+  upload(c, f->d_part_first, f->part_first);
+  f->partial.alloc((f->chunk_start.size() - 1) * 64 * MAX_RHS * w);
+  f->persum.alloc((size_t)64 * MAX_RHS * w);
+  f->gather.alloc((size_t)64 * MAX_RHS * w);
+  f->dotout.alloc((size_t)64 * MAX_RHS * w);
+  lrs_report& R = *rep;
+  double* hist_buf = R.history;
+  const int64_t cap = R.history_cap;
+  std::memset(&R, 0, sizeof(R));
+  R.history = hist_buf;
+  R.history_cap = cap;
+  R.converged = 1;
+  LRS_CUDA(cudaEventRecord(c->ev0, c->stream));
+  bool any_brk = false;
+  double worst = 0.0;
+  std::vector<double> hist_all;
+  auto call = [&](const lrs_operator& op, const S* in, S* out, int nr) {
+    LRS_CUDA(cudaStreamSynchronize(c->stream));
+    if (op.apply(op.user, in, out, n, nr) != 0)
+      throw LrsError(LRS_ERR_PARAMETER, "krylov: operator callback failed");
+  };
+  for (int c0 = 0; c0 < nrhs; c0 += MAX_RHS) {
+    const int nr = std::min(MAX_RHS, nrhs - c0);
+    Work<S> wk;
+    wk.f = f;
+    wk.n = n;
+    wk.lo = 0;
+    wk.nl = n;
+    wk.ch = f->chunks();
+    wk.nr = nr;
+    wk.rep = &R;
+    wk.init();
+    DevBuf<S> bb, xx, tmp;
+    bb.alloc((size_t)n * nr);
+    xx.alloc((size_t)n * nr);
+    tmp.alloc((size_t)n * nr);
+    copy_block(c, bb.get(), n, b + (int64_t)c0 * ldb, ldb, n, nr);
+    const bool has_x0 = cfg.x0 != nullptr;
+    if (has_x0)
+      copy_block(c, xx.get(), n, static_cast<const S*>(cfg.x0) + (int64_t)c0 * ldx, ldx, n, nr);
+    wk.Af = [&](S* in, S* out) { call(A, in, out, nr); };
+    if (M && M->apply) wk.Mf = [&](const S* in, S* out) { call(*M, in, out, nr); };
+    else wk.Mf = [&](const S* in, S* out) { copy_block(c, out, n, in, n, n, nr); };
+    wk.Rf = [&](const S* bv, S* xv, S* out) {
+      call(A, xv, out, nr);
+      wk.axpby(1, cs_const<S>(nr, 1.0), ColScalT<S>{}, cs_const<double>(nr, 1.0), nullptr, bv, out,
+               out);
+    };
+    std::vector<double> iters;
+    std::vector<bool> conv, brk;
+    if (cfg.method == LRS_BICGSTAB) {
+      run_bicgstab(wk, bb.get(), xx.get(), cfg, has_x0, iters, conv, brk);
+    } else if (cfg.method == LRS_GMRES) {
+      run_gmres(wk, bb.get(), xx.get(), cfg, has_x0, iters, conv);
+      brk.assign(nr, false);
+    } else if (cfg.method == LRS_CG) {
+      run_cg(wk, bb.get(), xx.get(), cfg, has_x0, iters, conv, brk);
+    } else {
+      throw LrsError(LRS_ERR_PARAMETER, "unknown Krylov method");
+    }
+    for (int j = 0; j < nr; ++j) {
+      R.iterations = std::max(R.iterations, iters[j]);
+      if (!conv[j]) R.converged = 0;
+      if (brk[j]) any_brk = true;
+    }
+    std::vector<double> bn(nr), rn(nr);
+    wk.norms(bb.get(), bn.data());
+    wk.Rf(bb.get(), xx.get(), tmp.get());
+    wk.norms(tmp.get(), rn.data());
+    for (int j = 0; j < nr; ++j) worst = std::max(worst, rn[j] / (bn[j] > 0 ? bn[j] : 1.0));
+    copy_block(c, x + (int64_t)c0 * ldx, ldx, xx.get(), n, n, nr);
+    hist_all.insert(hist_all.end(), wk.hist.begin(), wk.hist.end());
+  }
+  LRS_CUDA(cudaEventRecord(c->ev1, c->stream));
+  LRS_CUDA(cudaEventSynchronize(c->ev1));
+  R.t_solve = elapsed_ms(c->ev0, c->ev1) * 1e-3;
+  R.residual_final = worst;
+  R.breakdown = any_brk ? 1 : 0;
+  R.history_total = (int64_t)hist_all.size();
+  if (R.history && R.history_cap > 0) {
+    R.history_len = std::min<int64_t>(R.history_cap, (int64_t)hist_all.size());
+    std::memcpy(R.history, hist_all.data(), sizeof(double) * R.history_len);
+  }
+  if (any_brk)
+    throw LrsError(LRS_ERR_BREAKDOWN, cfg.method == LRS_CG ? "CG breakdown" : "BiCGStab stagnation detected (SF)");
+}
+
+void krylov_ops(Ctx* c, int64_t n, int32_t scalar, const lrs_operator& A, const lrs_operator* M,
+                const void* b, int64_t ldb, void* x, int64_t ldx, int nrhs,
+                const lrs_iter_cfg& cfg, lrs_report* rep) {
+  if (scalar == LRS_C128)
+    krylov_ops_t(c, n, A, M, static_cast<const zc*>(b), ldb, static_cast<zc*>(x), ldx, nrhs, cfg,
+                 rep);
+  else
+    krylov_ops_t(c, n, A, M, static_cast<const double*>(b), ldb, static_cast<double*>(x), ldx,
+                 nrhs, cfg, rep);
+}
+
 void apply_precond(Fact* f, const void* in, int64_t ldi, void* out, int64_t ldo, int nrhs,
                    int mode) {
   if (f->scalar == LRS_C128)
