@@ -219,6 +219,16 @@ LRS_API lrs_status lrs_apply_block_jacobi(lrs_fact* f, const void* in, int64_t l
 LRS_API lrs_status lrs_apply_precond_T(lrs_fact* f, const void* in, int64_t ld_in, void* out,
                                        int64_t ld_out, int64_t n_rhs, int32_t mem);
 
+/* ---- the reduced system ---------------------------------------- */
+/* ReducedVector blocks are 2 k p x n_rhs, column-major: partition i's top tip x_{i,t} in
+ * rows [2ki, 2ki + k), its bottom tip x_{i,b} in rows [2ki + k, 2k(i+1)).  kind:
+ * LRS_REDUCED_MATVEC_LOWRANK (matvec_lowrank), LRS_REDUCED_MATVEC_EXACT
+ * (matvec_otf = matvec_exact with the exact spike tips),
+ * LRS_REDUCED_TRUNC_PRECOND (apply_truncated_precond).  Single GPU. */
+enum { LRS_REDUCED_MATVEC_LOWRANK = 0, LRS_REDUCED_MATVEC_EXACT = 1, LRS_REDUCED_TRUNC_PRECOND = 2 };
+LRS_API lrs_status lrs_reduced_apply(lrs_fact* f, int32_t kind, const void* x, int64_t ldx,
+                                     void* y, int64_t ldy, int64_t n_rhs, int32_t mem);
+
 /* ---- solve ------------------------------------------------------------------------ */
 LRS_API lrs_status lrs_solve(lrs_fact* f, lrs_mat* a, const void* b, int64_t ldb, void* x,
                              int64_t ldx, int64_t n_rhs, const lrs_iter_cfg* cfg,

@@ -194,6 +194,7 @@ def lib():
         "lrs_apply_precond": (i32, [vp, vp, i64, vp, i64, i64, i32]),
         "lrs_apply_block_jacobi": (i32, [vp, vp, i64, vp, i64, i64, i32]),
         "lrs_apply_precond_T": (i32, [vp, vp, i64, vp, i64, i64, i32]),
+        "lrs_reduced_apply": (i32, [vp, i32, vp, i64, vp, i64, i64, i32]),
         "lrs_solve": (i32, [vp, vp, vp, i64, vp, i64, i64, P(IterCfgC), P(ReportC), i32]),
         "lrs_bench_dmma_peak": (i32, [vp, P(f64)]),
         "lrs_krylov": (i32, [vp, i64, i32, P(OperatorC), P(OperatorC), vp, i64, vp, i64, i64,
@@ -515,6 +516,27 @@ class SpikeFactorization:
     def apply_block_jacobi(self, f, out=None):
         """SPEC.md:512-519."""
         return self._apply(lib().lrs_apply_block_jacobi, f, out)
+
+    def _reduced(self, kind, xr):
+        xr = np.asfortranarray(np.asarray(xr, dtype=self.A.dtype))
+        if xr.ndim == 1:
+            xr = xr.reshape(-1, 1)
+        y = np.empty_like(xr, order="F")
+        _check(lib().lrs_reduced_apply(self.h, kind, xr.ctypes.data, xr.shape[0], y.ctypes.data,
+                                       y.shape[0], xr.shape[1], MEM_HOST), self.ctx.h)
+        return y
+
+    def matvec_lowrank(self, xr):
+        """SPEC.md:349-357 on a ReducedVector block (2 k p x n_rhs, tips [t_0; b_0; t_1; ...])."""
+        return self._reduced(0, xr)
+
+    def matvec_exact(self, xr):
+        """SPEC.md:340-348 / :358-366 (exact spike tips applied on the fly)."""
+        return self._reduced(1, xr)
+
+    def apply_truncated_precond(self, gr):
+        """SPEC.md:376-385 on a ReducedVector block."""
+        return self._reduced(2, gr)
 
     def solve_block(self, i: int, R, adjoint: bool = False):
         """SPEC.md:226-241 on partition i (host arrays)."""

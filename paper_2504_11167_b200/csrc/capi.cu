@@ -582,6 +582,32 @@ lrs_status lrs_solve(lrs_fact* f, lrs_mat* a, const void* b, int64_t ldb, void* 
   });
 }
 
+lrs_status lrs_reduced_apply(lrs_fact* f, int32_t kind, const void* x, int64_t ldx, void* y,
+                             int64_t ldy, int64_t n_rhs, int32_t mem) {
+  if (!f) return LRS_ERR_PARAMETER;
+  Ctx* c = f->ctx;
+  return guard(c, [&] {
+    check_mem(mem);
+    if (kind < 0 || kind > 2) throw LrsError(LRS_ERR_PARAMETER, "unknown reduced operator");
+    if (f->dist) throw LrsError(LRS_ERR_NOT_IMPLEMENTED, "lrs_reduced_apply: single GPU only");
+    const int64_t m = f->ldr;
+    if (ldx < m || ldy < m || n_rhs < 0)
+      throw LrsError(LRS_ERR_DIMENSION, "reduced vectors have 2 k p rows");
+    const int w = f->sw;
+    // device copies with ld = 2 k p (the kernels address full-length compact blocks)
+    DevBuf<double> xi, yo;
+    xi.alloc((size_t)std::max<int64_t>(1, m * n_rhs) * w);
+    yo.alloc((size_t)std::max<int64_t>(1, m * n_rhs) * w);
+    const size_t es = sizeof(double) * w;
+    const cudaMemcpyKind kin = mem == LRS_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+    if (n_rhs > 0) LRS_CUDA(cudaMemcpy2DAsync(xi.get(), es * m, x, es * ldx, es * m, n_rhs, kin, c->stream));
+    reduced_op(f, kind, xi.get(), yo.get(), (int)n_rhs);
+    const cudaMemcpyKind kout = mem == LRS_MEM_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+    if (n_rhs > 0) LRS_CUDA(cudaMemcpy2DAsync(y, es * ldy, yo.get(), es * m, es * m, n_rhs, kout, c->stream));
+    LRS_CUDA(cudaStreamSynchronize(c->stream));
+  });
+}
+
 lrs_status lrs_krylov(lrs_ctx* c, int64_t n, int32_t scalar, const lrs_operator* apply_A,
                       const lrs_operator* apply_M, const void* b, int64_t ldb, void* x,
                       int64_t ldx, int64_t n_rhs, const lrs_iter_cfg* cfg, lrs_report* report,

@@ -122,6 +122,9 @@ void apply_precond(Fact* f, const void* in, int64_t ldi, void* out, int64_t ldo,
                    int mode);
 void solve(Fact* f, Mat* a, const void* b, int64_t ldb, void* x, int64_t ldx, int nrhs,
            const lrs_iter_cfg& cfg, lrs_report* rep);
+// reduced-system operators on compact ReducedVectors (ld = f->ldr): kind 0
+// matvec_lowrank, 1 matvec_otf, 2 apply_truncated_precond
+void reduced_op(Fact* f, int kind, void* x, void* y, int nrhs);
 // BiCGStab / CG / GMRES(m) on caller operators (device buffers, ld = n)
 void krylov_ops(Ctx* c, int64_t n, int32_t scalar, const lrs_operator& A, const lrs_operator* M,
                 const void* b, int64_t ldb, void* x, int64_t ldx, int nrhs,

@@ -1944,6 +1944,35 @@ void krylov_ops(Ctx* c, int64_t n, int32_t scalar, const lrs_operator& A, const 
                  nrhs, cfg, rep);
 }
 
+// The reduced-system operators on compact ReducedVectors:
+// kind 0 matvec_lowrank, 1 matvec_otf (= matvec_exact with exact tips), 2
+// apply_truncated_precond.  x, y: 2 k p x nrhs blocks, ld = ldr (full length).
+template <class S>
+void reduced_op_t(Fact* f, int kind, S* x, S* y, int nrhs) {
+  if (f->Pg < 2) throw LrsError(LRS_ERR_PARAMETER, "reduced system needs p >= 2");
+  if (kind != 1 && f->r == 0)
+    throw LrsError(LRS_ERR_PARAMETER, "factorization has no low-rank spikes (n_svd = 0)");
+  for (int c0 = 0; c0 < nrhs; c0 += MAX_RHS) {
+    const int nr = std::min(MAX_RHS, nrhs - c0);
+    S* xc = x + (int64_t)c0 * f->ldr;
+    S* yc = y + (int64_t)c0 * f->ldr;
+    if (kind == 0) {
+      matvec_lowrank_t(f, xc, yc, nr);
+    } else if (kind == 1) {
+      DevBuf<S> z;
+      z.alloc((size_t)f->n * nr);
+      matvec_otf_t(f, xc, yc, z.get(), nr);
+    } else {
+      trunc_precond_t(f, xc, yc, nr);
+    }
+  }
+}
+
+void reduced_op(Fact* f, int kind, void* x, void* y, int nrhs) {
+  if (f->scalar == LRS_C128) reduced_op_t(f, kind, static_cast<zc*>(x), static_cast<zc*>(y), nrhs);
+  else reduced_op_t(f, kind, static_cast<double*>(x), static_cast<double*>(y), nrhs);
+}
+
 void apply_precond(Fact* f, const void* in, int64_t ldi, void* out, int64_t ldo, int nrhs,
                    int mode) {
   if (f->scalar == LRS_C128)

@@ -93,3 +93,21 @@ def test_complex_variants(ctx, variant):
     assert rep.converged and repo.converged
     assert abs(rep.iterations - repo.iterations) <= 2
     assert _rel(x, xo) <= 1e-8
+
+
+def test_reduced_system_operators_match_oracle(ctx):
+    """matvec_lowrank / matvec_exact / apply_truncated_precond (SPEC.md:340-385) on
+    ReducedVector blocks; the preconditioner inverts the assembled truncated system."""
+    cfg = configs.make_config("c1", 48 / 256)
+    S = cfg.matrix.to_scipy()
+    A = api.CsrMatrix.from_csr(ctx, cfg.matrix)
+    gc, oc = _cfgs(cfg, "T", 8)
+    F = api.factorize(ctx, A, gc)
+    Fo = O.factorize(S, oc)
+    p, k = cfg.P, cfg.b
+    xr = np.asfortranarray(np.random.default_rng(6).standard_normal((2 * k * p, 3)))
+    xt, xb = O._unpack(xr, p, k)
+    assert _rel(F.matvec_lowrank(xr), O._pack(*O.matvec_lowrank(Fo, xt, xb))) < 1e-12
+    assert _rel(F.matvec_exact(xr), O._pack(*O.matvec_otf(Fo, xt, xb))) < 1e-12
+    g = F.apply_truncated_precond(xr)
+    assert _rel(g, O._pack(*O.apply_truncated_precond(Fo.trunc, xt, xb))) < 1e-11
