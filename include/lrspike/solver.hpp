@@ -153,6 +153,33 @@ class SpikeFactorization {
   double t_factorize_ = 0.0;
 };
 
+/// the diagonal blocks A_i and the k x k corner couplings B_i (bottom-left
+/// of the super-diagonal block, coupling partition i to i+1; i = 0..p-2) and C_i (top-right
+/// of the sub-diagonal block, coupling i to i-1; i = 1..p-1, C[0] empty).  The couplings are
+/// kept sparse.  Throws NotBlockTridiagonalError(row, col) at the first entry
+/// (row-major) outside the pattern.  Host-side data movement only.
+struct PartitionBlocks {
+  PartitionLayout layout;
+  std::vector<CsrMatrix> A, B, C;
+};
+PartitionBlocks extract_blocks(const CsrMatrix& a, const PartitionLayout& layout);
+
+/// SPEC.md:211-225 (BlockFactor / factorize_block): the LU of one block on the GPU (the
+/// p = 1 Block Jacobi factorization of A_i).
+class BlockFactor {
+ public:
+  explicit BlockFactor(std::shared_ptr<SpikeFactorization> f) : f_(std::move(f)) {}
+  index_t n() const;
+  const SpikeFactorization& factorization() const { return *f_; }
+
+ private:
+  std::shared_ptr<SpikeFactorization> f_;
+};
+BlockFactor factorize_block(const CsrMatrix& a_i);
+/// SPEC.md:226-234 / :235-241.
+DenseBlock solve_block(const BlockFactor& f, const DenseBlock& rhs);
+DenseBlock solve_block_adjoint(const BlockFactor& f, const DenseBlock& rhs);
+
 /// SPEC.md:476-484.
 std::shared_ptr<SpikeFactorization> factorize(const CsrMatrix& a, const SolverConfig& cfg);
 /// SPEC.md:485-493.

@@ -283,6 +283,80 @@ std::shared_ptr<SpikeFactorization> factorize(const CsrMatrix& a, const SolverCo
   return std::make_shared<SpikeFactorization>(std::make_shared<DeviceMatrix>(a), cfg);
 }
 
+PartitionBlocks extract_blocks(const CsrMatrix& a, const PartitionLayout& lay) {
+  if (!a.square()) throw DimensionError("extract_blocks: A must be square");
+  index_t total = 0;
+  for (index_t s : lay.sizes) total += s;
+  if (total != a.n_rows || (index_t)lay.sizes.size() != lay.p)
+    throw DimensionError("extract_blocks: layout does not match A");
+  const index_t p = lay.p, k = lay.k;
+  std::vector<index_t> off(p + 1, 0);
+  for (index_t i = 0; i < p; ++i) off[i + 1] = off[i] + lay.sizes[i];
+  struct Trip {
+    std::vector<index_t> r, c;
+    std::vector<double> v;
+  };
+  std::vector<Trip> tA(p), tB(p), tC(p);
+  index_t part = 0;
+  for (index_t row = 0; row < a.n_rows; ++row) {
+    while (row >= off[part + 1]) ++part;
+    for (index_t q = a.row_ptr[row]; q < a.row_ptr[row + 1]; ++q) {
+      const index_t col = a.col_idx[q];
+      const double v = a.values[q];
+      if (col >= off[part] && col < off[part + 1]) {
+        tA[part].r.push_back(row - off[part]);
+        tA[part].c.push_back(col - off[part]);
+        tA[part].v.push_back(v);
+      } else if (part + 1 < p && col >= off[part + 1] && col < off[part + 1] + k &&
+                 row >= off[part + 1] - k) {  // B_part: bottom-left k x k of the super block
+        tB[part].r.push_back(row - (off[part + 1] - k));
+        tB[part].c.push_back(col - off[part + 1]);
+        tB[part].v.push_back(v);
+      } else if (part > 0 && col < off[part] && col >= off[part] - k && row < off[part] + k) {
+        tC[part].r.push_back(row - off[part]);  // C_part: top-right k x k of the sub block
+        tC[part].c.push_back(col - (off[part] - k));
+        tC[part].v.push_back(v);
+      } else {
+        throw NotBlockTridiagonalError("nonzero (" + std::to_string(row) + "," +
+                                           std::to_string(col) +
+                                           ") outside the block-tridiagonal pattern; increase k "
+                                           "or decrease p",
+                                       (long)row, (long)col);
+      }
+    }
+  }
+  PartitionBlocks out;
+  out.layout = lay;
+  for (index_t i = 0; i < p; ++i) {
+    out.A.push_back(CsrMatrix::from_triplets(lay.sizes[i], lay.sizes[i], tA[i].r, tA[i].c, tA[i].v));
+    out.B.push_back(i + 1 < p ? CsrMatrix::from_triplets(k, k, tB[i].r, tB[i].c, tB[i].v)
+                              : CsrMatrix{});
+    out.C.push_back(i > 0 ? CsrMatrix::from_triplets(k, k, tC[i].r, tC[i].c, tC[i].v)
+                          : CsrMatrix{});
+  }
+  return out;
+}
+
+index_t BlockFactor::n() const { return f_->layout().sizes.at(0); }
+
+BlockFactor factorize_block(const CsrMatrix& a_i) {
+  if (!a_i.square()) throw DimensionError("factorize_block: A_i must be square");
+  SolverConfig cfg;
+  cfg.variant = Variant::BLOCK_JACOBI;
+  cfg.p = 1;
+  cfg.k = 0;
+  cfg.n_svd = 0;
+  return BlockFactor(factorize(a_i, cfg));
+}
+
+DenseBlock solve_block(const BlockFactor& f, const DenseBlock& rhs) {
+  return f.factorization().solve_block(0, rhs);
+}
+
+DenseBlock solve_block_adjoint(const BlockFactor& f, const DenseBlock& rhs) {
+  return f.factorization().solve_block_adjoint(0, rhs);
+}
+
 using ApplyFn = lrs_status (*)(lrs_fact*, const void*, int64_t, void*, int64_t, int64_t, int32_t);
 
 static DenseBlock apply_impl(const SpikeFactorization& f, const DenseBlock& rhs, ApplyFn fn) {

@@ -97,6 +97,44 @@ static void cpu_tests() {
     auto t = m.transposed();
     CHECK(t.n_rows == 3 && t.coeff(2, 0) == 1.0 && t.coeff(0, 1) == 2.0 && t.coeff(1, 1) == 3.0);
   }
+  // extract_blocks: tridiagonal, p = 2, k = 1 -> B_0, C_1 are the
+  // boundary scalars; block diagonal -> zero couplings; reassembly is exact
+  {
+    std::vector<index_t> r, c;
+    std::vector<double> v;
+    for (index_t i = 0; i < 6; ++i) {
+      r.push_back(i); c.push_back(i); v.push_back(4.0 + i);
+      if (i + 1 < 6) { r.push_back(i); c.push_back(i + 1); v.push_back(-1.0 - i); }
+      if (i > 0) { r.push_back(i); c.push_back(i - 1); v.push_back(-2.0 - i); }
+    }
+    auto T = CsrMatrix::from_triplets(6, 6, r, c, v);
+    auto bl = extract_blocks(T, make_layout(6, 2, 1));
+    CHECK(bl.A.size() == 2 && bl.A[0].n_rows == 3 && bl.A[1].coeff(0, 0) == 7.0);
+    CHECK(bl.B[0].n_rows == 1 && bl.B[0].coeff(0, 0) == T.coeff(2, 3));
+    CHECK(bl.C[1].n_rows == 1 && bl.C[1].coeff(0, 0) == T.coeff(3, 2));
+    CHECK(bl.C[0].n_rows == 0 && bl.B[1].n_rows == 0);
+    double mism = 0.0;
+    for (index_t i = 0; i < 6; ++i)
+      for (index_t j = 0; j < 6; ++j) {
+        const index_t pi = i / 3, pj = j / 3;
+        double e = 0.0;
+        if (pi == pj) e = bl.A[pi].coeff(i % 3, j % 3);
+        else if (pj == pi + 1 && i == 2 && j == 3) e = bl.B[pi].coeff(0, 0);
+        else if (pi == pj + 1 && i == 3 && j == 2) e = bl.C[pi].coeff(0, 0);
+        mism += std::fabs(e - T.coeff(i, j));
+      }
+    CHECK(mism == 0.0);
+    auto D = CsrMatrix::from_triplets(4, 4, {0, 1, 2, 3}, {0, 1, 2, 3}, {1, 2, 3, 4});
+    auto bd = extract_blocks(D, make_layout(4, 2, 1));
+    CHECK(bd.B[0].nnz() == 0 && bd.C[1].nnz() == 0);
+    bool got = false;
+    try {
+      extract_blocks(T, make_layout(6, 3, 0));
+    } catch (const NotBlockTridiagonalError& e) {
+      got = e.row() == 1 && e.col() == 2;
+    }
+    CHECK(got);
+  }
 }
 
 static double resid(const CsrMatrix& a, const DenseBlock& x, const DenseBlock& b) {
@@ -126,6 +164,25 @@ static void gpu_tests() {
     CHECK(r.second.converged);
     CHECK(r.second.iterations == 0.5);
     CHECK(std::fabs(r.first(5, 0) - b(5, 0)) < 1e-14);
+  }
+  // factorize_block / solve_block: identity, diag(2, 4), adjoint
+  {
+    auto fb = factorize_block(CsrMatrix::identity(5));
+    DenseBlock b(5, 2);
+    for (index_t i = 0; i < 5; ++i) b(i, 0) = i + 1.0, b(i, 1) = -2.0 * i;
+    auto x = solve_block(fb, b);
+    CHECK(fb.n() == 5 && x(3, 0) == 4.0 && x(4, 1) == -8.0);
+    auto fd = factorize_block(CsrMatrix::from_triplets(2, 2, {0, 1}, {0, 1}, {2.0, 4.0}));
+    DenseBlock q(2, 1);
+    q(0, 0) = 4.0;
+    q(1, 0) = 4.0;
+    auto xd = solve_block(fd, q);
+    CHECK(xd(0, 0) == 2.0 && xd(1, 0) == 1.0);
+    auto fu = factorize_block(CsrMatrix::from_triplets(2, 2, {0, 0, 1}, {0, 1, 1}, {1.0, 2.0, 1.0}));
+    DenseBlock e1(2, 1);
+    e1(0, 0) = 1.0;
+    auto xa = solve_block_adjoint(fu, e1);
+    CHECK(xa(0, 0) == 1.0 && xa(1, 0) == -2.0);
   }
   // adjoint solve of [[1,2],[0,1]]: e1 -> (1,-2), one 2x2 block (p=1)
   {
