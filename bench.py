@@ -300,10 +300,12 @@ def run_ours(args):
     # ---- roofline: dominant kernel = band-LU trailing update (DMMA, FP64 tensor core)
     info = infos[-1]
     upd_ms, upd_n = kt["lu_update"]
-    # algorithmic (no-fill) flops of the bulk trailing update lu_gemm<1>: for pivot column
-    # j (row tile K = j / 128) the rank-1 update of rows and columns >= 128 (K + 2); the
-    # look-ahead row/column K + 1 is critical-path work timed with the panel
-    lu_upd_flops = sum(_rest_update_flops(s, info["kl"], info["ku"], info["nb"])
+    # algorithmic (no-fill) flops of the bulk trailing update: for pivot column j (row tile
+    # K = j / 128) the rank-1 update of rows and columns beyond the look-ahead row/column
+    # (>= K + 2; >= K0 + 3 for the two-step launches of steps K0, K0 + 1); the look-ahead
+    # rows/columns are critical-path work timed with the panel
+    lu_upd_flops = sum(_rest_update_flops(s, info["kl"], info["ku"], info["nb"],
+                                          bool(info.get("lu_pairs", 0)))
                        for s in _partition_sizes(cfg.matrix.n, cfg.P))
     per_launch_flops = lu_upd_flops * args.steps / max(upd_n, 1)
     avg_launch_s = upd_ms / max(upd_n, 1) / 1e3
@@ -337,7 +339,9 @@ def run_ours(args):
         "t_solve_s": reps[-1].wall_time,
         "e2e": {"value": e2e, "unit": "s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
         "gpu_launches": int(launches),
-        "roofline": {"bound": "tensor", "kernel": "lu_gemm_kernel<1> (DMMA trailing update)",
+        "roofline": {"bound": "tensor",
+                     "kernel": ("lu_gemm_kernel<4> (two-step DMMA trailing update)"
+                                if info.get("lu_pairs") else "lu_gemm_kernel<1> (DMMA trailing update)"),
                      "achieved": achieved_tf, "peak": dmma_peak, "unit": "TFLOP/s",
                      "frac": achieved_tf / dmma_peak if dmma_peak else None,
                      "peak_source": "in-run FP64 DMMA microbenchmark (MEASURED_PEAKS.json has no FP64); "
@@ -367,9 +371,12 @@ def run_ours(args):
     return 0
 
 
-def _rest_update_flops(s, kl, ku, nb=128):
+def _rest_update_flops(s, kl, ku, nb=128, pairs=False):
     j = np.arange(s, dtype=np.int64)
-    lo = (j // nb + 2) * nb
+    K = j // nb
+    # single steps: rows/cols >= K + 2; two-step (rank-256) launches for the pair (K0, K0+1),
+    # K0 even: rows/cols >= K0 + 4 (look-ahead depth 2)
+    lo = (K + (np.where(K % 2 == 0, 4, 3) if pairs else 2)) * nb
     ni = np.clip(np.minimum(j + kl, s - 1) - np.maximum(j + 1, lo) + 1, 0, None).astype(np.float64)
     nc = np.clip(np.minimum(j + ku, s - 1) - np.maximum(j + 1, lo) + 1, 0, None).astype(np.float64)
     return float(2.0 * np.sum(ni * nc))

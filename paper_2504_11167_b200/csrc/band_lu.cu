@@ -202,6 +202,9 @@ constexpr size_t GEMM_SMEM = sizeof(double) * GEMM_STAGES * (AS_STAGE + BS_STAGE
 #ifndef LRS_LU_PERSISTENT
 #define LRS_LU_PERSISTENT 0  // measured: persistent 0.311 s (TPC 2) vs 0.308 s per-tile CTAs
 #endif
+#ifndef LRS_LU_PAIRS
+#define LRS_LU_PAIRS 1  // two-step (rank-256) trailing updates
+#endif
 #ifndef LRS_REST_TPC
 #define LRS_REST_TPC 4
 #endif
@@ -336,6 +339,77 @@ __device__ __forceinline__ void tile_gemm(const double* A, const double* B, doub
   if (piv_status && bad_col != 0x7fffffff) atomicMin(piv_status, bad_col);
 }
 
+// Two-step trailing update C -= A0 B0 + A1 B1 (the rank-128 updates of steps K and K+1
+// in one pass over C: half the C traffic and one prologue/epilogue per 2 x 128 of K).
+// kbeg = 1 skips step K where its L / U tile lies outside the band.  Same fragments and
+// pipeline as tile_gemm; C is prefetched into L2 and subtracted in the epilogue.
+__device__ __forceinline__ void tile_gemm_pair(const double* A0, const double* B0,
+                                               const double* A1, const double* B1, double* C,
+                                               double* sm, int kbeg, int h) {
+  double* As = sm;
+  double* Bs = sm + GEMM_STAGES * AS_STAGE;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int wm = w & 1, wn = w >> 1;
+  const int g = lane >> 2, t = lane & 3;
+  const int n0 = h * GEMM_CN;
+  B0 += (int64_t)n0 * NB;
+  B1 += (int64_t)n0 * NB;
+  C += (int64_t)n0 * NB;
+  constexpr int NK = NB / KC;
+  const int q0 = kbeg * NK, q1 = 2 * NK;
+  auto load = [&](int q, int st) {
+    const double* A = q < NK ? A0 : A1;
+    const double* B = q < NK ? B0 : B1;
+    gemm_load_chunk(A, B, As + st * AS_STAGE, Bs + st * BS_STAGE, q % NK, tid);
+  };
+  if (tid == 0) bulk_prefetch_l2(C, sizeof(double) * NB * GEMM_CN);
+  double acc[4][8][2];
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[j][i][0] = acc[j][i][1] = 0.0;
+  load(q0, 0);
+#pragma unroll 1
+  for (int q = q0; q < q1; ++q) {
+    const int st = (q - q0) & 1;
+    if (q + 1 < q1) {
+      load(q + 1, st ^ 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const double* as = As + st * AS_STAGE;
+    const double* bs = Bs + st * BS_STAGE;
+#pragma unroll
+    for (int k4 = 0; k4 < KC / 4; ++k4) {
+      const int kk = k4 * 4 + t;
+      double fa[8], fb[4];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) fa[i] = as[kk * AS_LD + 64 * wm + 8 * i + g];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) fb[j] = bs[(32 * wn + 8 * j + g) * BS_LD + kk];
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) dmma_8x8x4(acc[j][i][0], acc[j][i][1], fb[j], fa[i]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int nn = 32 * wn + 8 * j + g;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      double2* cp = reinterpret_cast<double2*>(C + (int64_t)nn * NB + 64 * wm + 8 * i + 2 * t);
+      double2 v = *cp;
+      v.x -= acc[j][i][0];
+      v.y -= acc[j][i][1];
+      *cp = v;
+    }
+  }
+}
+
 template <int KIND>
 __global__ void __launch_bounds__(GEMM_THREADS, GEMM_SPLIT) lu_gemm_kernel(BandGeom g, double* tiles,
                                                                            int K, int* status) {
@@ -367,7 +441,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, GEMM_SPLIT) lu_gemm_kernel(BandG
     const int J = K + 2 + x % (g.wu - 1);
     if (I >= T || J >= T) return;
     tile_gemm<1, MASK_NONE, MASK_NONE>(tile(I, K), tile(K, J), tile(I, J), sm, nullptr, 0, h);
-  } else {
+  } else if (KIND == 2) {
     // look-ahead part of the trailing update: column K+1 (I = K+1..K+wl) and row K+1
     // (J = K+2..K+wu), i.e. everything diag/panel of step K+1 needs
     int I, J;
@@ -380,6 +454,36 @@ __global__ void __launch_bounds__(GEMM_THREADS, GEMM_SPLIT) lu_gemm_kernel(BandG
     }
     if (I >= T || J >= T) return;
     tile_gemm<1, MASK_NONE, MASK_NONE>(tile(I, K), tile(K, J), tile(I, J), sm, nullptr, 0, h);
+  } else {
+    // two-step updates with steps K and K+1 (K + 1 < T), look-ahead depth 2:
+    //   KIND 3 (look-ahead): columns K+2 (I = K+2..K+1+wl), K+3 (I = K+3..K+1+wl) and rows
+    //                        K+2 (J = K+3..K+1+wu), K+3 (J = K+4..K+1+wu)
+    //   KIND 4 (bulk):       I = K+4..K+1+wl, J = K+4..K+1+wu
+    int I, J;
+    if (KIND == 3) {
+      int y = x;
+      if (y < g.wl) {
+        I = K + 2 + y;
+        J = K + 2;
+      } else if ((y -= g.wl) < g.wl - 1) {
+        I = K + 3 + y;
+        J = K + 3;
+      } else if ((y -= g.wl - 1) < g.wu - 1) {
+        I = K + 2;
+        J = K + 3 + y;
+      } else {
+        y -= g.wu - 1;
+        I = K + 3;
+        J = K + 4 + y;
+      }
+    } else {
+      I = K + 4 + x / (g.wu - 2);
+      J = K + 4 + x % (g.wu - 2);
+    }
+    if (K + 1 >= T || I >= T || J >= T) return;
+    const int kbeg = (I - K > g.wl || J - K > g.wu) ? 1 : 0;
+    tile_gemm_pair(kbeg ? nullptr : tile(I, K), kbeg ? nullptr : tile(K, J), tile(I, K + 1),
+                   tile(K + 1, J), tile(I, J), sm, kbeg, h);
   }
 }
 
@@ -491,6 +595,10 @@ static void lu_attrs() {
                                 (int)GEMM_SMEM));
   LRS_CUDA(cudaFuncSetAttribute(lu_gemm_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)GEMM_SMEM));
+  LRS_CUDA(cudaFuncSetAttribute(lu_gemm_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)GEMM_SMEM));
+  LRS_CUDA(cudaFuncSetAttribute(lu_gemm_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)GEMM_SMEM));
   g_lu_attr_set = true;
 }
 
@@ -515,9 +623,15 @@ static void real_gemm(Ctx* c, cudaStream_t s, const BandGeom& g, void* tiles, in
   } else if (kind == 1)
     lu_gemm_kernel<1><<<dim3(S * (g.wl - 1) * (g.wu - 1), g.P), GEMM_THREADS, GEMM_SMEM, s>>>(
         g, t, K, status);
-  else
+  else if (kind == 2)
     lu_gemm_kernel<2><<<dim3(S * (g.wl + g.wu - 1), g.P), GEMM_THREADS, GEMM_SMEM, s>>>(g, t, K,
                                                                                        status);
+  else if (kind == 3)
+    lu_gemm_kernel<3><<<dim3(S * (2 * g.wl + 2 * g.wu - 4), g.P), GEMM_THREADS, GEMM_SMEM, s>>>(
+        g, t, K, status);
+  else
+    lu_gemm_kernel<4><<<dim3(S * (g.wl - 2) * (g.wu - 2), g.P), GEMM_THREADS, GEMM_SMEM, s>>>(
+        g, t, K, status);
 }
 
 static void lu_diag_panel(Ctx* c, cudaStream_t s, const BandGeom& g, void* tiles, int K,
@@ -534,9 +648,13 @@ static void lu_diag_panel(Ctx* c, cudaStream_t s, const BandGeom& g, void* tiles
   }
 }
 
+bool lu_real_pairs(const BandGeom& g) {
+  return lu_uses_pairs(g, LuKernels{real_diag, real_gemm, LRS_LU_PAIRS != 0});
+}
+
 void launch_band_lu(Ctx* c, const BandGeom& g, double* tiles, int Tmax, int* status) {
   lu_attrs();
-  run_band_lu(c, g, tiles, Tmax, status, LuKernels{real_diag, real_gemm});
+  run_band_lu(c, g, tiles, Tmax, status, LuKernels{real_diag, real_gemm, LRS_LU_PAIRS != 0});
 }
 
 // Right-looking tiled LU with look-ahead depth 1 over two streams:
@@ -544,6 +662,10 @@ void launch_band_lu(Ctx* c, const BandGeom& g, double* tiles, int Tmax, int* sta
 //   main               : [wait panel(K)]  rest(K)
 // next(K) applies step K to pivot row/column K+1 only, so diag/panel of step K+1
 // overlap the bulk trailing update rest(K) (I, J >= K+2) instead of idling the GPU.
+bool lu_uses_pairs(const BandGeom& g, const LuKernels& L) {
+  return L.pairs && g.wl >= 3 && g.wu >= 3;
+}
+
 void run_band_lu(Ctx* c, const BandGeom& g, void* tiles, int Tmax, int* status,
                  const LuKernels& L) {
   if (Tmax <= 0) return;
@@ -554,6 +676,40 @@ void run_band_lu(Ctx* c, const BandGeom& g, void* tiles, int Tmax, int* status,
   LRS_CUDA(cudaStreamWaitEvent(sc, ev_start, 0));
   lu_diag_panel(c, sc, g, tiles, 0, status, L);
   LRS_CUDA(cudaEventRecord(ev_panel, sc));
+  auto gemm = [&](cudaStream_t s, int K, int kind, int cls) {
+    ProfScope ps_(c, cls, s);
+    L.gemm(c, s, g, tiles, K, status, kind);
+    LRS_LAUNCHED(c);
+  };
+  if (lu_uses_pairs(g, L)) {
+    // Steps in pairs (K, K+1) with a rank-256 bulk update and look-ahead depth 2:
+    //   main: [wait panel(K+1)] rest2(K, K+1)                       (I, J >= K+4)
+    //   crit: [wait rest2(K-2, K-1)] next3(K, K+1) (rows/cols K+2, K+3) -> diag/panel(K+2)
+    //         -> next(K+2) (row/col K+3) -> diag/panel(K+3)
+    // so diag/panel(K+2), (K+3) run under rest2(K, K+1) and main never waits on crit.
+    if (Tmax > 1) {
+      gemm(sc, 0, 2, K_LU_PANEL);
+      lu_diag_panel(c, sc, g, tiles, 1, status, L);
+      LRS_CUDA(cudaEventRecord(ev_panel, sc));
+    }
+    bool have_rest = false;
+    for (int K = 0; K + 1 < Tmax; K += 2) {
+      if (have_rest) LRS_CUDA(cudaStreamWaitEvent(sc, ev_rest, 0));  // rest2(K-2, K-1)
+      LRS_CUDA(cudaStreamWaitEvent(sm, ev_panel, 0));                  // diag/panel(K+1)
+      gemm(sm, K, 4, K_LU_UPDATE);
+      LRS_CUDA(cudaEventRecord(ev_rest, sm));
+      have_rest = true;
+      if (K + 2 < Tmax) {
+        gemm(sc, K, 3, K_LU_PANEL);
+        lu_diag_panel(c, sc, g, tiles, K + 2, status, L);
+        if (K + 3 < Tmax) {
+          gemm(sc, K + 2, 2, K_LU_PANEL);
+          lu_diag_panel(c, sc, g, tiles, K + 3, status, L);
+        }
+        LRS_CUDA(cudaEventRecord(ev_panel, sc));
+      }
+    }
+  } else
   for (int K = 0; K < Tmax; ++K) {
     if (K + 1 < Tmax) {
       if (K >= 1) LRS_CUDA(cudaStreamWaitEvent(sc, ev_rest, 0));

@@ -50,11 +50,16 @@ void launch_band_lu_z(Ctx* c, const BandGeom& g, zc* tiles, int Tmax, int* statu
 // the look-ahead driver, shared by the real and complex kernels
 struct LuKernels {
   void (*diag)(Ctx*, cudaStream_t, const BandGeom&, void* tiles, int K, int* status);
-  // kind 0: panel, 1: rest of the trailing update, 2: look-ahead row/column
+  // kind 0: panel, 1: rest of the trailing update, 2: look-ahead row/column; with pairs:
+  // 3: look-ahead row/column K+2 with steps K, K+1; 4: the rest with steps K, K+1
   void (*gemm)(Ctx*, cudaStream_t, const BandGeom&, void* tiles, int K, int* status, int kind);
+  bool pairs = false;
 };
 void run_band_lu(Ctx* c, const BandGeom& g, void* tiles, int Tmax, int* status,
                  const LuKernels& L);
+bool lu_uses_pairs(const BandGeom& g, const LuKernels& L);
+// the real LU runs two-step (rank-256) bulk updates when the band spans >= 2 tiles
+bool lu_real_pairs(const BandGeom& g);
 void launch_extract_tiles_z(Ctx* c, const Mat* m, const BandGeom& g, zc* tiles, int64_t k,
                             int64_t row_lo, int64_t row_hi, unsigned long long* d_bad);
 

@@ -890,6 +890,7 @@ Fact* factorize(Ctx* c, Mat* m, const lrs_solver_cfg& cfg, const lrs_comm* comm)
   in.factor_bytes = f->total_tiles * TILE_ELEMS * (int64_t)sizeof(double) * w;
   in.rank_collapsed = f->rank_collapsed;
   in.variant = f->variant;
+  in.lu_pairs = cplx ? 0 : (lu_real_pairs(g) ? 1 : 0);
   in.t_lu = elapsed_ms(e0, e1) * 1e-3;
   in.t_spikes = elapsed_ms(e1, e2) * 1e-3;
   in.t_precond = 0.0;
