@@ -259,7 +259,9 @@ def _buf(a, n_rows, dtype=np.float64):
             return a.data_ptr(), n_rows, MEM_DEVICE, 1
         # torch: column-major blocks are stored as (n_rhs, n) row-major == (n, n_rhs) F-order
         if a.stride(0) == 1:
-            return a.data_ptr(), a.stride(1), MEM_DEVICE, a.shape[1]
+            # a single column's stride is arbitrary (numpy / torch relaxed strides)
+            ld = a.stride(1) if a.shape[1] > 1 else max(n_rows, 1)
+            return a.data_ptr(), ld, MEM_DEVICE, a.shape[1]
         raise DimensionError("device block must be column-major (stride(0) == 1)")
     arr = np.asarray(a)
     if arr.ndim == 1:
