@@ -24,6 +24,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <functional>
+#include <thread>
 #include <future>
 #include <type_traits>
 
@@ -227,15 +228,31 @@ void apply_precond_t(Fact* f, const S* in, int64_t ldi, S* out, int64_t ldo, int
 // ------------------------------------------------------------------------------------
 // Gaussian test blocks of the spikes of partitions [plo, phi): slot 2*i + side, k x l each
 // (real for both fields, as the shared generator draws them).
+// Drawn on the host with the shared counter-based generator (bit-identical to the
+// checker's Omega), split over host threads: every draw is a pure function of (seed,
+// stream, index), so the result does not depend on the thread count.
 std::vector<double> make_omega(uint64_t seed, int Pg, int plo, int phi, int64_t k, int l) {
   std::vector<double> h((size_t)Pg * 2 * k * l, 0.0);
+  std::vector<std::pair<int, int>> slots;
   for (int i = plo; i < phi; ++i)
-    for (int side = 0; side < 2; ++side) {
-      if ((side == LRS_SIDE_T && i == Pg - 1) || (side == LRS_SIDE_W && i == 0)) continue;
+    for (int side = 0; side < 2; ++side)
+      if (!((side == LRS_SIDE_T && i == Pg - 1) || (side == LRS_SIDE_W && i == 0)))
+        slots.push_back({i, side});
+  const int64_t per = k * l, total = per * (int64_t)slots.size();
+  if (total == 0) return h;
+  unsigned nt = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+  nt = (unsigned)std::min<int64_t>(nt, std::max<int64_t>(1, total / 65536));
+  auto work = [&](int64_t e0, int64_t e1) {
+    for (int64_t e = e0; e < e1; ++e) {
+      const auto [i, side] = slots[e / per];
       const uint64_t key = lrs_rng_key(seed, LRS_STREAM_OMEGA + 2ull * i + side);
-      double* o = h.data() + (size_t)(2 * i + side) * k * l;
-      for (int64_t e = 0; e < k * l; ++e) o[e] = lrs_rng_normal(key, (uint64_t)e);
+      h[(size_t)(2 * i + side) * per + e % per] = lrs_rng_normal(key, (uint64_t)(e % per));
     }
+  };
+  std::vector<std::thread> th;
+  for (unsigned t = 1; t < nt; ++t) th.emplace_back(work, total * t / nt, total * (t + 1) / nt);
+  work(0, total / nt);
+  for (auto& t : th) t.join();
   return h;
 }
 
