@@ -148,6 +148,7 @@ typedef struct lrs_fact_info {
   double t_lu, t_spikes, t_precond; /* stage split of t_factorize */
   double max_interface_cond;
   int32_t lu_pairs;             /* bulk LU updates ran two steps (rank 256) per launch */
+  int32_t pivoted;              /* some block needed row interchanges: partial-pivoting LU */
 } lrs_fact_info;
 
 typedef struct lrs_error_info {

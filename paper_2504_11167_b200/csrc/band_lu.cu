@@ -24,6 +24,7 @@
 #include "common.cuh"
 #include "kernels.h"
 #include "lrs_internal.h"
+#include "lu_common.cuh"
 
 namespace lrs {
 
@@ -129,44 +130,7 @@ __global__ void __launch_bounds__(DIAG_THREADS, 1) lu_diag_kernel(BandGeom g, do
     }
     __syncthreads();
   }
-  // ---- in-place inverses: threads 0..255 invert U (upper, non-unit, LAPACK dtrti2 'U'),
-  //      threads 256..511 invert L (unit lower, dtrti2 'L' 'U'); disjoint triangles.
-  const int half = tid >> 8;           // 0: U, 1: L
-  const int q = (tid >> 7) & 1;        // k-phase
-  double* pq = part + (half * 2 + q) * NB;
-  for (int s = 0; s < NB; ++s) {
-    // phase 1: partial triangular mat-vec products (reads only)
-    double ujj_inv = 0.0;
-    if (half == 0) {
-      const int j = s;
-      // t_i = sum_{k=i}^{j-1} invU[i][k] * U[k][j]   for i < j
-      double t = 0.0;
-      if (i < j)
-        for (int kk = i + q; kk < j; kk += 2) t = fma(A[kk * NB + i], A[j * NB + kk], t);
-      pq[i] = t;
-      ujj_inv = 1.0 / A[j * NB + j];
-    } else {
-      const int j = NB - 1 - s;
-      // t_i = sum_{k=j+1}^{i-1} invL[i][k] * L[k][j]   for i > j
-      double t = 0.0;
-      if (i > j)
-        for (int kk = j + 1 + q; kk < i; kk += 2) t = fma(A[kk * NB + i], A[j * NB + kk], t);
-      pq[i] = t;
-    }
-    __syncthreads();
-    // phase 2: write column j (disjoint addresses; no reads of other threads' outputs)
-    if (q == 0) {
-      if (half == 0) {
-        const int j = s;
-        if (i < j) A[j * NB + i] = -ujj_inv * (part[i] + part[NB + i]);
-        else if (i == j) A[j * NB + j] = ujj_inv;
-      } else {
-        const int j = NB - 1 - s;
-        if (i > j) A[j * NB + i] = -(A[j * NB + i] + part[2 * NB + i] + part[3 * NB + i]);
-      }
-    }
-    __syncthreads();
-  }
+  diag_inverses(A, part, tid);
   for (int e = tid; e < TILE_ELEMS; e += DIAG_THREADS) gt[e] = A[e];
 }
 
@@ -422,7 +386,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, GEMM_SPLIT) lu_gemm_kernel(BandG
     return tiles + (base + (int64_t)I * g.W + (J - I + g.wl)) * TILE_ELEMS;
   };
   const int x = blockIdx.x / GEMM_SPLIT, h = blockIdx.x % GEMM_SPLIT;
-  if (KIND == 0) {
+  if (KIND == 5) {
+    // pivoting path: only U_KJ = inv(L_KK) A_KJ (the panel kernel produced L_IK)
+    const int J = K + 1 + x;
+    if (J >= T) return;
+    tile_gemm<0, MASK_UNIT_LOWER, MASK_NONE>(tile(K, K), tile(K, J), tile(K, J), sm, nullptr, 0,
+                                             h);
+  } else if (KIND == 0) {
     if (x < g.wl) {
       const int I = K + 1 + x;
       if (I >= T) return;
@@ -599,6 +569,8 @@ static void lu_attrs() {
                                 (int)GEMM_SMEM));
   LRS_CUDA(cudaFuncSetAttribute(lu_gemm_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)GEMM_SMEM));
+  LRS_CUDA(cudaFuncSetAttribute(lu_gemm_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)GEMM_SMEM));
   g_lu_attr_set = true;
 }
 
@@ -626,6 +598,8 @@ static void real_gemm(Ctx* c, cudaStream_t s, const BandGeom& g, void* tiles, in
   else if (kind == 2)
     lu_gemm_kernel<2><<<dim3(S * (g.wl + g.wu - 1), g.P), GEMM_THREADS, GEMM_SMEM, s>>>(g, t, K,
                                                                                        status);
+  else if (kind == 5)
+    lu_gemm_kernel<5><<<dim3(S * g.wu, g.P), GEMM_THREADS, GEMM_SMEM, s>>>(g, t, K, status);
   else if (kind == 3)
     lu_gemm_kernel<3><<<dim3(S * (2 * g.wl + 2 * g.wu - 4), g.P), GEMM_THREADS, GEMM_SMEM, s>>>(
         g, t, K, status);
@@ -645,6 +619,35 @@ static void lu_diag_panel(Ctx* c, cudaStream_t s, const BandGeom& g, void* tiles
     ProfScope ps_(c, K_LU_PANEL, s);
     L.gemm(c, s, g, tiles, K, status, 0);
     LRS_LAUNCHED(c);
+  }
+}
+
+// Partial-pivoting band LU (band_lu_piv.cu for the panel; the DMMA kernels above for
+// U_KJ and the trailing update).  One stream, no look-ahead: the interchanges of step K
+// touch the tiles the trailing update of step K-1 writes.
+void launch_band_lu_piv(Ctx* c, const BandGeom& g, double* tiles, int Tmax, int* status,
+                        int* ipiv, int* perm) {
+  lu_attrs();
+  cudaStream_t s = c->stream;
+  for (int K = 0; K < Tmax; ++K) {
+    launch_lu_panel_piv(c, s, g, tiles, K, ipiv, perm, status);
+    if (g.wu > 0) {
+      ProfScope ps_(c, K_LU_PANEL, s);
+      real_gemm(c, s, g, tiles, K, status, 5);
+      LRS_LAUNCHED(c);
+    }
+    if (g.wl > 0 && g.wu > 0) {
+      {
+        ProfScope ps_(c, K_LU_PANEL, s);
+        real_gemm(c, s, g, tiles, K, status, 2);
+        LRS_LAUNCHED(c);
+      }
+      if (g.wl > 1 && g.wu > 1) {
+        ProfScope ps_(c, K_LU_UPDATE, s);
+        real_gemm(c, s, g, tiles, K, status, 1);
+        LRS_LAUNCHED(c);
+      }
+    }
   }
 }
 

@@ -1,0 +1,372 @@
+// Band LU with partial pivoting (LAPACK dgbtrf semantics) and the
+// matching solves (dgbtrs), for blocks the no-interchange path of band_lu.cu rejects.
+//
+// Storage: the same tiles as band_lu.cu with the upper band widened to ku + kl (the fill
+// of the row interchanges): wu' = ceil((ku + kl) / 128) tile columns.  Step K:
+//   lu_panel_piv : the tall panel (rows K*128 .. (K+1+wl)*128 of column tile K) factored
+//                  column by column with partial pivoting by a 16-CTA cluster (rows split
+//                  over the CTAs; pivot search = block argmax + fixed-rank-order reduction
+//                  over distributed shared memory, first maximum wins as in idamax).  The
+//                  interchanges are applied across the panel's 128 columns (so the panel
+//                  holds P_K-permuted L, like dgetrf on the panel) and recorded in ipiv;
+//                  the composed row permutation of the step is stored for the solves.
+//   diag_invert  : inv(L_KK) strictly below, inv(U_KK) on/above the diagonal (as always)
+//   swap_trail   : the step's interchanges on the trailing tile columns K+1 .. K+wu'
+//   then the DMMA kernels of band_lu.cu: U_KJ = inv(L_KK) A_KJ and the trailing update.
+// Solves: L (forward) and L^T (backward) step by step with the interleaved permutations
+// (dgbtrs); U and U^T with the dataflow kernels of band_solve.cu over the wider band.
+#include <cooperative_groups.h>
+
+#include "common.cuh"
+#include "kernels.h"
+#include "lrs_internal.h"
+#include "lu_common.cuh"
+
+namespace lrs {
+
+namespace cg = cooperative_groups;
+
+constexpr int PIV_CL = 16;       // CTAs per partition (non-portable cluster size)
+constexpr int PIV_THREADS = 512;
+constexpr int PIV_MAXPERM = 2 * NB;  // rows moved by one step's 128 interchanges
+
+__device__ __forceinline__ bool piv_better(double v, int i, double bv, int bi) {
+  return v > bv || (v == bv && i < bi);
+}
+
+__global__ void __cluster_dims__(PIV_CL, 1, 1) __launch_bounds__(PIV_THREADS, 1)
+    lu_panel_piv_kernel(BandGeom g, double* tiles, int K, int* ipiv, int* perm, int* status) {
+  cg::cluster_group cluster = cg::this_cluster();
+  const int crank = (int)cluster.block_rank();
+  const int p = blockIdx.x / PIV_CL;
+  const int T = g.T[p];
+  if (K >= T) return;  // the whole cluster returns together
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  constexpr int NW = PIV_THREADS / 32;
+  __shared__ double wv[NW];
+  __shared__ int wi[NW];
+  __shared__ double slot_v[2];
+  __shared__ int slot_i[2];
+  __shared__ double urow[NB];
+  __shared__ int s_piv;
+  __shared__ double s_pv;
+  const int64_t base = g.tbase[p];
+  const int r0 = K * NB;
+  const int Ilast = min(T - 1, K + g.wl);
+  const int rend = (Ilast + 1) * NB;
+  const int H = rend - r0;
+  const int per = (H + PIV_CL - 1) / PIV_CL;
+  const int slo = r0 + crank * per, shi = min(rend, slo + per);
+  auto el = [&](int r, int c) -> double* {
+    const int I = r >> 7;
+    return tiles + (base + (int64_t)I * g.W + (K - I + g.wl)) * TILE_ELEMS + (r & (NB - 1)) +
+           (int64_t)c * NB;
+  };
+  int* piv = ipiv + g.fbase[p] * NB;
+  int par = 0;
+  for (int c = 0; c < NB; ++c) {
+    const int j = r0 + c;
+    // ---- pivot search: first max |a_rj|, r >= j ----------------------------------------
+    double bv = -1.0;
+    int bi = 0x7fffffff;
+    for (int r = max(j, slo) + tid; r < shi; r += PIV_THREADS) {
+      const double v = fabs(*el(r, c));
+      if (piv_better(v, r, bv, bi)) bv = v, bi = r;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (piv_better(ov, oi, bv, bi)) bv = ov, bi = oi;
+    }
+    if (lane == 0) wv[w] = bv, wi[w] = bi;
+    __syncthreads();
+    if (tid == 0) {
+      double v = -1.0;
+      int ii = 0x7fffffff;
+      for (int q = 0; q < NW; ++q)
+        if (piv_better(wv[q], wi[q], v, ii)) v = wv[q], ii = wi[q];
+      slot_v[par] = v;
+      slot_i[par] = ii;
+    }
+    cluster.sync();
+    if (tid == 0) {
+      double v = -1.0;
+      int ii = 0x7fffffff;
+      for (int rk = 0; rk < PIV_CL; ++rk) {
+        const double ov = *cluster.map_shared_rank(&slot_v[par], rk);
+        const int oi = *cluster.map_shared_rank(&slot_i[par], rk);
+        if (piv_better(ov, oi, v, ii)) v = ov, ii = oi;
+      }
+      s_piv = ii;
+      s_pv = v;
+    }
+    __syncthreads();
+    const int prow = s_piv;
+    if (crank == 0) {
+      if (tid == 0) {
+        piv[j] = prow;
+        if (s_pv == 0.0) atomicMin(&status[2 * p + 1], j);
+      }
+      if (prow != j && tid < NB) {  // interchange across the panel's columns
+        double* a = el(j, tid);
+        double* b = el(prow, tid);
+        const double t = *a;
+        *a = *b;
+        *b = t;
+      }
+    }
+    cluster.sync();
+    par ^= 1;
+    // ---- scale the column and rank-1 update of this CTA's rows ------------------------
+    if (tid < NB) urow[tid] = tid > c ? *el(j, tid) : 0.0;
+    __syncthreads();
+    const double pv = *el(j, c);
+    if (pv != 0.0) {  // dgbtf2 skips scaling / update on an exact zero pivot
+      const double inv = 1.0 / pv;
+      for (int r = max(j + 1, slo) + tid; r < shi; r += PIV_THREADS) {
+        double* lr = el(r, c);
+        const double l = *lr * inv;
+        *lr = l;
+        if (l != 0.0)
+          for (int c2 = c + 1; c2 < NB; ++c2) {
+            double* a = el(r, c2);
+            *a = fma(-l, urow[c2], *a);
+          }
+      }
+    }
+    __syncthreads();
+  }
+  // ---- the step's composed permutation: new x[dst] = old x[src] (rank 0) ---------------
+  if (crank == 0) {
+    extern __shared__ int idx[];  // H entries
+    for (int e = tid; e < H; e += PIV_THREADS) idx[e] = r0 + e;
+    __syncthreads();
+    if (tid == 0) {
+      for (int c = 0; c < NB; ++c) {
+        const int a = c, b = piv[r0 + c] - r0;
+        const int t = idx[a];
+        idx[a] = idx[b];
+        idx[b] = t;
+      }
+      int* pl = perm + ((int64_t)g.fbase[p] + K) * (2 * PIV_MAXPERM + 1);
+      int cnt = 0;
+      for (int e = 0; e < H; ++e)
+        if (idx[e] != r0 + e) {
+          pl[1 + 2 * cnt] = r0 + e;     // dst
+          pl[2 + 2 * cnt] = idx[e];     // src
+          ++cnt;
+        }
+      pl[0] = cnt;
+    }
+  }
+  cluster.sync();
+}
+
+// inv(L_KK) / inv(U_KK) of the factored diagonal tile, in place
+__global__ void __launch_bounds__(512, 1) diag_invert_kernel(BandGeom g, double* tiles, int K) {
+  extern __shared__ double sm[];
+  double* A = sm;
+  double* part = sm + TILE_ELEMS;
+  const int p = blockIdx.x;
+  if (K >= g.T[p]) return;
+  double* gt = tiles + (g.tbase[p] + (int64_t)K * g.W + g.wl) * TILE_ELEMS;
+  for (int e = threadIdx.x; e < TILE_ELEMS; e += 512) A[e] = gt[e];
+  __syncthreads();
+  diag_inverses(A, part, threadIdx.x);
+  for (int e = threadIdx.x; e < TILE_ELEMS; e += 512) gt[e] = A[e];
+}
+
+// the step's interchanges (in order) on tile columns K+1 .. K+wu: one thread per column
+__global__ void swap_trailing_kernel(BandGeom g, double* tiles, int K, const int* ipiv) {
+  const int p = blockIdx.y;
+  const int T = g.T[p];
+  const int J = K + 1 + blockIdx.x;
+  if (K >= T || J >= T) return;
+  const int c = threadIdx.x;
+  const int64_t base = g.tbase[p];
+  const int* piv = ipiv + g.fbase[p] * NB;
+  auto el = [&](int r) -> double* {
+    const int I = r >> 7;
+    return tiles + (base + (int64_t)I * g.W + (J - I + g.wl)) * TILE_ELEMS + (r & (NB - 1)) +
+           (int64_t)c * NB;
+  };
+  for (int j = K * NB; j < (K + 1) * NB; ++j) {
+    const int pr = piv[j];
+    if (pr != j) {
+      double* a = el(j);
+      double* b = el(pr);
+      const double t = *a;
+      *a = *b;
+      *b = t;
+    }
+  }
+}
+
+bool lu_piv_attrs_set = false;
+
+void launch_lu_panel_piv(Ctx* c, cudaStream_t s, const BandGeom& g, double* tiles, int K, int* ipiv,
+                         int* perm, int* status) {
+  const size_t smem = sizeof(int) * (size_t)(g.wl + 1) * NB;
+  if (!lu_piv_attrs_set) {
+    LRS_CUDA(cudaFuncSetAttribute(lu_panel_piv_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    LRS_CUDA(cudaFuncSetAttribute(lu_panel_piv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)(sizeof(int) * 200 * NB)));
+    LRS_CUDA(cudaFuncSetAttribute(diag_invert_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)(sizeof(double) * (TILE_ELEMS + 4 * NB))));
+    lu_piv_attrs_set = true;
+  }
+  if (g.wl + 1 > 200) throw LrsError(LRS_ERR_PARAMETER, "pivoting LU: lower band > 199 tiles");
+  {
+    ProfScope ps_(c, K_LU_DIAG, s);
+    lu_panel_piv_kernel<<<g.P * PIV_CL, PIV_THREADS, smem, s>>>(g, tiles, K, ipiv, perm, status);
+    LRS_LAUNCHED(c);
+  }
+  {
+    ProfScope ps_(c, K_LU_DIAG, s);
+    diag_invert_kernel<<<g.P, 512, sizeof(double) * (TILE_ELEMS + 4 * NB), s>>>(g, tiles, K);
+    LRS_LAUNCHED(c);
+  }
+  if (g.wu > 0) {
+    ProfScope ps_(c, K_LU_PANEL, s);
+    swap_trailing_kernel<<<dim3(g.wu, g.P), NB, 0, s>>>(g, tiles, K, ipiv);
+    LRS_LAUNCHED(c);
+  }
+}
+
+size_t piv_perm_ints(int64_t total_rowtiles) { return (size_t)total_rowtiles * (2 * PIV_MAXPERM + 1); }
+
+// ---------------------------------------------------------------------------------------
+// Solves with the interleaved interchanges (dgbtrs), step by step.
+// Forward L, step K:  x <- P_K x (rows of the panel);  x_K <- inv(L_KK) x_K  (piv_fwd_a),
+//                     x_I -= L_IK x_K, I = K+1 .. K+wl                      (piv_fwd_b)
+// Backward L^T, step K: x_K -= sum_I L_IK^T x_I; x_K <- inv(L_KK)^T x_K; x <- P_K^T x
+// x: global-row layout (partition offset off_p), nrhs columns with leading dimension ld.
+// ---------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(NB) piv_fwd_a_kernel(BandGeom g, const double* tiles, int K,
+                                                      const int* perm, double* x, int64_t ld,
+                                                      int nrhs, int p_only) {
+  const int p = p_only >= 0 ? p_only : blockIdx.x;
+  if (K >= g.T[p]) return;
+  __shared__ double xs[NB];
+  __shared__ int pl_dst[PIV_MAXPERM], pl_src[PIV_MAXPERM];
+  __shared__ double pv[PIV_MAXPERM];
+  const int tid = threadIdx.x;
+  const int64_t off = g.off[p], size = g.size[p];
+  const int* pl = perm + ((int64_t)g.fbase[p] + K) * (2 * PIV_MAXPERM + 1);
+  const int cnt = pl[0];
+  for (int e = tid; e < cnt; e += NB) pl_dst[e] = pl[1 + 2 * e], pl_src[e] = pl[2 + 2 * e];
+  const double* Lt = tiles + (g.tbase[p] + (int64_t)K * g.W + g.wl) * TILE_ELEMS;
+  const int64_t row = (int64_t)K * NB + tid;
+  __syncthreads();
+  for (int j = 0; j < nrhs; ++j) {
+    double* xj = x + off + (int64_t)j * ld;
+    for (int e = tid; e < cnt; e += NB) pv[e] = pl_src[e] < size ? xj[pl_src[e]] : 0.0;
+    __syncthreads();
+    for (int e = tid; e < cnt; e += NB)
+      if (pl_dst[e] < size) xj[pl_dst[e]] = pv[e];
+    __syncthreads();
+    xs[tid] = row < size ? xj[row] : 0.0;
+    __syncthreads();
+    double v = xs[tid];  // unit diagonal
+    for (int k = 0; k < tid; ++k) v = fma(Lt[tid + k * NB], xs[k], v);
+    if (row < size) xj[row] = v;
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(NB) piv_fwd_b_kernel(BandGeom g, const double* tiles, int K,
+                                                      double* x, int64_t ld, int nrhs,
+                                                      int p_only) {
+  const int p = p_only >= 0 ? p_only : blockIdx.y;
+  const int T = g.T[p];
+  const int I = K + 1 + blockIdx.x;
+  if (K >= T || I >= T) return;
+  __shared__ double xs[NB];
+  const int tid = threadIdx.x;
+  const int64_t off = g.off[p], size = g.size[p];
+  const double* L = tiles + (g.tbase[p] + (int64_t)I * g.W + (K - I + g.wl)) * TILE_ELEMS;
+  const int64_t row = (int64_t)I * NB + tid, rk = (int64_t)K * NB + tid;
+  for (int j = 0; j < nrhs; ++j) {
+    double* xj = x + off + (int64_t)j * ld;
+    xs[tid] = rk < size ? xj[rk] : 0.0;
+    __syncthreads();
+    double acc = 0.0;
+    for (int k = 0; k < NB; ++k) acc = fma(L[tid + k * NB], xs[k], acc);
+    if (row < size) xj[row] -= acc;
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(NB) piv_bwd_kernel(BandGeom g, const double* tiles, int K,
+                                                    const int* perm, double* x, int64_t ld,
+                                                    int nrhs, int p_only) {
+  const int p = p_only >= 0 ? p_only : blockIdx.x;
+  const int T = g.T[p];
+  if (K >= T) return;
+  __shared__ double xs[NB];
+  __shared__ int pl_dst[PIV_MAXPERM], pl_src[PIV_MAXPERM];
+  __shared__ double pv[PIV_MAXPERM];
+  const int tid = threadIdx.x;
+  const int64_t off = g.off[p], size = g.size[p];
+  const int Ilast = min(T - 1, K + g.wl);
+  const int* pl = perm + ((int64_t)g.fbase[p] + K) * (2 * PIV_MAXPERM + 1);
+  const int cnt = pl[0];
+  for (int e = tid; e < cnt; e += NB) pl_dst[e] = pl[1 + 2 * e], pl_src[e] = pl[2 + 2 * e];
+  const int64_t base = g.tbase[p];
+  const double* Lt = tiles + (base + (int64_t)K * g.W + g.wl) * TILE_ELEMS;
+  const int64_t rk = (int64_t)K * NB + tid;
+  __syncthreads();
+  for (int j = 0; j < nrhs; ++j) {
+    double* xj = x + off + (int64_t)j * ld;
+    // x_K[m] -= sum_I sum_r L_IK[r][m] x_I[r]
+    double v = rk < size ? xj[rk] : 0.0;
+    for (int I = K + 1; I <= Ilast; ++I) {
+      const double* L = tiles + (base + (int64_t)I * g.W + (K - I + g.wl)) * TILE_ELEMS;
+      const int64_t r0 = (int64_t)I * NB;
+      double acc = 0.0;
+      for (int r = 0; r < NB; ++r) {
+        const double xr = r0 + r < size ? xj[r0 + r] : 0.0;
+        acc = fma(L[r + tid * NB], xr, acc);
+      }
+      v -= acc;
+    }
+    xs[tid] = v;
+    __syncthreads();
+    // x_K <- inv(L_KK)^T x_K: v_m = x_m + sum_{i > m} invL[i][m] x_i
+    double u = xs[tid];
+    for (int i = tid + 1; i < NB; ++i) u = fma(Lt[i + tid * NB], xs[i], u);
+    if (rk < size) xj[rk] = u;
+    __syncthreads();
+    // x <- P_K^T x: new x[src] = old x[dst]
+    for (int e = tid; e < cnt; e += NB) pv[e] = pl_dst[e] < size ? xj[pl_dst[e]] : 0.0;
+    __syncthreads();
+    for (int e = tid; e < cnt; e += NB)
+      if (pl_src[e] < size) xj[pl_src[e]] = pv[e];
+    __syncthreads();
+  }
+}
+
+void launch_piv_lsolve(Ctx* c, const BandGeom& g, const double* tiles, const int* perm, int Tmax,
+                       bool transposed, double* x, int64_t ld, int nrhs, int p_only) {
+  if (nrhs == 0) return;
+  const int np = p_only >= 0 ? 1 : g.P;
+  ProfScope ps_(c, c->in_setup ? K_SPIKE_SOLVE : (transposed ? K_SOLVE_ADJ : K_SOLVE));
+  if (!transposed) {
+    for (int K = 0; K < Tmax; ++K) {
+      piv_fwd_a_kernel<<<np, NB, 0, c->stream>>>(g, tiles, K, perm, x, ld, nrhs, p_only);
+      LRS_LAUNCHED(c);
+      if (g.wl > 0) {
+        piv_fwd_b_kernel<<<dim3(g.wl, np), NB, 0, c->stream>>>(g, tiles, K, x, ld, nrhs, p_only);
+        LRS_LAUNCHED(c);
+      }
+    }
+  } else {
+    for (int K = Tmax - 1; K >= 0; --K) {
+      piv_bwd_kernel<<<np, NB, 0, c->stream>>>(g, tiles, K, perm, x, ld, nrhs, p_only);
+      LRS_LAUNCHED(c);
+    }
+  }
+}
+
+}  // namespace lrs

@@ -39,6 +39,9 @@ struct Fact {
   unsigned epoch = 0;
   DevBuf<int> status;
   DevBuf<unsigned long long> bad;
+  // partial pivoting (band_lu_piv.cu): the blocks were factored with row interchanges
+  bool pivoted = false;
+  DevBuf<int> ipiv, perm;
   // low-rank spikes: u as n x r (global rows, ld n); v^T, sigma in GLOBAL partition slots
   DevBuf<double> uT, uW, vtT, vtW, sT, sW;
   // interfaces with at least one local side (jobs in global interface order)

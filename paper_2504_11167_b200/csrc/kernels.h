@@ -60,6 +60,16 @@ void run_band_lu(Ctx* c, const BandGeom& g, void* tiles, int Tmax, int* status,
 bool lu_uses_pairs(const BandGeom& g, const LuKernels& L);
 // the real LU runs two-step (rank-256) bulk updates when the band spans >= 2 tiles
 bool lu_real_pairs(const BandGeom& g);
+// partial pivoting (band_lu_piv.cu): ipiv [total_rowtiles * 128] partition-local pivot
+// rows; perm [total_rowtiles * piv_perm_ints stride]: each step's composed permutation
+void launch_band_lu_piv(Ctx* c, const BandGeom& g, double* tiles, int Tmax, int* status,
+                        int* ipiv, int* perm);
+void launch_lu_panel_piv(Ctx* c, cudaStream_t s, const BandGeom& g, double* tiles, int K,
+                         int* ipiv, int* perm, int* status);
+size_t piv_perm_ints(int64_t total_rowtiles);
+// forward L (transposed = false) or backward L^T solve with the interleaved interchanges
+void launch_piv_lsolve(Ctx* c, const BandGeom& g, const double* tiles, const int* perm, int Tmax,
+                       bool transposed, double* x, int64_t ld, int nrhs, int p_only);
 void launch_extract_tiles_z(Ctx* c, const Mat* m, const BandGeom& g, zc* tiles, int64_t k,
                             int64_t row_lo, int64_t row_hi, unsigned long long* d_bad);
 

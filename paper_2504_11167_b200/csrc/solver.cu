@@ -160,6 +160,14 @@ void dstage_t(Fact* f, S* x, int64_t ld, int nrhs, bool adjoint, int p_only) {
     S* xc = x + (int64_t)c0 * ld;
     for (int half = 0; half < 2; ++half) {
       const int mode = adjoint ? 2 + half : half;
+      if constexpr (!IsC<S>::value) {
+        // with row interchanges the L sweeps interleave the permutations (dgbtrs)
+        if (f->pivoted && (mode == 0 || mode == 3)) {
+          launch_piv_lsolve(f->ctx, g, f->tiles.get(), f->perm.get(), f->Tmax, mode == 3, xc, ld,
+                            nr, p_only);
+          continue;
+        }
+      }
       if constexpr (IsC<S>::value)
         launch_band_solve_z(f->ctx, g, sp<zc>(f->tiles), mode, xc, ld, nr, f->flags.get(),
                             f->next_epoch(), f->ticket.get(), p_only, ntiles, f->total_rowtiles);
@@ -684,8 +692,6 @@ Fact* factorize(Ctx* c, Mat* m, const lrs_solver_cfg& cfg, const lrs_comm* comm)
     }
   }
   const int P = f->P;
-  f->wl = (int)((f->kl + NB - 1) / NB);
-  f->wu = (int)((f->ku + NB - 1) / NB);
   f->T.resize(P);
   f->tbase.resize(P);
   f->fbase.resize(P);
@@ -697,35 +703,40 @@ Fact* factorize(Ctx* c, Mat* m, const lrs_solver_cfg& cfg, const lrs_comm* comm)
     f->T[i] = (int)((f->size[i] + NB - 1) / NB);
     f->Tmax = std::max(f->Tmax, f->T[i]);
   }
-  // band width in tiles from the global block sizes, identical on every rank
-  f->wl = std::min(f->wl, std::max(0, Tmax_all - 1));
-  f->wu = std::min(f->wu, std::max(0, Tmax_all - 1));
-  f->W = f->wl + f->wu + 1;
-  int64_t tb = 0, fb = 0;
-  for (int i = 0; i < P; ++i) {
-    f->tbase[i] = tb;
-    f->fbase[i] = fb;
-    tb += (int64_t)f->T[i] * f->W;
-    fb += f->T[i];
-  }
-  f->total_tiles = tb;
-  f->total_rowtiles = fb;
   upload(c, f->d_off, f->off);
   upload(c, f->d_size, f->size);
-  upload(c, f->d_tbase, f->tbase);
-  upload(c, f->d_fbase, f->fbase);
   upload(c, f->d_T, f->T);
   upload(c, f->d_goff, f->goff);
   upload(c, f->d_rank_pl, f->rank_pl);
-  f->tiles.alloc((size_t)tb * TILE_ELEMS * w);
-  f->flags.alloc((size_t)fb * SOLVE_GROUPS);
-  f->ticket.alloc(1);
-  f->status.alloc(2 * P);
-  f->bad.alloc(1);
-  LRS_CUDA(cudaMemsetAsync(f->tiles.get(), 0, sizeof(double) * tb * TILE_ELEMS * w, c->stream));
-  LRS_CUDA(cudaMemsetAsync(f->flags.get(), 0, sizeof(unsigned) * fb * SOLVE_GROUPS, c->stream));
-  LRS_CUDA(cudaMemsetAsync(f->status.get(), 0x7f, sizeof(int) * 2 * P, c->stream));
-  LRS_CUDA(cudaMemsetAsync(f->bad.get(), 0xff, sizeof(unsigned long long), c->stream));
+  // tile storage for an upper band of ku_eff (ku, or ku + kl with row interchanges); band
+  // widths in tiles from the global block sizes, identical on every rank
+  auto setup_tiles = [&](int64_t ku_eff) {
+    f->wl = std::min((int)((f->kl + NB - 1) / NB), std::max(0, Tmax_all - 1));
+    f->wu = std::min((int)((ku_eff + NB - 1) / NB), std::max(0, Tmax_all - 1));
+    f->W = f->wl + f->wu + 1;
+    int64_t tb = 0, fb = 0;
+    for (int i = 0; i < P; ++i) {
+      f->tbase[i] = tb;
+      f->fbase[i] = fb;
+      tb += (int64_t)f->T[i] * f->W;
+      fb += f->T[i];
+    }
+    f->total_tiles = tb;
+    f->total_rowtiles = fb;
+    upload(c, f->d_tbase, f->tbase);
+    upload(c, f->d_fbase, f->fbase);
+    f->tiles.reset();
+    f->tiles.alloc((size_t)tb * TILE_ELEMS * w);
+    f->flags.alloc((size_t)fb * SOLVE_GROUPS);
+    f->ticket.alloc(1);
+    f->status.alloc(2 * P);
+    f->bad.alloc(1);
+    LRS_CUDA(cudaMemsetAsync(f->tiles.get(), 0, sizeof(double) * tb * TILE_ELEMS * w, c->stream));
+    LRS_CUDA(cudaMemsetAsync(f->flags.get(), 0, sizeof(unsigned) * fb * SOLVE_GROUPS, c->stream));
+    LRS_CUDA(cudaMemsetAsync(f->status.get(), 0x7f, sizeof(int) * 2 * P, c->stream));
+    LRS_CUDA(cudaMemsetAsync(f->bad.get(), 0xff, sizeof(unsigned long long), c->stream));
+  };
+  setup_tiles(f->ku);
   // deterministic reduction chunks, partition aligned
   {
     const int64_t CH = 2048;
@@ -773,7 +784,7 @@ Fact* factorize(Ctx* c, Mat* m, const lrs_solver_cfg& cfg, const lrs_comm* comm)
   cudaEvent_t evs[4] = {e0, e1, e2, e3};
   EvGuard eg{evs};
   LRS_CUDA(cudaEventRecord(e0, c->stream));
-  const BandGeom g = f->geom();
+  BandGeom g = f->geom();
   if (cplx)
     launch_extract_tiles_z(c, m, g, sp<zc>(f->tiles), f->k, f->row_lo, f->row_hi, f->bad.get());
   else
@@ -820,39 +831,54 @@ Fact* factorize(Ctx* c, Mat* m, const lrs_solver_cfg& cfg, const lrs_comm* comm)
   }
   if (cplx) launch_band_lu_z(c, g, sp<zc>(f->tiles), f->Tmax, f->status.get());
   else launch_band_lu(c, g, f->tiles.get(), f->Tmax, f->status.get());
-  LRS_CUDA(cudaEventRecord(e1, c->stream));
-  {
+  // first (global block, column) needing a row interchange / holding an exact zero pivot,
+  // agreed over all ranks
+  auto first_problem = [&](int which) {
     std::vector<int> st(2 * P);
     download(c, st.data(), f->status.get(), st.size());
-    // (global block index, code: 1 zero pivot / 2 interchange, column) -- first in order
-    double blk = -1, code = 0, col = 0;
-    for (int i = 0; i < P && blk < 0; ++i) {
-      if (st[2 * i + 1] != 0x7f7f7f7f) {
+    double blk = -1, col = 0;
+    for (int i = 0; i < P && blk < 0; ++i)
+      if (st[2 * i + which] != 0x7f7f7f7f) {
         blk = f->p0 + i;
-        code = 1;
-        col = st[2 * i + 1];
-      } else if (st[2 * i] != 0x7f7f7f7f) {
-        blk = f->p0 + i;
-        code = 2;
-        col = st[2 * i];
+        col = st[2 * i + which];
       }
-    }
-    const std::vector<double> all = allgather_host(f.get(), {blk, code, col});
-    for (size_t q = 0; q < all.size(); q += 3) {
-      if (all[q] < 0) continue;
-      const int b = (int)all[q];
-      const int64_t cc = (int64_t)all[q + 2];
-      if (all[q + 1] == 1) {
-        LrsError e(LRS_ERR_SINGULAR_BLOCK, "exact zero pivot in column " + std::to_string(cc) +
-                                               " of block " + std::to_string(b));
-        e.column = cc;
-        throw e;
+    std::pair<int, int64_t> out{-1, 0};
+    const std::vector<double> all = allgather_host(f.get(), {blk, col});
+    for (size_t q = 0; q < all.size(); q += 2)
+      if (all[q] >= 0) {
+        out = {(int)all[q], (int64_t)all[q + 1]};
+        break;
       }
+    return out;
+  };
+  if (first_problem(0).first >= 0) {
+    // dgbtrf would interchange rows: redo the blocks with partial pivoting (upper band
+    // widened by kl for the fill of the interchanges)
+    if (cplx) {
+      const auto pr = first_problem(0);
       LrsError e(LRS_ERR_NOT_IMPLEMENTED,
-                 "block " + std::to_string(b) + " needs a row interchange at column " +
-                     std::to_string(cc) +
-                     " (partial pivoting); the interchange path is not implemented on the GPU yet");
-      e.column = cc;
+                 "block " + std::to_string(pr.first) + " needs a row interchange at column " +
+                     std::to_string(pr.second) +
+                     " (partial pivoting); the complex128 interchange path is not implemented");
+      e.column = pr.second;
+      throw e;
+    }
+    setup_tiles(f->ku + f->kl);
+    g = f->geom();
+    launch_extract_tiles(c, m, g, f->tiles.get(), f->k, f->row_lo, f->row_hi, f->bad.get());
+    f->pivoted = true;
+    f->ipiv.alloc((size_t)f->total_rowtiles * NB);
+    f->perm.alloc(piv_perm_ints(f->total_rowtiles));
+    launch_band_lu_piv(c, g, f->tiles.get(), f->Tmax, f->status.get(), f->ipiv.get(),
+                       f->perm.get());
+  }
+  LRS_CUDA(cudaEventRecord(e1, c->stream));
+  {
+    const auto pr = first_problem(1);
+    if (pr.first >= 0) {
+      LrsError e(LRS_ERR_SINGULAR_BLOCK, "exact zero pivot in column " + std::to_string(pr.second) +
+                                             " of block " + std::to_string(pr.first));
+      e.column = pr.second;
       throw e;
     }
   }
@@ -907,7 +933,8 @@ Fact* factorize(Ctx* c, Mat* m, const lrs_solver_cfg& cfg, const lrs_comm* comm)
   in.factor_bytes = f->total_tiles * TILE_ELEMS * (int64_t)sizeof(double) * w;
   in.rank_collapsed = f->rank_collapsed;
   in.variant = f->variant;
-  in.lu_pairs = cplx ? 0 : (lu_real_pairs(g) ? 1 : 0);
+  in.lu_pairs = (cplx || f->pivoted) ? 0 : (lu_real_pairs(g) ? 1 : 0);
+  in.pivoted = f->pivoted ? 1 : 0;
   in.t_lu = elapsed_ms(e0, e1) * 1e-3;
   in.t_spikes = elapsed_ms(e1, e2) * 1e-3;
   in.t_precond = 0.0;
