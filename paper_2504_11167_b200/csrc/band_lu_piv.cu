@@ -29,6 +29,7 @@ namespace cg = cooperative_groups;
 constexpr int PIV_CL = 16;       // CTAs per partition (non-portable cluster size)
 constexpr int PIV_THREADS = 512;
 constexpr int PIV_MAXPERM = 2 * NB;  // rows moved by one step's 128 interchanges
+constexpr int PIV_MAXROWS = 1664;    // panel rows per CTA: (wl + 1) * 128 / 16, wl <= 207
 
 __device__ __forceinline__ bool piv_better(double v, int i, double bv, int bi) {
   return v > bv || (v == bv && i < bi);
@@ -48,6 +49,7 @@ __global__ void __cluster_dims__(PIV_CL, 1, 1) __launch_bounds__(PIV_THREADS, 1)
   __shared__ double slot_v[2];
   __shared__ int slot_i[2];
   __shared__ double urow[NB];
+  __shared__ double lcol[PIV_MAXROWS];
   __shared__ int s_piv;
   __shared__ double s_pv;
   const int64_t base = g.tbase[p];
@@ -122,17 +124,25 @@ __global__ void __cluster_dims__(PIV_CL, 1, 1) __launch_bounds__(PIV_THREADS, 1)
     if (tid < NB) urow[tid] = tid > c ? *el(j, tid) : 0.0;
     __syncthreads();
     const double pv = *el(j, c);
-    if (pv != 0.0) {  // dgbtf2 skips scaling / update on an exact zero pivot
+    const int ra = max(j + 1, slo), nr = max(0, shi - ra);
+    if (pv != 0.0 && nr > 0) {  // dgbtf2 skips scaling / update on an exact zero pivot
       const double inv = 1.0 / pv;
-      for (int r = max(j + 1, slo) + tid; r < shi; r += PIV_THREADS) {
-        double* lr = el(r, c);
+      for (int e = tid; e < nr; e += PIV_THREADS) {
+        double* lr = el(ra + e, c);
         const double l = *lr * inv;
         *lr = l;
-        if (l != 0.0)
-          for (int c2 = c + 1; c2 < NB; ++c2) {
-            double* a = el(r, c2);
-            *a = fma(-l, urow[c2], *a);
-          }
+        lcol[e] = l;
+      }
+      __syncthreads();
+      // (row, column) pairs over all threads: consecutive threads take consecutive rows
+      const int ncols = NB - 1 - c, tot = nr * ncols;
+      for (int e = tid; e < tot; e += PIV_THREADS) {
+        const int rr = e % nr, c2 = c + 1 + e / nr;
+        const double l = lcol[rr];
+        if (l != 0.0) {
+          double* a = el(ra + rr, c2);
+          *a = fma(-l, urow[c2], *a);
+        }
       }
     }
     __syncthreads();
@@ -177,29 +187,32 @@ __global__ void __launch_bounds__(512, 1) diag_invert_kernel(BandGeom g, double*
   for (int e = threadIdx.x; e < TILE_ELEMS; e += 512) gt[e] = A[e];
 }
 
-// the step's interchanges (in order) on tile columns K+1 .. K+wu: one thread per column
-__global__ void swap_trailing_kernel(BandGeom g, double* tiles, int K, const int* ipiv) {
+// the step's interchanges on tile columns K+1 .. K+wu, applied as the composed
+// permutation (new row dst = old row src): gather all moved rows, then scatter.
+__global__ void __launch_bounds__(NB) swap_trailing_kernel(BandGeom g, double* tiles, int K,
+                                                           const int* perm) {
   const int p = blockIdx.y;
   const int T = g.T[p];
   const int J = K + 1 + blockIdx.x;
   if (K >= T || J >= T) return;
-  const int c = threadIdx.x;
+  __shared__ double vals[PIV_MAXPERM][17];
+  __shared__ int dst[PIV_MAXPERM], src[PIV_MAXPERM];
+  const int tid = threadIdx.x;
   const int64_t base = g.tbase[p];
-  const int* piv = ipiv + g.fbase[p] * NB;
-  auto el = [&](int r) -> double* {
+  const int* pl = perm + ((int64_t)g.fbase[p] + K) * (2 * PIV_MAXPERM + 1);
+  const int cnt = pl[0];
+  for (int e = tid; e < cnt; e += NB) dst[e] = pl[1 + 2 * e], src[e] = pl[2 + 2 * e];
+  __syncthreads();
+  auto el = [&](int r, int col) -> double* {
     const int I = r >> 7;
     return tiles + (base + (int64_t)I * g.W + (J - I + g.wl)) * TILE_ELEMS + (r & (NB - 1)) +
-           (int64_t)c * NB;
+           (int64_t)col * NB;
   };
-  for (int j = K * NB; j < (K + 1) * NB; ++j) {
-    const int pr = piv[j];
-    if (pr != j) {
-      double* a = el(j);
-      double* b = el(pr);
-      const double t = *a;
-      *a = *b;
-      *b = t;
-    }
+  for (int c0 = 0; c0 < NB; c0 += 16) {  // 16 columns at a time
+    for (int e = tid; e < cnt * 16; e += NB) vals[e >> 4][e & 15] = *el(src[e >> 4], c0 + (e & 15));
+    __syncthreads();
+    for (int e = tid; e < cnt * 16; e += NB) *el(dst[e >> 4], c0 + (e & 15)) = vals[e >> 4][e & 15];
+    __syncthreads();
   }
 }
 
@@ -216,7 +229,8 @@ void launch_lu_panel_piv(Ctx* c, cudaStream_t s, const BandGeom& g, double* tile
                                   (int)(sizeof(double) * (TILE_ELEMS + 4 * NB))));
     lu_piv_attrs_set = true;
   }
-  if (g.wl + 1 > 200) throw LrsError(LRS_ERR_PARAMETER, "pivoting LU: lower band > 199 tiles");
+  if ((g.wl + 1) * NB > PIV_CL * PIV_MAXROWS || g.wl + 1 > 200)
+    throw LrsError(LRS_ERR_PARAMETER, "pivoting LU: lower band > 199 tiles");
   {
     ProfScope ps_(c, K_LU_DIAG, s);
     lu_panel_piv_kernel<<<g.P * PIV_CL, PIV_THREADS, smem, s>>>(g, tiles, K, ipiv, perm, status);
@@ -229,7 +243,7 @@ void launch_lu_panel_piv(Ctx* c, cudaStream_t s, const BandGeom& g, double* tile
   }
   if (g.wu > 0) {
     ProfScope ps_(c, K_LU_PANEL, s);
-    swap_trailing_kernel<<<dim3(g.wu, g.P), NB, 0, s>>>(g, tiles, K, ipiv);
+    swap_trailing_kernel<<<dim3(g.wu, g.P), NB, 0, s>>>(g, tiles, K, perm);
     LRS_LAUNCHED(c);
   }
 }
@@ -243,9 +257,13 @@ size_t piv_perm_ints(int64_t total_rowtiles) { return (size_t)total_rowtiles * (
 // Backward L^T, step K: x_K -= sum_I L_IK^T x_I; x_K <- inv(L_KK)^T x_K; x <- P_K^T x
 // x: global-row layout (partition offset off_p), nrhs columns with leading dimension ld.
 // ---------------------------------------------------------------------------------------
+constexpr int PIV_COLS = 4;  // right-hand-side columns per CTA of the solve kernels
+
 __global__ void __launch_bounds__(NB) piv_fwd_a_kernel(BandGeom g, const double* tiles, int K,
                                                       const int* perm, double* x, int64_t ld,
                                                       int nrhs, int p_only) {
+  x += (int64_t)blockIdx.z * PIV_COLS * ld;
+  nrhs = min(PIV_COLS, nrhs - (int)blockIdx.z * PIV_COLS);
   const int p = p_only >= 0 ? p_only : blockIdx.x;
   if (K >= g.T[p]) return;
   __shared__ double xs[NB];
@@ -278,6 +296,8 @@ __global__ void __launch_bounds__(NB) piv_fwd_a_kernel(BandGeom g, const double*
 __global__ void __launch_bounds__(NB) piv_fwd_b_kernel(BandGeom g, const double* tiles, int K,
                                                       double* x, int64_t ld, int nrhs,
                                                       int p_only) {
+  x += (int64_t)blockIdx.z * PIV_COLS * ld;
+  nrhs = min(PIV_COLS, nrhs - (int)blockIdx.z * PIV_COLS);
   const int p = p_only >= 0 ? p_only : blockIdx.y;
   const int T = g.T[p];
   const int I = K + 1 + blockIdx.x;
@@ -301,6 +321,8 @@ __global__ void __launch_bounds__(NB) piv_fwd_b_kernel(BandGeom g, const double*
 __global__ void __launch_bounds__(NB) piv_bwd_kernel(BandGeom g, const double* tiles, int K,
                                                     const int* perm, double* x, int64_t ld,
                                                     int nrhs, int p_only) {
+  x += (int64_t)blockIdx.z * PIV_COLS * ld;
+  nrhs = min(PIV_COLS, nrhs - (int)blockIdx.z * PIV_COLS);
   const int p = p_only >= 0 ? p_only : blockIdx.x;
   const int T = g.T[p];
   if (K >= T) return;
@@ -351,19 +373,23 @@ void launch_piv_lsolve(Ctx* c, const BandGeom& g, const double* tiles, const int
                        bool transposed, double* x, int64_t ld, int nrhs, int p_only) {
   if (nrhs == 0) return;
   const int np = p_only >= 0 ? 1 : g.P;
+  const unsigned nz = (unsigned)((nrhs + PIV_COLS - 1) / PIV_COLS);
   ProfScope ps_(c, c->in_setup ? K_SPIKE_SOLVE : (transposed ? K_SOLVE_ADJ : K_SOLVE));
   if (!transposed) {
     for (int K = 0; K < Tmax; ++K) {
-      piv_fwd_a_kernel<<<np, NB, 0, c->stream>>>(g, tiles, K, perm, x, ld, nrhs, p_only);
+      piv_fwd_a_kernel<<<dim3(np, 1, nz), NB, 0, c->stream>>>(g, tiles, K, perm, x, ld, nrhs,
+                                                              p_only);
       LRS_LAUNCHED(c);
       if (g.wl > 0) {
-        piv_fwd_b_kernel<<<dim3(g.wl, np), NB, 0, c->stream>>>(g, tiles, K, x, ld, nrhs, p_only);
+        piv_fwd_b_kernel<<<dim3(g.wl, np, nz), NB, 0, c->stream>>>(g, tiles, K, x, ld, nrhs,
+                                                                   p_only);
         LRS_LAUNCHED(c);
       }
     }
   } else {
     for (int K = Tmax - 1; K >= 0; --K) {
-      piv_bwd_kernel<<<np, NB, 0, c->stream>>>(g, tiles, K, perm, x, ld, nrhs, p_only);
+      piv_bwd_kernel<<<dim3(np, 1, nz), NB, 0, c->stream>>>(g, tiles, K, perm, x, ld, nrhs,
+                                                            p_only);
       LRS_LAUNCHED(c);
     }
   }
