@@ -62,6 +62,8 @@ struct SolverConfig {
   double otf_tol = 1e-8;
   index_t otf_max_iters = 500;
   int otf_escalations = 4;
+  // FP32 off-diagonal factor tiles in the preconditioner applies
+  bool factor_fp32 = false;
 };
 
 /// SPEC.md:466-469.

@@ -101,6 +101,10 @@ typedef struct lrs_solver_cfg {
   double otf_tol;
   int64_t otf_max_iters;
   int32_t otf_escalations;
+  /* Mixed precision (paper section 4.3): the preconditioner applies read the
+     off-diagonal factor tiles in FP32 (the diagonal-tile inverses and every vector stay
+     FP64; the spike construction uses the FP64 factors).  0 = FP64 throughout. */
+  int32_t factor_fp32;
 } lrs_solver_cfg;
 
 /* IterConfig, SPEC.md:411-414 (+ method, GMRES restart). */

@@ -507,6 +507,7 @@ class SolverConfig:
     otf_tol: float = 1e-8
     otf_max_iters: int = 500
     otf_escalations: int = 4
+    factor_fp32: bool = False  # FP32 off-diagonal factor tiles in the applies
 
 
 @dataclass
@@ -522,6 +523,10 @@ class SpikeFactorization:
     rank_collapsed: bool = False
     inner_iterations: float = 0.0  # LR-SPIKE-I: inner half-iterations summed over applies
     inner_solves: int = 0
+    factors32: list | None = None  # the applies' factors with FP32 off-diagonal tiles
+
+    def apply_factors(self):
+        return self.factors32 if self.factors32 is not None else self.factors
 
 
 def factorize(A: sp.csr_matrix, cfg: SolverConfig) -> SpikeFactorization:
@@ -546,7 +551,27 @@ def factorize(A: sp.csr_matrix, cfg: SolverConfig) -> SpikeFactorization:
             if attempt == 1 or n_svd // 2 < 1:
                 raise
             n_svd //= 2
-    return SpikeFactorization(blocks, factors, spT, spW, trunc, cfg, n_svd, rank_collapsed=coll)
+    F = SpikeFactorization(blocks, factors, spT, spW, trunc, cfg, n_svd, rank_collapsed=coll)
+    if cfg.factor_fp32:
+        F.factors32 = [round_offdiag_tiles(fo) for fo in factors]
+    return F
+
+
+TILE = 128  # the GPU's factor tile (csrc/lrs_internal.h NB)
+
+
+def round_offdiag_tiles(F: BlockFactor) -> BlockFactor:
+    """The mixed-precision apply's factors (the paper applies single-precision
+    preconditioners, section 4.3): L / U entries (i, j) outside the 128 x 128 diagonal tiles
+    rounded to FP32 (the GPU keeps those tiles in FP32 and the diagonal-tile inverses in
+    FP64).  Band storage: ab[kl + ku + i - j, j] holds entry (i, j)."""
+    ab = F.ab.copy()
+    kv = F.kl + F.ku
+    rows, cols = np.indices(ab.shape)
+    i = rows - kv + cols
+    mask = (rows >= F.kl) & (i >= 0) & (i < F.n) & ((i // TILE) != (cols // TILE))
+    ab[mask] = ab[mask].astype(np.float32).astype(ab.dtype)
+    return BlockFactor(F.n, F.kl, F.ku, ab, F.ipiv, F.dtype)
 
 
 def _build_spikes(blocks, factors, cfg, n_svd, k):
@@ -570,7 +595,7 @@ def _split(F: SpikeFactorization, f: np.ndarray):
 def apply_block_jacobi(F: SpikeFactorization, f: np.ndarray) -> np.ndarray:
     """D^-1 f, no communication."""
     f2 = f.reshape(f.shape[0], -1)
-    y = np.concatenate([solve_block(Fi, fi) for Fi, fi in zip(F.factors, _split(F, f2))])
+    y = np.concatenate([solve_block(Fi, fi) for Fi, fi in zip(F.apply_factors(), _split(F, f2))])
     return y.reshape(f.shape)
 
 
@@ -581,7 +606,7 @@ def apply_precond_T(F: SpikeFactorization, f: np.ndarray) -> np.ndarray:
         return apply_block_jacobi(F, f)
     f2 = f.reshape(f.shape[0], -1)
     k = F.blocks.layout.k
-    ys = [solve_block(Fi, fi) for Fi, fi in zip(F.factors, _split(F, f2))]
+    ys = [solve_block(Fi, fi) for Fi, fi in zip(F.apply_factors(), _split(F, f2))]
     top = [y[:k] for y in ys]
     bot = [y[-k:] for y in ys]
     xt, xb = apply_truncated_precond(F.trunc, top, bot, F.ledger)
@@ -642,7 +667,7 @@ def _coupled_solve(F: SpikeFactorization, xt: list, xb: list, nr: int):
             rhs[:k] += np.asarray(F.blocks.C[i] @ xb[i - 1])
         if i < p - 1:
             rhs[n_i - k:] += np.asarray(F.blocks.B[i] @ xt[i + 1])
-        zs.append(solve_block(F.factors[i], rhs))
+        zs.append(solve_block(F.apply_factors()[i], rhs))
     return zs
 
 
@@ -695,7 +720,7 @@ def apply_precond_I(F: SpikeFactorization, f: np.ndarray) -> np.ndarray:
     f2 = f.reshape(f.shape[0], -1)
     lay = F.blocks.layout
     k, p = lay.k, lay.p
-    ys = [solve_block(Fi, fi) for Fi, fi in zip(F.factors, _split(F, f2))]
+    ys = [solve_block(Fi, fi) for Fi, fi in zip(F.apply_factors(), _split(F, f2))]
     g = _pack([y[:k] for y in ys], [y[-k:] for y in ys])
     # the inner solve runs on the column-normalised reduced right-hand side (and scales
     # back): the reduced system is linear, and the absolute breakdown threshold then
@@ -730,7 +755,7 @@ def solve_otf(A: sp.csr_matrix, F: SpikeFactorization, f: np.ndarray, it: "IterC
     lay = F.blocks.layout
     k, p = lay.k, lay.p
     nr = f2.shape[1]
-    ys = [solve_block(Fi, fi) for Fi, fi in zip(F.factors, _split(F, f2))]
+    ys = [solve_block(Fi, fi) for Fi, fi in zip(F.apply_factors(), _split(F, f2))]
     g = _pack([y[:k] for y in ys], [y[-k:] for y in ys])
     rep = SolveReport()
     rep.precond_applications = 1  # the D-stage

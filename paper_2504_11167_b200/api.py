@@ -45,7 +45,8 @@ vp = ctypes.c_void_p
 class SolverCfgC(ctypes.Structure):
     _fields_ = [("variant", i32), ("passes", i32), ("p", i64), ("k", i64), ("n_svd", i64),
                 ("oversample", i64), ("seed", u64), ("inner_tol", f64), ("inner_max_iters", i64),
-                ("otf_tol", f64), ("otf_max_iters", i64), ("otf_escalations", i32)]
+                ("otf_tol", f64), ("otf_max_iters", i64), ("otf_escalations", i32),
+                ("factor_fp32", i32)]
 
 
 class IterCfgC(ctypes.Structure):
@@ -417,6 +418,7 @@ class SolverConfig:
     otf_tol: float = 1e-8
     otf_max_iters: int = 500
     otf_escalations: int = 4
+    factor_fp32: bool = False  # FP32 off-diagonal factor tiles in the applies
 
     def c(self):
         if self.variant not in _VARIANTS:
@@ -424,7 +426,7 @@ class SolverConfig:
         return SolverCfgC(_VARIANTS[self.variant], self.passes, self.p, self.k or 0, self.n_svd,
                           -1 if self.oversample is None else self.oversample, self.seed,
                           self.inner_tol, self.inner_max_iters, self.otf_tol, self.otf_max_iters,
-                          self.otf_escalations)
+                          self.otf_escalations, 1 if self.factor_fp32 else 0)
 
 
 @dataclass

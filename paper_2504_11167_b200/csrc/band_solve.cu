@@ -58,7 +58,7 @@ template <int MODE, int NR>
 __global__ void __launch_bounds__(SOLVE_THREADS, 1)
     band_solve_kernel(BandGeom g, const double* __restrict__ tiles, double* x, int64_t ld,
                       int nrhs, unsigned* flags, unsigned epoch, int* ticket, int p_only,
-                      int ngroups, int64_t flag_stride) {
+                      int ngroups, int64_t flag_stride, const float* __restrict__ t32) {
   constexpr int STAGES = SolveCfg<NR>::STAGES;
   constexpr int XLD = SolveCfg<NR>::XLD;
   constexpr bool FWD = (MODE == 0 || MODE == 2);
@@ -106,9 +106,17 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1)
     return tiles + (base + (int64_t)s * W + (t - s + wl)) * TILE_ELEMS;
   };
   const int Q = (ndeps + 1) * NCH;
-  // producer: one 32 KB bulk copy per chunk (32 contiguous tile columns)
+  // producer: one 32 KB bulk copy per chunk (32 contiguous tile columns); with FP32
+  // off-diagonal factors (t32) those chunks are 16 KB
   auto issue = [&](int q, int st) {
-    const double* src = tile_ptr(q / NCH) + (size_t)(q % NCH) * CH_COLS * NB;
+    const int d = q / NCH;
+    if (t32 && d != ndeps) {
+      const float* src = t32 + (tile_ptr(d) - tiles) + (size_t)(q % NCH) * CH_COLS * NB;
+      mbar_expect_tx(&bars[st], CH_COLS * NB * sizeof(float));
+      bulk_g2s(ring + (size_t)st * CH_SM, src, CH_COLS * NB * sizeof(float), &bars[st]);
+      return;
+    }
+    const double* src = tile_ptr(d) + (size_t)(q % NCH) * CH_COLS * NB;
     mbar_expect_tx(&bars[st], CH_COLS * NB * sizeof(double));
     bulk_g2s(ring + (size_t)st * CH_SM, src, CH_COLS * NB * sizeof(double), &bars[st]);
   };
@@ -205,8 +213,14 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1)
     }
     mbar_wait(&bars[st], (unsigned)((q / STAGES) & 1));
     const double* ch = ring + (size_t)st * CH_SM;
+    const float* chf = reinterpret_cast<const float*>(ch);
+    const bool f32 = t32 != nullptr && !diag;
     const int cbase = sub * CH_COLS;
-    if (!TRANS && !MMA) {
+    if (!TRANS && !MMA && f32) {
+#pragma unroll 4
+      for (int cc = hh * 16; cc < hh * 16 + 16; ++cc)
+        acc1 = fma(-(double)chf[cc * NB + row], xs[cbase + cc], acc1);
+    } else if (!TRANS && !MMA) {
       // out[row] (+|-)= sum_c Tile[row][c] xs[c], half the chunk columns per thread
 #pragma unroll 4
       for (int cc = hh * 16; cc < hh * 16 + 16; ++cc) {
@@ -225,7 +239,7 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1)
 #pragma unroll
         for (int mi = 0; mi < 2; ++mi) {
           const int m = 16 * w + 8 * mi + gq;
-          double v = ch[k * CLD + m];
+          double v = f32 ? (double)chf[k * NB + m] : ch[k * CLD + m];
           if (diag) v = (MODE == 0) ? (m > kg ? v : 0.0) : (m <= kg ? v : 0.0);
           else v = -v;
           a[mi] = v;
@@ -343,7 +357,7 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1)
 template <int MODE, int NR>
 static void launch_mode(Ctx* c, const BandGeom& g, const double* tiles, double* x, int64_t ld,
                         int nrhs, unsigned* flags, unsigned epoch, int* ticket, int p_only,
-                        int ntiles, int64_t flag_stride) {
+                        int ntiles, int64_t flag_stride, const float* t32) {
   const int ngroups = (nrhs + NR - 1) / NR;
   static bool attr = false;
   const size_t smem = solve_smem_bytes<NR>();
@@ -354,37 +368,52 @@ static void launch_mode(Ctx* c, const BandGeom& g, const double* tiles, double* 
   }
   ProfScope ps_(c, c->in_setup ? K_SPIKE_SOLVE : (MODE >= 2 ? K_SOLVE_ADJ : K_SOLVE));
   band_solve_kernel<MODE, NR><<<ntiles * ngroups, SOLVE_THREADS, smem, c->stream>>>(
-      g, tiles, x, ld, nrhs, flags, epoch, ticket, p_only, ngroups, flag_stride);
+      g, tiles, x, ld, nrhs, flags, epoch, ticket, p_only, ngroups, flag_stride,
+      MODE <= 1 ? t32 : nullptr);
   LRS_LAUNCHED(c);
 }
 
 template <int MODE>
 static void launch_nr(Ctx* c, const BandGeom& g, const double* tiles, double* x, int64_t ld,
                       int nrhs, unsigned* flags, unsigned epoch, int* ticket, int p_only,
-                      int ntiles, int64_t fs) {
+                      int ntiles, int64_t fs, const float* t32) {
   // every width runs the same DMMA code (one n8 tile for <= 8 columns, 16-column groups
   // beyond 16), so each column's arithmetic is independent of the batch: multi-column ==
   // column-by-column bit-exactly
   if (nrhs <= 1 && c->solve_fma1)
-    launch_mode<MODE, 1>(c, g, tiles, x, ld, nrhs, flags, epoch, ticket, p_only, ntiles, fs);
+    launch_mode<MODE, 1>(c, g, tiles, x, ld, nrhs, flags, epoch, ticket, p_only, ntiles, fs, t32);
   else if (nrhs <= 8)
-    launch_mode<MODE, 8>(c, g, tiles, x, ld, nrhs, flags, epoch, ticket, p_only, ntiles, fs);
+    launch_mode<MODE, 8>(c, g, tiles, x, ld, nrhs, flags, epoch, ticket, p_only, ntiles, fs, t32);
   else
-    launch_mode<MODE, 16>(c, g, tiles, x, ld, nrhs, flags, epoch, ticket, p_only, ntiles, fs);
+    launch_mode<MODE, 16>(c, g, tiles, x, ld, nrhs, flags, epoch, ticket, p_only, ntiles, fs, t32);
 }
 
 void launch_band_solve(Ctx* c, const BandGeom& g, const double* tiles, int mode, double* x,
                        int64_t ld, int nrhs, unsigned* flags, unsigned epoch, int* ticket,
-                       int p_only, int ntiles, int64_t fs) {
+                       int p_only, int ntiles, int64_t fs, const float* t32) {
   if (ntiles == 0 || nrhs == 0) return;
   if (nrhs > SOLVE_MAX_RHS) throw LrsError(LRS_ERR_PARAMETER, "band solve batch > 48 columns");
   LRS_CUDA(cudaMemsetAsync(ticket, 0, sizeof(int), c->stream));
   switch (mode) {
-    case 0: launch_nr<0>(c, g, tiles, x, ld, nrhs, flags, epoch, ticket, p_only, ntiles, fs); break;
-    case 1: launch_nr<1>(c, g, tiles, x, ld, nrhs, flags, epoch, ticket, p_only, ntiles, fs); break;
-    case 2: launch_nr<2>(c, g, tiles, x, ld, nrhs, flags, epoch, ticket, p_only, ntiles, fs); break;
-    default: launch_nr<3>(c, g, tiles, x, ld, nrhs, flags, epoch, ticket, p_only, ntiles, fs); break;
+    case 0: launch_nr<0>(c, g, tiles, x, ld, nrhs, flags, epoch, ticket, p_only, ntiles, fs, t32); break;
+    case 1: launch_nr<1>(c, g, tiles, x, ld, nrhs, flags, epoch, ticket, p_only, ntiles, fs, t32); break;
+    case 2: launch_nr<2>(c, g, tiles, x, ld, nrhs, flags, epoch, ticket, p_only, ntiles, fs, t32); break;
+    default: launch_nr<3>(c, g, tiles, x, ld, nrhs, flags, epoch, ticket, p_only, ntiles, fs, t32); break;
   }
+}
+
+__global__ void tiles_to_fp32_kernel(const double* __restrict__ t, float* __restrict__ t32,
+                                     int64_t n) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x)
+    t32[e] = (float)t[e];
+}
+
+void launch_tiles_to_fp32(Ctx* c, const double* tiles, float* t32, int64_t count) {
+  if (count == 0) return;
+  ProfScope ps_(c, K_SETUP);
+  tiles_to_fp32_kernel<<<c->num_sms * 8, 256, 0, c->stream>>>(tiles, t32, count);
+  LRS_LAUNCHED(c);
 }
 
 }  // namespace lrs

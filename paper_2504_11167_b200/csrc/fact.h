@@ -42,6 +42,9 @@ struct Fact {
   // partial pivoting (band_lu_piv.cu): the blocks were factored with row interchanges
   bool pivoted = false;
   DevBuf<int> ipiv, perm;
+  // mixed precision: FP32 copy of the tiles, read for the off-diagonal tiles of the applies
+  bool fp32 = false;
+  DevBuf<float> tiles32;
   // low-rank spikes: u as n x r (global rows, ld n); v^T, sigma in GLOBAL partition slots
   DevBuf<double> uT, uW, vtT, vtW, sT, sW;
   // interfaces with at least one local side (jobs in global interface order)

@@ -173,7 +173,8 @@ void dstage_t(Fact* f, S* x, int64_t ld, int nrhs, bool adjoint, int p_only) {
                             f->next_epoch(), f->ticket.get(), p_only, ntiles, f->total_rowtiles);
       else
         launch_band_solve(f->ctx, g, f->tiles.get(), mode, xc, ld, nr, f->flags.get(),
-                          f->next_epoch(), f->ticket.get(), p_only, ntiles, f->total_rowtiles);
+                          f->next_epoch(), f->ticket.get(), p_only, ntiles, f->total_rowtiles,
+                          (f->fp32 && !f->ctx->in_setup) ? f->tiles32.get() : nullptr);
     }
   }
 }
@@ -873,6 +874,14 @@ Fact* factorize(Ctx* c, Mat* m, const lrs_solver_cfg& cfg, const lrs_comm* comm)
                        f->perm.get());
   }
   LRS_CUDA(cudaEventRecord(e1, c->stream));
+  if (cfg.factor_fp32) {
+    if (cplx || f->pivoted)
+      throw LrsError(LRS_ERR_NOT_IMPLEMENTED,
+                     "FP32 factors: real blocks without row interchanges only");
+    f->fp32 = true;
+    f->tiles32.alloc((size_t)f->total_tiles * TILE_ELEMS);
+    launch_tiles_to_fp32(c, f->tiles.get(), f->tiles32.get(), f->total_tiles * TILE_ELEMS);
+  }
   {
     const auto pr = first_problem(1);
     if (pr.first >= 0) {
@@ -930,7 +939,8 @@ Fact* factorize(Ctx* c, Mat* m, const lrs_solver_cfg& cfg, const lrs_comm* comm)
   in.nb = NB;
   in.wl = f->wl;
   in.wu = f->wu;
-  in.factor_bytes = f->total_tiles * TILE_ELEMS * (int64_t)sizeof(double) * w;
+  in.factor_bytes = f->total_tiles * TILE_ELEMS * (int64_t)sizeof(double) * w +
+                    (f->fp32 ? f->total_tiles * TILE_ELEMS * (int64_t)sizeof(float) : 0);
   in.rank_collapsed = f->rank_collapsed;
   in.variant = f->variant;
   in.lu_pairs = (cplx || f->pivoted) ? 0 : (lu_real_pairs(g) ? 1 : 0);
@@ -954,7 +964,13 @@ Fact* factorize(Ctx* c, Mat* m, const lrs_solver_cfg& cfg, const lrs_comm* comm)
   }
   const double nl = (double)(f->row_hi - f->row_lo);
   in.lu_flops = (int64_t)(flops * (cplx ? 4.0 : 1.0));
-  in.apply_bytes = (int64_t)(8.0 * w * (fbytes + 2.0 * nl + 2.0 * nl * f->r));
+  // FP32 factors: the off-diagonal band entries at 4 bytes, the diagonal tiles at 8
+  double diag_entries = 0.0;
+  for (int i = 0; i < P; ++i) diag_entries += (double)f->T[i] * NB * NB;
+  diag_entries = std::min(diag_entries, fbytes);
+  in.apply_bytes = f->fp32 ? (int64_t)(4.0 * (fbytes - diag_entries) + 8.0 * diag_entries +
+                                       8.0 * (2.0 * nl + 2.0 * nl * f->r))
+                           : (int64_t)(8.0 * w * (fbytes + 2.0 * nl + 2.0 * nl * f->r));
   return f.release();
 }
 
