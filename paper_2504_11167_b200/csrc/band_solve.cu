@@ -40,18 +40,23 @@ constexpr int CLD = NB;                  // column stride of a chunk in shared m
 constexpr int CH_SM = CH_COLS * CLD;     // doubles per shared chunk
 constexpr int NCH = NB / CH_COLS;        // chunks per tile
 
+// NR == 1 (the Krylov apply): the diagonal tile is bulk-copied into a resident region at
+// CTA start, so the per-tile critical path (last dependency -> inv(L_tt) / inv(U_tt) ->
+// publish) never waits on HBM; the dependency tiles stream through a 3-stage ring.
 template <int NR> struct SolveCfg {
-  static constexpr int STAGES = 5;
+  static constexpr bool DIAGRES = NR == 1;
+  static constexpr int STAGES = DIAGRES ? 3 : 5;
   static constexpr int XLD = NR == 1 ? 1 : NR + 4;  // padded row stride of xs / red
   static constexpr int PLD = NR + 1;                // K-quarter partials (adjoint DMMA)
   static constexpr int PART = NR == 1 ? 0 : 4 * CH_COLS * PLD;
+  static constexpr int DREG = DIAGRES ? (int)TILE_ELEMS : 0;
 };
 
 template <int NR>
 constexpr size_t solve_smem_bytes() {
-  return sizeof(double) * ((size_t)SolveCfg<NR>::STAGES * CH_SM + 2 * (size_t)NB * SolveCfg<NR>::XLD +
-                           SolveCfg<NR>::PART) +
-         16 * SolveCfg<NR>::STAGES + 64;
+  return sizeof(double) * ((size_t)SolveCfg<NR>::STAGES * CH_SM + SolveCfg<NR>::DREG +
+                           2 * (size_t)NB * SolveCfg<NR>::XLD + SolveCfg<NR>::PART) +
+         16 * (SolveCfg<NR>::STAGES + 1) + 64;
 }
 
 template <int MODE, int NR>
@@ -65,12 +70,14 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1)
   constexpr bool TRANS = (MODE >= 2);
   constexpr bool MMA = NR >= 8;
   extern __shared__ __align__(128) unsigned char smraw[];
+  constexpr bool DIAGRES = SolveCfg<NR>::DIAGRES;
   double* ring = reinterpret_cast<double*>(smraw);
-  double* xs = ring + (size_t)STAGES * CH_SM;  // [NB][XLD]: x_s, or the diagonal-step input
+  double* dreg = ring + (size_t)STAGES * CH_SM;  // resident diagonal tile (NR == 1)
+  double* xs = dreg + SolveCfg<NR>::DREG;      // [NB][XLD]: x_s, or the diagonal-step input
   double* red = xs + NB * XLD;                 // [NB][XLD]: half sums / transposed accumulator
   double* part = red + NB * XLD;               // [4][CH_COLS][PLD]: adjoint K-quarter partials
-  uint64_t* bars = reinterpret_cast<uint64_t*>(part + SolveCfg<NR>::PART);
-  int* s_tk = reinterpret_cast<int*>(bars + STAGES);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(part + SolveCfg<NR>::PART);  // + [STAGES]: diag
+  int* s_tk = reinterpret_cast<int*>(bars + STAGES + 1);
 
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   if (tid == 0) *s_tk = atomicAdd(ticket, 1);
@@ -106,6 +113,7 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1)
     return tiles + (base + (int64_t)s * W + (t - s + wl)) * TILE_ELEMS;
   };
   const int Q = (ndeps + 1) * NCH;
+  const int Qring = DIAGRES ? ndeps * NCH : Q;  // chunks that go through the ring
   // producer: one 32 KB bulk copy per chunk (32 contiguous tile columns); with FP32
   // off-diagonal factors (t32) those chunks are 16 KB
   auto issue = [&](int q, int st) {
@@ -121,12 +129,20 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1)
     bulk_g2s(ring + (size_t)st * CH_SM, src, CH_COLS * NB * sizeof(double), &bars[st]);
   };
   if (tid == 0) {
-    for (int st = 0; st < STAGES; ++st) mbar_init(&bars[st], 1);
+    for (int st = 0; st <= STAGES; ++st) mbar_init(&bars[st], 1);
     fence_mbar_init();
   }
   __syncthreads();
-  if (tid == 0)
-    for (int q = 0; q < STAGES && q < Q; ++q) issue(q, q);
+  if (tid == 0) {
+    if (DIAGRES) {
+      const double* dt = tile_ptr(ndeps);
+      mbar_expect_tx(&bars[STAGES], TILE_ELEMS * sizeof(double));
+      for (int c4 = 0; c4 < NCH; ++c4)
+        bulk_g2s(dreg + (size_t)c4 * CH_SM, dt + (size_t)c4 * CH_SM, CH_SM * sizeof(double),
+                 &bars[STAGES]);
+    }
+    for (int q = 0; q < STAGES && q < Qring; ++q) issue(q, q);
+  }
 
   const int64_t row0 = (int64_t)t * NB;
   const int gq = lane >> 2, tq = lane & 3;  // DMMA fragment coordinates
@@ -211,8 +227,14 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1)
       }
       __syncthreads();
     }
-    mbar_wait(&bars[st], (unsigned)((q / STAGES) & 1));
-    const double* ch = ring + (size_t)st * CH_SM;
+    const double* ch;
+    if (DIAGRES && diag) {
+      mbar_wait(&bars[STAGES], 0u);
+      ch = dreg + (size_t)sub * CH_SM;
+    } else {
+      mbar_wait(&bars[st], (unsigned)((q / STAGES) & 1));
+      ch = ring + (size_t)st * CH_SM;
+    }
     const float* chf = reinterpret_cast<const float*>(ch);
     const bool f32 = t32 != nullptr && !diag;
     const int cbase = sub * CH_COLS;
@@ -312,7 +334,7 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1)
       }
     }
     __syncthreads();
-    if (tid == 0 && q + STAGES < Q) issue(q + STAGES, st);
+    if (tid == 0 && q + STAGES < Qring) issue(q + STAGES, st);
   }
   // ---- write x_t and publish -----------------------------------------------------------
   if (!TRANS && !MMA) {
