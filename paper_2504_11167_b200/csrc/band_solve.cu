@@ -40,11 +40,16 @@ constexpr int CLD = NB;                  // column stride of a chunk in shared m
 constexpr int CH_SM = CH_COLS * CLD;     // doubles per shared chunk
 constexpr int NCH = NB / CH_COLS;        // chunks per tile
 
-// NR == 1 (the Krylov apply): the diagonal tile is bulk-copied into a resident region at
-// CTA start, so the per-tile critical path (last dependency -> inv(L_tt) / inv(U_tt) ->
-// publish) never waits on HBM; the dependency tiles stream through a 3-stage ring.
+// DIAGRES: bulk-copy the diagonal tile into a resident region at CTA start so the per-tile
+// critical path never waits on HBM for it (the dependency tiles then stream through a
+// 3-stage ring).  Measured on c2: apply 3.02 ms with it vs 2.90 ms with the 5-stage ring
+// and no resident tile (the shallower ring costs more than the resident tile saves), so it
+// is off; kept as a switch for narrower-band configurations.
+#ifndef LRS_SOLVE_DIAGRES
+#define LRS_SOLVE_DIAGRES 0
+#endif
 template <int NR> struct SolveCfg {
-  static constexpr bool DIAGRES = NR == 1;
+  static constexpr bool DIAGRES = LRS_SOLVE_DIAGRES && NR == 1;
   static constexpr int STAGES = DIAGRES ? 3 : 5;
   static constexpr int XLD = NR == 1 ? 1 : NR + 4;  // padded row stride of xs / red
   static constexpr int PLD = NR + 1;                // K-quarter partials (adjoint DMMA)

@@ -6,6 +6,7 @@
 #include <cstring>
 #include <memory>
 #include <new>
+#include <thread>
 #include <vector>
 
 #include "fact.h"
@@ -231,42 +232,80 @@ lrs_status lrs_mat_upload_csr(lrs_ctx* c, int64_t n, int64_t nnz, const int64_t*
     if (n >= (1ll << 31) || nnz >= (1ll << 31))
       throw LrsError(LRS_ERR_DIMENSION, "n and nnz must be < 2^31 on the device");
     const int w = scalar == LRS_C128 ? 2 : 1;  // complex values are interleaved (re, im)
-    std::vector<int64_t> rp(n + 1), ci(nnz);
-    std::vector<double> va((size_t)nnz * w);
-    if (mem == LRS_MEM_HOST) {
-      std::memcpy(rp.data(), row_ptr, sizeof(int64_t) * (n + 1));
+    // host views of the arrays (DEVICE inputs are copied down once for validate())
+    std::vector<int64_t> rp_h, ci_h;
+    std::vector<double> va_h;
+    const int64_t* rp = row_ptr;
+    const int64_t* ci = col_idx;
+    const double* va = static_cast<const double*>(values);
+    if (mem == LRS_MEM_DEVICE) {
+      rp_h.resize(n + 1);
+      ci_h.resize(nnz);
+      va_h.resize((size_t)nnz * w);
+      LRS_CUDA(cudaMemcpy(rp_h.data(), row_ptr, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToHost));
       if (nnz) {
-        std::memcpy(ci.data(), col_idx, sizeof(int64_t) * nnz);
-        std::memcpy(va.data(), values, sizeof(double) * nnz * w);
+        LRS_CUDA(cudaMemcpy(ci_h.data(), col_idx, sizeof(int64_t) * nnz, cudaMemcpyDeviceToHost));
+        LRS_CUDA(cudaMemcpy(va_h.data(), values, sizeof(double) * nnz * w, cudaMemcpyDeviceToHost));
       }
-    } else {
-      LRS_CUDA(cudaMemcpy(rp.data(), row_ptr, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToHost));
-      if (nnz) {
-        LRS_CUDA(cudaMemcpy(ci.data(), col_idx, sizeof(int64_t) * nnz, cudaMemcpyDeviceToHost));
-        LRS_CUDA(cudaMemcpy(va.data(), values, sizeof(double) * nnz * w, cudaMemcpyDeviceToHost));
-      }
+      rp = rp_h.data();
+      ci = ci_h.data();
+      va = va_h.data();
     }
     auto absv = [&](int64_t p) {
       return w == 1 ? std::fabs(va[p]) : std::hypot(va[2 * p], va[2 * p + 1]);
     };
-    // validate() -- matrix.cpp:21-37
+    // validate() -- matrix.cpp:21-37 -- and band_metrics, over fixed row chunks on host
+    // threads; the chunk partials combine in chunk order (independent of the thread count)
     if (rp[0] != 0) throw LrsError(LRS_ERR_DIMENSION, "row_ptr[0] must be 0");
     if (rp[n] != nnz) throw LrsError(LRS_ERR_DIMENSION, "row_ptr[n_rows] must equal nnz");
+    const int64_t CH = 65536, nch = (n + CH - 1) / CH;
+    struct Part {
+      int64_t ku = 0, kl = 0, bad_row = -1;
+      int bad = 0;
+      double dsum = 0.0, tsum = 0.0;
+    };
+    std::vector<Part> parts((size_t)nch);
+    std::vector<int> rp32(n + 1), ci32(nnz);
+    auto work = [&](int64_t c0, int64_t c1) {
+      for (int64_t ch = c0; ch < c1; ++ch) {
+        Part& pt = parts[ch];
+        for (int64_t i = ch * CH; i < std::min(n, (ch + 1) * CH) && pt.bad == 0; ++i) {
+          rp32[i] = (int)rp[i];
+          if (rp[i] > rp[i + 1]) { pt.bad = 1; pt.bad_row = i; break; }
+          for (int64_t p = rp[i]; p < rp[i + 1]; ++p) {
+            const int64_t j = ci[p];
+            if (j < 0 || j >= n) { pt.bad = 2; pt.bad_row = i; break; }
+            if (p > rp[i] && j <= ci[p - 1]) { pt.bad = 3; pt.bad_row = i; break; }
+            ci32[p] = (int)j;
+            if (j > i) pt.ku = std::max(pt.ku, j - i);
+            if (j < i) pt.kl = std::max(pt.kl, i - j);
+            const double a = absv(p);
+            pt.tsum += a;
+            if (i == j) pt.dsum += a;
+          }
+        }
+      }
+    };
+    {
+      const unsigned nt = (unsigned)std::max<int64_t>(
+          1, std::min<int64_t>({nch, 16, (int64_t)std::max(1u, std::thread::hardware_concurrency())}));
+      std::vector<std::thread> th;
+      for (unsigned t = 1; t < nt; ++t) th.emplace_back(work, nch * t / nt, nch * (t + 1) / nt);
+      work(0, nch / nt);
+      for (auto& t : th) t.join();
+    }
+    rp32[n] = (int)rp[n];
     int64_t ku = 0, kl = 0;
     double dsum = 0.0, tsum = 0.0;
-    for (int64_t i = 0; i < n; ++i) {
-      if (rp[i] > rp[i + 1]) throw LrsError(LRS_ERR_DIMENSION, "row_ptr must be non-decreasing");
-      for (int64_t p = rp[i]; p < rp[i + 1]; ++p) {
-        const int64_t j = ci[p];
-        if (j < 0 || j >= n) throw LrsError(LRS_ERR_DIMENSION, "column index out of range");
-        if (p > rp[i] && j <= ci[p - 1])
-          throw LrsError(LRS_ERR_DIMENSION,
-                         "column indices must be strictly increasing within a row");
-        if (j > i) ku = std::max(ku, j - i);
-        if (j < i) kl = std::max(kl, i - j);
-        tsum += absv(p);
-        if (i == j) dsum += absv(p);
-      }
+    for (const Part& pt : parts) {
+      if (pt.bad == 1) throw LrsError(LRS_ERR_DIMENSION, "row_ptr must be non-decreasing");
+      if (pt.bad == 2) throw LrsError(LRS_ERR_DIMENSION, "column index out of range");
+      if (pt.bad == 3)
+        throw LrsError(LRS_ERR_DIMENSION, "column indices must be strictly increasing within a row");
+      ku = std::max(ku, pt.ku);
+      kl = std::max(kl, pt.kl);
+      dsum += pt.dsum;
+      tsum += pt.tsum;
     }
     m->ctx = c;
     m->n = n;
@@ -278,36 +317,17 @@ lrs_status lrs_mat_upload_csr(lrs_ctx* c, int64_t n, int64_t nnz, const int64_t*
     m->diag_weight = tsum > 0 ? dsum / tsum : 0.0;
     const double cells = (double)(ku + kl + 1) * (double)n;
     m->band_density = cells > 0 ? (double)nnz / cells : 0.0;
-    // device CSR with int32 indices, and the transpose (host counting sort, structural)
-    std::vector<int> rp32(n + 1), ci32(nnz), trp(n + 1, 0), tci(nnz);
-    std::vector<double> tva((size_t)nnz * w);
-    for (int64_t i = 0; i <= n; ++i) rp32[i] = (int)rp[i];
-    for (int64_t p = 0; p < nnz; ++p) {
-      ci32[p] = (int)ci[p];
-      trp[ci[p] + 1]++;
-    }
-    for (int64_t i = 0; i < n; ++i) trp[i + 1] += trp[i];
-    std::vector<int> next(trp.begin(), trp.end() - 1);
-    for (int64_t i = 0; i < n; ++i)
-      for (int64_t p = rp[i]; p < rp[i + 1]; ++p) {
-        const int q = next[ci[p]]++;
-        tci[q] = (int)i;
-        for (int e = 0; e < w; ++e) tva[(size_t)q * w + e] = va[(size_t)p * w + e];
-      }
+    // device CSR with int32 indices; the transpose is built on the device (csr.cu)
     m->row_ptr.alloc(n + 1);
     m->col_idx.alloc(std::max<int64_t>(nnz, 1));
     m->vals.alloc(std::max<int64_t>(nnz, 1) * w);
-    m->trow_ptr.alloc(n + 1);
-    m->tcol_idx.alloc(std::max<int64_t>(nnz, 1));
-    m->tvals.alloc(std::max<int64_t>(nnz, 1) * w);
     LRS_CUDA(cudaMemcpy(m->row_ptr.get(), rp32.data(), sizeof(int) * (n + 1), cudaMemcpyHostToDevice));
-    LRS_CUDA(cudaMemcpy(m->trow_ptr.get(), trp.data(), sizeof(int) * (n + 1), cudaMemcpyHostToDevice));
     if (nnz) {
       LRS_CUDA(cudaMemcpy(m->col_idx.get(), ci32.data(), sizeof(int) * nnz, cudaMemcpyHostToDevice));
-      LRS_CUDA(cudaMemcpy(m->vals.get(), va.data(), sizeof(double) * nnz * w, cudaMemcpyHostToDevice));
-      LRS_CUDA(cudaMemcpy(m->tcol_idx.get(), tci.data(), sizeof(int) * nnz, cudaMemcpyHostToDevice));
-      LRS_CUDA(cudaMemcpy(m->tvals.get(), tva.data(), sizeof(double) * nnz * w, cudaMemcpyHostToDevice));
+      LRS_CUDA(cudaMemcpy(m->vals.get(), va, sizeof(double) * nnz * w, cudaMemcpyHostToDevice));
     }
+    launch_csr_transpose(c, m.get());
+    LRS_CUDA(cudaStreamSynchronize(c->stream));
   });
   if (s == LRS_OK) *out = m.release();
   return s;

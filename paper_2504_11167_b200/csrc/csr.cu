@@ -1,0 +1,86 @@
+// Device-side CSR transpose (the CSR of A^T used by the spike range finder's adjoint
+// coupling products).  Structural and deterministic: column counts, a
+// prefix sum, an atomic scatter, then every transposed row sorted by its (original) row
+// index -- the same arrays a sequential counting sort produces.
+#include <cub/device/device_scan.cuh>
+
+#include "common.cuh"
+#include "kernels.h"
+#include "lrs_internal.h"
+
+namespace lrs {
+
+__global__ void csr_count_cols_kernel(const int* __restrict__ ci, int64_t nnz, int* cnt) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nnz;
+       e += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(&cnt[ci[e] + 1], 1);
+}
+
+__global__ void csr_scatter_kernel(const int* __restrict__ rp, const int* __restrict__ ci,
+                                   const double* __restrict__ va, int64_t n, int w, int* pos,
+                                   int* tci, double* tva) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  for (int q = rp[r]; q < rp[r + 1]; ++q) {
+    const int slot = atomicAdd(&pos[ci[q]], 1);
+    tci[slot] = (int)r;
+    for (int e = 0; e < w; ++e) tva[(int64_t)slot * w + e] = va[(int64_t)q * w + e];
+  }
+}
+
+__global__ void csr_sort_segments_kernel(const int* __restrict__ trp, int64_t n, int w, int* tci,
+                                         double* tva) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  const int s = trp[c], e = trp[c + 1];
+  for (int i = s + 1; i < e; ++i) {  // insertion sort by row index (segments are short)
+    const int key = tci[i];
+    double v0 = tva[(int64_t)i * w], v1 = w == 2 ? tva[(int64_t)i * w + 1] : 0.0;
+    int j = i - 1;
+    while (j >= s && tci[j] > key) {
+      tci[j + 1] = tci[j];
+      for (int q = 0; q < w; ++q) tva[(int64_t)(j + 1) * w + q] = tva[(int64_t)j * w + q];
+      --j;
+    }
+    tci[j + 1] = key;
+    tva[(int64_t)(j + 1) * w] = v0;
+    if (w == 2) tva[(int64_t)(j + 1) * w + 1] = v1;
+  }
+}
+
+void launch_csr_transpose(Ctx* c, Mat* m) {
+  const int64_t n = m->n, nnz = m->nnz;
+  const int w = m->scalar == LRS_C128 ? 2 : 1;
+  m->trow_ptr.alloc(n + 1);
+  m->tcol_idx.alloc(std::max<int64_t>(nnz, 1));
+  m->tvals.alloc(std::max<int64_t>(nnz, 1) * w);
+  DevBuf<int> cnt, pos;
+  cnt.alloc(n + 1);
+  pos.alloc(std::max<int64_t>(n, 1));
+  LRS_CUDA(cudaMemsetAsync(cnt.get(), 0, sizeof(int) * (n + 1), c->stream));
+  ProfScope ps_(c, K_SETUP);
+  if (nnz > 0) {
+    csr_count_cols_kernel<<<c->num_sms * 4, 256, 0, c->stream>>>(m->col_idx.get(), nnz, cnt.get());
+    LRS_LAUNCHED(c);
+  }
+  size_t tmp_bytes = 0;
+  LRS_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tmp_bytes, cnt.get(), m->trow_ptr.get(),
+                                         (int)(n + 1), c->stream));
+  DevBuf<unsigned char> tmp;
+  tmp.alloc(std::max<size_t>(tmp_bytes, 1));
+  LRS_CUDA(cub::DeviceScan::InclusiveSum(tmp.get(), tmp_bytes, cnt.get(), m->trow_ptr.get(),
+                                         (int)(n + 1), c->stream));
+  if (nnz == 0 || n == 0) return;
+  LRS_CUDA(cudaMemcpyAsync(pos.get(), m->trow_ptr.get(), sizeof(int) * n, cudaMemcpyDeviceToDevice,
+                           c->stream));
+  const unsigned blocks = (unsigned)((n + 255) / 256);
+  csr_scatter_kernel<<<blocks, 256, 0, c->stream>>>(m->row_ptr.get(), m->col_idx.get(),
+                                                     m->vals.get(), n, w, pos.get(),
+                                                     m->tcol_idx.get(), m->tvals.get());
+  LRS_LAUNCHED(c);
+  csr_sort_segments_kernel<<<blocks, 256, 0, c->stream>>>(m->trow_ptr.get(), n, w,
+                                                           m->tcol_idx.get(), m->tvals.get());
+  LRS_LAUNCHED(c);
+}
+
+}  // namespace lrs

@@ -216,6 +216,10 @@ template <class S>
 void launch_multi_axpy_t(Ctx* c, int64_t n, int nrhs, const S* V, int64_t ldv, int64_t strideV,
                          int nvec, const S* y_dev, double sign, S* x, int64_t ldx);
 
+// ---- csr.cu ----------------------------------------------------------------------------
+// m->trow_ptr / tcol_idx / tvals from m->row_ptr / col_idx / vals (deterministic)
+void launch_csr_transpose(Ctx* c, Mat* m);
+
 // ---- bench ---------------------------------------------------------------------------
 double run_dmma_peak(Ctx* c);
 
