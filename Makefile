@@ -5,8 +5,10 @@
 #   tests/cpp/test_api C++ API tests (run from pytest)
 PKG      := paper_2504_11167_b200
 NVCC     ?= nvcc
-CXX      ?= g++
-CC       ?= gcc
+# the host compilers nvcc uses (first g++ / gcc on PATH): one libstdc++ for every library
+# (an environment CXX that links libstdc++ statically would give liblrspike.so a second copy)
+CXX      := g++
+CC       := gcc
 ARCH     := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS  := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xptxas -v --expt-relaxed-constexpr \
             -Iinclude -I$(PKG)/gen -I$(PKG)/csrc

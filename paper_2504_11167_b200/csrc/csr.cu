@@ -2,8 +2,6 @@
 // coupling products).  Structural and deterministic: column counts, a
 // prefix sum, an atomic scatter, then every transposed row sorted by its (original) row
 // index -- the same arrays a sequential counting sort produces.
-#include <cub/device/device_scan.cuh>
-
 #include "common.cuh"
 #include "kernels.h"
 #include "lrs_internal.h"
@@ -48,6 +46,53 @@ __global__ void csr_sort_segments_kernel(const int* __restrict__ trp, int64_t n,
   }
 }
 
+// inclusive prefix sum of n ints (out may alias in): per-1024 block scans, a scan of the
+// block totals in one CTA, and the block offsets added back
+constexpr int SCAN_B = 1024;
+
+__global__ void __launch_bounds__(SCAN_B) scan_blocks_kernel(const int* in, int* out, int64_t n,
+                                                             int* totals) {
+  __shared__ int s[SCAN_B];
+  const int64_t i = (int64_t)blockIdx.x * SCAN_B + threadIdx.x;
+  s[threadIdx.x] = i < n ? in[i] : 0;
+  __syncthreads();
+  for (int o = 1; o < SCAN_B; o <<= 1) {
+    const int v = threadIdx.x >= o ? s[threadIdx.x - o] : 0;
+    __syncthreads();
+    s[threadIdx.x] += v;
+    __syncthreads();
+  }
+  if (i < n) out[i] = s[threadIdx.x];
+  if (threadIdx.x == SCAN_B - 1) totals[blockIdx.x] = s[SCAN_B - 1];
+}
+
+__global__ void __launch_bounds__(SCAN_B) scan_totals_kernel(int* totals, int nb) {
+  __shared__ int carry;
+  __shared__ int s[SCAN_B];
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int b0 = 0; b0 < nb; b0 += SCAN_B) {
+    const int i = b0 + threadIdx.x;
+    s[threadIdx.x] = i < nb ? totals[i] : 0;
+    __syncthreads();
+    for (int o = 1; o < SCAN_B; o <<= 1) {
+      const int v = threadIdx.x >= o ? s[threadIdx.x - o] : 0;
+      __syncthreads();
+      s[threadIdx.x] += v;
+      __syncthreads();
+    }
+    if (i < nb) totals[i] = carry + s[threadIdx.x];
+    __syncthreads();
+    if (threadIdx.x == 0) carry += s[SCAN_B - 1];
+    __syncthreads();
+  }
+}
+
+__global__ void scan_add_kernel(int* out, int64_t n, const int* totals) {
+  const int64_t i = (int64_t)blockIdx.x * SCAN_B + threadIdx.x;
+  if (blockIdx.x > 0 && i < n) out[i] += totals[blockIdx.x - 1];
+}
+
 void launch_csr_transpose(Ctx* c, Mat* m) {
   const int64_t n = m->n, nnz = m->nnz;
   const int w = m->scalar == LRS_C128 ? 2 : 1;
@@ -63,13 +108,18 @@ void launch_csr_transpose(Ctx* c, Mat* m) {
     csr_count_cols_kernel<<<c->num_sms * 4, 256, 0, c->stream>>>(m->col_idx.get(), nnz, cnt.get());
     LRS_LAUNCHED(c);
   }
-  size_t tmp_bytes = 0;
-  LRS_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tmp_bytes, cnt.get(), m->trow_ptr.get(),
-                                         (int)(n + 1), c->stream));
-  DevBuf<unsigned char> tmp;
-  tmp.alloc(std::max<size_t>(tmp_bytes, 1));
-  LRS_CUDA(cub::DeviceScan::InclusiveSum(tmp.get(), tmp_bytes, cnt.get(), m->trow_ptr.get(),
-                                         (int)(n + 1), c->stream));
+  {
+    const int64_t len = n + 1;
+    const int nb = (int)((len + SCAN_B - 1) / SCAN_B);
+    DevBuf<int> totals;
+    totals.alloc(nb);
+    scan_blocks_kernel<<<nb, SCAN_B, 0, c->stream>>>(cnt.get(), m->trow_ptr.get(), len, totals.get());
+    LRS_LAUNCHED(c);
+    scan_totals_kernel<<<1, SCAN_B, 0, c->stream>>>(totals.get(), nb);
+    LRS_LAUNCHED(c);
+    scan_add_kernel<<<nb, SCAN_B, 0, c->stream>>>(m->trow_ptr.get(), len, totals.get());
+    LRS_LAUNCHED(c);
+  }
   if (nnz == 0 || n == 0) return;
   LRS_CUDA(cudaMemcpyAsync(pos.get(), m->trow_ptr.get(), sizeof(int) * n, cudaMemcpyDeviceToDevice,
                            c->stream));

@@ -111,3 +111,28 @@ def test_reduced_system_operators_match_oracle(ctx):
     assert _rel(F.matvec_exact(xr), O._pack(*O.matvec_otf(Fo, xt, xb))) < 1e-12
     g = F.apply_truncated_precond(xr)
     assert _rel(g, O._pack(*O.apply_truncated_precond(Fo.trunc, xt, xb))) < 1e-11
+
+
+def test_cli_solve_with_reorder_pipeline(tmp_path):
+    """Matrix Market in, reorder pipeline, GPU solve, solution mapped back."""
+    import json
+
+    from paper_2504_11167_b200 import cli, reorder
+    from paper_2504_11167_b200.configs import Csr
+
+    S = configs.make_config("c1", 48 / 256).matrix.to_scipy()
+    n = S.shape[0]
+    p = np.random.default_rng(2).permutation(n)
+    Sp = sp.csr_matrix((S.data, S.indices, S.indptr), shape=S.shape)[p][:, p].tocsr()
+    Sp.sort_indices()
+    src = tmp_path / "a.mtx"
+    reorder.write_matrix_market(str(src), Csr(n, Sp.indptr.astype(np.int64),
+                                              Sp.indices.astype(np.int64), Sp.data))
+    rep_path, x_path = tmp_path / "r.json", tmp_path / "x.npy"
+    assert cli.main(["solve", "--in", str(src), "--rhs", "ones", "--variant", "t", "-p", "4",
+                     "--nsvd", "8", "--tol", "1e-9", "--method", "gmres", "--reorder",
+                     "--report", str(rep_path), "--x-out", str(x_path)]) == 0
+    r = json.load(open(rep_path))
+    assert r["converged"] and r["residual_final"] <= 1e-8
+    x = np.load(x_path)
+    assert _rel(Sp @ x, np.ones((n, 1))) <= 1e-8
