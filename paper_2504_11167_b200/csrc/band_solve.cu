@@ -26,11 +26,21 @@
 // row, which keeps less work on the per-tile critical path and streams the
 // factor at ~96% of the measured HBM copy bandwidth.
 //
+// One-RHS L and U sweeps (the Krylov hot path) hand x_t to their dependants through a
+// self-validating mailbox instead of x + a ready flag: each double of x_t travels as two
+// 8-byte words (epoch << 32 | 32-bit half), stored relaxed and polled relaxed, one word
+// per consumer thread.  A consumer's poll IS its data load (one L2 round trip instead of
+// flag-acquire then load), and the producer needs no fence before publishing.
+//
 // Modes: 0  L  forward (unit lower),   1  U  backward,
 //        2  U^T forward (adjoint),     3  L^T backward (adjoint).
 #include "common.cuh"
 #include "kernels.h"
 #include "lrs_internal.h"
+
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
 
 namespace lrs {
 
@@ -40,22 +50,31 @@ constexpr int CLD = NB;                  // column stride of a chunk in shared m
 constexpr int CH_SM = CH_COLS * CLD;     // doubles per shared chunk
 constexpr int NCH = NB / CH_COLS;        // chunks per tile
 
-// DIAGRES: bulk-copy the diagonal tile into a resident region at CTA start so the per-tile
-// critical path never waits on HBM for it (the dependency tiles then stream through a
-// 3-stage ring).  Measured on c2: apply 3.02 ms with it vs 2.90 ms with the 5-stage ring
-// and no resident tile (the shallower ring costs more than the resident tile saves), so it
-// is off; kept as a switch for narrower-band configurations.
-#ifndef LRS_SOLVE_DIAGRES
-#define LRS_SOLVE_DIAGRES 0
+// DIAGPK (NR == 1, L and U sweeps; off): the triangle of the diagonal tile the sweep uses
+// (strictly lower inv(L) in mode 0, upper inv(U) in mode 1: 8128 / 8256 doubles) is
+// copied packed into a resident 64.5 KB region at CTA start (cp.async), next to the full
+// 5-stage ring, so no diagonal chunk is fetched after the last dependency resolves.
+// Measured on c2 with the mailbox handoff: apply 2.63 ms with it, 2.51 ms without (the
+// triangular product's shared-memory reads cost more than the chunk refetch, which the
+// ring already overlaps); kept as a switch.  (A resident full 128 KB tile, which forces the
+// ring down to 3 stages, was slower still.)
+#ifndef LRS_SOLVE_DIAGPK
+#define LRS_SOLVE_DIAGPK 0
 #endif
+constexpr int DPK_ELEMS = NB * (NB + 1) / 2;  // 8256: upper incl. diagonal (lower: 8128)
 template <int NR> struct SolveCfg {
-  static constexpr bool DIAGRES = LRS_SOLVE_DIAGRES && NR == 1;
-  static constexpr int STAGES = DIAGRES ? 3 : 5;
+  static constexpr bool DIAGPK = LRS_SOLVE_DIAGPK && NR == 1;
+  static constexpr int STAGES = 5;
   static constexpr int XLD = NR == 1 ? 1 : NR + 4;  // padded row stride of xs / red
   static constexpr int PLD = NR + 1;                // K-quarter partials (adjoint DMMA)
   static constexpr int PART = NR == 1 ? 0 : 4 * CH_COLS * PLD;
-  static constexpr int DREG = DIAGRES ? (int)TILE_ELEMS : 0;
+  static constexpr int DREG = DIAGPK ? DPK_ELEMS : 0;
 };
+// packed index of diagonal-tile element (r, c) of the triangle the sweep uses
+template <int MODE>
+__device__ __forceinline__ int dpk_col(int c) {
+  return MODE == 0 ? c * NB - c * (c + 1) / 2 - c - 1 : c * (c + 1) / 2;
+}
 
 template <int NR>
 constexpr size_t solve_smem_bytes() {
@@ -64,20 +83,39 @@ constexpr size_t solve_smem_bytes() {
          16 * (SolveCfg<NR>::STAGES + 1) + 64;
 }
 
+#ifdef LRS_SOLVE_TRACE
+// development aid: per-CTA globaltimer stamps (start, last-dependency wait begins, last
+// dependency ready, diagonal step, diagonal product done, published)
+__device__ unsigned long long* g_strace = nullptr;
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define STRACE(i) \
+  if (g_strace && tid == 0) g_strace[(size_t)tk0 * 8 + (i)] = gtimer()
+#else
+#define STRACE(i)
+#endif
+
+
 template <int MODE, int NR>
 __global__ void __launch_bounds__(SOLVE_THREADS, 1)
     band_solve_kernel(BandGeom g, const double* __restrict__ tiles, double* x, int64_t ld,
                       int nrhs, unsigned* flags, unsigned epoch, int* ticket, int p_only,
-                      int ngroups, int64_t flag_stride, const float* __restrict__ t32) {
+                      int ngroups, int64_t flag_stride, const float* __restrict__ t32,
+                      unsigned long long* mbox) {
   constexpr int STAGES = SolveCfg<NR>::STAGES;
   constexpr int XLD = SolveCfg<NR>::XLD;
   constexpr bool FWD = (MODE == 0 || MODE == 2);
   constexpr bool TRANS = (MODE >= 2);
   constexpr bool MMA = NR >= 8;
   extern __shared__ __align__(128) unsigned char smraw[];
-  constexpr bool DIAGRES = SolveCfg<NR>::DIAGRES;
+  constexpr bool DPK = SolveCfg<NR>::DIAGPK && !TRANS;
+  constexpr bool LLM = NR == 1 && !TRANS;  // mailbox handoff (2 words per row of x_t)
+  static_assert(!LLM || SOLVE_THREADS == 2 * NB, "one mailbox word per thread");
   double* ring = reinterpret_cast<double*>(smraw);
-  double* dreg = ring + (size_t)STAGES * CH_SM;  // resident diagonal tile (NR == 1)
+  double* dreg = ring + (size_t)STAGES * CH_SM;  // resident packed diagonal triangle
   double* xs = dreg + SolveCfg<NR>::DREG;      // [NB][XLD]: x_s, or the diagonal-step input
   double* red = xs + NB * XLD;                 // [NB][XLD]: half sums / transposed accumulator
   double* part = red + NB * XLD;               // [4][CH_COLS][PLD]: adjoint K-quarter partials
@@ -88,6 +126,7 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1)
   if (tid == 0) *s_tk = atomicAdd(ticket, 1);
   __syncthreads();
   const int tk0 = *s_tk;
+  STRACE(0);
   // column group (adjacent tickets: the groups of one row tile start together)
   const int grp = tk0 % ngroups, tk = tk0 / ngroups;
   x += (int64_t)grp * NR * ld;
@@ -118,7 +157,7 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1)
     return tiles + (base + (int64_t)s * W + (t - s + wl)) * TILE_ELEMS;
   };
   const int Q = (ndeps + 1) * NCH;
-  const int Qring = DIAGRES ? ndeps * NCH : Q;  // chunks that go through the ring
+  const int Qring = DPK ? ndeps * NCH : Q;  // chunks that go through the ring
   // producer: one 32 KB bulk copy per chunk (32 contiguous tile columns); with FP32
   // off-diagonal factors (t32) those chunks are 16 KB
   auto issue = [&](int q, int st) {
@@ -138,15 +177,17 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1)
     fence_mbar_init();
   }
   __syncthreads();
-  if (tid == 0) {
-    if (DIAGRES) {
-      const double* dt = tile_ptr(ndeps);
-      mbar_expect_tx(&bars[STAGES], TILE_ELEMS * sizeof(double));
-      for (int c4 = 0; c4 < NCH; ++c4)
-        bulk_g2s(dreg + (size_t)c4 * CH_SM, dt + (size_t)c4 * CH_SM, CH_SM * sizeof(double),
-                 &bars[STAGES]);
-    }
+  if (tid == 0)
     for (int q = 0; q < STAGES && q < Qring; ++q) issue(q, q);
+  if (DPK) {
+    // warp per column: column c of the triangle is contiguous in the tile (column-major)
+    const double* dt = tile_ptr(ndeps);
+    for (int c = w; c < NB; c += SOLVE_THREADS / 32) {
+      const int r0 = MODE == 0 ? c + 1 : 0, r1 = MODE == 0 ? NB : c + 1;
+      double* dst = dreg + dpk_col<MODE>(c);
+      for (int r = r0 + lane; r < r1; r += 32) cp_async8(dst + r, dt + (size_t)c * NB + r);
+    }
+    cp_async_commit();
   }
 
   const int64_t row0 = (int64_t)t * NB;
@@ -192,21 +233,34 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1)
     if (sub == 0) {
       if (!diag) {
         const int s = s0 + d * sstep;
-        if (tid == 0) {
-          const unsigned* f = flags + g.fbase[p] + s;
-          while (ld_acquire_u32(f) != epoch) __nanosleep(32);
-        }
-        __syncthreads();
-        const int64_t srow0 = (int64_t)s * NB;
-        for (int e = tid; e < NB * NR; e += SOLVE_THREADS) {
-          const int r = e % NB, j = e / NB;
-          xs[r * XLD + j] = (j < nrhs && srow0 + r < size) ? __ldcg(x + off + srow0 + r + j * ld) : 0.0;
+        if (d == ndeps - 1) STRACE(1);
+        if (LLM) {
+          const unsigned long long* mb = mbox + (size_t)(g.fbase[p] + s) * (2 * NB) + tid;
+          unsigned long long v = ld_relaxed_u64(mb);
+          while ((unsigned)(v >> 32) != epoch) {
+            __nanosleep(16);
+            v = ld_relaxed_u64(mb);
+          }
+          reinterpret_cast<unsigned*>(xs)[tid] = (unsigned)v;
+          if (d == ndeps - 1) STRACE(2);
+        } else {
+          if (tid == 0) {
+            const unsigned* f = flags + g.fbase[p] + s;
+            while (ld_acquire_u32(f) != epoch) __nanosleep(32);
+          }
+          __syncthreads();
+          const int64_t srow0 = (int64_t)s * NB;
+          for (int e = tid; e < NB * NR; e += SOLVE_THREADS) {
+            const int r = e % NB, j = e / NB;
+            xs[r * XLD + j] = (j < nrhs && srow0 + r < size) ? __ldcg(x + off + srow0 + r + j * ld) : 0.0;
+          }
         }
       } else {
         // diagonal step: the accumulated right-hand side becomes the product input
         if (!TRANS) {
           if (!MMA) {
             if (hh == 1) red[row] = acc1;
+            if (DPK) cp_async_wait<0>();
             __syncthreads();
             if (hh == 0) xs[row] = acc1 + red[row];
             acc1 = 0.0;
@@ -232,14 +286,24 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1)
       }
       __syncthreads();
     }
-    const double* ch;
-    if (DIAGRES && diag) {
-      mbar_wait(&bars[STAGES], 0u);
-      ch = dreg + (size_t)sub * CH_SM;
-    } else {
-      mbar_wait(&bars[st], (unsigned)((q / STAGES) & 1));
-      ch = ring + (size_t)st * CH_SM;
+    if (diag && sub == 0) STRACE(3);
+    if (DPK && diag) {
+      // the whole diagonal product from the resident triangle; columns split by parity
+      // between the two row halves, two independent chains per thread
+      double a0 = 0.0, a1 = 0.0;
+#pragma unroll 4
+      for (int c = hh; c < NB; c += 4) {
+        const int c2 = c + 2;
+        const bool u0 = MODE == 0 ? row > c : row <= c, u1 = MODE == 0 ? row > c2 : row <= c2;
+        if (u0) a0 = fma(dreg[dpk_col<MODE>(c) + row], xs[c], a0);
+        if (u1) a1 = fma(dreg[dpk_col<MODE>(c2) + row], xs[c2], a1);
+      }
+      acc1 = a0 + a1;
+      STRACE(4);
+      break;
     }
+    mbar_wait(&bars[st], (unsigned)((q / STAGES) & 1));
+    const double* ch = ring + (size_t)st * CH_SM;
     const float* chf = reinterpret_cast<const float*>(ch);
     const bool f32 = t32 != nullptr && !diag;
     const int cbase = sub * CH_COLS;
@@ -345,10 +409,27 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1)
   if (!TRANS && !MMA) {
     if (hh == 1) red[row] = acc1;
     __syncthreads();
-    if (hh == 0 && row0 + row < size && nrhs > 0) {
-      double v = acc1 + red[row];
-      if (MODE == 0) v += xs[row];  // unit diagonal of inv(L)
-      x[off + row0 + row] = v;
+    if (hh == 0) {
+      double v = 0.0;
+      if (row0 + row < size && nrhs > 0) {
+        v = acc1 + red[row];
+        if (MODE == 0) v += xs[row];  // unit diagonal of inv(L)
+      }
+      if (LLM) {
+        const unsigned long long tag = (unsigned long long)epoch << 32;
+        const unsigned long long bits = (unsigned long long)__double_as_longlong(v);
+        unsigned long long* mb = mbox + (size_t)(g.fbase[p] + t) * (2 * NB) + 2 * row;
+        st_relaxed_u64(mb, tag | (bits & 0xffffffffull));
+        st_relaxed_u64(mb + 1, tag | (bits >> 32));
+      }
+      if (row0 + row < size && nrhs > 0) x[off + row0 + row] = v;
+    }
+    if (LLM) {
+      STRACE(5);
+#ifdef LRS_SOLVE_TRACE
+      if (g_strace && tid == 0) g_strace[(size_t)tk0 * 8 + 6] = ((unsigned long long)p << 32) | t;
+#endif
+      return;
     }
   } else if (!TRANS) {
 #pragma unroll
@@ -379,12 +460,17 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1)
   __threadfence();
   __syncthreads();
   if (tid == 0) st_release_u32(flags + g.fbase[p] + t, epoch);
+  STRACE(5);
+#ifdef LRS_SOLVE_TRACE
+  if (g_strace && tid == 0) g_strace[(size_t)tk0 * 8 + 6] = ((unsigned long long)p << 32) | t;
+#endif
 }
 
 template <int MODE, int NR>
 static void launch_mode(Ctx* c, const BandGeom& g, const double* tiles, double* x, int64_t ld,
                         int nrhs, unsigned* flags, unsigned epoch, int* ticket, int p_only,
-                        int ntiles, int64_t flag_stride, const float* t32) {
+                        int ntiles, int64_t flag_stride, const float* t32,
+                        unsigned long long* mbox) {
   const int ngroups = (nrhs + NR - 1) / NR;
   static bool attr = false;
   const size_t smem = solve_smem_bytes<NR>();
@@ -394,38 +480,66 @@ static void launch_mode(Ctx* c, const BandGeom& g, const double* tiles, double* 
     attr = true;
   }
   ProfScope ps_(c, c->in_setup ? K_SPIKE_SOLVE : (MODE >= 2 ? K_SOLVE_ADJ : K_SOLVE));
+#ifdef LRS_SOLVE_TRACE
+  static int launches = 0;
+  unsigned long long* tb = nullptr;
+  const bool tr = NR == 1 && MODE <= 1 && std::getenv("LRS_STRACE") && ++launches >= 40 &&
+                  launches < 44;
+  if (tr) {
+    LRS_CUDA(cudaStreamSynchronize(c->stream));
+    LRS_CUDA(cudaMalloc(&tb, (size_t)ntiles * 8 * 8));
+    LRS_CUDA(cudaMemset(tb, 0, (size_t)ntiles * 8 * 8));
+    LRS_CUDA(cudaMemcpyToSymbol(g_strace, &tb, sizeof(tb)));
+  }
+#endif
   band_solve_kernel<MODE, NR><<<ntiles * ngroups, SOLVE_THREADS, smem, c->stream>>>(
       g, tiles, x, ld, nrhs, flags, epoch, ticket, p_only, ngroups, flag_stride,
-      MODE <= 1 ? t32 : nullptr);
+      MODE <= 1 ? t32 : nullptr, mbox);
   LRS_LAUNCHED(c);
+#ifdef LRS_SOLVE_TRACE
+  if (tr) {
+    LRS_CUDA(cudaStreamSynchronize(c->stream));
+    std::vector<unsigned long long> h((size_t)ntiles * 8);
+    LRS_CUDA(cudaMemcpy(h.data(), tb, h.size() * 8, cudaMemcpyDeviceToHost));
+    unsigned long long* z = nullptr;
+    LRS_CUDA(cudaMemcpyToSymbol(g_strace, &z, sizeof(z)));
+    LRS_CUDA(cudaFree(tb));
+    FILE* f = std::fopen(std::getenv("LRS_STRACE"), "ab");
+    const int hdr[2] = {MODE, ntiles};
+    std::fwrite(hdr, sizeof(int), 2, f);
+    std::fwrite(h.data(), 8, h.size(), f);
+    std::fclose(f);
+  }
+#endif
 }
 
 template <int MODE>
 static void launch_nr(Ctx* c, const BandGeom& g, const double* tiles, double* x, int64_t ld,
                       int nrhs, unsigned* flags, unsigned epoch, int* ticket, int p_only,
-                      int ntiles, int64_t fs, const float* t32) {
+                      int ntiles, int64_t fs, const float* t32, unsigned long long* mb) {
   // every width runs the same DMMA code (one n8 tile for <= 8 columns, 16-column groups
   // beyond 16), so each column's arithmetic is independent of the batch: multi-column ==
   // column-by-column bit-exactly
   if (nrhs <= 1 && c->solve_fma1)
-    launch_mode<MODE, 1>(c, g, tiles, x, ld, nrhs, flags, epoch, ticket, p_only, ntiles, fs, t32);
+    launch_mode<MODE, 1>(c, g, tiles, x, ld, nrhs, flags, epoch, ticket, p_only, ntiles, fs, t32, mb);
   else if (nrhs <= 8)
-    launch_mode<MODE, 8>(c, g, tiles, x, ld, nrhs, flags, epoch, ticket, p_only, ntiles, fs, t32);
+    launch_mode<MODE, 8>(c, g, tiles, x, ld, nrhs, flags, epoch, ticket, p_only, ntiles, fs, t32, mb);
   else
-    launch_mode<MODE, 16>(c, g, tiles, x, ld, nrhs, flags, epoch, ticket, p_only, ntiles, fs, t32);
+    launch_mode<MODE, 16>(c, g, tiles, x, ld, nrhs, flags, epoch, ticket, p_only, ntiles, fs, t32, mb);
 }
 
 void launch_band_solve(Ctx* c, const BandGeom& g, const double* tiles, int mode, double* x,
                        int64_t ld, int nrhs, unsigned* flags, unsigned epoch, int* ticket,
-                       int p_only, int ntiles, int64_t fs, const float* t32) {
+                       int p_only, int ntiles, int64_t fs, const float* t32,
+                       unsigned long long* mb) {
   if (ntiles == 0 || nrhs == 0) return;
   if (nrhs > SOLVE_MAX_RHS) throw LrsError(LRS_ERR_PARAMETER, "band solve batch > 48 columns");
   LRS_CUDA(cudaMemsetAsync(ticket, 0, sizeof(int), c->stream));
   switch (mode) {
-    case 0: launch_nr<0>(c, g, tiles, x, ld, nrhs, flags, epoch, ticket, p_only, ntiles, fs, t32); break;
-    case 1: launch_nr<1>(c, g, tiles, x, ld, nrhs, flags, epoch, ticket, p_only, ntiles, fs, t32); break;
-    case 2: launch_nr<2>(c, g, tiles, x, ld, nrhs, flags, epoch, ticket, p_only, ntiles, fs, t32); break;
-    default: launch_nr<3>(c, g, tiles, x, ld, nrhs, flags, epoch, ticket, p_only, ntiles, fs, t32); break;
+    case 0: launch_nr<0>(c, g, tiles, x, ld, nrhs, flags, epoch, ticket, p_only, ntiles, fs, t32, mb); break;
+    case 1: launch_nr<1>(c, g, tiles, x, ld, nrhs, flags, epoch, ticket, p_only, ntiles, fs, t32, mb); break;
+    case 2: launch_nr<2>(c, g, tiles, x, ld, nrhs, flags, epoch, ticket, p_only, ntiles, fs, t32, mb); break;
+    default: launch_nr<3>(c, g, tiles, x, ld, nrhs, flags, epoch, ticket, p_only, ntiles, fs, t32, mb); break;
   }
 }
 

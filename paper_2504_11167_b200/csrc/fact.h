@@ -35,6 +35,7 @@ struct Fact {
   DevBuf<int> d_T;
   DevBuf<double> tiles;
   DevBuf<unsigned> flags;
+  DevBuf<unsigned long long> mbox;  // one-RHS sweeps: x_t handoff words [rowtiles][2 NB]
   DevBuf<int> ticket;
   unsigned epoch = 0;
   DevBuf<int> status;

@@ -78,10 +78,12 @@ void launch_extract_tiles_z(Ctx* c, const Mat* m, const BandGeom& g, zc* tiles, 
 // mode 0: L (forward), 1: U (backward), 2: U^T (forward), 3: L^T (backward).
 // x is the global-row-layout block (n rows, ld), columns [0, nrhs), nrhs <= SOLVE_MAX_RHS.
 // flags: SOLVE_GROUPS x flag_stride ready flags (one set per 16-column group).
-// t32: FP32 copy of the tiles (off-diagonal tiles read from it in modes 0 / 1) or null
+// t32: FP32 copy of the tiles (off-diagonal tiles read from it in modes 0 / 1) or null.
+// mbox: [flag_stride][2 NB] zero-initialised handoff words of the one-RHS L / U sweeps
 void launch_band_solve(Ctx* c, const BandGeom& g, const double* tiles, int mode, double* x,
                        int64_t ld, int nrhs, unsigned* flags, unsigned epoch, int* ticket,
-                       int p_only, int ntiles, int64_t flag_stride, const float* t32 = nullptr);
+                       int p_only, int ntiles, int64_t flag_stride, const float* t32,
+                       unsigned long long* mbox);
 // tiles32[e] = (float)tiles[e] for the off-diagonal tiles (mixed-precision apply)
 void launch_tiles_to_fp32(Ctx* c, const double* tiles, float* t32, int64_t count);
 constexpr int ZSOLVE_MAX_RHS = 16 * SOLVE_GROUPS;  // 96

@@ -174,7 +174,8 @@ void dstage_t(Fact* f, S* x, int64_t ld, int nrhs, bool adjoint, int p_only) {
       else
         launch_band_solve(f->ctx, g, f->tiles.get(), mode, xc, ld, nr, f->flags.get(),
                           f->next_epoch(), f->ticket.get(), p_only, ntiles, f->total_rowtiles,
-                          (f->fp32 && !f->ctx->in_setup) ? f->tiles32.get() : nullptr);
+                          (f->fp32 && !f->ctx->in_setup) ? f->tiles32.get() : nullptr,
+                          f->mbox.get());
     }
   }
 }
@@ -729,11 +730,13 @@ Fact* factorize(Ctx* c, Mat* m, const lrs_solver_cfg& cfg, const lrs_comm* comm)
     f->tiles.reset();
     f->tiles.alloc((size_t)tb * TILE_ELEMS * w);
     f->flags.alloc((size_t)fb * SOLVE_GROUPS);
+    f->mbox.alloc((size_t)fb * 2 * NB);
     f->ticket.alloc(1);
     f->status.alloc(2 * P);
     f->bad.alloc(1);
     LRS_CUDA(cudaMemsetAsync(f->tiles.get(), 0, sizeof(double) * tb * TILE_ELEMS * w, c->stream));
     LRS_CUDA(cudaMemsetAsync(f->flags.get(), 0, sizeof(unsigned) * fb * SOLVE_GROUPS, c->stream));
+    LRS_CUDA(cudaMemsetAsync(f->mbox.get(), 0, sizeof(unsigned long long) * fb * 2 * NB, c->stream));
     LRS_CUDA(cudaMemsetAsync(f->status.get(), 0x7f, sizeof(int) * 2 * P, c->stream));
     LRS_CUDA(cudaMemsetAsync(f->bad.get(), 0xff, sizeof(unsigned long long), c->stream));
   };
