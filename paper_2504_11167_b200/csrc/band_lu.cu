@@ -574,7 +574,13 @@ static void lu_attrs() {
   g_lu_attr_set = true;
 }
 
+// LRS_LU_SKIP (timing experiments only, wrong factors): 4 drops the bulk two-step update,
+// 1 drops everything else (diag, panels, look-ahead updates)
+#ifndef LRS_LU_SKIP
+#define LRS_LU_SKIP 0
+#endif
 static void real_diag(Ctx* c, cudaStream_t s, const BandGeom& g, void* tiles, int K, int* status) {
+  if (LRS_LU_SKIP == 1) return;
   lu_diag_kernel<<<g.P, DIAG_THREADS, sizeof(double) * (TILE_ELEMS + 4 * NB), s>>>(
       g, static_cast<double*>(tiles), K, status);
 }
@@ -582,6 +588,7 @@ static void real_gemm(Ctx* c, cudaStream_t s, const BandGeom& g, void* tiles, in
                       int kind) {
   double* t = static_cast<double*>(tiles);
   constexpr int S = GEMM_SPLIT;
+  if ((LRS_LU_SKIP == 4 && kind == 4) || (LRS_LU_SKIP == 1 && kind != 4)) return;
   if (kind == 0)
     lu_gemm_kernel<0><<<dim3(S * (g.wl + g.wu), g.P), GEMM_THREADS, GEMM_SMEM, s>>>(g, t, K, status);
   else if (kind == 1 && LRS_LU_PERSISTENT) {
@@ -655,9 +662,40 @@ bool lu_real_pairs(const BandGeom& g) {
   return lu_uses_pairs(g, LuKernels{real_diag, real_gemm, LRS_LU_PAIRS != 0});
 }
 
+// The two-step updates (kinds 3 / 4) run integer-sliced on the INT8 tensor cores (lu_i8.cu)
+// unless LRS_LU_I8=0, the band is too narrow for the pair schedule, or the two panel
+// buffers would take more than a quarter of the free device memory.
+static bool lu_i8_wanted(const BandGeom& g, const LuKernels& L) {
+  const char* e = std::getenv("LRS_LU_I8");
+  if (e && e[0] == '0') return false;
+  if (!lu_uses_pairs(g, L)) return false;
+  size_t fr = 0, tot = 0;
+  if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) return false;
+  return 2 * lu_i8_panel_bytes(g) < fr / 4;
+}
+
 void launch_band_lu(Ctx* c, const BandGeom& g, double* tiles, int Tmax, int* status) {
   lu_attrs();
-  run_band_lu(c, g, tiles, Tmax, status, LuKernels{real_diag, real_gemm, LRS_LU_PAIRS != 0});
+  LuKernels L{real_diag, real_gemm, LRS_LU_PAIRS != 0};
+  DevBuf<uint8_t> buf;
+  I8Panel pn[2];
+  if (lu_i8_wanted(g, L)) {
+    auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
+    const size_t a = al((size_t)g.P * g.wl * TILE_ELEMS * 2 * 8),
+                 b = al((size_t)g.P * g.wu * TILE_ELEMS * 2 * 8),
+                 ea = al(sizeof(int) * g.P * g.wl * NB), eb = al(sizeof(int) * g.P * g.wu * NB);
+    buf.alloc(2 * (a + b + ea + eb));
+    uint8_t* q = buf.get();
+    for (int k = 0; k < 2; ++k) {
+      pn[k].A = q;
+      pn[k].B = q + a;
+      pn[k].ea = reinterpret_cast<int*>(q + a + b);
+      pn[k].eb = reinterpret_cast<int*>(q + a + b + ea);
+      q += a + b + ea + eb;
+    }
+    L.i8 = pn;
+  }
+  run_band_lu(c, g, tiles, Tmax, status, L);
 }
 
 // Right-looking tiled LU with look-ahead depth 1 over two streams:
@@ -684,6 +722,19 @@ void run_band_lu(Ctx* c, const BandGeom& g, void* tiles, int Tmax, int* status,
     L.gemm(c, s, g, tiles, K, status, kind);
     LRS_LAUNCHED(c);
   };
+  // INT8 path: slice(K) digitises the panels of pair K right after panel(K+1) on the
+  // critical stream; the pair buffers alternate (pair K-4's readers -- rest2(K-4) on main,
+  // next3(K-4) on crit -- completed before crit reaches slice(K)).
+  auto slice = [&](int K) {
+    if (!L.i8) return;
+    ProfScope ps_(c, K_LU_PANEL, sc);
+    launch_lu_i8_slice(c, sc, g, static_cast<const double*>(tiles), K, L.i8[(K >> 1) & 1]);
+  };
+  auto upd2 = [&](cudaStream_t s, int K, int kind, int cls) {
+    if (!L.i8) return gemm(s, K, kind, cls);
+    ProfScope ps_(c, cls, s);
+    launch_lu_i8_gemm(c, s, g, static_cast<double*>(tiles), K, kind, L.i8[(K >> 1) & 1]);
+  };
   if (lu_uses_pairs(g, L)) {
     // Steps in pairs (K, K+1) with a rank-256 bulk update and look-ahead depth 2:
     //   main: [wait panel(K+1)] rest2(K, K+1)                       (I, J >= K+4)
@@ -693,21 +744,23 @@ void run_band_lu(Ctx* c, const BandGeom& g, void* tiles, int Tmax, int* status,
     if (Tmax > 1) {
       gemm(sc, 0, 2, K_LU_PANEL);
       lu_diag_panel(c, sc, g, tiles, 1, status, L);
+      slice(0);
       LRS_CUDA(cudaEventRecord(ev_panel, sc));
     }
     bool have_rest = false;
     for (int K = 0; K + 1 < Tmax; K += 2) {
       if (have_rest) LRS_CUDA(cudaStreamWaitEvent(sc, ev_rest, 0));  // rest2(K-2, K-1)
       LRS_CUDA(cudaStreamWaitEvent(sm, ev_panel, 0));                  // diag/panel(K+1)
-      gemm(sm, K, 4, K_LU_UPDATE);
+      upd2(sm, K, 4, K_LU_UPDATE);
       LRS_CUDA(cudaEventRecord(ev_rest, sm));
       have_rest = true;
       if (K + 2 < Tmax) {
-        gemm(sc, K, 3, K_LU_PANEL);
+        upd2(sc, K, 3, K_LU_PANEL);
         lu_diag_panel(c, sc, g, tiles, K + 2, status, L);
         if (K + 3 < Tmax) {
           gemm(sc, K + 2, 2, K_LU_PANEL);
           lu_diag_panel(c, sc, g, tiles, K + 3, status, L);
+          slice(K + 2);
         }
         LRS_CUDA(cudaEventRecord(ev_panel, sc));
       }

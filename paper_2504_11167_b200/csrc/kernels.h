@@ -47,6 +47,19 @@ void launch_extract_tiles(Ctx* c, const Mat* m, const BandGeom& g, double* tiles
 // status[2p] = min column needing a row interchange, status[2p+1] = min zero-pivot column.
 void launch_band_lu(Ctx* c, const BandGeom& g, double* tiles, int Tmax, int* status);
 void launch_band_lu_z(Ctx* c, const BandGeom& g, zc* tiles, int Tmax, int* status);
+// integer-sliced (INT8 tensor core) two-step trailing update, lu_i8.cu: digit slices of one
+// step pair's A panel (rows K+2..K+1+wl) and B panel (columns K+2..K+1+wu)
+struct I8Panel {
+  uint8_t* A;  // [P][wl][8 chunks][8 slices][128 x 32 UMMA core layout]
+  uint8_t* B;  // [P][wu][2 halves][8 chunks][8 slices][64 x 32]
+  int* ea;     // [P][wl][128] row exponents
+  int* eb;     // [P][wu][128] column exponents
+};
+size_t lu_i8_panel_bytes(const BandGeom& g);  // A + B + exponents, one step pair
+void launch_lu_i8_slice(Ctx* c, cudaStream_t s, const BandGeom& g, const double* tiles, int K,
+                        const I8Panel& pn);
+void launch_lu_i8_gemm(Ctx* c, cudaStream_t s, const BandGeom& g, double* tiles, int K, int kind,
+                       const I8Panel& pn);
 // the look-ahead driver, shared by the real and complex kernels
 struct LuKernels {
   void (*diag)(Ctx*, cudaStream_t, const BandGeom&, void* tiles, int K, int* status);
@@ -54,6 +67,7 @@ struct LuKernels {
   // 3: look-ahead row/column K+2 with steps K, K+1; 4: the rest with steps K, K+1
   void (*gemm)(Ctx*, cudaStream_t, const BandGeom&, void* tiles, int K, int* status, int kind);
   bool pairs = false;
+  const I8Panel* i8 = nullptr;  // [2] (pair parity): kinds 3 / 4 on the INT8 tensor cores
 };
 void run_band_lu(Ctx* c, const BandGeom& g, void* tiles, int Tmax, int* status,
                  const LuKernels& L);

@@ -1,0 +1,517 @@
+// Integer-sliced FP64 trailing update of the band LU on the 5th-generation tensor cores
+// (tcgen05.mma kind::i8, INT8 x INT8 -> INT32 accumulators in TMEM).
+//
+// The two-step update C -= A B of factorize_block (the rank-256 update
+// lu_gemm<3/4> of band_lu.cu computes on DMMA) has A = [L(I,K) L(I,K+1)] (128 x 256) and
+// B = [U(K,J); U(K+1,J)] (256 x 128).  B200 runs FP64 at 37 TF/s but INT8 at 4.5 POPS, so the
+// product is formed exactly in integers (the Ozaki splitting):
+//
+//   row i of A:     a_ik = 2^ea_i * sum_{p=1..8} 2^-7p d_p(i,k),   d_p in [-127, 127]
+//   column j of B:  b_kj = 2^eb_j * sum_{q=1..8} 2^-7q e_q(k,j)
+//   (A B)_ij = 2^(ea_i + eb_j) * sum_{s=2..9} 2^-7s G_s(i,j),   G_s = sum_{p+q=s} D_p E_q
+//
+// with ea_i the binary exponent of max_k |a_ik| (so |a_ik| 2^-ea_i < 1) and each digit the
+// truncation of the running remainder times 2^7 (exact in FP64).  Eight 7-bit digits carry
+// 56 bits, so every entry within 2^-3 of its row (column) maximum is represented exactly;
+// the s <= 9 truncation drops terms below 2^-63 of the row x column scale.  Both errors are
+// of the order of FP64's own rounding bound k u max|a| max|b| for the 256-long products.
+// G_s sums <= 8 products of 256 INT8 pairs: |G_s| <= 8 * 256 * 127^2 < 2^31, exact in INT32.
+//
+// lu_i8_slice (once per step pair, on the critical-path stream): digits of the whole
+// A panel (rows I = K+2 .. K+1+wl) and B panel (columns J = K+2 .. K+1+wu), written in the
+// UMMA shared-memory operand layout (K-major, no swizzle: 8-row x 16-byte core matrices) so
+// one pipeline stage is two contiguous bulk copies.
+//
+// lu_i8_gemm (kinds 3 / 4 of the pair schedule): a warp-specialised kernel per 128 x 128
+// output tile.  The MMA shape is M=128, N=128, K=32 (N < 128 leaves the INT8 pipe at 2/3
+// rate); 4 group accumulators of 128 INT32 columns fill the 512 TMEM columns, so a tile runs
+// two passes over K: pass A forms G_6..G_9 (26 MMAs per K chunk of 32, all 8 + 8 slices),
+// pass B G_2..G_5 (10 MMAs, slices 1-4).  Warp 0 streams the chunks (64 / 32 KB) through a
+// 3-stage TMA ring; warp 1's elected thread issues the MMAs, A slice outer so consecutive
+// MMAs reuse it from the operand collector; warps 2-9 drain each group accumulator into
+// FP64 registers (tcgen05.ld; smallest group first) and release it at once, so the next
+// pass's MMAs refill a group while the others are still being read.  After pass B they
+// subtract 2^(ea+eb) sum_s 2^-7s G_s from C.  Each CTA walks I8_TPC consecutive tiles (same
+// I first, so A slices are shared through L2) and retires, leaving SMs for the high-priority
+// diag / panel kernels of the look-ahead.
+#include <cstdlib>
+
+#include "common.cuh"
+#include "kernels.h"
+#include "lrs_internal.h"
+
+namespace lrs {
+
+constexpr int I8_S = 8;                               // digit slices per operand
+constexpr int I8_KC = 32;                             // K per MMA and per pipeline chunk
+constexpr int I8_NCH = 2 * NB / I8_KC;                // 8 chunks over K = 256
+constexpr int I8_SL = NB * I8_KC;                     // 4096 B: one slice of one chunk
+constexpr int I8_BLK = I8_S * I8_SL;                  // 32 KB: all slices of one chunk
+constexpr int I8_STAGE = 2 * I8_BLK;                  // A + B
+constexpr int I8_STAGES = 3;
+constexpr int I8_GROUPS = 4;                          // accumulators per pass (4 x 128 cols)
+constexpr int I8_THREADS = 320;                       // producer, MMA, 8 epilogue warps
+constexpr int I8_TPC = 4;                             // tiles per CTA
+// LRS_I8_EXP (timing experiments only, wrong results): 1 skips the epilogue arithmetic,
+// 2 also skips the operand copies
+#ifndef LRS_I8_EXP
+#define LRS_I8_EXP 0
+#endif
+constexpr size_t I8_SMEM = (size_t)I8_STAGES * I8_STAGE + 2048;
+
+size_t lu_i8_panel_bytes(const BandGeom& g) {
+  return (size_t)g.P * (g.wl + g.wu) * (I8_NCH * I8_BLK + sizeof(int) * NB);
+}
+
+// ---- tcgen05 helpers ------------------------------------------------------------------
+__device__ __forceinline__ uint64_t umma_sdesc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+  return (uint64_t)((addr >> 4) & 0x3fff) | ((uint64_t)((lbo >> 4) & 0x3fff) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3fff) << 32) | ((uint64_t)1 << 46);  // SWIZZLE_NONE, v1
+}
+// D: s32, A / B: signed int8, K-major, M = N = 128
+constexpr uint32_t I8_IDESC = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(NB >> 3) << 17) |
+                              ((uint32_t)(NB >> 4) << 24);
+// COLL: the A-operand collector -- 0 none, 1 fill (keep A for the next MMA), 2 use + keep,
+// 3 last use.  Consecutive MMAs on one A slice then read it from shared memory once.
+template <int COLL>
+__device__ __forceinline__ void umma_i8(uint32_t d, uint64_t a, uint64_t b, uint32_t acc) {
+#define LRS_UMMA_I8(Q)                                                                     \
+  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"                          \
+               "tcgen05.mma.cta_group::1.kind::i8" Q " [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d), \
+               "l"(a), "l"(b), "r"(I8_IDESC), "r"(acc))
+  if (COLL == 0) LRS_UMMA_I8("");
+  else if (COLL == 1) LRS_UMMA_I8(".collector::a::fill");
+  else if (COLL == 2) LRS_UMMA_I8(".collector::a::use");
+  else LRS_UMMA_I8(".collector::a::lastuse");
+#undef LRS_UMMA_I8
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t* v) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_ld_wait() {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive1(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+// bounded wait: a lost arrival traps (a launch error) instead of hanging the device.
+// SLEEP > 0 backs off between probes so waiting warps leave the shared-memory pipe to the
+// tensor core's operand reads.
+template <int SLEEP = 0>
+__device__ __forceinline__ void mbar_wait_trap(uint64_t* bar, unsigned parity) {
+  uint32_t ok = 0;
+  for (long i = 0;; ++i) {
+    if (SLEEP && i) __nanosleep(SLEEP);
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (ok) return;
+    if (i > (SLEEP ? (1l << 24) : (1l << 28))) __trap();
+  }
+}
+__device__ __forceinline__ void red_add_f64(double* p, double v) {
+  asm volatile("red.relaxed.gpu.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+__device__ __forceinline__ double exp2i(int e) {
+  if (e >= -1022 && e <= 1023) return __longlong_as_double((long long)(e + 1023) << 52);
+  return ldexp(1.0, e);
+}
+
+// eight digits of v in [-1, 1): packed into byte lane `b` of words[q]
+__device__ __forceinline__ void digits8(double v, uint32_t* words, int b) {
+#pragma unroll
+  for (int q = 0; q < I8_S; ++q) {
+    v *= 128.0;
+    const double d = trunc(v);
+    v -= d;
+    words[q] |= (uint32_t)(uint8_t)(int8_t)(int)d << (8 * b);
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// lu_i8_slice: grid (wl + wu, P), 256 threads.  Blocks x < wl slice A tile row I = K+2+x,
+// the others B tile column J = K+2+(x-wl).  Tiles outside the band are zeros.
+// ---------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) lu_i8_slice_kernel(BandGeom g, const double* tiles, int K,
+                                                          I8Panel pn) {
+  __shared__ __align__(16) uint8_t st[I8_BLK];  // 32 KB: one chunk of all slices
+  __shared__ double mx[2][NB];
+  __shared__ int ex[NB];
+  const int p = blockIdx.y, T = g.T[p];
+  const int64_t base = g.tbase[p];
+  auto tile = [&](int I, int J) -> const double* {
+    return tiles + (base + (int64_t)I * g.W + (J - I + g.wl)) * TILE_ELEMS;
+  };
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int x = blockIdx.x;
+  if (x < g.wl) {
+    // ---- A = [L(I,K) L(I,K+1)]: row exponents, then digits (row i, 16 k per thread)
+    const int ia = x, I = K + 2 + ia;
+    if (I >= T) return;
+    const double* t0 = (I - K <= g.wl) ? tile(I, K) : nullptr;
+    const double* t1 = tile(I, K + 1);
+    const int i = tid & (NB - 1), half = tid >> 7;
+    const double* src = half ? t1 : t0;
+    double m = 0.0;
+    if (src)
+      for (int k = 0; k < NB; ++k) m = fmax(m, fabs(src[(int64_t)k * NB + i]));
+    mx[half][i] = m;
+    __syncthreads();
+    if (tid < NB) {
+      const double mm = fmax(mx[0][tid], mx[1][tid]);
+      int e = 0;
+      if (mm > 0.0) frexp(mm, &e);
+      ex[tid] = e;
+      pn.ea[((int64_t)p * g.wl + ia) * NB + tid] = e;
+    }
+    __syncthreads();
+    const double sc = exp2i(-ex[i]);
+    uint8_t* dst = pn.A + ((int64_t)p * g.wl + ia) * I8_NCH * I8_BLK;
+    for (int kc = 0; kc < I8_NCH; ++kc) {
+      const int k0 = kc * I8_KC + 16 * half;  // this thread: k0 .. k0+15 of row i
+      const double* s = k0 < NB ? t0 : t1;
+      uint32_t wd[I8_S][4];
+#pragma unroll
+      for (int q = 0; q < I8_S; ++q) wd[q][0] = wd[q][1] = wd[q][2] = wd[q][3] = 0u;
+#pragma unroll
+      for (int kk = 0; kk < 16; ++kk) {
+        const double v = s ? s[(int64_t)((k0 + kk) & (NB - 1)) * NB + i] * sc : 0.0;
+        uint32_t tmp[I8_S] = {0, 0, 0, 0, 0, 0, 0, 0};
+        digits8(v, tmp, kk & 3);
+#pragma unroll
+        for (int q = 0; q < I8_S; ++q) wd[q][kk >> 2] |= tmp[q];
+      }
+      // core matrix (K-core half, row group i/8), row i%8: 16 contiguous bytes per slice
+      const int off = (half * (NB / 8) + (i >> 3)) * 128 + (i & 7) * 16;
+#pragma unroll
+      for (int q = 0; q < I8_S; ++q)
+        *reinterpret_cast<uint4*>(st + q * I8_SL + off) =
+            make_uint4(wd[q][0], wd[q][1], wd[q][2], wd[q][3]);
+      __syncthreads();
+      const uint4* s4 = reinterpret_cast<const uint4*>(st);
+      uint4* d4 = reinterpret_cast<uint4*>(dst + (int64_t)kc * I8_BLK);
+      for (int e = tid; e < I8_BLK / 16; e += 256) d4[e] = s4[e];
+      __syncthreads();
+    }
+  } else {
+    // ---- B = [U(K,J); U(K+1,J)]: column exponents (warp per column), digits (column j,
+    // 16 k per thread); column j is operand row j of the K-major B
+    const int jb = x - g.wl, J = K + 2 + jb;
+    if (J >= T) return;
+    const double* t0 = (J - K <= g.wu) ? tile(K, J) : nullptr;
+    const double* t1 = tile(K + 1, J);
+    for (int j = w; j < NB; j += 8) {
+      double m = 0.0;
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        if (t0) m = fmax(m, fabs(t0[(int64_t)j * NB + lane + 32 * r]));
+        m = fmax(m, fabs(t1[(int64_t)j * NB + lane + 32 * r]));
+      }
+      m = warp_max(m);
+      if (lane == 0) {
+        int e = 0;
+        if (m > 0.0) frexp(m, &e);
+        ex[j] = e;
+        pn.eb[((int64_t)p * g.wu + jb) * NB + j] = e;
+      }
+    }
+    __syncthreads();
+    const int j = tid >> 1, kh = tid & 1;
+    const double sc = exp2i(-ex[j]);
+    uint8_t* dst = pn.B + ((int64_t)p * g.wu + jb) * I8_NCH * I8_BLK;
+    for (int kc = 0; kc < I8_NCH; ++kc) {
+      const int k0 = kc * I8_KC + 16 * kh;
+      const double* s = k0 < NB ? t0 : t1;
+      uint32_t wd[I8_S][4];
+#pragma unroll
+      for (int q = 0; q < I8_S; ++q) wd[q][0] = wd[q][1] = wd[q][2] = wd[q][3] = 0u;
+#pragma unroll
+      for (int kk = 0; kk < 16; ++kk) {
+        const double v = s ? s[(int64_t)j * NB + ((k0 + kk) & (NB - 1))] * sc : 0.0;
+        uint32_t tmp[I8_S] = {0, 0, 0, 0, 0, 0, 0, 0};
+        digits8(v, tmp, kk & 3);
+#pragma unroll
+        for (int q = 0; q < I8_S; ++q) wd[q][kk >> 2] |= tmp[q];
+      }
+      const int off = (kh * (NB / 8) + (j >> 3)) * 128 + (j & 7) * 16;
+#pragma unroll
+      for (int q = 0; q < I8_S; ++q)
+        *reinterpret_cast<uint4*>(st + off + q * I8_SL) =
+            make_uint4(wd[q][0], wd[q][1], wd[q][2], wd[q][3]);
+      __syncthreads();
+      const uint4* s4 = reinterpret_cast<const uint4*>(st);
+      uint4* d4 = reinterpret_cast<uint4*>(dst + (int64_t)kc * I8_BLK);
+      for (int e = tid; e < I8_BLK / 16; e += 256) d4[e] = s4[e];
+      __syncthreads();
+    }
+  }
+}
+
+// tile t of the kind-3 / kind-4 lists -> (p, ia, jb); false when outside the blocks
+template <int KIND>
+__device__ __forceinline__ bool i8_decode(const BandGeom& g, int K, int t, int& p, int& ia,
+                                          int& jb) {
+  const int per = KIND == 4 ? (g.wl - 2) * (g.wu - 2) : 2 * g.wl + 2 * g.wu - 4;
+  p = t / per;
+  int r = t % per;
+  int I, J;
+  if (KIND == 4) {
+    I = K + 4 + r / (g.wu - 2);
+    J = K + 4 + r % (g.wu - 2);
+  } else if (r < g.wl) {
+    I = K + 2 + r;
+    J = K + 2;
+  } else if ((r -= g.wl) < g.wl - 1) {
+    I = K + 3 + r;
+    J = K + 3;
+  } else if ((r -= g.wl - 1) < g.wu - 1) {
+    I = K + 2;
+    J = K + 3 + r;
+  } else {
+    r -= g.wu - 1;
+    I = K + 3;
+    J = K + 4 + r;
+  }
+  ia = I - K - 2;
+  jb = J - K - 2;
+  const int T = g.T[p];
+  return K + 1 < T && I < T && J < T;
+}
+
+// MMAs of one K chunk of one pass: A slice p outer (collector), B slice q descending, so the
+// first writes of the groups (p = 1) go to slots 3, 2, 1, 0 -- the order the epilogue
+// releases them.  PASS 0 (A): G_6..G_9; PASS 1 (B): G_2..G_5.
+template <int PASS>
+__device__ __forceinline__ void i8_chunk_mmas(uint32_t tm, uint32_t a0, uint32_t b0, bool first,
+                                              uint64_t* tempty, int u) {
+  constexpr int base = PASS == 0 ? 6 : 2;
+  constexpr int pmax = PASS == 0 ? I8_S : 4;
+#pragma unroll
+  for (int pp = 1; pp <= pmax; ++pp) {
+    constexpr int dummy = 0;
+    (void)dummy;
+    const int qhi = min(I8_S, base + 3 - pp), qlo = max(1, base - pp);
+#pragma unroll
+    for (int q = 8; q >= 1; --q) {
+      if (q > qhi || q < qlo) continue;
+      const int slot = pp + q - base;
+      if (first && pp == 1 && u > 0) {
+        mbar_wait_trap(&tempty[slot], (u - 1) & 1);
+        tc_fence_after();
+      }
+      const uint32_t dd = tm + slot * NB;
+      const uint64_t ad = umma_sdesc(a0 + (pp - 1) * I8_SL, NB * 16, 128);
+      const uint64_t bd = umma_sdesc(b0 + (q - 1) * I8_SL, NB * 16, 128);
+      const uint32_t ac = (first && pp == 1) ? 0u : 1u;
+      if (qhi == qlo) umma_i8<0>(dd, ad, bd, ac);
+      else if (q == qhi) umma_i8<1>(dd, ad, bd, ac);
+      else if (q == qlo) umma_i8<3>(dd, ad, bd, ac);
+      else umma_i8<2>(dd, ad, bd, ac);
+    }
+  }
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(I8_THREADS, 1)
+    lu_i8_gemm_kernel(BandGeom g, double* tiles, int K, I8Panel pn, int total) {
+  extern __shared__ __align__(1024) uint8_t smraw[];
+  uint8_t* stage = smraw;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smraw + I8_STAGES * I8_STAGE);
+  uint64_t* empty = full + I8_STAGES;
+  uint64_t* tfull = empty + I8_STAGES;
+  uint64_t* tempty = tfull + 1;  // [I8_GROUPS]: slot drained by the epilogue
+  uint32_t* tbase = reinterpret_cast<uint32_t*>(tempty + I8_GROUPS);
+  double* sj = reinterpret_cast<double*>(smraw + I8_STAGES * I8_STAGE + 1024);  // [128]
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int t0 = blockIdx.x * I8_TPC, t1 = min(total, t0 + I8_TPC);
+  auto ctile = [&](int p, int ia, int jb) -> double* {
+    const int I = K + 2 + ia, J = K + 2 + jb;
+    return tiles + (g.tbase[p] + (int64_t)I * g.W + (J - I + g.wl)) * TILE_ELEMS;
+  };
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < I8_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tfull, 1);
+    for (int gi = 0; gi < I8_GROUPS; ++gi) mbar_init(&tempty[gi], 8);
+    fence_mbar_init();
+  }
+  if (w == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                     smem_u32(tbase))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tm = *tbase;
+
+  if (w == 0) {
+    // ---- producer: per tile, pass A (all slices) then pass B (slices 1-4) ----------------
+    if (lane == 0) {
+      int it = 0;
+      for (int t = t0; t < t1; ++t) {
+        int p, ia, jb;
+        if (!i8_decode<KIND>(g, K, t, p, ia, jb)) continue;
+        bulk_prefetch_l2(ctile(p, ia, jb), sizeof(double) * TILE_ELEMS);
+        const uint8_t* a = pn.A + ((int64_t)p * g.wl + ia) * I8_NCH * I8_BLK;
+        const uint8_t* b = pn.B + ((int64_t)p * g.wu + jb) * I8_NCH * I8_BLK;
+        for (int pass = 0; pass < 2; ++pass) {
+          const unsigned bytes = pass == 0 ? I8_BLK : I8_BLK / 2;
+          for (int kc = 0; kc < I8_NCH; ++kc, ++it) {
+            const int s = it % I8_STAGES;
+            if (it >= I8_STAGES) mbar_wait_trap<64>(&empty[s], ((it / I8_STAGES) & 1) ^ 1);
+            if (LRS_I8_EXP >= 2) {
+              mbar_arrive1(&full[s]);
+              continue;
+            }
+            mbar_expect_tx(&full[s], 2 * bytes);
+            bulk_g2s(stage + s * I8_STAGE, a + kc * I8_BLK, bytes, &full[s]);
+            bulk_g2s(stage + s * I8_STAGE + I8_BLK, b + kc * I8_BLK, bytes, &full[s]);
+          }
+        }
+      }
+    }
+  } else if (w == 1) {
+    // ---- MMA issuer ------------------------------------------------------------------
+    if (lane == 0) {
+      int it = 0, u = 0;
+      for (int t = t0; t < t1; ++t) {
+        int p, ia, jb;
+        if (!i8_decode<KIND>(g, K, t, p, ia, jb)) continue;
+        for (int pass = 0; pass < 2; ++pass, ++u) {
+          for (int kc = 0; kc < I8_NCH; ++kc, ++it) {
+            const int s = it % I8_STAGES;
+            mbar_wait_trap(&full[s], (it / I8_STAGES) & 1);
+            tc_fence_after();
+            const uint32_t a0 = smem_u32(stage + s * I8_STAGE), b0 = a0 + I8_BLK;
+            if (pass == 0) i8_chunk_mmas<0>(tm, a0, b0, kc == 0, tempty, u);
+            else i8_chunk_mmas<1>(tm, a0, b0, kc == 0, tempty, u);
+            umma_commit(&empty[s]);
+          }
+          umma_commit(tfull);
+        }
+      }
+    }
+  } else {
+    // ---- epilogue: warp w drains TMEM lanes 32 (w % 4).. (rows) and column half
+    // (w - 2) / 4 of every slot.  INT32 -> FP64 by the exponent trick (2^52 + 2^31 + x is
+    // exact), so a conversion is an xor and an FP64 add instead of an XU I2F.
+    const int qd = w & 3, ch = (w - 2) >> 2, i = 32 * qd + lane;
+    constexpr double BIAS = 4503601774854144.0;  // 2^52 + 2^31
+    int u = 0;
+    for (int t = t0; t < t1; ++t) {
+      int p, ia, jb;
+      if (!i8_decode<KIND>(g, K, t, p, ia, jb)) continue;
+      double* C = ctile(p, ia, jb) + (int64_t)ch * 64 * NB;
+      const double si = exp2i(pn.ea[((int64_t)p * g.wl + ia) * NB + i]);
+      if (w == 2) {  // the previous tile's readers of sj passed the closing barrier
+        const int* eb = pn.eb + ((int64_t)p * g.wu + jb) * NB;
+#pragma unroll
+        for (int r = 0; r < 4; ++r) sj[lane + 32 * r] = exp2i(eb[lane + 32 * r]);
+      }
+      const uint32_t trow = tm + ((uint32_t)(32 * qd) << 16) + ch * 64;
+      double acc[64];
+#pragma unroll
+      for (int j = 0; j < 64; ++j) acc[j] = 0.0;
+#pragma unroll
+      for (int pass = 0; pass < 2; ++pass, ++u) {
+        mbar_wait_trap<128>(tfull, u & 1);
+        tc_fence_after();
+        if (LRS_I8_EXP == 3) {
+          __syncwarp();
+          if (lane == 0)
+            for (int slot = 0; slot < I8_GROUPS; ++slot) mbar_arrive1(&tempty[slot]);
+          continue;
+        }
+#pragma unroll
+        for (int slot = I8_GROUPS - 1; slot >= 0; --slot) {
+          const double sc = exp2i(-7 * (slot + (pass == 0 ? 6 : 2)));
+#pragma unroll
+          for (int h2 = 0; h2 < 2; ++h2) {
+            uint32_t v[32];
+#pragma unroll
+            for (int c8 = 0; c8 < 32; c8 += 8) tmem_ld8(trow + slot * NB + h2 * 32 + c8, v + c8);
+            tmem_ld_wait();
+            if (h2 == 1) {  // this warp's part of the slot is in registers: release it
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive1(&tempty[slot]);
+            }
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              acc[h2 * 32 + j] = fma(
+                  __hiloint2double(0x43300000, (int)(v[j] ^ 0x80000000u)) - BIAS, sc,
+                  acc[h2 * 32 + j]);
+          }
+        }
+      }
+      asm volatile("bar.sync 1, 256;" ::: "memory");  // sj written
+      // C -= 2^(ea+eb) acc as fire-and-forget L2 reductions: no load round trip in the
+      // epilogue, and with one contribution per element fl(c + (-r)) == fl(c - r) exactly
+      if (!LRS_I8_EXP) {
+#pragma unroll
+        for (int j = 0; j < 64; ++j)
+          red_add_f64(C + (int64_t)j * NB + i, -(acc[j] * si * sj[ch * 64 + j]));
+      }
+      asm volatile("bar.sync 1, 256;" ::: "memory");  // sj free for the next tile
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (w == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tm) : "memory");
+  }
+}
+
+void launch_lu_i8_slice(Ctx* c, cudaStream_t s, const BandGeom& g, const double* tiles, int K,
+                        const I8Panel& pn) {
+  lu_i8_slice_kernel<<<dim3(g.wl + g.wu, g.P), 256, 0, s>>>(g, tiles, K, pn);
+  LRS_LAUNCHED(c);
+}
+
+void launch_lu_i8_gemm(Ctx* c, cudaStream_t s, const BandGeom& g, double* tiles, int K, int kind,
+                       const I8Panel& pn) {
+  static bool attr = false;
+  if (!attr) {
+    LRS_CUDA(cudaFuncSetAttribute(lu_i8_gemm_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)I8_SMEM));
+    LRS_CUDA(cudaFuncSetAttribute(lu_i8_gemm_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)I8_SMEM));
+    attr = true;
+  }
+  const int per = kind == 4 ? (g.wl - 2) * (g.wu - 2) : 2 * g.wl + 2 * g.wu - 4;
+  const int total = per * g.P;
+  const int grid = (total + I8_TPC - 1) / I8_TPC;
+  if (total <= 0) return;
+  if (kind == 4)
+    lu_i8_gemm_kernel<4><<<grid, I8_THREADS, I8_SMEM, s>>>(g, tiles, K, pn, total);
+  else
+    lu_i8_gemm_kernel<3><<<grid, I8_THREADS, I8_SMEM, s>>>(g, tiles, K, pn, total);
+  LRS_LAUNCHED(c);
+}
+
+}  // namespace lrs
