@@ -12,9 +12,12 @@ preconditioned BiCGStab solve.  metric = time-to-tolerance in seconds
   e2e         the same step through the public C-ABI with HOST buffers: CSR
               upload (validate + transpose + H2D), factorize, solve with a host
               RHS, x copied back -- host<->device copies inside the timed region
-  roofline    dominant kernel = the DMMA trailing-update GEMM of the band LU
-              (FP64 tensor-core bound), from per-launch CUDA events in the timed
-              region; roofline_apply = the HBM-bound preconditioner apply
+  roofline    dominant kernel = the two-step trailing update of the band LU: the
+              INT8-sliced tcgen05 kernel lu_i8_gemm<4> (INT8 tensor-core bound, its
+              int8 ops against the in-run INT8 peak; fp64_equiv = the algorithmic
+              FP64 flops it retires against the DMMA peak), or the DMMA GEMM when the
+              INT8 path is off; per-launch CUDA events in the timed region;
+              roofline_apply = the HBM-bound preconditioner apply
   cpu_baseline the oracle port (scipy/OpenBLAS dgbtrf/dgbtrs) on a bounded
               sample of the same blocks, extrapolated by the algorithmic work
 
@@ -232,6 +235,7 @@ def run_ours(args):
     b_dev = torch.from_numpy(np.asfortranarray(cfg.rhs)).cuda()
     x_dev = torch.empty_like(b_dev)
     dmma_peak = ctx.dmma_peak_tflops()
+    i8_peak = ctx.i8_peak_tops()
 
     def make_fact(Amat):
         if comm is None:
@@ -321,6 +325,36 @@ def run_ours(args):
     if napply:
         apply_ms_each = (kt["band_solve"][0] + kt["iface_apply"][0] + kt["recovery"][0]) / 1.0
     total_ms = sum(v[0] for v in kt.values())
+    if info.get("lu_int8"):
+        # INT8 ops the launch issues: 36 digit-slice products (M = N = 128, K = 256) per
+        # 128 x 128 tile of the bulk update
+        tiles = sum(_i8_bulk_tiles(s, info["wl"], info["wu"], info["nb"])
+                    for s in _partition_sizes(cfg.matrix.n, cfg.P))
+        ops_launch = tiles * args.steps * 2.0 * 128 * 128 * 256 * 36 / max(upd_n, 1)
+        achieved_tops = ops_launch / avg_launch_s / 1e12 if upd_n else 0.0
+        roofline = {"bound": "tensor",
+                    "kernel": "lu_i8_gemm_kernel<4> (INT8-sliced FP64 two-step trailing update, "
+                              "tcgen05.mma kind::i8)",
+                    "achieved": achieved_tops, "peak": i8_peak, "unit": "TOPS (int8)",
+                    "frac": achieved_tops / i8_peak if i8_peak else None,
+                    "peak_source": "in-run INT8 tcgen05 microbenchmark (M=128, N=256, resident "
+                                   "operands); nominal dense 4.5 POPS",
+                    "traffic": None, "launches": int(upd_n), "avg_launch_ms": avg_launch_s * 1e3,
+                    "int8_ops_per_launch": ops_launch,
+                    "fp64_equiv": {"achieved": achieved_tf, "unit": "TFLOP/s",
+                                   "dmma_peak": dmma_peak,
+                                   "ratio_to_dmma_peak": achieved_tf / dmma_peak if dmma_peak else None,
+                                   "flops_per_launch": per_launch_flops}}
+    else:
+        roofline = {"bound": "tensor",
+                    "kernel": ("lu_gemm_kernel<4> (two-step DMMA trailing update)"
+                               if info.get("lu_pairs") else "lu_gemm_kernel<1> (DMMA trailing update)"),
+                    "achieved": achieved_tf, "peak": dmma_peak, "unit": "TFLOP/s",
+                    "frac": achieved_tf / dmma_peak if dmma_peak else None,
+                    "peak_source": "in-run FP64 DMMA microbenchmark (MEASURED_PEAKS.json has no FP64); "
+                                   "nominal 148 SM x 64 FMA x 2 x 1.965 GHz = 37.2",
+                    "traffic": None, "launches": int(upd_n), "avg_launch_ms": avg_launch_s * 1e3,
+                    "flops_per_launch": per_launch_flops}
     line = {
         "metric": "preconditioned solve time-to-tolerance (s)",
         "value": value, "unit": "s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
@@ -339,15 +373,7 @@ def run_ours(args):
         "t_solve_s": reps[-1].wall_time,
         "e2e": {"value": e2e, "unit": "s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
         "gpu_launches": int(launches),
-        "roofline": {"bound": "tensor",
-                     "kernel": ("lu_gemm_kernel<4> (two-step DMMA trailing update)"
-                                if info.get("lu_pairs") else "lu_gemm_kernel<1> (DMMA trailing update)"),
-                     "achieved": achieved_tf, "peak": dmma_peak, "unit": "TFLOP/s",
-                     "frac": achieved_tf / dmma_peak if dmma_peak else None,
-                     "peak_source": "in-run FP64 DMMA microbenchmark (MEASURED_PEAKS.json has no FP64); "
-                                    "nominal 148 SM x 64 FMA x 2 x 1.965 GHz = 37.2",
-                     "traffic": None, "launches": int(upd_n), "avg_launch_ms": avg_launch_s * 1e3,
-                     "flops_per_launch": per_launch_flops},
+        "roofline": roofline,
         "roofline_lu_all": {"achieved": info["lu_flops"] / info["t_lu"] / 1e12, "unit": "TFLOP/s",
                             "frac": info["lu_flops"] / info["t_lu"] / 1e12 / dmma_peak},
         "roofline_apply": _apply_roofline(kt, reps, info, hbm_peak, peak_src, args.steps),
@@ -380,6 +406,17 @@ def _rest_update_flops(s, kl, ku, nb=128, pairs=False):
     ni = np.clip(np.minimum(j + kl, s - 1) - np.maximum(j + 1, lo) + 1, 0, None).astype(np.float64)
     nc = np.clip(np.minimum(j + ku, s - 1) - np.maximum(j + 1, lo) + 1, 0, None).astype(np.float64)
     return float(2.0 * np.sum(ni * nc))
+
+
+def _i8_bulk_tiles(s, wl, wu, nb=128):
+    """128 x 128 tiles of the INT8 bulk launches (I, J >= K + 4 of each pair (K, K + 1))."""
+    T = -(-s // nb)
+    tot = 0
+    for K in range(0, T - 1, 2):
+        ni = max(0, min(K + 1 + wl, T - 1) - (K + 4) + 1)
+        nj = max(0, min(K + 1 + wu, T - 1) - (K + 4) + 1)
+        tot += ni * nj
+    return tot
 
 
 def _partition_sizes(n, P):

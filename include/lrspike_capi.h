@@ -153,6 +153,7 @@ typedef struct lrs_fact_info {
   double max_interface_cond;
   int32_t lu_pairs;             /* bulk LU updates ran two steps (rank 256) per launch */
   int32_t pivoted;              /* some block needed row interchanges: partial-pivoting LU */
+  int32_t lu_int8;              /* two-step updates ran INT8-sliced on tcgen05 (LRS_LU_I8) */
 } lrs_fact_info;
 
 typedef struct lrs_error_info {
@@ -286,6 +287,9 @@ LRS_API lrs_status lrs_factorize_dist(lrs_ctx* ctx, lrs_mat* a, const lrs_solver
 /* ---- microbenchmarks used by bench.py for the roofline denominators --------------- */
 /* FP64 DMMA peak: runs a register-resident mma.sync f64 loop, returns TFLOP/s. */
 LRS_API lrs_status lrs_bench_dmma_peak(lrs_ctx* ctx, double* tflops);
+/* INT8 tensor-core peak: tcgen05.mma kind::i8 (M=128, N=256) from resident shared-memory
+   operands on every SM, returns dense TOPS (the roofline denominator of lu_i8_gemm). */
+LRS_API lrs_status lrs_bench_i8_peak(lrs_ctx* ctx, double* tops);
 
 #ifdef __cplusplus
 }

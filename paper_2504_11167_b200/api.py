@@ -69,7 +69,7 @@ class FactInfoC(ctypes.Structure):
                 ("lu_flops", i64), ("apply_bytes", i64), ("rank_collapsed", i32),
                 ("variant", i32), ("t_factorize", f64), ("t_lu", f64), ("t_spikes", f64),
                 ("t_precond", f64), ("max_interface_cond", f64), ("lu_pairs", i32),
-                ("pivoted", i32)]
+                ("pivoted", i32), ("lu_int8", i32)]
 
 
 _OPFN = ctypes.CFUNCTYPE(i32, vp, vp, vp, i64, i64)
@@ -199,6 +199,7 @@ def lib():
         "lrs_reduced_apply": (i32, [vp, i32, vp, i64, vp, i64, i64, i32]),
         "lrs_solve": (i32, [vp, vp, vp, i64, vp, i64, i64, P(IterCfgC), P(ReportC), i32]),
         "lrs_bench_dmma_peak": (i32, [vp, P(f64)]),
+        "lrs_bench_i8_peak": (i32, [vp, P(f64)]),
         "lrs_krylov": (i32, [vp, i64, i32, P(OperatorC), P(OperatorC), vp, i64, vp, i64, i64,
                              P(IterCfgC), P(ReportC), i32]),
         "lrs_ctx_set_profiling": (i32, [vp, i32]),
@@ -315,6 +316,11 @@ class Context:
     def dmma_peak_tflops(self) -> float:
         out = f64()
         _check(lib().lrs_bench_dmma_peak(self.h, ctypes.byref(out)), self.h)
+        return out.value
+
+    def i8_peak_tops(self) -> float:
+        out = f64()
+        _check(lib().lrs_bench_i8_peak(self.h, ctypes.byref(out)), self.h)
         return out.value
 
 

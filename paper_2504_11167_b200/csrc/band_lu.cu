@@ -674,7 +674,7 @@ static bool lu_i8_wanted(const BandGeom& g, const LuKernels& L) {
   return 2 * lu_i8_panel_bytes(g) < fr / 4;
 }
 
-void launch_band_lu(Ctx* c, const BandGeom& g, double* tiles, int Tmax, int* status) {
+bool launch_band_lu(Ctx* c, const BandGeom& g, double* tiles, int Tmax, int* status) {
   lu_attrs();
   LuKernels L{real_diag, real_gemm, LRS_LU_PAIRS != 0};
   DevBuf<uint8_t> buf;
@@ -696,6 +696,7 @@ void launch_band_lu(Ctx* c, const BandGeom& g, double* tiles, int Tmax, int* sta
     L.i8 = pn;
   }
   run_band_lu(c, g, tiles, Tmax, status, L);
+  return L.i8 != nullptr;
 }
 
 // Right-looking tiled LU with look-ahead depth 1 over two streams:

@@ -668,4 +668,9 @@ lrs_status lrs_bench_dmma_peak(lrs_ctx* c, double* tflops) {
   return guard(c, [&] { *tflops = run_dmma_peak(c); });
 }
 
+lrs_status lrs_bench_i8_peak(lrs_ctx* c, double* tops) {
+  if (!c || !tops) return LRS_ERR_PARAMETER;
+  return guard(c, [&] { *tops = run_i8_peak(c); });
+}
+
 }  // extern "C"

@@ -45,7 +45,8 @@ void launch_extract_tiles(Ctx* c, const Mat* m, const BandGeom& g, double* tiles
                           int64_t row_lo, int64_t row_hi, unsigned long long* d_bad);
 // Tiled no-pivot band LU of all partitions (Tmax steps, look-ahead over two streams).
 // status[2p] = min column needing a row interchange, status[2p+1] = min zero-pivot column.
-void launch_band_lu(Ctx* c, const BandGeom& g, double* tiles, int Tmax, int* status);
+// returns true when the two-step updates ran INT8-sliced on the tensor cores (lu_i8.cu)
+bool launch_band_lu(Ctx* c, const BandGeom& g, double* tiles, int Tmax, int* status);
 void launch_band_lu_z(Ctx* c, const BandGeom& g, zc* tiles, int Tmax, int* status);
 // integer-sliced (INT8 tensor core) two-step trailing update, lu_i8.cu: digit slices of one
 // step pair's A panel (rows K+2..K+1+wl) and B panel (columns K+2..K+1+wu)
@@ -238,5 +239,6 @@ void launch_csr_transpose(Ctx* c, Mat* m);
 
 // ---- bench ---------------------------------------------------------------------------
 double run_dmma_peak(Ctx* c);
+double run_i8_peak(Ctx* c);  // lu_i8.cu: dense INT8 tcgen05 TOPS
 
 }  // namespace lrs

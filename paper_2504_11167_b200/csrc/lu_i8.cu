@@ -487,6 +487,82 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
   }
 }
 
+// ---- INT8 peak (roofline denominator): every SM issues M=128, N=256, K=32 MMAs from
+// resident operands into 2 accumulators (the best-rate shape), 8 K-steps each
+__global__ void __launch_bounds__(128, 1) i8_peak_kernel(int iters, int* out) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tb;
+  constexpr int N = 256, KK = 256;
+  constexpr uint32_t ID = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) |
+                          ((uint32_t)(NB >> 4) << 24);
+  const int w = threadIdx.x >> 5;
+  for (int e = threadIdx.x; e < (NB + N) * KK; e += blockDim.x) sm[e] = (uint8_t)((e * 7) & 63);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+  }
+  if (w == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                     smem_u32(&tb))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tm = tb;
+  if (threadIdx.x == 0) {
+    const uint32_t a0 = smem_u32(sm), b0 = a0 + NB * KK;
+    for (int it = 0; it < iters; ++it)
+      for (int a = 0; a < 2; ++a)
+        for (int k = 0; k < KK / 32; ++k)
+          asm volatile(
+              "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+              "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tm + a * N),
+              "l"(umma_sdesc(a0 + 2 * k * NB * 16, NB * 16, 128)),
+              "l"(umma_sdesc(b0 + 2 * k * N * 16, N * 16, 128)), "r"(ID),
+              "r"((uint32_t)(it + k > 0)));
+    umma_commit(&bar);
+  }
+  mbar_wait_trap<64>(&bar, 0);
+  tc_fence_after();
+  uint32_t v[8];
+  tmem_ld8(tm + ((uint32_t)(32 * w) << 16), v);
+  tmem_ld_wait();
+  if (v[0] == 12345u) out[threadIdx.x] = (int)v[1];
+  tc_fence_before();
+  __syncthreads();
+  if (w == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tm) : "memory");
+  }
+}
+
+double run_i8_peak(Ctx* c) {
+  constexpr int smem = (NB + 256) * 256;
+  LRS_CUDA(cudaFuncSetAttribute(i8_peak_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  int* out = nullptr;
+  LRS_CUDA(cudaMalloc(&out, 4096));
+  cudaEvent_t e0, e1;
+  LRS_CUDA(cudaEventCreate(&e0));
+  LRS_CUDA(cudaEventCreate(&e1));
+  const int iters = 2048;
+  i8_peak_kernel<<<c->num_sms, 128, smem, c->stream>>>(8, out);
+  LRS_CUDA(cudaEventRecord(e0, c->stream));
+  i8_peak_kernel<<<c->num_sms, 128, smem, c->stream>>>(iters, out);
+  LRS_CUDA(cudaEventRecord(e1, c->stream));
+  LRS_CUDA(cudaEventSynchronize(e1));
+  float ms = 0.f;
+  LRS_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+  LRS_CUDA(cudaEventDestroy(e0));
+  LRS_CUDA(cudaEventDestroy(e1));
+  LRS_CUDA(cudaFree(out));
+  const double ops = 2.0 * NB * 256 * 256 * 2.0 * iters * c->num_sms;
+  return ops / (ms * 1e-3) / 1e12;
+}
+
 void launch_lu_i8_slice(Ctx* c, cudaStream_t s, const BandGeom& g, const double* tiles, int K,
                         const I8Panel& pn) {
   lu_i8_slice_kernel<<<dim3(g.wl + g.wu, g.P), 256, 0, s>>>(g, tiles, K, pn);

@@ -834,7 +834,7 @@ Fact* factorize(Ctx* c, Mat* m, const lrs_solver_cfg& cfg, const lrs_comm* comm)
                                 f->p0 + P, f->k, l0);
   }
   if (cplx) launch_band_lu_z(c, g, sp<zc>(f->tiles), f->Tmax, f->status.get());
-  else launch_band_lu(c, g, f->tiles.get(), f->Tmax, f->status.get());
+  else f->lu_int8 = launch_band_lu(c, g, f->tiles.get(), f->Tmax, f->status.get());
   // first (global block, column) needing a row interchange / holding an exact zero pivot,
   // agreed over all ranks
   auto first_problem = [&](int which) {
@@ -948,6 +948,7 @@ Fact* factorize(Ctx* c, Mat* m, const lrs_solver_cfg& cfg, const lrs_comm* comm)
   in.variant = f->variant;
   in.lu_pairs = (cplx || f->pivoted) ? 0 : (lu_real_pairs(g) ? 1 : 0);
   in.pivoted = f->pivoted ? 1 : 0;
+  in.lu_int8 = f->lu_int8 ? 1 : 0;
   in.t_lu = elapsed_ms(e0, e1) * 1e-3;
   in.t_spikes = elapsed_ms(e1, e2) * 1e-3;
   in.t_precond = 0.0;
