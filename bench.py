@@ -339,7 +339,10 @@ def run_ours(args):
                     "frac": achieved_tops / i8_peak if i8_peak else None,
                     "peak_source": "in-run INT8 tcgen05 microbenchmark (M=128, N=256, resident "
                                    "operands); nominal dense 4.5 POPS",
-                    "traffic": None, "launches": int(upd_n), "avg_launch_ms": avg_launch_s * 1e3,
+                    # DRAM read + write of one launch from `ncu --set full`
+                    # (profiles/r01b_ncu_lu_i8_gemm.txt): the C tiles' read-modify-write
+                    "traffic": 1.996e9, "traffic_source": "profiles/r01b_ncu_lu_i8_gemm.txt",
+                    "launches": int(upd_n), "avg_launch_ms": avg_launch_s * 1e3,
                     "int8_ops_per_launch": ops_launch,
                     "fp64_equiv": {"achieved": achieved_tf, "unit": "TFLOP/s",
                                    "dmma_peak": dmma_peak,
