@@ -17,10 +17,10 @@
 // of the order of FP64's own rounding bound k u max|a| max|b| for the 256-long products.
 // G_s sums <= 8 products of 256 INT8 pairs: |G_s| <= 8 * 256 * 127^2 < 2^31, exact in INT32.
 //
-// lu_i8_slice (once per step pair, on the critical-path stream): digits of the whole
-// A panel (rows I = K+2 .. K+1+wl) and B panel (columns J = K+2 .. K+1+wu), written in the
-// UMMA shared-memory operand layout (K-major, no swizzle: 8-row x 16-byte core matrices) so
-// one pipeline stage is two contiguous bulk copies.
+// lu_i8_slice (once per step pair, on the critical-path stream): exponents and digits of
+// the whole A panel (rows I = K+2 .. K+1+wl) and B panel (columns J = K+2 .. K+1+wu),
+// written in the UMMA shared-memory operand layout (K-major, no swizzle: 8-row x 16-byte
+// core matrices) so one pipeline stage is two contiguous bulk copies.
 //
 // lu_i8_gemm (kinds 3 / 4 of the pair schedule): a warp-specialised kernel per 128 x 128
 // output tile.  The MMA shape is M=128, N=128, K=32 (N < 128 leaves the INT8 pipe at 2/3
@@ -137,133 +137,110 @@ __device__ __forceinline__ double exp2i(int e) {
   return ldexp(1.0, e);
 }
 
-// eight digits of v in [-1, 1): packed into byte lane `b` of words[q]
-__device__ __forceinline__ void digits8(double v, uint32_t* words, int b) {
+// the eight 7-bit digits of x 2^-e (|x| < 2^e), sign-magnitude, straight from the bits:
+// F = |x| 2^(56 - e) is an integer (< 2^56, low bits truncated), digit p is bits
+// [56 - 7p, 63 - 7p) of F -- the digits of the exact FP64 recurrence v <- 128 v - trunc(128 v),
+// in integer ops
+__device__ __forceinline__ void digits8_bits(double x, int e, uint32_t* words, int b) {
+  const unsigned long long bits = (unsigned long long)__double_as_longlong(x);
+  const int bex = (int)((bits >> 52) & 0x7ff);
+  unsigned long long mant = bits & 0xfffffffffffffull;
+  int ex = bex;
+  if (bex == 0) ex = 1;
+  else mant |= 1ull << 52;
+  const int sh = ex - 1019 - e;  // F = mant * 2^sh
+  unsigned long long F = 0;
+  if (mant != 0 && sh > -64) F = sh >= 0 ? mant << sh : mant >> (-sh);
+  const bool neg = (bits >> 63) != 0;
 #pragma unroll
   for (int q = 0; q < I8_S; ++q) {
-    v *= 128.0;
-    const double d = trunc(v);
-    v -= d;
-    words[q] |= (uint32_t)(uint8_t)(int8_t)(int)d << (8 * b);
+    int d = (int)((F >> (49 - 7 * q)) & 127u);
+    d = neg ? -d : d;
+    words[q] |= (uint32_t)(uint8_t)(int8_t)d << (8 * b);
   }
 }
 
+}
+
 // ---------------------------------------------------------------------------------------
-// lu_i8_slice: grid (wl + wu, P), 256 threads.  Blocks x < wl slice A tile row I = K+2+x,
-// the others B tile column J = K+2+(x-wl).  Tiles outside the band are zeros.
+// lu_i8_slice: grid (wl + wu, 4, P), 256 threads.  Blocks x < wl slice 32 rows (y) of the A
+// tile row I = K+2+x, the others 32 columns of the B tile column J = K+2+(x-wl); tiles
+// outside the band are zeros.  Thread (line = tid % 32, chunk = tid / 32): the line's
+// maximum over its 32 K values of the chunk (then over the 8 chunks in shared memory), then
+// the chunk's eight digit slices, two 16-byte K-core rows per slice stored straight into the
+// core-matrix layout (a warp writes 512 contiguous bytes per slice and K-core).
 // ---------------------------------------------------------------------------------------
+constexpr int I8_SLICE_SPLIT = 4;  // CTAs per tile (32 rows / columns each)
+
 __global__ void __launch_bounds__(256) lu_i8_slice_kernel(BandGeom g, const double* tiles, int K,
                                                           I8Panel pn) {
-  __shared__ __align__(16) uint8_t st[I8_BLK];  // 32 KB: one chunk of all slices
-  __shared__ double mx[2][NB];
-  __shared__ int ex[NB];
-  const int p = blockIdx.y, T = g.T[p];
+  __shared__ double mx[I8_NCH][32];
+  const int p = blockIdx.z, T = g.T[p];
   const int64_t base = g.tbase[p];
   auto tile = [&](int I, int J) -> const double* {
     return tiles + (base + (int64_t)I * g.W + (J - I + g.wl)) * TILE_ELEMS;
   };
-  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int tid = threadIdx.x, ln = tid & 31, kc = tid >> 5;
+  const int line = 32 * blockIdx.y + ln;  // A: row i, B: column j of the tile
   const int x = blockIdx.x;
-  if (x < g.wl) {
-    // ---- A = [L(I,K) L(I,K+1)]: row exponents, then digits (row i, 16 k per thread)
-    const int ia = x, I = K + 2 + ia;
-    if (I >= T) return;
-    const double* t0 = (I - K <= g.wl) ? tile(I, K) : nullptr;
-    const double* t1 = tile(I, K + 1);
-    const int i = tid & (NB - 1), half = tid >> 7;
-    const double* src = half ? t1 : t0;
-    double m = 0.0;
-    if (src)
-      for (int k = 0; k < NB; ++k) m = fmax(m, fabs(src[(int64_t)k * NB + i]));
-    mx[half][i] = m;
-    __syncthreads();
-    if (tid < NB) {
-      const double mm = fmax(mx[0][tid], mx[1][tid]);
-      int e = 0;
-      if (mm > 0.0) frexp(mm, &e);
-      ex[tid] = e;
-      pn.ea[((int64_t)p * g.wl + ia) * NB + tid] = e;
-    }
-    __syncthreads();
-    const double sc = exp2i(-ex[i]);
-    uint8_t* dst = pn.A + ((int64_t)p * g.wl + ia) * I8_NCH * I8_BLK;
-    for (int kc = 0; kc < I8_NCH; ++kc) {
-      const int k0 = kc * I8_KC + 16 * half;  // this thread: k0 .. k0+15 of row i
-      const double* s = k0 < NB ? t0 : t1;
-      uint32_t wd[I8_S][4];
-#pragma unroll
-      for (int q = 0; q < I8_S; ++q) wd[q][0] = wd[q][1] = wd[q][2] = wd[q][3] = 0u;
-#pragma unroll
-      for (int kk = 0; kk < 16; ++kk) {
-        const double v = s ? s[(int64_t)((k0 + kk) & (NB - 1)) * NB + i] * sc : 0.0;
-        uint32_t tmp[I8_S] = {0, 0, 0, 0, 0, 0, 0, 0};
-        digits8(v, tmp, kk & 3);
-#pragma unroll
-        for (int q = 0; q < I8_S; ++q) wd[q][kk >> 2] |= tmp[q];
-      }
-      // core matrix (K-core half, row group i/8), row i%8: 16 contiguous bytes per slice
-      const int off = (half * (NB / 8) + (i >> 3)) * 128 + (i & 7) * 16;
-#pragma unroll
-      for (int q = 0; q < I8_S; ++q)
-        *reinterpret_cast<uint4*>(st + q * I8_SL + off) =
-            make_uint4(wd[q][0], wd[q][1], wd[q][2], wd[q][3]);
-      __syncthreads();
-      const uint4* s4 = reinterpret_cast<const uint4*>(st);
-      uint4* d4 = reinterpret_cast<uint4*>(dst + (int64_t)kc * I8_BLK);
-      for (int e = tid; e < I8_BLK / 16; e += 256) d4[e] = s4[e];
-      __syncthreads();
-    }
+  const bool isA = x < g.wl;
+  const int idx = isA ? x : x - g.wl;
+  const int IJ = K + 2 + idx;
+  if (IJ >= T) return;
+  const double* t0;
+  const double* t1;
+  if (isA) {
+    t0 = (IJ - K <= g.wl) ? tile(IJ, K) : nullptr;
+    t1 = tile(IJ, K + 1);
   } else {
-    // ---- B = [U(K,J); U(K+1,J)]: column exponents (warp per column), digits (column j,
-    // 16 k per thread); column j is operand row j of the K-major B
-    const int jb = x - g.wl, J = K + 2 + jb;
-    if (J >= T) return;
-    const double* t0 = (J - K <= g.wu) ? tile(K, J) : nullptr;
-    const double* t1 = tile(K + 1, J);
-    for (int j = w; j < NB; j += 8) {
-      double m = 0.0;
+    t0 = (IJ - K <= g.wu) ? tile(K, IJ) : nullptr;
+    t1 = tile(K + 1, IJ);
+  }
+  // the 32 K values k0 .. k0+31 of this line: A reads a column-major tile along its row
+  // (stride 128), B reads a column (contiguous)
+  const int k0 = kc * I8_KC;
+  const double* src = k0 < NB ? t0 : t1;
+  double v[32];
 #pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        if (t0) m = fmax(m, fabs(t0[(int64_t)j * NB + lane + 32 * r]));
-        m = fmax(m, fabs(t1[(int64_t)j * NB + lane + 32 * r]));
-      }
-      m = warp_max(m);
-      if (lane == 0) {
-        int e = 0;
-        if (m > 0.0) frexp(m, &e);
-        ex[j] = e;
-        pn.eb[((int64_t)p * g.wu + jb) * NB + j] = e;
-      }
+  for (int kk = 0; kk < 32; ++kk) {
+    const int k = (k0 + kk) & (NB - 1);
+    v[kk] = src ? (isA ? __ldcg(src + (int64_t)k * NB + line) : __ldcg(src + (int64_t)line * NB + k))
+                : 0.0;
+  }
+  double m = 0.0;
+#pragma unroll
+  for (int kk = 0; kk < 32; ++kk) m = fmax(m, fabs(v[kk]));
+  mx[kc][ln] = m;
+  __syncthreads();
+  m = mx[0][ln];
+#pragma unroll
+  for (int c = 1; c < I8_NCH; ++c) m = fmax(m, mx[c][ln]);
+  int e = 0;
+  if (m > 0.0) frexp(m, &e);
+  if (kc == 0) {
+    int* ex = isA ? pn.ea + ((int64_t)p * g.wl + idx) * NB : pn.eb + ((int64_t)p * g.wu + idx) * NB;
+    ex[line] = e;
+  }
+  uint8_t* dst = (isA ? pn.A + ((int64_t)p * g.wl + idx) * I8_NCH * I8_BLK
+                      : pn.B + ((int64_t)p * g.wu + idx) * I8_NCH * I8_BLK) +
+                 (int64_t)kc * I8_BLK;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {  // K-core: k0 + 16h .. k0 + 16h + 15
+    uint32_t wd[I8_S][4];
+#pragma unroll
+    for (int q = 0; q < I8_S; ++q) wd[q][0] = wd[q][1] = wd[q][2] = wd[q][3] = 0u;
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) {
+      uint32_t tmp[I8_S] = {0, 0, 0, 0, 0, 0, 0, 0};
+      digits8_bits(v[16 * h + kk], e, tmp, kk & 3);
+#pragma unroll
+      for (int q = 0; q < I8_S; ++q) wd[q][kk >> 2] |= tmp[q];
     }
-    __syncthreads();
-    const int j = tid >> 1, kh = tid & 1;
-    const double sc = exp2i(-ex[j]);
-    uint8_t* dst = pn.B + ((int64_t)p * g.wu + jb) * I8_NCH * I8_BLK;
-    for (int kc = 0; kc < I8_NCH; ++kc) {
-      const int k0 = kc * I8_KC + 16 * kh;
-      const double* s = k0 < NB ? t0 : t1;
-      uint32_t wd[I8_S][4];
+    const int off = (h * (NB / 8) + (line >> 3)) * 128 + (line & 7) * 16;
 #pragma unroll
-      for (int q = 0; q < I8_S; ++q) wd[q][0] = wd[q][1] = wd[q][2] = wd[q][3] = 0u;
-#pragma unroll
-      for (int kk = 0; kk < 16; ++kk) {
-        const double v = s ? s[(int64_t)j * NB + ((k0 + kk) & (NB - 1))] * sc : 0.0;
-        uint32_t tmp[I8_S] = {0, 0, 0, 0, 0, 0, 0, 0};
-        digits8(v, tmp, kk & 3);
-#pragma unroll
-        for (int q = 0; q < I8_S; ++q) wd[q][kk >> 2] |= tmp[q];
-      }
-      const int off = (kh * (NB / 8) + (j >> 3)) * 128 + (j & 7) * 16;
-#pragma unroll
-      for (int q = 0; q < I8_S; ++q)
-        *reinterpret_cast<uint4*>(st + off + q * I8_SL) =
-            make_uint4(wd[q][0], wd[q][1], wd[q][2], wd[q][3]);
-      __syncthreads();
-      const uint4* s4 = reinterpret_cast<const uint4*>(st);
-      uint4* d4 = reinterpret_cast<uint4*>(dst + (int64_t)kc * I8_BLK);
-      for (int e = tid; e < I8_BLK / 16; e += 256) d4[e] = s4[e];
-      __syncthreads();
-    }
+    for (int q = 0; q < I8_S; ++q)
+      *reinterpret_cast<uint4*>(dst + q * I8_SL + off) =
+          make_uint4(wd[q][0], wd[q][1], wd[q][2], wd[q][3]);
   }
 }
 
@@ -565,7 +542,7 @@ double run_i8_peak(Ctx* c) {
 
 void launch_lu_i8_slice(Ctx* c, cudaStream_t s, const BandGeom& g, const double* tiles, int K,
                         const I8Panel& pn) {
-  lu_i8_slice_kernel<<<dim3(g.wl + g.wu, g.P), 256, 0, s>>>(g, tiles, K, pn);
+  lu_i8_slice_kernel<<<dim3(g.wl + g.wu, I8_SLICE_SPLIT, g.P), 256, 0, s>>>(g, tiles, K, pn);
   LRS_LAUNCHED(c);
 }
 
