@@ -160,8 +160,6 @@ __device__ __forceinline__ void digits8_bits(double x, int e, uint32_t* words, i
   }
 }
 
-}
-
 // ---------------------------------------------------------------------------------------
 // lu_i8_slice: grid (wl + wu, 4, P), 256 threads.  Blocks x < wl slice 32 rows (y) of the A
 // tile row I = K+2+x, the others 32 columns of the B tile column J = K+2+(x-wl); tiles
