@@ -462,7 +462,10 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1)
   if (tid == 0) st_release_u32(flags + g.fbase[p] + t, epoch);
   STRACE(5);
 #ifdef LRS_SOLVE_TRACE
-  if (g_strace && tid == 0) g_strace[(size_t)tk0 * 8 + 6] = ((unsigned long long)p << 32) | t;
+  if (g_strace && tid == 0) {
+    g_strace[(size_t)tk0 * 8 + 6] = ((unsigned long long)p << 32) | t;
+    g_strace[(size_t)tk0 * 8 + 7] = grp;
+  }
 #endif
 }
 
@@ -483,12 +486,16 @@ static void launch_mode(Ctx* c, const BandGeom& g, const double* tiles, double* 
 #ifdef LRS_SOLVE_TRACE
   static int launches = 0;
   unsigned long long* tb = nullptr;
-  const bool tr = NR == 1 && MODE <= 1 && std::getenv("LRS_STRACE") && ++launches >= 40 &&
-                  launches < 44;
+  // LRS_STRACE_NR selects the width traced (default 1: the Krylov sweeps; 16: the spike
+  // solves, traced from their first launch)
+  const char* tnr = std::getenv("LRS_STRACE_NR");
+  const int want = tnr ? std::atoi(tnr) : 1;
+  const bool tr = NR == want && std::getenv("LRS_STRACE") &&
+                  (want == 1 ? (MODE <= 1 && ++launches >= 40 && launches < 44) : ++launches <= 4);
   if (tr) {
     LRS_CUDA(cudaStreamSynchronize(c->stream));
-    LRS_CUDA(cudaMalloc(&tb, (size_t)ntiles * 8 * 8));
-    LRS_CUDA(cudaMemset(tb, 0, (size_t)ntiles * 8 * 8));
+    LRS_CUDA(cudaMalloc(&tb, (size_t)ntiles * ngroups * 8 * 8));
+    LRS_CUDA(cudaMemset(tb, 0, (size_t)ntiles * ngroups * 8 * 8));
     LRS_CUDA(cudaMemcpyToSymbol(g_strace, &tb, sizeof(tb)));
   }
 #endif
@@ -499,13 +506,13 @@ static void launch_mode(Ctx* c, const BandGeom& g, const double* tiles, double* 
 #ifdef LRS_SOLVE_TRACE
   if (tr) {
     LRS_CUDA(cudaStreamSynchronize(c->stream));
-    std::vector<unsigned long long> h((size_t)ntiles * 8);
+    std::vector<unsigned long long> h((size_t)ntiles * ngroups * 8);
     LRS_CUDA(cudaMemcpy(h.data(), tb, h.size() * 8, cudaMemcpyDeviceToHost));
     unsigned long long* z = nullptr;
     LRS_CUDA(cudaMemcpyToSymbol(g_strace, &z, sizeof(z)));
     LRS_CUDA(cudaFree(tb));
     FILE* f = std::fopen(std::getenv("LRS_STRACE"), "ab");
-    const int hdr[2] = {MODE, ntiles};
+    const int hdr[2] = {MODE, ntiles * ngroups};
     std::fwrite(hdr, sizeof(int), 2, f);
     std::fwrite(h.data(), 8, h.size(), f);
     std::fclose(f);

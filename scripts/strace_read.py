@@ -11,10 +11,13 @@ while o < len(raw):
     a = np.frombuffer(raw[o:o + nt * 64], dtype=np.uint64).reshape(nt, 8).astype(np.int64)
     o += nt * 64
     t0 = a[:, 0].min()
-    p = a[:, 6] >> 32
+    p = (a[:, 6] >> 32) * 64 + a[:, 7]  # chain = (partition, column group)
     t = a[:, 6] & 0xffffffff
     pub = a[:, 5] - t0
     print(f"mode {mode} tiles {nt} span {(a[:, 5].max() - t0) / 1e3:.1f} us")
+    a = a[a[:, 5] > 0]
+    p = (a[:, 6] >> 32) * 64 + a[:, 7]
+    t = a[:, 6] & 0xffffffff
     steps, lat_flag, lat_dep, lat_diag, lat_pub, late = [], [], [], [], [], []
     for pp in np.unique(p):
         idx = np.flatnonzero(p == pp)
