@@ -62,12 +62,18 @@ constexpr int NCH = NB / CH_COLS;        // chunks per tile
 #define LRS_SOLVE_DIAGPK 0
 #endif
 constexpr int DPK_ELEMS = NB * (NB + 1) / 2;  // 8256: upper incl. diagonal (lower: 8128)
-template <int NR> struct SolveCfg {
+// Shared-memory plan per (mode, width).  `red` (half sums of the FMA path, the transposed
+// accumulator) and `part` (K-quarter partials of the transposed DMMA path) exist only where
+// they are used, so the 48-column DMMA sweeps fit: forward 5 x 32 KB ring + 53 KB of x_s,
+// adjoint 2-stage ring + x_s + red + part.
+template <int MODE, int NR> struct SolveCfg {
+  static constexpr bool TRANS = MODE >= 2;
   static constexpr bool DIAGPK = LRS_SOLVE_DIAGPK && NR == 1;
-  static constexpr int STAGES = 5;
+  static constexpr int STAGES = (TRANS && NR > 16) ? 2 : 5;
   static constexpr int XLD = NR == 1 ? 1 : NR + 4;  // padded row stride of xs / red
   static constexpr int PLD = NR + 1;                // K-quarter partials (adjoint DMMA)
-  static constexpr int PART = NR == 1 ? 0 : 4 * CH_COLS * PLD;
+  static constexpr int RED = (NR == 1 || TRANS) ? NB * XLD : 0;
+  static constexpr int PART = (NR > 1 && TRANS) ? 4 * CH_COLS * PLD : 0;
   static constexpr int DREG = DIAGPK ? DPK_ELEMS : 0;
 };
 // packed index of diagonal-tile element (r, c) of the triangle the sweep uses
@@ -76,11 +82,12 @@ __device__ __forceinline__ int dpk_col(int c) {
   return MODE == 0 ? c * NB - c * (c + 1) / 2 - c - 1 : c * (c + 1) / 2;
 }
 
-template <int NR>
+template <int MODE, int NR>
 constexpr size_t solve_smem_bytes() {
-  return sizeof(double) * ((size_t)SolveCfg<NR>::STAGES * CH_SM + SolveCfg<NR>::DREG +
-                           2 * (size_t)NB * SolveCfg<NR>::XLD + SolveCfg<NR>::PART) +
-         16 * (SolveCfg<NR>::STAGES + 1) + 64;
+  using C = SolveCfg<MODE, NR>;
+  return sizeof(double) * ((size_t)C::STAGES * CH_SM + C::DREG + (size_t)NB * C::XLD + C::RED +
+                           C::PART) +
+         16 * (C::STAGES + 1) + 64;
 }
 
 #ifdef LRS_SOLVE_TRACE
@@ -105,21 +112,22 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1)
                       int nrhs, unsigned* flags, unsigned epoch, int* ticket, int p_only,
                       int ngroups, int64_t flag_stride, const float* __restrict__ t32,
                       unsigned long long* mbox) {
-  constexpr int STAGES = SolveCfg<NR>::STAGES;
-  constexpr int XLD = SolveCfg<NR>::XLD;
+  using Cfg = SolveCfg<MODE, NR>;
+  constexpr int STAGES = Cfg::STAGES;
+  constexpr int XLD = Cfg::XLD;
   constexpr bool FWD = (MODE == 0 || MODE == 2);
   constexpr bool TRANS = (MODE >= 2);
   constexpr bool MMA = NR >= 8;
   extern __shared__ __align__(128) unsigned char smraw[];
-  constexpr bool DPK = SolveCfg<NR>::DIAGPK && !TRANS;
+  constexpr bool DPK = Cfg::DIAGPK && !TRANS;
   constexpr bool LLM = NR == 1 && !TRANS;  // mailbox handoff (2 words per row of x_t)
   static_assert(!LLM || SOLVE_THREADS == 2 * NB, "one mailbox word per thread");
   double* ring = reinterpret_cast<double*>(smraw);
   double* dreg = ring + (size_t)STAGES * CH_SM;  // resident packed diagonal triangle
-  double* xs = dreg + SolveCfg<NR>::DREG;      // [NB][XLD]: x_s, or the diagonal-step input
+  double* xs = dreg + Cfg::DREG;      // [NB][XLD]: x_s, or the diagonal-step input
   double* red = xs + NB * XLD;                 // [NB][XLD]: half sums / transposed accumulator
-  double* part = red + NB * XLD;               // [4][CH_COLS][PLD]: adjoint K-quarter partials
-  uint64_t* bars = reinterpret_cast<uint64_t*>(part + SolveCfg<NR>::PART);  // + [STAGES]: diag
+  double* part = red + Cfg::RED;               // [4][CH_COLS][PLD]: adjoint K-quarter partials
+  uint64_t* bars = reinterpret_cast<uint64_t*>(part + Cfg::PART);  // + [STAGES]: diag
   int* s_tk = reinterpret_cast<int*>(bars + STAGES + 1);
 
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
@@ -364,7 +372,7 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1)
       // so each warp runs 4 NJ / 2 independent accumulator chains of 8 DMMAs; the four
       // K-quarter partials are then summed in fixed order (the same for every NR, so
       // multi-column stays bit-identical to column-by-column).
-      constexpr int PLD = SolveCfg<NR>::PLD;
+      constexpr int PLD = Cfg::PLD;
       constexpr int TPH = 2 * NJ;  // output tiles per warp
       const int kq = w & 3, th = w >> 2;
       double cacc[TPH][2];
@@ -476,7 +484,7 @@ static void launch_mode(Ctx* c, const BandGeom& g, const double* tiles, double* 
                         unsigned long long* mbox) {
   const int ngroups = (nrhs + NR - 1) / NR;
   static bool attr = false;
-  const size_t smem = solve_smem_bytes<NR>();
+  const size_t smem = solve_smem_bytes<MODE, NR>();
   if (!attr) {
     LRS_CUDA(cudaFuncSetAttribute(band_solve_kernel<MODE, NR>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -520,6 +528,15 @@ static void launch_mode(Ctx* c, const BandGeom& g, const double* tiles, double* 
 #endif
 }
 
+// 17..48 columns (the spike blocks) run as ONE 48-column group: each row tile's factor
+// chunks are streamed once for all columns and the chains have 3x fewer CTAs in flight to
+// share the SMs with (16-column groups read every tile three times through L2)
+#ifndef LRS_SOLVE_NR48
+#define LRS_SOLVE_NR48 1
+#endif
+#ifndef LRS_SOLVE_NR48_TRANS
+#define LRS_SOLVE_NR48_TRANS 1
+#endif
 template <int MODE>
 static void launch_nr(Ctx* c, const BandGeom& g, const double* tiles, double* x, int64_t ld,
                       int nrhs, unsigned* flags, unsigned epoch, int* ticket, int p_only,
@@ -531,8 +548,10 @@ static void launch_nr(Ctx* c, const BandGeom& g, const double* tiles, double* x,
     launch_mode<MODE, 1>(c, g, tiles, x, ld, nrhs, flags, epoch, ticket, p_only, ntiles, fs, t32, mb);
   else if (nrhs <= 8)
     launch_mode<MODE, 8>(c, g, tiles, x, ld, nrhs, flags, epoch, ticket, p_only, ntiles, fs, t32, mb);
-  else
+  else if (nrhs <= 16 || (MODE >= 2 && !LRS_SOLVE_NR48_TRANS) || !LRS_SOLVE_NR48)
     launch_mode<MODE, 16>(c, g, tiles, x, ld, nrhs, flags, epoch, ticket, p_only, ntiles, fs, t32, mb);
+  else
+    launch_mode<MODE, 48>(c, g, tiles, x, ld, nrhs, flags, epoch, ticket, p_only, ntiles, fs, t32, mb);
 }
 
 void launch_band_solve(Ctx* c, const BandGeom& g, const double* tiles, int mode, double* x,
