@@ -45,12 +45,23 @@ namespace lrs {
 constexpr int I8_S = 8;                               // digit slices per operand
 constexpr int I8_KC = 32;                             // K per MMA and per pipeline chunk
 constexpr int I8_NCH = 2 * NB / I8_KC;                // 8 chunks over K = 256
-constexpr int I8_SL = NB * I8_KC;                     // 4096 B: one slice of one chunk
-constexpr int I8_BLK = I8_S * I8_SL;                  // 32 KB: all slices of one chunk
-constexpr int I8_STAGE = 2 * I8_BLK;                  // A + B
-constexpr int I8_STAGES = 3;
-constexpr int I8_GROUPS = 4;                          // accumulators per pass (4 x 128 cols)
-constexpr int I8_THREADS = 320;                       // producer, MMA, 8 epilogue warps
+constexpr int I8_SL = NB * I8_KC;                     // 4096 B: one A slice of one chunk
+constexpr int I8_BLK = I8_S * I8_SL;                  // 32 KB: all A slices of one chunk
+// output columns per CTA: 128 (one CTA per SM, all 512 TMEM columns) or 64 (two CTAs per SM
+// with 256 columns each, so one CTA's MMAs run while the other drains)
+#ifndef LRS_I8_TN
+#define LRS_I8_TN 128
+#endif
+constexpr int I8_TN = LRS_I8_TN;
+constexpr int I8_NH = NB / I8_TN;                     // column blocks per tile
+constexpr int I8_BSL = I8_TN * I8_KC;                 // one B slice of one chunk
+constexpr int I8_BBLK = I8_S * I8_BSL;                // all B slices of one chunk
+constexpr int I8_STAGE = I8_BLK + I8_BBLK;            // A + B
+constexpr int I8_STAGES = I8_TN == 128 ? 3 : 2;
+constexpr int I8_GROUPS = 4;                          // accumulators per pass (4 x TN cols)
+constexpr int I8_TMEM = I8_GROUPS * I8_TN;            // 512 or 256 columns
+constexpr int I8_EPI = 4 * I8_TN / 64;                // epilogue warps (64 columns each)
+constexpr int I8_THREADS = 32 * (2 + I8_EPI);         // producer, MMA, epilogue warps
 constexpr int I8_TPC = 4;                             // tiles per CTA
 // LRS_I8_EXP (timing experiments only, wrong results): 1 skips the epilogue arithmetic,
 // 2 also skips the operand copies
@@ -58,6 +69,7 @@ constexpr int I8_TPC = 4;                             // tiles per CTA
 #define LRS_I8_EXP 0
 #endif
 constexpr size_t I8_SMEM = (size_t)I8_STAGES * I8_STAGE + 2048;
+static_assert(I8_TN == 128 || I8_SMEM * 2 <= 227 * 1024, "two CTAs per SM");
 
 size_t lu_i8_panel_bytes(const BandGeom& g) {
   return (size_t)g.P * (g.wl + g.wu) * (I8_NCH * I8_BLK + sizeof(int) * NB);
@@ -68,8 +80,8 @@ __device__ __forceinline__ uint64_t umma_sdesc(uint32_t addr, uint32_t lbo, uint
   return (uint64_t)((addr >> 4) & 0x3fff) | ((uint64_t)((lbo >> 4) & 0x3fff) << 16) |
          ((uint64_t)((sbo >> 4) & 0x3fff) << 32) | ((uint64_t)1 << 46);  // SWIZZLE_NONE, v1
 }
-// D: s32, A / B: signed int8, K-major, M = N = 128
-constexpr uint32_t I8_IDESC = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(NB >> 3) << 17) |
+// D: s32, A / B: signed int8, K-major, M = 128, N = I8_TN
+constexpr uint32_t I8_IDESC = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(I8_TN >> 3) << 17) |
                               ((uint32_t)(NB >> 4) << 24);
 // COLL: the A-operand collector -- 0 none, 1 fill (keep A for the next MMA), 2 use + keep,
 // 3 last use.  Consecutive MMAs on one A slice then read it from shared memory once.
@@ -219,9 +231,13 @@ __global__ void __launch_bounds__(256) lu_i8_slice_kernel(BandGeom g, const doub
     int* ex = isA ? pn.ea + ((int64_t)p * g.wl + idx) * NB : pn.eb + ((int64_t)p * g.wu + idx) * NB;
     ex[line] = e;
   }
-  uint8_t* dst = (isA ? pn.A + ((int64_t)p * g.wl + idx) * I8_NCH * I8_BLK
-                      : pn.B + ((int64_t)p * g.wu + idx) * I8_NCH * I8_BLK) +
-                 (int64_t)kc * I8_BLK;
+  // B: column block h = line / TN, operand row line % TN, in [p][jb][h][chunk][slice]
+  const int bl = isA ? line : (line & (I8_TN - 1));
+  const int sl = isA ? I8_SL : I8_BSL;
+  uint8_t* dst = isA ? pn.A + (((int64_t)p * g.wl + idx) * I8_NCH + kc) * I8_BLK
+                     : pn.B + ((((int64_t)p * g.wu + idx) * I8_NH + line / I8_TN) * I8_NCH + kc) *
+                                  I8_BBLK;
+  const int rows = isA ? NB : I8_TN;
 #pragma unroll
   for (int h = 0; h < 2; ++h) {  // K-core: k0 + 16h .. k0 + 16h + 15
     uint32_t wd[I8_S][4];
@@ -234,19 +250,22 @@ __global__ void __launch_bounds__(256) lu_i8_slice_kernel(BandGeom g, const doub
 #pragma unroll
       for (int q = 0; q < I8_S; ++q) wd[q][kk >> 2] |= tmp[q];
     }
-    const int off = (h * (NB / 8) + (line >> 3)) * 128 + (line & 7) * 16;
+    const int off = (h * (rows / 8) + (bl >> 3)) * 128 + (bl & 7) * 16;
 #pragma unroll
     for (int q = 0; q < I8_S; ++q)
-      *reinterpret_cast<uint4*>(dst + q * I8_SL + off) =
+      *reinterpret_cast<uint4*>(dst + q * sl + off) =
           make_uint4(wd[q][0], wd[q][1], wd[q][2], wd[q][3]);
   }
 }
 
-// tile t of the kind-3 / kind-4 lists -> (p, ia, jb); false when outside the blocks
+// work item t of the kind-3 / kind-4 lists -> (p, ia, jb, column block h); false when
+// outside the blocks
 template <int KIND>
 __device__ __forceinline__ bool i8_decode(const BandGeom& g, int K, int t, int& p, int& ia,
-                                          int& jb) {
+                                          int& jb, int& h) {
   const int per = KIND == 4 ? (g.wl - 2) * (g.wu - 2) : 2 * g.wl + 2 * g.wu - 4;
+  h = t % I8_NH;
+  t /= I8_NH;
   p = t / per;
   int r = t % per;
   int I, J;
@@ -294,9 +313,9 @@ __device__ __forceinline__ void i8_chunk_mmas(uint32_t tm, uint32_t a0, uint32_t
         mbar_wait_trap(&tempty[slot], (u - 1) & 1);
         tc_fence_after();
       }
-      const uint32_t dd = tm + slot * NB;
+      const uint32_t dd = tm + slot * I8_TN;
       const uint64_t ad = umma_sdesc(a0 + (pp - 1) * I8_SL, NB * 16, 128);
-      const uint64_t bd = umma_sdesc(b0 + (q - 1) * I8_SL, NB * 16, 128);
+      const uint64_t bd = umma_sdesc(b0 + (q - 1) * I8_BSL, I8_TN * 16, 128);
       const uint32_t ac = (first && pp == 1) ? 0u : 1u;
       if (qhi == qlo) umma_i8<0>(dd, ad, bd, ac);
       else if (q == qhi) umma_i8<1>(dd, ad, bd, ac);
@@ -307,7 +326,7 @@ __device__ __forceinline__ void i8_chunk_mmas(uint32_t tm, uint32_t a0, uint32_t
 }
 
 template <int KIND>
-__global__ void __launch_bounds__(I8_THREADS, 1)
+__global__ void __launch_bounds__(I8_THREADS, I8_TN == 128 ? 1 : 2)
     lu_i8_gemm_kernel(BandGeom g, double* tiles, int K, I8Panel pn, int total) {
   extern __shared__ __align__(1024) uint8_t smraw[];
   uint8_t* stage = smraw;
@@ -319,9 +338,10 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
   double* sj = reinterpret_cast<double*>(smraw + I8_STAGES * I8_STAGE + 1024);  // [128]
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int t0 = blockIdx.x * I8_TPC, t1 = min(total, t0 + I8_TPC);
-  auto ctile = [&](int p, int ia, int jb) -> double* {
+  auto ctile = [&](int p, int ia, int jb, int h) -> double* {
     const int I = K + 2 + ia, J = K + 2 + jb;
-    return tiles + (g.tbase[p] + (int64_t)I * g.W + (J - I + g.wl)) * TILE_ELEMS;
+    return tiles + (g.tbase[p] + (int64_t)I * g.W + (J - I + g.wl)) * TILE_ELEMS +
+           (int64_t)h * I8_TN * NB;
   };
   if (threadIdx.x == 0) {
     for (int s = 0; s < I8_STAGES; ++s) {
@@ -329,12 +349,12 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
       mbar_init(&empty[s], 1);
     }
     mbar_init(tfull, 1);
-    for (int gi = 0; gi < I8_GROUPS; ++gi) mbar_init(&tempty[gi], 8);
+    for (int gi = 0; gi < I8_GROUPS; ++gi) mbar_init(&tempty[gi], I8_EPI);
     fence_mbar_init();
   }
   if (w == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
-                     smem_u32(tbase))
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tbase)), "n"(I8_TMEM)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
@@ -348,13 +368,14 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
     if (lane == 0) {
       int it = 0;
       for (int t = t0; t < t1; ++t) {
-        int p, ia, jb;
-        if (!i8_decode<KIND>(g, K, t, p, ia, jb)) continue;
-        bulk_prefetch_l2(ctile(p, ia, jb), sizeof(double) * TILE_ELEMS);
+        int p, ia, jb, h;
+        if (!i8_decode<KIND>(g, K, t, p, ia, jb, h)) continue;
+        bulk_prefetch_l2(ctile(p, ia, jb, h), sizeof(double) * NB * I8_TN);
         const uint8_t* a = pn.A + ((int64_t)p * g.wl + ia) * I8_NCH * I8_BLK;
-        const uint8_t* b = pn.B + ((int64_t)p * g.wu + jb) * I8_NCH * I8_BLK;
+        const uint8_t* b = pn.B + (((int64_t)p * g.wu + jb) * I8_NH + h) * I8_NCH * I8_BBLK;
         for (int pass = 0; pass < 2; ++pass) {
-          const unsigned bytes = pass == 0 ? I8_BLK : I8_BLK / 2;
+          const unsigned abytes = pass == 0 ? I8_BLK : I8_BLK / 2;
+          const unsigned bbytes = pass == 0 ? I8_BBLK : I8_BBLK / 2;
           for (int kc = 0; kc < I8_NCH; ++kc, ++it) {
             const int s = it % I8_STAGES;
             if (it >= I8_STAGES) mbar_wait_trap<64>(&empty[s], ((it / I8_STAGES) & 1) ^ 1);
@@ -362,9 +383,9 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
               mbar_arrive1(&full[s]);
               continue;
             }
-            mbar_expect_tx(&full[s], 2 * bytes);
-            bulk_g2s(stage + s * I8_STAGE, a + kc * I8_BLK, bytes, &full[s]);
-            bulk_g2s(stage + s * I8_STAGE + I8_BLK, b + kc * I8_BLK, bytes, &full[s]);
+            mbar_expect_tx(&full[s], abytes + bbytes);
+            bulk_g2s(stage + s * I8_STAGE, a + kc * I8_BLK, abytes, &full[s]);
+            bulk_g2s(stage + s * I8_STAGE + I8_BLK, b + kc * I8_BBLK, bbytes, &full[s]);
           }
         }
       }
@@ -374,8 +395,8 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
     if (lane == 0) {
       int it = 0, u = 0;
       for (int t = t0; t < t1; ++t) {
-        int p, ia, jb;
-        if (!i8_decode<KIND>(g, K, t, p, ia, jb)) continue;
+        int p, ia, jb, h;
+        if (!i8_decode<KIND>(g, K, t, p, ia, jb, h)) continue;
         for (int pass = 0; pass < 2; ++pass, ++u) {
           for (int kc = 0; kc < I8_NCH; ++kc, ++it) {
             const int s = it % I8_STAGES;
@@ -398,14 +419,14 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
     constexpr double BIAS = 4503601774854144.0;  // 2^52 + 2^31
     int u = 0;
     for (int t = t0; t < t1; ++t) {
-      int p, ia, jb;
-      if (!i8_decode<KIND>(g, K, t, p, ia, jb)) continue;
-      double* C = ctile(p, ia, jb) + (int64_t)ch * 64 * NB;
+      int p, ia, jb, h;
+      if (!i8_decode<KIND>(g, K, t, p, ia, jb, h)) continue;
+      double* C = ctile(p, ia, jb, h) + (int64_t)ch * 64 * NB;
       const double si = exp2i(pn.ea[((int64_t)p * g.wl + ia) * NB + i]);
       if (w == 2) {  // the previous tile's readers of sj passed the closing barrier
-        const int* eb = pn.eb + ((int64_t)p * g.wu + jb) * NB;
+        const int* eb = pn.eb + ((int64_t)p * g.wu + jb) * NB + h * I8_TN;
 #pragma unroll
-        for (int r = 0; r < 4; ++r) sj[lane + 32 * r] = exp2i(eb[lane + 32 * r]);
+        for (int r = 0; r < I8_TN / 32; ++r) sj[lane + 32 * r] = exp2i(eb[lane + 32 * r]);
       }
       const uint32_t trow = tm + ((uint32_t)(32 * qd) << 16) + ch * 64;
       double acc[64];
@@ -428,7 +449,7 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
           for (int h2 = 0; h2 < 2; ++h2) {
             uint32_t v[32];
 #pragma unroll
-            for (int c8 = 0; c8 < 32; c8 += 8) tmem_ld8(trow + slot * NB + h2 * 32 + c8, v + c8);
+            for (int c8 = 0; c8 < 32; c8 += 8) tmem_ld8(trow + slot * I8_TN + h2 * 32 + c8, v + c8);
             tmem_ld_wait();
             if (h2 == 1) {  // this warp's part of the slot is in registers: release it
               tc_fence_before();
@@ -443,7 +464,7 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
           }
         }
       }
-      asm volatile("bar.sync 1, 256;" ::: "memory");  // sj written
+      asm volatile("bar.sync 1, %0;" ::"n"(32 * I8_EPI) : "memory");  // sj written
       // C -= 2^(ea+eb) acc as fire-and-forget L2 reductions: no load round trip in the
       // epilogue, and with one contribution per element fl(c + (-r)) == fl(c - r) exactly
       if (!LRS_I8_EXP) {
@@ -451,14 +472,15 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
         for (int j = 0; j < 64; ++j)
           red_add_f64(C + (int64_t)j * NB + i, -(acc[j] * si * sj[ch * 64 + j]));
       }
-      asm volatile("bar.sync 1, 256;" ::: "memory");  // sj free for the next tile
+      asm volatile("bar.sync 1, %0;" ::"n"(32 * I8_EPI) : "memory");  // sj free for the next tile
     }
   }
   tc_fence_before();
   __syncthreads();
   if (w == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tm) : "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tm), "n"(I8_TMEM)
+                 : "memory");
   }
 }
 
@@ -555,7 +577,7 @@ void launch_lu_i8_gemm(Ctx* c, cudaStream_t s, const BandGeom& g, double* tiles,
     attr = true;
   }
   const int per = kind == 4 ? (g.wl - 2) * (g.wu - 2) : 2 * g.wl + 2 * g.wu - 4;
-  const int total = per * g.P;
+  const int total = per * g.P * I8_NH;
   const int grid = (total + I8_TPC - 1) / I8_TPC;
   if (total <= 0) return;
   if (kind == 4)
