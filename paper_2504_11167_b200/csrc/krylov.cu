@@ -116,7 +116,11 @@ __global__ void __launch_bounds__(KV_THREADS) axpby_kernel(int64_t n, int nrhs, 
                                                            int64_t ldz, S* W, int64_t ldw) {
   const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (row >= n) return;
-  for (int j = 0; j < nrhs; ++j) {
+  // compile-time column indices into the by-value scalar arrays: a runtime index would copy
+  // the 3 x 16 parameters into local memory in every thread
+#pragma unroll
+  for (int j = 0; j < MAX_RHS; ++j) {
+    if (j >= nrhs) break;
     if (act.v[j] == 0.0) continue;
     const S aj = a.v[j], bj = b.v[j];
     switch (op) {

@@ -167,7 +167,7 @@ size_t iface_work_doubles(int njobs, int r, int64_t k) {
 // x[row, j] = y[row, j] - sum_a uW[row, a] scW_p[a, j] - sum_a uT[row, a] scT_p[a, j]
 // for the local rows; scT / scW: one r x MAX_RHS block per GLOBAL partition (scT of the
 // last partition and scW of the first are never read).
-template <class S>
+template <class S, int NRC>
 __global__ void __launch_bounds__(256) recovery_kernel(BandGeom g, int64_t n, int64_t row_lo,
                                                        int64_t row_hi, const S* y, int64_t ldy,
                                                        S* x, int64_t ldx, int nrhs,
@@ -185,23 +185,33 @@ __global__ void __launch_bounds__(256) recovery_kernel(BandGeom g, int64_t n, in
   }
   const int pg = g.p0 + lo;
   const bool hasW = pg > 0, hasT = pg < g.Pg - 1;
-  S acc[MAX_RHS];
-  for (int j = 0; j < nrhs; ++j) acc[j] = y[row + j * ldy];
+  // NRC: compile-time bound of the column loops (1 for the Krylov hot path), so acc[] stays
+  // in registers
+  S acc[NRC];
+#pragma unroll
+  for (int j = 0; j < NRC; ++j)
+    if (j < nrhs) acc[j] = y[row + j * ldy];
   if (hasW) {
     const S* sc = scW + (int64_t)pg * r * MAX_RHS;
     for (int a = 0; a < r; ++a) {
       const S u = uW[row + a * n];
-      for (int j = 0; j < nrhs; ++j) acc[j] = s_sub(acc[j], s_mul(u, sc[a + j * r]));
+#pragma unroll
+      for (int j = 0; j < NRC; ++j)
+        if (j < nrhs) acc[j] = s_sub(acc[j], s_mul(u, sc[a + j * r]));
     }
   }
   if (hasT) {
     const S* sc = scT + (int64_t)pg * r * MAX_RHS;
     for (int a = 0; a < r; ++a) {
       const S u = uT[row + a * n];
-      for (int j = 0; j < nrhs; ++j) acc[j] = s_sub(acc[j], s_mul(u, sc[a + j * r]));
+#pragma unroll
+      for (int j = 0; j < NRC; ++j)
+        if (j < nrhs) acc[j] = s_sub(acc[j], s_mul(u, sc[a + j * r]));
     }
   }
-  for (int j = 0; j < nrhs; ++j) x[row + j * ldx] = acc[j];
+#pragma unroll
+  for (int j = 0; j < NRC; ++j)
+    if (j < nrhs) x[row + j * ldx] = acc[j];
 }
 
 template <class S>
@@ -210,8 +220,13 @@ void launch_recovery_t(Ctx* c, const BandGeom& g, int64_t n, int64_t row_lo, int
                        const S* uW, int r, const S* scT, const S* scW) {
   if (row_hi <= row_lo) return;
   ProfScope ps_(c, K_RECOVERY);
-  recovery_kernel<S><<<(unsigned)((row_hi - row_lo + 255) / 256), 256, 0, c->stream>>>(
-      g, n, row_lo, row_hi, y, ldy, x, ldx, nrhs, uT, uW, r, scT, scW);
+  const unsigned grid = (unsigned)((row_hi - row_lo + 255) / 256);
+  if (nrhs == 1)
+    recovery_kernel<S, 1><<<grid, 256, 0, c->stream>>>(g, n, row_lo, row_hi, y, ldy, x, ldx, nrhs,
+                                                       uT, uW, r, scT, scW);
+  else
+    recovery_kernel<S, MAX_RHS><<<grid, 256, 0, c->stream>>>(g, n, row_lo, row_hi, y, ldy, x, ldx,
+                                                             nrhs, uT, uW, r, scT, scW);
   LRS_LAUNCHED(c);
 }
 
