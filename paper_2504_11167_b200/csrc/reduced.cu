@@ -51,7 +51,7 @@ void launch_tips_gather_t(Ctx* c, const BandGeom& g, int64_t k, const S* y, int6
 
 // mode 0 (matvec_lowrank): both terms on every tip row; mode 1 (truncated precond): W
 // term on top rows, T term on bottom rows.  sign: +1 / -1.
-template <class S>
+template <class S, int NRC>
 __global__ void __launch_bounds__(256) tips_lowrank_kernel(BandGeom g, int64_t n, int64_t k,
                                                            const S* in, S* out, int64_t ldr,
                                                            int nrhs, const S* __restrict__ uT,
@@ -70,29 +70,32 @@ __global__ void __launch_bounds__(256) tips_lowrank_kernel(BandGeom g, int64_t n
   const int64_t cr = (int64_t)pg * per + q;
   const bool useW = pg > 0 && (mode == 0 || top);
   const bool useT = pg < g.Pg - 1 && (mode == 0 || !top);
-  S acc[MAX_RHS];
-  for (int j = 0; j < nrhs; ++j) acc[j] = in[cr + j * ldr];
-  if (useW) {
-    const S* sc = scW + (int64_t)pg * r * MAX_RHS;
-    S d[MAX_RHS];
-    for (int j = 0; j < nrhs; ++j) d[j] = s_zero(S());
+  // NRC: compile-time bound of the column loops, so acc[] / d[] stay in registers
+  S acc[NRC];
+#pragma unroll
+  for (int j = 0; j < NRC; ++j)
+    if (j < nrhs) acc[j] = in[cr + j * ldr];
+#pragma unroll
+  for (int side = 0; side < 2; ++side) {
+    if (side == 0 ? !useW : !useT) continue;
+    const S* sc = (side == 0 ? scW : scT) + (int64_t)pg * r * MAX_RHS;
+    const S* u = side == 0 ? uW : uT;
+    S d[NRC];
+#pragma unroll
+    for (int j = 0; j < NRC; ++j) d[j] = s_zero(S());
     for (int a = 0; a < r; ++a) {
-      const S u = uW[urow + a * n];
-      for (int j = 0; j < nrhs; ++j) d[j] = s_fma(u, sc[a + j * r], d[j]);
+      const S ua = u[urow + a * n];
+#pragma unroll
+      for (int j = 0; j < NRC; ++j)
+        if (j < nrhs) d[j] = s_fma(ua, sc[a + j * r], d[j]);
     }
-    for (int j = 0; j < nrhs; ++j) acc[j] = s_add(acc[j], s_scale(d[j], sign));
+#pragma unroll
+    for (int j = 0; j < NRC; ++j)
+      if (j < nrhs) acc[j] = s_add(acc[j], s_scale(d[j], sign));
   }
-  if (useT) {
-    const S* sc = scT + (int64_t)pg * r * MAX_RHS;
-    S d[MAX_RHS];
-    for (int j = 0; j < nrhs; ++j) d[j] = s_zero(S());
-    for (int a = 0; a < r; ++a) {
-      const S u = uT[urow + a * n];
-      for (int j = 0; j < nrhs; ++j) d[j] = s_fma(u, sc[a + j * r], d[j]);
-    }
-    for (int j = 0; j < nrhs; ++j) acc[j] = s_add(acc[j], s_scale(d[j], sign));
-  }
-  for (int j = 0; j < nrhs; ++j) out[cr + j * ldr] = acc[j];
+#pragma unroll
+  for (int j = 0; j < NRC; ++j)
+    if (j < nrhs) out[cr + j * ldr] = acc[j];
 }
 
 template <class S>
@@ -102,8 +105,13 @@ void launch_tips_lowrank_t(Ctx* c, const BandGeom& g, int64_t n, int64_t k, cons
   const int64_t tot = 2 * k * g.P;
   if (tot == 0 || nrhs == 0) return;
   ProfScope ps_(c, K_RECOVERY);
-  tips_lowrank_kernel<S><<<(unsigned)((tot + 255) / 256), 256, 0, c->stream>>>(
-      g, n, k, in, out, ldr, nrhs, uT, uW, r, scT, scW, mode, sign);
+  const unsigned grid = (unsigned)((tot + 255) / 256);
+  if (nrhs == 1)
+    tips_lowrank_kernel<S, 1><<<grid, 256, 0, c->stream>>>(g, n, k, in, out, ldr, nrhs, uT, uW, r,
+                                                          scT, scW, mode, sign);
+  else
+    tips_lowrank_kernel<S, MAX_RHS><<<grid, 256, 0, c->stream>>>(g, n, k, in, out, ldr, nrhs, uT,
+                                                                uW, r, scT, scW, mode, sign);
   LRS_LAUNCHED(c);
 }
 
