@@ -44,6 +44,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 C2_APPLIES = 71  # preconditioner applications of the c2 BiCGStab solve (GPU run == oracle +-2 it)
+I8_PRODUCTS = 28  # digit-slice products per K chunk of the INT8 update (I8_PRODUCTS, csrc/lu_i8.cu)
 
 
 def _dist():
@@ -326,11 +327,11 @@ def run_ours(args):
         apply_ms_each = (kt["band_solve"][0] + kt["iface_apply"][0] + kt["recovery"][0]) / 1.0
     total_ms = sum(v[0] for v in kt.values())
     if info.get("lu_int8"):
-        # INT8 ops the launch issues: 36 digit-slice products (M = N = 128, K = 256) per
+        # INT8 ops the launch issues: 28 digit-slice products (M = N = 128, K = 256) per
         # 128 x 128 tile of the bulk update
         tiles = sum(_i8_bulk_tiles(s, info["wl"], info["wu"], info["nb"])
                     for s in _partition_sizes(cfg.matrix.n, cfg.P))
-        ops_launch = tiles * args.steps * 2.0 * 128 * 128 * 256 * 36 / max(upd_n, 1)
+        ops_launch = tiles * args.steps * 2.0 * 128 * 128 * 256 * I8_PRODUCTS / max(upd_n, 1)
         achieved_tops = ops_launch / avg_launch_s / 1e12 if upd_n else 0.0
         roofline = {"bound": "tensor",
                     "kernel": "lu_i8_gemm_kernel<4> (INT8-sliced FP64 two-step trailing update, "

@@ -97,41 +97,146 @@ void launch_extract_tiles(Ctx* c, const Mat* m, const BandGeom& g, double* tiles
 }
 
 // ---------------------------------------------------------------------------------------
-// lu_diag: one CTA (512 threads) per partition factors tile (K,K) in shared memory.
+// lu_diag: one CTA (512 threads) per partition factors tile (K,K) with the tile held in
+// registers: thread t owns rows (t & 31) + 32 r (r = 0..3) and columns (t >> 5) + 16 c
+// (c = 0..7), both cyclic so every warp keeps work until the last steps.  Step j of the
+// right-looking LU (no interchanges; dgbtrf's pivot rule checked per column) publishes
+// column j of L and row j of U through a double-buffered shared vector pair and applies
+// the rank-1 update in registers: one barrier per step, no shared-memory round trip of
+// the trailing matrix.  The inverses follow the same pattern (rows of inv(L) forward and
+// rows of inv(U) backward in the same sweep): the tile leaves with inv(L_KK) strictly
+// below and inv(U_KK) on/above the diagonal.  Register blocks are indexed with
+// compile-time r / c only (the step loops are unrolled over 16- / 32-step blocks).
 // ---------------------------------------------------------------------------------------
 constexpr int DIAG_THREADS = 512;
+constexpr size_t DIAG_SMEM = sizeof(double) * (TILE_ELEMS + 4 * NB);
 
 __global__ void __launch_bounds__(DIAG_THREADS, 1) lu_diag_kernel(BandGeom g, double* tiles,
                                                                   int K, int* status) {
   extern __shared__ double sm[];
-  double* A = sm;                  // 128 x 128 column-major
-  double* part = sm + TILE_ELEMS;  // 4 x 128 partial sums
+  double* A = sm;                   // the LU factors (column-major), read by the inverses
+  double* vec = sm + TILE_ELEMS;    // [2 buffers][2 vectors][128]
   const int p = blockIdx.x;
   if (K >= g.T[p]) return;
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, tc = tid >> 5;
   double* gt = tiles + (g.tbase[p] + (int64_t)K * g.W + g.wl) * TILE_ELEMS;
-  for (int e = tid; e < TILE_ELEMS; e += DIAG_THREADS) A[e] = gt[e];
-  __syncthreads();
   const int col0 = K * NB;
-  const int i = tid & (NB - 1), cg = tid >> 7;  // row, column group 0..3
-  // ---- unblocked right-looking LU, pivot rule checked per column -------------------
-  for (int j = 0; j < NB; ++j) {
-    const double piv = A[j * NB + j];
-    if (cg == 0 && i > j) {
-      const double a = A[j * NB + i];
-      if (fabs(a) > fabs(piv)) atomicMin(&status[2 * p], col0 + j);  // dgbtrf would swap
-      A[j * NB + i] = a / piv;
+  double a[4][8];
+#pragma unroll
+  for (int c = 0; c < 8; ++c)
+#pragma unroll
+    for (int r = 0; r < 4; ++r) a[r][c] = gt[(tc + 16 * c) * NB + lane + 32 * r];
+
+  // ---- LU: step j = 16 jb + jj; column j lives in register column jb of warp jj ------
+#pragma unroll
+  for (int jb = 0; jb < 8; ++jb) {
+    constexpr int dummy = 0;
+    (void)dummy;
+    const int rs = jb >> 1;  // register row block of row j
+    for (int jj = 0; jj < 16; ++jj) {
+      const int j = 16 * jb + jj;
+      double* lcol = vec + (j & 1) * 2 * NB;
+      double* urow = lcol + NB;
+      if (tc == jj) {  // the warp owning column j: multipliers below the pivot
+        const double piv = __shfl_sync(0xffffffffu, a[rs][jb], j & 31);
+#pragma unroll
+        for (int r = rs; r < 4; ++r) {
+          const int i = lane + 32 * r;
+          if (i > j) {
+            const double v = a[r][jb];
+            if (fabs(v) > fabs(piv)) atomicMin(&status[2 * p], col0 + j);  // dgbtrf would swap
+            a[r][jb] = v / piv;
+            lcol[i] = a[r][jb];
+          }
+        }
+        if (lane == 0 && piv == 0.0) atomicMin(&status[2 * p + 1], col0 + j);
+      }
+      if (lane == (j & 31)) {  // row j of U, right of the pivot
+#pragma unroll
+        for (int c = jb; c < 8; ++c)
+          if (tc + 16 * c > j) urow[tc + 16 * c] = a[rs][c];
+      }
+      __syncthreads();
+      double l[4], u[8];
+#pragma unroll
+      for (int r = rs; r < 4; ++r) l[r] = (lane + 32 * r > j) ? lcol[lane + 32 * r] : 0.0;
+#pragma unroll
+      for (int c = jb; c < 8; ++c) u[c] = (tc + 16 * c > j) ? urow[tc + 16 * c] : 0.0;
+#pragma unroll
+      for (int r = rs; r < 4; ++r)
+#pragma unroll
+        for (int c = jb; c < 8; ++c) a[r][c] = fma(-l[r], u[c], a[r][c]);
     }
-    if (tid == 0 && piv == 0.0) atomicMin(&status[2 * p + 1], col0 + j);
-    __syncthreads();
-    if (i > j) {
-      const double lij = A[j * NB + i];
-      for (int c = j + 1 + cg; c < NB; c += 4) A[c * NB + i] -= lij * A[c * NB + j];
-    }
-    __syncthreads();
   }
-  diag_inverses(A, part, tid);
-  for (int e = tid; e < TILE_ELEMS; e += DIAG_THREADS) gt[e] = A[e];
+  // the factors to shared memory (columns of L and U for the inverse sweeps)
+#pragma unroll
+  for (int c = 0; c < 8; ++c)
+#pragma unroll
+    for (int r = 0; r < 4; ++r) A[(tc + 16 * c) * NB + lane + 32 * r] = a[r][c];
+  // inverse registers: identity (strictly lower part: inv(L); upper incl. diagonal: the
+  // right-hand side of U Y = I, turned into inv(U) row by row)
+#pragma unroll
+  for (int c = 0; c < 8; ++c)
+#pragma unroll
+    for (int r = 0; r < 4; ++r) a[r][c] = (lane + 32 * r == tc + 16 * c) ? 1.0 : 0.0;
+  __syncthreads();
+
+  // ---- inverses: step s forward for L (row s of inv(L) final), backward for U (row
+  // k = 127 - s of inv(U) final after the division by u_kk) ----------------------------
+#pragma unroll
+  for (int sb = 0; sb < 4; ++sb) {
+    constexpr int dummy = 0;
+    (void)dummy;
+    const int rb = 3 - sb;  // register row block of row k
+    for (int ss = 0; ss < 32; ++ss) {
+      const int s = 32 * sb + ss, k = NB - 1 - s;
+      double* xrow = vec + (s & 1) * 2 * NB;
+      double* yrow = xrow + NB;
+      if (lane == ss) {  // row s of inv(L): columns < s final, X[s][s] = 1
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const int m = tc + 16 * c;
+          if (m < s) xrow[m] = a[sb][c];
+          else if (m == s) xrow[m] = 1.0;  // (s, s) holds the U side
+        }
+      }
+      if (lane == (k & 31)) {  // row k of inv(U): divide the finished right-hand side
+        const double ukk = A[k * NB + k];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const int m = tc + 16 * c;
+          if (m >= k) {
+            a[rb][c] = a[rb][c] / ukk;
+            yrow[m] = a[rb][c];
+          }
+        }
+      }
+      __syncthreads();
+      double lv[4], uv[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int i = lane + 32 * r;
+        lv[r] = i > s ? A[s * NB + i] : 0.0;  // L[i][s]
+        uv[r] = i < k ? A[k * NB + i] : 0.0;  // U[i][k]
+      }
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const int m = tc + 16 * c;
+        const double xv = m <= s ? xrow[m] : 0.0;
+        const double yv = m >= k ? yrow[m] : 0.0;
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const int i = lane + 32 * r;
+          if (i > m) a[r][c] = fma(-lv[r], xv, a[r][c]);  // X[i][m] -= L[i][s] X[s][m]
+          else a[r][c] = fma(-uv[r], yv, a[r][c]);        // Y[i][m] -= U[i][k] Y[k][m]
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < 8; ++c)
+#pragma unroll
+    for (int r = 0; r < 4; ++r) gt[(tc + 16 * c) * NB + lane + 32 * r] = a[r][c];
 }
 
 // ---------------------------------------------------------------------------------------
@@ -556,7 +661,7 @@ static bool g_lu_attr_set = false;
 static void lu_attrs() {
   if (g_lu_attr_set) return;
   LRS_CUDA(cudaFuncSetAttribute(lu_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)(sizeof(double) * (TILE_ELEMS + 4 * NB))));
+                                (int)DIAG_SMEM));
   LRS_CUDA(cudaFuncSetAttribute(lu_gemm_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)GEMM_SMEM));
   LRS_CUDA(cudaFuncSetAttribute(lu_rest_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -581,7 +686,7 @@ static void lu_attrs() {
 #endif
 static void real_diag(Ctx* c, cudaStream_t s, const BandGeom& g, void* tiles, int K, int* status) {
   if (LRS_LU_SKIP == 1) return;
-  lu_diag_kernel<<<g.P, DIAG_THREADS, sizeof(double) * (TILE_ELEMS + 4 * NB), s>>>(
+  lu_diag_kernel<<<g.P, DIAG_THREADS, DIAG_SMEM, s>>>(
       g, static_cast<double*>(tiles), K, status);
 }
 static void real_gemm(Ctx* c, cudaStream_t s, const BandGeom& g, void* tiles, int K, int* status,

@@ -6,16 +6,19 @@
 // B = [U(K,J); U(K+1,J)] (256 x 128).  B200 runs FP64 at 37 TF/s but INT8 at 4.5 POPS, so the
 // product is formed exactly in integers (the Ozaki splitting):
 //
-//   row i of A:     a_ik = 2^ea_i * sum_{p=1..8} 2^-7p d_p(i,k),   d_p in [-127, 127]
-//   column j of B:  b_kj = 2^eb_j * sum_{q=1..8} 2^-7q e_q(k,j)
-//   (A B)_ij = 2^(ea_i + eb_j) * sum_{s=2..9} 2^-7s G_s(i,j),   G_s = sum_{p+q=s} D_p E_q
+//   row i of A:     a_ik = 2^ea_i * sum_{p=1..7} 2^(2-8p) d_p(i,k)
+//   column j of B:  b_kj = 2^eb_j * sum_{q=1..7} 2^(2-8q) e_q(k,j)
+//   (A B)_ij = 2^(ea_i + eb_j) * sum_{s=2..8} 2^(4-8s) G_s(i,j),   G_s = sum_{p+q=s} D_p E_q
 //
-// with ea_i the binary exponent of max_k |a_ik| (so |a_ik| 2^-ea_i < 1) and each digit the
-// truncation of the running remainder times 2^7 (exact in FP64).  Eight 7-bit digits carry
-// 56 bits, so every entry within 2^-3 of its row (column) maximum is represented exactly;
-// the s <= 9 truncation drops terms below 2^-63 of the row x column scale.  Both errors are
-// of the order of FP64's own rounding bound k u max|a| max|b| for the 256-long products.
-// G_s sums <= 8 products of 256 INT8 pairs: |G_s| <= 8 * 256 * 127^2 < 2^31, exact in INT32.
+// with ea_i the binary exponent of max_k |a_ik| (so |a_ik| 2^-ea_i < 1).  The digits are
+// the balanced base-256 expansion of F = round(a_ik 2^(54 - ea_i)) (|F| < 2^54): six low
+// digits in [-128, 127] and a top digit in [-65, 65], all INT8.  54 bits represent every
+// entry within 2^-1 of its row (column) maximum exactly; balanced digits have random signs,
+// so the dropped s >= 9 terms (below 2^-68 of the row x column scale each) and the
+// rounding of F average out like FP64's own rounding: both are of the order of the
+// k u max|a| max|b| bound of the 256-long FP64 products.  G_s sums <= 7 products of 256
+// INT8 pairs: |G_s| <= 7 * 256 * 2^14 < 2^31, exact in INT32.  (The earlier 8 x 7-bit
+// sign-magnitude split needed 36 products; this one needs 28.)
 //
 // lu_i8_slice (once per step pair, on the critical-path stream): exponents and digits of
 // the whole A panel (rows I = K+2 .. K+1+wl) and B panel (columns J = K+2 .. K+1+wu),
@@ -25,13 +28,13 @@
 // lu_i8_gemm (kinds 3 / 4 of the pair schedule): a warp-specialised kernel per 128 x 128
 // output tile.  The MMA shape is M=128, N=128, K=32 (N < 128 leaves the INT8 pipe at 2/3
 // rate); 4 group accumulators of 128 INT32 columns fill the 512 TMEM columns, so a tile runs
-// two passes over K: pass A forms G_6..G_9 (26 MMAs per K chunk of 32, all 8 + 8 slices),
-// pass B G_2..G_5 (10 MMAs, slices 1-4).  Warp 0 streams the chunks (64 / 32 KB) through a
+// two passes over K: pass A forms G_5..G_8 (22 MMAs per K chunk of 32, all 7 + 7 slices),
+// pass B G_2..G_4 (6 MMAs, slices 1-3; its fourth slot is handed back at once).  Warp 0 streams the chunks (64 / 32 KB) through a
 // 3-stage TMA ring; warp 1's elected thread issues the MMAs, A slice outer so consecutive
 // MMAs reuse it from the operand collector; warps 2-9 drain each group accumulator into
 // FP64 registers (tcgen05.ld; smallest group first) and release it at once, so the next
 // pass's MMAs refill a group while the others are still being read.  After pass B they
-// subtract 2^(ea+eb) sum_s 2^-7s G_s from C.  Each CTA walks I8_TPC consecutive tiles (same
+// subtract 2^(ea+eb) sum_s 2^(4-8s) G_s from C.  Each CTA walks I8_TPC consecutive tiles (same
 // I first, so A slices are shared through L2) and retires, leaving SMs for the high-priority
 // diag / panel kernels of the look-ahead.
 #include <cstdlib>
@@ -42,11 +45,11 @@
 
 namespace lrs {
 
-constexpr int I8_S = 8;                               // digit slices per operand
+constexpr int I8_S = 7;                               // digit slices per operand
 constexpr int I8_KC = 32;                             // K per MMA and per pipeline chunk
 constexpr int I8_NCH = 2 * NB / I8_KC;                // 8 chunks over K = 256
 constexpr int I8_SL = NB * I8_KC;                     // 4096 B: one A slice of one chunk
-constexpr int I8_BLK = I8_S * I8_SL;                  // 32 KB: all A slices of one chunk
+constexpr int I8_BLK = I8_S * I8_SL;                  // 28 KB: all A slices of one chunk
 // output columns per CTA: 128 (one CTA per SM, all 512 TMEM columns) or 64 (two CTAs per SM
 // with 256 columns each, so one CTA's MMAs run while the other drains)
 #ifndef LRS_I8_TN
@@ -59,6 +62,11 @@ constexpr int I8_BBLK = I8_S * I8_BSL;                // all B slices of one chu
 constexpr int I8_STAGE = I8_BLK + I8_BBLK;            // A + B
 constexpr int I8_STAGES = I8_TN == 128 ? 3 : 2;
 constexpr int I8_GROUPS = 4;                          // accumulators per pass (4 x TN cols)
+// pass A: G_5..G_8 from slices 1..7; pass B: G_2..G_4 from slices 1..3
+__host__ __device__ constexpr int i8_base(int pass) { return pass == 0 ? 5 : 2; }  // lowest s
+__host__ __device__ constexpr int i8_ng(int pass) { return pass == 0 ? 4 : 3; }    // groups
+__host__ __device__ constexpr int i8_pmax(int pass) { return pass == 0 ? I8_S : 3; }  // slices
+constexpr int I8_PRODUCTS = 28;                       // digit-slice products per K chunk
 constexpr int I8_TMEM = I8_GROUPS * I8_TN;            // 512 or 256 columns
 constexpr int I8_EPI = 4 * I8_TN / 64;                // epilogue warps (64 columns each)
 constexpr int I8_THREADS = 32 * (2 + I8_EPI);         // producer, MMA, epilogue warps
@@ -149,27 +157,28 @@ __device__ __forceinline__ double exp2i(int e) {
   return ldexp(1.0, e);
 }
 
-// the eight 7-bit digits of x 2^-e (|x| < 2^e), sign-magnitude, straight from the bits:
-// F = |x| 2^(56 - e) is an integer (< 2^56, low bits truncated), digit p is bits
-// [56 - 7p, 63 - 7p) of F -- the digits of the exact FP64 recurrence v <- 128 v - trunc(128 v),
-// in integer ops
-__device__ __forceinline__ void digits8_bits(double x, int e, uint32_t* words, int b) {
+// the seven balanced base-256 digits of F = round(x 2^(54 - e)) (|x| < 2^e), from the bits:
+// G = F + 0x808080808080 carries the balancing, so digit 1 (the top) is G >> 48 and digits
+// 2..7 are the bytes 5..0 of G minus 128 (an xor with 0x80 as int8)
+__device__ __forceinline__ void digits7_bits(double x, int e, uint32_t* words, int b) {
   const unsigned long long bits = (unsigned long long)__double_as_longlong(x);
   const int bex = (int)((bits >> 52) & 0x7ff);
   unsigned long long mant = bits & 0xfffffffffffffull;
   int ex = bex;
   if (bex == 0) ex = 1;
   else mant |= 1ull << 52;
-  const int sh = ex - 1019 - e;  // F = mant * 2^sh
+  const int sh = ex - 1021 - e;  // x 2^(54-e) = mant * 2^sh
   unsigned long long F = 0;
-  if (mant != 0 && sh > -64) F = sh >= 0 ? mant << sh : mant >> (-sh);
-  const bool neg = (bits >> 63) != 0;
-#pragma unroll
-  for (int q = 0; q < I8_S; ++q) {
-    int d = (int)((F >> (49 - 7 * q)) & 127u);
-    d = neg ? -d : d;
-    words[q] |= (uint32_t)(uint8_t)(int8_t)d << (8 * b);
+  if (mant != 0) {
+    if (sh >= 0) F = mant << sh;  // sh <= 1: |x| < 2^e
+    else if (sh > -64) F = (mant + (1ull << (-sh - 1))) >> (-sh);  // round half up
   }
+  const long long Fs = (bits >> 63) ? -(long long)F : (long long)F;
+  const long long G = Fs + 0x808080808080ll;
+  words[0] |= (uint32_t)(uint8_t)(int8_t)(G >> 48) << (8 * b);
+#pragma unroll
+  for (int q = 1; q < I8_S; ++q)
+    words[q] |= ((uint32_t)((G >> (8 * (I8_S - 1 - q))) & 255) ^ 0x80u) << (8 * b);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -245,8 +254,8 @@ __global__ void __launch_bounds__(256) lu_i8_slice_kernel(BandGeom g, const doub
     for (int q = 0; q < I8_S; ++q) wd[q][0] = wd[q][1] = wd[q][2] = wd[q][3] = 0u;
 #pragma unroll
     for (int kk = 0; kk < 16; ++kk) {
-      uint32_t tmp[I8_S] = {0, 0, 0, 0, 0, 0, 0, 0};
-      digits8_bits(v[16 * h + kk], e, tmp, kk & 3);
+      uint32_t tmp[I8_S] = {0, 0, 0, 0, 0, 0, 0};
+      digits7_bits(v[16 * h + kk], e, tmp, kk & 3);
 #pragma unroll
       for (int q = 0; q < I8_S; ++q) wd[q][kk >> 2] |= tmp[q];
     }
@@ -293,20 +302,17 @@ __device__ __forceinline__ bool i8_decode(const BandGeom& g, int K, int t, int& 
 }
 
 // MMAs of one K chunk of one pass: A slice p outer (collector), B slice q descending, so the
-// first writes of the groups (p = 1) go to slots 3, 2, 1, 0 -- the order the epilogue
-// releases them.  PASS 0 (A): G_6..G_9; PASS 1 (B): G_2..G_5.
+// first writes of the groups (p = 1) go to slots NG-1 .. 0 -- the order the epilogue
+// releases them.  PASS 0 (A): G_5..G_8; PASS 1 (B): G_2..G_4.
 template <int PASS>
 __device__ __forceinline__ void i8_chunk_mmas(uint32_t tm, uint32_t a0, uint32_t b0, bool first,
                                               uint64_t* tempty, int u) {
-  constexpr int base = PASS == 0 ? 6 : 2;
-  constexpr int pmax = PASS == 0 ? I8_S : 4;
+  constexpr int base = i8_base(PASS), ng = i8_ng(PASS), pmax = i8_pmax(PASS);
 #pragma unroll
   for (int pp = 1; pp <= pmax; ++pp) {
-    constexpr int dummy = 0;
-    (void)dummy;
-    const int qhi = min(I8_S, base + 3 - pp), qlo = max(1, base - pp);
+    const int qhi = min(I8_S, base + ng - 1 - pp), qlo = max(1, base - pp);
 #pragma unroll
-    for (int q = 8; q >= 1; --q) {
+    for (int q = I8_S; q >= 1; --q) {
       if (q > qhi || q < qlo) continue;
       const int slot = pp + q - base;
       if (first && pp == 1 && u > 0) {
@@ -374,8 +380,8 @@ __global__ void __launch_bounds__(I8_THREADS, I8_TN == 128 ? 1 : 2)
         const uint8_t* a = pn.A + ((int64_t)p * g.wl + ia) * I8_NCH * I8_BLK;
         const uint8_t* b = pn.B + (((int64_t)p * g.wu + jb) * I8_NH + h) * I8_NCH * I8_BBLK;
         for (int pass = 0; pass < 2; ++pass) {
-          const unsigned abytes = pass == 0 ? I8_BLK : I8_BLK / 2;
-          const unsigned bbytes = pass == 0 ? I8_BBLK : I8_BBLK / 2;
+          const unsigned abytes = i8_pmax(pass) * I8_SL;
+          const unsigned bbytes = i8_pmax(pass) * I8_BSL;
           for (int kc = 0; kc < I8_NCH; ++kc, ++it) {
             const int s = it % I8_STAGES;
             if (it >= I8_STAGES) mbar_wait_trap<64>(&empty[s], ((it / I8_STAGES) & 1) ^ 1);
@@ -442,9 +448,18 @@ __global__ void __launch_bounds__(I8_THREADS, I8_TN == 128 ? 1 : 2)
             for (int slot = 0; slot < I8_GROUPS; ++slot) mbar_arrive1(&tempty[slot]);
           continue;
         }
+        if (pass == 1) {
+          // pass B leaves the top slot(s) unused: hand them to the next tile's pass A.  Safe
+          // only now -- pass B's MMAs (so tfull) needed every warp's release of the lower
+          // slots, which each warp gave after releasing the top one.
+          __syncwarp();
+          if (lane == 0)
+            for (int slot = i8_ng(1); slot < I8_GROUPS; ++slot) mbar_arrive1(&tempty[slot]);
+        }
 #pragma unroll
         for (int slot = I8_GROUPS - 1; slot >= 0; --slot) {
-          const double sc = exp2i(-7 * (slot + (pass == 0 ? 6 : 2)));
+          if (slot >= i8_ng(pass)) continue;
+          const double sc = exp2i(4 - 8 * (slot + i8_base(pass)));
 #pragma unroll
           for (int h2 = 0; h2 < 2; ++h2) {
             uint32_t v[32];
