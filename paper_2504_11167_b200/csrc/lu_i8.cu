@@ -60,21 +60,54 @@ constexpr int I8_NH = NB / I8_TN;                     // column blocks per tile
 constexpr int I8_BSL = I8_TN * I8_KC;                 // one B slice of one chunk
 constexpr int I8_BBLK = I8_S * I8_BSL;                // all B slices of one chunk
 constexpr int I8_STAGE = I8_BLK + I8_BBLK;            // A + B
-constexpr int I8_STAGES = I8_TN == 128 ? 3 : 2;
+#ifndef LRS_I8_STAGES
+#define LRS_I8_STAGES 4  // 4 x 56 KB + 2 KB barriers fit the 227 KB opt-in limit
+#endif
+constexpr int I8_STAGES = I8_TN == 128 ? LRS_I8_STAGES : 2;
 constexpr int I8_GROUPS = 4;                          // accumulators per pass (4 x TN cols)
-// pass A: G_5..G_8 from slices 1..7; pass B: G_2..G_4 from slices 1..3
-__host__ __device__ constexpr int i8_base(int pass) { return pass == 0 ? 5 : 2; }  // lowest s
-__host__ __device__ constexpr int i8_ng(int pass) { return pass == 0 ? 4 : 3; }    // groups
-__host__ __device__ constexpr int i8_pmax(int pass) { return pass == 0 ? I8_S : 3; }  // slices
+// Passes over K per tile.  Pass k forms the groups s = top(k), top(k) - 1, .. (ng(k) of them)
+// from slices 1..pmax(k).  The group accumulators take the TMEM slots as a ring: a pass
+// takes the next ng slots after the previous pass's, so while the epilogue drains one pass
+// the next pass already runs in the other slots.  3 passes (G_8,7 | G_6,5 | G_4,3,2) keep the
+// tensor pipe busy during the drains at the price of streaming slices 1..5 and 1..3 again;
+// 2 passes (G_8..5 | G_4..2) stream less but stall on the drains.  Measured on c2 (ncu launch
+// list, 128 launches): 2 passes 96.4 ms, 3 passes 107.8 ms -- the epilogue (drain + C
+// reductions, ~21k cycles per tile with 3 passes) becomes the bottleneck; 16 epilogue warps
+// of 32 columns instead of 8 of 64 (LRS_I8_EPC=32) do not change that (98.4 / 109.5 ms).
+#ifndef LRS_I8_NPASS
+#define LRS_I8_NPASS 2  // measured: 3 passes 0.84 ms vs 2 passes 0.75 ms per c2 launch
+#endif
+constexpr int I8_NP = LRS_I8_NPASS;
+static_assert(I8_NP == 2 || I8_NP == 3, "pass split");
+__host__ __device__ constexpr int i8_top(int k) {
+  return I8_NP == 3 ? (k == 0 ? 8 : k == 1 ? 6 : 4) : (k == 0 ? 8 : 4);
+}
+__host__ __device__ constexpr int i8_ng(int k) {
+  return I8_NP == 3 ? (k == 2 ? 3 : 2) : (k == 0 ? 4 : 3);
+}
+__host__ __device__ constexpr int i8_pmax(int k) { return i8_top(k) - 1 < I8_S ? i8_top(k) - 1 : I8_S; }
 constexpr int I8_PRODUCTS = 28;                       // digit-slice products per K chunk
 constexpr int I8_TMEM = I8_GROUPS * I8_TN;            // 512 or 256 columns
-constexpr int I8_EPI = 4 * I8_TN / 64;                // epilogue warps (64 columns each)
+#ifndef LRS_I8_EPC
+#define LRS_I8_EPC 64
+#endif
+constexpr int I8_EPC = LRS_I8_EPC;                    // columns per epilogue warp (64 or 32)
+constexpr int I8_EPI = 4 * I8_TN / I8_EPC;            // epilogue warps
 constexpr int I8_THREADS = 32 * (2 + I8_EPI);         // producer, MMA, epilogue warps
 constexpr int I8_TPC = 4;                             // tiles per CTA
 // LRS_I8_EXP (timing experiments only, wrong results): 1 skips the epilogue arithmetic,
 // 2 also skips the operand copies
 #ifndef LRS_I8_EXP
 #define LRS_I8_EXP 0
+#endif
+// LRS_I8_PROBE (development aid): clock64 accounting of the warp roles, printed by a few CTAs
+#ifndef LRS_I8_PROBE
+#define LRS_I8_PROBE 0
+#endif
+#if LRS_I8_PROBE
+#define PRB(...) __VA_ARGS__
+#else
+#define PRB(...)
 #endif
 constexpr size_t I8_SMEM = (size_t)I8_STAGES * I8_STAGE + 2048;
 static_assert(I8_TN == 128 || I8_SMEM * 2 <= 227 * 1024, "two CTAs per SM");
@@ -302,21 +335,22 @@ __device__ __forceinline__ bool i8_decode(const BandGeom& g, int K, int t, int& 
 }
 
 // MMAs of one K chunk of one pass: A slice p outer (collector), B slice q descending, so the
-// first writes of the groups (p = 1) go to slots NG-1 .. 0 -- the order the epilogue
-// releases them.  PASS 0 (A): G_5..G_8; PASS 1 (B): G_2..G_4.
+// first writes of the groups (p = 1) go to the pass's slots in ring order -- the order the
+// epilogue releases them.  Before its first write a slot waits for the drain of its
+// previous use (uses[slot] counts them).
 template <int PASS>
 __device__ __forceinline__ void i8_chunk_mmas(uint32_t tm, uint32_t a0, uint32_t b0, bool first,
-                                              uint64_t* tempty, int u) {
-  constexpr int base = i8_base(PASS), ng = i8_ng(PASS), pmax = i8_pmax(PASS);
+                                              uint64_t* tempty, int ptr, const int* uses) {
+  constexpr int top = i8_top(PASS), ng = i8_ng(PASS), pmax = i8_pmax(PASS);
 #pragma unroll
   for (int pp = 1; pp <= pmax; ++pp) {
-    const int qhi = min(I8_S, base + ng - 1 - pp), qlo = max(1, base - pp);
+    const int qhi = min(I8_S, top - pp), qlo = max(1, top - ng + 1 - pp);
 #pragma unroll
     for (int q = I8_S; q >= 1; --q) {
       if (q > qhi || q < qlo) continue;
-      const int slot = pp + q - base;
-      if (first && pp == 1 && u > 0) {
-        mbar_wait_trap(&tempty[slot], (u - 1) & 1);
+      const int slot = (ptr + top - pp - q) & (I8_GROUPS - 1);
+      if (first && pp == 1 && uses[slot] > 0) {
+        mbar_wait_trap(&tempty[slot], (uses[slot] - 1) & 1);
         tc_fence_after();
       }
       const uint32_t dd = tm + slot * I8_TN;
@@ -339,7 +373,9 @@ __global__ void __launch_bounds__(I8_THREADS, I8_TN == 128 ? 1 : 2)
   uint64_t* full = reinterpret_cast<uint64_t*>(smraw + I8_STAGES * I8_STAGE);
   uint64_t* empty = full + I8_STAGES;
   uint64_t* tfull = empty + I8_STAGES;
-  uint64_t* tempty = tfull + 1;  // [I8_GROUPS]: slot drained by the epilogue
+  // tfull[2]: pass u's accumulators complete, alternating by pass parity -- pass u+2 needs
+  // slots pass u's drain frees, so a barrier never completes twice ahead of its waiter
+  uint64_t* tempty = tfull + 2;  // [I8_GROUPS]: slot drained by the epilogue
   uint32_t* tbase = reinterpret_cast<uint32_t*>(tempty + I8_GROUPS);
   double* sj = reinterpret_cast<double*>(smraw + I8_STAGES * I8_STAGE + 1024);  // [128]
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -354,7 +390,8 @@ __global__ void __launch_bounds__(I8_THREADS, I8_TN == 128 ? 1 : 2)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(tfull, 1);
+    mbar_init(&tfull[0], 1);
+    mbar_init(&tfull[1], 1);
     for (int gi = 0; gi < I8_GROUPS; ++gi) mbar_init(&tempty[gi], I8_EPI);
     fence_mbar_init();
   }
@@ -370,7 +407,7 @@ __global__ void __launch_bounds__(I8_THREADS, I8_TN == 128 ? 1 : 2)
   const uint32_t tm = *tbase;
 
   if (w == 0) {
-    // ---- producer: per tile, pass A (all slices) then pass B (slices 1-4) ----------------
+    // ---- producer: per tile and pass, slices 1..pmax of every K chunk -----------------
     if (lane == 0) {
       int it = 0;
       for (int t = t0; t < t1; ++t) {
@@ -379,7 +416,7 @@ __global__ void __launch_bounds__(I8_THREADS, I8_TN == 128 ? 1 : 2)
         bulk_prefetch_l2(ctile(p, ia, jb, h), sizeof(double) * NB * I8_TN);
         const uint8_t* a = pn.A + ((int64_t)p * g.wl + ia) * I8_NCH * I8_BLK;
         const uint8_t* b = pn.B + (((int64_t)p * g.wu + jb) * I8_NH + h) * I8_NCH * I8_BBLK;
-        for (int pass = 0; pass < 2; ++pass) {
+        for (int pass = 0; pass < I8_NP; ++pass) {
           const unsigned abytes = i8_pmax(pass) * I8_SL;
           const unsigned bbytes = i8_pmax(pass) * I8_BSL;
           for (int kc = 0; kc < I8_NCH; ++kc, ++it) {
@@ -399,23 +436,37 @@ __global__ void __launch_bounds__(I8_THREADS, I8_TN == 128 ? 1 : 2)
   } else if (w == 1) {
     // ---- MMA issuer ------------------------------------------------------------------
     if (lane == 0) {
-      int it = 0, u = 0;
+      int it = 0, ptr = 0, u = 0;
+      int uses[I8_GROUPS] = {0, 0, 0, 0};
+      PRB(long long c_full = 0, c_chunk0 = 0; const long long c_start = clock64();)
       for (int t = t0; t < t1; ++t) {
         int p, ia, jb, h;
         if (!i8_decode<KIND>(g, K, t, p, ia, jb, h)) continue;
-        for (int pass = 0; pass < 2; ++pass, ++u) {
+#pragma unroll
+        for (int pass = 0; pass < I8_NP; ++pass) {
           for (int kc = 0; kc < I8_NCH; ++kc, ++it) {
             const int s = it % I8_STAGES;
+            PRB(long long c0 = clock64();)
             mbar_wait_trap(&full[s], (it / I8_STAGES) & 1);
+            PRB(c_full += clock64() - c0; c0 = clock64();)
             tc_fence_after();
             const uint32_t a0 = smem_u32(stage + s * I8_STAGE), b0 = a0 + I8_BLK;
-            if (pass == 0) i8_chunk_mmas<0>(tm, a0, b0, kc == 0, tempty, u);
-            else i8_chunk_mmas<1>(tm, a0, b0, kc == 0, tempty, u);
+            if (pass == 0) i8_chunk_mmas<0>(tm, a0, b0, kc == 0, tempty, ptr, uses);
+            else if (pass == 1) i8_chunk_mmas<1>(tm, a0, b0, kc == 0, tempty, ptr, uses);
+            else i8_chunk_mmas<2 % I8_NP>(tm, a0, b0, kc == 0, tempty, ptr, uses);
+            PRB(if (kc == 0) c_chunk0 += clock64() - c0;)
             umma_commit(&empty[s]);
           }
-          umma_commit(tfull);
+          umma_commit(&tfull[u & 1]);
+          ++u;
+#pragma unroll
+          for (int gi = 0; gi < i8_ng(pass); ++gi) ++uses[(ptr + gi) & (I8_GROUPS - 1)];
+          ptr = (ptr + i8_ng(pass)) & (I8_GROUPS - 1);
         }
       }
+      PRB(if (KIND == 4 && K == 100 && (blockIdx.x % 300) == 0) printf(
+              "PROBE mma cta %d tiles %d total %lld full_wait %lld chunk0(tempty) %lld\n",
+              blockIdx.x, t1 - t0, clock64() - c_start, c_full, c_chunk0);)
     }
   } else {
     // ---- epilogue: warp w drains TMEM lanes 32 (w % 4).. (rows) and column half
@@ -423,50 +474,49 @@ __global__ void __launch_bounds__(I8_THREADS, I8_TN == 128 ? 1 : 2)
     // exact), so a conversion is an xor and an FP64 add instead of an XU I2F.
     const int qd = w & 3, ch = (w - 2) >> 2, i = 32 * qd + lane;
     constexpr double BIAS = 4503601774854144.0;  // 2^52 + 2^31
-    int u = 0;
+    int u = 0, ptr = 0;
+    PRB(long long c_tf = 0, c_drain = 0, c_red = 0; const long long c_start = clock64();)
     for (int t = t0; t < t1; ++t) {
       int p, ia, jb, h;
       if (!i8_decode<KIND>(g, K, t, p, ia, jb, h)) continue;
-      double* C = ctile(p, ia, jb, h) + (int64_t)ch * 64 * NB;
+      double* C = ctile(p, ia, jb, h) + (int64_t)ch * I8_EPC * NB;
       const double si = exp2i(pn.ea[((int64_t)p * g.wl + ia) * NB + i]);
       if (w == 2) {  // the previous tile's readers of sj passed the closing barrier
         const int* eb = pn.eb + ((int64_t)p * g.wu + jb) * NB + h * I8_TN;
 #pragma unroll
         for (int r = 0; r < I8_TN / 32; ++r) sj[lane + 32 * r] = exp2i(eb[lane + 32 * r]);
       }
-      const uint32_t trow = tm + ((uint32_t)(32 * qd) << 16) + ch * 64;
-      double acc[64];
+      const uint32_t trow = tm + ((uint32_t)(32 * qd) << 16) + ch * I8_EPC;
+      double acc[I8_EPC];
 #pragma unroll
-      for (int j = 0; j < 64; ++j) acc[j] = 0.0;
+      for (int j = 0; j < I8_EPC; ++j) acc[j] = 0.0;
 #pragma unroll
-      for (int pass = 0; pass < 2; ++pass, ++u) {
-        mbar_wait_trap<128>(tfull, u & 1);
+      for (int pass = 0; pass < I8_NP; ++pass, ++u) {
+        PRB(long long c0 = clock64();)
+        mbar_wait_trap<128>(&tfull[u & 1], (u >> 1) & 1);
+        PRB(c_tf += clock64() - c0; c0 = clock64();)
         tc_fence_after();
         if (LRS_I8_EXP == 3) {
           __syncwarp();
           if (lane == 0)
-            for (int slot = 0; slot < I8_GROUPS; ++slot) mbar_arrive1(&tempty[slot]);
+            for (int gi = 0; gi < i8_ng(pass); ++gi)
+              mbar_arrive1(&tempty[(ptr + gi) & (I8_GROUPS - 1)]);
+          ptr = (ptr + i8_ng(pass)) & (I8_GROUPS - 1);
           continue;
         }
-        if (pass == 1) {
-          // pass B leaves the top slot(s) unused: hand them to the next tile's pass A.  Safe
-          // only now -- pass B's MMAs (so tfull) needed every warp's release of the lower
-          // slots, which each warp gave after releasing the top one.
-          __syncwarp();
-          if (lane == 0)
-            for (int slot = i8_ng(1); slot < I8_GROUPS; ++slot) mbar_arrive1(&tempty[slot]);
-        }
+        // drain in ring order (the next pass reuses the first slots first), smallest
+        // group weight first for the FP64 accumulation
 #pragma unroll
-        for (int slot = I8_GROUPS - 1; slot >= 0; --slot) {
-          if (slot >= i8_ng(pass)) continue;
-          const double sc = exp2i(4 - 8 * (slot + i8_base(pass)));
+        for (int gi = 0; gi < i8_ng(pass); ++gi) {
+          const int slot = (ptr + gi) & (I8_GROUPS - 1);
+          const double sc = exp2i(4 - 8 * (i8_top(pass) - gi));
 #pragma unroll
-          for (int h2 = 0; h2 < 2; ++h2) {
+          for (int h2 = 0; h2 < I8_EPC / 32; ++h2) {
             uint32_t v[32];
 #pragma unroll
             for (int c8 = 0; c8 < 32; c8 += 8) tmem_ld8(trow + slot * I8_TN + h2 * 32 + c8, v + c8);
             tmem_ld_wait();
-            if (h2 == 1) {  // this warp's part of the slot is in registers: release it
+            if (h2 == I8_EPC / 32 - 1) {  // the warp's part of the slot is in registers: release it
               tc_fence_before();
               __syncwarp();
               if (lane == 0) mbar_arrive1(&tempty[slot]);
@@ -478,17 +528,24 @@ __global__ void __launch_bounds__(I8_THREADS, I8_TN == 128 ? 1 : 2)
                   acc[h2 * 32 + j]);
           }
         }
+        ptr = (ptr + i8_ng(pass)) & (I8_GROUPS - 1);
+        PRB(c_drain += clock64() - c0;)
       }
+      PRB(long long c1 = clock64();)
       asm volatile("bar.sync 1, %0;" ::"n"(32 * I8_EPI) : "memory");  // sj written
       // C -= 2^(ea+eb) acc as fire-and-forget L2 reductions: no load round trip in the
       // epilogue, and with one contribution per element fl(c + (-r)) == fl(c - r) exactly
       if (!LRS_I8_EXP) {
 #pragma unroll
-        for (int j = 0; j < 64; ++j)
-          red_add_f64(C + (int64_t)j * NB + i, -(acc[j] * si * sj[ch * 64 + j]));
+        for (int j = 0; j < I8_EPC; ++j)
+          red_add_f64(C + (int64_t)j * NB + i, -(acc[j] * si * sj[ch * I8_EPC + j]));
       }
       asm volatile("bar.sync 1, %0;" ::"n"(32 * I8_EPI) : "memory");  // sj free for the next tile
+      PRB(c_red += clock64() - c1;)
     }
+    PRB(if (KIND == 4 && K == 100 && (blockIdx.x % 300) == 0 && lane == 0 && (w == 2 || w == 9))
+            printf("PROBE epi cta %d warp %d total %lld tfull_wait %lld drain %lld red %lld\n",
+                   blockIdx.x, w, clock64() - c_start, c_tf, c_drain, c_red);)
   }
   tc_fence_before();
   __syncthreads();
