@@ -65,7 +65,7 @@ typedef enum lrs_status {
   LRS_ERR_CUDA = 11,
   LRS_ERR_OOM = 12,
   LRS_ERR_NCCL = 13,
-  LRS_ERR_NOT_IMPLEMENTED = 14,           /* e.g. a block that needs row interchanges */
+  LRS_ERR_NOT_IMPLEMENTED = 14,           /* an option outside the GPU path (e.g. FP32 factors of pivoted blocks) */
   LRS_ERR_PRECOND_FAILURE = 15            /* LR-SPIKE-I inner solve did not converge */
 } lrs_status;
 

@@ -10,6 +10,7 @@
 #include "common.cuh"
 #include "kernels.h"
 #include "lrs_internal.h"
+#include "lu_common.cuh"
 
 namespace lrs {
 
@@ -105,38 +106,7 @@ __global__ void __launch_bounds__(512, 1) lu_diag_z_kernel(BandGeom g, zc* tiles
     }
     __syncthreads();
   }
-  const int half = tid >> 8, q = (tid >> 7) & 1;
-  zc* pq = part + (half * 2 + q) * NB;
-  for (int s = 0; s < NB; ++s) {
-    zc ujj_inv = {0.0, 0.0};
-    if (half == 0) {
-      const int j = s;
-      zc t = {0.0, 0.0};
-      if (i < j)
-        for (int kk = i + q; kk < j; kk += 2) t = s_fma(A[kk * NB + i], A[j * NB + kk], t);
-      pq[i] = t;
-      ujj_inv = s_inv(A[j * NB + j]);
-    } else {
-      const int j = NB - 1 - s;
-      zc t = {0.0, 0.0};
-      if (i > j)
-        for (int kk = j + 1 + q; kk < i; kk += 2) t = s_fma(A[kk * NB + i], A[j * NB + kk], t);
-      pq[i] = t;
-    }
-    __syncthreads();
-    if (q == 0) {
-      if (half == 0) {
-        const int j = s;
-        if (i < j) A[j * NB + i] = s_neg(s_mul(ujj_inv, s_add(part[i], part[NB + i])));
-        else if (i == j) A[j * NB + j] = ujj_inv;
-      } else {
-        const int j = NB - 1 - s;
-        if (i > j)
-          A[j * NB + i] = s_neg(s_add(A[j * NB + i], s_add(part[2 * NB + i], part[3 * NB + i])));
-      }
-    }
-    __syncthreads();
-  }
+  diag_inverses_z(A, part, tid);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -284,6 +254,11 @@ __global__ void __launch_bounds__(ZG_THREADS, 1) lu_zgemm_kernel(BandGeom g, zc*
       ztile_gemm<0, ZMASK_UNIT_LOWER, ZMASK_NONE>(tile(K, K), tile(K, J), tile(K, J), nbase, sm,
                                                   nullptr, 0, nullptr);
     }
+  } else if (KIND == 5) {  // U_KJ only (the pivoting path factors L_IK in its panel)
+    const int J = K + 1 + x;
+    if (J >= T) return;
+    ztile_gemm<0, ZMASK_UNIT_LOWER, ZMASK_NONE>(tile(K, K), tile(K, J), tile(K, J), nbase, sm,
+                                                nullptr, 0, nullptr);
   } else if (KIND == 1) {
     const int I = K + 2 + x / (g.wu - 1);
     const int J = K + 2 + x % (g.wu - 1);
@@ -314,6 +289,8 @@ static void z_gemm(Ctx* c, cudaStream_t s, const BandGeom& g, void* tiles, int K
   zc* t = static_cast<zc*>(tiles);
   if (kind == 0)
     lu_zgemm_kernel<0><<<dim3(2 * (g.wl + g.wu), g.P), ZG_THREADS, ZGEMM_SMEM, s>>>(g, t, K, status);
+  else if (kind == 5)
+    lu_zgemm_kernel<5><<<dim3(2 * g.wu, g.P), ZG_THREADS, ZGEMM_SMEM, s>>>(g, t, K, status);
   else if (kind == 1)
     lu_zgemm_kernel<1><<<dim3(2 * (g.wl - 1) * (g.wu - 1), g.P), ZG_THREADS, ZGEMM_SMEM, s>>>(
         g, t, K, status);
@@ -322,7 +299,7 @@ static void z_gemm(Ctx* c, cudaStream_t s, const BandGeom& g, void* tiles, int K
                                                                                        status);
 }
 
-void launch_band_lu_z(Ctx* c, const BandGeom& g, zc* tiles, int Tmax, int* status) {
+static void zgemm_attrs() {
   static bool attr = false;
   if (!attr) {
     LRS_CUDA(cudaFuncSetAttribute(lu_zgemm_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -331,9 +308,43 @@ void launch_band_lu_z(Ctx* c, const BandGeom& g, zc* tiles, int Tmax, int* statu
                                   (int)ZGEMM_SMEM));
     LRS_CUDA(cudaFuncSetAttribute(lu_zgemm_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)ZGEMM_SMEM));
+    LRS_CUDA(cudaFuncSetAttribute(lu_zgemm_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)ZGEMM_SMEM));
     attr = true;
   }
+}
+
+void launch_band_lu_z(Ctx* c, const BandGeom& g, zc* tiles, int Tmax, int* status) {
+  zgemm_attrs();
   run_band_lu(c, g, tiles, Tmax, status, LuKernels{z_diag, z_gemm});
+}
+
+// Partial-pivoting complex band LU (zgbtrf): the panel kernels of band_lu_piv.cu, then
+// U_KJ and the trailing update on the complex DMMA kernels; one stream, no look-ahead.
+void launch_band_lu_piv_z(Ctx* c, const BandGeom& g, zc* tiles, int Tmax, int* status, int* ipiv,
+                          int* perm) {
+  zgemm_attrs();
+  cudaStream_t s = c->stream;
+  for (int K = 0; K < Tmax; ++K) {
+    launch_lu_panel_piv_z(c, s, g, tiles, K, ipiv, perm, status);
+    if (g.wu > 0) {
+      ProfScope ps_(c, K_LU_PANEL, s);
+      z_gemm(c, s, g, tiles, K, status, 5);
+      LRS_LAUNCHED(c);
+    }
+    if (g.wl > 0 && g.wu > 0) {
+      {
+        ProfScope ps_(c, K_LU_PANEL, s);
+        z_gemm(c, s, g, tiles, K, status, 2);
+        LRS_LAUNCHED(c);
+      }
+      if (g.wl > 1 && g.wu > 1) {
+        ProfScope ps_(c, K_LU_UPDATE, s);
+        z_gemm(c, s, g, tiles, K, status, 1);
+        LRS_LAUNCHED(c);
+      }
+    }
+  }
 }
 
 }  // namespace lrs

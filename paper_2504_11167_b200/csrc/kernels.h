@@ -82,6 +82,13 @@ void launch_band_lu_piv(Ctx* c, const BandGeom& g, double* tiles, int Tmax, int*
 void launch_lu_panel_piv(Ctx* c, cudaStream_t s, const BandGeom& g, double* tiles, int K,
                          int* ipiv, int* perm, int* status);
 size_t piv_perm_ints(int64_t total_rowtiles);
+// complex128 (zgbtrf / zgbtrs): the same over zc tiles; the transposed L solve is L^H
+void launch_band_lu_piv_z(Ctx* c, const BandGeom& g, zc* tiles, int Tmax, int* status, int* ipiv,
+                          int* perm);
+void launch_lu_panel_piv_z(Ctx* c, cudaStream_t s, const BandGeom& g, zc* tiles, int K,
+                           int* ipiv, int* perm, int* status);
+void launch_piv_lsolve_z(Ctx* c, const BandGeom& g, const zc* tiles, const int* perm, int Tmax,
+                         bool transposed, zc* x, int64_t ld, int nrhs, int p_only);
 // forward L (transposed = false) or backward L^T solve with the interleaved interchanges
 void launch_piv_lsolve(Ctx* c, const BandGeom& g, const double* tiles, const int* perm, int Tmax,
                        bool transposed, double* x, int64_t ld, int nrhs, int p_only);

@@ -160,13 +160,15 @@ void dstage_t(Fact* f, S* x, int64_t ld, int nrhs, bool adjoint, int p_only) {
     S* xc = x + (int64_t)c0 * ld;
     for (int half = 0; half < 2; ++half) {
       const int mode = adjoint ? 2 + half : half;
-      if constexpr (!IsC<S>::value) {
-        // with row interchanges the L sweeps interleave the permutations (dgbtrs)
-        if (f->pivoted && (mode == 0 || mode == 3)) {
+      // with row interchanges the L sweeps interleave the permutations (?gbtrs)
+      if (f->pivoted && (mode == 0 || mode == 3)) {
+        if constexpr (IsC<S>::value)
+          launch_piv_lsolve_z(f->ctx, g, sp<zc>(f->tiles), f->perm.get(), f->Tmax, mode == 3, xc,
+                              ld, nr, p_only);
+        else
           launch_piv_lsolve(f->ctx, g, f->tiles.get(), f->perm.get(), f->Tmax, mode == 3, xc, ld,
                             nr, p_only);
-          continue;
-        }
+        continue;
       }
       if constexpr (IsC<S>::value)
         launch_band_solve_z(f->ctx, g, sp<zc>(f->tiles), mode, xc, ld, nr, f->flags.get(),
@@ -858,23 +860,21 @@ Fact* factorize(Ctx* c, Mat* m, const lrs_solver_cfg& cfg, const lrs_comm* comm)
   if (first_problem(0).first >= 0) {
     // dgbtrf would interchange rows: redo the blocks with partial pivoting (upper band
     // widened by kl for the fill of the interchanges)
-    if (cplx) {
-      const auto pr = first_problem(0);
-      LrsError e(LRS_ERR_NOT_IMPLEMENTED,
-                 "block " + std::to_string(pr.first) + " needs a row interchange at column " +
-                     std::to_string(pr.second) +
-                     " (partial pivoting); the complex128 interchange path is not implemented");
-      e.column = pr.second;
-      throw e;
-    }
     setup_tiles(f->ku + f->kl);
     g = f->geom();
-    launch_extract_tiles(c, m, g, f->tiles.get(), f->k, f->row_lo, f->row_hi, f->bad.get());
+    if (cplx)
+      launch_extract_tiles_z(c, m, g, sp<zc>(f->tiles), f->k, f->row_lo, f->row_hi, f->bad.get());
+    else
+      launch_extract_tiles(c, m, g, f->tiles.get(), f->k, f->row_lo, f->row_hi, f->bad.get());
     f->pivoted = true;
     f->ipiv.alloc((size_t)f->total_rowtiles * NB);
     f->perm.alloc(piv_perm_ints(f->total_rowtiles));
-    launch_band_lu_piv(c, g, f->tiles.get(), f->Tmax, f->status.get(), f->ipiv.get(),
-                       f->perm.get());
+    if (cplx)
+      launch_band_lu_piv_z(c, g, sp<zc>(f->tiles), f->Tmax, f->status.get(), f->ipiv.get(),
+                           f->perm.get());
+    else
+      launch_band_lu_piv(c, g, f->tiles.get(), f->Tmax, f->status.get(), f->ipiv.get(),
+                         f->perm.get());
   }
   LRS_CUDA(cudaEventRecord(e1, c->stream));
   if (cfg.factor_fp32) {

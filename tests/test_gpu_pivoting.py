@@ -79,3 +79,60 @@ def test_zero_diagonal_needs_interchange(ctx):
     assert F.info["pivoted"] == 1
     R = np.asfortranarray(np.arange(8.0).reshape(8, 1))
     assert _rel(F.solve_block(0, R), np.linalg.solve(M.toarray(), R)) < 1e-14
+
+
+def _band_z(n, k, seed):
+    """complex128 analogue of _band: random complex band, rows scaled by 10^U[-1.5, 1.5],
+    row-dominant diagonal -- zgbtrf (izamax: |Re| + |Im|) interchanges in every block."""
+    rng = np.random.default_rng(seed)
+    offs = [d for d in range(-k, k + 1) if d != 0]
+    A = sp.diags([rng.standard_normal(n - abs(d)) + 1j * rng.standard_normal(n - abs(d))
+                  for d in offs], offs, shape=(n, n)).tocsr()
+    A = (sp.diags(10.0 ** rng.uniform(-1.5, 1.5, n)) @ A).tocsr()
+    d = np.asarray(abs(A).sum(axis=1)).ravel() * 1.2 + 1e-3
+    ph = np.exp(1j * rng.uniform(0, 2 * np.pi, n))
+    return (A + sp.diags(d * ph)).tocsr()
+
+
+@pytest.mark.parametrize("n,k,P", [(1200, 40, 3), (4000, 300, 4)])
+def test_pivoted_complex_block_solves_match_lapack(ctx, n, k, P):
+    S = _band_z(n, k, 13)
+    lay = O.make_layout(n, P, k)
+    blocks = O.extract_blocks(S, lay)
+    fos = [O.factorize_block(Ai) for Ai in blocks.A]
+    assert all(fo.swaps > 0 for fo in fos)
+    F = api.factorize(ctx, _gpu(ctx, S), api.SolverConfig(variant="BJ", p=P, k=k, n_svd=0))
+    assert F.info["pivoted"] == 1
+    rng = np.random.default_rng(4)
+    for i in range(P):
+        R = np.asfortranarray(rng.standard_normal((lay.sizes[i], 3))
+                              + 1j * rng.standard_normal((lay.sizes[i], 3)))
+        X = F.solve_block(i, R)
+        assert _rel(X, O.solve_block(fos[i], R)) < 1e-10
+        assert _rel(F.solve_block_adjoint(i, R), O.solve_block_adjoint(fos[i], R)) < 1e-10
+        Ad = blocks.A[i].toarray()
+        assert _rel(Ad @ X, R) < 1e-9
+        assert _rel(Ad.conj().T @ F.solve_block_adjoint(i, R), R) < 1e-9
+        assert np.array_equal(X[:, 2], F.solve_block(i, R[:, 2:3])[:, 0])
+
+
+def test_pivoted_complex_lowrank_solve_parity(ctx):
+    n, k, P = 5000, 100, 4
+    S = _band_z(n, k, 7)
+    rng = np.random.default_rng(1)
+    b = np.asfortranarray(rng.uniform(-1, 1, (n, 2)) + 1j * rng.uniform(-1, 1, (n, 2)))
+    gc = api.SolverConfig(variant="T", p=P, k=k, n_svd=16, seed=3)
+    oc = O.SolverConfig(variant="T", p=P, k=k, n_svd=16, seed=3)
+    A = _gpu(ctx, S)
+    F = api.factorize(ctx, A, gc)
+    Fo = O.factorize(S, oc)
+    assert F.info["pivoted"] == 1
+    f = np.asfortranarray(rng.standard_normal((n, 2)) + 1j * rng.standard_normal((n, 2)))
+    assert _rel(F.apply_precond_T(f), O.apply_precond_T(Fo, f)) < 1e-9
+    it = api.IterConfig(tol=1e-9, method="gmres", restart=40, max_iters=600)
+    x, rep, _ = api.solve(A, b, it=it, F=F)
+    xo, repo, _ = O.solve(S, b, oc, O.IterConfig(tol=1e-9, restart=40, max_iters=600),
+                          method="gmres", F=Fo)
+    assert rep.converged and repo.converged
+    assert abs(rep.iterations - repo.iterations) <= 2
+    assert _rel(x, xo) <= 1e-8
