@@ -309,8 +309,8 @@ def run_ours(args):
     # K = j / 128) the rank-1 update of rows and columns beyond the look-ahead row/column
     # (>= K + 2; >= K0 + 3 for the two-step launches of steps K0, K0 + 1); the look-ahead
     # rows/columns are critical-path work timed with the panel
-    lu_upd_flops = sum(_rest_update_flops(s, info["kl"], info["ku"], info["nb"],
-                                          bool(info.get("lu_pairs", 0)))
+    lu_steps = int(info.get("lu_pairs", 0))
+    lu_upd_flops = sum(_rest_update_flops(s, info["kl"], info["ku"], info["nb"], lu_steps)
                        for s in _partition_sizes(cfg.matrix.n, cfg.P))
     per_launch_flops = lu_upd_flops * args.steps / max(upd_n, 1)
     avg_launch_s = upd_ms / max(upd_n, 1) / 1e3
@@ -327,15 +327,16 @@ def run_ours(args):
         apply_ms_each = (kt["band_solve"][0] + kt["iface_apply"][0] + kt["recovery"][0]) / 1.0
     total_ms = sum(v[0] for v in kt.values())
     if info.get("lu_int8"):
-        # INT8 ops the launch issues: 28 digit-slice products (M = N = 128, K = 256) per
-        # 128 x 128 tile of the bulk update
-        tiles = sum(_i8_bulk_tiles(s, info["wl"], info["wu"], info["nb"])
+        # INT8 ops the launch issues: 28 digit-slice products (M = N = 128, K = 128 x steps)
+        # per 128 x 128 tile of the bulk update
+        tiles = sum(_i8_bulk_tiles(s, info["wl"], info["wu"], info["nb"], lu_steps)
                     for s in _partition_sizes(cfg.matrix.n, cfg.P))
-        ops_launch = tiles * args.steps * 2.0 * 128 * 128 * 256 * I8_PRODUCTS / max(upd_n, 1)
+        ops_launch = (tiles * args.steps * 2.0 * 128 * 128 * 128 * lu_steps * I8_PRODUCTS /
+                      max(upd_n, 1))
         achieved_tops = ops_launch / avg_launch_s / 1e12 if upd_n else 0.0
         roofline = {"bound": "tensor",
-                    "kernel": "lu_i8_gemm_kernel<4> (INT8-sliced FP64 two-step trailing update, "
-                              "tcgen05.mma kind::i8)",
+                    "kernel": f"lu_i8_gemm_kernel<4, {lu_steps}> (INT8-sliced FP64 {lu_steps}-step "
+                              "trailing update, tcgen05.mma kind::i8)",
                     "achieved": achieved_tops, "peak": i8_peak, "unit": "TOPS (int8)",
                     "frac": achieved_tops / i8_peak if i8_peak else None,
                     "peak_source": "in-run INT8 tcgen05 microbenchmark (M=128, N=256, resident "
@@ -401,24 +402,24 @@ def run_ours(args):
     return 0
 
 
-def _rest_update_flops(s, kl, ku, nb=128, pairs=False):
+def _rest_update_flops(s, kl, ku, nb=128, steps=0):
     j = np.arange(s, dtype=np.int64)
     K = j // nb
-    # single steps: rows/cols >= K + 2; two-step (rank-256) launches for the pair (K0, K0+1),
-    # K0 even: rows/cols >= K0 + 4 (look-ahead depth 2)
-    lo = (K + (np.where(K % 2 == 0, 4, 3) if pairs else 2)) * nb
+    # single steps: rows/cols >= K + 2; D-step launches (D = 2: rank 256, D = 4: rank 512) for
+    # steps K0 .. K0+D-1, K0 = K - K % D: rows/cols >= K0 + 2D (look-ahead depth D)
+    lo = ((K - K % steps + 2 * steps) if steps else K + 2) * nb
     ni = np.clip(np.minimum(j + kl, s - 1) - np.maximum(j + 1, lo) + 1, 0, None).astype(np.float64)
     nc = np.clip(np.minimum(j + ku, s - 1) - np.maximum(j + 1, lo) + 1, 0, None).astype(np.float64)
     return float(2.0 * np.sum(ni * nc))
 
 
-def _i8_bulk_tiles(s, wl, wu, nb=128):
-    """128 x 128 tiles of the INT8 bulk launches (I, J >= K + 4 of each pair (K, K + 1))."""
+def _i8_bulk_tiles(s, wl, wu, nb=128, steps=2):
+    """128 x 128 tiles of the INT8 bulk launches (I, J >= K + 2D of each D-step update)."""
     T = -(-s // nb)
     tot = 0
-    for K in range(0, T - 1, 2):
-        ni = max(0, min(K + 1 + wl, T - 1) - (K + 4) + 1)
-        nj = max(0, min(K + 1 + wu, T - 1) - (K + 4) + 1)
+    for K in range(0, T, steps):
+        ni = max(0, min(K + steps - 1 + wl, T - 1) - (K + 2 * steps) + 1)
+        nj = max(0, min(K + steps - 1 + wu, T - 1) - (K + 2 * steps) + 1)
         tot += ni * nj
     return tot
 

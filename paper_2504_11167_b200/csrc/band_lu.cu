@@ -109,6 +109,9 @@ void launch_extract_tiles(Ctx* c, const Mat* m, const BandGeom& g, double* tiles
 // compile-time r / c only (the step loops are unrolled over 16- / 32-step blocks).
 // ---------------------------------------------------------------------------------------
 constexpr int DIAG_THREADS = 512;
+#ifndef LRS_DIAG_EXP
+#define LRS_DIAG_EXP 0  // 1: skip the inverses (timing only, wrong factors)
+#endif
 constexpr size_t DIAG_SMEM = sizeof(double) * (TILE_ELEMS + 4 * NB);
 
 __global__ void __launch_bounds__(DIAG_THREADS, 1) lu_diag_kernel(BandGeom g, double* tiles,
@@ -139,13 +142,14 @@ __global__ void __launch_bounds__(DIAG_THREADS, 1) lu_diag_kernel(BandGeom g, do
       double* urow = lcol + NB;
       if (tc == jj) {  // the warp owning column j: multipliers below the pivot
         const double piv = __shfl_sync(0xffffffffu, a[rs][jb], j & 31);
+        const double rpiv = 1.0 / piv;  // dgbtf2 scales the column by 1 / pivot (dscal)
 #pragma unroll
         for (int r = rs; r < 4; ++r) {
           const int i = lane + 32 * r;
           if (i > j) {
             const double v = a[r][jb];
             if (fabs(v) > fabs(piv)) atomicMin(&status[2 * p], col0 + j);  // dgbtrf would swap
-            a[r][jb] = v / piv;
+            a[r][jb] = v * rpiv;
             lcol[i] = a[r][jb];
           }
         }
@@ -181,6 +185,9 @@ __global__ void __launch_bounds__(DIAG_THREADS, 1) lu_diag_kernel(BandGeom g, do
     for (int r = 0; r < 4; ++r) a[r][c] = (lane + 32 * r == tc + 16 * c) ? 1.0 : 0.0;
   __syncthreads();
 
+#if LRS_DIAG_EXP == 1
+  return;  // timing experiment: LU only
+#endif
   // ---- inverses: step s forward for L (row s of inv(L) final), backward for U (row
   // k = 127 - s of inv(U) final after the division by u_kk) ----------------------------
 #pragma unroll
@@ -200,35 +207,48 @@ __global__ void __launch_bounds__(DIAG_THREADS, 1) lu_diag_kernel(BandGeom g, do
           else if (m == s) xrow[m] = 1.0;  // (s, s) holds the U side
         }
       }
-      if (lane == (k & 31)) {  // row k of inv(U): divide the finished right-hand side
-        const double ukk = A[k * NB + k];
+      if (lane == (k & 31)) {  // row k of inv(U): scale the finished right-hand side
+        const double rkk = 1.0 / A[k * NB + k];
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
           const int m = tc + 16 * c;
           if (m >= k) {
-            a[rb][c] = a[rb][c] / ukk;
+            a[rb][c] = a[rb][c] * rkk;
             yrow[m] = a[rb][c];
           }
         }
       }
       __syncthreads();
+      // Only the register blocks the step can touch, classified at compile time: the X
+      // update needs rows i > s (r >= sb) and columns m <= s (c <= 2 sb + 1), the Y update
+      // rows i < k (r <= rb) and columns m >= k (c >= 2 rb); block (r, c) is entirely
+      // lower (i > m) when 32 r - 16 c >= 16, entirely upper when c >= 2 r + 2.
       double lv[4], uv[4];
 #pragma unroll
       for (int r = 0; r < 4; ++r) {
         const int i = lane + 32 * r;
-        lv[r] = i > s ? A[s * NB + i] : 0.0;  // L[i][s]
-        uv[r] = i < k ? A[k * NB + i] : 0.0;  // U[i][k]
+        lv[r] = (r >= sb && i > s) ? A[s * NB + i] : 0.0;  // L[i][s]
+        uv[r] = (r <= rb && i < k) ? A[k * NB + i] : 0.0;  // U[i][k]
       }
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
         const int m = tc + 16 * c;
-        const double xv = m <= s ? xrow[m] : 0.0;
-        const double yv = m >= k ? yrow[m] : 0.0;
+        const bool cx = c <= 2 * sb + 1, cy = c >= 2 * rb;
+        const double xv = (cx && m <= s) ? xrow[m] : 0.0;
+        const double yv = (cy && m >= k) ? yrow[m] : 0.0;
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
-          const int i = lane + 32 * r;
-          if (i > m) a[r][c] = fma(-lv[r], xv, a[r][c]);  // X[i][m] -= L[i][s] X[s][m]
-          else a[r][c] = fma(-uv[r], yv, a[r][c]);        // Y[i][m] -= U[i][k] Y[k][m]
+          const bool lower = 32 * r - 16 * c >= 16, upper = c >= 2 * r + 2;
+          const bool ex = cx && r >= sb && !upper, ey = cy && r <= rb && !lower;
+          if (ex && ey) {
+            const int i = lane + 32 * r;
+            if (i > m) a[r][c] = fma(-lv[r], xv, a[r][c]);  // X[i][m] -= L[i][s] X[s][m]
+            else a[r][c] = fma(-uv[r], yv, a[r][c]);        // Y[i][m] -= U[i][k] Y[k][m]
+          } else if (ex) {
+            if (lower || lane + 32 * r > m) a[r][c] = fma(-lv[r], xv, a[r][c]);
+          } else if (ey) {
+            if (upper || lane + 32 * r <= m) a[r][c] = fma(-uv[r], yv, a[r][c]);
+          }
         }
       }
     }
@@ -481,7 +501,8 @@ __device__ __forceinline__ void tile_gemm_pair(const double* A0, const double* B
 
 template <int KIND>
 __global__ void __launch_bounds__(GEMM_THREADS, GEMM_SPLIT) lu_gemm_kernel(BandGeom g, double* tiles,
-                                                                           int K, int* status) {
+                                                                           int K, int* status,
+                                                                           int m = 0) {
   extern __shared__ double sm[];
   const int p = blockIdx.y;
   const int T = g.T[p];
@@ -514,6 +535,21 @@ __global__ void __launch_bounds__(GEMM_THREADS, GEMM_SPLIT) lu_gemm_kernel(BandG
     // trailing update away from the next pivot row/column: I, J >= K + 2
     const int I = K + 2 + x / (g.wu - 1);
     const int J = K + 2 + x % (g.wu - 1);
+    if (I >= T || J >= T) return;
+    tile_gemm<1, MASK_NONE, MASK_NONE>(tile(I, K), tile(K, J), tile(I, J), sm, nullptr, 0, h);
+  } else if (KIND == 6) {
+    // quad schedule, inside the look-ahead quad: step K applied to rows / columns
+    // K+1 .. K+m only -- columns K+1..K+m (I = K+1..K+wl) and rows K+1..K+m
+    // (J = K+m+1..K+wu); the rest of the trailing matrix waits for the bulk update
+    int I, J;
+    if (x < m * g.wl) {
+      I = K + 1 + x % g.wl;
+      J = K + 1 + x / g.wl;
+    } else {
+      const int y = x - m * g.wl;
+      I = K + 1 + y / (g.wu - m);
+      J = K + m + 1 + y % (g.wu - m);
+    }
     if (I >= T || J >= T) return;
     tile_gemm<1, MASK_NONE, MASK_NONE>(tile(I, K), tile(K, J), tile(I, J), sm, nullptr, 0, h);
   } else if (KIND == 2) {
@@ -676,6 +712,8 @@ static void lu_attrs() {
                                 (int)GEMM_SMEM));
   LRS_CUDA(cudaFuncSetAttribute(lu_gemm_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)GEMM_SMEM));
+  LRS_CUDA(cudaFuncSetAttribute(lu_gemm_kernel<6>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)GEMM_SMEM));
   g_lu_attr_set = true;
 }
 
@@ -694,7 +732,11 @@ static void real_gemm(Ctx* c, cudaStream_t s, const BandGeom& g, void* tiles, in
   double* t = static_cast<double*>(tiles);
   constexpr int S = GEMM_SPLIT;
   if ((LRS_LU_SKIP == 4 && kind == 4) || (LRS_LU_SKIP == 1 && kind != 4)) return;
-  if (kind == 0)
+  if (kind > 60) {  // kind 60 + m: rows / columns K+1 .. K+m with step K (quad look-ahead)
+    const int m = kind - 60;
+    lu_gemm_kernel<6><<<dim3(S * m * (g.wl + g.wu - m), g.P), GEMM_THREADS, GEMM_SMEM, s>>>(
+        g, t, K, status, m);
+  } else if (kind == 0)
     lu_gemm_kernel<0><<<dim3(S * (g.wl + g.wu), g.P), GEMM_THREADS, GEMM_SMEM, s>>>(g, t, K, status);
   else if (kind == 1 && LRS_LU_PERSISTENT) {
     // each CTA takes at most LRS_REST_TPC half-tiles and retires, so the high-priority
@@ -770,24 +812,35 @@ bool lu_real_pairs(const BandGeom& g) {
 // The two-step updates (kinds 3 / 4) run integer-sliced on the INT8 tensor cores (lu_i8.cu)
 // unless LRS_LU_I8=0, the band is too narrow for the pair schedule, or the two panel
 // buffers would take more than a quarter of the free device memory.
-static bool lu_i8_wanted(const BandGeom& g, const LuKernels& L) {
+static bool lu_i8_wanted(const BandGeom& g, const LuKernels& L, int steps) {
   const char* e = std::getenv("LRS_LU_I8");
   if (e && e[0] == '0') return false;
   if (!lu_uses_pairs(g, L)) return false;
   size_t fr = 0, tot = 0;
   if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) return false;
-  return 2 * lu_i8_panel_bytes(g) < fr / 4;
+  return 2 * lu_i8_panel_bytes(g, steps) < fr / 4;
+}
+// LRS_LU_QUAD=1: the INT8 bulk update runs four steps (K = 512) per launch (band >= 8 tiles
+// each side): the bulk gets 29% faster per step (c2: 68.6 ms for 63 launches vs 96.4 ms for
+// 128), but the look-ahead inside the quad (DMMA, 6 tile-steps per column of the band per
+// quad instead of 2 per pair) and the wider INT8 look-ahead put more work on the critical
+// stream: c2 LU 0.179 s vs 0.157 s with pairs, so pairs stay the default.
+static int lu_i8_steps(const BandGeom& g) {
+  const char* e = std::getenv("LRS_LU_QUAD");
+  if (!(e && e[0] == '1')) return 2;
+  return (g.wl >= 8 && g.wu >= 8) ? 4 : 2;
 }
 
-bool launch_band_lu(Ctx* c, const BandGeom& g, double* tiles, int Tmax, int* status) {
+int launch_band_lu(Ctx* c, const BandGeom& g, double* tiles, int Tmax, int* status) {
   lu_attrs();
   LuKernels L{real_diag, real_gemm, LRS_LU_PAIRS != 0};
   DevBuf<uint8_t> buf;
   I8Panel pn[2];
-  if (lu_i8_wanted(g, L)) {
+  const int steps = lu_i8_steps(g);
+  if (lu_i8_wanted(g, L, steps)) {
     auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
-    const size_t a = al((size_t)g.P * g.wl * TILE_ELEMS * 2 * 8),
-                 b = al((size_t)g.P * g.wu * TILE_ELEMS * 2 * 8),
+    const size_t a = al((size_t)g.P * g.wl * TILE_ELEMS * steps * 8),
+                 b = al((size_t)g.P * g.wu * TILE_ELEMS * steps * 8),
                  ea = al(sizeof(int) * g.P * g.wl * NB), eb = al(sizeof(int) * g.P * g.wu * NB);
     buf.alloc(2 * (a + b + ea + eb));
     uint8_t* q = buf.get();
@@ -799,9 +852,10 @@ bool launch_band_lu(Ctx* c, const BandGeom& g, double* tiles, int Tmax, int* sta
       q += a + b + ea + eb;
     }
     L.i8 = pn;
+    L.steps = steps;
   }
   run_band_lu(c, g, tiles, Tmax, status, L);
-  return L.i8 != nullptr;
+  return L.i8 != nullptr ? L.steps : 0;
 }
 
 // Right-looking tiled LU with look-ahead depth 1 over two streams:
@@ -834,14 +888,45 @@ void run_band_lu(Ctx* c, const BandGeom& g, void* tiles, int Tmax, int* status,
   auto slice = [&](int K) {
     if (!L.i8) return;
     ProfScope ps_(c, K_LU_PANEL, sc);
-    launch_lu_i8_slice(c, sc, g, static_cast<const double*>(tiles), K, L.i8[(K >> 1) & 1]);
+    launch_lu_i8_slice(c, sc, g, static_cast<const double*>(tiles), K, L.steps,
+                       L.i8[(K / L.steps) & 1]);
   };
   auto upd2 = [&](cudaStream_t s, int K, int kind, int cls) {
     if (!L.i8) return gemm(s, K, kind, cls);
     ProfScope ps_(c, cls, s);
-    launch_lu_i8_gemm(c, s, g, static_cast<double*>(tiles), K, kind, L.i8[(K >> 1) & 1]);
+    launch_lu_i8_gemm(c, s, g, static_cast<double*>(tiles), K, kind, L.steps,
+                      L.i8[(K / L.steps) & 1]);
   };
-  if (lu_uses_pairs(g, L)) {
+  if (L.i8 && L.steps == 4) {
+    // Steps in quads (K .. K+3) with a rank-512 INT8 bulk update and look-ahead depth 4:
+    //   main: [wait slice(K)] rest4(K)                                   (I, J >= K+8)
+    //   crit: [wait rest4(K-4)] next4(K) (rows / columns K+4..K+7, INT8) -> for s = K+4..K+7:
+    //         diag/panel(s), step s on rows / columns s+1..K+7 (DMMA kind 60 + m)
+    //         -> slice(K+4)
+    // Every tile takes its updates in step order; main never waits on crit's latency chain.
+    auto mini = [&](int K0) {  // the serial LU of steps K0 .. K0+3 inside the look-ahead
+      const int last = std::min(K0 + 3, Tmax - 1);
+      for (int st = K0; st <= last; ++st) {
+        if (st > 0) lu_diag_panel(c, sc, g, tiles, st, status, L);  // step 0: done above
+        if (last - st > 0 && g.wl > 0 && g.wu > 0) gemm(sc, st, 60 + (last - st), K_LU_PANEL);
+      }
+    };
+    mini(0);
+    if (Tmax > 4) slice(0);
+    LRS_CUDA(cudaEventRecord(ev_panel, sc));
+    bool have_rest = false;
+    for (int K = 0; K + 4 < Tmax; K += 4) {
+      if (have_rest) LRS_CUDA(cudaStreamWaitEvent(sc, ev_rest, 0));  // rest4(K-4)
+      LRS_CUDA(cudaStreamWaitEvent(sm, ev_panel, 0));                  // slice(K)
+      upd2(sm, K, 4, K_LU_UPDATE);
+      LRS_CUDA(cudaEventRecord(ev_rest, sm));
+      have_rest = true;
+      upd2(sc, K, 3, K_LU_PANEL);
+      mini(K + 4);
+      if (K + 8 < Tmax) slice(K + 4);
+      LRS_CUDA(cudaEventRecord(ev_panel, sc));
+    }
+  } else if (lu_uses_pairs(g, L)) {
     // Steps in pairs (K, K+1) with a rank-256 bulk update and look-ahead depth 2:
     //   main: [wait panel(K+1)] rest2(K, K+1)                       (I, J >= K+4)
     //   crit: [wait rest2(K-2, K-1)] next3(K, K+1) (rows/cols K+2, K+3) -> diag/panel(K+2)

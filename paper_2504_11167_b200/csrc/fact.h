@@ -42,7 +42,7 @@ struct Fact {
   DevBuf<unsigned long long> bad;
   // partial pivoting (band_lu_piv.cu): the blocks were factored with row interchanges
   bool pivoted = false;
-  bool lu_int8 = false;  // the two-step LU updates ran INT8-sliced (lu_i8.cu)
+  int lu_int8 = 0;  // steps per INT8-sliced LU update (2 or 4; lu_i8.cu), 0: DMMA
   DevBuf<int> ipiv, perm;
   // mixed precision: FP32 copy of the tiles, read for the off-diagonal tiles of the applies
   bool fp32 = false;

@@ -45,22 +45,24 @@ void launch_extract_tiles(Ctx* c, const Mat* m, const BandGeom& g, double* tiles
                           int64_t row_lo, int64_t row_hi, unsigned long long* d_bad);
 // Tiled no-pivot band LU of all partitions (Tmax steps, look-ahead over two streams).
 // status[2p] = min column needing a row interchange, status[2p+1] = min zero-pivot column.
-// returns true when the two-step updates ran INT8-sliced on the tensor cores (lu_i8.cu)
-bool launch_band_lu(Ctx* c, const BandGeom& g, double* tiles, int Tmax, int* status);
+// returns the steps per INT8-sliced tensor-core update (2 or 4; lu_i8.cu), 0 on DMMA
+int launch_band_lu(Ctx* c, const BandGeom& g, double* tiles, int Tmax, int* status);
 void launch_band_lu_z(Ctx* c, const BandGeom& g, zc* tiles, int Tmax, int* status);
 // integer-sliced (INT8 tensor core) two-step trailing update, lu_i8.cu: digit slices of one
 // step pair's A panel (rows K+2..K+1+wl) and B panel (columns K+2..K+1+wu)
 struct I8Panel {
-  uint8_t* A;  // [P][wl][8 chunks][8 slices][128 x 32 UMMA core layout]
-  uint8_t* B;  // [P][wu][2 halves][8 chunks][8 slices][64 x 32]
+  uint8_t* A;  // [P][wl][4 steps chunks][7 slices][128 x 32 UMMA core layout]
+  uint8_t* B;  // [P][wu][4 steps chunks][7 slices][128 x 32]
   int* ea;     // [P][wl][128] row exponents
   int* eb;     // [P][wu][128] column exponents
 };
-size_t lu_i8_panel_bytes(const BandGeom& g);  // A + B + exponents, one step pair
+// A + B + exponents of one update's panels; steps = 2 (pair, K = 256) or 4 (quad, K = 512)
+size_t lu_i8_panel_bytes(const BandGeom& g, int steps);
 void launch_lu_i8_slice(Ctx* c, cudaStream_t s, const BandGeom& g, const double* tiles, int K,
-                        const I8Panel& pn);
+                        int steps, const I8Panel& pn);
+// kind 3: look-ahead rows / columns K+steps .. K+2 steps-1; kind 4: the bulk (I, J >= K+2 steps)
 void launch_lu_i8_gemm(Ctx* c, cudaStream_t s, const BandGeom& g, double* tiles, int K, int kind,
-                       const I8Panel& pn);
+                       int steps, const I8Panel& pn);
 // the look-ahead driver, shared by the real and complex kernels
 struct LuKernels {
   void (*diag)(Ctx*, cudaStream_t, const BandGeom&, void* tiles, int K, int* status);
@@ -68,7 +70,8 @@ struct LuKernels {
   // 3: look-ahead row/column K+2 with steps K, K+1; 4: the rest with steps K, K+1
   void (*gemm)(Ctx*, cudaStream_t, const BandGeom&, void* tiles, int K, int* status, int kind);
   bool pairs = false;
-  const I8Panel* i8 = nullptr;  // [2] (pair parity): kinds 3 / 4 on the INT8 tensor cores
+  const I8Panel* i8 = nullptr;  // [2] (update parity): kinds 3 / 4 on the INT8 tensor cores
+  int steps = 2;                // steps per INT8 update: 2 (pairs) or 4 (quads, K = 512)
 };
 void run_band_lu(Ctx* c, const BandGeom& g, void* tiles, int Tmax, int* status,
                  const LuKernels& L);

@@ -47,7 +47,8 @@ namespace lrs {
 
 constexpr int I8_S = 7;                               // digit slices per operand
 constexpr int I8_KC = 32;                             // K per MMA and per pipeline chunk
-constexpr int I8_NCH = 2 * NB / I8_KC;                // 8 chunks over K = 256
+// chunks over K = 128 STEPS (STEPS = 2: the pair update, K = 256; STEPS = 4: K = 512)
+__host__ __device__ constexpr int i8_nch(int steps) { return steps * NB / I8_KC; }
 constexpr int I8_SL = NB * I8_KC;                     // 4096 B: one A slice of one chunk
 constexpr int I8_BLK = I8_S * I8_SL;                  // 28 KB: all A slices of one chunk
 // output columns per CTA: 128 (one CTA per SM, all 512 TMEM columns) or 64 (two CTAs per SM
@@ -112,8 +113,8 @@ constexpr int I8_TPC = 4;                             // tiles per CTA
 constexpr size_t I8_SMEM = (size_t)I8_STAGES * I8_STAGE + 2048;
 static_assert(I8_TN == 128 || I8_SMEM * 2 <= 227 * 1024, "two CTAs per SM");
 
-size_t lu_i8_panel_bytes(const BandGeom& g) {
-  return (size_t)g.P * (g.wl + g.wu) * (I8_NCH * I8_BLK + sizeof(int) * NB);
+size_t lu_i8_panel_bytes(const BandGeom& g, int steps) {
+  return (size_t)g.P * (g.wl + g.wu) * (i8_nch(steps) * I8_BLK + sizeof(int) * NB);
 }
 
 // ---- tcgen05 helpers ------------------------------------------------------------------
@@ -224,9 +225,11 @@ __device__ __forceinline__ void digits7_bits(double x, int e, uint32_t* words, i
 // ---------------------------------------------------------------------------------------
 constexpr int I8_SLICE_SPLIT = 4;  // CTAs per tile (32 rows / columns each)
 
-__global__ void __launch_bounds__(256) lu_i8_slice_kernel(BandGeom g, const double* tiles, int K,
-                                                          I8Panel pn) {
-  __shared__ double mx[I8_NCH][32];
+template <int STEPS>
+__global__ void __launch_bounds__(32 * STEPS * 4) lu_i8_slice_kernel(BandGeom g, const double* tiles,
+                                                                   int K, I8Panel pn) {
+  constexpr int NCH = i8_nch(STEPS);
+  __shared__ double mx[NCH][32];
   const int p = blockIdx.z, T = g.T[p];
   const int64_t base = g.tbase[p];
   auto tile = [&](int I, int J) -> const double* {
@@ -237,25 +240,21 @@ __global__ void __launch_bounds__(256) lu_i8_slice_kernel(BandGeom g, const doub
   const int x = blockIdx.x;
   const bool isA = x < g.wl;
   const int idx = isA ? x : x - g.wl;
-  const int IJ = K + 2 + idx;
+  const int IJ = K + STEPS + idx;
   if (IJ >= T) return;
-  const double* t0;
-  const double* t1;
-  if (isA) {
-    t0 = (IJ - K <= g.wl) ? tile(IJ, K) : nullptr;
-    t1 = tile(IJ, K + 1);
-  } else {
-    t0 = (IJ - K <= g.wu) ? tile(K, IJ) : nullptr;
-    t1 = tile(K + 1, IJ);
-  }
+  // this thread's chunk kc covers K values 32 (kc % 4) .. +31 of step K + kc / 4; tiles
+  // outside the band are zeros
+  const int d = kc >> 2;
+  const double* src;
+  if (isA) src = (IJ - (K + d) <= g.wl) ? tile(IJ, K + d) : nullptr;
+  else src = (IJ - (K + d) <= g.wu) ? tile(K + d, IJ) : nullptr;
   // the 32 K values k0 .. k0+31 of this line: A reads a column-major tile along its row
   // (stride 128), B reads a column (contiguous)
-  const int k0 = kc * I8_KC;
-  const double* src = k0 < NB ? t0 : t1;
+  const int k0 = (kc & 3) * I8_KC;
   double v[32];
 #pragma unroll
   for (int kk = 0; kk < 32; ++kk) {
-    const int k = (k0 + kk) & (NB - 1);
+    const int k = k0 + kk;
     v[kk] = src ? (isA ? __ldcg(src + (int64_t)k * NB + line) : __ldcg(src + (int64_t)line * NB + k))
                 : 0.0;
   }
@@ -266,7 +265,7 @@ __global__ void __launch_bounds__(256) lu_i8_slice_kernel(BandGeom g, const doub
   __syncthreads();
   m = mx[0][ln];
 #pragma unroll
-  for (int c = 1; c < I8_NCH; ++c) m = fmax(m, mx[c][ln]);
+  for (int c = 1; c < NCH; ++c) m = fmax(m, mx[c][ln]);
   int e = 0;
   if (m > 0.0) frexp(m, &e);
   if (kc == 0) {
@@ -276,8 +275,8 @@ __global__ void __launch_bounds__(256) lu_i8_slice_kernel(BandGeom g, const doub
   // B: column block h = line / TN, operand row line % TN, in [p][jb][h][chunk][slice]
   const int bl = isA ? line : (line & (I8_TN - 1));
   const int sl = isA ? I8_SL : I8_BSL;
-  uint8_t* dst = isA ? pn.A + (((int64_t)p * g.wl + idx) * I8_NCH + kc) * I8_BLK
-                     : pn.B + ((((int64_t)p * g.wu + idx) * I8_NH + line / I8_TN) * I8_NCH + kc) *
+  uint8_t* dst = isA ? pn.A + (((int64_t)p * g.wl + idx) * NCH + kc) * I8_BLK
+                     : pn.B + ((((int64_t)p * g.wu + idx) * I8_NH + line / I8_TN) * NCH + kc) *
                                   I8_BBLK;
   const int rows = isA ? NB : I8_TN;
 #pragma unroll
@@ -300,38 +299,51 @@ __global__ void __launch_bounds__(256) lu_i8_slice_kernel(BandGeom g, const doub
   }
 }
 
-// work item t of the kind-3 / kind-4 lists -> (p, ia, jb, column block h); false when
-// outside the blocks
-template <int KIND>
+// work item t of the kind-3 / kind-4 lists of a STEPS-step update (steps K .. K+D-1, D =
+// STEPS) -> (p, ia, jb, column block h); false when outside the blocks.
+//   KIND 3 (look-ahead): columns K+D .. K+2D-1 (rows K+D .. K+D-1+wl) and rows
+//                        K+D .. K+2D-1 (columns K+2D .. K+D-1+wu)
+//   KIND 4 (bulk):       I = K+2D .. K+D-1+wl, J = K+2D .. K+D-1+wu
+template <int KIND, int STEPS>
 __device__ __forceinline__ bool i8_decode(const BandGeom& g, int K, int t, int& p, int& ia,
                                           int& jb, int& h) {
-  const int per = KIND == 4 ? (g.wl - 2) * (g.wu - 2) : 2 * g.wl + 2 * g.wu - 4;
+  constexpr int D = STEPS;
+  const int per = KIND == 4 ? (g.wl - D) * (g.wu - D) : D * g.wl + D * (g.wu - D);
   h = t % I8_NH;
   t /= I8_NH;
   p = t / per;
   int r = t % per;
   int I, J;
   if (KIND == 4) {
-    I = K + 4 + r / (g.wu - 2);
-    J = K + 4 + r % (g.wu - 2);
-  } else if (r < g.wl) {
-    I = K + 2 + r;
-    J = K + 2;
-  } else if ((r -= g.wl) < g.wl - 1) {
-    I = K + 3 + r;
-    J = K + 3;
-  } else if ((r -= g.wl - 1) < g.wu - 1) {
-    I = K + 2;
-    J = K + 3 + r;
+    I = K + 2 * D + r / (g.wu - D);
+    J = K + 2 * D + r % (g.wu - D);
+  } else if (D == 2) {  // pairs: column K+2, column K+3, row K+2, row K+3
+    if (r < g.wl) {
+      I = K + 2 + r;
+      J = K + 2;
+    } else if ((r -= g.wl) < g.wl - 1) {
+      I = K + 3 + r;
+      J = K + 3;
+    } else if ((r -= g.wl - 1) < g.wu - 1) {
+      I = K + 2;
+      J = K + 3 + r;
+    } else {
+      r -= g.wu - 1;
+      I = K + 3;
+      J = K + 4 + r;
+    }
+  } else if (r < D * g.wl) {
+    I = K + D + r % g.wl;
+    J = K + D + r / g.wl;
   } else {
-    r -= g.wu - 1;
-    I = K + 3;
-    J = K + 4 + r;
+    r -= D * g.wl;
+    I = K + D + r / (g.wu - D);
+    J = K + 2 * D + r % (g.wu - D);
   }
-  ia = I - K - 2;
-  jb = J - K - 2;
+  ia = I - K - D;
+  jb = J - K - D;
   const int T = g.T[p];
-  return K + 1 < T && I < T && J < T;
+  return I < T && J < T;  // I, J >= K + D: every step K .. K+D-1 exists
 }
 
 // MMAs of one K chunk of one pass: A slice p outer (collector), B slice q descending, so the
@@ -365,9 +377,10 @@ __device__ __forceinline__ void i8_chunk_mmas(uint32_t tm, uint32_t a0, uint32_t
   }
 }
 
-template <int KIND>
+template <int KIND, int STEPS>
 __global__ void __launch_bounds__(I8_THREADS, I8_TN == 128 ? 1 : 2)
     lu_i8_gemm_kernel(BandGeom g, double* tiles, int K, I8Panel pn, int total) {
+  constexpr int I8_NCH = i8_nch(STEPS);
   extern __shared__ __align__(1024) uint8_t smraw[];
   uint8_t* stage = smraw;
   uint64_t* full = reinterpret_cast<uint64_t*>(smraw + I8_STAGES * I8_STAGE);
@@ -381,7 +394,7 @@ __global__ void __launch_bounds__(I8_THREADS, I8_TN == 128 ? 1 : 2)
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int t0 = blockIdx.x * I8_TPC, t1 = min(total, t0 + I8_TPC);
   auto ctile = [&](int p, int ia, int jb, int h) -> double* {
-    const int I = K + 2 + ia, J = K + 2 + jb;
+    const int I = K + STEPS + ia, J = K + STEPS + jb;
     return tiles + (g.tbase[p] + (int64_t)I * g.W + (J - I + g.wl)) * TILE_ELEMS +
            (int64_t)h * I8_TN * NB;
   };
@@ -412,7 +425,7 @@ __global__ void __launch_bounds__(I8_THREADS, I8_TN == 128 ? 1 : 2)
       int it = 0;
       for (int t = t0; t < t1; ++t) {
         int p, ia, jb, h;
-        if (!i8_decode<KIND>(g, K, t, p, ia, jb, h)) continue;
+        if (!i8_decode<KIND, STEPS>(g, K, t, p, ia, jb, h)) continue;
         bulk_prefetch_l2(ctile(p, ia, jb, h), sizeof(double) * NB * I8_TN);
         const uint8_t* a = pn.A + ((int64_t)p * g.wl + ia) * I8_NCH * I8_BLK;
         const uint8_t* b = pn.B + (((int64_t)p * g.wu + jb) * I8_NH + h) * I8_NCH * I8_BBLK;
@@ -441,7 +454,7 @@ __global__ void __launch_bounds__(I8_THREADS, I8_TN == 128 ? 1 : 2)
       PRB(long long c_full = 0, c_chunk0 = 0; const long long c_start = clock64();)
       for (int t = t0; t < t1; ++t) {
         int p, ia, jb, h;
-        if (!i8_decode<KIND>(g, K, t, p, ia, jb, h)) continue;
+        if (!i8_decode<KIND, STEPS>(g, K, t, p, ia, jb, h)) continue;
 #pragma unroll
         for (int pass = 0; pass < I8_NP; ++pass) {
           for (int kc = 0; kc < I8_NCH; ++kc, ++it) {
@@ -478,7 +491,7 @@ __global__ void __launch_bounds__(I8_THREADS, I8_TN == 128 ? 1 : 2)
     PRB(long long c_tf = 0, c_drain = 0, c_red = 0; const long long c_start = clock64();)
     for (int t = t0; t < t1; ++t) {
       int p, ia, jb, h;
-      if (!i8_decode<KIND>(g, K, t, p, ia, jb, h)) continue;
+      if (!i8_decode<KIND, STEPS>(g, K, t, p, ia, jb, h)) continue;
       double* C = ctile(p, ia, jb, h) + (int64_t)ch * I8_EPC * NB;
       const double si = exp2i(pn.ea[((int64_t)p * g.wl + ia) * NB + i]);
       if (w == 2) {  // the previous tile's readers of sj passed the closing barrier
@@ -633,30 +646,41 @@ double run_i8_peak(Ctx* c) {
 }
 
 void launch_lu_i8_slice(Ctx* c, cudaStream_t s, const BandGeom& g, const double* tiles, int K,
-                        const I8Panel& pn) {
-  lu_i8_slice_kernel<<<dim3(g.wl + g.wu, I8_SLICE_SPLIT, g.P), 256, 0, s>>>(g, tiles, K, pn);
+                        int steps, const I8Panel& pn) {
+  if (steps == 4)
+    lu_i8_slice_kernel<4><<<dim3(g.wl + g.wu, I8_SLICE_SPLIT, g.P), 512, 0, s>>>(g, tiles, K, pn);
+  else
+    lu_i8_slice_kernel<2><<<dim3(g.wl + g.wu, I8_SLICE_SPLIT, g.P), 256, 0, s>>>(g, tiles, K, pn);
+  LRS_LAUNCHED(c);
+}
+
+template <int KIND, int STEPS>
+static void i8_gemm_launch(Ctx* c, cudaStream_t s, const BandGeom& g, double* tiles, int K,
+                           const I8Panel& pn) {
+  static bool attr = false;
+  if (!attr) {
+    LRS_CUDA(cudaFuncSetAttribute(lu_i8_gemm_kernel<KIND, STEPS>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)I8_SMEM));
+    attr = true;
+  }
+  constexpr int D = STEPS;
+  const int per = KIND == 4 ? (g.wl - D) * (g.wu - D) : D * g.wl + D * (g.wu - D);
+  const int total = per * g.P * I8_NH;
+  if (total <= 0) return;
+  const int grid = (total + I8_TPC - 1) / I8_TPC;
+  lu_i8_gemm_kernel<KIND, STEPS><<<grid, I8_THREADS, I8_SMEM, s>>>(g, tiles, K, pn, total);
   LRS_LAUNCHED(c);
 }
 
 void launch_lu_i8_gemm(Ctx* c, cudaStream_t s, const BandGeom& g, double* tiles, int K, int kind,
-                       const I8Panel& pn) {
-  static bool attr = false;
-  if (!attr) {
-    LRS_CUDA(cudaFuncSetAttribute(lu_i8_gemm_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)I8_SMEM));
-    LRS_CUDA(cudaFuncSetAttribute(lu_i8_gemm_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)I8_SMEM));
-    attr = true;
+                       int steps, const I8Panel& pn) {
+  if (steps == 4) {
+    if (kind == 4) i8_gemm_launch<4, 4>(c, s, g, tiles, K, pn);
+    else i8_gemm_launch<3, 4>(c, s, g, tiles, K, pn);
+  } else {
+    if (kind == 4) i8_gemm_launch<4, 2>(c, s, g, tiles, K, pn);
+    else i8_gemm_launch<3, 2>(c, s, g, tiles, K, pn);
   }
-  const int per = kind == 4 ? (g.wl - 2) * (g.wu - 2) : 2 * g.wl + 2 * g.wu - 4;
-  const int total = per * g.P * I8_NH;
-  const int grid = (total + I8_TPC - 1) / I8_TPC;
-  if (total <= 0) return;
-  if (kind == 4)
-    lu_i8_gemm_kernel<4><<<grid, I8_THREADS, I8_SMEM, s>>>(g, tiles, K, pn, total);
-  else
-    lu_i8_gemm_kernel<3><<<grid, I8_THREADS, I8_SMEM, s>>>(g, tiles, K, pn, total);
-  LRS_LAUNCHED(c);
 }
 
 }  // namespace lrs

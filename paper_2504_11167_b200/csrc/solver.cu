@@ -946,7 +946,8 @@ Fact* factorize(Ctx* c, Mat* m, const lrs_solver_cfg& cfg, const lrs_comm* comm)
                     (f->fp32 ? f->total_tiles * TILE_ELEMS * (int64_t)sizeof(float) : 0);
   in.rank_collapsed = f->rank_collapsed;
   in.variant = f->variant;
-  in.lu_pairs = (cplx || f->pivoted) ? 0 : (lu_real_pairs(g) ? 1 : 0);
+  // steps per bulk update launch: 4 (INT8 quads), 2 (pairs), 0 (single steps)
+  in.lu_pairs = (cplx || f->pivoted) ? 0 : (f->lu_int8 ? f->lu_int8 : (lu_real_pairs(g) ? 2 : 0));
   in.pivoted = f->pivoted ? 1 : 0;
   in.lu_int8 = f->lu_int8 ? 1 : 0;
   in.t_lu = elapsed_ms(e0, e1) * 1e-3;

@@ -14,23 +14,27 @@ from paper_2504_11167_b200.configs import Csr
 pytestmark = pytest.mark.gpu
 
 
-def _factor(ctx, csr, cfg, i8):
-    old = os.environ.get("LRS_LU_I8")
+def _factor(ctx, csr, cfg, i8, quad=False):
+    old = {k: os.environ.get(k) for k in ("LRS_LU_I8", "LRS_LU_QUAD")}
     os.environ["LRS_LU_I8"] = "1" if i8 else "0"
+    os.environ["LRS_LU_QUAD"] = "1" if quad else "0"
     try:
         A = api.CsrMatrix.from_csr(ctx, csr)
         return api.factorize(ctx, A, api.SolverConfig(variant="BJ", p=cfg.P, k=cfg.b, n_svd=0))
     finally:
-        if old is None:
-            os.environ.pop("LRS_LU_I8")
-        else:
-            os.environ["LRS_LU_I8"] = old
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k)
+            else:
+                os.environ[k] = v
 
 
-def _compare(ctx, csr, cfg):
-    F8 = _factor(ctx, csr, cfg, True)
+def _compare(ctx, csr, cfg, quad=False):
+    F8 = _factor(ctx, csr, cfg, True, quad)
     F64 = _factor(ctx, csr, cfg, False)
     assert F8.info["lu_int8"] == 1 and F64.info["lu_int8"] == 0
+    if not F8.info["pivoted"]:
+        assert F8.info["lu_pairs"] == (4 if quad else 2)
     worst = 0.0
     for i in range(cfg.P):
         a, b = F8.tiles(i), F64.tiles(i)
@@ -48,6 +52,14 @@ def test_int8_update_matches_dmma(ctx, name, scale):
     cfg = configs.make_config(name, scale)
     assert -(-cfg.b // 128) >= 3  # the pair schedule (and so the INT8 update) is in play
     assert _compare(ctx, cfg.system(0), cfg) <= 1e-12
+
+
+@pytest.mark.parametrize("name,scale", [("c2", 0.5), ("c4", 0.05)])
+def test_int8_quad_update_matches_dmma(ctx, name, scale):
+    """LRS_LU_QUAD=1: four steps (K = 512) per INT8 update, DMMA look-ahead inside the quad."""
+    cfg = configs.make_config(name, scale)
+    assert -(-cfg.b // 128) >= 8
+    assert _compare(ctx, cfg.system(0), cfg, quad=True) <= 1e-12
 
 
 @pytest.mark.parametrize("e", [-300, 300])
