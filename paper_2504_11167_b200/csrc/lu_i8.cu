@@ -95,7 +95,10 @@ constexpr int I8_TMEM = I8_GROUPS * I8_TN;            // 512 or 256 columns
 constexpr int I8_EPC = LRS_I8_EPC;                    // columns per epilogue warp (64 or 32)
 constexpr int I8_EPI = 4 * I8_TN / I8_EPC;            // epilogue warps
 constexpr int I8_THREADS = 32 * (2 + I8_EPI);         // producer, MMA, epilogue warps
-constexpr int I8_TPC = 4;                             // tiles per CTA
+#ifndef LRS_I8_TPC
+#define LRS_I8_TPC 8  // c2 LU median 0.1535 s vs 0.1596 s (4 tiles), 0.161 s (16)
+#endif
+constexpr int I8_TPC = LRS_I8_TPC;                    // tiles per CTA
 // LRS_I8_EXP (timing experiments only, wrong results): 1 skips the epilogue arithmetic,
 // 2 also skips the operand copies
 #ifndef LRS_I8_EXP
