@@ -113,6 +113,9 @@ __global__ void __launch_bounds__(512, 1) lu_diag_z_kernel(BandGeom g, zc* tiles
 // complex tile GEMM on DMMA: C(128 x 64 half tile) = / -= A(128 x 128) B(128 x 64)
 // ---------------------------------------------------------------------------------------
 constexpr int ZG_THREADS = 256;
+#ifndef LRS_ZGEMM_3M
+#define LRS_ZGEMM_3M 1
+#endif
 constexpr int ZKC = 16;
 constexpr int ZAS_LD = NB + 2;   // 130 complex: conflict-free 16-byte fragment loads
 constexpr int ZBS_LD = ZKC + 4;  // 20
@@ -148,6 +151,18 @@ __device__ __forceinline__ void ztile_gemm(const zc* A, const zc* B, zc* C, int 
   const int g = lane >> 2, t = lane & 3;
   constexpr int NK = NB / ZKC;
   double ar[2][8][2], ai[2][8][2];  // [n tile][m tile][pair] real / imaginary parts
+  // 3M form (LRS_ZGEMM_3M): q1 = sum br ar, q2 = sum bi ai, q3 = sum (br + bi)(ar + ai);
+  // C = (ar + q1 - q2, ai + q3 - q1 - q2): three DMMAs per complex product instead of four
+  double q1[LRS_ZGEMM_3M ? 2 : 1][8][2], q2[LRS_ZGEMM_3M ? 2 : 1][8][2],
+      q3[LRS_ZGEMM_3M ? 2 : 1][8][2];
+  if (LRS_ZGEMM_3M) {
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) q1[j][i][e] = q2[j][i][e] = q3[j][i][e] = 0.0;
+  }
   zgemm_load_chunk(A, B, As, Bs, 0, nbase, tid);
 #pragma unroll
   for (int j = 0; j < 2; ++j)
@@ -155,7 +170,7 @@ __device__ __forceinline__ void ztile_gemm(const zc* A, const zc* B, zc* C, int 
     for (int i = 0; i < 8; ++i)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
-        if (MODE == 1) {
+        if (MODE == 1 && !LRS_ZGEMM_3M) {  // (3M: C is added in the epilogue)
           const zc v = C[(int64_t)(nbase + 16 * wn + 8 * j + g) * NB + 64 * wm + 8 * i + 2 * t + e];
           ar[j][i][e] = v.x;
           ai[j][i][e] = v.y;
@@ -196,16 +211,35 @@ __device__ __forceinline__ void ztile_gemm(const zc* A, const zc* B, zc* C, int 
         fbr[j] = v.x;
         fbi[j] = v.y;
       }
+      if (LRS_ZGEMM_3M) {
+        double fas[8], fbs[2];
 #pragma unroll
-      for (int j = 0; j < 2; ++j)
+        for (int i = 0; i < 8; ++i) fas[i] = far_[i] + fai[i];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          // C^T = B^T A^T, complex: re += br ar - bi ai ; im += br ai + bi ar
-          dmma_8x8x4(ar[j][i][0], ar[j][i][1], fbr[j], far_[i]);
-          dmma_8x8x4(ar[j][i][0], ar[j][i][1], -fbi[j], fai[i]);
-          dmma_8x8x4(ai[j][i][0], ai[j][i][1], fbr[j], fai[i]);
-          dmma_8x8x4(ai[j][i][0], ai[j][i][1], fbi[j], far_[i]);
-        }
+        for (int j = 0; j < 2; ++j) fbs[j] = fbr[j] + fbi[j];
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            dmma_8x8x4(q1[j & (LRS_ZGEMM_3M ? 1 : 0)][i][0], q1[j & (LRS_ZGEMM_3M ? 1 : 0)][i][1],
+                       fbr[j], far_[i]);
+            dmma_8x8x4(q2[j & (LRS_ZGEMM_3M ? 1 : 0)][i][0], q2[j & (LRS_ZGEMM_3M ? 1 : 0)][i][1],
+                       fbi[j], fai[i]);
+            dmma_8x8x4(q3[j & (LRS_ZGEMM_3M ? 1 : 0)][i][0], q3[j & (LRS_ZGEMM_3M ? 1 : 0)][i][1],
+                       fbs[j], fas[i]);
+          }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            // C^T = B^T A^T, complex: re += br ar - bi ai ; im += br ai + bi ar
+            dmma_8x8x4(ar[j][i][0], ar[j][i][1], fbr[j], far_[i]);
+            dmma_8x8x4(ar[j][i][0], ar[j][i][1], -fbi[j], fai[i]);
+            dmma_8x8x4(ai[j][i][0], ai[j][i][1], fbr[j], fai[i]);
+            dmma_8x8x4(ai[j][i][0], ai[j][i][1], fbi[j], far_[i]);
+          }
+      }
     }
     __syncthreads();
   }
@@ -219,7 +253,13 @@ __device__ __forceinline__ void ztile_gemm(const zc* A, const zc* B, zc* C, int 
     for (int i = 0; i < 8; ++i)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
-        const zc v = {ar[j][i][e], ai[j][i][e]};
+        zc v = {ar[j][i][e], ai[j][i][e]};
+        if (LRS_ZGEMM_3M) {
+          const int jj = j & (LRS_ZGEMM_3M ? 1 : 0);
+          const double a1 = q1[jj][i][e], a2 = q2[jj][i][e], a3 = q3[jj][i][e];
+          if (MODE == 1) v = C[(int64_t)nn * NB + 64 * wm + 8 * i + 2 * t + e];
+          v = {v.x + (a1 - a2), v.y + (a3 - (a1 + a2))};
+        }
         C[(int64_t)nn * NB + 64 * wm + 8 * i + 2 * t + e] = v;
         // izamax: the panel entry a_ij = l_ij u_jj would out-rank u_jj
         if (MODE == 0 && piv_status && s_abs1(s_mul(v, u)) > s_abs1(u))

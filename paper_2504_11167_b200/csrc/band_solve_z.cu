@@ -25,6 +25,14 @@ constexpr size_t zsolve_smem_bytes() {
          16 * ZSTAGES + 64;
 }
 
+#ifndef LRS_ZSOLVE_3M
+#define LRS_ZSOLVE_3M 1
+#endif
+// (base_r + p1 - p2, base_i + p3 - p1 - p2)
+__device__ __forceinline__ zc zacc(double br, double bi, double q1, double q2, double q3) {
+  return {br + (q1 - q2), bi + (q3 - (q1 + q2))};
+}
+
 template <int MODE, int NR>
 __global__ void __launch_bounds__(ZS_THREADS, 1)
     band_solve_z_kernel(BandGeom g, const zc* __restrict__ tiles, zc* x, int64_t ld, int nrhs,
@@ -90,6 +98,16 @@ __global__ void __launch_bounds__(ZS_THREADS, 1)
   const int64_t row0 = (int64_t)t * NB;
   const int gq = lane >> 2, tq = lane & 3;
   double accr[2][NJ][2], acci[2][NJ][2];
+  // forward products in the 3M form (LRS_ZSOLVE_3M): p1 = sum ar br, p2 = sum ai bi,
+  // p3 = sum (ar + ai)(br + bi); re = p1 - p2, im = p3 - p1 - p2 (three DMMAs per complex
+  // product instead of four); accr / acci carry the right-hand side
+  double p1[2][NJ][2], p2[2][NJ][2], p3[2][NJ][2];
+#pragma unroll
+  for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+    for (int nj = 0; nj < NJ; ++nj)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) p1[mi][nj][e] = p2[mi][nj][e] = p3[mi][nj][e] = 0.0;
 #pragma unroll
   for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
@@ -148,8 +166,10 @@ __global__ void __launch_bounds__(ZS_THREADS, 1)
             for (int nj = 0; nj < NJ; ++nj)
 #pragma unroll
               for (int e = 0; e < 2; ++e) {
-                xs[(16 * w + 8 * mi + gq) * XLD + 8 * nj + 2 * tq + e] = {accr[mi][nj][e], acci[mi][nj][e]};
+                xs[(16 * w + 8 * mi + gq) * XLD + 8 * nj + 2 * tq + e] = zacc(
+                    accr[mi][nj][e], acci[mi][nj][e], p1[mi][nj][e], p2[mi][nj][e], p3[mi][nj][e]);
                 accr[mi][nj][e] = acci[mi][nj][e] = 0.0;
+                p1[mi][nj][e] = p2[mi][nj][e] = p3[mi][nj][e] = 0.0;
               }
         } else {
           __syncthreads();
@@ -188,15 +208,31 @@ __global__ void __launch_bounds__(ZS_THREADS, 1)
           br[nj] = v.x;
           bi[nj] = v.y;
         }
+        if (LRS_ZSOLVE_3M) {
+          double as[2], bs[NJ];
 #pragma unroll
-        for (int mi = 0; mi < 2; ++mi)
+          for (int mi = 0; mi < 2; ++mi) as[mi] = ar[mi] + ai[mi];
 #pragma unroll
-          for (int nj = 0; nj < NJ; ++nj) {
-            dmma_8x8x4(accr[mi][nj][0], accr[mi][nj][1], ar[mi], br[nj]);
-            dmma_8x8x4(accr[mi][nj][0], accr[mi][nj][1], -ai[mi], bi[nj]);
-            dmma_8x8x4(acci[mi][nj][0], acci[mi][nj][1], ar[mi], bi[nj]);
-            dmma_8x8x4(acci[mi][nj][0], acci[mi][nj][1], ai[mi], br[nj]);
-          }
+          for (int nj = 0; nj < NJ; ++nj) bs[nj] = br[nj] + bi[nj];
+#pragma unroll
+          for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+            for (int nj = 0; nj < NJ; ++nj) {
+              dmma_8x8x4(p1[mi][nj][0], p1[mi][nj][1], ar[mi], br[nj]);
+              dmma_8x8x4(p2[mi][nj][0], p2[mi][nj][1], ai[mi], bi[nj]);
+              dmma_8x8x4(p3[mi][nj][0], p3[mi][nj][1], as[mi], bs[nj]);
+            }
+        } else {
+#pragma unroll
+          for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+            for (int nj = 0; nj < NJ; ++nj) {
+              dmma_8x8x4(accr[mi][nj][0], accr[mi][nj][1], ar[mi], br[nj]);
+              dmma_8x8x4(accr[mi][nj][0], accr[mi][nj][1], -ai[mi], bi[nj]);
+              dmma_8x8x4(acci[mi][nj][0], acci[mi][nj][1], ar[mi], bi[nj]);
+              dmma_8x8x4(acci[mi][nj][0], acci[mi][nj][1], ai[mi], br[nj]);
+            }
+        }
       }
     } else {
       // out(16 x NR) (+|-)= conj(Tile)^T (16 x 128) xs (128 x NR).  Warp w takes K-quarter
@@ -257,7 +293,7 @@ __global__ void __launch_bounds__(ZS_THREADS, 1)
         for (int e = 0; e < 2; ++e) {
           const int n = 8 * nj + 2 * tq + e;
           if (n >= nrhs) continue;
-          zc v = {accr[mi][nj][e], acci[mi][nj][e]};
+          zc v = zacc(accr[mi][nj][e], acci[mi][nj][e], p1[mi][nj][e], p2[mi][nj][e], p3[mi][nj][e]);
           if (MODE == 0) v = s_add(v, xs[m * XLD + n]);
           x[off + row0 + m + n * ld] = v;
         }
