@@ -227,6 +227,9 @@ __device__ __forceinline__ void digits7_bits(double x, int e, uint32_t* words, i
 // core-matrix layout (a warp writes 512 contiguous bytes per slice and K-core).
 // ---------------------------------------------------------------------------------------
 constexpr int I8_SLICE_SPLIT = 4;  // CTAs per tile (32 rows / columns each)
+#ifndef LRS_I8_SLICE_L1
+#define LRS_I8_SLICE_L1 1
+#endif
 
 template <int STEPS>
 __global__ void __launch_bounds__(32 * STEPS * 4) lu_i8_slice_kernel(BandGeom g, const double* tiles,
@@ -258,8 +261,15 @@ __global__ void __launch_bounds__(32 * STEPS * 4) lu_i8_slice_kernel(BandGeom g,
 #pragma unroll
   for (int kk = 0; kk < 32; ++kk) {
     const int k = k0 + kk;
+    // A: lanes read consecutive rows (coalesced); B: lanes read different columns, so the
+    // loads go through L1 (LRS_I8_SLICE_L1): the 32-byte sectors serve 4 consecutive k
+#if LRS_I8_SLICE_L1
+    v[kk] = src ? (isA ? __ldcg(src + (int64_t)k * NB + line) : __ldca(src + (int64_t)line * NB + k))
+                : 0.0;
+#else
     v[kk] = src ? (isA ? __ldcg(src + (int64_t)k * NB + line) : __ldcg(src + (int64_t)line * NB + k))
                 : 0.0;
+#endif
   }
   double m = 0.0;
 #pragma unroll
