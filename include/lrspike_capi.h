@@ -153,7 +153,7 @@ typedef struct lrs_fact_info {
   double max_interface_cond;
   int32_t lu_pairs;             /* steps per bulk LU update launch: 4 (INT8, K = 512), 2, or 0 */
   int32_t pivoted;              /* some block needed row interchanges: partial-pivoting LU */
-  int32_t lu_int8;              /* two-step updates ran INT8-sliced on tcgen05 (LRS_LU_I8) */
+  int32_t lu_int8;              /* bulk updates ran INT8-sliced on tcgen05 (LRS_LU_I8) */
 } lrs_fact_info;
 
 typedef struct lrs_error_info {
