@@ -343,7 +343,7 @@ def run_ours(args):
                                    "operands); nominal dense 4.5 POPS",
                     # DRAM read + write of one launch from `ncu --set full`
                     # (profiles/r01b_ncu_lu_i8_gemm.txt): the C tiles' read-modify-write
-                    "traffic": 1.977e9, "traffic_source": "profiles/r01c_ncu_lu_i8_gemm.txt",
+                    "traffic": 2.117e9, "traffic_source": "profiles/r01d_ncu_lu_i8_gemm.txt",
                     "launches": int(upd_n), "avg_launch_ms": avg_launch_s * 1e3,
                     "int8_ops_per_launch": ops_launch,
                     "fp64_equiv": {"achieved": achieved_tf, "unit": "TFLOP/s",
