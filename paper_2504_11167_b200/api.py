@@ -363,10 +363,12 @@ class CsrMatrix:
         return cls(ctx, csr.n, csr.row_ptr, csr.col_idx, csr.values)
 
     def __del__(self):
+        # a matrix outliving its Context (e.g. held by a pytest traceback past the fixture's
+        # close) must not touch the destroyed context: its device memory went with it
         try:
-            if self.h:
+            if self.h and self.ctx.h:
                 lib().lrs_mat_destroy(self.h)
-                self.h = None
+            self.h = None
         except Exception:
             pass
 
@@ -484,9 +486,9 @@ class SpikeFactorization:
 
     def __del__(self):
         try:
-            if self.h:
+            if self.h and self.ctx.h:  # see CsrMatrix.__del__
                 lib().lrs_fact_destroy(self.h)
-                self.h = None
+            self.h = None
         except Exception:
             pass
 
