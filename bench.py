@@ -12,12 +12,15 @@ preconditioned BiCGStab solve.  metric = time-to-tolerance in seconds
   e2e         the same step through the public C-ABI with HOST buffers: CSR
               upload (validate + transpose + H2D), factorize, solve with a host
               RHS, x copied back -- host<->device copies inside the timed region
-  roofline    dominant kernel = the two-step trailing update of the band LU: the
-              INT8-sliced tcgen05 kernel lu_i8_gemm<4> (INT8 tensor-core bound, its
-              int8 ops against the in-run INT8 peak; fp64_equiv = the algorithmic
-              FP64 flops it retires against the DMMA peak), or the DMMA GEMM when the
-              INT8 path is off; per-launch CUDA events in the timed region;
-              roofline_apply = the HBM-bound preconditioner apply
+  roofline    the dominant kernel of the step by CUDA-event time per step (c2: the
+              preconditioner apply's band solves, HBM-bound, since the INT8 LU update
+              went under it), with its DRAM traffic from a committed ncu capture;
+              roofline_apply = the HBM-bound apply (the two one-RHS dataflow sweeps +
+              interface + recovery, algorithmic bytes of SURVEY 8(d)); roofline_lu_update =
+              the bulk trailing update of the band LU: the INT8-sliced tcgen05 kernel
+              lu_i8_gemm<4, 2> (its int8 ops against the in-run INT8 peak; fp64_equiv =
+              the algorithmic FP64 flops it retires against the DMMA peak), or the DMMA
+              GEMM when the INT8 path is off; per-launch CUDA events in the timed region
   cpu_baseline the oracle port (scipy/OpenBLAS dgbtrf/dgbtrs) on a bounded
               sample of the same blocks, extrapolated by the algorithmic work
 
@@ -360,6 +363,12 @@ def run_ours(args):
                                    "nominal 148 SM x 64 FMA x 2 x 1.965 GHz = 37.2",
                     "traffic": None, "launches": int(upd_n), "avg_launch_ms": avg_launch_s * 1e3,
                     "flops_per_launch": per_launch_flops}
+    apply_rl = _apply_roofline(kt, reps, info, hbm_peak, peak_src, args.steps)
+    upd_ms_step = upd_ms / max(args.steps, 1)
+    roofline["ms_per_step"] = upd_ms_step
+    dominant = roofline
+    if apply_rl and apply_rl["ms_per_step"] > upd_ms_step:
+        dominant = apply_rl
     line = {
         "metric": "preconditioned solve time-to-tolerance (s)",
         "value": value, "unit": "s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
@@ -378,10 +387,13 @@ def run_ours(args):
         "t_solve_s": reps[-1].wall_time,
         "e2e": {"value": e2e, "unit": "s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
         "gpu_launches": int(launches),
-        "roofline": roofline,
+        # the dominant kernel of the step (by CUDA-event time per step) carries `roofline`;
+        # the other one is reported beside it
+        "roofline": dominant,
         "roofline_lu_all": {"achieved": info["lu_flops"] / info["t_lu"] / 1e12, "unit": "TFLOP/s",
                             "frac": info["lu_flops"] / info["t_lu"] / 1e12 / dmma_peak},
-        "roofline_apply": _apply_roofline(kt, reps, info, hbm_peak, peak_src, args.steps),
+        "roofline_apply": apply_rl,
+        "roofline_lu_update": roofline,
         "kernel_ms_per_step": {k: v[0] / args.steps for k, v in kt.items()},
         "kernel_launches_per_step": {k: v[1] / args.steps for k, v in kt.items()},
         "kernel_ms_total_share": {k: (v[0] / total_ms if total_ms else 0) for k, v in kt.items()},
@@ -440,10 +452,16 @@ def _apply_roofline(kt, reps, info, hbm_peak, peak_src, steps):
     ms_iface = kt["iface_apply"][0] + kt["recovery"][0]
     per_apply_ms = (ms * (2 * applies / n) + ms_iface) / applies
     gbs = info["apply_bytes"] / (per_apply_ms / 1e3) / 1e9
-    return {"bound": "hbm", "kernel": "band_solve_kernel<L/U> + iface + recovery",
+    return {"bound": "hbm",
+            "kernel": "band_solve_kernel<0, 1> + <1, 1> (one-RHS L and U dataflow sweeps of "
+                      "the apply) + iface + recovery",
             "achieved": gbs, "peak": hbm_peak, "unit": "GB/s", "frac": gbs / hbm_peak,
             "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_src})",
+            # DRAM read + write of one apply's two sweeps from `ncu --set full`
+            # (profiles/r01d_ncu_band_solve_apply.txt): 3% above the algorithmic bytes
+            "traffic": 16.649e9, "traffic_source": "profiles/r01d_ncu_band_solve_apply.txt",
             "bytes_per_apply": info["apply_bytes"], "ms_per_apply": per_apply_ms,
+            "ms_per_step": per_apply_ms * applies / steps,
             "frac_of_8TBs_nominal": gbs / 8000.0}
 
 
