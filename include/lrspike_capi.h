@@ -178,6 +178,8 @@ LRS_API lrs_status lrs_ctx_synchronize(lrs_ctx* ctx);
  * band_solve, band_solve_adjoint, spmv, iface_apply, recovery, krylov_vec, setup_misc,
  * spike_band_solve (the multi-RHS solves of the randomized spike SVD). */
 #define LRS_NUM_KERNEL_CLASSES 11
+/* on = 0: off; 1: every class; otherwise bit k + 1 of `on` selects class k (timing only the
+ * classes asked for keeps the event-record overhead off the other launches). */
 LRS_API lrs_status lrs_ctx_set_profiling(lrs_ctx* ctx, int32_t on);
 /* Totals since the last reset (reset = 1 clears after reading). */
 LRS_API lrs_status lrs_ctx_kernel_times(lrs_ctx* ctx, double* ms, int64_t* counts, int32_t reset);

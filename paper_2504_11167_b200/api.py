@@ -304,8 +304,13 @@ class Context:
     def synchronize(self):
         _check(lib().lrs_ctx_synchronize(self.h), self.h)
 
-    def set_profiling(self, on: bool):
-        _check(lib().lrs_ctx_set_profiling(self.h, 1 if on else 0), self.h)
+    def set_profiling(self, on: bool, classes=None):
+        """Per-kernel-class CUDA-event timing; `classes` (names of KERNEL_CLASSES) limits it
+        to those classes."""
+        v = 1 if on else 0
+        if on and classes is not None:
+            v = sum(1 << (KERNEL_CLASSES.index(k) + 1) for k in classes) or 0
+        _check(lib().lrs_ctx_set_profiling(self.h, v), self.h)
 
     def kernel_times(self, reset: bool = False) -> dict:
         """{class: (total_ms, launches)} of the CUDA-event timed launches."""

@@ -192,6 +192,7 @@ lrs_status lrs_ctx_set_profiling(lrs_ctx* c, int32_t on) {
   return guard(c, [&] {
     c->collect();
     c->prof = on != 0;
+    c->prof_mask = on == 1 ? ~0u : ((uint32_t)on >> 1);
   });
 }
 

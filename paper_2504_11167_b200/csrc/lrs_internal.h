@@ -111,6 +111,7 @@ struct Ctx {
   double* dots_host = nullptr;
   // profiling: (class, start, end) event triples, summed on demand
   bool prof = false;
+  uint32_t prof_mask = ~0u;  // classes timed while profiling (bit k: class k)
   std::vector<cudaEvent_t> ev_pool;
   std::vector<int> prof_class;
   std::vector<cudaEvent_t> prof_ev;  // 2 per record
@@ -149,13 +150,13 @@ struct ProfScope {
   cudaStream_t s;
   cudaEvent_t b = nullptr;
   ProfScope(Ctx* ctx, int k, cudaStream_t st = nullptr) : c(ctx), cls(k), s(st ? st : ctx->stream) {
-    if (c->prof) {
+    if (c->prof && ((c->prof_mask >> cls) & 1u)) {
       b = c->take_event();
       cudaEventRecord(b, s);
     }
   }
   ~ProfScope() {
-    if (c->prof) {
+    if (b) {
       cudaEvent_t e = c->take_event();
       cudaEventRecord(e, s);
       c->prof_class.push_back(cls);
