@@ -363,14 +363,17 @@ __device__ __forceinline__ void tile_gemm(const double* A, const double* B, doub
         acc[j][i][0] = acc[j][i][1] = 0.0;
       }
     }
+  // B = inv(U) (upper): the output columns n0 .. n0+CN-1 take only k < n0 + CN (the other
+  // K chunks are exact zeros), so the first column block stops early
+  const int nk = (MODE == 0 && maskB == MASK_UPPER) ? (n0 + GEMM_CN + KC - 1) / KC : NK;
 #pragma unroll 1
-  for (int kc = 0; kc < NK; ++kc) {
-    if (kc + DIST < NK) {
+  for (int kc = 0; kc < nk; ++kc) {
+    if (kc + DIST < nk) {
       const int s2 = (kc + DIST) % GEMM_STAGES;
       gemm_load_chunk(A, B, As + s2 * AS_STAGE, Bs + s2 * BS_STAGE, kc + DIST, tid);
     }
-    // chunk kc has landed once at most min(DIST, NK-1-kc) younger groups are pending
-    const int pend = min(DIST, NK - 1 - kc);
+    // chunk kc has landed once at most min(DIST, nk-1-kc) younger groups are pending
+    const int pend = min(DIST, nk - 1 - kc);
     if (pend >= 2) cp_async_wait<2>();
     else if (pend == 1) cp_async_wait<1>();
     else cp_async_wait<0>();
@@ -403,6 +406,12 @@ __device__ __forceinline__ void tile_gemm(const double* A, const double* B, doub
         for (int i = 0; i < 8; ++i) dmma_8x8x4(acc[j][i][0], acc[j][i][1], fb[j], fa[i]);
     }
     __syncthreads();
+  }
+  if (MODE == 0 && maskB == MASK_UPPER && GEMM_SPLIT == 2) {
+    // L_IK = A_IK inv(U_KK) is formed in place and each half-tile CTA reads all of A_IK:
+    // the two halves (a cluster of 2) write only after both have read their operands
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" :::
+                     "memory");
   }
   int bad_col = 0x7fffffff;
 #pragma unroll
@@ -736,8 +745,22 @@ static void real_gemm(Ctx* c, cudaStream_t s, const BandGeom& g, void* tiles, in
     const int m = kind - 60;
     lu_gemm_kernel<6><<<dim3(S * m * (g.wl + g.wu - m), g.P), GEMM_THREADS, GEMM_SMEM, s>>>(
         g, t, K, status, m);
-  } else if (kind == 0)
-    lu_gemm_kernel<0><<<dim3(S * (g.wl + g.wu), g.P), GEMM_THREADS, GEMM_SMEM, s>>>(g, t, K, status);
+  } else if (kind == 0) {
+    // the two half-tile CTAs of a tile form a cluster (tile_gemm's in-place L panel)
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(S * (g.wl + g.wu), g.P);
+    cfg.blockDim = dim3(GEMM_THREADS);
+    cfg.dynamicSmemBytes = GEMM_SMEM;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = S;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    LRS_CUDA(cudaLaunchKernelEx(&cfg, lu_gemm_kernel<0>, g, t, K, status, 0));
+  }
   else if (kind == 1 && LRS_LU_PERSISTENT) {
     // each CTA takes at most LRS_REST_TPC half-tiles and retires, so the high-priority
     // look-ahead kernels (next / diag / panel of step K+1) still get SMs mid-update
