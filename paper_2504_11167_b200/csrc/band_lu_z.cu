@@ -243,6 +243,12 @@ __device__ __forceinline__ void ztile_gemm(const zc* A, const zc* B, zc* C, int 
     }
     __syncthreads();
   }
+  if (MODE == 0 && maskB == ZMASK_UPPER) {
+    // in-place L_IK = A_IK inv(U_KK): both half-tile CTAs (a cluster of 2) read all of A_IK
+    // before either writes its half
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" :::
+                     "memory");
+  }
   int bad_col = 0x7fffffff;
 #pragma unroll
   for (int j = 0; j < 2; ++j) {
@@ -327,8 +333,21 @@ static void z_diag(Ctx* c, cudaStream_t s, const BandGeom& g, void* tiles, int K
 static void z_gemm(Ctx* c, cudaStream_t s, const BandGeom& g, void* tiles, int K, int* status,
                    int kind) {
   zc* t = static_cast<zc*>(tiles);
-  if (kind == 0)
-    lu_zgemm_kernel<0><<<dim3(2 * (g.wl + g.wu), g.P), ZG_THREADS, ZGEMM_SMEM, s>>>(g, t, K, status);
+  if (kind == 0) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * (g.wl + g.wu), g.P);
+    cfg.blockDim = dim3(ZG_THREADS);
+    cfg.dynamicSmemBytes = ZGEMM_SMEM;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;  // the two half-tile CTAs of a tile
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    LRS_CUDA(cudaLaunchKernelEx(&cfg, lu_zgemm_kernel<0>, g, t, K, status));
+  }
   else if (kind == 5)
     lu_zgemm_kernel<5><<<dim3(2 * g.wu, g.P), ZG_THREADS, ZGEMM_SMEM, s>>>(g, t, K, status);
   else if (kind == 1)
