@@ -49,10 +49,12 @@ def cpu_comm_worker(rank, world, port, out_dir):
     dist.destroy_process_group()
 
 
-def gpu_solve_worker(rank, world, port, out_dir, name, scale, method, P, variant="T"):
+def gpu_solve_worker(rank, world, port, out_dir, name, scale, method, P, variant="T",
+                     backend="gloo"):
     """One rank of a sharded factorize + solve on cuda:0 (ranks share the GPU; all
-    cross-rank dependencies are host-synchronous gloo calls)."""
-    dist = _init(rank, world, port)
+    cross-rank dependencies are host-synchronous gloo calls).  backend="nccl" (one rank:
+    NCCL refuses two ranks on one device) runs the adapter's device-buffer path."""
+    dist = _init(rank, world, port, backend)
     import torch
 
     from paper_2504_11167_b200 import api, configs
@@ -71,8 +73,19 @@ def gpu_solve_worker(rank, world, port, out_dir, name, scale, method, P, variant
     x, rep, _ = api.solve(A, np.asfortranarray(cfg.rhs), it=it, F=F)
     xg = gather_rows(x, F.row_lo, F.row_hi, cfg.matrix.n, comm)
     yg = gather_rows(y, F.row_lo, F.row_hi, cfg.matrix.n, comm)
+    adapter = np.zeros(0)
+    if backend == "nccl":
+        # the library makes no exchanges on one rank: drive the device-buffer callbacks
+        # directly (all-gather, and a send / receive to this rank itself)
+        s = torch.arange(6, dtype=torch.float64, device="cuda") + 1.0
+        r = torch.zeros(6 * world, dtype=torch.float64, device="cuda")
+        assert comm._allgather(None, s.data_ptr(), r.data_ptr(), 6) == 0
+        r2 = torch.zeros(6, dtype=torch.float64, device="cuda")
+        assert comm._sendrecv(None, s.data_ptr(), 6, rank, r2.data_ptr(), 6, rank) == 0
+        adapter = np.concatenate([r.cpu().numpy(), r2.cpu().numpy()])
     if rank == 0:
         np.savez(os.path.join(out_dir, "dist.npz"), x=xg, y=yg, iterations=rep.iterations,
+                 adapter=adapter,
                  residual=rep.residual_final, history=np.array(rep.residual_history),
                  ledger=np.array([rep.comm["precond-apply"][1], rep.comm["recovery"][1]]),
                  calls=np.array([comm.calls["allgather"], comm.calls["sendrecv"]]))

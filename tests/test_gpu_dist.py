@@ -27,13 +27,14 @@ def _port():
     return p
 
 
-@pytest.mark.parametrize("name,scale,method,P,world,variant",
-                         [("c2", 16 / 64, "bicgstab", 8, 2, "T"),
-                          ("c2", 16 / 64, "bicgstab", 8, 3, "T"),
-                          ("c1", 64 / 256, "gmres", 4, 2, "T"),
-                          ("c2", 16 / 64, "bicgstab", 8, 3, "I"),
-                          ("c1", 64 / 256, "gmres", 4, 2, "OTF")])
-def test_sharded_solve_matches_single_gpu(ctx, name, scale, method, P, world, variant):
+@pytest.mark.parametrize("name,scale,method,P,world,variant,backend",
+                         [("c2", 16 / 64, "bicgstab", 8, 2, "T", "gloo"),
+                          ("c2", 16 / 64, "bicgstab", 8, 3, "T", "gloo"),
+                          ("c1", 64 / 256, "gmres", 4, 2, "T", "gloo"),
+                          ("c2", 16 / 64, "bicgstab", 8, 3, "I", "gloo"),
+                          ("c1", 64 / 256, "gmres", 4, 2, "OTF", "gloo"),
+                          ("c2", 16 / 64, "bicgstab", 8, 1, "T", "nccl")])
+def test_sharded_solve_matches_single_gpu(ctx, name, scale, method, P, world, variant, backend):
     from paper_2504_11167_b200 import api, configs
 
     cfg = configs.make_config(name, scale, P)
@@ -46,10 +47,15 @@ def test_sharded_solve_matches_single_gpu(ctx, name, scale, method, P, world, va
     x1, rep1, _ = api.solve(A, np.asfortranarray(cfg.rhs), it=it, F=F)
     with tempfile.TemporaryDirectory() as d:
         mp.spawn(dist_worker.gpu_solve_worker,
-                 args=(world, _port(), d, name, scale, method, P, variant), nprocs=world,
+                 args=(world, _port(), d, name, scale, method, P, variant, backend),
+                 nprocs=world,
                  join=True)
         z = np.load(os.path.join(d, "dist.npz"))
     assert np.array_equal(z["y"], y1)  # the preconditioner apply, bit for bit
     assert float(z["iterations"]) == rep1.iterations
     assert np.array_equal(z["x"], x1)  # identical iterates on any number of GPUs
-    assert z["calls"][0] > 0 and z["calls"][1] > 0
+    if world > 1:
+        assert z["calls"][0] > 0 and z["calls"][1] > 0
+    if backend == "nccl":  # the adapter's NCCL device-buffer path, driven directly
+        ref = np.arange(6, dtype=np.float64) + 1.0
+        assert np.array_equal(z["adapter"], np.concatenate([ref, ref]))
