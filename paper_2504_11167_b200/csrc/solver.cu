@@ -1118,6 +1118,10 @@ void run_bicgstab(Work<S>& w, const S* b, S* x, const lrs_iter_cfg& cfg, bool ha
   w.zero(v);
   const bool trace = std::getenv("LRS_TRACE") != nullptr;
   const auto t_start = std::chrono::steady_clock::now();
+  // rho = rhat^H r of the next iteration comes with the norm of the new r (one reduction,
+  // one host round trip: r and rhat sit one block apart)
+  bool have_rho = false;
+  std::vector<H> rr2(2 * nr), rho_next(nr);
   for (int64_t it = 1; it <= cfg.max_iters; ++it) {
     if (trace)
       std::fprintf(stderr, "[lrs] bicgstab it %lld host %.3f ms\n", (long long)it,
@@ -1126,7 +1130,9 @@ void run_bicgstab(Work<S>& w, const S* b, S* x, const lrs_iter_cfg& cfg, bool ha
     std::vector<bool> act(nr);
     for (int j = 0; j < nr; ++j) act[j] = !conv[j] && !brk[j];
     if (!any(act)) break;
-    w.dots(rhat, 0, 1, r, rho.data());
+    if (have_rho) rho = rho_next;
+    else w.dots(rhat, 0, 1, r, rho.data());
+    have_rho = false;
     for (int j = 0; j < nr; ++j)
       if (act[j] && std::abs(rho[j]) < cfg.breakdown_eps) {
         brk[j] = true;
@@ -1174,11 +1180,12 @@ void run_bicgstab(Work<S>& w, const S* b, S* x, const lrs_iter_cfg& cfg, bool ha
     if (!any(act)) break;
     w.M(s, shat);
     w.Aop(shat, t);
-    std::vector<H> tt(nr), ts(nr);
-    w.dots(t, 0, 1, t, tt.data());
-    w.dots(t, 0, 1, s, ts.data());
-    for (int j = 0; j < nr; ++j)
-      if (act[j]) omega[j] = ts[j] / (tt[j] != H(0.0) ? tt[j] : H(1.0));
+    std::vector<H> st(2 * nr);
+    w.dots(s, (int64_t)blk, 2, t, st.data());  // [s^H t, t^H t] (t follows s in buf)
+    for (int j = 0; j < nr; ++j) {
+      const H tt = st[nr + j], ts = hconj(st[j]);
+      if (act[j]) omega[j] = ts / (tt != H(0.0) ? tt : H(1.0));
+    }
     for (int j = 0; j < nr; ++j)
       if (act[j] && std::abs(omega[j]) < cfg.breakdown_eps) {
         brk[j] = true;
@@ -1186,7 +1193,12 @@ void run_bicgstab(Work<S>& w, const S* b, S* x, const lrs_iter_cfg& cfg, bool ha
       }
     w.axpby(2, cs_fill<S>(alpha), cs_fill<S>(omega), cs_mask(act), x, phat, shat, nullptr);
     w.axpby(1, cs_fill<S>(omega), none, cs_mask(act), nullptr, s, t, r);
-    w.norms(r, tmpv.data());
+    w.dots(r, (int64_t)blk, 2, r, rr2.data());  // [r^H r, rhat^H r] (rhat follows r)
+    for (int j = 0; j < nr; ++j) {
+      tmpv[j] = std::sqrt(hreal(rr2[j]));
+      rho_next[j] = rr2[nr + j];
+    }
+    have_rho = true;
     std::vector<bool> full(nr, false);
     for (int j = 0; j < nr; ++j) full[j] = act[j] && tmpv[j] / bns[j] <= cfg.tol;
     if (any(full)) {
