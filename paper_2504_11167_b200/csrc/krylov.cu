@@ -15,7 +15,13 @@ constexpr int KV_THREADS = 256;
 __device__ __forceinline__ double kv_warp_sum(double v) { return warp_sum(v); }
 __device__ __forceinline__ zc kv_warp_sum(zc v) { return warp_sum_z(v); }
 
-template <int NR, class S>
+// Each pass over the chunk's rows serves QB vectors X_q at once, so Y (the GMRES w, bigger
+// than L2 for the 16-column complex batches of c5) is read once per QB vectors instead of
+// once per vector (measured on c5: 340 -> 319 ms of Krylov kernels per 80 GMRES steps;
+// splitting the 16 columns over two CTAs per chunk was slower, 427 ms).  Per (q, column)
+// the row order of each thread's sum and the reduction tree are those of one vector at a
+// time: the results are bit-identical.
+template <int NR, int QB, class S>
 __global__ void __launch_bounds__(KV_THREADS) multidot_partial_kernel(
     const int64_t* __restrict__ cstart, const S* __restrict__ X, int64_t ldx, int64_t strideX,
     int nvec, const S* __restrict__ Y, int64_t ldy, int nrhs, S* __restrict__ partial) {
@@ -23,28 +29,41 @@ __global__ void __launch_bounds__(KV_THREADS) multidot_partial_kernel(
   const int c = blockIdx.x;
   const int64_t r0 = cstart[c], r1 = cstart[c + 1];
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  for (int q = 0; q < nvec; ++q) {
-    const S* Xq = X + q * strideX;
-    S acc[NR];
+  for (int q0 = 0; q0 < nvec; q0 += QB) {
+    S acc[QB][NR];
 #pragma unroll
-    for (int j = 0; j < NR; ++j) acc[j] = s_zero(S());
+    for (int qq = 0; qq < QB; ++qq)
+#pragma unroll
+      for (int j = 0; j < NR; ++j) acc[qq][j] = s_zero(S());
     for (int64_t row = r0 + tid; row < r1; row += KV_THREADS) {
+      S y[NR];
 #pragma unroll
-      for (int j = 0; j < NR; ++j)
-        if (j < nrhs) acc[j] = s_cfma(Xq[row + j * ldx], Y[row + j * ldy], acc[j]);
+      for (int j = 0; j < NR; ++j) y[j] = j < nrhs ? Y[row + j * ldy] : s_zero(S());
+#pragma unroll
+      for (int qq = 0; qq < QB; ++qq) {
+        if (q0 + qq >= nvec) break;
+        const S* Xq = X + (q0 + qq) * strideX;
+#pragma unroll
+        for (int j = 0; j < NR; ++j)
+          if (j < nrhs) acc[qq][j] = s_cfma(Xq[row + j * ldx], y[j], acc[qq][j]);
+      }
     }
 #pragma unroll
-    for (int j = 0; j < NR; ++j) {
-      const S s = kv_warp_sum(acc[j]);
-      if (lane == 0) red[w][j] = s;
+    for (int qq = 0; qq < QB; ++qq) {
+      if (q0 + qq >= nvec) break;
+#pragma unroll
+      for (int j = 0; j < NR; ++j) {
+        const S s = kv_warp_sum(acc[qq][j]);
+        if (lane == 0) red[w][j] = s;
+      }
+      __syncthreads();
+      if (tid < nrhs) {
+        S s = s_zero(S());
+        for (int ww = 0; ww < KV_THREADS / 32; ++ww) s = s_add(s, red[ww][tid]);
+        partial[((int64_t)c * nvec + q0 + qq) * nrhs + tid] = s;
+      }
+      __syncthreads();
     }
-    __syncthreads();
-    if (tid < nrhs) {
-      S s = s_zero(S());
-      for (int ww = 0; ww < KV_THREADS / 32; ++ww) s = s_add(s, red[ww][tid]);
-      partial[((int64_t)c * nvec + q) * nrhs + tid] = s;
-    }
-    __syncthreads();
   }
 }
 
@@ -79,10 +98,11 @@ void launch_multidot_partition_t(Ctx* c, const Chunks& ch, const S* X, int64_t l
   if (nvec == 0 || nrhs == 0) return;
   ProfScope ps_(c, K_KRYLOV);
   if (nrhs == 1)
-    multidot_partial_kernel<1, S><<<ch.nchunks, KV_THREADS, 0, c->stream>>>(
+    multidot_partial_kernel<1, 8, S><<<ch.nchunks, KV_THREADS, 0, c->stream>>>(
         ch.start, X, ldx, strideX, nvec, Y, ldy, nrhs, partial);
   else
-    multidot_partial_kernel<MAX_RHS, S><<<ch.nchunks, KV_THREADS, 0, c->stream>>>(
+    multidot_partial_kernel<MAX_RHS, sizeof(S) == 16 ? 2 : 4, S><<<ch.nchunks, KV_THREADS, 0,
+                                                                 c->stream>>>(
         ch.start, X, ldx, strideX, nvec, Y, ldy, nrhs, partial);
   LRS_LAUNCHED(c);
   const int nout = nvec * nrhs * (int)(sizeof(S) / sizeof(double));
