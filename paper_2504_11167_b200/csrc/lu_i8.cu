@@ -37,6 +37,7 @@
 // subtract 2^(ea+eb) sum_s 2^(4-8s) G_s from C.  Each CTA walks I8_TPC consecutive tiles (same
 // I first, so A slices are shared through L2) and retires, leaving SMs for the high-priority
 // diag / panel kernels of the look-ahead.
+#include <algorithm>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -98,7 +99,10 @@ constexpr int I8_THREADS = 32 * (2 + I8_EPI);         // producer, MMA, epilogue
 #ifndef LRS_I8_TPC
 #define LRS_I8_TPC 8  // c2 LU median 0.1535 s vs 0.1596 s (4 tiles), 0.161 s (16)
 #endif
-constexpr int I8_TPC = LRS_I8_TPC;                    // tiles per CTA
+constexpr int I8_TPC = LRS_I8_TPC;                    // tiles per CTA (bulk)
+#ifndef LRS_I8_TPC3
+#define LRS_I8_TPC3 8  // c2 LU medians: 1 tile 0.156 s, 2: 0.155, 4: 0.155, 8: 0.154 (noise level)
+#endif
 // LRS_I8_EXP (timing experiments only, wrong results): 1 skips the epilogue arithmetic,
 // 2 also skips the operand copies
 #ifndef LRS_I8_EXP
@@ -392,7 +396,7 @@ __device__ __forceinline__ void i8_chunk_mmas(uint32_t tm, uint32_t a0, uint32_t
 
 template <int KIND, int STEPS>
 __global__ void __launch_bounds__(I8_THREADS, I8_TN == 128 ? 1 : 2)
-    lu_i8_gemm_kernel(BandGeom g, double* tiles, int K, I8Panel pn, int total) {
+    lu_i8_gemm_kernel(BandGeom g, double* tiles, int K, I8Panel pn, int total, int tpc) {
   constexpr int I8_NCH = i8_nch(STEPS);
   extern __shared__ __align__(1024) uint8_t smraw[];
   uint8_t* stage = smraw;
@@ -405,7 +409,7 @@ __global__ void __launch_bounds__(I8_THREADS, I8_TN == 128 ? 1 : 2)
   uint32_t* tbase = reinterpret_cast<uint32_t*>(tempty + I8_GROUPS);
   double* sj = reinterpret_cast<double*>(smraw + I8_STAGES * I8_STAGE + 1024);  // [128]
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int t0 = blockIdx.x * I8_TPC, t1 = min(total, t0 + I8_TPC);
+  const int t0 = blockIdx.x * tpc, t1 = min(total, t0 + tpc);
   auto ctile = [&](int p, int ia, int jb, int h) -> double* {
     const int I = K + STEPS + ia, J = K + STEPS + jb;
     return tiles + (g.tbase[p] + (int64_t)I * g.W + (J - I + g.wl)) * TILE_ELEMS +
@@ -680,8 +684,12 @@ static void i8_gemm_launch(Ctx* c, cudaStream_t s, const BandGeom& g, double* ti
   const int per = KIND == 4 ? (g.wl - D) * (g.wu - D) : D * g.wl + D * (g.wu - D);
   const int total = per * g.P * I8_NH;
   if (total <= 0) return;
-  const int grid = (total + I8_TPC - 1) / I8_TPC;
-  lu_i8_gemm_kernel<KIND, STEPS><<<grid, I8_THREADS, I8_SMEM, s>>>(g, tiles, K, pn, total);
+  // the look-ahead launch (kind 3, on the critical stream) takes fewer tiles per CTA
+  static const int tpc3 = std::getenv("LRS_I8_TPC3") ? std::atoi(std::getenv("LRS_I8_TPC3"))
+                                                      : LRS_I8_TPC3;
+  const int tpc = KIND == 4 ? I8_TPC : std::max(1, tpc3);
+  const int grid = (total + tpc - 1) / tpc;
+  lu_i8_gemm_kernel<KIND, STEPS><<<grid, I8_THREADS, I8_SMEM, s>>>(g, tiles, K, pn, total, tpc);
   LRS_LAUNCHED(c);
 }
 
