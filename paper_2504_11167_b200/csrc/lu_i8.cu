@@ -25,18 +25,21 @@
 // written in the UMMA shared-memory operand layout (K-major, no swizzle: 8-row x 16-byte
 // core matrices) so one pipeline stage is two contiguous bulk copies.
 //
-// lu_i8_gemm (kinds 3 / 4 of the pair schedule): a warp-specialised kernel per 128 x 128
-// output tile.  The MMA shape is M=128, N=128, K=32 (N < 128 leaves the INT8 pipe at 2/3
-// rate); 4 group accumulators of 128 INT32 columns fill the 512 TMEM columns, so a tile runs
+// lu_i8_gemm (kinds 3 / 4 of the pair schedule; the quad schedule, LRS_LU_QUAD=1, runs the
+// same kernel with K = 512): a warp-specialised kernel per 128 x 128 output tile.  The MMA
+// shape is M=128, N=128, K=32 (N < 128 leaves the INT8 pipe at 2/3 rate: SS-mode operand
+// reads); the seven group accumulators do not fit the 4 x 128 TMEM columns, so a tile runs
 // two passes over K: pass A forms G_5..G_8 (22 MMAs per K chunk of 32, all 7 + 7 slices),
-// pass B G_2..G_4 (6 MMAs, slices 1-3; its fourth slot is handed back at once).  Warp 0 streams the chunks (64 / 32 KB) through a
-// 3-stage TMA ring; warp 1's elected thread issues the MMAs, A slice outer so consecutive
-// MMAs reuse it from the operand collector; warps 2-9 drain each group accumulator into
-// FP64 registers (tcgen05.ld; smallest group first) and release it at once, so the next
-// pass's MMAs refill a group while the others are still being read.  After pass B they
-// subtract 2^(ea+eb) sum_s 2^(4-8s) G_s from C.  Each CTA walks I8_TPC consecutive tiles (same
-// I first, so A slices are shared through L2) and retires, leaving SMs for the high-priority
-// diag / panel kernels of the look-ahead.
+// pass B G_2..G_4 (6 MMAs, slices 1-3).  The group accumulators take the four TMEM slots as
+// a ring (a pass takes the slots after the previous pass's, so pass B starts in the slots
+// pass A's drain frees first); two tfull barriers alternate by pass parity.  Warp 0 streams
+// the chunks (56 / 24 KB) through a 4-stage TMA ring; warp 1's elected thread issues the
+// MMAs, A slice outer so consecutive MMAs reuse it from the operand collector; warps 2-9
+// drain each group accumulator into FP64 registers (tcgen05.ld; smallest group first) and
+// release it, and after pass B subtract 2^(ea+eb) sum_s 2^(4-8s) G_s from C with L2
+// reductions.  Each CTA walks I8_TPC consecutive tiles (same I first, so A slices are shared
+// through L2) and retires, leaving SMs for the high-priority diag / panel kernels of the
+// look-ahead.
 #include <algorithm>
 #include <cstdlib>
 
