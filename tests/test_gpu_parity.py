@@ -238,3 +238,23 @@ def test_cg_parity(ctx, name, scale):
     assert abs(rep.iterations - repo.iterations) <= 2
     assert _rel(x, xo) <= 1e-8
     assert rep.precond_applications == 2 * rep.iterations
+
+
+def test_kernel_class_profiling_mask(ctx):
+    """set_profiling(classes=...) times only those kernel classes (the bench keeps the
+    event-record overhead off the other launches); all classes when no mask is given."""
+    cfg = configs.make_config("c1", 48 / 256)
+    A = api.CsrMatrix.from_csr(ctx, cfg.matrix)
+    scfg = api.SolverConfig(variant="T", p=cfg.P, k=cfg.b, n_svd=cfg.r, seed=cfg.seed)
+    it = api.IterConfig(tol=cfg.tol, method="gmres", restart=cfg.m)
+    ctx.set_profiling(True, classes=("band_solve", "lu_diag"))
+    ctx.kernel_times(reset=True)
+    api.solve(A, cfg.rhs, scfg, it)
+    kt = ctx.kernel_times(reset=True)
+    assert kt["band_solve"][1] > 0 and kt["lu_diag"][1] > 0
+    assert all(n == 0 for k, (_, n) in kt.items() if k not in ("band_solve", "lu_diag"))
+    ctx.set_profiling(True)
+    api.solve(A, cfg.rhs, scfg, it)
+    kt = ctx.kernel_times(reset=True)
+    ctx.set_profiling(False)
+    assert kt["krylov_vec"][1] > 0 and kt["spmv"][1] > 0 and kt["lu_diag"][1] > 0
