@@ -240,9 +240,12 @@ __global__ void __launch_bounds__(ZS_THREADS, 1)
       // the four partials are summed in fixed order (NR independent: bit-exact columns).
       constexpr int PLD = NR + 1;
       const int kq = w & 3, th = w >> 2;
-      double cr[NJ][2], ci[NJ][2];
+      double cr[NJ][2], ci[NJ][2], c3[LRS_ZSOLVE_3M ? NJ : 1][2];
 #pragma unroll
       for (int u = 0; u < NJ; ++u) cr[u][0] = cr[u][1] = ci[u][0] = ci[u][1] = 0.0;
+      if (LRS_ZSOLVE_3M)
+#pragma unroll
+        for (int u = 0; u < (LRS_ZSOLVE_3M ? NJ : 1); ++u) c3[u][0] = c3[u][1] = 0.0;
 #pragma unroll
       for (int k4 = 0; k4 < 8; ++k4) {
         const int r = 32 * kq + 4 * k4 + tq;
@@ -255,10 +258,17 @@ __global__ void __launch_bounds__(ZS_THREADS, 1)
           if (diag && !(MODE == 2 ? r <= cbase + mloc : r > cbase + mloc)) a = {0.0, 0.0};
           const double ar = a.x, ai = -a.y;  // conjugate
           const zc b = xs[r * XLD + 8 * nj + gq];
-          dmma_8x8x4(cr[u][0], cr[u][1], ar, b.x);
-          dmma_8x8x4(ci[u][0], ci[u][1], ar, b.y);
-          dmma_8x8x4(cr[u][0], cr[u][1], -ai, b.y);
-          dmma_8x8x4(ci[u][0], ci[u][1], ai, b.x);
+          if (LRS_ZSOLVE_3M) {  // cr = sum ar br, ci = sum ai bi, c3 = sum (ar + ai)(br + bi)
+            const int uu = LRS_ZSOLVE_3M ? u : 0;
+            dmma_8x8x4(cr[u][0], cr[u][1], ar, b.x);
+            dmma_8x8x4(ci[u][0], ci[u][1], ai, b.y);
+            dmma_8x8x4(c3[uu][0], c3[uu][1], ar + ai, b.x + b.y);
+          } else {
+            dmma_8x8x4(cr[u][0], cr[u][1], ar, b.x);
+            dmma_8x8x4(ci[u][0], ci[u][1], ar, b.y);
+            dmma_8x8x4(cr[u][0], cr[u][1], -ai, b.y);
+            dmma_8x8x4(ci[u][0], ci[u][1], ai, b.x);
+          }
         }
       }
 #pragma unroll
@@ -266,8 +276,17 @@ __global__ void __launch_bounds__(ZS_THREADS, 1)
         const int ti = th * NJ + u;
         const int mi = ti & 1, nj = ti >> 1;
         zc* pp = part + (kq * ZCH_COLS + 8 * mi + gq) * PLD + 8 * nj + 2 * tq;
-        pp[0] = {cr[u][0], ci[u][0]};
-        pp[1] = {cr[u][1], ci[u][1]};
+        if (LRS_ZSOLVE_3M) {
+          const int uu = LRS_ZSOLVE_3M ? u : 0;
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const double q1 = cr[u][e], q2 = ci[u][e], q3 = c3[uu][e];
+            pp[e] = {q1 - q2, q3 - (q1 + q2)};
+          }
+        } else {
+          pp[0] = {cr[u][0], ci[u][0]};
+          pp[1] = {cr[u][1], ci[u][1]};
+        }
       }
       __syncthreads();
       for (int e = tid; e < ZCH_COLS * NR; e += ZS_THREADS) {
