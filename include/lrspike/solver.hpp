@@ -47,6 +47,8 @@ struct IterConfig {
 };
 
 /// SPEC.md:470-473.
+enum class SpikeMode { SpikeSvd, CouplingSvd };
+
 struct SolverConfig {
   Variant variant = Variant::LR_SPIKE_T;
   index_t p = 4;
@@ -64,6 +66,9 @@ struct SolverConfig {
   int otf_escalations = 4;
   // FP32 off-diagonal factor tiles in the preconditioner applies
   bool factor_fp32 = false;
+  // how the low-rank spikes are built: the SPEC's randomized spike SVD, or
+  // the truncated SVD of B_i / C_i followed by padded solves (north_star setup (1))
+  SpikeMode spike_mode = SpikeMode::SpikeSvd;
 };
 
 /// SPEC.md:466-469.

@@ -80,6 +80,11 @@ typedef enum lrs_variant {
 } lrs_variant;
 typedef enum lrs_method { LRS_GMRES = 0, LRS_BICGSTAB = 1, LRS_CG = 2 } lrs_method;
 typedef enum lrs_side { LRS_SIDE_T = 0, LRS_SIDE_W = 1 } lrs_side;
+/* How the low-rank spikes are built:
+   LRS_SPIKE_SVD       randomized SVD of the spike T_i = A_i^-1 [0; B_i] (default)
+   LRS_SPIKE_COUPLING  rank-r randomized SVD of B_i / C_i, spike = r padded solves against its
+                       singular vectors (BASELINE.json north_star setup (1)) */
+typedef enum lrs_spike_mode { LRS_SPIKE_SVD = 0, LRS_SPIKE_COUPLING = 1 } lrs_spike_mode;
 
 /* Ledger stages. */
 enum { LRS_STAGE_REDUCED_MATVEC = 0, LRS_STAGE_PRECOND_APPLY = 1, LRS_STAGE_RECOVERY = 2 };
@@ -105,6 +110,7 @@ typedef struct lrs_solver_cfg {
      off-diagonal factor tiles in FP32 (the diagonal-tile inverses and every vector stay
      FP64; the spike construction uses the FP64 factors).  0 = FP64 throughout. */
   int32_t factor_fp32;
+  int32_t spike_mode; /* lrs_spike_mode */
 } lrs_solver_cfg;
 
 /* IterConfig, SPEC.md:411-414 (+ method, GMRES restart). */

@@ -86,6 +86,22 @@ class BreakdownError(Error):
         self.x, self.report = x, report
 
 
+def _pmap(fn, *seqs):
+    """list(map(fn, *seqs)) over LRS_ORACLE_THREADS host threads (default 1: sequential).
+    Partitions and spikes are independent (results must not depend on the
+    scheduling), and LAPACK releases the GIL, so the baseline runs partitions concurrently
+    with OPENBLAS_NUM_THREADS=1; the results are identical."""
+    import os
+
+    t = int(os.environ.get("LRS_ORACLE_THREADS", "1") or 1)
+    if t <= 1:
+        return list(map(fn, *seqs))
+    from concurrent.futures import ThreadPoolExecutor
+
+    with ThreadPoolExecutor(t) as ex:
+        return list(ex.map(fn, *seqs))
+
+
 COND_LIMIT = 1e12  # interface condition limit (SPEC.md:371, :394); same constant on the GPU
 
 # --------------------------------------------------------------------------------------
@@ -198,9 +214,10 @@ class BlockFactor:
     n: int
     kl: int
     ku: int
-    ab: np.ndarray  # LAPACK band storage (2kl+ku+1, n)
+    ab: np.ndarray  # LAPACK band storage (2kl+ku+1, n); the getrf n x n LU if dense
     ipiv: np.ndarray  # 0-based pivot rows
     dtype: np.dtype
+    dense: bool = False  # ?getrf / ?getrs storage (see factorize_block)
 
     @property
     def swaps(self) -> int:
@@ -219,6 +236,15 @@ def factorize_block(Ai: sp.csr_matrix, kl: int | None = None, ku: int | None = N
     if ku is None:
         ku = int(max(0, d.max(initial=0)))
     dt = np.result_type(Ai.dtype, np.float64)
+    if _dense_storage(n, kl, ku, np.dtype(dt).itemsize):
+        a = np.asfortranarray(Ai.toarray().astype(dt))
+        getrf, = lapack.get_lapack_funcs(("getrf",), (a,))
+        lu, ipiv, info = getrf(a, overwrite_a=True)
+        if info > 0:
+            raise SingularBlockError(f"exact zero pivot in column {info - 1}", info - 1)
+        if info < 0:
+            raise ParameterError(f"getrf illegal argument {-info}")
+        return BlockFactor(n, kl, ku, lu, ipiv, dt, True)
     ab = np.zeros((2 * kl + ku + 1, n), dtype=dt, order="F")
     ab[kl + ku + coo.row - coo.col, coo.col] = coo.data
     gbtrf, = lapack.get_lapack_funcs(("gbtrf",), (ab,))
@@ -230,17 +256,30 @@ def factorize_block(Ai: sp.csr_matrix, kl: int | None = None, ku: int | None = N
     return BlockFactor(n, kl, ku, lu, ipiv, dt)
 
 
+def _dense_storage(n: int, kl: int, ku: int, itemsize: int) -> bool:
+    """Store a block as a dense ?getrf LU when the band storage (2kl+ku+1) x n would be both
+    larger than n x n and over 1 GiB (c3 at P = 64: 4.2 GB band vs 1.5 GB dense per block).
+    Same factorization (LAPACK partial pivoting, first max |a| / izamax pivot, D3); only the
+    storage and the blocking of the roundoff differ."""
+    band = (2 * kl + ku + 1) * n * itemsize
+    return band > n * n * itemsize and band > (1 << 30)
+
+
 def _gbtrs(F: BlockFactor, R: np.ndarray, trans: int) -> np.ndarray:
     R = np.asarray(R)
     if R.shape[0] != F.n:
         raise DimensionError("solve_block: RHS rows must equal the block size")
     dt = np.result_type(F.dtype, R.dtype)
-    gbtrs, = lapack.get_lapack_funcs(("gbtrs",), (F.ab,))
     vec = R.ndim == 1
     Rm = np.array(R.reshape(F.n, -1), dtype=dt, order="F")
     if Rm.shape[1] == 0:
         return Rm.reshape(R.shape)
-    x, info = gbtrs(F.ab, F.kl, F.ku, Rm, F.ipiv, trans=trans)
+    if F.dense:
+        getrs, = lapack.get_lapack_funcs(("getrs",), (F.ab,))
+        x, info = getrs(F.ab, F.ipiv, Rm, trans=trans)
+    else:
+        gbtrs, = lapack.get_lapack_funcs(("gbtrs",), (F.ab,))
+        x, info = gbtrs(F.ab, F.kl, F.ku, Rm, F.ipiv, trans=trans)
     if info != 0:
         raise ParameterError(f"gbtrs failed {info}")
     return x.reshape(R.shape) if vec else x
@@ -349,6 +388,54 @@ def randomized_spike_svd(F: BlockFactor, coupling, side: int, n_svd: int, oversa
         collapsed = True
         sigma[sigma < 1e-14 * sigma[0]] = 0.0
         if s[0] == 0:
+            sigma[:] = 0.0
+    return LowRankSpike(u, sigma, v, side, collapsed)
+
+
+def coupling_spike_svd(F: BlockFactor, coupling, side: int, n_svd: int, oversample: int,
+                       passes: int, seed: int, partition: int) -> LowRankSpike:
+    """spike_mode = "coupling" (BASELINE.json north_star setup (1): "truncated rank-k SVD of
+    B_j and C_j ... form the low-rank spikes by multi-RHS solves against the k singular
+    vectors"; the construction the paper compares against at PAPER.md:939-943, :1272-1276
+    and SPEC acceptance 6).
+
+    Rank-r randomized SVD of the k x k coupling block (Halko range finder with exactly r
+    columns -- the first r columns of the spike mode's Omega stream -- and (passes - 2) / 2
+    power iterations):  Q_B = orth(B Omega_r),  Z^H = B^H Q_B,  Z = U^ S V^H, so
+    B_r = U_B S_B V_B^H with U_B = Q_B U^.  B_r = Q_B Q_B^H B is fixed by span(B Omega_r)
+    even when B's spectrum is flat (B ~ -I for the natural-ordered stencils), so no tie
+    among equal singular values decides the result.  The spike is
+    T~ = A_i^-1 pad(U_B S_B) V_B^H (r padded solves), returned in the LowRankSpike form
+    (orthonormal u, non-increasing sigma, orthonormal v) through Y = Q2 R2,
+    R2 = U2 S2 V2^H:  u = Q2 U2, sigma = S2, v = V2^H V_B^H."""
+    Cs = coupling.tocsr() if sp.issparse(coupling) else sp.csr_matrix(coupling)
+    k = Cs.shape[0]
+    l = n_svd + oversample
+    if n_svd < 1 or n_svd > k:
+        raise ParameterError("coupling_spike_svd: 1 <= n_svd <= k required")
+    if oversample < 0 or l > k:
+        raise ParameterError("coupling_spike_svd: n_svd + oversample <= k required")
+    if passes < 2:
+        raise ParameterError("coupling_spike_svd: passes >= 2 required")
+    Om = omega_block(seed, partition, side, k, l)[:, :n_svd]
+    CsH = Cs.conj().T if np.iscomplexobj(Cs.data) else Cs.T
+    QB = _orth(np.asarray(Cs @ Om))
+    for _ in range((passes - 2) // 2):
+        QB = _orth(np.asarray(Cs @ _orth(np.asarray(CsH @ QB))))
+    Zt = np.asarray(CsH @ QB)  # k x r = (Q_B^H B)^H
+    Uh, sB, VBh = np.linalg.svd(Zt.conj().T, full_matrices=False)  # Z = Uh diag(sB) VBh
+    UB = QB @ Uh
+    Y = solve_block(F, _pad(UB * sB, F.n, side))
+    Q2, R2 = np.linalg.qr(Y, mode="reduced")
+    U2, s2, V2h = np.linalg.svd(R2)
+    u = Q2 @ U2
+    sigma = s2.copy()
+    v = V2h @ VBh
+    collapsed = False
+    if sigma.size and (sigma[0] == 0 or np.any(sigma < 1e-14 * sigma[0])):
+        collapsed = True
+        sigma[sigma < 1e-14 * sigma[0]] = 0.0
+        if s2[0] == 0:
             sigma[:] = 0.0
     return LowRankSpike(u, sigma, v, side, collapsed)
 
@@ -508,6 +595,10 @@ class SolverConfig:
     otf_max_iters: int = 500
     otf_escalations: int = 4
     factor_fp32: bool = False  # FP32 off-diagonal factor tiles in the applies
+    # "spike": randomized SVD of the spike T_i = A_i^-1 [0; B_i] (default);
+    # "coupling": truncated SVD of B_i / C_i, spikes by multi-RHS solves against the
+    # singular vectors (BASELINE.json north_star setup (1))
+    spike_mode: str = "spike"
 
 
 @dataclass
@@ -537,7 +628,7 @@ def factorize(A: sp.csr_matrix, cfg: SolverConfig) -> SpikeFactorization:
     k = cfg.k if cfg.k is not None else band_metrics(A)[2]
     lay = make_layout(A.shape[0], cfg.p, k)
     blocks = extract_blocks(A, lay)
-    factors = [factorize_block(Ai) for Ai in blocks.A]
+    factors = _pmap(factorize_block, blocks.A)
     if cfg.variant not in ("T", "I", "OTF", "BJ"):
         raise ParameterError(f"unknown variant {cfg.variant!r}")
     n_svd = cfg.n_svd if cfg.variant in ("T", "I", "OTF") else 0
@@ -565,6 +656,8 @@ def round_offdiag_tiles(F: BlockFactor) -> BlockFactor:
     preconditioners, section 4.3): L / U entries (i, j) outside the 128 x 128 diagonal tiles
     rounded to FP32 (the GPU keeps those tiles in FP32 and the diagonal-tile inverses in
     FP64).  Band storage: ab[kl + ku + i - j, j] holds entry (i, j)."""
+    if F.dense:
+        raise ParameterError("factor_fp32 emulation needs band storage")
     ab = F.ab.copy()
     kv = F.kl + F.ku
     rows, cols = np.indices(ab.shape)
@@ -579,10 +672,13 @@ def _build_spikes(blocks, factors, cfg, n_svd, k):
     if n_svd == 0 or p == 1:
         return [], [None] * p, None, False
     os_ = cfg.oversample if cfg.oversample is not None else (n_svd + 1) // 2
-    spT = [randomized_spike_svd(factors[i], blocks.B[i], SIDE_T, n_svd, os_, cfg.passes,
-                                cfg.seed, i) for i in range(p - 1)]
-    spW = [None] + [randomized_spike_svd(factors[i], blocks.C[i], SIDE_W, n_svd, os_,
-                                         cfg.passes, cfg.seed, i) for i in range(1, p)]
+    if cfg.spike_mode not in ("spike", "coupling"):
+        raise ParameterError(f"unknown spike_mode {cfg.spike_mode!r}")
+    svd = randomized_spike_svd if cfg.spike_mode == "spike" else coupling_spike_svd
+    spT = _pmap(lambda i: svd(factors[i], blocks.B[i], SIDE_T, n_svd, os_, cfg.passes,
+                              cfg.seed, i), range(p - 1))
+    spW = [None] + _pmap(lambda i: svd(factors[i], blocks.C[i], SIDE_W, n_svd, os_, cfg.passes,
+                                       cfg.seed, i), range(1, p))
     coll = any(s.rank_collapsed for s in spT) or any(s.rank_collapsed for s in spW[1:])
     return spT, spW, None, coll
 
@@ -595,7 +691,7 @@ def _split(F: SpikeFactorization, f: np.ndarray):
 def apply_block_jacobi(F: SpikeFactorization, f: np.ndarray) -> np.ndarray:
     """D^-1 f, no communication."""
     f2 = f.reshape(f.shape[0], -1)
-    y = np.concatenate([solve_block(Fi, fi) for Fi, fi in zip(F.apply_factors(), _split(F, f2))])
+    y = np.concatenate(_pmap(solve_block, F.apply_factors(), _split(F, f2)))
     return y.reshape(f.shape)
 
 
@@ -606,7 +702,7 @@ def apply_precond_T(F: SpikeFactorization, f: np.ndarray) -> np.ndarray:
         return apply_block_jacobi(F, f)
     f2 = f.reshape(f.shape[0], -1)
     k = F.blocks.layout.k
-    ys = [solve_block(Fi, fi) for Fi, fi in zip(F.apply_factors(), _split(F, f2))]
+    ys = _pmap(solve_block, F.apply_factors(), _split(F, f2))
     top = [y[:k] for y in ys]
     bot = [y[-k:] for y in ys]
     xt, xb = apply_truncated_precond(F.trunc, top, bot, F.ledger)
@@ -720,7 +816,7 @@ def apply_precond_I(F: SpikeFactorization, f: np.ndarray) -> np.ndarray:
     f2 = f.reshape(f.shape[0], -1)
     lay = F.blocks.layout
     k, p = lay.k, lay.p
-    ys = [solve_block(Fi, fi) for Fi, fi in zip(F.apply_factors(), _split(F, f2))]
+    ys = _pmap(solve_block, F.apply_factors(), _split(F, f2))
     g = _pack([y[:k] for y in ys], [y[-k:] for y in ys])
     # the inner solve runs on the column-normalised reduced right-hand side (and scales
     # back): the reduced system is linear, and the absolute breakdown threshold then
@@ -755,7 +851,7 @@ def solve_otf(A: sp.csr_matrix, F: SpikeFactorization, f: np.ndarray, it: "IterC
     lay = F.blocks.layout
     k, p = lay.k, lay.p
     nr = f2.shape[1]
-    ys = [solve_block(Fi, fi) for Fi, fi in zip(F.apply_factors(), _split(F, f2))]
+    ys = _pmap(solve_block, F.apply_factors(), _split(F, f2))
     g = _pack([y[:k] for y in ys], [y[-k:] for y in ys])
     rep = SolveReport()
     rep.precond_applications = 1  # the D-stage

@@ -34,6 +34,7 @@ _VARIANTS = {"T": VARIANT_T, "BJ": VARIANT_BJ, "I": VARIANT_I, "OTF": VARIANT_OT
 GMRES, BICGSTAB, CG = 0, 1, 2
 _METHODS = {"gmres": GMRES, "bicgstab": BICGSTAB, "cg": CG}
 SIDE_T, SIDE_W = 0, 1
+_SPIKE_MODES = {"spike": 0, "coupling": 1}  # lrs_spike_mode
 STAGES = ("reduced-matvec", "precond-apply", "recovery")
 KERNEL_CLASSES = ("lu_diag", "lu_panel", "lu_update", "band_solve", "band_solve_adjoint", "spmv",
                   "iface_apply", "recovery", "krylov_vec", "setup_misc", "spike_band_solve")
@@ -46,7 +47,7 @@ class SolverCfgC(ctypes.Structure):
     _fields_ = [("variant", i32), ("passes", i32), ("p", i64), ("k", i64), ("n_svd", i64),
                 ("oversample", i64), ("seed", u64), ("inner_tol", f64), ("inner_max_iters", i64),
                 ("otf_tol", f64), ("otf_max_iters", i64), ("otf_escalations", i32),
-                ("factor_fp32", i32)]
+                ("factor_fp32", i32), ("spike_mode", i32)]
 
 
 class IterCfgC(ctypes.Structure):
@@ -274,6 +275,15 @@ def _buf(a, n_rows, dtype=np.float64):
     return arr.ctypes.data, arr.shape[0], MEM_HOST, arr.shape[1]
 
 
+def _check_out(mem, nc, memx, ncx):
+    """x_out must live where b lives (the library copies / writes through one memory
+    kind per call) and hold at least b's columns."""
+    if memx != mem:
+        raise DimensionError("x_out must live in the same memory as the right-hand side")
+    if ncx < nc:
+        raise DimensionError(f"x_out has {ncx} columns, the right-hand side {nc}")
+
+
 class Context:
     """One device + one stream (lrs_ctx).  ``stream`` may be a torch stream handle."""
 
@@ -368,10 +378,11 @@ class CsrMatrix:
         return cls(ctx, csr.n, csr.row_ptr, csr.col_idx, csr.values)
 
     def __del__(self):
-        # a matrix outliving its Context (e.g. held by a pytest traceback past the fixture's
-        # close) must not touch the destroyed context: its device memory went with it
+        # a matrix may outlive Context.close() (e.g. held by a pytest traceback past the
+        # fixture's close): lrs_ctx_destroy defers the context teardown until its last
+        # matrix / factorization handle is destroyed, so the handle is always freed here
         try:
-            if self.h and self.ctx.h:
+            if self.h:
                 lib().lrs_mat_destroy(self.h)
             self.h = None
         except Exception:
@@ -432,14 +443,20 @@ class SolverConfig:
     otf_max_iters: int = 500
     otf_escalations: int = 4
     factor_fp32: bool = False  # FP32 off-diagonal factor tiles in the applies
+    # "spike" (default) | "coupling" (truncated SVD of B_i / C_i, then
+    # padded solves against its singular vectors; north_star setup (1))
+    spike_mode: str = "spike"
 
     def c(self):
         if self.variant not in _VARIANTS:
             raise ParameterError(f"unknown variant {self.variant!r}")
+        if self.spike_mode not in _SPIKE_MODES:
+            raise ParameterError(f"unknown spike_mode {self.spike_mode!r}")
         return SolverCfgC(_VARIANTS[self.variant], self.passes, self.p, self.k or 0, self.n_svd,
                           -1 if self.oversample is None else self.oversample, self.seed,
                           self.inner_tol, self.inner_max_iters, self.otf_tol, self.otf_max_iters,
-                          self.otf_escalations, 1 if self.factor_fp32 else 0)
+                          self.otf_escalations, 1 if self.factor_fp32 else 0,
+                          _SPIKE_MODES[self.spike_mode])
 
 
 @dataclass
@@ -491,7 +508,7 @@ class SpikeFactorization:
 
     def __del__(self):
         try:
-            if self.h and self.ctx.h:  # see CsrMatrix.__del__
+            if self.h:  # see CsrMatrix.__del__
                 lib().lrs_fact_destroy(self.h)
             self.h = None
         except Exception:
@@ -616,11 +633,12 @@ def solve(A: CsrMatrix, f, cfg: SolverConfig | None = None, it: IterConfig | Non
             x_out = torch.empty((nc, A.n), dtype=_torch_dtype(dt), device=f.device).t()
         else:
             x_out = np.empty((A.n, nc), dtype=dt, order="F")
-    px, ldx, memx, _ = _buf(x_out, A.n, dt)
+    px, ldx, memx, ncx = _buf(x_out, A.n, dt)
+    _check_out(mem, nc, memx, ncx)
     x0p = None
     if it.initial_guess is not None:
-        x0p, ldx0, mem0, _ = _buf(it.initial_guess, A.n, dt)
-        if mem0 != mem or ldx0 != ldx:
+        x0p, ldx0, mem0, nc0 = _buf(it.initial_guess, A.n, dt)
+        if mem0 != mem or ldx0 != ldx or nc0 < nc:
             raise DimensionError("initial guess must match x's memory kind and layout")
     if it.method not in _METHODS:
         raise ParameterError(f"unknown Krylov method {it.method!r}")
@@ -694,12 +712,15 @@ def krylov(ctx: Context, apply_A, b, it: IterConfig | None = None, apply_M=None,
             x_out = torch.empty((nc, n), dtype=_torch_dtype(dt), device=b.device).t()
         else:
             x_out = np.empty((n, nc), dtype=dt, order="F")
-    px, ldx, _, _ = _buf(x_out, n, dt)
+    px, ldx, memx, ncx = _buf(x_out, n, dt)
+    _check_out(mem, nc, memx, ncx)
     if it.method not in _METHODS:
         raise ParameterError(f"unknown Krylov method {it.method!r}")
     x0p = None
     if it.initial_guess is not None:
-        x0p, _, _, _ = _buf(it.initial_guess, n, dt)
+        x0p, ldx0, mem0, nc0 = _buf(it.initial_guess, n, dt)
+        if mem0 != mem or ldx0 != ldx or nc0 < nc:
+            raise DimensionError("initial guess must match x's memory kind and layout")
     ic = IterCfgC(_METHODS[it.method], it.restart, it.tol, it.max_iters, it.breakdown_eps, x0p)
     opA, keepA = _operator(apply_A, n, dt)
     opM, keepM = (_operator(apply_M, n, dt) if apply_M is not None else (None, None))

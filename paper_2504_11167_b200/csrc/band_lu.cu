@@ -410,6 +410,11 @@ __device__ __forceinline__ void tile_gemm(const double* A, const double* B, doub
   if (MODE == 0 && maskB == MASK_UPPER && GEMM_SPLIT == 2) {
     // L_IK = A_IK inv(U_KK) is formed in place and each half-tile CTA reads all of A_IK:
     // the two halves (a cluster of 2) write only after both have read their operands
+    // a launch without the 2-CTA cluster attribute would make the barrier a no-op and
+    // bring the write-after-read race back silently: refuse to run instead
+    uint32_t ncta;
+    asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(ncta));
+    if (ncta != 2) __trap();
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" :::
                      "memory");
   }

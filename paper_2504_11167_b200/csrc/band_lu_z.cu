@@ -246,6 +246,11 @@ __device__ __forceinline__ void ztile_gemm(const zc* A, const zc* B, zc* C, int 
   if (MODE == 0 && maskB == ZMASK_UPPER) {
     // in-place L_IK = A_IK inv(U_KK): both half-tile CTAs (a cluster of 2) read all of A_IK
     // before either writes its half
+    // a launch without the 2-CTA cluster attribute would make the barrier a no-op and
+    // bring the write-after-read race back silently: refuse to run instead
+    uint32_t ncta;
+    asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(ncta));
+    if (ncta != 2) __trap();
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" :::
                      "memory");
   }

@@ -163,8 +163,7 @@ lrs_status lrs_ctx_create(int device, void* stream, lrs_ctx** out) {
   return s;
 }
 
-void lrs_ctx_destroy(lrs_ctx* c) {
-  if (!c) return;
+static void ctx_teardown(Ctx* c) {
   cudaStreamSynchronize(c->stream);
   c->collect();
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
@@ -175,7 +174,22 @@ void lrs_ctx_destroy(lrs_ctx* c) {
   if (c->ev1) cudaEventDestroy(c->ev1);
   if (c->own_stream) cudaStreamDestroy(c->stream);
   if (c->stream_hi) cudaStreamDestroy(c->stream_hi);
-  delete c;
+  delete static_cast<lrs_ctx*>(c);
+}
+
+// a matrix or factorization handle was destroyed: finish a deferred lrs_ctx_destroy
+static void ctx_release(Ctx* c) {
+  if (c && --c->children == 0 && c->closing) ctx_teardown(c);
+}
+
+void lrs_ctx_destroy(lrs_ctx* c) {
+  if (!c || c->closing) return;
+  if (c->children > 0) {  // handles still alive: tear down with the last of them
+    cudaStreamSynchronize(c->stream);
+    c->closing = true;
+    return;
+  }
+  ctx_teardown(c);
 }
 
 void* lrs_ctx_stream(lrs_ctx* c) { return c ? (void*)c->stream : nullptr; }
@@ -330,11 +344,19 @@ lrs_status lrs_mat_upload_csr(lrs_ctx* c, int64_t n, int64_t nnz, const int64_t*
     launch_csr_transpose(c, m.get());
     LRS_CUDA(cudaStreamSynchronize(c->stream));
   });
-  if (s == LRS_OK) *out = m.release();
+  if (s == LRS_OK) {
+    *out = m.release();
+    ++c->children;
+  }
   return s;
 }
 
-void lrs_mat_destroy(lrs_mat* m) { delete m; }
+void lrs_mat_destroy(lrs_mat* m) {
+  if (!m) return;
+  Ctx* c = m->ctx;
+  delete m;
+  ctx_release(c);
+}
 
 lrs_status lrs_mat_band_metrics(lrs_mat* m, int64_t* ku, int64_t* kl, int64_t* k,
                                 double* diag_weight, double* band_density) {
@@ -390,6 +412,7 @@ lrs_status lrs_factorize(lrs_ctx* c, lrs_mat* a, const lrs_solver_cfg* cfg, lrs_
     LRS_CUDA(cudaSetDevice(c->device));
     Fact* f = factorize(c, a, *cfg, nullptr);
     *out = static_cast<lrs_fact*>(f);
+    ++c->children;
   });
 }
 
@@ -401,6 +424,7 @@ lrs_status lrs_factorize_dist(lrs_ctx* c, lrs_mat* a, const lrs_solver_cfg* cfg,
     LRS_CUDA(cudaSetDevice(c->device));
     Fact* f = factorize(c, a, *cfg, comm);
     *out = static_cast<lrs_fact*>(f);
+    ++c->children;
   });
 }
 
@@ -421,8 +445,10 @@ lrs_status lrs_shard_plan(int64_t n, int64_t p, int32_t size, int32_t rank, int6
 
 void lrs_fact_destroy(lrs_fact* f) {
   if (!f) return;
-  cudaStreamSynchronize(f->ctx->stream);
+  Ctx* c = f->ctx;
+  cudaStreamSynchronize(c->stream);
   delete static_cast<Fact*>(f);
+  ctx_release(c);
 }
 
 lrs_status lrs_fact_get_info(lrs_fact* f, lrs_fact_info* info) {

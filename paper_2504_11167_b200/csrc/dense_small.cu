@@ -610,7 +610,26 @@ void launch_sigma_trunc(Ctx* c, const SigmaJob* d_jobs, int njobs, int r, int* d
   LRS_LAUNCHED(c);
 }
 
+template <class S>
+__global__ void scale_cols_kernel(const ScaleColsJobT<S>* jobs, int64_t m, int ncols) {
+  const ScaleColsJobT<S> jb = jobs[blockIdx.x];
+  for (int64_t e = threadIdx.x; e < m * ncols; e += blockDim.x) {
+    const int64_t i = e % m;
+    const int j = (int)(e / m);
+    jb.X[i + j * jb.ld] = s_scale(jb.X[i + j * jb.ld], jb.s[j]);
+  }
+}
+
+template <class S>
+void launch_scale_cols_t(Ctx* c, const ScaleColsJobT<S>* d_jobs, int njobs, int64_t m, int ncols) {
+  if (njobs == 0) return;
+  ProfScope ps_(c, K_SETUP);
+  scale_cols_kernel<S><<<njobs, 256, 0, c->stream>>>(d_jobs, m, ncols);
+  LRS_LAUNCHED(c);
+}
+
 #define LRS_INST(S)                                                                          \
+  template void launch_scale_cols_t<S>(Ctx*, const ScaleColsJobT<S>*, int, int64_t, int);    \
   template void launch_householder_qr_t<S>(Ctx*, const QrJobT<S>*, int, int, int64_t);       \
   template void launch_jacobi_svd_t<S>(Ctx*, const SvdJobT<S>*, int, int);                   \
   template void launch_small_gemm_t<S>(Ctx*, const GemmJobT<S>*, int, int64_t, int);         \

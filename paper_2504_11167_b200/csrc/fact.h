@@ -26,6 +26,7 @@ struct Fact {
   int64_t n = 0, k = 0, kl = 0, ku = 0;
   int r = 0, os = 0, l = 0, passes = 2;
   uint64_t seed = 0;
+  int spike_mode = LRS_SPIKE_SVD;
   int wl = 0, wu = 0, W = 1, Tmax = 0;
   std::vector<int64_t> off, size, tbase, fbase;  // local partitions (global row offsets)
   std::vector<int64_t> goff;                     // global partition offsets [Pg + 1]

@@ -189,6 +189,11 @@ size_t iface_work_doubles(int njobs, int r, int64_t k);  // in units of S
 // dst[j] = sig[j] for j < r, zeroed where sig[j] < 1e-14 sig[0] (rank collapse);
 // *flag = 1 if any spike collapsed.
 struct SigmaJob { const double* sig; double* dst; };
+// X[:, j] *= s[j] for the ncols columns of an m-row block (ld), one job per CTA
+template <class S>
+struct ScaleColsJobT { S* X; int64_t ld; const double* s; };
+template <class S>
+void launch_scale_cols_t(Ctx* c, const ScaleColsJobT<S>* d_jobs, int njobs, int64_t m, int ncols);
 void launch_sigma_trunc(Ctx* c, const SigmaJob* d_jobs, int njobs, int r, int* d_flag);
 // x[row] = y[row] - uW[row,:] scW[part] - uT[row,:] scT[part] over the local rows
 // [row_lo, row_hi); scT / scW hold one r x MAX_RHS block per GLOBAL partition.

@@ -94,6 +94,10 @@ struct Ctx {
   cudaStream_t stream = nullptr;
   cudaStream_t stream_hi = nullptr;  // high-priority side stream (LU look-ahead critical path)
   bool own_stream = false;
+  // live lrs_mat / lrs_fact handles created on this context: lrs_ctx_destroy defers the
+  // teardown (stream, pool, staging) until the last of them is destroyed
+  int64_t children = 0;
+  bool closing = false;
   int64_t launches = 0;
   lrs_error_info last{};
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;

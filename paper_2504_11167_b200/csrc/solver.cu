@@ -268,6 +268,165 @@ std::vector<double> make_omega(uint64_t seed, int Pg, int plo, int phi, int64_t 
   return h;
 }
 
+// spike_mode = coupling (BASELINE.json north_star setup (1)):
+// rank-r randomized SVD of each coupling block, then the spike by r padded solves against
+// its singular vectors.  Mirrors the checker's coupling_spike_svd step by step:
+//   Q_B = orth(B Om_r) [+ power passes]; B^H Q_B = Q_z R_1, R_1 = U_1 S_1 V_1^H
+//   => B_r = (Q_B V_1) S_1 (Q_z U_1)^H = U_B S_B V_B^H;
+//   Y = A_i^-1 pad(U_B S_B) = Q_2 R_2, R_2 = U_2 S_2 V_2^H
+//   => T~ = (Q_2 U_2) S_2 (V_B V_2)^H:  u = Q_2 U_2, sigma = S_2, v^T = conj(V_B V_2).
+// The k x l slots of Om / Zt hold k x r blocks (ld k); Rz / Ur / Vr slots r x r (ld r);
+// Y holds side T in columns [0, r) and side W in [r, 2r) (ld n).
+template <class S>
+void coupling_spikes(Fact* f, int r, int l, const std::vector<std::pair<int, int>>& spk,
+                     const S* Om, S* Y, S* Rz, S* Ur, S* Vr, double* sig) {
+  Ctx* c = f->ctx;
+  Mat* m = f->mat;
+  const int Pg = f->Pg;
+  const int64_t n = f->n, k = f->k;
+  constexpr int w = SW<S>;
+  auto slot = [&](int i, int side) { return (size_t)(2 * i + side); };
+  auto goff = [&](int i) { return f->goff[i]; };
+  auto gsize = [&](int i) { return f->goff[i + 1] - f->goff[i]; };
+  DevBuf<double> QBb, UBb, VBb, sig1b;
+  QBb.alloc((size_t)Pg * 2 * k * r * w);
+  UBb.alloc((size_t)Pg * 2 * k * r * w);
+  VBb.alloc((size_t)Pg * 2 * k * r * w);
+  sig1b.alloc((size_t)Pg * 2 * r);
+  S* QB = sp<S>(QBb);
+  S* UB = sp<S>(UBb);
+  S* VB = sp<S>(VBb);
+  const size_t kr = (size_t)k * r, ll = (size_t)l * l;
+  // X (k x r, slot stride k*l or k*r) -> B X / B^H X (k x r, slot stride k*r)
+  DevBuf<CoupleJobT<S>> cj;
+  auto couple = [&](bool adj, const S* src, size_t src_stride, S* dst, size_t dst_stride) {
+    std::vector<CoupleJobT<S>> jobs;
+    for (auto [i, side] : spk) {
+      CoupleJobT<S> j{};
+      const bool T = side == LRS_SIDE_T;
+      if (!adj) {  // B_i = A[off_i+n_i-k.., off_{i+1}..];  C_i = A[off_i.., off_i-k..]
+        j.r0 = T ? goff(i) + gsize(i) - k : goff(i);
+        j.c0 = T ? goff(i + 1) : goff(i) - k;
+      } else {  // B_i^H, C_i^H from the CSR of A^H
+        j.r0 = T ? goff(i + 1) : goff(i) - k;
+        j.c0 = T ? goff(i) + gsize(i) - k : goff(i);
+      }
+      j.b = k;
+      j.dst0 = 0;
+      j.X = src + slot(i, side) * src_stride;
+      j.ldx = k;
+      j.out = dst + slot(i, side) * dst_stride;
+      j.ldo = k;
+      j.ncols = r;
+      jobs.push_back(j);
+    }
+    upload(c, cj, jobs);
+    launch_coupling_t<S>(c, m, adj, cj.get(), (int)jobs.size(), k, r);
+  };
+  DevBuf<QrJobT<S>> qj;
+  auto orth_k = [&](S* base, size_t stride, bool keepR) {
+    std::vector<QrJobT<S>> jobs;
+    for (auto [i, side] : spk)
+      jobs.push_back(QrJobT<S>{base + slot(i, side) * stride, k, k,
+                               keepR ? Rz + slot(i, side) * ll : nullptr});
+    upload(c, qj, jobs);
+    launch_householder_qr_t<S>(c, qj.get(), (int)jobs.size(), r, k);
+  };
+  DevBuf<SvdJobT<S>> sj;
+  auto svd_r = [&](double* sg) {
+    std::vector<SvdJobT<S>> jobs;
+    for (auto [i, side] : spk) {
+      const size_t s = slot(i, side);
+      jobs.push_back(SvdJobT<S>{Rz + s * ll, Vr + s * ll, Ur + s * ll, sg + s * r});
+    }
+    upload(c, sj, jobs);
+    launch_jacobi_svd_t<S>(c, sj.get(), (int)jobs.size(), r);
+  };
+  DevBuf<GemmJobT<S>> gj;
+  auto gemm = [&](const std::vector<GemmJobT<S>>& jobs, int64_t maxm) {
+    upload(c, gj, jobs);
+    launch_small_gemm_t<S>(c, gj.get(), (int)jobs.size(), maxm, r);
+  };
+  // (1) range of B: Q_B = orth(B Om_r) (+ (passes - 2) / 2 power passes)
+  couple(false, Om, (size_t)k * l, QB, kr);
+  orth_k(QB, kr, false);
+  for (int pi = 0; pi < (f->passes - 2) / 2; ++pi) {
+    couple(true, QB, kr, UB, kr);
+    orth_k(UB, kr, false);
+    couple(false, UB, kr, QB, kr);
+    orth_k(QB, kr, false);
+  }
+  // (2) B^H Q_B = Q_z R_1 (Q_z in VB), R_1 = U_1 S_1 V_1^H
+  couple(true, QB, kr, VB, kr);
+  orth_k(VB, kr, true);
+  svd_r(sig1b.get());
+  // (3) U_B S_B = Q_B (V_1 S_1) into the padded RHS rows of Y; V_B = Q_z U_1 (into UB)
+  {
+    std::vector<ScaleColsJobT<S>> sc;
+    for (auto [i, side] : spk) {
+      const size_t s = slot(i, side);
+      sc.push_back(ScaleColsJobT<S>{Vr + s * ll, r, sig1b.get() + s * r});
+    }
+    DevBuf<ScaleColsJobT<S>> dsc;
+    upload(c, dsc, sc);
+    launch_scale_cols_t<S>(c, dsc.get(), (int)sc.size(), r, r);
+  }
+  LRS_CUDA(cudaMemsetAsync(Y, 0, sizeof(S) * n * 2 * r, c->stream));
+  {
+    std::vector<GemmJobT<S>> g1, g2;
+    for (auto [i, side] : spk) {
+      const size_t s = slot(i, side);
+      const int64_t row0 = side == LRS_SIDE_T ? goff(i) + gsize(i) - k : goff(i);
+      g1.push_back(GemmJobT<S>{QB + s * kr, k, Vr + s * ll, r, Y + row0 + (int64_t)side * r * n,
+                               n, k, r, r, 0});
+      g2.push_back(GemmJobT<S>{VB + s * kr, k, Ur + s * ll, r, UB + s * kr, k, k, r, r, 0});
+    }
+    gemm(g1, k);
+    gemm(g2, k);
+  }
+  // (4) Y = A_i^-1 pad(U_B S_B) (2r columns: the T and W sides), Y = Q_2 R_2
+  dstage_t(f, Y, n, 2 * r, false, -1);
+  {
+    std::vector<QrJobT<S>> jobs;
+    int64_t mm = n;
+    for (auto [i, side] : spk) {
+      jobs.push_back(QrJobT<S>{Y + goff(i) + (int64_t)side * r * n, gsize(i), n,
+                               Rz + slot(i, side) * ll});
+      mm = std::min(mm, gsize(i));
+    }
+    upload(c, qj, jobs);
+    launch_householder_qr_t<S>(c, qj.get(), (int)jobs.size(), r, mm);
+  }
+  // (5) R_2 = U_2 S_2 V_2^H:  u = Q_2 U_2, v^T = conj(V_B V_2), sigma = S_2 (rank collapse)
+  svd_r(sig);
+  std::vector<GemmJobT<S>> gu, gv;
+  std::vector<SigmaJob> sjobs;
+  int64_t maxm = 0;
+  for (auto [i, side] : spk) {
+    const size_t s = slot(i, side);
+    S* ubuf = side == LRS_SIDE_T ? sp<S>(f->uT) : sp<S>(f->uW);
+    S* vbuf = side == LRS_SIDE_T ? sp<S>(f->vtT) : sp<S>(f->vtW);
+    double* sbuf = side == LRS_SIDE_T ? f->sT.get() : f->sW.get();
+    gu.push_back(GemmJobT<S>{Y + goff(i) + (int64_t)side * r * n, n, Ur + s * ll, r,
+                             ubuf + goff(i), n, gsize(i), r, r, 0});
+    gv.push_back(GemmJobT<S>{UB + s * kr, k, Vr + s * ll, r, vbuf + (size_t)i * k * r, k, k, r,
+                             r, IsC<S>::value ? 1 : 0});
+    sjobs.push_back(SigmaJob{sig + s * r, sbuf + (size_t)i * r});
+    maxm = std::max(maxm, gsize(i));
+  }
+  gemm(gu, maxm);
+  gemm(gv, k);
+  DevBuf<SigmaJob> dsj;
+  upload(c, dsj, sjobs);
+  DevBuf<int> flag;
+  flag.alloc(1);
+  LRS_CUDA(cudaMemsetAsync(flag.get(), 0, sizeof(int), c->stream));
+  launch_sigma_trunc(c, dsj.get(), (int)sjobs.size(), r, flag.get());
+  int hflag = 0;
+  download(c, &hflag, flag.get(), 1);
+  f->rank_collapsed = hflag != 0;
+}
+
 template <class S>
 bool build_lowrank(Fact* f, int r, int* bad_iface, double* bad_cond, std::vector<double>* pre) {
   Ctx* c = f->ctx;
@@ -322,90 +481,6 @@ bool build_lowrank(Fact* f, int r, int* bad_iface, double* bad_cond, std::vector
     }
     LRS_CUDA(cudaMemcpy(Om, h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice));
   }
-  auto ycol = [&](S* base, int i, int side) { return base + goff(i) + (int64_t)side * l * n; };
-  // T_apply: Y = A_i^-1 pad(coupling X) for every spike, X = k x l blocks in src[slot]
-  DevBuf<CoupleJobT<S>> cj;
-  auto T_apply = [&](const S* src) {
-    std::vector<CoupleJobT<S>> jobs;
-    for (auto [i, side] : spk) {
-      CoupleJobT<S> j{};
-      if (side == LRS_SIDE_T) {
-        j.r0 = goff(i) + gsize(i) - k;
-        j.c0 = goff(i + 1);
-      } else {
-        j.r0 = goff(i);
-        j.c0 = goff(i) - k;
-      }
-      j.b = k;
-      j.dst0 = j.r0;
-      j.X = src + slot(i, side) * k * l;
-      j.ldx = k;
-      j.out = Y + (int64_t)side * l * n;
-      j.ldo = n;
-      j.ncols = l;
-      jobs.push_back(j);
-    }
-    LRS_CUDA(cudaMemsetAsync(Y, 0, sizeof(S) * n * L2, c->stream));
-    upload(c, cj, jobs);
-    launch_coupling_t<S>(c, m, false, cj.get(), (int)jobs.size(), k, l);
-    dstage_t(f, Y, n, L2, false, -1);
-  };
-  // Tt_apply: Zt[slot] = coupling^H (A_i^-H Q)|tip, Q = columns of Y  (= T^H Q)
-  auto Tt_apply = [&]() {
-    copy_block(c, Sx, n, Y, n, n, L2);
-    dstage_t(f, Sx, n, L2, true, -1);
-    std::vector<CoupleJobT<S>> jobs;
-    for (auto [i, side] : spk) {
-      CoupleJobT<S> j{};
-      if (side == LRS_SIDE_T) {  // B_i^H = A^H[off_{i+1} .., off_i+n_i-k ..]
-        j.r0 = goff(i + 1);
-        j.c0 = goff(i) + gsize(i) - k;
-      } else {  // C_i^H = A^H[off_i - k .., off_i ..]
-        j.r0 = goff(i) - k;
-        j.c0 = goff(i);
-      }
-      j.b = k;
-      j.dst0 = 0;
-      j.X = Sx + j.c0 + (int64_t)side * l * n;
-      j.ldx = n;
-      j.out = Zt + slot(i, side) * k * l;
-      j.ldo = k;
-      j.ncols = l;
-      jobs.push_back(j);
-    }
-    upload(c, cj, jobs);
-    launch_coupling_t<S>(c, m, true, cj.get(), (int)jobs.size(), k, l);
-  };
-  DevBuf<QrJobT<S>> qj;
-  auto orth_Y = [&]() {
-    std::vector<QrJobT<S>> jobs;
-    int64_t mm = n;
-    for (auto [i, side] : spk) {
-      jobs.push_back(QrJobT<S>{ycol(Y, i, side), gsize(i), n, nullptr});
-      mm = std::min(mm, gsize(i));
-    }
-    upload(c, qj, jobs);
-    launch_householder_qr_t<S>(c, qj.get(), (int)jobs.size(), l, mm);
-  };
-  auto orth_Zt = [&](bool keepR) {
-    std::vector<QrJobT<S>> jobs;
-    for (auto [i, side] : spk)
-      jobs.push_back(QrJobT<S>{Zt + slot(i, side) * k * l, k, k,
-                               keepR ? Rz + slot(i, side) * l * l : nullptr});
-    upload(c, qj, jobs);
-    launch_householder_qr_t<S>(c, qj.get(), (int)jobs.size(), l, k);
-  };
-
-  T_apply(Om);
-  orth_Y();
-  for (int pi = 0; pi < (f->passes - 2) / 2; ++pi) {
-    Tt_apply();
-    orth_Zt(false);
-    T_apply(Zt);
-    orth_Y();
-  }
-  Tt_apply();          // Zt = (Q^H T)^H, k x l
-  orth_Zt(true);       // Zt = Q_z R_z
   f->uT.alloc((size_t)n * r * w);
   f->uW.alloc((size_t)n * r * w);
   f->vtT.alloc((size_t)Pg * k * r * w);
@@ -418,46 +493,134 @@ bool build_lowrank(Fact* f, int r, int* bad_iface, double* bad_cond, std::vector
   LRS_CUDA(cudaMemsetAsync(f->vtW.get(), 0, sizeof(S) * Pg * k * r, c->stream));
   LRS_CUDA(cudaMemsetAsync(f->sT.get(), 0, sizeof(double) * Pg * r, c->stream));
   LRS_CUDA(cudaMemsetAsync(f->sW.get(), 0, sizeof(double) * Pg * r, c->stream));
-  {
-    std::vector<SvdJobT<S>> jobs;
-    for (auto [i, side] : spk) {
-      const size_t s = slot(i, side);
-      jobs.push_back(SvdJobT<S>{Rz + s * l * l, Vr + s * l * l, Ur + s * l * l, sig.get() + s * l});
+  if (f->spike_mode == LRS_SPIKE_COUPLING) {
+    coupling_spikes<S>(f, r, l, spk, Om, Y, Rz, Ur, Vr, sig.get());
+  } else {
+    auto ycol = [&](S* base, int i, int side) { return base + goff(i) + (int64_t)side * l * n; };
+    // T_apply: Y = A_i^-1 pad(coupling X) for every spike, X = k x l blocks in src[slot]
+    DevBuf<CoupleJobT<S>> cj;
+    auto T_apply = [&](const S* src) {
+      std::vector<CoupleJobT<S>> jobs;
+      for (auto [i, side] : spk) {
+        CoupleJobT<S> j{};
+        if (side == LRS_SIDE_T) {
+          j.r0 = goff(i) + gsize(i) - k;
+          j.c0 = goff(i + 1);
+        } else {
+          j.r0 = goff(i);
+          j.c0 = goff(i) - k;
+        }
+        j.b = k;
+        j.dst0 = j.r0;
+        j.X = src + slot(i, side) * k * l;
+        j.ldx = k;
+        j.out = Y + (int64_t)side * l * n;
+        j.ldo = n;
+        j.ncols = l;
+        jobs.push_back(j);
+      }
+      LRS_CUDA(cudaMemsetAsync(Y, 0, sizeof(S) * n * L2, c->stream));
+      upload(c, cj, jobs);
+      launch_coupling_t<S>(c, m, false, cj.get(), (int)jobs.size(), k, l);
+      dstage_t(f, Y, n, L2, false, -1);
+    };
+    // Tt_apply: Zt[slot] = coupling^H (A_i^-H Q)|tip, Q = columns of Y  (= T^H Q)
+    auto Tt_apply = [&]() {
+      copy_block(c, Sx, n, Y, n, n, L2);
+      dstage_t(f, Sx, n, L2, true, -1);
+      std::vector<CoupleJobT<S>> jobs;
+      for (auto [i, side] : spk) {
+        CoupleJobT<S> j{};
+        if (side == LRS_SIDE_T) {  // B_i^H = A^H[off_{i+1} .., off_i+n_i-k ..]
+          j.r0 = goff(i + 1);
+          j.c0 = goff(i) + gsize(i) - k;
+        } else {  // C_i^H = A^H[off_i - k .., off_i ..]
+          j.r0 = goff(i) - k;
+          j.c0 = goff(i);
+        }
+        j.b = k;
+        j.dst0 = 0;
+        j.X = Sx + j.c0 + (int64_t)side * l * n;
+        j.ldx = n;
+        j.out = Zt + slot(i, side) * k * l;
+        j.ldo = k;
+        j.ncols = l;
+        jobs.push_back(j);
+      }
+      upload(c, cj, jobs);
+      launch_coupling_t<S>(c, m, true, cj.get(), (int)jobs.size(), k, l);
+    };
+    DevBuf<QrJobT<S>> qj;
+    auto orth_Y = [&]() {
+      std::vector<QrJobT<S>> jobs;
+      int64_t mm = n;
+      for (auto [i, side] : spk) {
+        jobs.push_back(QrJobT<S>{ycol(Y, i, side), gsize(i), n, nullptr});
+        mm = std::min(mm, gsize(i));
+      }
+      upload(c, qj, jobs);
+      launch_householder_qr_t<S>(c, qj.get(), (int)jobs.size(), l, mm);
+    };
+    auto orth_Zt = [&](bool keepR) {
+      std::vector<QrJobT<S>> jobs;
+      for (auto [i, side] : spk)
+        jobs.push_back(QrJobT<S>{Zt + slot(i, side) * k * l, k, k,
+                                 keepR ? Rz + slot(i, side) * l * l : nullptr});
+      upload(c, qj, jobs);
+      launch_householder_qr_t<S>(c, qj.get(), (int)jobs.size(), l, k);
+    };
+
+    T_apply(Om);
+    orth_Y();
+    for (int pi = 0; pi < (f->passes - 2) / 2; ++pi) {
+      Tt_apply();
+      orth_Zt(false);
+      T_apply(Zt);
+      orth_Y();
     }
-    DevBuf<SvdJobT<S>> sj;
-    upload(c, sj, jobs);
-    launch_jacobi_svd_t<S>(c, sj.get(), (int)jobs.size(), l);
-    // Z = V_R S (Q_z U_R)^H  =>  u = Q V_R[:, :r],  v^T = conj(Q_z U_R[:, :r])
-    std::vector<GemmJobT<S>> gu, gv;
-    std::vector<SigmaJob> sjobs;
-    int64_t maxm = 0;
-    for (auto [i, side] : spk) {
-      const size_t s = slot(i, side);
-      S* ubuf = side == LRS_SIDE_T ? sp<S>(f->uT) : sp<S>(f->uW);
-      S* vbuf = side == LRS_SIDE_T ? sp<S>(f->vtT) : sp<S>(f->vtW);
-      double* sbuf = side == LRS_SIDE_T ? f->sT.get() : f->sW.get();
-      gu.push_back(GemmJobT<S>{ycol(Y, i, side), n, Vr + s * l * l, l, ubuf + goff(i), n,
-                               gsize(i), r, l, 0});
-      gv.push_back(GemmJobT<S>{Zt + s * k * l, k, Ur + s * l * l, l, vbuf + (size_t)i * k * r, k,
-                               k, r, l, IsC<S>::value ? 1 : 0});
-      sjobs.push_back(SigmaJob{sig.get() + s * l, sbuf + (size_t)i * r});
-      maxm = std::max(maxm, gsize(i));
+    Tt_apply();          // Zt = (Q^H T)^H, k x l
+    orth_Zt(true);       // Zt = Q_z R_z
+    {
+      std::vector<SvdJobT<S>> jobs;
+      for (auto [i, side] : spk) {
+        const size_t s = slot(i, side);
+        jobs.push_back(SvdJobT<S>{Rz + s * l * l, Vr + s * l * l, Ur + s * l * l, sig.get() + s * l});
+      }
+      DevBuf<SvdJobT<S>> sj;
+      upload(c, sj, jobs);
+      launch_jacobi_svd_t<S>(c, sj.get(), (int)jobs.size(), l);
+      // Z = V_R S (Q_z U_R)^H  =>  u = Q V_R[:, :r],  v^T = conj(Q_z U_R[:, :r])
+      std::vector<GemmJobT<S>> gu, gv;
+      std::vector<SigmaJob> sjobs;
+      int64_t maxm = 0;
+      for (auto [i, side] : spk) {
+        const size_t s = slot(i, side);
+        S* ubuf = side == LRS_SIDE_T ? sp<S>(f->uT) : sp<S>(f->uW);
+        S* vbuf = side == LRS_SIDE_T ? sp<S>(f->vtT) : sp<S>(f->vtW);
+        double* sbuf = side == LRS_SIDE_T ? f->sT.get() : f->sW.get();
+        gu.push_back(GemmJobT<S>{ycol(Y, i, side), n, Vr + s * l * l, l, ubuf + goff(i), n,
+                                 gsize(i), r, l, 0});
+        gv.push_back(GemmJobT<S>{Zt + s * k * l, k, Ur + s * l * l, l, vbuf + (size_t)i * k * r, k,
+                                 k, r, l, IsC<S>::value ? 1 : 0});
+        sjobs.push_back(SigmaJob{sig.get() + s * l, sbuf + (size_t)i * r});
+        maxm = std::max(maxm, gsize(i));
+      }
+      DevBuf<GemmJobT<S>> dgu, dgv;
+      upload(c, dgu, gu);
+      upload(c, dgv, gv);
+      launch_small_gemm_t<S>(c, dgu.get(), (int)gu.size(), maxm, r);
+      launch_small_gemm_t<S>(c, dgv.get(), (int)gv.size(), k, r);
+      DevBuf<SigmaJob> dsj;
+      upload(c, dsj, sjobs);
+      DevBuf<int> flag;
+      flag.alloc(1);
+      LRS_CUDA(cudaMemsetAsync(flag.get(), 0, sizeof(int), c->stream));
+      launch_sigma_trunc(c, dsj.get(), (int)sjobs.size(), r, flag.get());
+      int hflag = 0;
+      download(c, &hflag, flag.get(), 1);
+      f->rank_collapsed = hflag != 0;
     }
-    DevBuf<GemmJobT<S>> dgu, dgv;
-    upload(c, dgu, gu);
-    upload(c, dgv, gv);
-    launch_small_gemm_t<S>(c, dgu.get(), (int)gu.size(), maxm, r);
-    launch_small_gemm_t<S>(c, dgv.get(), (int)gv.size(), k, r);
-    DevBuf<SigmaJob> dsj;
-    upload(c, dsj, sjobs);
-    DevBuf<int> flag;
-    flag.alloc(1);
-    LRS_CUDA(cudaMemsetAsync(flag.get(), 0, sizeof(int), c->stream));
-    launch_sigma_trunc(c, dsj.get(), (int)sjobs.size(), r, flag.get());
-    int hflag = 0;
-    download(c, &hflag, flag.get(), 1);
-    f->rank_collapsed = hflag != 0;
-  }
+  }  // spike_mode
   // C5: ship the T side of the last local partition right and the W side of the first
   // local partition left: [u tip (k x r) | v^T (k x r) | sigma (r, real)]
   if (f->dist) {
@@ -661,6 +824,9 @@ Fact* factorize(Ctx* c, Mat* m, const lrs_solver_cfg& cfg, const lrs_comm* comm)
   f->passes = cfg.passes > 0 ? cfg.passes : 2;
   f->seed = cfg.seed;
   f->os = (int)cfg.oversample;
+  if (cfg.spike_mode != LRS_SPIKE_SVD && cfg.spike_mode != LRS_SPIKE_COUPLING)
+    throw LrsError(LRS_ERR_PARAMETER, "spike_mode must be LRS_SPIKE_SVD or LRS_SPIKE_COUPLING");
+  f->spike_mode = cfg.spike_mode;
   // global layout and this rank's shard
   {
     const int64_t Pg = f->Pg, n = f->n;

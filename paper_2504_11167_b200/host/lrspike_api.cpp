@@ -221,6 +221,7 @@ SpikeFactorization::SpikeFactorization(std::shared_ptr<DeviceMatrix> a, const So
   c.otf_max_iters = cfg.otf_max_iters;
   c.otf_escalations = cfg.otf_escalations;
   c.factor_fp32 = cfg.factor_fp32 ? 1 : 0;
+  c.spike_mode = cfg.spike_mode == SpikeMode::CouplingSvd ? LRS_SPIKE_COUPLING : LRS_SPIKE_SVD;
   c.passes = cfg.passes;
   c.p = cfg.p;
   c.k = cfg.k;
