@@ -4,6 +4,9 @@
   workload): the oracle's full solve is too slow to repeat in a test (c2: ~10 min, 26 GB),
   so tests/golden/make_full_fixtures.py ran it once and committed x, the iteration count
   and the residual (tests/golden/full_c1.*, full_c2.*).
+* c3 at FULL size with P = 64 (BASELINE.json configs[2], the bench workload): the oracle
+  run needs ~100 GB and ~6 min on 16 cores, so it ran once on the GPU box's host
+  (LRS_ORACLE_THREADS=16; tests/golden/c3_s1_P64.*).
 * LR-SPIKE-T + GMRES(50) on the c3 structure (27-point, 10^4 coefficient contrast, r = 32:
   l = 48 spike columns) at P = 8 and P = 16, and on the c4 structure (random band,
   P = 64, r = 64: l = 96, the 96-column sweep groups), with the INT8-sliced LU update on
@@ -31,6 +34,9 @@ CASES = [  # (fixture tag, config, scale, P)
     ("c3_s0.333333_P16", "c3", 32 / 96, 16),
     ("c3_s0.416667_P32", "c3", 40 / 96, 32),  # 90 GMRES(50) steps: one restart
     ("c4_s0.05_P64", "c4", 0.05, 64),
+    # the bench workload itself: c3 at full size, P = 64 (312 GMRES(50) steps, 6 restarts);
+    # the oracle run took 91 s + 272 s on the GPU box's 16 host cores
+    ("c3_s1_P64", "c3", 1.0, 64),
 ]
 
 
