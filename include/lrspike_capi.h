@@ -22,6 +22,9 @@
  *   lrs_solve               solve + bicgstab / cg / GMRES(m), solve_otf for LR-SPIKE-OTF
  *                           SPEC.md:520-528, :421-436, :503-511 (GMRES: SURVEY D1)
  *   lrs_krylov              bicgstab / cg / GMRES(m) on caller operators
+ *   lrs_reduced_apply       matvec_lowrank / matvec_otf / apply_truncated_precond
+ *   lrs_trunc_precond_create build_truncated_precond from explicit spikes
+ *   lrs_dense_qr / _svd / _gemm  the dense steps of randomized_spike_svd
  *   lrs_last_error          the exception taxonomy      proj/core/include/lrspike/errors.hpp:11-94
  *
  * Memory: pointers tagged LRS_MEM_HOST are copied by the library (the caller
@@ -243,6 +246,32 @@ LRS_API lrs_status lrs_apply_precond_T(lrs_fact* f, const void* in, int64_t ld_i
 enum { LRS_REDUCED_MATVEC_LOWRANK = 0, LRS_REDUCED_MATVEC_EXACT = 1, LRS_REDUCED_TRUNC_PRECOND = 2 };
 LRS_API lrs_status lrs_reduced_apply(lrs_fact* f, int32_t kind, const void* x, int64_t ldx,
                                      void* y, int64_t ldy, int64_t n_rhs, int32_t mem);
+
+/* ---- small dense GPU operations (building blocks of randomized_spike_svd) -- */
+/* Householder QR of the m x ncols block A (1 <= ncols <= 96 <= ..., ncols <= m): A is
+ * overwritten by the explicit Q; R (ncols x ncols, ld ncols) is written if non-NULL. */
+LRS_API lrs_status lrs_dense_qr(lrs_ctx* ctx, int32_t scalar, int64_t m, int64_t ncols, void* A,
+                                int64_t lda, void* R, int32_t mem);
+/* One-sided Jacobi SVD of the l x l matrix R (ld l, l <= 96; destroyed):
+ * R = U diag(sigma) V^H, sigma descending, U and V l x l (ld l). */
+LRS_API lrs_status lrs_dense_svd(lrs_ctx* ctx, int32_t scalar, int64_t l, void* R, void* U,
+                                 void* V, double* sigma, int32_t mem);
+/* C (m x n) = A (m x k) B (k x n) with k x n <= 96 x 64 (conjC: C = conj(A B)). */
+LRS_API lrs_status lrs_dense_gemm(lrs_ctx* ctx, int32_t scalar, int64_t m, int64_t n, int64_t k,
+                                  const void* A, int64_t lda, const void* B, int64_t ldb, void* C,
+                                  int64_t ldc, int32_t conjC, int32_t mem);
+/* build_truncated_precond from explicit LowRankSpikes of p partitions:
+ *   uT_tips  (p-1) consecutive k x r blocks: the bottom tip of u of T_i, i = 0..p-2
+ *   vT       (p-1) consecutive r x k blocks: v of T_i;  sT (p-1) x r: sigma of T_i
+ *   uW_tips  (p-1) consecutive k x r blocks: the top tip of u of W_i, i = 1..p-1
+ *   vW, sW   likewise for W_i.
+ * Returns a handle whose lrs_reduced_apply runs apply_truncated_precond and
+ * matvec_lowrank on ReducedVectors; IllConditionedInterfaceError (interface
+ * index, cond_1) when cond_1(K) or cond_1(H) of an interface exceeds 1e12. */
+LRS_API lrs_status lrs_trunc_precond_create(lrs_ctx* ctx, int32_t scalar, int64_t p, int64_t k,
+                                            int64_t r, const void* uT_tips, const void* vT,
+                                            const double* sT, const void* uW_tips, const void* vW,
+                                            const double* sW, int32_t mem, lrs_fact** out);
 
 /* ---- solve ------------------------------------------------------------------------ */
 LRS_API lrs_status lrs_solve(lrs_fact* f, lrs_mat* a, const void* b, int64_t ldb, void* x,

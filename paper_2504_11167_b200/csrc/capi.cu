@@ -690,6 +690,156 @@ lrs_status lrs_krylov(lrs_ctx* c, int64_t n, int32_t scalar, const lrs_operator*
   });
 }
 
+// ---- small dense operations and the truncated preconditioner from explicit spikes --------
+static int scalar_w(int32_t scalar) {
+  if (scalar != LRS_F64 && scalar != LRS_C128)
+    throw LrsError(LRS_ERR_PARAMETER, "scalar must be LRS_F64 or LRS_C128");
+  return scalar == LRS_C128 ? 2 : 1;
+}
+
+lrs_status lrs_dense_qr(lrs_ctx* c, int32_t scalar, int64_t m, int64_t ncols, void* A, int64_t lda,
+                        void* R, int32_t mem) {
+  if (!c || !A) return LRS_ERR_PARAMETER;
+  return guard(c, [&] {
+    check_mem(mem);
+    const int w = scalar_w(scalar);
+    if (ncols < 1 || ncols > 96 || m < ncols || lda < m)
+      throw LrsError(LRS_ERR_DIMENSION, "dense_qr: 1 <= ncols <= 96, ncols <= m <= lda");
+    LRS_CUDA(cudaSetDevice(c->device));
+    DevBuf<double> ao, ro;
+    int64_t la;
+    void* ad = dev_in(c, A, lda, m, ncols, mem, ao, &la, w);
+    void* rd = nullptr;
+    if (R) {
+      if (mem == LRS_MEM_DEVICE) {
+        rd = R;
+      } else {
+        ro.alloc((size_t)ncols * ncols * w);
+        rd = ro.get();
+      }
+    }
+    if (scalar == LRS_C128) {
+      DevBuf<QrJobT<zc>> j;
+      std::vector<QrJobT<zc>> h{{static_cast<zc*>(ad), m, la, static_cast<zc*>(rd)}};
+      j.alloc(1);
+      c->stage_h2d(j.get(), h.data(), sizeof(h[0]));
+      launch_householder_qr_t<zc>(c, j.get(), 1, (int)ncols, m);
+    } else {
+      DevBuf<QrJobT<double>> j;
+      std::vector<QrJobT<double>> h{{static_cast<double*>(ad), m, la, static_cast<double*>(rd)}};
+      j.alloc(1);
+      c->stage_h2d(j.get(), h.data(), sizeof(h[0]));
+      launch_householder_qr_t<double>(c, j.get(), 1, (int)ncols, m);
+    }
+    dev_out_finish(c, A, lda, ad, m, ncols, mem, w);
+    if (R) dev_out_finish(c, R, ncols, rd, ncols, ncols, mem, w);
+    LRS_CUDA(cudaStreamSynchronize(c->stream));
+  });
+}
+
+lrs_status lrs_dense_svd(lrs_ctx* c, int32_t scalar, int64_t l, void* R, void* U, void* V,
+                         double* sigma, int32_t mem) {
+  if (!c || !R || !U || !V || !sigma) return LRS_ERR_PARAMETER;
+  return guard(c, [&] {
+    check_mem(mem);
+    const int w = scalar_w(scalar);
+    if (l < 1 || l > 96) throw LrsError(LRS_ERR_DIMENSION, "dense_svd: 1 <= l <= 96");
+    LRS_CUDA(cudaSetDevice(c->device));
+    DevBuf<double> ro, uo, vo, so;
+    int64_t lr, lu, lv;
+    void* rd = dev_in(c, R, l, l, l, mem, ro, &lr, w);
+    void* ud = dev_in(c, U, l, l, l, mem, uo, &lu, w);
+    void* vd = dev_in(c, V, l, l, l, mem, vo, &lv, w);
+    double* sd = sigma;
+    if (mem == LRS_MEM_HOST) {
+      so.alloc(l);
+      sd = so.get();
+    }
+    if (scalar == LRS_C128) {
+      DevBuf<SvdJobT<zc>> j;
+      SvdJobT<zc> h{static_cast<zc*>(rd), static_cast<zc*>(vd), static_cast<zc*>(ud), sd};
+      j.alloc(1);
+      c->stage_h2d(j.get(), &h, sizeof(h));
+      launch_jacobi_svd_t<zc>(c, j.get(), 1, (int)l);
+    } else {
+      DevBuf<SvdJobT<double>> j;
+      SvdJobT<double> h{static_cast<double*>(rd), static_cast<double*>(vd),
+                        static_cast<double*>(ud), sd};
+      j.alloc(1);
+      c->stage_h2d(j.get(), &h, sizeof(h));
+      launch_jacobi_svd_t<double>(c, j.get(), 1, (int)l);
+    }
+    dev_out_finish(c, U, l, ud, l, l, mem, w);
+    dev_out_finish(c, V, l, vd, l, l, mem, w);
+    if (mem == LRS_MEM_HOST)
+      LRS_CUDA(cudaMemcpy(sigma, sd, sizeof(double) * l, cudaMemcpyDeviceToHost));
+    LRS_CUDA(cudaStreamSynchronize(c->stream));
+  });
+}
+
+lrs_status lrs_dense_gemm(lrs_ctx* c, int32_t scalar, int64_t m, int64_t n, int64_t k,
+                          const void* A, int64_t lda, const void* B, int64_t ldb, void* C,
+                          int64_t ldc, int32_t conjC, int32_t mem) {
+  if (!c || !A || !B || !C) return LRS_ERR_PARAMETER;
+  return guard(c, [&] {
+    check_mem(mem);
+    const int w = scalar_w(scalar);
+    if (m < 0 || n < 1 || k < 1 || n * k > 96 * 64 || lda < m || ldb < k || ldc < m)
+      throw LrsError(LRS_ERR_DIMENSION, "dense_gemm: k x n <= 96 x 64 and ld >= rows");
+    LRS_CUDA(cudaSetDevice(c->device));
+    DevBuf<double> ao, bo, co;
+    int64_t la, lb, lc;
+    const void* ad = dev_in(c, A, lda, m, k, mem, ao, &la, w);
+    const void* bd = dev_in(c, B, ldb, k, n, mem, bo, &lb, w);
+    void* cd = dev_in(c, C, ldc, m, n, mem, co, &lc, w);
+    if (scalar == LRS_C128) {
+      DevBuf<GemmJobT<zc>> j;
+      GemmJobT<zc> h{static_cast<const zc*>(ad), la, static_cast<const zc*>(bd), lb,
+                     static_cast<zc*>(cd), lc, m, (int)n, (int)k, conjC ? 1 : 0};
+      j.alloc(1);
+      c->stage_h2d(j.get(), &h, sizeof(h));
+      launch_small_gemm_t<zc>(c, j.get(), 1, m, (int)n);
+    } else {
+      DevBuf<GemmJobT<double>> j;
+      GemmJobT<double> h{static_cast<const double*>(ad), la, static_cast<const double*>(bd), lb,
+                         static_cast<double*>(cd), lc, m, (int)n, (int)k, conjC ? 1 : 0};
+      j.alloc(1);
+      c->stage_h2d(j.get(), &h, sizeof(h));
+      launch_small_gemm_t<double>(c, j.get(), 1, m, (int)n);
+    }
+    dev_out_finish(c, C, ldc, cd, m, n, mem, w);
+    LRS_CUDA(cudaStreamSynchronize(c->stream));
+  });
+}
+
+lrs_status lrs_trunc_precond_create(lrs_ctx* c, int32_t scalar, int64_t p, int64_t k, int64_t r,
+                                    const void* uT_tips, const void* vT, const double* sT,
+                                    const void* uW_tips, const void* vW, const double* sW,
+                                    int32_t mem, lrs_fact** out) {
+  if (!c || !out || !uT_tips || !vT || !sT || !uW_tips || !vW || !sW) return LRS_ERR_PARAMETER;
+  *out = nullptr;
+  return guard(c, [&] {
+    check_mem(mem);
+    const int w = scalar_w(scalar);
+    if (p < 2 || k < 1 || r < 1 || r > k || r > 96)
+      throw LrsError(LRS_ERR_PARAMETER, "trunc_precond: p >= 2, 1 <= n_svd <= min(k, 96)");
+    LRS_CUDA(cudaSetDevice(c->device));
+    const int64_t cnt = (p - 1) * k * r;
+    DevBuf<double> a, b, d, e, sa, sb;
+    int64_t ld;
+    const void* uTd = dev_in(c, uT_tips, cnt, cnt, 1, mem, a, &ld, w);
+    const void* vTd = dev_in(c, vT, cnt, cnt, 1, mem, b, &ld, w);
+    const void* uWd = dev_in(c, uW_tips, cnt, cnt, 1, mem, d, &ld, w);
+    const void* vWd = dev_in(c, vW, cnt, cnt, 1, mem, e, &ld, w);
+    const double* sTd = static_cast<const double*>(dev_in(c, sT, (p - 1) * r, (p - 1) * r, 1, mem, sa, &ld, 1));
+    const double* sWd = static_cast<const double*>(dev_in(c, sW, (p - 1) * r, (p - 1) * r, 1, mem, sb, &ld, 1));
+    Fact* f = make_trunc_precond(c, scalar, p, k, (int)r, uTd, vTd, sTd, uWd, vWd, sWd);
+    LRS_CUDA(cudaStreamSynchronize(c->stream));
+    *out = static_cast<lrs_fact*>(f);
+    ++c->children;
+  });
+}
+
 lrs_status lrs_bench_dmma_peak(lrs_ctx* c, double* tflops) {
   if (!c || !tflops) return LRS_ERR_PARAMETER;
   return guard(c, [&] { *tflops = run_dmma_peak(c); });

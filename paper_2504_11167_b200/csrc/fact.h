@@ -134,6 +134,10 @@ void solve(Fact* f, Mat* a, const void* b, int64_t ldb, void* x, int64_t ldx, in
 // reduced-system operators on compact ReducedVectors (ld = f->ldr): kind 0
 // matvec_lowrank, 1 matvec_otf, 2 apply_truncated_precond
 void reduced_op(Fact* f, int kind, void* x, void* y, int nrhs);
+// build_truncated_precond from explicit spikes (device arrays; see solver.cu)
+Fact* make_trunc_precond(Ctx* c, int32_t scalar, int64_t p, int64_t k, int r, const void* uTb,
+                         const void* vT, const double* sT, const void* uWt, const void* vW,
+                         const double* sW);
 // BiCGStab / CG / GMRES(m) on caller operators (device buffers, ld = n)
 void krylov_ops(Ctx* c, int64_t n, int32_t scalar, const lrs_operator& A, const lrs_operator* M,
                 const void* b, int64_t ldb, void* x, int64_t ldx, int nrhs,

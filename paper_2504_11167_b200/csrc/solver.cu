@@ -427,6 +427,133 @@ void coupling_spikes(Fact* f, int r, int l, const std::vector<std::pair<int, int
   f->rank_collapsed = hflag != 0;
 }
 
+// Per-interface Woodbury factors (K, E, H^-1, cond_1; Appendix A.1 of
+// SURVEY.md) and the apply-time job tables, from the spikes in f->uT/uW/vtT/vtW/sT/sW.
+// Returns false (without throwing) if an interface is ill-conditioned on ANY rank.
+template <class S>
+bool finish_interfaces(Fact* f, int r, int* bad_iface, double* bad_cond) {
+  Ctx* c = f->ctx;
+  const int Pg = f->Pg, p0 = f->p0, P = f->P;
+  const int64_t n = f->n, k = f->k;
+  constexpr int w = SW<S>;
+  auto goff = [&](int i) { return f->goff[i]; };
+  auto gsize = [&](int i) { return f->goff[i + 1] - f->goff[i]; };
+  (void)n;
+  // interfaces with at least one local side: global i in [iface0, iface0 + ni)
+  f->iface0 = std::max(0, p0 - 1);
+  const int ilast = std::min(Pg - 2, p0 + P - 1);
+  const int ni = std::max(0, ilast - f->iface0 + 1);
+  f->ni = ni;
+  const size_t rr = (size_t)r * r;
+  f->Kd.alloc((size_t)std::max(ni, 1) * rr * w);
+  f->Ed.alloc((size_t)std::max(ni, 1) * rr * w);
+  f->Hinv.alloc((size_t)std::max(ni, 1) * rr * w);
+  f->cond.alloc((size_t)std::max(ni, 1) * 2);
+  f->degen.alloc((size_t)std::max(ni, 1));
+  double mx = 1.0;
+  int bad_i = -1;
+  double bad_c = 0.0;
+  if (ni > 0) {
+    std::vector<IfaceSetupJobT<S>> jobs;
+    for (int q = 0; q < ni; ++q) {
+      const int i = f->iface0 + q;
+      IfaceSetupJobT<S> j{};
+      j.uTb = sp<S>(f->uT) + goff(i) + gsize(i) - k;
+      j.ld_uT = n;
+      j.uWt = sp<S>(f->uW) + goff(i + 1);
+      j.ld_uW = n;
+      j.vtT = sp<S>(f->vtT) + (size_t)i * k * r;
+      j.vtW = sp<S>(f->vtW) + (size_t)(i + 1) * k * r;
+      j.sT = f->sT.get() + (size_t)i * r;
+      j.sW = f->sW.get() + (size_t)(i + 1) * r;
+      j.K = sp<S>(f->Kd) + q * rr;
+      j.E = sp<S>(f->Ed) + q * rr;
+      j.Hinv = sp<S>(f->Hinv) + q * rr;
+      j.cond = f->cond.get() + 2 * q;
+      j.degenerate = f->degen.get() + q;
+      jobs.push_back(j);
+    }
+    DevBuf<IfaceSetupJobT<S>> dj;
+    upload(c, dj, jobs);
+    launch_iface_setup_t<S>(c, dj.get(), ni, r, k);
+    std::vector<double> hc(2 * ni);
+    download(c, hc.data(), f->cond.get(), hc.size());
+    for (int q = 0; q < ni; ++q) {
+      const double ci = std::max(hc[2 * q], hc[2 * q + 1]);
+      if (!(ci <= COND_LIMIT) && bad_i < 0) {
+        bad_i = f->iface0 + q;
+        bad_c = ci;
+      }
+      if (ci <= COND_LIMIT) mx = std::max(mx, ci);
+    }
+  }
+  // every rank takes the same decision (first ill-conditioned interface in global order)
+  {
+    const std::vector<double> all = allgather_host(
+        f, {bad_i >= 0 ? (double)bad_i : -1.0, bad_c, mx, f->rank_collapsed ? 1.0 : 0.0});
+    bad_i = -1;
+    for (size_t q = 0; q < all.size(); q += 4) {
+      if (all[q] >= 0 && (bad_i < 0 || all[q] < bad_i)) {
+        bad_i = (int)all[q];
+        bad_c = all[q + 1];
+      }
+      mx = std::max(mx, all[q + 2]);
+      f->rank_collapsed = f->rank_collapsed || all[q + 3] != 0.0;
+    }
+  }
+  if (bad_i >= 0) {
+    *bad_iface = bad_i;
+    *bad_cond = bad_c;
+    return false;
+  }
+  f->info.max_interface_cond = mx;
+  // apply-time jobs
+  const size_t scn = (size_t)Pg * r * MAX_RHS, msgn = (size_t)std::max(ni, 1) * 2 * r * MAX_RHS;
+  f->scT.alloc(scn * w);
+  f->scW.alloc(scn * w);
+  f->iface_msg.alloc(msgn * w);
+  LRS_CUDA(cudaMemsetAsync(f->scT.get(), 0, sizeof(S) * scn, c->stream));
+  LRS_CUDA(cudaMemsetAsync(f->scW.get(), 0, sizeof(S) * scn, c->stream));
+  LRS_CUDA(cudaMemsetAsync(f->iface_msg.get(), 0, sizeof(S) * msgn, c->stream));
+  f->job_left = f->job_right = -1;
+  {
+    std::vector<IfaceApplyJobT<S>> jobs;
+    for (int q = 0; q < ni; ++q) {
+      const int i = f->iface0 + q;
+      IfaceApplyJobT<S> j{};
+      j.vtT = sp<S>(f->vtT) + (size_t)i * k * r;
+      j.vtW = sp<S>(f->vtW) + (size_t)(i + 1) * k * r;
+      j.sT = f->sT.get() + (size_t)i * r;
+      j.sW = f->sW.get() + (size_t)(i + 1) * r;
+      j.K = sp<S>(f->Kd) + q * rr;
+      j.E = sp<S>(f->Ed) + q * rr;
+      j.Hinv = sp<S>(f->Hinv) + q * rr;
+      j.yb_row = goff(i) + gsize(i) - k;
+      j.yt_row = goff(i + 1);
+      j.scT = sp<S>(f->scT) + (size_t)i * r * MAX_RHS;
+      j.scW = sp<S>(f->scW) + (size_t)(i + 1) * r * MAX_RHS;
+      j.msg = sp<S>(f->iface_msg) + (size_t)q * 2 * r * MAX_RHS;
+      j.has_left = (i >= p0 && i < p0 + P) ? 1 : 0;
+      j.has_right = (i + 1 >= p0 && i + 1 < p0 + P) ? 1 : 0;
+      if (!j.has_left) f->job_left = q;
+      if (!j.has_right) f->job_right = q;
+      jobs.push_back(j);
+    }
+    upload_raw(c, f->iface_jobs, jobs);
+    // the same interfaces addressed in the compact reduced layout (LR-SPIKE-I / OTF):
+    // bottom tip of partition i at row 2ki + k, top tip of partition i+1 at 2k(i+1)
+    for (int q = 0; q < ni; ++q) {
+      const int i = f->iface0 + q;
+      jobs[q].yb_row = 2 * k * i + k;
+      jobs[q].yt_row = 2 * k * (i + 1);
+    }
+    upload_raw(c, f->iface_jobs_red, jobs);
+    f->iface_work.alloc(iface_work_doubles(std::max(ni, 1), r, k) * w);
+  }
+  LRS_CUDA(cudaStreamSynchronize(c->stream));
+  return true;
+}
+
 template <class S>
 bool build_lowrank(Fact* f, int r, int* bad_iface, double* bad_cond, std::vector<double>* pre) {
   Ctx* c = f->ctx;
@@ -656,119 +783,7 @@ bool build_lowrank(Fact* f, int r, int* bad_iface, double* bad_cond, std::vector
     if (iR < Pg - 1)  // W side of partition iR + 1
       unpack(r_next, sp<S>(f->uW), goff(iR + 1), sp<S>(f->vtW), f->sW.get(), iR + 1);
   }
-  // interfaces with at least one local side: global i in [iface0, iface0 + ni)
-  f->iface0 = std::max(0, p0 - 1);
-  const int ilast = std::min(Pg - 2, p0 + P - 1);
-  const int ni = std::max(0, ilast - f->iface0 + 1);
-  f->ni = ni;
-  const size_t rr = (size_t)r * r;
-  f->Kd.alloc((size_t)std::max(ni, 1) * rr * w);
-  f->Ed.alloc((size_t)std::max(ni, 1) * rr * w);
-  f->Hinv.alloc((size_t)std::max(ni, 1) * rr * w);
-  f->cond.alloc((size_t)std::max(ni, 1) * 2);
-  f->degen.alloc((size_t)std::max(ni, 1));
-  double mx = 1.0;
-  int bad_i = -1;
-  double bad_c = 0.0;
-  if (ni > 0) {
-    std::vector<IfaceSetupJobT<S>> jobs;
-    for (int q = 0; q < ni; ++q) {
-      const int i = f->iface0 + q;
-      IfaceSetupJobT<S> j{};
-      j.uTb = sp<S>(f->uT) + goff(i) + gsize(i) - k;
-      j.ld_uT = n;
-      j.uWt = sp<S>(f->uW) + goff(i + 1);
-      j.ld_uW = n;
-      j.vtT = sp<S>(f->vtT) + (size_t)i * k * r;
-      j.vtW = sp<S>(f->vtW) + (size_t)(i + 1) * k * r;
-      j.sT = f->sT.get() + (size_t)i * r;
-      j.sW = f->sW.get() + (size_t)(i + 1) * r;
-      j.K = sp<S>(f->Kd) + q * rr;
-      j.E = sp<S>(f->Ed) + q * rr;
-      j.Hinv = sp<S>(f->Hinv) + q * rr;
-      j.cond = f->cond.get() + 2 * q;
-      j.degenerate = f->degen.get() + q;
-      jobs.push_back(j);
-    }
-    DevBuf<IfaceSetupJobT<S>> dj;
-    upload(c, dj, jobs);
-    launch_iface_setup_t<S>(c, dj.get(), ni, r, k);
-    std::vector<double> hc(2 * ni);
-    download(c, hc.data(), f->cond.get(), hc.size());
-    for (int q = 0; q < ni; ++q) {
-      const double ci = std::max(hc[2 * q], hc[2 * q + 1]);
-      if (!(ci <= COND_LIMIT) && bad_i < 0) {
-        bad_i = f->iface0 + q;
-        bad_c = ci;
-      }
-      if (ci <= COND_LIMIT) mx = std::max(mx, ci);
-    }
-  }
-  // every rank takes the same decision (first ill-conditioned interface in global order)
-  {
-    const std::vector<double> all = allgather_host(
-        f, {bad_i >= 0 ? (double)bad_i : -1.0, bad_c, mx, f->rank_collapsed ? 1.0 : 0.0});
-    bad_i = -1;
-    for (size_t q = 0; q < all.size(); q += 4) {
-      if (all[q] >= 0 && (bad_i < 0 || all[q] < bad_i)) {
-        bad_i = (int)all[q];
-        bad_c = all[q + 1];
-      }
-      mx = std::max(mx, all[q + 2]);
-      f->rank_collapsed = f->rank_collapsed || all[q + 3] != 0.0;
-    }
-  }
-  if (bad_i >= 0) {
-    *bad_iface = bad_i;
-    *bad_cond = bad_c;
-    return false;
-  }
-  f->info.max_interface_cond = mx;
-  // apply-time jobs
-  const size_t scn = (size_t)Pg * r * MAX_RHS, msgn = (size_t)std::max(ni, 1) * 2 * r * MAX_RHS;
-  f->scT.alloc(scn * w);
-  f->scW.alloc(scn * w);
-  f->iface_msg.alloc(msgn * w);
-  LRS_CUDA(cudaMemsetAsync(f->scT.get(), 0, sizeof(S) * scn, c->stream));
-  LRS_CUDA(cudaMemsetAsync(f->scW.get(), 0, sizeof(S) * scn, c->stream));
-  LRS_CUDA(cudaMemsetAsync(f->iface_msg.get(), 0, sizeof(S) * msgn, c->stream));
-  f->job_left = f->job_right = -1;
-  {
-    std::vector<IfaceApplyJobT<S>> jobs;
-    for (int q = 0; q < ni; ++q) {
-      const int i = f->iface0 + q;
-      IfaceApplyJobT<S> j{};
-      j.vtT = sp<S>(f->vtT) + (size_t)i * k * r;
-      j.vtW = sp<S>(f->vtW) + (size_t)(i + 1) * k * r;
-      j.sT = f->sT.get() + (size_t)i * r;
-      j.sW = f->sW.get() + (size_t)(i + 1) * r;
-      j.K = sp<S>(f->Kd) + q * rr;
-      j.E = sp<S>(f->Ed) + q * rr;
-      j.Hinv = sp<S>(f->Hinv) + q * rr;
-      j.yb_row = goff(i) + gsize(i) - k;
-      j.yt_row = goff(i + 1);
-      j.scT = sp<S>(f->scT) + (size_t)i * r * MAX_RHS;
-      j.scW = sp<S>(f->scW) + (size_t)(i + 1) * r * MAX_RHS;
-      j.msg = sp<S>(f->iface_msg) + (size_t)q * 2 * r * MAX_RHS;
-      j.has_left = (i >= p0 && i < p0 + P) ? 1 : 0;
-      j.has_right = (i + 1 >= p0 && i + 1 < p0 + P) ? 1 : 0;
-      if (!j.has_left) f->job_left = q;
-      if (!j.has_right) f->job_right = q;
-      jobs.push_back(j);
-    }
-    upload_raw(c, f->iface_jobs, jobs);
-    // the same interfaces addressed in the compact reduced layout (LR-SPIKE-I / OTF):
-    // bottom tip of partition i at row 2ki + k, top tip of partition i+1 at 2k(i+1)
-    for (int q = 0; q < ni; ++q) {
-      const int i = f->iface0 + q;
-      jobs[q].yb_row = 2 * k * i + k;
-      jobs[q].yt_row = 2 * k * (i + 1);
-    }
-    upload_raw(c, f->iface_jobs_red, jobs);
-    f->iface_work.alloc(iface_work_doubles(std::max(ni, 1), r, k) * w);
-  }
-  LRS_CUDA(cudaStreamSynchronize(c->stream));
-  return true;
+  return finish_interfaces<S>(f, r, bad_iface, bad_cond);
 }
 
 }  // namespace
@@ -2210,6 +2225,103 @@ void reduced_op_t(Fact* f, int kind, S* x, S* y, int nrhs) {
       trunc_precond_t(f, xc, yc, nr);
     }
   }
+}
+
+// build_truncated_precond from explicit spikes: a factorization handle
+// with no band factors whose "n-layout" is the compact reduced layout (partition i owns
+// rows [2ki, 2k(i+1)): top tip, then bottom tip), so the interface setup and the
+// reduced-system operators (apply_truncated_precond, matvec_lowrank) run unchanged.
+// Spike arrays are device pointers: uTb[i] (k x r, bottom tip of u_{T_i}, i < p-1),
+// vT[i] (r x k), sT[i] (r); uWt[i] (k x r, top tip of u_{W_{i+1}}), vW[i], sW[i].
+template <class S>
+Fact* trunc_precond_t(Ctx* c, int64_t p, int64_t k, int r, const S* uTb, const S* vT,
+                      const double* sT, const S* uWt, const S* vW, const double* sW) {
+  std::unique_ptr<Fact> f(new Fact());
+  constexpr int w = SW<S>;
+  f->ctx = c;
+  f->scalar = IsC<S>::value ? LRS_C128 : LRS_F64;
+  f->sw = w;
+  f->variant = LRS_VARIANT_T;
+  f->P = f->Pg = (int)p;
+  f->p0 = 0;
+  f->k = k;
+  f->n = 2 * k * p;
+  f->ldr = f->n;
+  f->row_lo = 0;
+  f->row_hi = f->n;
+  f->r = r;
+  f->l = r;
+  for (int64_t i = 0; i <= p; ++i) f->goff.push_back(2 * k * i);
+  for (int64_t i = 0; i < p; ++i) {
+    f->off.push_back(2 * k * i);
+    f->size.push_back(2 * k);
+    f->T.push_back(0);
+    f->tbase.push_back(0);
+    f->fbase.push_back(0);
+  }
+  upload(c, f->d_off, f->off);
+  upload(c, f->d_size, f->size);
+  upload(c, f->d_T, f->T);
+  upload(c, f->d_goff, f->goff);
+  upload(c, f->d_tbase, f->tbase);
+  upload(c, f->d_fbase, f->fbase);
+  const int64_t n = f->n, kr = k * r;
+  f->uT.alloc((size_t)n * r * w);
+  f->uW.alloc((size_t)n * r * w);
+  f->vtT.alloc((size_t)p * kr * w);
+  f->vtW.alloc((size_t)p * kr * w);
+  f->sT.alloc((size_t)p * r);
+  f->sW.alloc((size_t)p * r);
+  for (DevBuf<double>* b : {&f->uT, &f->uW, &f->vtT, &f->vtW, &f->sT, &f->sW})
+    LRS_CUDA(cudaMemsetAsync(b->get(), 0, b->bytes, c->stream));
+  const size_t es = sizeof(S);
+  for (int64_t i = 0; i + 1 < p; ++i) {
+    // u tips into the compact rows; v (r x k) transposed into v^T (k x r) by a 2D copy
+    LRS_CUDA(cudaMemcpy2DAsync(sp<S>(f->uT) + 2 * k * i + k, es * n, uTb + i * kr, es * k, es * k,
+                               r, cudaMemcpyDeviceToDevice, c->stream));
+    LRS_CUDA(cudaMemcpy2DAsync(sp<S>(f->uW) + 2 * k * (i + 1), es * n, uWt + i * kr, es * k,
+                               es * k, r, cudaMemcpyDeviceToDevice, c->stream));
+    for (int a = 0; a < r; ++a) {  // row a of v -> column a of v^T
+      LRS_CUDA(cudaMemcpy2DAsync(sp<S>(f->vtT) + i * kr + (int64_t)a * k, es, vT + i * kr + a,
+                                 es * r, es, k, cudaMemcpyDeviceToDevice, c->stream));
+      LRS_CUDA(cudaMemcpy2DAsync(sp<S>(f->vtW) + (i + 1) * kr + (int64_t)a * k, es,
+                                 vW + i * kr + a, es * r, es, k, cudaMemcpyDeviceToDevice,
+                                 c->stream));
+    }
+    LRS_CUDA(cudaMemcpyAsync(f->sT.get() + i * r, sT + i * r, sizeof(double) * r,
+                             cudaMemcpyDeviceToDevice, c->stream));
+    LRS_CUDA(cudaMemcpyAsync(f->sW.get() + (i + 1) * r, sW + i * r, sizeof(double) * r,
+                             cudaMemcpyDeviceToDevice, c->stream));
+  }
+  int bad_i = -1;
+  double bad_c = 0.0;
+  if (!finish_interfaces<S>(f.get(), r, &bad_i, &bad_c)) {
+    LrsError e(LRS_ERR_ILL_CONDITIONED_INTERFACE,
+               "interface " + std::to_string(bad_i) + " is ill-conditioned (cond_1 = " +
+                   std::to_string(bad_c) + ")");
+    e.iface = bad_i;
+    e.cond = bad_c;
+    throw e;
+  }
+  f->info.n = f->n;
+  f->info.p = p;
+  f->info.k = k;
+  f->info.n_svd = r;
+  f->info.l = r;
+  f->info.variant = LRS_VARIANT_T;
+  return f.release();
+}
+
+Fact* make_trunc_precond(Ctx* c, int32_t scalar, int64_t p, int64_t k, int r, const void* uTb,
+                         const void* vT, const double* sT, const void* uWt, const void* vW,
+                         const double* sW) {
+  if (scalar == LRS_C128)
+    return trunc_precond_t<zc>(c, p, k, r, static_cast<const zc*>(uTb), static_cast<const zc*>(vT),
+                               sT, static_cast<const zc*>(uWt), static_cast<const zc*>(vW), sW);
+  return trunc_precond_t<double>(c, p, k, r, static_cast<const double*>(uTb),
+                                 static_cast<const double*>(vT), sT,
+                                 static_cast<const double*>(uWt), static_cast<const double*>(vW),
+                                 sW);
 }
 
 void reduced_op(Fact* f, int kind, void* x, void* y, int nrhs) {

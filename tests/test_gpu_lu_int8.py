@@ -215,12 +215,17 @@ def test_int8_componentwise_backward_error(ctx, name, scale):
     """|A_i - L U| for the INT8-sliced factors on the c3 (10^4 coefficient contrast) and c4
     (random band) structures, beside the FP64 DMMA factors and LAPACK dgbtrf.
 
-    Measured: the INT8 update is FP64-accurate relative to the row x
-    column scale (`scaled` <= 64 u, as the DMMA factors), but NOT componentwise: an entry
-    2^-e below its row x column scale keeps ~54 - e bits, so the componentwise error grows
-    as 2^-54 / (|L||U|_ij / scale) -- up to ~3e-8 on c4 -- where the DMMA and LAPACK factors
-    stay at a few u.  Bars: scaled <= 64 u for all three; componentwise <= 256 u for DMMA and
-    LAPACK; componentwise <= 2^-54 2^40 64 for INT8 (the digit-split bound at the 2^-40 floor)."""
+    Measured on the B200 (profiles/r02_lu_componentwise.jsonl):
+      scaled (|A - LU|_ij / (max|L_i.| max|U_.j|)): INT8 8.8e-16 - 9.7e-16, DMMA the same,
+        LAPACK 5e-16 - 1.2e-15 -- the INT8 update is FP64-accurate relative to the row x
+        column scale;
+      componentwise (/ (|L||U|)_ij): LAPACK <= 1.5e-15; DMMA <= 2.1e-12 (its panels form
+        L = A inv(U) with the explicit diagonal-tile inverses); INT8 by band of
+        (|L||U|)_ij / scale: <= 8e-14 in [2^-10, 1], 6.5e-11 in [2^-20, 2^-10), 4.9e-8 in
+        [2^-30, 2^-20), 1.7e-5 in [2^-40, 2^-30) -- an entry 2^-e below its row x column
+        scale keeps ~54 - e bits: normwise FP64, not componentwise.
+    Bars: scaled <= 32 u for all three; LAPACK componentwise <= 32 u; DMMA <= 1e-11; INT8 per
+    band <= 64 2^-54 / (band floor), the digit-split bound."""
     rep = componentwise_report(ctx, name, scale)
     print(rep)
     u = rep["u"]
@@ -228,7 +233,9 @@ def test_int8_componentwise_backward_error(ctx, name, scale):
         if not key.startswith("partition"):
             continue
         for tag in ("int8", "dmma", "lapack"):
-            assert e[tag]["scaled"] <= 64 * u, (tag, rep)
-        for tag in ("dmma", "lapack"):
-            assert e[tag]["cw"] <= 256 * u, (tag, rep)
-        assert e["int8"]["cw"] <= 2.0 ** -54 * 2.0 ** 40 * 64, rep
+            assert e[tag]["scaled"] <= 32 * u, (tag, rep)
+        assert e["lapack"]["cw"] <= 32 * u, rep
+        assert e["dmma"]["cw"] <= 1e-11, rep
+        for tag, floor in (("b0", -10), ("b10", -20), ("b20", -30), ("b30", -40)):
+            if e["int8"][tag] is not None:
+                assert e["int8"][tag] <= 64 * 2.0 ** -54 / 2.0 ** floor, (tag, rep)
