@@ -37,7 +37,7 @@ build/%.o: $(PKG)/csrc/%.cu $(CU_HDR)
 	$(NVCC) $(NVFLAGS) -c -o $@ $< 2> build/$*.ptxas.log || (cat build/$*.ptxas.log; false)
 
 $(PKG)/liblrspike_cuda.so: $(CU_OBJ)
-	$(NVCC) $(ARCH) -shared -Xcompiler -fPIC -o $@ $(CU_OBJ) -lcudart
+	$(NVCC) $(ARCH) -shared -Xcompiler -fPIC -o $@ $(CU_OBJ) -lcudart -ldl
 
 $(PKG)/liblrspike.so: $(HOST_SRC) $(API_HDR) $(PKG)/liblrspike_cuda.so
 	$(CXX) $(CXXFLAGS) -shared -o $@ $(HOST_SRC) -L$(PKG) -llrspike_cuda \
@@ -59,6 +59,6 @@ build/var_$(V)/%.o: $(PKG)/csrc/%.cu $(CU_HDR)
 	@mkdir -p build/var_$(V)
 	$(NVCC) $(NVFLAGS) $(DEFS) -c -o $@ $< 2> build/var_$(V)/$*.ptxas.log || (cat build/var_$(V)/$*.ptxas.log; false)
 build/var_$(V)/liblrspike_cuda.so: $(VOBJ)
-	$(NVCC) $(ARCH) -shared -Xcompiler -fPIC -o $@ $(VOBJ) -lcudart
+	$(NVCC) $(ARCH) -shared -Xcompiler -fPIC -o $@ $(VOBJ) -lcudart -ldl
 variant: build/var_$(V)/liblrspike_cuda.so
 .PHONY: variant

@@ -353,15 +353,17 @@ def run_ours(args):
     if ws > 1:
         import torch.distributed as dist
 
-        from paper_2504_11167_b200.dist import TorchComm
-
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        comm = TorchComm(device_buffers=True)
     # a dedicated stream shared by torch and the library: the CUDA events of the timed
     # region are recorded on the stream every kernel of the step is launched on
     stream = torch.cuda.Stream(device=local)
     torch.cuda.set_stream(stream)
     ctx = api.Context(local, stream.cuda_stream)
+    if ws > 1:
+        # the in-library NCCL data plane: exchanges enqueued on the context stream
+        from paper_2504_11167_b200.dist import LibNcclComm
+
+        comm = LibNcclComm(ctx)
     assert ctx.stream == stream.cuda_stream != 0
     P = args.P if args.P is not None else DEFAULT_P.get(args.config)
     cfg = configs.make_config(args.config, args.scale, P)
@@ -555,6 +557,9 @@ def run_ours(args):
         "residual_final": reps[-1].residual_final,
         "t_factorize_s": info["t_factorize"], "t_lu_s": info["t_lu"], "t_spikes_s": info["t_spikes"],
         "t_solve_s": reps[-1].wall_time,
+        # host round trips of the solve: transport calls, stream syncs forced before them
+        # (0: the in-library NCCL plane is stream-ordered), syncs to read Krylov scalars
+        "round_trips": reps[-1].round_trips,
         # the band LU's bulk update ran INT8-sliced on tcgen05 (lu_int8 = 1) or DMMA;
         # t_lu_dmma_s = the same LU with LRS_LU_I8=0 (one extra untimed factorization)
         "lu_int8": int(info.get("lu_int8", 0)), "t_lu_dmma_s": t_lu_dmma,

@@ -144,6 +144,10 @@ typedef struct lrs_report {
   int64_t history_total;
   double inner_iterations;      /* LR-SPIKE-I: inner half-iterations summed over the applies */
   int64_t inner_solves;         /* LR-SPIKE-I: inner solves (one per applied column batch) */
+  /* host round trips of this solve: calls into the transport (lrs_comm), stream
+     synchronizations a host-callback transport forced before them (0 with the in-library
+     NCCL plane), and synchronizations to read the Krylov scalars */
+  int64_t comm_calls, comm_host_syncs, scalar_syncs;
 } lrs_report;
 
 /* Read-only facts about a factorization. */
@@ -310,7 +314,23 @@ typedef struct lrs_comm {
   int32_t (*allgather)(void* user, const double* send, double* recv, int64_t count);
   int32_t (*sendrecv)(void* user, const double* send, int64_t scount, int32_t dest, double* recv,
                       int64_t rcount, int32_t source);
+  /* optional: both neighbour directions in one call (to_next -> rank+1 into its from_prev,
+   * to_prev -> rank-1 into its from_next; NULL pointers where there is no neighbour) */
+  int32_t (*neighbors)(void* user, const double* to_next, double* from_prev,
+                       const double* to_prev, double* from_next, int64_t count);
+  /* 1: the callbacks enqueue their transfers on the context's stream in stream order (the
+   * in-library NCCL plane); the library then does not synchronize before calling them */
+  int32_t stream_ordered;
 } lrs_comm;
+
+/* The in-library NCCL data plane (libnccl.so.2 loaded on first use): an lrs_comm whose
+ * callbacks are grouped ncclSend / ncclRecv (both neighbour directions in one group) and
+ * ncclAllGather on the context stream (stream_ordered = 1).  id: the 128-byte
+ * ncclUniqueId from lrs_comm_nccl_unique_id on rank 0, shared by the launcher. */
+LRS_API lrs_status lrs_comm_nccl_unique_id(void* id128);
+LRS_API lrs_status lrs_comm_nccl_create(lrs_ctx* ctx, const void* id128, int32_t rank,
+                                        int32_t size, lrs_comm** out);
+LRS_API void lrs_comm_nccl_destroy(lrs_comm* comm);
 
 /* Partitions [*p_lo, *p_hi) and rows [*row_lo, *row_hi) owned by `rank` (host only). */
 LRS_API lrs_status lrs_shard_plan(int64_t n, int64_t p, int32_t size, int32_t rank, int64_t* p_lo,

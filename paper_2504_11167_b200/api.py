@@ -61,7 +61,8 @@ class ReportC(ctypes.Structure):
                 ("comm_messages", i64 * 3), ("comm_scalars", i64 * 3), ("t_solve", f64),
                 ("seed", u64), ("history", ctypes.POINTER(f64)), ("history_cap", i64),
                 ("history_len", i64), ("history_total", i64), ("inner_iterations", f64),
-                ("inner_solves", i64)]
+                ("inner_solves", i64), ("comm_calls", i64), ("comm_host_syncs", i64),
+                ("scalar_syncs", i64)]
 
 
 class FactInfoC(ctypes.Structure):
@@ -203,6 +204,11 @@ def lib():
         "lrs_bench_i8_peak": (i32, [vp, P(f64)]),
         "lrs_krylov": (i32, [vp, i64, i32, P(OperatorC), P(OperatorC), vp, i64, vp, i64, i64,
                              P(IterCfgC), P(ReportC), i32]),
+        "lrs_trunc_precond_create": (i32, [vp, i32, i64, i64, i64, vp, vp, vp, vp, vp, vp, i32,
+                                           P(vp)]),
+        "lrs_dense_qr": (i32, [vp, i32, i64, i64, vp, i64, vp, i32]),
+        "lrs_dense_svd": (i32, [vp, i32, i64, vp, vp, vp, vp, i32]),
+        "lrs_dense_gemm": (i32, [vp, i32, i64, i64, i64, vp, i64, vp, i64, vp, i64, i32, i32]),
         "lrs_ctx_set_profiling": (i32, [vp, i32]),
         "lrs_ctx_kernel_times": (i32, [vp, vp, vp, i32]),
     }
@@ -487,6 +493,9 @@ class SolveReport:
     breakdown: bool
     inner_iterations: float = 0.0  # LR-SPIKE-I inner half-iterations (summed)
     inner_solves: int = 0
+    # host round trips of the solve (lrs_report): transport calls, stream syncs forced by a
+    # host-callback transport, syncs to read Krylov scalars
+    round_trips: dict = None
 
 
 class SpikeFactorization:
@@ -613,6 +622,62 @@ class SpikeFactorization:
         return {STAGES[i]: (m[i], s[i]) for i in range(3)}
 
 
+class TruncatedPrecond:
+    """build_truncated_precond from explicit spikes, on the device.
+
+    spikes_T[i] = (u, sigma, v) of T_i (i = 0..p-2), spikes_W[i] = those of W_{i+1}; only
+    the k-row tips of u are used.  apply(g) = apply_truncated_precond and
+    matvec_lowrank(x) on ReducedVector blocks (2 k p x n_rhs, partition
+    i's top tip in rows [2ki, 2ki + k), its bottom tip in [2ki + k, 2k(i+1))).
+    IllConditionedInterfaceError(interface, cond_1) above cond_1 = 1e12."""
+
+    def __init__(self, ctx: Context, spikes_T, spikes_W, k: int):
+        self.ctx, self.k = ctx, int(k)
+        self.p = len(spikes_T) + 1
+        r = len(spikes_T[0][1])
+        cplx = any(np.iscomplexobj(s[0]) or np.iscomplexobj(s[2]) for s in spikes_T + spikes_W)
+        self.dtype = np.dtype(np.complex128 if cplx else np.float64)
+        cat = lambda blocks: np.ascontiguousarray(  # noqa: E731
+            np.concatenate([np.asarray(b, dtype=self.dtype).ravel(order="F") for b in blocks]))
+        uT = cat([u[-self.k:] for u, _, _ in spikes_T])
+        uW = cat([u[:self.k] for u, _, _ in spikes_W])
+        vT = cat([v for _, _, v in spikes_T])
+        vW = cat([v for _, _, v in spikes_W])
+        sT = np.ascontiguousarray(np.concatenate([np.asarray(s, float) for _, s, _ in spikes_T]))
+        sW = np.ascontiguousarray(np.concatenate([np.asarray(s, float) for _, s, _ in spikes_W]))
+        h = vp()
+        _check(lib().lrs_trunc_precond_create(ctx.h, C128 if cplx else F64, self.p, self.k, r,
+                                              uT.ctypes.data, vT.ctypes.data, sT.ctypes.data,
+                                              uW.ctypes.data, vW.ctypes.data, sW.ctypes.data,
+                                              MEM_HOST, ctypes.byref(h)), ctx.h)
+        self.h, self.n_svd = h, r
+
+    def __del__(self):
+        try:
+            if self.h:
+                lib().lrs_fact_destroy(self.h)
+            self.h = None
+        except Exception:
+            pass
+
+    def _op(self, kind, x):
+        X = np.asfortranarray(np.asarray(x, dtype=self.dtype).reshape(2 * self.k * self.p, -1))
+        Y = np.empty_like(X, order="F")
+        _check(lib().lrs_reduced_apply(self.h, kind, X.ctypes.data, X.shape[0], Y.ctypes.data,
+                                       Y.shape[0], X.shape[1], MEM_HOST), self.ctx.h)
+        return Y
+
+    def apply(self, g):
+        return self._op(2, g)
+
+    def matvec_lowrank(self, x):
+        return self._op(0, x)
+
+
+def build_truncated_precond(ctx: Context, spikes_T, spikes_W, k: int) -> TruncatedPrecond:
+    return TruncatedPrecond(ctx, spikes_T, spikes_W, k)
+
+
 def factorize(ctx: Context, A: CsrMatrix, cfg: SolverConfig) -> SpikeFactorization:
     return SpikeFactorization(ctx, A, cfg)
 
@@ -653,7 +718,9 @@ def solve(A: CsrMatrix, f, cfg: SolverConfig | None = None, it: IterConfig | Non
                          rep.precond_applications, rep.matvecs, rep.residual_final,
                          {STAGES[i]: (rep.comm_messages[i], rep.comm_scalars[i]) for i in range(3)},
                          rep.seed, rep.t_solve, bool(rep.breakdown), rep.inner_iterations,
-                         rep.inner_solves)
+                         rep.inner_solves, {"comm_calls": rep.comm_calls,
+                                            "comm_host_syncs": rep.comm_host_syncs,
+                                            "scalar_syncs": rep.scalar_syncs})
     if st == 10:
         info = ErrorInfoC()
         lib().lrs_last_error(A.ctx.h, ctypes.byref(info))

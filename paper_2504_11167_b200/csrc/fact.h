@@ -84,6 +84,9 @@ struct Fact {
   // multi-GPU
   bool dist = false;
   lrs_comm comm{};
+  // host round trips: transport calls, stream synchronizations forced by a host-callback
+  // transport before them, and synchronizations to read Krylov scalars (dot products)
+  int64_t comm_calls = 0, comm_syncs = 0, scalar_syncs = 0;
   DevBuf<double> xch;          // staging for neighbour exchanges
   // ledger, info
   int64_t ledger_msgs[3] = {0, 0, 0}, ledger_sc[3] = {0, 0, 0};

@@ -85,14 +85,29 @@ void comm_rc(int32_t rc, const char* what) {
   if (rc != 0) throw LrsError(LRS_ERR_NCCL, std::string("communication callback failed: ") + what);
 }
 
-// Two-phase neighbour exchange of `count` doubles: to_next -> rank+1 (received there in
-// from_prev), then to_prev -> rank-1 (received in from_next).
+// Neighbour exchange of `count` doubles: to_next -> rank+1 (received there in from_prev)
+// and to_prev -> rank-1 (received in from_next).  A stream-ordered transport (the
+// in-library NCCL plane) enqueues both directions as one group on the context stream, so
+// no host synchronization happens here; a host-callback transport gets a drained stream.
 void neighbor_exchange(Fact* f, const void* to_next, void* from_prev, const void* to_prev,
                        void* from_next, int64_t count) {
   if (!f->dist || count == 0) return;
-  LRS_CUDA(cudaStreamSynchronize(f->ctx->stream));
+  if (!f->comm.stream_ordered) {
+    LRS_CUDA(cudaStreamSynchronize(f->ctx->stream));
+    ++f->comm_syncs;
+  }
   const int r = f->comm.rank, G = f->comm.size;
   const int next = r + 1 < G ? r + 1 : -1, prev = r > 0 ? r - 1 : -1;
+  if (f->comm.neighbors) {
+    ++f->comm_calls;
+    comm_rc(f->comm.neighbors(f->comm.user, next >= 0 ? static_cast<const double*>(to_next) : nullptr,
+                              prev >= 0 ? static_cast<double*>(from_prev) : nullptr,
+                              prev >= 0 ? static_cast<const double*>(to_prev) : nullptr,
+                              next >= 0 ? static_cast<double*>(from_next) : nullptr, count),
+            "neighbors");
+    return;
+  }
+  f->comm_calls += 2;
   comm_rc(f->comm.sendrecv(f->comm.user, static_cast<const double*>(to_next),
                            next >= 0 ? count : 0, next, static_cast<double*>(from_prev),
                            prev >= 0 ? count : 0, prev),
@@ -103,18 +118,27 @@ void neighbor_exchange(Fact* f, const void* to_next, void* from_prev, const void
           "sendrecv");
 }
 
-// All-gather of a small host vector (every rank contributes v.size() doubles).
+// All-gather of a small host vector (every rank contributes v.size() doubles): setup
+// decisions every rank must take identically.
 std::vector<double> allgather_host(Fact* f, const std::vector<double>& v) {
   if (!f->dist) return v;
   const int G = f->comm.size;
+  Ctx* c = f->ctx;
   DevBuf<double> d;
   d.alloc(v.size() * (G + 1));
-  LRS_CUDA(cudaMemcpy(d.get(), v.data(), sizeof(double) * v.size(), cudaMemcpyHostToDevice));
+  std::vector<double> out(v.size() * G);
+  LRS_CUDA(cudaMemcpyAsync(d.get(), v.data(), sizeof(double) * v.size(), cudaMemcpyHostToDevice,
+                           c->stream));
+  if (!f->comm.stream_ordered) {
+    LRS_CUDA(cudaStreamSynchronize(c->stream));
+    ++f->comm_syncs;
+  }
+  ++f->comm_calls;
   comm_rc(f->comm.allgather(f->comm.user, d.get(), d.get() + v.size(), (int64_t)v.size()),
           "allgather");
-  std::vector<double> out(v.size() * G);
-  LRS_CUDA(cudaMemcpy(out.data(), d.get() + v.size(), sizeof(double) * out.size(),
-                      cudaMemcpyDeviceToHost));
+  LRS_CUDA(cudaMemcpyAsync(out.data(), d.get() + v.size(), sizeof(double) * out.size(),
+                           cudaMemcpyDeviceToHost, c->stream));
+  LRS_CUDA(cudaStreamSynchronize(c->stream));
   return out;
 }
 
@@ -182,9 +206,10 @@ void dstage_t(Fact* f, S* x, int64_t ld, int nrhs, bool adjoint, int p_only) {
   }
 }
 
-// C1 across the GPU boundaries: m_W (computed left) goes right, m_T goes left
+// C1 across the GPU boundaries: m_W (computed left) goes right, m_T goes left; the
+// messages of nr columns are the first r * nr scalars of their r x MAX_RHS slots
 template <class S>
-void exchange_msgs(Fact* f) {
+void exchange_msgs(Fact* f, int nr) {
   if (!f->dist) return;
   const int64_t blk = (int64_t)f->r * MAX_RHS;
   S* mbase = sp<S>(f->iface_msg);
@@ -192,7 +217,7 @@ void exchange_msgs(Fact* f) {
   S* from_prev = f->job_left >= 0 ? mbase + (2 * f->job_left + 0) * blk : mbase;
   const S* to_prev = f->job_left >= 0 ? mbase + (2 * f->job_left + 1) * blk : mbase;
   S* from_next = f->job_right >= 0 ? mbase + (2 * f->job_right + 1) * blk : mbase;
-  neighbor_exchange(f, to_next, from_prev, to_prev, from_next, blk * SW<S>);
+  neighbor_exchange(f, to_next, from_prev, to_prev, from_next, (int64_t)f->r * nr * SW<S>);
 }
 
 // `per_iface` messages of `scalars` each for every interface this GPU owns (the GPU of
@@ -220,7 +245,7 @@ void apply_precond_t(Fact* f, const S* in, int64_t ldi, S* out, int64_t ldo, int
     const int nr = std::min(MAX_RHS, nrhs - c0);
     S* xc = out + (int64_t)c0 * ldo;
     launch_iface_messages_t<S>(c, jobs, f->ni, r, f->k, xc, ldo, nr, sp<S>(f->iface_work));
-    exchange_msgs<S>(f);
+    exchange_msgs<S>(f, nr);
     launch_iface_solve_t<S>(c, jobs, f->ni, r, nr);
     launch_recovery_t<S>(c, f->geom(), f->n, f->row_lo, f->row_hi, xc, ldo, xc, ldo, nr,
                          sp<S>(f->uT), sp<S>(f->uW), r, sp<S>(f->scT), sp<S>(f->scW));
@@ -1192,7 +1217,11 @@ struct Work {
     launch_multidot_partition_t<S>(c(), ch, X, n, strideX, nvec, Y, n, nr,
                                    sp<S>(f->partial), sp<S>(f->persum));
     if (f->dist) {
-      LRS_CUDA(cudaStreamSynchronize(c()->stream));
+      if (!f->comm.stream_ordered) {
+        LRS_CUDA(cudaStreamSynchronize(c()->stream));
+        ++f->comm_syncs;
+      }
+      ++f->comm_calls;
       comm_rc(f->comm.allgather(f->comm.user, f->persum.get(), f->gather.get(),
                                 (int64_t)f->pl_max * nout),
               "allgather");
@@ -1205,6 +1234,7 @@ struct Work {
     LRS_CUDA(cudaMemcpyAsync(hbuf, f->dotout.get(), sizeof(double) * nout, cudaMemcpyDeviceToHost,
                              c()->stream));
     LRS_CUDA(cudaStreamSynchronize(c()->stream));
+    ++f->scalar_syncs;
     std::memcpy(static_cast<void*>(out), hbuf, sizeof(double) * nout);
   }
   void norms(const S* X, double* out) {
@@ -1672,7 +1702,7 @@ template <class S>
 void reduced_messages(Fact* f, const S* xr, int nr) {
   launch_iface_messages_t<S>(f->ctx, red_jobs<S>(f), f->ni, f->r, f->k, xr, f->ldr, nr,
                              sp<S>(f->iface_work));
-  exchange_msgs<S>(f);
+  exchange_msgs<S>(f, nr);
 }
 
 // matvec_lowrank: y = x + W~ x_{i-1,b} + T~ x_{i+1,t}
@@ -1969,6 +1999,7 @@ void solve_t(Fact* f, Mat* a, const S* b, int64_t ldb, S* x, int64_t ldx, int nr
   R.history_cap = cap;
   R.seed = f->seed;
   R.converged = 1;
+  const int64_t calls0 = f->comm_calls, csync0 = f->comm_syncs, ssync0 = f->scalar_syncs;
   const double inner0 = f->inner_iterations;
   const int64_t solves0 = f->inner_solves;
   LRS_CUDA(cudaEventRecord(c->ev0, c->stream));
@@ -2042,6 +2073,9 @@ void solve_t(Fact* f, Mat* a, const S* b, int64_t ldb, S* x, int64_t ldx, int nr
   LRS_CUDA(cudaEventSynchronize(c->ev1));
   R.t_solve = elapsed_ms(c->ev0, c->ev1) * 1e-3;
   R.residual_final = worst;
+  R.comm_calls = f->comm_calls - calls0;
+  R.comm_host_syncs = f->comm_syncs - csync0;
+  R.scalar_syncs = f->scalar_syncs - ssync0;
   R.breakdown = any_brk ? 1 : 0;
   R.inner_iterations = f->inner_iterations - inner0;
   R.inner_solves = f->inner_solves - solves0;

@@ -29,9 +29,16 @@ _SENDRECV = ctypes.CFUNCTYPE(ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p, c
                              ctypes.c_int32, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32)
 
 
+_NEIGHBORS = ctypes.CFUNCTYPE(ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                              ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64)
+
+
 class CommC(ctypes.Structure):
+    """lrs_comm (include/lrspike_capi.h); host callbacks: neighbors NULL, stream_ordered 0."""
+
     _fields_ = [("rank", ctypes.c_int32), ("size", ctypes.c_int32), ("user", ctypes.c_void_p),
-                ("allgather", _ALLGATHER), ("sendrecv", _SENDRECV)]
+                ("allgather", _ALLGATHER), ("sendrecv", _SENDRECV), ("neighbors", _NEIGHBORS),
+                ("stream_ordered", ctypes.c_int32)]
 
 
 class _DevArray:
@@ -60,7 +67,10 @@ class TorchComm:
     ``device_buffers``: the library hands device pointers (True, the GPU library) or host
     pointers (False, CPU tests of the exchange semantics)."""
 
-    def __init__(self, group=None, device_buffers: bool = True):
+    def __init__(self, group=None, device_buffers: bool = True, stream_ordered: bool = False):
+        """stream_ordered (NCCL on device buffers only): the library's context stream is
+        torch's current stream, so a collective enqueued by torch is ordered with the
+        library's kernels without a host synchronization on either side."""
         import torch
         import torch.distributed as dist
 
@@ -69,9 +79,11 @@ class TorchComm:
         self.size = dist.get_world_size(group)
         self.nccl = dist.get_backend(group) == "nccl"
         self.device_buffers = device_buffers
+        self.stream_ordered = bool(stream_ordered and self.nccl and device_buffers)
         self._ag = _ALLGATHER(self._allgather)
         self._sr = _SENDRECV(self._sendrecv)
-        self.c = CommC(self.rank, self.size, None, self._ag, self._sr)
+        self.c = CommC(self.rank, self.size, None, self._ag, self._sr, _NEIGHBORS(),
+                       1 if self.stream_ordered else 0)
         self.calls = {"allgather": 0, "sendrecv": 0, "bytes": 0}
 
     # -- buffer views ---------------------------------------------------------------------
@@ -101,7 +113,7 @@ class TorchComm:
             if self.device_buffers and not self.nccl:
                 r = self.torch.empty(count * self.size, dtype=self.torch.float64)
             self.dist.all_gather_into_tensor(r, s, group=self.group)
-            if self.device_buffers and self.nccl:
+            if self.device_buffers and self.nccl and not self.stream_ordered:
                 self.torch.cuda.synchronize()
             self._writeback(recv, count * self.size, r)
             self.calls["allgather"] += 1
@@ -126,7 +138,7 @@ class TorchComm:
             if ops:
                 for req in self.dist.batch_isend_irecv(ops):
                     req.wait()
-                if self.device_buffers and self.nccl:
+                if self.device_buffers and self.nccl and not self.stream_ordered:
                     self.torch.cuda.synchronize()
             if r is not None:
                 self._writeback(recv, rcount, r)
@@ -136,6 +148,44 @@ class TorchComm:
         except Exception as e:
             print(f"[lrs dist] sendrecv failed: {e}")
             return 1
+
+
+class LibNcclComm:
+    """The in-library NCCL data plane (lrs_comm_nccl_create, csrc/comm_nccl.cu): grouped
+    ncclSend / ncclRecv and ncclAllGather enqueued on the context stream, no host callbacks.
+    torch.distributed only carries the 128-byte ncclUniqueId from rank 0 to the others.
+    Must outlive the factorizations built on it."""
+
+    def __init__(self, ctx: api.Context, group=None):
+        import torch.distributed as dist
+
+        L = api.lib()
+        L.lrs_comm_nccl_unique_id.restype = ctypes.c_int32
+        L.lrs_comm_nccl_unique_id.argtypes = [ctypes.c_void_p]
+        L.lrs_comm_nccl_create.restype = ctypes.c_int32
+        L.lrs_comm_nccl_create.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32,
+                                           ctypes.c_int32, ctypes.POINTER(ctypes.POINTER(CommC))]
+        L.lrs_comm_nccl_destroy.restype = None
+        L.lrs_comm_nccl_destroy.argtypes = [ctypes.POINTER(CommC)]
+        import torch
+
+        self.torch, self.dist, self.group = torch, dist, group
+        self.rank, self.size = dist.get_rank(group), dist.get_world_size(group)
+        uid = (ctypes.c_ubyte * 128)()
+        if self.rank == 0:
+            api._check(L.lrs_comm_nccl_unique_id(uid))
+        obj = [bytes(uid)]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        ctypes.memmove(uid, obj[0], 128)
+        self._p = ctypes.POINTER(CommC)()
+        api._check(L.lrs_comm_nccl_create(ctx.h, uid, self.rank, self.size,
+                                          ctypes.byref(self._p)), ctx.h)
+        self.c = self._p.contents
+
+    def close(self):
+        if self._p:
+            api.lib().lrs_comm_nccl_destroy(self._p)
+            self._p = None
 
 
 class DistFactorization(api.SpikeFactorization):

@@ -3,12 +3,17 @@
 //   test_api gpu   factorize / apply / solve through liblrspike_cuda.so
 // A tiny check macro stands in for doctest (absent from the image).
 #include <cmath>
+#include <complex>
 #include <cstdio>
 #include <cstring>
+#include <fstream>
 #include <functional>
+#include <map>
+#include <sstream>
 #include <string>
 #include <vector>
 
+#include "lrspike/comm.hpp"
 #include "lrspike/errors.hpp"
 #include "lrspike/matrix.hpp"
 #include "lrspike/solver.hpp"
@@ -268,10 +273,188 @@ static void gpu_tests() {
   }
 }
 
+// ---- oracle fixtures (written by tests/test_gpu_cpp_api.py from the CPU oracle) ----------
+// manifest.txt: "<name> <rows> <cols> <f64|c128|i64> <extra int>" per line; <name>.bin raw
+struct Fixtures {
+  std::string dir;
+  std::map<std::string, std::vector<long>> meta;
+  explicit Fixtures(const std::string& d) : dir(d) {
+    std::ifstream m(d + "/manifest.txt");
+    std::string line;
+    while (std::getline(m, line)) {
+      std::istringstream is(line);
+      std::string name, type;
+      long r, c, extra = 0;
+      is >> name >> r >> c >> type >> extra;
+      meta[name] = {r, c, type == "f64" ? 1L : type == "c128" ? 2L : 3L, extra};
+    }
+  }
+  long rows(const std::string& n) const { return meta.at(n)[0]; }
+  long cols(const std::string& n) const { return meta.at(n)[1]; }
+  long extra(const std::string& n) const { return meta.at(n)[3]; }
+  template <class T>
+  std::vector<T> raw(const std::string& n) const {
+    std::ifstream f(dir + "/" + n + ".bin", std::ios::binary);
+    f.seekg(0, std::ios::end);
+    const size_t bytes = (size_t)f.tellg();
+    f.seekg(0);
+    std::vector<T> v(bytes / sizeof(T));
+    f.read(reinterpret_cast<char*>(v.data()), (std::streamsize)bytes);
+    return v;
+  }
+  template <class S>
+  DenseBlockT<S> block(const std::string& n) const {
+    DenseBlockT<S> b(rows(n), cols(n));
+    const auto v = raw<S>(n);
+    std::copy(v.begin(), v.end(), b.data());
+    return b;
+  }
+  template <class S>
+  CsrMatrixT<S> csr(const std::string& n) const {
+    CsrMatrixT<S> a;
+    a.n_rows = a.n_cols = rows(n + "_rowptr") - 1;
+    a.row_ptr = raw<index_t>(n + "_rowptr");
+    a.col_idx = raw<index_t>(n + "_colidx");
+    a.values = raw<S>(n + "_values");
+    return a;
+  }
+};
+
+template <class S>
+static double rel(const DenseBlockT<S>& a, const DenseBlockT<S>& b) {
+  double d = 0, n = 0;
+  for (index_t e = 0; e < a.size(); ++e) {
+    d += std::norm(a.data()[e] - b.data()[e]);
+    n += std::norm(b.data()[e]);
+  }
+  return std::sqrt(d / std::max(n, 1e-300));
+}
+
+template <class S>
+static DenseBlockT<S> usv(const LowRankSpikeT<S>& s) {  // u diag(sigma) v
+  DenseBlockT<S> o(s.u.rows(), s.v.cols());
+  for (index_t a = 0; a < (index_t)s.sigma.size(); ++a)
+    for (index_t j = 0; j < s.v.cols(); ++j) {
+      const S w = s.sigma[a] * s.v(a, j);
+      for (index_t i = 0; i < s.u.rows(); ++i) o(i, j) += s.u(i, a) * w;
+    }
+  return o;
+}
+
+static void report(const char* what, double v, double bar) {
+  std::printf("  %-44s %.3e (bar %.0e)\n", what, v, bar);
+  CHECK(v <= bar);
+}
+
+static void oracle_tests(const std::string& dir) {
+  Fixtures F(dir);
+  // ---- real case (c1 structure): every SPEC op of the C++ surface against the oracle
+  {
+    const auto A = F.csr<double>("A");
+    const index_t p = F.extra("A_rowptr"), k = F.extra("A_colidx"), r = F.extra("A_values");
+    const auto lay = make_layout(A.n_rows, p, k);
+    const auto blocks = extract_blocks(A, lay);
+    // randomized_spike_svd, both sides, and the coupling mode
+    const auto F0 = factorize_block(blocks.A[0]);
+    const auto F1 = factorize_block(blocks.A[1]);
+    const index_t os = (r + 1) / 2;
+    const auto sT = randomized_spike_svd(F0, blocks.B[0], Side::T, r, os, 2, F.extra("rhs"), 0);
+    const auto sW = randomized_spike_svd(F1, blocks.C[1], Side::W, r, os, 2, F.extra("rhs"), 1);
+    const auto sC = randomized_spike_svd(F0, blocks.B[0], Side::T, r, os, 2, F.extra("rhs"), 0,
+                                         SpikeMode::CouplingSvd);
+    report("randomized_spike_svd T_0: u S v", rel(usv(sT), F.block<double>("usvT0")), 1e-9);
+    report("randomized_spike_svd W_1: u S v", rel(usv(sW), F.block<double>("usvW1")), 1e-9);
+    report("coupling-mode spike T_0: u S v", rel(usv(sC), F.block<double>("usvC0")), 1e-9);
+    DenseBlock sig(r, 1);
+    for (index_t a = 0; a < r; ++a) sig(a, 0) = sT.sigma[a];
+    report("randomized_spike_svd T_0: sigma", rel(sig, F.block<double>("sigT0")), 1e-10);
+    const auto tips = spike_tips(sT, k);
+    CHECK(tips.first.rows() == k && tips.second.rows() == k && tips.second(0, 0) == sT.u(sT.u.rows() - k, 0));
+    // build / apply_truncated_precond and matvec_lowrank from the ORACLE's spikes
+    std::vector<LowRankSpike> spT, spW;
+    for (index_t i = 0; i + 1 < p; ++i) {
+      LowRankSpike t, w;
+      t.u = F.block<double>("uT" + std::to_string(i));
+      t.v = F.block<double>("vT" + std::to_string(i));
+      w.u = F.block<double>("uW" + std::to_string(i + 1));
+      w.v = F.block<double>("vW" + std::to_string(i + 1));
+      const auto st = F.block<double>("sT" + std::to_string(i));
+      const auto sw = F.block<double>("sW" + std::to_string(i + 1));
+      t.sigma.assign(st.data(), st.data() + st.size());
+      w.sigma.assign(sw.data(), sw.data() + sw.size());
+      w.side = Side::W;
+      spT.push_back(t);
+      spW.push_back(w);
+    }
+    const auto P = build_truncated_precond(spT, spW, k);
+    ReducedVector g(p, k, 2);
+    g.data = F.block<double>("g");
+    report("apply_truncated_precond", rel(apply_truncated_precond(*P, g).data, F.block<double>("trunc_g")), 1e-12);
+    report("matvec_lowrank", rel(matvec_lowrank(*P, g).data, F.block<double>("lowrank_g")), 1e-12);
+    // Krylov drivers on operator contracts: A = SpMV, M = LR-SPIKE-T
+    SolverConfig cfg;
+    cfg.p = p;
+    cfg.k = k;
+    cfg.n_svd = r;
+    cfg.seed = F.extra("rhs");
+    auto fac = factorize(A, cfg);
+    const auto b = F.block<double>("rhs");
+    const auto opA = as_operator(*fac->matrix());
+    const auto opM = as_operator(*fac);
+    IterConfig it;
+    it.tol = 1e-8;
+    auto bi = bicgstab(opA, &opM, b, it);
+    report("bicgstab(operators) x vs oracle", rel(bi.first, F.block<double>("x_bicgstab")), 1e-8);
+    CHECK(std::fabs(bi.second.iterations - F.extra("x_bicgstab")) <= 2 && bi.second.residual_final <= 1e-8);
+    it.restart = 30;
+    auto gm = gmres(opA, &opM, b, it);
+    report("gmres(operators) x vs oracle", rel(gm.first, F.block<double>("x_gmres")), 1e-8);
+    CHECK(std::fabs(gm.second.iterations - F.extra("x_gmres")) <= 2 && gm.second.residual_final <= 1e-8);
+    // matvec_exact / matvec_otf on the factorization vs the oracle's exact reduced matvec
+    report("matvec_exact (otf)", rel(matvec_exact(*fac, g).data, F.block<double>("exact_g")), 1e-11);
+    // spmv reuses the device copy: same result, no re-upload
+    const auto y1 = spmv(A, b);
+    const auto y2 = spmv(A, b);
+    CHECK(A.device_cache && rel(y1, y2) == 0.0);
+    // factorize_dist on a one-rank in-library NCCL communicator == factorize
+    try {
+      NcclCommunicator comm(Device::default_device(), NcclCommunicator::nccl_unique_id(), 0, 1);
+      auto fd = factorize_dist(A, cfg, comm);
+      const auto xd = solve(A, b, cfg, fd);
+      const auto xs = solve(A, b, cfg, fac);
+      report("factorize_dist (1-rank NCCL) vs factorize", rel(xd.first, xs.first), 0.0);
+    } catch (const Error& e) {
+      std::printf("  NCCL communicator unavailable: %s\n", e.what());
+      CHECK(false);
+    }
+  }
+  // ---- complex128 (c5 structure, 2 RHS): solve through the templated API
+  {
+    const auto Az = F.csr<complex128>("Z");
+    SolverConfigZ cz;
+    cz.p = F.extra("Z_rowptr");
+    cz.k = F.extra("Z_colidx");
+    cz.n_svd = F.extra("Z_values");
+    cz.seed = F.extra("zrhs");
+    cz.outer.method = Method::GMRES;
+    cz.outer.restart = 40;
+    cz.outer.tol = 1e-10;
+    const auto bz = F.block<complex128>("zrhs");
+    const auto sz = solve(Az, bz, cz);
+    report("complex128 GMRES solve x vs oracle", rel(sz.first, F.block<complex128>("zx")), 1e-8);
+    CHECK(sz.second.converged && sz.second.residual_final <= 1e-10);
+    CHECK(std::fabs(sz.second.iterations - F.extra("zx")) <= 2);
+    const auto fz = factorize(Az, cz);
+    const auto spz = fz->spike(0, Side::T);
+    report("complex128 spike T_0: u S v", rel(usv(spz), F.block<complex128>("zusvT0")), 1e-9);
+  }
+}
+
 int main(int argc, char** argv) {
   const std::string mode = argc > 1 ? argv[1] : "cpu";
   cpu_tests();
   if (mode == "gpu") gpu_tests();
+  if (mode == "oracle" && argc > 2) oracle_tests(argv[2]);
   std::printf("%d passed, %d failed\n", g_pass, g_fail);
   return g_fail ? 1 : 0;
 }

@@ -54,16 +54,17 @@ def gpu_solve_worker(rank, world, port, out_dir, name, scale, method, P, variant
     """One rank of a sharded factorize + solve on cuda:0 (ranks share the GPU; all
     cross-rank dependencies are host-synchronous gloo calls).  backend="nccl" (one rank:
     NCCL refuses two ranks on one device) runs the adapter's device-buffer path."""
-    dist = _init(rank, world, port, backend)
+    dist = _init(rank, world, port, "gloo" if backend == "libnccl" else backend)
     import torch
 
     from paper_2504_11167_b200 import api, configs
-    from paper_2504_11167_b200.dist import DistFactorization, TorchComm, gather_rows
+    from paper_2504_11167_b200.dist import DistFactorization, LibNcclComm, TorchComm, gather_rows
 
     torch.cuda.set_device(0)
-    comm = TorchComm(device_buffers=True)
     cfg = configs.make_config(name, scale, P)
     ctx = api.Context(0)
+    # libnccl: the in-library NCCL data plane (torch.distributed/gloo only shares the id)
+    comm = LibNcclComm(ctx) if backend == "libnccl" else TorchComm(device_buffers=True)
     A = api.CsrMatrix.from_csr(ctx, cfg.matrix)
     scfg = api.SolverConfig(variant=variant, p=cfg.P, k=cfg.b, n_svd=cfg.r, seed=cfg.seed)
     F = DistFactorization(ctx, A, scfg, comm)
@@ -83,11 +84,30 @@ def gpu_solve_worker(rank, world, port, out_dir, name, scale, method, P, variant
         r2 = torch.zeros(6, dtype=torch.float64, device="cuda")
         assert comm._sendrecv(None, s.data_ptr(), 6, rank, r2.data_ptr(), 6, rank) == 0
         adapter = np.concatenate([r.cpu().numpy(), r2.cpu().numpy()])
+    if backend == "libnccl":
+        # one rank: drive the library's stream-ordered NCCL callbacks directly (all-gather,
+        # a send / receive to this rank itself, and the grouped two-direction exchange)
+        s = torch.arange(6, dtype=torch.float64, device="cuda") + 1.0
+        r = torch.zeros(6 * world, dtype=torch.float64, device="cuda")
+        r2 = torch.zeros(6, dtype=torch.float64, device="cuda")
+        torch.cuda.synchronize()
+        c = comm.c
+        assert c.stream_ordered == 1
+        assert c.allgather(c.user, s.data_ptr(), r.data_ptr(), 6) == 0
+        assert c.sendrecv(c.user, s.data_ptr(), 6, rank, r2.data_ptr(), 6, rank) == 0
+        ctx.synchronize()
+        adapter = np.concatenate([r.cpu().numpy(), r2.cpu().numpy()])
     if rank == 0:
         np.savez(os.path.join(out_dir, "dist.npz"), x=xg, y=yg, iterations=rep.iterations,
                  adapter=adapter,
                  residual=rep.residual_final, history=np.array(rep.residual_history),
                  ledger=np.array([rep.comm["precond-apply"][1], rep.comm["recovery"][1]]),
-                 calls=np.array([comm.calls["allgather"], comm.calls["sendrecv"]]))
+                 calls=np.array([comm.calls["allgather"], comm.calls["sendrecv"]])
+                 if hasattr(comm, "calls") else np.array([0, 0]),
+                 round_trips=np.array([rep.round_trips["comm_calls"],
+                                       rep.round_trips["comm_host_syncs"]]))
     dist.barrier()
+    del F
+    if backend == "libnccl":
+        comm.close()
     dist.destroy_process_group()

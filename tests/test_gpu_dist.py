@@ -33,7 +33,8 @@ def _port():
                           ("c1", 64 / 256, "gmres", 4, 2, "T", "gloo"),
                           ("c2", 16 / 64, "bicgstab", 8, 3, "I", "gloo"),
                           ("c1", 64 / 256, "gmres", 4, 2, "OTF", "gloo"),
-                          ("c2", 16 / 64, "bicgstab", 8, 1, "T", "nccl")])
+                          ("c2", 16 / 64, "bicgstab", 8, 1, "T", "nccl"),
+                          ("c2", 16 / 64, "bicgstab", 8, 1, "T", "libnccl")])
 def test_sharded_solve_matches_single_gpu(ctx, name, scale, method, P, world, variant, backend):
     from paper_2504_11167_b200 import api, configs
 
@@ -56,6 +57,8 @@ def test_sharded_solve_matches_single_gpu(ctx, name, scale, method, P, world, va
     assert np.array_equal(z["x"], x1)  # identical iterates on any number of GPUs
     if world > 1:
         assert z["calls"][0] > 0 and z["calls"][1] > 0
-    if backend == "nccl":  # the adapter's NCCL device-buffer path, driven directly
+    if world > 1:  # host-callback transport: every exchange is a host round trip
+        assert z["round_trips"][0] > 0 and z["round_trips"][1] > 0
+    if backend in ("nccl", "libnccl"):  # the NCCL device-buffer paths, driven directly
         ref = np.arange(6, dtype=np.float64) + 1.0
         assert np.array_equal(z["adapter"], np.concatenate([ref, ref]))
