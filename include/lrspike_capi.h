@@ -265,9 +265,10 @@ LRS_API lrs_status lrs_dense_gemm(lrs_ctx* ctx, int32_t scalar, int64_t m, int64
                                   const void* A, int64_t lda, const void* B, int64_t ldb, void* C,
                                   int64_t ldc, int32_t conjC, int32_t mem);
 /* build_truncated_precond from explicit LowRankSpikes of p partitions:
- *   uT_tips  (p-1) consecutive k x r blocks: the bottom tip of u of T_i, i = 0..p-2
+ *   uT_tips  (p-1) consecutive 2k x r blocks: the top then the bottom k-row tip of u of T_i,
+ *            i = 0..p-2 (spike_tips)
  *   vT       (p-1) consecutive r x k blocks: v of T_i;  sT (p-1) x r: sigma of T_i
- *   uW_tips  (p-1) consecutive k x r blocks: the top tip of u of W_i, i = 1..p-1
+ *   uW_tips  (p-1) consecutive 2k x r blocks: the tips of u of W_i, i = 1..p-1
  *   vW, sW   likewise for W_i.
  * Returns a handle whose lrs_reduced_apply runs apply_truncated_precond and
  * matvec_lowrank on ReducedVectors; IllConditionedInterfaceError (interface

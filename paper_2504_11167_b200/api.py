@@ -626,7 +626,7 @@ class TruncatedPrecond:
     """build_truncated_precond from explicit spikes, on the device.
 
     spikes_T[i] = (u, sigma, v) of T_i (i = 0..p-2), spikes_W[i] = those of W_{i+1}; only
-    the k-row tips of u are used.  apply(g) = apply_truncated_precond and
+    the two k-row tips of u are used (spike_tips).  apply(g) = apply_truncated_precond and
     matvec_lowrank(x) on ReducedVector blocks (2 k p x n_rhs, partition
     i's top tip in rows [2ki, 2ki + k), its bottom tip in [2ki + k, 2k(i+1))).
     IllConditionedInterfaceError(interface, cond_1) above cond_1 = 1e12."""
@@ -639,8 +639,9 @@ class TruncatedPrecond:
         self.dtype = np.dtype(np.complex128 if cplx else np.float64)
         cat = lambda blocks: np.ascontiguousarray(  # noqa: E731
             np.concatenate([np.asarray(b, dtype=self.dtype).ravel(order="F") for b in blocks]))
-        uT = cat([u[-self.k:] for u, _, _ in spikes_T])
-        uW = cat([u[:self.k] for u, _, _ in spikes_W])
+        tips = lambda u: np.concatenate([u[:self.k], u[-self.k:]])  # noqa: E731  2k x r
+        uT = cat([tips(u) for u, _, _ in spikes_T])
+        uW = cat([tips(u) for u, _, _ in spikes_W])
         vT = cat([v for _, _, v in spikes_T])
         vW = cat([v for _, _, v in spikes_W])
         sT = np.ascontiguousarray(np.concatenate([np.asarray(s, float) for _, s, _ in spikes_T]))

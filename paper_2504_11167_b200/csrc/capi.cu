@@ -827,9 +827,9 @@ lrs_status lrs_trunc_precond_create(lrs_ctx* c, int32_t scalar, int64_t p, int64
     const int64_t cnt = (p - 1) * k * r;
     DevBuf<double> a, b, d, e, sa, sb;
     int64_t ld;
-    const void* uTd = dev_in(c, uT_tips, cnt, cnt, 1, mem, a, &ld, w);
+    const void* uTd = dev_in(c, uT_tips, 2 * cnt, 2 * cnt, 1, mem, a, &ld, w);
     const void* vTd = dev_in(c, vT, cnt, cnt, 1, mem, b, &ld, w);
-    const void* uWd = dev_in(c, uW_tips, cnt, cnt, 1, mem, d, &ld, w);
+    const void* uWd = dev_in(c, uW_tips, 2 * cnt, 2 * cnt, 1, mem, d, &ld, w);
     const void* vWd = dev_in(c, vW, cnt, cnt, 1, mem, e, &ld, w);
     const double* sTd = static_cast<const double*>(dev_in(c, sT, (p - 1) * r, (p - 1) * r, 1, mem, sa, &ld, 1));
     const double* sWd = static_cast<const double*>(dev_in(c, sW, (p - 1) * r, (p - 1) * r, 1, mem, sb, &ld, 1));

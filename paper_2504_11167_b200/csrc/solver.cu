@@ -2265,8 +2265,10 @@ void reduced_op_t(Fact* f, int kind, S* x, S* y, int nrhs) {
 // with no band factors whose "n-layout" is the compact reduced layout (partition i owns
 // rows [2ki, 2k(i+1)): top tip, then bottom tip), so the interface setup and the
 // reduced-system operators (apply_truncated_precond, matvec_lowrank) run unchanged.
-// Spike arrays are device pointers: uTb[i] (k x r, bottom tip of u_{T_i}, i < p-1),
-// vT[i] (r x k), sT[i] (r); uWt[i] (k x r, top tip of u_{W_{i+1}}), vW[i], sW[i].
+// Spike arrays are device pointers: uT[i] (2k x r: the top then the bottom k-row tip of
+// u of T_i, i < p-1), vT[i] (r x k), sT[i] (r); uW[i] (2k x r, tips of u of W_{i+1}),
+// vW[i], sW[i].  apply_truncated_precond reads the bottom tips of T and the top tips of W,
+// matvec_lowrank all four.
 template <class S>
 Fact* trunc_precond_t(Ctx* c, int64_t p, int64_t k, int r, const S* uTb, const S* vT,
                       const double* sT, const S* uWt, const S* vW, const double* sW) {
@@ -2310,11 +2312,12 @@ Fact* trunc_precond_t(Ctx* c, int64_t p, int64_t k, int r, const S* uTb, const S
     LRS_CUDA(cudaMemsetAsync(b->get(), 0, b->bytes, c->stream));
   const size_t es = sizeof(S);
   for (int64_t i = 0; i + 1 < p; ++i) {
-    // u tips into the compact rows; v (r x k) transposed into v^T (k x r) by a 2D copy
-    LRS_CUDA(cudaMemcpy2DAsync(sp<S>(f->uT) + 2 * k * i + k, es * n, uTb + i * kr, es * k, es * k,
-                               r, cudaMemcpyDeviceToDevice, c->stream));
-    LRS_CUDA(cudaMemcpy2DAsync(sp<S>(f->uW) + 2 * k * (i + 1), es * n, uWt + i * kr, es * k,
-                               es * k, r, cudaMemcpyDeviceToDevice, c->stream));
+    // both u tips into the compact rows of their partition; v (r x k) transposed into
+    // v^T (k x r) by a strided 2D copy
+    LRS_CUDA(cudaMemcpy2DAsync(sp<S>(f->uT) + 2 * k * i, es * n, uTb + 2 * i * kr, es * 2 * k,
+                               es * 2 * k, r, cudaMemcpyDeviceToDevice, c->stream));
+    LRS_CUDA(cudaMemcpy2DAsync(sp<S>(f->uW) + 2 * k * (i + 1), es * n, uWt + 2 * i * kr,
+                               es * 2 * k, es * 2 * k, r, cudaMemcpyDeviceToDevice, c->stream));
     for (int a = 0; a < r; ++a) {  // row a of v -> column a of v^T
       LRS_CUDA(cudaMemcpy2DAsync(sp<S>(f->vtT) + i * kr + (int64_t)a * k, es, vT + i * kr + a,
                                  es * r, es, k, cudaMemcpyDeviceToDevice, c->stream));

@@ -4,6 +4,16 @@
 // spmv follows reference proj/core/src/matrix.cpp:121-136: every output row
 // sums its entries in ascending column order (one thread per row walks the
 // row sequentially), so the summation order is the reference's.
+//
+// spmv_staged_kernel (default): a CTA owns 256 consecutive rows; their nonzeros, one
+// contiguous range of col_idx / values, are staged through shared memory in chunks of
+// SPMV_CAP entries with coalesced loads (a warp reads 32 consecutive 8-byte values and
+// 4-byte indices), then each thread sums its own row from shared memory in ascending
+// column order -- the one-thread-per-row kernel's summation order, without its strided
+// per-thread loads (27-point rows put a warp's loads ~216 B apart).  LRS_SPMV_SCALAR=1
+// selects the one-thread-per-row kernel.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.h"
 #include "lrs_internal.h"
@@ -41,6 +51,53 @@ __global__ void __launch_bounds__(256) spmv_kernel(int64_t n, const int* __restr
   }
 }
 
+constexpr int SPMV_ROWS = 256;
+constexpr int SPMV_CAP = 4096;  // staged nonzeros per chunk: 48 KB (real), 80 KB (complex)
+
+template <int NR, class S>
+__global__ void __launch_bounds__(SPMV_ROWS) spmv_staged_kernel(
+    int64_t n, const int* __restrict__ rp, const int* __restrict__ ci, const S* __restrict__ va,
+    const S* __restrict__ x, int64_t ldx, S* __restrict__ y, int64_t ldy, int nrhs, int mode,
+    const S* __restrict__ b, int64_t ldb, int64_t row_lo) {
+  extern __shared__ __align__(16) unsigned char spmv_sm[];
+  S* sv = reinterpret_cast<S*>(spmv_sm);
+  int* sc = reinterpret_cast<int*>(sv + SPMV_CAP);
+  const int64_t r0 = row_lo + (int64_t)blockIdx.x * SPMV_ROWS;
+  const int64_t r1 = r0 + SPMV_ROWS < n ? r0 + SPMV_ROWS : n;
+  const int64_t row = r0 + threadIdx.x;
+  const int q0 = rp[r0], q1 = rp[r1];
+  const int s = row < r1 ? rp[row] : q1, e = row < r1 ? rp[row + 1] : q1;
+  S acc[NR];
+#pragma unroll
+  for (int j = 0; j < NR; ++j) acc[j] = s_zero(S());
+  for (int base = q0; base < q1; base += SPMV_CAP) {
+    const int cnt = q1 - base < SPMV_CAP ? q1 - base : SPMV_CAP;
+    for (int t = threadIdx.x; t < cnt; t += SPMV_ROWS) {
+      sv[t] = va[base + t];
+      sc[t] = ci[base + t];
+    }
+    __syncthreads();
+    const int a = s > base ? s : base, z = e < base + cnt ? e : base + cnt;
+    for (int q = a; q < z; ++q) {
+      const S v = sv[q - base];
+      const int64_t col = sc[q - base];
+#pragma unroll
+      for (int j = 0; j < NR; ++j)
+        if (j < nrhs) acc[j] = s_fma(v, x[col + j * ldx], acc[j]);
+    }
+    __syncthreads();
+  }
+  if (row >= r1) return;
+#pragma unroll
+  for (int j = 0; j < NR; ++j) {
+    if (j >= nrhs) break;
+    S* yo = y + row + j * ldy;
+    if (mode == 0) *yo = acc[j];
+    else if (mode == 1) *yo = s_add(*yo, acc[j]);
+    else *yo = s_sub(b[row + j * ldb], acc[j]);
+  }
+}
+
 template <class S>
 static void spmv_t(Ctx* c, const Mat* m, const S* x, int64_t ldx, S* y, int64_t ldy, int nrhs,
                    int mode, const S* b, int64_t ldb, int64_t row_lo, int64_t row_hi) {
@@ -54,9 +111,26 @@ static void spmv_t(Ctx* c, const Mat* m, const S* x, int64_t ldx, S* y, int64_t 
     S* yj = y + j0 * ldy;
     const S* bj = b ? b + j0 * ldb : nullptr;
     ProfScope ps_(c, K_SPMV);
+    static const bool scalar = std::getenv("LRS_SPMV_SCALAR") && std::getenv("LRS_SPMV_SCALAR")[0] == '1';
+    constexpr size_t smem = (sizeof(S) + sizeof(int)) * SPMV_CAP;
 #define LRS_SPMV(NRV)                                                                          \
-  spmv_kernel<NRV, S><<<grid, 256, 0, c->stream>>>(n, m->row_ptr.get(), m->col_idx.get(), va,  \
-                                                   xj, ldx, yj, ldy, nr, mode, bj, ldb, row_lo)
+  do {                                                                                         \
+    if (scalar) {                                                                              \
+      spmv_kernel<NRV, S><<<grid, 256, 0, c->stream>>>(n, m->row_ptr.get(), m->col_idx.get(),  \
+                                                       va, xj, ldx, yj, ldy, nr, mode, bj, ldb, \
+                                                       row_lo);                                \
+    } else {                                                                                   \
+      static bool attr_ = false;                                                               \
+      if (!attr_) {                                                                            \
+        LRS_CUDA(cudaFuncSetAttribute(spmv_staged_kernel<NRV, S>,                              \
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+        attr_ = true;                                                                          \
+      }                                                                                        \
+      spmv_staged_kernel<NRV, S><<<grid, SPMV_ROWS, smem, c->stream>>>(                        \
+          n, m->row_ptr.get(), m->col_idx.get(), va, xj, ldx, yj, ldy, nr, mode, bj, ldb,      \
+          row_lo);                                                                             \
+    }                                                                                          \
+  } while (0)
     if (nr == 1) LRS_SPMV(1);
     else if (nr <= 2) LRS_SPMV(2);
     else if (nr <= 4) LRS_SPMV(4);

@@ -627,7 +627,8 @@ std::shared_ptr<TruncatedPrecondT<S>> build_truncated_precond(
   if (spT.empty() || spT.size() != spW.size())
     throw DimensionError("build_truncated_precond: p-1 spikes of each side required");
   const index_t p = (index_t)spT.size() + 1, r = (index_t)spT[0].sigma.size();
-  std::vector<S> uT((size_t)(p - 1) * k * r), vT(uT.size()), uW(uT.size()), vW(uT.size());
+  std::vector<S> uT((size_t)(p - 1) * 2 * k * r), uW(uT.size());
+  std::vector<S> vT((size_t)(p - 1) * k * r), vW(vT.size());
   std::vector<double> sT((size_t)(p - 1) * r), sW(sT.size());
   for (index_t i = 0; i + 1 < p; ++i) {
     const LowRankSpikeT<S>& t = spT[i];
@@ -635,10 +636,15 @@ std::shared_ptr<TruncatedPrecondT<S>> build_truncated_precond(
     if ((index_t)t.sigma.size() != r || (index_t)w.sigma.size() != r || t.v.cols() != k ||
         w.v.cols() != k || t.u.rows() < k || w.u.rows() < k)
       throw DimensionError("build_truncated_precond: spike shapes differ");
-    const auto tb = spike_tips(t, k).second;  // bottom tip of u_{T_i}
-    const auto wt = spike_tips(w, k).first;   // top tip of u_{W_{i+1}}
-    std::copy_n(tb.data(), k * r, uT.begin() + i * k * r);
-    std::copy_n(wt.data(), k * r, uW.begin() + i * k * r);
+    for (int side = 0; side < 2; ++side) {  // [top tip; bottom tip], 2k x r per spike
+      const LowRankSpikeT<S>& sp = side == 0 ? t : w;
+      std::vector<S>& dst = side == 0 ? uT : uW;
+      const auto tips = spike_tips(sp, k);
+      for (index_t a = 0; a < r; ++a) {
+        std::copy_n(tips.first.data() + a * k, k, dst.begin() + (i * r + a) * 2 * k);
+        std::copy_n(tips.second.data() + a * k, k, dst.begin() + (i * r + a) * 2 * k + k);
+      }
+    }
     std::copy_n(t.v.data(), k * r, vT.begin() + i * k * r);
     std::copy_n(w.v.data(), k * r, vW.begin() + i * k * r);
     std::copy_n(t.sigma.begin(), r, sT.begin() + i * r);

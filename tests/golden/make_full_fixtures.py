@@ -39,22 +39,29 @@ def cpu_model() -> str:
     return platform.processor() or "unknown"
 
 
-def run(name: str, scale: float = 1.0, P: int | None = None) -> dict:
+def run(name: str, scale: float = 1.0, P: int | None = None, shift: int | None = None,
+        nrhs: int | None = None) -> dict:
     c = configs.make_config(name, scale, P)
-    A = c.matrix.to_scipy()
+    A = c.system(shift).to_scipy() if shift is not None else c.matrix.to_scipy()
+    rhs = c.rhs if nrhs is None else c.rhs[:, :nrhs]
+    if shift is not None:
+        rhs = np.asfortranarray(rhs.astype(np.complex128))
     scfg = O.SolverConfig(variant="T", p=c.P, k=c.b, n_svd=c.r, seed=c.seed)
     it = O.IterConfig(tol=c.tol, restart=c.m or 30)
     t0 = time.perf_counter()
     F = O.factorize(A, scfg)
     print(f"{name}: factorize {time.perf_counter() - t0:.1f} s", flush=True)
     t1 = time.perf_counter()
-    x, rep, _ = O.solve(A, c.rhs, scfg, it, method=c.method, F=F)
+    x, rep, _ = O.solve(A, rhs, scfg, it, method=c.method, F=F)
     t2 = time.perf_counter()
     tag = f"full_{name}" if scale == 1.0 and P is None else f"{name}_s{scale:g}_P{c.P}"
-    np.savez_compressed(os.path.join(OUT, f"{tag}.npz"), x=x.astype(np.float64))
+    if shift is not None:
+        tag += f"_z{shift}_r{rhs.shape[1]}"
+    np.savez_compressed(os.path.join(OUT, f"{tag}.npz"), x=x)
     meta = {
         "config": name, "scale": scale, "P": c.P, "n": int(A.shape[0]), "nnz": int(A.nnz),
         "k": c.b, "n_svd": F.n_svd, "method": c.method, "restart": c.m, "tol": c.tol,
+        "shift": shift, "nrhs": int(rhs.shape[1]),
         "iterations": rep.iterations, "residual_final": rep.residual_final,
         "converged": rep.converged, "precond_applications": rep.precond_applications,
         "matvecs": rep.matvecs, "x_norm": float(np.linalg.norm(x)),
@@ -73,6 +80,8 @@ def run(name: str, scale: float = 1.0, P: int | None = None) -> dict:
 
 if __name__ == "__main__":
     for arg in sys.argv[1:] or ["c1"]:
-        parts = arg.split(":")  # name[:scale[:P]]
+        parts = arg.split(":")  # name[:scale[:P[:shift[:nrhs]]]]
         run(parts[0], float(parts[1]) if len(parts) > 1 else 1.0,
-            int(parts[2]) if len(parts) > 2 else None)
+            int(parts[2]) if len(parts) > 2 else None,
+            int(parts[3]) if len(parts) > 3 else None,
+            int(parts[4]) if len(parts) > 4 else None)
