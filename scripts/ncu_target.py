@@ -1,5 +1,5 @@
-"""Small fixed workload for ncu captures: one c2 factorize + 3 preconditioner
-applies (+ optional solve).  Usage: python scripts/ncu_target.py [config] [scale] [solve]"""
+"""Small fixed workload for ncu captures: one factorize + 3 preconditioner applies
+(+ optional solve).  Usage: python scripts/ncu_target.py [config] [scale] [solve] [P]"""
 import os
 import sys
 
@@ -11,8 +11,9 @@ from paper_2504_11167_b200 import api, configs  # noqa: E402
 name = sys.argv[1] if len(sys.argv) > 1 else "c2"
 scale = float(sys.argv[2]) if len(sys.argv) > 2 else 1.0
 do_solve = len(sys.argv) > 3 and sys.argv[3] == "solve"
+P = int(sys.argv[4]) if len(sys.argv) > 4 else None
 ctx = api.Context(0)
-cfg = configs.make_config(name, scale)
+cfg = configs.make_config(name, scale, P)
 A = api.CsrMatrix.from_csr(ctx, cfg.matrix)
 F = api.factorize(ctx, A, api.SolverConfig(p=cfg.P, k=cfg.b, n_svd=cfg.r, seed=cfg.seed))
 f = np.asfortranarray(cfg.rhs)

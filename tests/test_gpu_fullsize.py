@@ -27,13 +27,15 @@ pytestmark = pytest.mark.gpu
 
 GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 
-CASES = [  # (fixture tag, config, scale, P)
+CASES = [  # (fixture tag, config, scale, P[, shift, n_rhs])
     ("full_c1", "c1", 1.0, None),
     ("full_c2", "c2", 1.0, None),
     ("c3_s0.333333_P8", "c3", 32 / 96, 8),
     ("c3_s0.333333_P16", "c3", 32 / 96, 16),
     ("c3_s0.416667_P32", "c3", 40 / 96, 32),  # 90 GMRES(50) steps: one restart
     ("c4_s0.05_P64", "c4", 0.05, 64),
+    # c5 at its own P = 16 (24^3 grid, complex128, shift 5, 2 RHS, GMRES(40) to 1e-10)
+    ("c5_s0.3_P16_z5_r2", "c5", 0.3, 16, 5, 2),
     # the bench workload itself: c3 at full size, P = 64 (312 GMRES(50) steps, 6 restarts);
     # the oracle run took 91 s + 272 s on the GPU box's 16 host cores
     ("c3_s1_P64", "c3", 1.0, 64),
@@ -47,20 +49,27 @@ def _fixture(tag):
     return meta, x
 
 
-@pytest.mark.parametrize("tag,name,scale,P", CASES)
-def test_solve_matches_oracle_fixture(ctx, tag, name, scale, P):
+@pytest.mark.parametrize("case", CASES, ids=[c[0] for c in CASES])
+def test_solve_matches_oracle_fixture(ctx, case):
+    tag, name, scale, P = case[:4]
     meta, xo = _fixture(tag)
     cfg = configs.make_config(name, scale, P)
     assert (meta["n"], meta["P"], meta["k"], meta["method"]) == (cfg.matrix.n, cfg.P, cfg.b,
                                                                  cfg.method)
-    A = api.CsrMatrix.from_csr(ctx, cfg.matrix)
+    rhs = cfg.rhs
+    csr = cfg.matrix
+    if len(case) > 4:  # a c5 contour system z_j I - A with the first n_rhs columns
+        csr = cfg.system(case[4])
+        rhs = np.asfortranarray(cfg.rhs[:, :case[5]].astype(np.complex128))
+    A = api.CsrMatrix.from_csr(ctx, csr)
     scfg = api.SolverConfig(variant="T", p=cfg.P, k=cfg.b, n_svd=cfg.r, seed=cfg.seed)
     it = api.IterConfig(tol=cfg.tol, method=cfg.method, restart=cfg.m or 30, max_iters=2000)
-    x, rep, F = api.solve(A, cfg.rhs, scfg, it)
+    x, rep, F = api.solve(A, rhs, scfg, it)
     assert F.n_svd == meta["n_svd"]
     if cfg.b >= 3 * 128:
         assert F.info["lu_int8"] == 1  # the INT8-sliced update carried the bulk of the LU
-    rel = float(np.linalg.norm(x.ravel() - xo.ravel()) / np.linalg.norm(xo))
+    rel = float(np.linalg.norm(np.ravel(x, order="F") - np.ravel(xo, order="F")) /
+                np.linalg.norm(xo))
     print(f"{tag}: iterations {rep.iterations} (oracle {meta['iterations']}), "
           f"rel diff {rel:.2e}, residual {rep.residual_final:.2e}")
     assert rep.converged
