@@ -139,8 +139,11 @@ WORKLOADS = {
     "c3": ("BASELINE.json configs[2] (at P=64: the largest single-GPU config, BASELINE.md 2 / "
            "SURVEY D7): 96^3 27-pt heterogeneous diffusion, n=884,736, nnz=23.4M, k=9,313, "
            "n_svd=32, GMRES(50) to 1e-8"),
+    "c5": ("BASELINE.json configs[4]: FEAST contour system z_j I - A, 80^3 7-pt + symmetric "
+           "perturbation, complex128, n=512,000, k=6,400, P=16, n_svd=32, 16 RHS, GMRES(40) to "
+           "1e-10; one shift per rank (replicas, PAPER.md:1628)"),
 }
-DEFAULT_P = {"c2": None, "c3": 64}
+DEFAULT_P = {"c2": None, "c3": 64, "c5": 16}
 
 
 def _workload(name, P, scale):
@@ -367,10 +370,14 @@ def run_ours(args):
     assert ctx.stream == stream.cuda_stream != 0
     P = args.P if args.P is not None else DEFAULT_P.get(args.config)
     cfg = configs.make_config(args.config, args.scale, P)
-    A = api.CsrMatrix.from_csr(ctx, cfg.matrix)
+    # c5: the 8 FEAST contour systems are independent -- replicas, rank q solves shift q % 8
+    shift = rank % 8 if args.config == "c5" else None
+    matrix = cfg.system(shift) if shift is not None else cfg.matrix
+    rhs_h = np.asfortranarray(cfg.rhs.astype(np.complex128) if shift is not None else cfg.rhs)
+    A = api.CsrMatrix.from_csr(ctx, matrix)
     scfg = api.SolverConfig(variant="T", p=cfg.P, k=cfg.b, n_svd=cfg.r, seed=cfg.seed)
     it = api.IterConfig(tol=cfg.tol, method=cfg.method, restart=cfg.m or 30, max_iters=3000)
-    b_dev = torch.from_numpy(np.asfortranarray(cfg.rhs)).cuda()
+    b_dev = torch.from_numpy(rhs_h).cuda()
     x_dev = torch.empty_like(b_dev)
     dmma_peak = ctx.dmma_peak_tflops()
     i8_peak = ctx.i8_peak_tops()
@@ -443,9 +450,9 @@ def run_ours(args):
 
     # ---- e2e: public C-ABI with host buffers (CSR upload + factorize + solve + x back)
     e2e_vals = []
-    csr = cfg.matrix
-    h2d = 8 * (csr.n + 1) + 16 * csr.nnz + 8 * cfg.rhs.size
-    d2h = 8 * cfg.rhs.size
+    csr = matrix
+    h2d = 8 * (csr.n + 1) + 8 * csr.nnz + csr.values.nbytes + rhs_h.nbytes
+    d2h = rhs_h.nbytes
 
     def pinned(a):  # a page-locked host copy (numpy view), made outside the timed region
         t = torch.empty(a.size, dtype=torch.from_numpy(a[:0].copy()).dtype, pin_memory=True)
@@ -454,8 +461,8 @@ def run_ours(args):
         return v, t
     (h_rp, _k1), (h_ci, _k2), (h_va, _k3) = (pinned(csr.row_ptr), pinned(csr.col_idx),
                                              pinned(csr.values))
-    h_b, _k4 = pinned(np.asfortranarray(cfg.rhs))
-    h_b = h_b.reshape(cfg.rhs.shape, order="F")
+    h_b, _k4 = pinned(rhs_h)
+    h_b = h_b.reshape(rhs_h.shape, order="F")
     # e2e: 1 warm-up + min(steps, 5) timed (each c3 step re-uploads 300 MB of CSR and
     # refactorizes 87 GB of band factors; five steps bound the run time)
     e2e_warm, e2e_steps = 1, min(args.steps, 5)
@@ -544,7 +551,8 @@ def run_ours(args):
     line = {
         "metric": "preconditioned solve time-to-tolerance (s)",
         "value": value, "unit": "s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms, "higher_is_better": False, "scaling": "strong",
+        "ms_per_step": ms, "higher_is_better": False,
+        "scaling": "weak" if shift is not None else "strong",
         "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
         "config": {"workload": _workload(args.config, P, args.scale),
@@ -579,7 +587,11 @@ def run_ours(args):
     }
     clocks = clk.summary()
     line["clocks"] = clocks
-    if rank == 0 and not args.no_cpu_baseline:
+    if shift is not None:
+        line["config"]["shift"] = {"index": shift, "z": [cfg.shifts[shift].real, cfg.shifts[shift].imag],
+                                   "n_rhs": int(rhs_h.shape[1])}
+        line["dtype"] = "c128"
+    if rank == 0 and not args.no_cpu_baseline and shift is None:
         try:
             line["cpu_baseline"] = cpu_baseline(args.config, args.scale, P,
                                                 reps[-1].precond_applications, reps[-1].matvecs)

@@ -112,6 +112,9 @@ struct SolveReport {
   double residual_final = 0.0;
   double inner_iterations = 0.0;  // LR-SPIKE-I: inner half-iterations summed over applies
   index_t inner_solves = 0;
+  // host round trips: transport calls, stream syncs a host-callback transport forced before
+  // them (0 with NcclCommunicator), syncs to read the Krylov scalars
+  index_t comm_calls = 0, comm_host_syncs = 0, scalar_syncs = 0;
 };
 
 /// A CUDA device + stream (lrs_ctx).  The context outlives its matrices and factorizations

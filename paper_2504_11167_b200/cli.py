@@ -87,7 +87,7 @@ def cmd_solve(args) -> int:
     A = api.CsrMatrix(ctx, m.n, m.row_ptr, m.col_idx, m.values)
     k = args.k if args.k else A.band_metrics().k
     cfg = api.SolverConfig(variant=_VARIANTS[args.variant], p=args.p, k=k, n_svd=args.nsvd,
-                           seed=args.seed)
+                           seed=args.seed, spike_mode=args.spike_mode)
     it = api.IterConfig(tol=args.tol, method=args.method, restart=args.restart,
                         max_iters=args.max_iters)
     t0 = time.perf_counter()
@@ -132,6 +132,9 @@ def main(argv=None) -> int:
     s.add_argument("--nsvd", type=int, default=8)
     s.add_argument("--tol", type=float, default=1e-8)
     s.add_argument("--seed", type=int, default=0)
+    s.add_argument("--spike-mode", default="spike", choices=["spike", "coupling"],
+                   help="spike construction: randomized SVD of the spike (SPEC.md:286) or "
+                        "truncated SVD of the coupling blocks (north_star setup (1))")
     s.add_argument("--method", default="bicgstab", choices=["bicgstab", "gmres", "cg"])
     s.add_argument("--restart", type=int, default=30)
     s.add_argument("--max-iters", type=int, default=1000)

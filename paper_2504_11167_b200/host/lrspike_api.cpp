@@ -92,6 +92,9 @@ SolveReport from_c(const lrs_report& r, const std::vector<double>& hist) {
   rep.residual_final = r.residual_final;
   rep.inner_iterations = r.inner_iterations;
   rep.inner_solves = r.inner_solves;
+  rep.comm_calls = r.comm_calls;
+  rep.comm_host_syncs = r.comm_host_syncs;
+  rep.scalar_syncs = r.scalar_syncs;
   return rep;
 }
 
