@@ -14,9 +14,9 @@ do_solve = len(sys.argv) > 3 and sys.argv[3] == "solve"
 P = int(sys.argv[4]) if len(sys.argv) > 4 else None
 ctx = api.Context(0)
 cfg = configs.make_config(name, scale, P)
-A = api.CsrMatrix.from_csr(ctx, cfg.matrix)
+A = api.CsrMatrix.from_csr(ctx, cfg.system(0))  # c5: shift 0 (complex)
 F = api.factorize(ctx, A, api.SolverConfig(p=cfg.P, k=cfg.b, n_svd=cfg.r, seed=cfg.seed))
-f = np.asfortranarray(cfg.rhs)
+f = np.asfortranarray(cfg.rhs.astype(np.complex128) if cfg.shifts else cfg.rhs)
 for _ in range(3):
     x = F.apply_precond_T(f)
 if do_solve:

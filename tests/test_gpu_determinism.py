@@ -47,8 +47,11 @@ def test_repeated_applies_and_solves_bitwise(ctx, name, scale):
     f = np.asfortranarray(configs.vector("uniform", 5, cfg.matrix.n))
     fd = torch.from_numpy(f.T.copy()).cuda().t()
     torch.cuda.synchronize()
-    y0 = F.apply_precond_T(fd).clone()
+    # the library runs on its own stream: wait for it before torch reads the output
+    y0 = F.apply_precond_T(fd)
     ctx.synchronize()
+    y0 = y0.clone()
+    torch.cuda.synchronize()
     for _ in range(100):
         y = F.apply_precond_T(fd)
         ctx.synchronize()
