@@ -237,6 +237,14 @@ void launch_multidot_partition_t(Ctx* c, const Chunks& ch, const S* X, int64_t l
 // out[o] = sum over the gathered per-partition blocks, in global partition order:
 // blocks[rank][p][o] for p < counts[rank], stride pmax * nout per rank (doubles; a complex
 // output is two independent doubles).
+// y = A x on the local chunks (one CTA per chunk) plus the chunk partials of
+// [X^H y, y^H y] (nvec = 2), bit-identical to spmv + launch_multidot_partition_t's partials
+template <class S>
+void launch_spmv_dot2_t(Ctx* c, const Mat* m, const Chunks& ch, const S* x, int64_t ldx, S* y,
+                        int64_t ldy, int nrhs, const S* X, int64_t ldX, S* partial);
+// persum of the chunk partials (the second half of launch_multidot_partition_t)
+void launch_multidot_persum(Ctx* c, const Chunks& ch, int nout, const double* partial,
+                            double* persum);
 void launch_partition_total(Ctx* c, const double* blocks, const int* counts, int nranks,
                             int pmax, int nout, double* out);
 template <class S>

@@ -112,6 +112,15 @@ void launch_multidot_partition_t(Ctx* c, const Chunks& ch, const S* X, int64_t l
   LRS_LAUNCHED(c);
 }
 
+void launch_multidot_persum(Ctx* c, const Chunks& ch, int nout, const double* partial,
+                            double* persum) {
+  if (nout == 0) return;
+  ProfScope ps_(c, K_KRYLOV);
+  multidot_partition_kernel<<<dim3((nout + 127) / 128, ch.Pl), 128, 0, c->stream>>>(
+      ch.part_first, ch.Pl, nout, partial, persum);
+  LRS_LAUNCHED(c);
+}
+
 void launch_partition_total(Ctx* c, const double* blocks, const int* counts, int nranks,
                             int pmax, int nout, double* out) {
   if (nout == 0) return;

@@ -589,6 +589,304 @@ __global__ void __launch_bounds__(I8_THREADS, I8_TN == 128 ? 1 : 2)
   }
 }
 
+// ---- 2-SM bulk update (LRS_I8_2SM=1): tcgen05.mma.cta_group::2, M = 256 ------------------
+// A cluster of two CTAs on one SM pair computes tile rows I0 (rank 0) and I0 + 1 (rank 1)
+// of tile column J: each CTA stages its own 128 rows of the A slices and HALF of the B
+// slices (columns 64 r .. 64 r + 63), the leader's elected thread issues the M = 256, N = 128
+// MMAs for both (the pair's tensor cores exchange the B halves), and each CTA's TMEM holds
+// its 128 rows x 128 columns -- so per SM a K chunk streams 42 KB instead of 56 KB (pass A)
+// and the shared-memory B reads per MMA halve.  Hand-offs: the peer's idle MMA warp relays
+// "stage landed" to the leader (fullp), the leader's commits multicast to both CTAs' empty /
+// tfull barriers, and both CTAs' epilogue warps arrive on the leader's tempty.  The pass
+// structure, digit products, drain order and C reductions are those of lu_i8_gemm_kernel,
+// so the factors are bitwise identical.  An odd last row pair runs a dummy rank-1 half
+// (rows of I0, product discarded).
+#ifndef LRS_I8_2SM_STAGES
+#define LRS_I8_2SM_STAGES 5
+#endif
+constexpr int I8P_BSL = 64 * I8_KC;            // 2 KB: one half B slice of one chunk
+constexpr int I8P_BBLK = I8_S * I8P_BSL;       // 14 KB
+constexpr int I8P_STAGE = I8_BLK + I8P_BBLK;   // 42 KB
+constexpr int I8P_STAGES = LRS_I8_2SM_STAGES;
+constexpr size_t I8P_SMEM = (size_t)I8P_STAGES * I8P_STAGE + 2048;
+static_assert(I8P_SMEM <= 227 * 1024, "2-SM stages");
+constexpr uint32_t I8P_IDESC = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(NB >> 3) << 17) |
+                               ((uint32_t)(2 * NB >> 4) << 24);
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t mapa_rank(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+               : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+template <int COLL>
+__device__ __forceinline__ void umma_i8_2sm(uint32_t d, uint64_t a, uint64_t b, uint32_t acc) {
+#define LRS_UMMA_I8P(Q)                                                                    \
+  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"                          \
+               "tcgen05.mma.cta_group::2.kind::i8" Q " [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d), \
+               "l"(a), "l"(b), "r"(I8P_IDESC), "r"(acc))
+  if (COLL == 0) LRS_UMMA_I8P("");
+  else if (COLL == 1) LRS_UMMA_I8P(".collector::a::fill");
+  else if (COLL == 2) LRS_UMMA_I8P(".collector::a::use");
+  else LRS_UMMA_I8P(".collector::a::lastuse");
+#undef LRS_UMMA_I8P
+}
+// arrive on the barrier at this offset in BOTH CTAs of the pair when the MMAs complete
+__device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 "
+      "[%0], %1;" ::"r"(smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+
+// work item t -> (p, ia, jb) of this rank; false outside the blocks.  own = this rank's
+// rows exist (else it runs the dummy half on row I0).
+template <int STEPS>
+__device__ __forceinline__ bool i8p_decode(const BandGeom& g, int K, int t, int rank, int& p,
+                                           int& ia, int& jb, bool& own) {
+  constexpr int D = STEPS;
+  const int R = g.wl - D, Cn = g.wu - D, per = ((R + 1) / 2) * Cn;
+  p = t / per;
+  const int r = t % per, rp = r / Cn;
+  const int J = K + 2 * D + r % Cn, I0 = K + 2 * D + 2 * rp;
+  const int T = g.T[p];
+  if (I0 >= T || J >= T) return false;
+  own = 2 * rp + rank < R && I0 + rank < T;
+  ia = (own ? I0 + rank : I0) - K - D;
+  jb = J - K - D;
+  return true;
+}
+
+template <int PASS>
+__device__ __forceinline__ void i8p_chunk_mmas(uint32_t tm, uint32_t a0, uint32_t b0, bool first,
+                                               uint64_t* tempty, int ptr, const int* uses) {
+  constexpr int top = i8_top(PASS), ng = i8_ng(PASS), pmax = i8_pmax(PASS);
+#pragma unroll
+  for (int pp = 1; pp <= pmax; ++pp) {
+    const int qhi = min(I8_S, top - pp), qlo = max(1, top - ng + 1 - pp);
+#pragma unroll
+    for (int q = I8_S; q >= 1; --q) {
+      if (q > qhi || q < qlo) continue;
+      const int slot = (ptr + top - pp - q) & (I8_GROUPS - 1);
+      if (first && pp == 1 && uses[slot] > 0) {
+        mbar_wait_trap(&tempty[slot], (uses[slot] - 1) & 1);
+        tc_fence_after();
+      }
+      const uint32_t dd = tm + slot * NB;
+      const uint64_t ad = umma_sdesc(a0 + (pp - 1) * I8_SL, NB * 16, 128);
+      const uint64_t bd = umma_sdesc(b0 + (q - 1) * I8P_BSL, 64 * 16, 128);
+      const uint32_t ac = (first && pp == 1) ? 0u : 1u;
+      if (qhi == qlo) umma_i8_2sm<0>(dd, ad, bd, ac);
+      else if (q == qhi) umma_i8_2sm<1>(dd, ad, bd, ac);
+      else if (q == qlo) umma_i8_2sm<3>(dd, ad, bd, ac);
+      else umma_i8_2sm<2>(dd, ad, bd, ac);
+    }
+  }
+}
+
+template <int STEPS>
+__global__ void __cluster_dims__(2, 1, 1) __maxnreg__(200)
+    lu_i8_gemm2_kernel(BandGeom g, double* tiles, int K, I8Panel pn, int total, int tpc) {
+  static_assert(I8_TN == 128 && I8_NP == 2, "2-SM update: 128-column tiles, two passes");
+  constexpr int NCH = i8_nch(STEPS);
+  constexpr int ST = I8P_STAGES;
+  extern __shared__ __align__(1024) uint8_t smraw[];
+  uint8_t* stage = smraw;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smraw + ST * I8P_STAGE);
+  uint64_t* fullp = full + ST;    // leader: the peer's copy of the stage landed
+  uint64_t* empty = fullp + ST;   // the pair's MMAs finished reading the stage
+  uint64_t* tfull = empty + ST;   // [2]
+  uint64_t* tempty = tfull + 2;   // [I8_GROUPS] leader: both CTAs drained the slot
+  uint32_t* tbase = reinterpret_cast<uint32_t*>(tempty + I8_GROUPS);
+  double* sj = reinterpret_cast<double*>(smraw + ST * I8P_STAGE + 1024);  // [128]
+  const int rank = (int)cluster_rank();
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int t0 = (blockIdx.x >> 1) * tpc, t1 = min(total, t0 + tpc);
+  auto ctile = [&](int p, int ia, int jb) -> double* {
+    const int I = K + STEPS + ia, J = K + STEPS + jb;
+    return tiles + (g.tbase[p] + (int64_t)I * g.W + (J - I + g.wl)) * TILE_ELEMS;
+  };
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < ST; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&fullp[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(&tfull[0], 1);
+    mbar_init(&tfull[1], 1);
+    for (int gi = 0; gi < I8_GROUPS; ++gi) mbar_init(&tempty[gi], 2 * I8_EPI);
+    fence_mbar_init();
+  }
+  if (w == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tbase)), "n"(I8_TMEM)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  cluster_sync_all();  // both CTAs' barriers initialised and TMEM allocated
+  tc_fence_after();
+  const uint32_t tm = *tbase;
+
+  if (w == 0) {
+    // ---- producer (both CTAs): own A rows, own half of the B slices ---------------------
+    if (lane == 0) {
+      int it = 0;
+      for (int t = t0; t < t1; ++t) {
+        int p, ia, jb;
+        bool own;
+        if (!i8p_decode<STEPS>(g, K, t, rank, p, ia, jb, own)) continue;
+        if (own) bulk_prefetch_l2(ctile(p, ia, jb), sizeof(double) * NB * NB);
+        const uint8_t* a = pn.A + ((int64_t)p * g.wl + ia) * NCH * I8_BLK;
+        const uint8_t* b = pn.B + ((int64_t)p * g.wu + jb) * NCH * I8_BBLK + (8 * rank) * 128;
+        for (int pass = 0; pass < I8_NP; ++pass) {
+          const int pm = i8_pmax(pass);
+          for (int kc = 0; kc < NCH; ++kc, ++it) {
+            const int s = it % ST;
+            if (it >= ST) mbar_wait_trap<64>(&empty[s], ((it / ST) & 1) ^ 1);
+            uint8_t* dst = stage + s * I8P_STAGE;
+            mbar_expect_tx(&full[s], pm * (I8_SL + I8P_BSL));
+            bulk_g2s(dst, a + kc * I8_BLK, pm * I8_SL, &full[s]);
+            for (int q = 0; q < pm; ++q)
+#pragma unroll
+              for (int kcore = 0; kcore < 2; ++kcore)
+                bulk_g2s(dst + I8_BLK + q * I8P_BSL + kcore * 1024,
+                         b + kc * I8_BBLK + q * I8_BSL + kcore * (NB / 8) * 128, 1024, &full[s]);
+          }
+        }
+      }
+      // drain: every commit into this CTA's empty barriers has landed before it exits
+      for (int k = (it > ST ? it - ST : 0); k < it; ++k)
+        mbar_wait_trap<64>(&empty[k % ST], (k / ST) & 1);
+    }
+  } else if (w == 1) {
+    if (lane == 0 && rank == 1) {
+      // ---- relay (peer): "my copy of the stage landed" -> the leader's fullp ----------
+      const uint32_t rem0 = mapa_rank(smem_u32(fullp), 0);
+      int it = 0;
+      for (int t = t0; t < t1; ++t) {
+        int p, ia, jb;
+        bool own;
+        if (!i8p_decode<STEPS>(g, K, t, rank, p, ia, jb, own)) continue;
+        for (int pass = 0; pass < I8_NP; ++pass)
+          for (int kc = 0; kc < NCH; ++kc, ++it) {
+            const int s = it % ST;
+            mbar_wait_trap<32>(&full[s], (it / ST) & 1);
+            mbar_arrive_remote(rem0 + s * 8);
+          }
+      }
+    } else if (lane == 0) {
+      // ---- MMA issuer (leader) ---------------------------------------------------------
+      int it = 0, ptr = 0, u = 0;
+      int uses[I8_GROUPS] = {0, 0, 0, 0};
+      for (int t = t0; t < t1; ++t) {
+        int p, ia, jb;
+        bool own;
+        if (!i8p_decode<STEPS>(g, K, t, rank, p, ia, jb, own)) continue;
+#pragma unroll
+        for (int pass = 0; pass < I8_NP; ++pass) {
+          for (int kc = 0; kc < NCH; ++kc, ++it) {
+            const int s = it % ST;
+            mbar_wait_trap(&full[s], (it / ST) & 1);
+            mbar_wait_trap(&fullp[s], (it / ST) & 1);
+            tc_fence_after();
+            const uint32_t a0 = smem_u32(stage + s * I8P_STAGE), b0 = a0 + I8_BLK;
+            if (pass == 0) i8p_chunk_mmas<0>(tm, a0, b0, kc == 0, tempty, ptr, uses);
+            else i8p_chunk_mmas<1>(tm, a0, b0, kc == 0, tempty, ptr, uses);
+            umma_commit_pair(&empty[s]);
+          }
+          umma_commit_pair(&tfull[u & 1]);
+          ++u;
+#pragma unroll
+          for (int gi = 0; gi < i8_ng(pass); ++gi) ++uses[(ptr + gi) & (I8_GROUPS - 1)];
+          ptr = (ptr + i8_ng(pass)) & (I8_GROUPS - 1);
+        }
+      }
+    }
+  } else {
+    // ---- epilogue (both CTAs): drain own TMEM rows, release to the leader, C update ----
+    const int qd = w & 3, ch = (w - 2) >> 2, i = 32 * qd + lane;
+    constexpr double BIAS = 4503601774854144.0;  // 2^52 + 2^31
+    const uint32_t rem_tempty = mapa_rank(smem_u32(tempty), 0);
+    int u = 0, ptr = 0;
+    for (int t = t0; t < t1; ++t) {
+      int p, ia, jb;
+      bool own;
+      if (!i8p_decode<STEPS>(g, K, t, rank, p, ia, jb, own)) continue;
+      double* C = ctile(p, ia, jb) + (int64_t)ch * I8_EPC * NB;
+      const double si = exp2i(pn.ea[((int64_t)p * g.wl + ia) * NB + i]);
+      if (w == 2) {
+        const int* eb = pn.eb + ((int64_t)p * g.wu + jb) * NB;
+#pragma unroll
+        for (int r = 0; r < NB / 32; ++r) sj[lane + 32 * r] = exp2i(eb[lane + 32 * r]);
+      }
+      const uint32_t trow = tm + ((uint32_t)(32 * qd) << 16) + ch * I8_EPC;
+      double acc[I8_EPC];
+#pragma unroll
+      for (int j = 0; j < I8_EPC; ++j) acc[j] = 0.0;
+#pragma unroll
+      for (int pass = 0; pass < I8_NP; ++pass, ++u) {
+        mbar_wait_trap<128>(&tfull[u & 1], (u >> 1) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int gi = 0; gi < i8_ng(pass); ++gi) {
+          const int slot = (ptr + gi) & (I8_GROUPS - 1);
+          const double sc = exp2i(4 - 8 * (i8_top(pass) - gi));
+#pragma unroll
+          for (int h2 = 0; h2 < I8_EPC / 32; ++h2) {
+            uint32_t v[32];
+#pragma unroll
+            for (int c8 = 0; c8 < 32; c8 += 8) tmem_ld8(trow + slot * NB + h2 * 32 + c8, v + c8);
+            tmem_ld_wait();
+            if (h2 == I8_EPC / 32 - 1) {
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) {
+                if (rank == 0) mbar_arrive1(&tempty[slot]);
+                else mbar_arrive_remote(rem_tempty + slot * 8);
+              }
+            }
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              acc[h2 * 32 + j] = fma(
+                  __hiloint2double(0x43300000, (int)(v[j] ^ 0x80000000u)) - BIAS, sc,
+                  acc[h2 * 32 + j]);
+          }
+        }
+        ptr = (ptr + i8_ng(pass)) & (I8_GROUPS - 1);
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(32 * I8_EPI) : "memory");  // sj written
+      if (own) {
+#pragma unroll
+        for (int j = 0; j < I8_EPC; ++j)
+          red_add_f64(C + (int64_t)j * NB + i, -(acc[j] * si * sj[ch * I8_EPC + j]));
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(32 * I8_EPI) : "memory");  // sj free
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();  // no CTA leaves while its peer can still signal its barriers
+  if (w == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tm), "n"(I8_TMEM)
+                 : "memory");
+  }
+}
+
 // ---- INT8 peak (roofline denominator): every SM issues M=128, N=256, K=32 MMAs from
 // resident operands into 2 accumulators (the best-rate shape), 8 K-steps each
 __global__ void __launch_bounds__(128, 1) i8_peak_kernel(int iters, int* out) {
@@ -696,8 +994,39 @@ static void i8_gemm_launch(Ctx* c, cudaStream_t s, const BandGeom& g, double* ti
   LRS_LAUNCHED(c);
 }
 
+template <int STEPS>
+static void i8_gemm2_launch(Ctx* c, cudaStream_t s, const BandGeom& g, double* tiles, int K,
+                            const I8Panel& pn) {
+  static bool attr = false;
+  if (!attr) {
+    LRS_CUDA(cudaFuncSetAttribute(lu_i8_gemm2_kernel<STEPS>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)I8P_SMEM));
+    attr = true;
+  }
+  constexpr int D = STEPS;
+  const int per = ((g.wl - D + 1) / 2) * (g.wu - D);
+  const int total = per * g.P;
+  if (total <= 0) return;
+  static const int tpc = std::getenv("LRS_I8_2SM_TPC") ? std::atoi(std::getenv("LRS_I8_2SM_TPC"))
+                                                        : I8_TPC;
+  const int clusters = (total + tpc - 1) / tpc;
+  lu_i8_gemm2_kernel<STEPS><<<2 * clusters, I8_THREADS, I8P_SMEM, s>>>(g, tiles, K, pn, total,
+                                                                       tpc);
+  LRS_LAUNCHED(c);
+}
+
+bool lu_i8_2sm() {
+  const char* e = std::getenv("LRS_I8_2SM");
+  return e && e[0] == '1';
+}
+
 void launch_lu_i8_gemm(Ctx* c, cudaStream_t s, const BandGeom& g, double* tiles, int K, int kind,
                        int steps, const I8Panel& pn) {
+  if (kind == 4 && lu_i8_2sm()) {
+    if (steps == 4) i8_gemm2_launch<4>(c, s, g, tiles, K, pn);
+    else i8_gemm2_launch<2>(c, s, g, tiles, K, pn);
+    return;
+  }
   if (steps == 4) {
     if (kind == 4) i8_gemm_launch<4, 4>(c, s, g, tiles, K, pn);
     else i8_gemm_launch<3, 4>(c, s, g, tiles, K, pn);

@@ -163,6 +163,12 @@ void halo_exchange(Fact* f, S* x, int64_t ld, int nrhs) {
   if (rk + 1 < f->comm.size) copy_block(c, x + f->row_hi, ld, r_next, hb, hb, nrhs);
 }
 
+// LRS_SPMV_DOT=0: BiCGStab's t = A shat and its omega dots as separate kernels
+bool spmv_dot_unfused() {
+  static const bool off = std::getenv("LRS_SPMV_DOT") && std::getenv("LRS_SPMV_DOT")[0] == '0';
+  return off;
+}
+
 template <class S>
 void spmv_s(Ctx* c, const Mat* m, const S* x, int64_t ldx, S* y, int64_t ldy, int nrhs, int mode,
             const S* b, int64_t ldb, int64_t lo, int64_t hi) {
@@ -1208,14 +1214,31 @@ struct Work {
   std::function<void(const S*, S*)> Mf;            // out = M^-1 in
   std::function<void(S*, S*)> Af;                  // out = A in (halo rows of in may be written)
   std::function<void(const S*, S*, S*)> Rf;        // out = b - A x
+  std::function<void(S*, S*, const S*)> AfD;       // out = A in + chunk partials of [X^H out, out^H out]
   void init() { hbuf = f->ctx->dots_host; }
   Ctx* c() const { return f->ctx; }
   S* dotout() const { return sp<S>(f->dotout); }
   // out[q*nr + j] = X_q[:, j]^H Y[:, j] over ALL rows (partition-ordered, any GPU count)
   void dots(const S* X, int64_t strideX, int nvec, const S* Y, H* out) {
-    const int nout = nvec * nr * SW<S>;  // doubles
     launch_multidot_partition_t<S>(c(), ch, X, n, strideX, nvec, Y, n, nr,
                                    sp<S>(f->partial), sp<S>(f->persum));
+    dots_finish(nvec, out);
+  }
+  // out = A in and [X^H out, out^H out] (BiCGStab's t = A shat with t^H s, t^H t): the
+  // fused SpMV-dot kernel where the operator is the CSR (AfD set), else SpMV + dots
+  void Aop_dots2(S* in, S* out, const S* X, H* res) {
+    if (!AfD) {
+      Aop(in, out);
+      return dots(X, (int64_t)(out - X), 2, out, res);
+    }
+    AfD(in, out, X);
+    rep->matvecs++;
+    launch_multidot_persum(c(), ch, 2 * nr * SW<S>, f->partial.get(), f->persum.get());
+    dots_finish(2, res);
+  }
+  // per-partition sums (persum) -> global partition-ordered totals -> host
+  void dots_finish(int nvec, H* out) {
+    const int nout = nvec * nr * SW<S>;  // doubles
     if (f->dist) {
       if (!f->comm.stream_ordered) {
         LRS_CUDA(cudaStreamSynchronize(c()->stream));
@@ -1390,9 +1413,8 @@ void run_bicgstab(Work<S>& w, const S* b, S* x, const lrs_iter_cfg& cfg, bool ha
     w.push(mx);
     if (!any(act)) break;
     w.M(s, shat);
-    w.Aop(shat, t);
     std::vector<H> st(2 * nr);
-    w.dots(s, (int64_t)blk, 2, t, st.data());  // [s^H t, t^H t] (t follows s in buf)
+    w.Aop_dots2(shat, t, s, st.data());  // t = A shat, [s^H t, t^H t] (t follows s in buf)
     for (int j = 0; j < nr; ++j) {
       const H tt = st[nr + j], ts = hconj(st[j]);
       if (act[j]) omega[j] = ts / (tt != H(0.0) ? tt : H(1.0));
@@ -2027,6 +2049,11 @@ void solve_t(Fact* f, Mat* a, const S* b, int64_t ldb, S* x, int64_t ldx, int nr
       halo_exchange(f, xv, n, nr);
       spmv_s<S>(c, a, xv, n, out, n, nr, 2, bv, n, lo, lo + nl);
     };
+    if (!spmv_dot_unfused())
+      w.AfD = [&](S* in, S* out, const S* X) {
+        halo_exchange(f, in, n, nr);
+        launch_spmv_dot2_t<S>(c, a, w.ch, in, n, out, n, nr, X, n, sp<S>(f->partial));
+      };
     // full-length device copies (ld = n) of this column batch; local rows only
     DevBuf<S> bb, xx;
     bb.alloc((size_t)n * nr);

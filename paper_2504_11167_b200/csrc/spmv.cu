@@ -20,6 +20,9 @@
 
 namespace lrs {
 
+__device__ __forceinline__ double kv_sum(double v) { return warp_sum(v); }
+__device__ __forceinline__ zc kv_sum(zc v) { return warp_sum_z(v); }
+
 template <int NR, class S>
 __global__ void __launch_bounds__(256) spmv_kernel(int64_t n, const int* __restrict__ rp,
                                                    const int* __restrict__ ci,
@@ -151,6 +154,130 @@ void launch_spmv_z(Ctx* c, const Mat* m, const zc* x, int64_t ldx, zc* y, int64_
                    int mode, const zc* b, int64_t ldb, int64_t row_lo, int64_t row_hi) {
   spmv_t<zc>(c, m, x, ldx, y, ldy, nrhs, mode, b, ldb, row_lo, row_hi);
 }
+
+// ---- SpMV with the BiCGStab omega dots in its epilogue --------------------------------
+// y = A x over one deterministic reduction chunk per CTA (the partition-aligned 2048-row
+// chunks of the Krylov dots), then the chunk partials of [X^H y, y^H y] -- the t^H s and
+// t^H t of BiCGStab's omega -- in the SAME per-thread row order and reduction tree as
+// multidot_partial_kernel (krylov.cu): thread tid < 256 chains rows r0 + tid + 256 i in
+// order, then a warp sum and the fixed-order sum over the 8 warps.  The partials are
+// therefore bit-identical to the unfused SpMV + multidot, and one pass over t (and the
+// launch of the dot kernel) disappears.  The SpMV half uses all SPMVD_THREADS threads
+// with the staged coalesced nonzero loads of spmv_staged_kernel; each row's sum is in
+// ascending column order (matrix.cpp:127-136), so y equals the plain SpMV bitwise.
+constexpr int DOT_THREADS = 256;  // KV_THREADS of krylov.cu
+// SpMV threads per CTA: 1024 for one or two columns; wider blocks keep 256 (register budget)
+template <int NR, class S>
+constexpr int spmvd_threads() { return NR * sizeof(S) <= 16 ? 1024 : DOT_THREADS; }
+
+template <int NR, class S>
+__global__ void __launch_bounds__(spmvd_threads<NR, S>()) spmv_dot2_kernel(
+    const int64_t* __restrict__ cstart, const int* __restrict__ rp, const int* __restrict__ ci,
+    const S* __restrict__ va, const S* __restrict__ x, int64_t ldx, S* y, int64_t ldy, int nrhs,
+    const S* X, int64_t ldX, S* __restrict__ partial) {
+  constexpr int SPMVD_THREADS = spmvd_threads<NR, S>();
+  extern __shared__ __align__(16) unsigned char spmv_sm[];
+  S* sv = reinterpret_cast<S*>(spmv_sm);
+  int* sc = reinterpret_cast<int*>(sv + SPMV_CAP);
+  __shared__ S red[DOT_THREADS / 32][NR];
+  const int cidx = blockIdx.x, tid = threadIdx.x;
+  const int64_t c0 = cstart[cidx], c1 = cstart[cidx + 1];
+  for (int64_t r0 = c0; r0 < c1; r0 += SPMVD_THREADS) {
+    const int64_t r1 = r0 + SPMVD_THREADS < c1 ? r0 + SPMVD_THREADS : c1;
+    const int64_t row = r0 + tid;
+    const int q0 = rp[r0], q1 = rp[r1];
+    const int s = row < r1 ? rp[row] : q1, e = row < r1 ? rp[row + 1] : q1;
+    S acc[NR];
+#pragma unroll
+    for (int j = 0; j < NR; ++j) acc[j] = s_zero(S());
+    for (int base = q0; base < q1; base += SPMV_CAP) {
+      const int cnt = q1 - base < SPMV_CAP ? q1 - base : SPMV_CAP;
+      for (int t = tid; t < cnt; t += SPMVD_THREADS) {
+        sv[t] = va[base + t];
+        sc[t] = ci[base + t];
+      }
+      __syncthreads();
+      const int a = s > base ? s : base, z = e < base + cnt ? e : base + cnt;
+      for (int q = a; q < z; ++q) {
+        const S v = sv[q - base];
+        const int64_t col = sc[q - base];
+#pragma unroll
+        for (int j = 0; j < NR; ++j)
+          if (j < nrhs) acc[j] = s_fma(v, x[col + j * ldx], acc[j]);
+      }
+      __syncthreads();
+    }
+    if (row < r1)
+#pragma unroll
+      for (int j = 0; j < NR; ++j)
+        if (j < nrhs) y[row + j * ldy] = acc[j];
+  }
+  __syncthreads();  // the CTA's own y stores are visible to the CTA after the barrier
+  if (tid >= DOT_THREADS) return;
+  const int lane = tid & 31, w = tid >> 5;
+  S d0[NR], d1[NR];
+#pragma unroll
+  for (int j = 0; j < NR; ++j) d0[j] = d1[j] = s_zero(S());
+  for (int64_t row = c0 + tid; row < c1; row += DOT_THREADS) {
+#pragma unroll
+    for (int j = 0; j < NR; ++j) {
+      if (j >= nrhs) break;
+      const S yv = y[row + j * ldy];
+      d0[j] = s_cfma(X[row + j * ldX], yv, d0[j]);
+      d1[j] = s_cfma(yv, yv, d1[j]);
+    }
+  }
+#pragma unroll
+  for (int qq = 0; qq < 2; ++qq) {
+#pragma unroll
+    for (int j = 0; j < NR; ++j) {
+      const S v = kv_sum(qq == 0 ? d0[j] : d1[j]);
+      if (lane == 0) red[w][j] = v;
+    }
+    asm volatile("bar.sync 1, %0;" ::"n"(DOT_THREADS) : "memory");
+    if (tid < nrhs) {
+      S v = s_zero(S());
+      for (int ww = 0; ww < DOT_THREADS / 32; ++ww) v = s_add(v, red[ww][tid]);
+      partial[((int64_t)cidx * 2 + qq) * nrhs + tid] = v;
+    }
+    asm volatile("bar.sync 1, %0;" ::"n"(DOT_THREADS) : "memory");
+  }
+}
+
+template <class S>
+void launch_spmv_dot2_t(Ctx* c, const Mat* m, const Chunks& ch, const S* x, int64_t ldx, S* y,
+                        int64_t ldy, int nrhs, const S* X, int64_t ldX, S* partial) {
+  if (ch.nchunks == 0 || nrhs == 0) return;
+  if (nrhs > MAX_RHS) throw LrsError(LRS_ERR_PARAMETER, "fused SpMV-dot batch > MAX_RHS");
+  const S* va = reinterpret_cast<const S*>(m->vals.get());
+  constexpr size_t smem = (sizeof(S) + sizeof(int)) * SPMV_CAP;
+  {
+    ProfScope ps_(c, K_SPMV);
+#define LRS_SPMVD(NRV)                                                                         \
+  do {                                                                                         \
+    static bool attr_ = false;                                                                 \
+    if (!attr_) {                                                                              \
+      LRS_CUDA(cudaFuncSetAttribute(spmv_dot2_kernel<NRV, S>,                                  \
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));  \
+      attr_ = true;                                                                            \
+    }                                                                                          \
+    spmv_dot2_kernel<NRV, S><<<ch.nchunks, spmvd_threads<NRV, S>(), smem, c->stream>>>(                  \
+        ch.start, m->row_ptr.get(), m->col_idx.get(), va, x, ldx, y, ldy, nrhs, X, ldX,        \
+        partial);                                                                              \
+  } while (0)
+    if (nrhs == 1) LRS_SPMVD(1);
+    else if (nrhs <= 2) LRS_SPMVD(2);
+    else if (nrhs <= 4) LRS_SPMVD(4);
+    else if (nrhs <= 8) LRS_SPMVD(8);
+    else LRS_SPMVD(16);
+#undef LRS_SPMVD
+    LRS_LAUNCHED(c);
+  }
+}
+template void launch_spmv_dot2_t<double>(Ctx*, const Mat*, const Chunks&, const double*, int64_t,
+                                         double*, int64_t, int, const double*, int64_t, double*);
+template void launch_spmv_dot2_t<zc>(Ctx*, const Mat*, const Chunks&, const zc*, int64_t, zc*,
+                                     int64_t, int, const zc*, int64_t, zc*);
 
 // out[dst0 + (row - r0), j] = sum_{col in [c0, c0+b)} A[row, col] * X[col - c0, j]
 // for row in [r0, r0 + b): the coupling block B_i / C_i (or their transposes,

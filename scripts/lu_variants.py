@@ -3,7 +3,7 @@ config R times in its own process; prints the median t_lu / t_factorize (library
 events) and the LU's FP64-equivalent rate.
 
   python scripts/lu_variants.py c3 1.0 64 [R]
-Variants: default, LRS_LU_QUAD=1, and the builds in build/var_*/ (make variant V=...)."""
+Variants: default, LRS_LU_QUAD=1, LRS_I8_2SM=1, both, and the builds in build/var_*/ (make variant V=...)."""
 import glob
 import json
 import os
@@ -42,7 +42,8 @@ if __name__ == "__main__":
     if os.environ.get("LRS_VARIANT_CHILD"):
         print(json.dumps(one(name, scale, P, R)), flush=True)
         sys.exit(0)
-    variants = [("default", {}), ("quad", {"LRS_LU_QUAD": "1"})]
+    variants = [("default", {}), ("quad", {"LRS_LU_QUAD": "1"}), ("2sm", {"LRS_I8_2SM": "1"}),
+                ("quad+2sm", {"LRS_LU_QUAD": "1", "LRS_I8_2SM": "1"})]
     for lib in sorted(glob.glob(os.path.join(ROOT, "build", "var_*", "liblrspike_cuda.so"))):
         variants.append((os.path.basename(os.path.dirname(lib)), {"LRS_LIB": lib}))
     for tag, env in variants:

@@ -14,10 +14,12 @@ from paper_2504_11167_b200.configs import Csr
 pytestmark = pytest.mark.gpu
 
 
-def _factor(ctx, csr, cfg, i8, quad=False):
-    old = {k: os.environ.get(k) for k in ("LRS_LU_I8", "LRS_LU_QUAD")}
+def _factor(ctx, csr, cfg, i8, quad=False, two_sm=None):
+    old = {k: os.environ.get(k) for k in ("LRS_LU_I8", "LRS_LU_QUAD", "LRS_I8_2SM")}
     os.environ["LRS_LU_I8"] = "1" if i8 else "0"
     os.environ["LRS_LU_QUAD"] = "1" if quad else "0"
+    if two_sm is not None:
+        os.environ["LRS_I8_2SM"] = "1" if two_sm else "0"
     try:
         A = api.CsrMatrix.from_csr(ctx, csr)
         return api.factorize(ctx, A, api.SolverConfig(variant="BJ", p=cfg.P, k=cfg.b, n_svd=0))
@@ -40,6 +42,20 @@ def _compare(ctx, csr, cfg, quad=False):
         a, b = F8.tiles(i), F64.tiles(i)
         worst = max(worst, float(np.max(np.abs(a - b)) / np.max(np.abs(b))))
     return worst
+
+
+@pytest.mark.parametrize("name,scale,quad", [("c2", 0.5, False), ("c3", 24 / 96, False),
+                                             ("c4", 0.05, False), ("c2", 0.5, True)])
+def test_int8_2sm_update_bitwise(ctx, name, scale, quad):
+    """The 2-SM bulk update (cta_group::2, M = 256: a CTA pair shares the B slices) forms
+    the same integer products and the same FP64 epilogue as the 1-SM kernel: the factors
+    are bitwise identical, including an odd last row pair (c3 at 24^3: 3 bulk rows)."""
+    cfg = configs.make_config(name, scale)
+    F2 = _factor(ctx, cfg.system(0), cfg, True, quad, two_sm=True)
+    F1 = _factor(ctx, cfg.system(0), cfg, True, quad, two_sm=False)
+    assert F2.info["lu_int8"] == 1
+    for i in range(cfg.P):
+        assert np.array_equal(F2.tiles(i), F1.tiles(i)), i
 
 
 def test_i8_peak_positive(ctx):
