@@ -521,8 +521,8 @@ def run_ours(args):
                     "frac": achieved_tops / i8_peak if i8_peak else None,
                     "peak_source": "in-run INT8 tcgen05 microbenchmark (M=128, N=256, resident "
                                    "operands); nominal dense 4.5 POPS",
-                    # DRAM read + write of one launch from `ncu --set full`
-                    # (profiles/r01b_ncu_lu_i8_gemm.txt): the C tiles' read-modify-write
+                    # DRAM read + write of one (large, K = 20) launch from `ncu --set full`
+                    # (profiles/r02_ncu_summaries.txt): the C tiles' read-modify-write
                     "traffic": _ncu_traffic(f"{args.config}_P{cfg.P}_lu_i8").get("value"),
                     "traffic_source": _ncu_traffic(f"{args.config}_P{cfg.P}_lu_i8").get("source"),
                     "launches": int(upd_n), "avg_launch_ms": avg_launch_s * 1e3,
@@ -661,9 +661,11 @@ def _apply_roofline(kt, reps, info, hbm_peak, peak_src, steps, cfg_key):
             "achieved": gbs, "peak": hbm_peak, "unit": "GB/s", "frac": gbs / hbm_peak,
             "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_src})",
             # DRAM read + write of one apply's two sweeps from `ncu --set full`
-            # (profiles/r01d_ncu_band_solve_apply.txt): 3% above the algorithmic bytes
+            # (profiles/r02_ncu_summaries.txt): 2.6% above the algorithmic bytes
             "traffic": traffic.get("value"), "traffic_source": traffic.get("source"),
             "bytes_per_apply": info["apply_bytes"], "ms_per_apply": per_apply_ms,
+            # the two sweeps alone (the iface / recovery kernels and launch gaps excluded)
+            "sweeps_gbs": info["apply_bytes"] / (ms * 2 / n / 1e3) / 1e9,
             "ms_per_step": per_apply_ms * applies / steps,
             "frac_of_8TBs_nominal": gbs / 8000.0}
 

@@ -297,6 +297,19 @@ __global__ void __launch_bounds__(SVD_THREADS) jacobi_svd_kernel(const SvdJobT<S
     V[e] = (r == c) ? s_real<S>(1.0) : s_zero(S());
   }
   for (int e = tid; e < L2; e += SVD_THREADS) pos[e] = e;
+  // ||R||_F^2: columns below 1e-100 ||R||_F count as converged (zero).  A rank-deficient R
+  // (a collapsed spike) has more columns than its rank, and Jacobi keeps
+  // shrinking the surplus ones pair against pair -- left alone they reach the denormal range,
+  // where the phase cc / |cc| overflowed into NaN.
+  double* fro = sg;  // scratch until the singular values are formed
+  if (w == 0) {
+    double t = 0.0;
+    for (int e = lane; e < L2 * L2; e += 32) t += s_abs2(R[e]);
+    t = warp_sum(t);
+    if (lane == 0) fro[0] = t;
+  }
+  __syncthreads();
+  const double tiny = 1e-200 * fro[0];
   __syncthreads();
   const int npairs = L2 / 2;
   for (int sweep = 0; sweep < 60; ++sweep) {
@@ -318,11 +331,11 @@ __global__ void __launch_bounds__(SVD_THREADS) jacobi_svd_kernel(const SvdJobT<S
         b = warp_sum(b);
         cc = ds_warp_sum(cc);
         const double cabs = s_abs(cc);
-        if (cabs > 1e-15 * sqrt(a * b) && cabs != 0.0) {
+        if (cabs > 1e-15 * sqrt(a * b) && cabs != 0.0 && a > tiny && b > tiny) {
           const double zeta = (b - a) / (2.0 * cabs);
           const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
           const double cs = 1.0 / sqrt(1.0 + t * t), sn = cs * t;
-          const S ph = s_scale(s_conj(cc), 1.0 / cabs);  // q~ = ph q, p^H q~ = |c|
+          const S ph = s_unit_phase(s_conj(cc), cabs);  // q~ = ph q, p^H q~ = |c|
           for (int r = lane; r < L2; r += 32) {
             const S x = R[r + p * L2], y = s_mul(ph, R[r + q * L2]);
             R[r + p * L2] = s_sub(s_scale(x, cs), s_scale(y, sn));

@@ -61,6 +61,9 @@ __host__ __device__ __forceinline__ double s_abs1(double a) { return fabs(a); }
 __host__ __device__ __forceinline__ double s_abs1(zc a) { return fabs(a.x) + fabs(a.y); }
 // |a| and |a|^2
 __host__ __device__ __forceinline__ double s_abs(double a) { return fabs(a); }
+// a / m for m = |a| > 0 without forming 1 / m (which overflows for a denormal m)
+__host__ __device__ __forceinline__ double s_unit_phase(double a, double) { return copysign(1.0, a); }
+__host__ __device__ __forceinline__ zc s_unit_phase(zc a, double m) { return {a.x / m, a.y / m}; }
 __host__ __device__ __forceinline__ double s_abs(zc a) { return hypot(a.x, a.y); }
 __host__ __device__ __forceinline__ double s_abs2(double a) { return a * a; }
 __host__ __device__ __forceinline__ double s_abs2(zc a) { return a.x * a.x + a.y * a.y; }

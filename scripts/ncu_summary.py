@@ -18,6 +18,13 @@ METRICS = [
     "sm__inst_executed_pipe_tensor_subpipe_dmma.avg.pct_of_peak_sustained_active",
     "sm__pipe_tensor_subpipe_imma_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
     "sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
+    "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__pipe_shared_cycles_active.avg.pct_of_peak_sustained_active",
+    "l1tex__data_pipe_tc_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
+    "lts__throughput.avg.pct_of_peak_sustained_elapsed",
+    "gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed",
+    "sm__issue_active.avg.pct_of_peak_sustained_elapsed",
+    "sm__cycles_elapsed.avg.per_second",
     "lts__t_bytes.sum",
     "l1tex__m_xbar2l1tex_read_bytes.sum",
     "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
@@ -26,7 +33,6 @@ METRICS = [
     "launch__grid_size",
     "launch__shared_mem_per_block_dynamic",
     "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum",
-    "lts__t_bytes.sum",
     "smsp__average_warp_latency_issue_stalled_barrier.ratio",
     "smsp__average_warp_latency_issue_stalled_long_scoreboard.ratio",
     "smsp__average_warp_latency_issue_stalled_math_pipe_throttle.ratio",
