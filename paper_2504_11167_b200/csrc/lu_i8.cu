@@ -698,7 +698,7 @@ __device__ __forceinline__ void i8p_chunk_mmas(uint32_t tm, uint32_t a0, uint32_
 }
 
 template <int STEPS>
-__global__ void __cluster_dims__(2, 1, 1) __maxnreg__(200)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8_THREADS, 1)
     lu_i8_gemm2_kernel(BandGeom g, double* tiles, int K, I8Panel pn, int total, int tpc) {
   static_assert(I8_TN == 128 && I8_NP == 2, "2-SM update: 128-column tiles, two passes");
   constexpr int NCH = i8_nch(STEPS);
@@ -820,7 +820,6 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(200)
     // ---- epilogue (both CTAs): drain own TMEM rows, release to the leader, C update ----
     const int qd = w & 3, ch = (w - 2) >> 2, i = 32 * qd + lane;
     constexpr double BIAS = 4503601774854144.0;  // 2^52 + 2^31
-    const uint32_t rem_tempty = mapa_rank(smem_u32(tempty), 0);
     int u = 0, ptr = 0;
     for (int t = t0; t < t1; ++t) {
       int p, ia, jb;
@@ -856,7 +855,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(200)
               __syncwarp();
               if (lane == 0) {
                 if (rank == 0) mbar_arrive1(&tempty[slot]);
-                else mbar_arrive_remote(rem_tempty + slot * 8);
+                else mbar_arrive_remote(mapa_rank(smem_u32(&tempty[slot]), 0));
               }
             }
 #pragma unroll

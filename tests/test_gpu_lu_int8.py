@@ -26,7 +26,7 @@ def _factor(ctx, csr, cfg, i8, quad=False, two_sm=None):
     finally:
         for k, v in old.items():
             if v is None:
-                os.environ.pop(k)
+                os.environ.pop(k, None)
             else:
                 os.environ[k] = v
 
