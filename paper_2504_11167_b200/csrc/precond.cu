@@ -66,6 +66,48 @@ __global__ void __launch_bounds__(IA_THREADS) iface_dots_kernel(const IfaceApply
   }
 }
 
+// One right-hand side (the Krylov hot path): the same partial dots -- per row one product,
+// a warp sum, the 8 warp sums in order, so bitwise the values of iface_dots_kernel -- but
+// every thread loads its IA_AB columns of v at once and the warp sums of all r columns go
+// to shared memory before ONE barrier (iface_dots_kernel waits on a barrier per column, so
+// its v loads run one DRAM round trip at a time).
+constexpr int IA_AB = 16;  // columns of v in flight per thread
+template <class S>
+__global__ void __launch_bounds__(IA_THREADS) iface_dots1_kernel(const IfaceApplyJobT<S>* jobs,
+                                                                 int r, int64_t k, const S* y,
+                                                                 S* part) {
+  extern __shared__ __align__(16) unsigned char ia1_raw[];
+  S* red = reinterpret_cast<S*>(ia1_raw);  // [IA_THREADS / 32][r]
+  const int job = blockIdx.y >> 1, which = blockIdx.y & 1, chunk = blockIdx.x;
+  const int nchunk = gridDim.x;
+  const IfaceApplyJobT<S> jb = jobs[job];
+  if (which == 0 ? !jb.has_left : !jb.has_right) return;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int64_t row = (int64_t)chunk * IA_ROWS + tid;
+  const bool valid = row < k;
+  const S* vt = which ? jb.vtT : jb.vtW;
+  const S yv = valid ? y[(which ? jb.yt_row : jb.yb_row) + row] : s_zero(S());
+  for (int a0 = 0; a0 < r; a0 += IA_AB) {
+    S v[IA_AB];
+#pragma unroll
+    for (int u = 0; u < IA_AB; ++u)
+      v[u] = (valid && a0 + u < r) ? vt[row + (a0 + u) * k] : s_zero(S());
+#pragma unroll
+    for (int u = 0; u < IA_AB; ++u) {
+      if (a0 + u >= r) break;
+      const S sm = warp_sum_s(s_mul(v[u], yv));
+      if (lane == 0) red[w * r + a0 + u] = sm;
+    }
+  }
+  __syncthreads();
+  S* out = part + ((size_t)(job * 2 + which) * nchunk + chunk) * r * MAX_RHS;
+  for (int a = tid; a < r; a += IA_THREADS) {
+    S sm = s_zero(S());
+    for (int q = 0; q < IA_THREADS / 32; ++q) sm = s_add(sm, red[q * r + a]);
+    out[a] = sm;
+  }
+}
+
 // msg[which] = sum over chunks (fixed order) of the local partial messages
 template <class S>
 __global__ void iface_reduce_kernel(const IfaceApplyJobT<S>* jobs, int r, int nrhs, int nchunk,
@@ -144,8 +186,12 @@ void launch_iface_messages_t(Ctx* c, const IfaceApplyJobT<S>* d_jobs, int njobs,
   if (njobs == 0) return;
   const int nchunk = (int)((k + IA_ROWS - 1) / IA_ROWS);
   ProfScope ps_(c, K_IFACE);
-  iface_dots_kernel<S><<<dim3(nchunk, 2 * njobs), IA_THREADS, 0, c->stream>>>(d_jobs, r, k, y, ldy,
-                                                                              nrhs, work);
+  if (nrhs == 1)
+    iface_dots1_kernel<S><<<dim3(nchunk, 2 * njobs), IA_THREADS,
+                            sizeof(S) * (IA_THREADS / 32) * r, c->stream>>>(d_jobs, r, k, y, work);
+  else
+    iface_dots_kernel<S><<<dim3(nchunk, 2 * njobs), IA_THREADS, 0, c->stream>>>(d_jobs, r, k, y,
+                                                                                ldy, nrhs, work);
   LRS_LAUNCHED(c);
   iface_reduce_kernel<S><<<njobs, 128, 0, c->stream>>>(d_jobs, r, nrhs, nchunk, work);
   LRS_LAUNCHED(c);
