@@ -289,6 +289,8 @@ __global__ void __launch_bounds__(SVD_THREADS) jacobi_svd_kernel(const SvdJobT<S
   int* pos = reinterpret_cast<int*>(sg + L2);
   int* order = pos + L2;
   int* rotated = order + L2;
+  S* scr = reinterpret_cast<S*>(ssm_raw + ((sizeof(S) * 2 * L2 * L2 + sizeof(double) * L2 +
+                                            sizeof(int) * (2 * L2 + 1) + 15) & ~size_t(15)));
   const SvdJobT<S> jb = jobs[blockIdx.x];
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, nw = SVD_THREADS / 32;
   for (int e = tid; e < L2 * L2; e += SVD_THREADS) {
@@ -378,13 +380,66 @@ __global__ void __launch_bounds__(SVD_THREADS) jacobi_svd_kernel(const SvdJobT<S
     }
   }
   __syncthreads();
+  // U = R / sigma in place; the null columns (sigma^2 <= tiny: a rank-deficient R, whose
+  // surplus columns took no rotations) get an orthonormal completion instead, in output
+  // order -- as LAPACK's singular vectors of a zero singular value -- so u and v stay
+  // orthonormal and the interface matrices K = vW uT of build_truncated_precond stay
+  // invertible (the spike operators u S v do not depend on the completion).
+  for (int e = tid; e < L2 * l; e += SVD_THREADS) {
+    const int r = e % L2, c = e / L2;
+    if (sg[c] * sg[c] > tiny) R[r + c * L2] = s_scale(R[r + c * L2], 1.0 / sg[c]);
+  }
+  __syncthreads();
+  for (int oc = 0; oc < l; ++oc) {
+    const int src = order[oc];
+    if (sg[src] * sg[src] > tiny) continue;
+    if (w == 0) {  // e_j with the largest residual against the output columns before oc
+      double best = -1.0;
+      int bj = 0;
+      for (int j = lane; j < l; j += 32) {
+        double res = 1.0;
+        for (int q = 0; q < oc; ++q) res -= s_abs2(R[j + order[q] * L2]);
+        if (res > best) { best = res; bj = j; }
+      }
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_down_sync(0xffffffffu, best, o);
+        const int oj = __shfl_down_sync(0xffffffffu, bj, o);
+        if (ob > best || (ob == best && oj < bj)) { best = ob; bj = oj; }
+      }
+      if (lane == 0) *rotated = bj;
+    }
+    __syncthreads();
+    const int jbest = *rotated;
+    S* x = R + src * L2;
+    for (int r = tid; r < L2; r += SVD_THREADS) {  // e_j - U (U^H e_j)
+      S v = (r == jbest) ? s_real<S>(1.0) : s_zero(S());
+      for (int q = 0; q < oc; ++q)
+        v = s_sub(v, s_mul(R[r + order[q] * L2], s_conj(R[jbest + order[q] * L2])));
+      x[r] = r < l ? v : s_zero(S());
+    }
+    __syncthreads();
+    for (int q = tid; q < oc; q += SVD_THREADS) {  // second Gram-Schmidt pass: coefficients
+      S cq = s_zero(S());
+      for (int r = 0; r < l; ++r) cq = s_cfma(R[r + order[q] * L2], x[r], cq);
+      scr[q] = cq;
+    }
+    __syncthreads();
+    double nrm = 0.0;
+    for (int r = tid; r < l; r += SVD_THREADS) {
+      S v = x[r];
+      for (int q = 0; q < oc; ++q) v = s_sub(v, s_mul(R[r + order[q] * L2], scr[q]));
+      x[r] = v;
+      nrm += s_abs2(v);
+    }
+    nrm = block_sum(nrm, reinterpret_cast<double*>(scr));
+    for (int r = tid; r < l; r += SVD_THREADS) x[r] = s_scale(x[r], 1.0 / sqrt(nrm));
+    __syncthreads();
+  }
   for (int e = tid; e < l * l; e += SVD_THREADS) {
     const int r = e % l, c = e / l;
     const int src = order[c];
-    const double s = sg[src];
     jb.V[r + c * l] = V[r + src * L2];
-    jb.U[r + c * l] = s > 0.0 ? s_scale(R[r + src * L2], 1.0 / s)
-                              : (r == c ? s_real<S>(1.0) : s_zero(S()));
+    jb.U[r + c * l] = R[r + src * L2];
   }
   for (int c = tid; c < l; c += SVD_THREADS) jb.sigma[c] = sg[order[c]];
 }
@@ -394,7 +449,8 @@ void launch_jacobi_svd_t(Ctx* c, const SvdJobT<S>* d_jobs, int njobs, int l) {
   if (njobs == 0) return;
   if (l > SVD_MAXL) throw LrsError(LRS_ERR_PARAMETER, "n_svd + oversample > 96 not supported");
   const int L2 = (l + 1) & ~1;
-  const size_t smem = sizeof(S) * 2 * L2 * L2 + sizeof(double) * L2 + sizeof(int) * (2 * L2 + 1);
+  const size_t smem = ((sizeof(S) * 2 * L2 * L2 + sizeof(double) * L2 + sizeof(int) * (2 * L2 + 1) +
+                       15) & ~size_t(15)) + sizeof(S) * L2 + sizeof(double) * 32;
   if (smem > 227 * 1024)  // complex: l <= 84
     throw LrsError(LRS_ERR_PARAMETER, "n_svd + oversample too large for the shared-memory SVD");
   static size_t attr = 0;
