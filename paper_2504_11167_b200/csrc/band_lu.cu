@@ -848,15 +848,24 @@ static bool lu_i8_wanted(const BandGeom& g, const LuKernels& L, int steps) {
   if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) return false;
   return 2 * lu_i8_panel_bytes(g, steps) < fr / 4;
 }
-// LRS_LU_QUAD=1: the INT8 bulk update runs four steps (K = 512) per launch (band >= 8 tiles
-// each side): the bulk gets 29% faster per step (c2: 68.6 ms for 63 launches vs 96.4 ms for
-// 128), but the look-ahead inside the quad (DMMA, 6 tile-steps per column of the band per
-// quad instead of 2 per pair) and the wider INT8 look-ahead put more work on the critical
-// stream: c2 LU 0.179 s vs 0.157 s with pairs, so pairs stay the default.
-static int lu_i8_steps(const BandGeom& g) {
+// Quads: the INT8 bulk update runs four steps (K = 512) per launch (band >= 8 tiles each
+// side), half the C traffic, TMEM drains and pass hand-offs per MMA, but the look-ahead
+// inside the quad (DMMA, 6 tile-steps per column of the band per quad instead of 2 per
+// pair) and four serial diagonal factorizations per quad lengthen the critical stream.
+// They pay when the bulk launch is large against that chain: measured (profiles/
+// r02_lu_variants_*.jsonl) c3 at P = 64 (305k tiles per quad launch, 2060 per SM) LU
+// 1.167 s vs 1.237 s with pairs; c2 (6.3k tiles, 42 per SM) 0.162 s vs 0.152 s.  So quads
+// when the first bulk launch holds >= LRS_QUAD_TILES_PER_SM (200) tiles per SM;
+// LRS_LU_QUAD=0 / 1 forces pairs / quads.
+static int lu_i8_steps(const BandGeom& g, int num_sms) {
+  if (!(g.wl >= 8 && g.wu >= 8)) return 2;
   const char* e = std::getenv("LRS_LU_QUAD");
-  if (!(e && e[0] == '1')) return 2;
-  return (g.wl >= 8 && g.wu >= 8) ? 4 : 2;
+  if (e && e[0] == '1') return 4;
+  if (e && e[0] == '0') return 2;
+  const char* t = std::getenv("LRS_QUAD_TILES_PER_SM");
+  const double per_sm = t ? std::atof(t) : 200.0;
+  const double tiles = (double)g.P * (g.wl - 4) * (g.wu - 4);
+  return tiles >= per_sm * num_sms ? 4 : 2;
 }
 
 int launch_band_lu(Ctx* c, const BandGeom& g, double* tiles, int Tmax, int* status) {
@@ -864,7 +873,7 @@ int launch_band_lu(Ctx* c, const BandGeom& g, double* tiles, int Tmax, int* stat
   LuKernels L{real_diag, real_gemm, LRS_LU_PAIRS != 0};
   DevBuf<uint8_t> buf;
   I8Panel pn[2];
-  const int steps = lu_i8_steps(g);
+  const int steps = lu_i8_steps(g, c->num_sms);
   if (lu_i8_wanted(g, L, steps)) {
     auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
     const size_t a = al((size_t)g.P * g.wl * TILE_ELEMS * steps * 8),
