@@ -35,7 +35,6 @@ __global__ void __launch_bounds__(KV_THREADS) multidot_partial_kernel(
     for (int qq = 0; qq < QB; ++qq)
 #pragma unroll
       for (int j = 0; j < NR; ++j) acc[qq][j] = s_zero(S());
-#pragma unroll (NR == 1 ? 4 : 1)
     for (int64_t row = r0 + tid; row < r1; row += KV_THREADS) {
       S y[NR];
 #pragma unroll
@@ -191,7 +190,6 @@ __global__ void __launch_bounds__(KV_THREADS) multi_axpy_kernel(int64_t n, int n
   if (row >= n) return;
   for (int j = 0; j < nrhs; ++j) {
     S s = s_zero(S());
-#pragma unroll 8
     for (int q = 0; q < nvec; ++q) s = s_fma(V[q * strideV + row + j * ldv], y[q * nrhs + j], s);
     x[row + j * ldx] = s_add(x[row + j * ldx], s_scale(s, sign));
   }
