@@ -222,6 +222,11 @@ using ColScal = ColScalT<double>;
 // product is summed per chunk in a fixed tree, per partition over its chunks in order,
 // then over the GLOBAL partitions in order -- the same sequence of floating-point
 // additions for any number of GPUs.
+// Rows per deterministic reduction chunk of the Krylov dot products (partition aligned):
+// one CTA of the partial-dot kernels per chunk.  512 rows -- 2 rows per thread -- keeps
+// ~1.7k CTAs in flight on c3 (n = 884,736); with 2048-row chunks the 432 CTAs of a dot ran
+// latency-bound at ~2.5x the HBM time.
+constexpr int64_t KRYLOV_CHUNK = 512;
 struct Chunks {
   const int64_t* start;  // [nchunks+1] global row boundaries of the local chunks
   const int* part_first; // [Pl+1] first chunk of each local partition

@@ -957,7 +957,7 @@ Fact* factorize(Ctx* c, Mat* m, const lrs_solver_cfg& cfg, const lrs_comm* comm)
   setup_tiles(f->ku);
   // deterministic reduction chunks, partition aligned
   {
-    const int64_t CH = 2048;
+    const int64_t CH = KRYLOV_CHUNK;
     f->chunk_start.clear();
     f->part_first.assign(P + 1, 0);
     for (int i = 0; i < P; ++i) {
@@ -2161,7 +2161,7 @@ void krylov_ops_t(Ctx* c, int64_t n, const lrs_operator& A, const lrs_operator* 
   f->rank_pl.assign(1, 1);
   f->pl_max = 1;
   upload(c, f->d_rank_pl, f->rank_pl);
-  const int64_t CH = 2048;
+  const int64_t CH = KRYLOV_CHUNK;
   for (int64_t r0 = 0; r0 < n; r0 += CH) f->chunk_start.push_back(r0);
   f->part_first = {0, (int)f->chunk_start.size()};
   f->chunk_start.push_back(n);
