@@ -235,6 +235,14 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1)
     }
   }
 
+  // multi-RHS sweeps: x_s of the NEXT dependency is loaded into registers while the chunks
+  // of the current one run (when its ready flag is already up -- always, except for the last
+  // few dependencies), so the 128 x NR load from L2 leaves the per-dependency critical path
+  constexpr int XPT = (MMA && !LLM) ? NB * NR / SOLVE_THREADS : 1;
+  static_assert(!MMA || (NB * NR) % SOLVE_THREADS == 0, "x prefetch split");
+  double xpre[XPT];
+  bool have_pre = false;
+  int* s_ready = s_tk;  // the ticket slot is free once every thread has read it
   for (int q = 0; q < Q; ++q) {
     const int d = q / NCH, sub = q % NCH, st = q % STAGES;
     const bool diag = (d == ndeps);
@@ -242,7 +250,39 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1)
       if (!diag) {
         const int s = s0 + d * sstep;
         if (d == ndeps - 1) STRACE(1);
-        if (LLM) {
+        if (!LLM && MMA) {
+          if (have_pre) {
+#pragma unroll
+            for (int i = 0; i < XPT; ++i) {
+              const int e = tid + i * SOLVE_THREADS;
+              xs[(e % NB) * XLD + e / NB] = xpre[i];
+            }
+          } else {
+            if (tid == 0) {
+              const unsigned* f = flags + g.fbase[p] + s;
+              while (ld_acquire_u32(f) != epoch) __nanosleep(32);
+            }
+            __syncthreads();
+            const int64_t srow0 = (int64_t)s * NB;
+            for (int e = tid; e < NB * NR; e += SOLVE_THREADS) {
+              const int r = e % NB, j = e / NB;
+              xs[r * XLD + j] = (j < nrhs && srow0 + r < size) ? __ldcg(x + off + srow0 + r + j * ld) : 0.0;
+            }
+          }
+          if (tid == 0)
+            *s_ready = d + 1 < ndeps && ld_acquire_u32(flags + g.fbase[p] + s + sstep) == epoch;
+          __syncthreads();
+          have_pre = *s_ready != 0;
+          if (have_pre) {
+            const int64_t srow0 = (int64_t)(s + sstep) * NB;
+#pragma unroll
+            for (int i = 0; i < XPT; ++i) {
+              const int e = tid + i * SOLVE_THREADS;
+              const int r = e % NB, j = e / NB;
+              xpre[i] = (j < nrhs && srow0 + r < size) ? __ldcg(x + off + srow0 + r + j * ld) : 0.0;
+            }
+          }
+        } else if (LLM) {
           const unsigned long long* mb = mbox + (size_t)(g.fbase[p] + s) * (2 * NB) + tid;
           unsigned long long v = ld_relaxed_u64(mb);
           while ((unsigned)(v >> 32) != epoch) {

@@ -137,27 +137,55 @@ __global__ void __launch_bounds__(ZS_THREADS, 1)
       red[r * XLD + j] = (j < nrhs && row0 + r < size) ? x[off + row0 + r + j * ld] : zc{0.0, 0.0};
     }
   }
+  // x_s of the next dependency is loaded into registers while the current one's chunks run
+  // (when its flag is already up), as in band_solve_kernel
+  constexpr int XPT = NB * NR / ZS_THREADS;
+  static_assert((NB * NR) % ZS_THREADS == 0, "x prefetch split");
+  zc xpre[XPT];
+  bool have_pre = false;
+  int* s_ready = s_tk;  // free once every thread has read its ticket
+  auto load_x = [&](int sdep, int i) -> zc {
+    const int e = tid + i * ZS_THREADS;
+    const int r = e % NB, j = e / NB;
+    const int64_t srow0 = (int64_t)sdep * NB;
+    zc v = {0.0, 0.0};
+    if (j < nrhs && srow0 + r < size) {
+      const double2 raw = __ldcg(reinterpret_cast<const double2*>(x + off + srow0 + r + j * ld));
+      v = {raw.x, raw.y};
+    }
+    return v;
+  };
   for (int q = 0; q < Q; ++q) {
     const int d = q / ZNCH, sub = q % ZNCH, st = q % ZSTAGES;
     const bool diag = (d == ndeps);
     if (sub == 0) {
       if (!diag) {
         const int s = s0 + d * sstep;
-        if (tid == 0) {
-          const unsigned* f = flags + g.fbase[p] + s;
-          while (ld_acquire_u32(f) != epoch) __nanosleep(32);
-        }
-        __syncthreads();
-        const int64_t srow0 = (int64_t)s * NB;
-        for (int e = tid; e < NB * NR; e += ZS_THREADS) {
-          const int r = e % NB, j = e / NB;
-          zc v = {0.0, 0.0};
-          if (j < nrhs && srow0 + r < size) {
-            const double2 raw = __ldcg(reinterpret_cast<const double2*>(x + off + srow0 + r + j * ld));
-            v = {raw.x, raw.y};
+        if (have_pre) {
+#pragma unroll
+          for (int i = 0; i < XPT; ++i) {
+            const int e = tid + i * ZS_THREADS;
+            xs[(e % NB) * XLD + e / NB] = xpre[i];
           }
-          xs[r * XLD + j] = v;
+        } else {
+          if (tid == 0) {
+            const unsigned* f = flags + g.fbase[p] + s;
+            while (ld_acquire_u32(f) != epoch) __nanosleep(32);
+          }
+          __syncthreads();
+#pragma unroll
+          for (int i = 0; i < XPT; ++i) {
+            const int e = tid + i * ZS_THREADS;
+            xs[(e % NB) * XLD + e / NB] = load_x(s, i);
+          }
         }
+        if (tid == 0)
+          *s_ready = d + 1 < ndeps && ld_acquire_u32(flags + g.fbase[p] + s + sstep) == epoch;
+        __syncthreads();
+        have_pre = *s_ready != 0;
+        if (have_pre)
+#pragma unroll
+          for (int i = 0; i < XPT; ++i) xpre[i] = load_x(s + sstep, i);
       } else {
         if (!TRANS) {
 #pragma unroll
