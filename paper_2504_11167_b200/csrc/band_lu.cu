@@ -839,14 +839,18 @@ bool lu_real_pairs(const BandGeom& g) {
 
 // The two-step updates (kinds 3 / 4) run integer-sliced on the INT8 tensor cores (lu_i8.cu)
 // unless LRS_LU_I8=0, the band is too narrow for the pair schedule, or the two panel
-// buffers would take more than a quarter of the free device memory.
-static bool lu_i8_wanted(const BandGeom& g, const LuKernels& L, int steps) {
-  const char* e = std::getenv("LRS_LU_I8");
-  if (e && e[0] == '0') return false;
-  if (!lu_uses_pairs(g, L)) return false;
+// buffers do not fit the free device memory (driver free + the pool's cached blocks, which
+// an allocation releases on failure) with 2 GB to spare.
+static bool lu_i8_fits(const BandGeom& g, int steps) {
   size_t fr = 0, tot = 0;
   if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) return false;
-  return 2 * lu_i8_panel_bytes(g, steps) < fr / 4;
+  const size_t avail = fr + pool_cached_bytes(), margin = size_t(2) << 30;
+  return avail > margin && 2 * lu_i8_panel_bytes(g, steps) < avail - margin;
+}
+static bool lu_i8_wanted(const BandGeom& g, const LuKernels& L) {
+  const char* e = std::getenv("LRS_LU_I8");
+  if (e && e[0] == '0') return false;
+  return lu_uses_pairs(g, L);
 }
 // Quads: the INT8 bulk update runs four steps (K = 512) per launch (band >= 8 tiles each
 // side), half the C traffic, TMEM drains and pass hand-offs per MMA, but the look-ahead
@@ -873,8 +877,9 @@ int launch_band_lu(Ctx* c, const BandGeom& g, double* tiles, int Tmax, int* stat
   LuKernels L{real_diag, real_gemm, LRS_LU_PAIRS != 0};
   DevBuf<uint8_t> buf;
   I8Panel pn[2];
-  const int steps = lu_i8_steps(g, c->num_sms);
-  if (lu_i8_wanted(g, L, steps)) {
+  int steps = lu_i8_steps(g, c->num_sms);
+  if (steps == 4 && !lu_i8_fits(g, 4)) steps = 2;
+  if (lu_i8_wanted(g, L) && lu_i8_fits(g, steps)) {
     auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
     const size_t a = al((size_t)g.P * g.wl * TILE_ELEMS * steps * 8),
                  b = al((size_t)g.P * g.wu * TILE_ELEMS * steps * 8),
