@@ -106,12 +106,28 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #endif
 
 
+// the int slot after the barriers: the CTA's ticket (then the x-prefetch "ready" word)
 template <int MODE, int NR>
-__global__ void __launch_bounds__(SOLVE_THREADS, 1)
-    band_solve_kernel(BandGeom g, const double* __restrict__ tiles, double* x, int64_t ld,
-                      int nrhs, unsigned* flags, unsigned epoch, int* ticket, int p_only,
-                      int ngroups, int64_t flag_stride, const float* __restrict__ t32,
-                      unsigned long long* mbox) {
+__device__ __forceinline__ int* solve_ticket_slot(unsigned char* smraw) {
+  using Cfg = SolveCfg<MODE, NR>;
+  return reinterpret_cast<int*>(smraw + sizeof(double) * ((size_t)Cfg::STAGES * CH_SM + Cfg::DREG +
+                                                          (size_t)NB * Cfg::XLD + Cfg::RED +
+                                                          Cfg::PART) +
+                                8 * (Cfg::STAGES + 1));
+}
+
+// One CTA of a sweep: ticket tk0 (taken by the caller).  FUSED_U: the U sweep of the fused
+// one-RHS L + U launch -- tile t's right-hand side comes from the L sweep's mailbox words of
+// tile t (epoch epoch_l: the values the L sweep also stores into x), so the U CTAs need no
+// kernel boundary after the L sweep.
+template <int MODE, int NR, bool FUSED_U = false>
+__device__ __forceinline__ void band_solve_body(BandGeom g, const double* __restrict__ tiles,
+                                                double* x, int64_t ld, int nrhs, unsigned* flags,
+                                                unsigned epoch, int p_only, int ngroups,
+                                                int64_t flag_stride,
+                                                const float* __restrict__ t32,
+                                                unsigned long long* mbox, const int tk0,
+                                                unsigned epoch_l) {
   using Cfg = SolveCfg<MODE, NR>;
   constexpr int STAGES = Cfg::STAGES;
   constexpr int XLD = Cfg::XLD;
@@ -131,9 +147,6 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1)
   int* s_tk = reinterpret_cast<int*>(bars + STAGES + 1);
 
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  if (tid == 0) *s_tk = atomicAdd(ticket, 1);
-  __syncthreads();
-  const int tk0 = *s_tk;
   STRACE(0);
   // column group (adjacent tickets: the groups of one row tile start together)
   const int grp = tk0 % ngroups, tk = tk0 / ngroups;
@@ -212,7 +225,19 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1)
 #pragma unroll
     for (int nj = 0; nj < NJ; ++nj) acc[mi][nj][0] = acc[mi][nj][1] = 0.0;
   if (!TRANS) {
-    if (!MMA) {
+    if (FUSED_U) {
+      static_assert(!FUSED_U || (LLM && MODE == 1), "fused U sweep: one-RHS mailbox path");
+      const unsigned long long* mb = mbox + (size_t)(g.fbase[p] + t) * (2 * NB) + tid;
+      unsigned long long v = ld_relaxed_u64(mb);
+      while ((unsigned)(v >> 32) != epoch_l) {
+        __nanosleep(16);
+        v = ld_relaxed_u64(mb);
+      }
+      reinterpret_cast<unsigned*>(xs)[tid] = (unsigned)v;
+      __syncthreads();
+      if (hh == 0 && row0 + row < size && nrhs > 0) acc1 = xs[row];
+      __syncthreads();  // xs is rewritten by the first dependency's poll
+    } else if (!MMA) {
       if (hh == 0 && row0 + row < size && nrhs > 0) acc1 = x[off + row0 + row];
     } else {
 #pragma unroll
@@ -515,6 +540,61 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1)
     g_strace[(size_t)tk0 * 8 + 7] = grp;
   }
 #endif
+}
+
+template <int MODE, int NR>
+__global__ void __launch_bounds__(SOLVE_THREADS, 1)
+    band_solve_kernel(BandGeom g, const double* __restrict__ tiles, double* x, int64_t ld,
+                      int nrhs, unsigned* flags, unsigned epoch, int* ticket, int p_only,
+                      int ngroups, int64_t flag_stride, const float* __restrict__ t32,
+                      unsigned long long* mbox) {
+  extern __shared__ __align__(128) unsigned char smraw[];
+  int* s_tk = solve_ticket_slot<MODE, NR>(smraw);
+  if (threadIdx.x == 0) *s_tk = atomicAdd(ticket, 1);
+  __syncthreads();
+  const int tk0 = *s_tk;
+  band_solve_body<MODE, NR>(g, tiles, x, ld, nrhs, flags, epoch, p_only, ngroups, flag_stride,
+                            t32, mbox, tk0, 0u);
+}
+
+// The one-RHS apply's L and U sweeps in ONE launch: tickets [0, ntiles) are the L sweep's
+// CTAs, [ntiles, 2 ntiles) the U sweep's.  Every wait targets a CTA with a smaller ticket
+// (an L CTA, or an earlier U tile), which has started, so there is no deadlock for any
+// residency; the SMs stream the U sweep's factor panels while the L sweep drains instead of
+// idling across a kernel boundary.
+__global__ void __launch_bounds__(SOLVE_THREADS, 1)
+    band_solve_lu1_kernel(BandGeom g, const double* __restrict__ tiles, double* x, int64_t ld,
+                          int nrhs, unsigned epoch_l, unsigned epoch_u, int* ticket, int ntiles,
+                          const float* __restrict__ t32, unsigned long long* mbox) {
+  extern __shared__ __align__(128) unsigned char smraw[];
+  static_assert(solve_smem_bytes<0, 1>() == solve_smem_bytes<1, 1>(), "one shared-memory plan");
+  int* s_tk = solve_ticket_slot<0, 1>(smraw);
+  if (threadIdx.x == 0) *s_tk = atomicAdd(ticket, 1);
+  __syncthreads();
+  const int tk0 = *s_tk;
+  if (tk0 < ntiles)
+    band_solve_body<0, 1>(g, tiles, x, ld, nrhs, nullptr, epoch_l, -1, 1, 0, t32, mbox, tk0, 0u);
+  else
+    band_solve_body<1, 1, true>(g, tiles, x, ld, nrhs, nullptr, epoch_u, -1, 1, 0, t32, mbox,
+                                tk0 - ntiles, epoch_l);
+}
+
+void launch_band_solve_lu1(Ctx* c, const BandGeom& g, const double* tiles, double* x,
+                           int64_t ld, unsigned epoch_l, unsigned epoch_u, int* ticket,
+                           int ntiles, const float* t32, unsigned long long* mb) {
+  if (ntiles == 0) return;
+  static bool attr = false;
+  constexpr size_t smem = solve_smem_bytes<0, 1>();
+  if (!attr) {
+    LRS_CUDA(cudaFuncSetAttribute(band_solve_lu1_kernel,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  LRS_CUDA(cudaMemsetAsync(ticket, 0, sizeof(int), c->stream));
+  ProfScope ps_(c, K_SOLVE);
+  band_solve_lu1_kernel<<<2 * ntiles, SOLVE_THREADS, smem, c->stream>>>(
+      g, tiles, x, ld, 1, epoch_l, epoch_u, ticket, ntiles, t32, mb);
+  LRS_LAUNCHED(c);
 }
 
 template <int MODE, int NR>

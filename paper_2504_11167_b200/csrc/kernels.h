@@ -105,6 +105,11 @@ void launch_extract_tiles_z(Ctx* c, const Mat* m, const BandGeom& g, zc* tiles, 
 // flags: SOLVE_GROUPS x flag_stride ready flags (one set per 16-column group).
 // t32: FP32 copy of the tiles (off-diagonal tiles read from it in modes 0 / 1) or null.
 // mbox: [flag_stride][2 NB] zero-initialised handoff words of the one-RHS L / U sweeps
+// The one-RHS L then U sweeps of the apply in one launch (band_solve_lu1_kernel): real,
+// no interchanges, all local partitions; epochs epoch_l < epoch_u fresh for this apply.
+void launch_band_solve_lu1(Ctx* c, const BandGeom& g, const double* tiles, double* x,
+                           int64_t ld, unsigned epoch_l, unsigned epoch_u, int* ticket,
+                           int ntiles, const float* t32, unsigned long long* mb);
 void launch_band_solve(Ctx* c, const BandGeom& g, const double* tiles, int mode, double* x,
                        int64_t ld, int nrhs, unsigned* flags, unsigned epoch, int* ticket,
                        int p_only, int ntiles, int64_t flag_stride, const float* t32,

@@ -185,6 +185,18 @@ void dstage_t(Fact* f, S* x, int64_t ld, int nrhs, bool adjoint, int p_only) {
   const BandGeom g = f->geom();
   const int ntiles = p_only >= 0 ? f->T[p_only] : (int)f->total_rowtiles;
   constexpr int MAXR = IsC<S>::value ? ZSOLVE_MAX_RHS : SOLVE_MAX_RHS;
+  if constexpr (!IsC<S>::value) {
+    // the apply's one-RHS L + U sweeps as one launch (LRS_SOLVE_FUSED=0: two launches)
+    static const bool fused = !(std::getenv("LRS_SOLVE_FUSED") &&
+                                std::getenv("LRS_SOLVE_FUSED")[0] == '0');
+    if (fused && nrhs == 1 && !adjoint && !f->pivoted && p_only < 0 && f->ctx->solve_fma1) {
+      const unsigned el = f->next_epoch(), eu = f->next_epoch();
+      launch_band_solve_lu1(f->ctx, g, f->tiles.get(), x, ld, el, eu, f->ticket.get(), ntiles,
+                            (f->fp32 && !f->ctx->in_setup) ? f->tiles32.get() : nullptr,
+                            f->mbox.get());
+      return;
+    }
+  }
   for (int c0 = 0; c0 < nrhs; c0 += MAXR) {
     const int nr = std::min(MAXR, nrhs - c0);
     S* xc = x + (int64_t)c0 * ld;

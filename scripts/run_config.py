@@ -3,7 +3,8 @@
   python scripts/run_config.py c3 [scale] [P] [shift]
 
 The apply is timed on device-resident blocks of all RHS columns (CUDA events through
-ctx.synchronize), with the per-kernel-class profile of one apply.
+ctx.synchronize), with the per-kernel-class profile of one apply.  nvidia-smi clocks and
+throttle reasons are sampled for the whole run (bench.ClockSampler) and reported as "clocks".
 """
 import json
 import os
@@ -13,6 +14,7 @@ import time
 import numpy as np
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from bench import ClockSampler  # noqa: E402
 from paper_2504_11167_b200 import api, configs  # noqa: E402
 
 name = sys.argv[1]
@@ -28,6 +30,7 @@ A = api.CsrMatrix.from_csr(ctx, cfg.system(shift))
 tup = time.perf_counter() - t0
 out = {"config": name, "scale": scale, "n": cfg.matrix.n, "nnz": cfg.matrix.nnz, "b": cfg.b,
        "P": cfg.P, "r": cfg.r, "method": cfg.method, "t_gen": tgen, "t_upload": tup}
+clk = ClockSampler(0).__enter__()
 try:
     t0 = time.perf_counter()
     F = api.factorize(ctx, A, api.SolverConfig(p=cfg.P, k=cfg.b, n_svd=cfg.r, seed=cfg.seed))
@@ -69,4 +72,7 @@ try:
                 "precond_applications": rep.precond_applications})
 except api.Error as e:
     out["error"] = f"{type(e).__name__}: {e}"
+finally:
+    clk.__exit__(None, None, None)
+out["clocks"] = clk.summary()
 print(json.dumps(out), flush=True)
