@@ -582,15 +582,49 @@ __global__ void __launch_bounds__(IF_THREADS) iface_setup_kernel(const IfaceSetu
   const IfaceSetupJobT<S> jb = jobs[blockIdx.x];
   const int tid = threadIdx.x;
   // K[a][c] = sum_row vtW[row, a] uTb[row, c];  E[a][c] = sum_row vtT[row, a] uWt[row, c]
-  for (int e = tid; e < 2 * r * r; e += IF_THREADS) {
-    const int which = e / (r * r), ac = e % (r * r);
-    const int a = ac % r, c = ac / r;
-    const S* vt = which ? jb.vtT : jb.vtW;
-    const S* u = which ? jb.uWt : jb.uTb;
-    const int64_t ldu = which ? jb.ld_uW : jb.ld_uT;
-    S s = s_zero(S());
-    for (int64_t row = 0; row < k; ++row) s = s_fma(vt[row + a * k], u[row + c * ldu], s);
-    (which ? Es : Ks)[a + c * r] = s;
+  // The k rows stream through shared memory in tiles of KT rows (coalesced column reads;
+  // the staging area is M, free until the inverses), IF_ACC entries per thread per pass;
+  // each entry still sums its rows in ascending order.
+  {
+    constexpr int IF_ACC = 8;
+    const int KT = r >= 2 ? min(16, r / 2) : 1;
+    S* st = r >= 2 ? M : M + 2 * r * r;  // [4][KT][r]: vtW, uTb, vtT, uWt rows
+    for (int e0 = 0; e0 < 2 * r * r; e0 += IF_THREADS * IF_ACC) {
+      S acc[IF_ACC];
+#pragma unroll
+      for (int j = 0; j < IF_ACC; ++j) acc[j] = s_zero(S());
+      for (int64_t r0 = 0; r0 < k; r0 += KT) {
+        const int kt = (int)(k - r0 < KT ? k - r0 : KT);
+        __syncthreads();
+        for (int xx = tid; xx < 4 * KT * r; xx += IF_THREADS) {
+          const int which = xx / (KT * r), rem = xx % (KT * r), col = rem / KT, rr = rem % KT;
+          const S* src = which == 0   ? jb.vtW + (int64_t)col * k
+                         : which == 1 ? jb.uTb + (int64_t)col * jb.ld_uT
+                         : which == 2 ? jb.vtT + (int64_t)col * k
+                                      : jb.uWt + (int64_t)col * jb.ld_uW;
+          st[(which * KT + rr) * r + col] = rr < kt ? src[r0 + rr] : s_zero(S());
+        }
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < IF_ACC; ++j) {
+          const int e = e0 + tid + j * IF_THREADS;
+          if (e < 2 * r * r) {
+            const int which = e / (r * r), ac = e % (r * r), a = ac % r, c = ac / r;
+            const S* V = st + (which ? 2 : 0) * KT * r;
+            const S* U = st + (which ? 3 : 1) * KT * r;
+            for (int rr = 0; rr < kt; ++rr) acc[j] = s_fma(V[rr * r + a], U[rr * r + c], acc[j]);
+          }
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < IF_ACC; ++j) {
+        const int e = e0 + tid + j * IF_THREADS;
+        if (e < 2 * r * r) {
+          const int which = e / (r * r), ac = e % (r * r), a = ac % r, c = ac / r;
+          (which ? Es : Ks)[a + c * r] = acc[j];
+        }
+      }
+    }
   }
   __syncthreads();
   bool anyT = false, anyW = false;
@@ -647,7 +681,7 @@ __global__ void __launch_bounds__(IF_THREADS) iface_setup_kernel(const IfaceSetu
 template <class S>
 void launch_iface_setup_t(Ctx* c, const IfaceSetupJobT<S>* d_jobs, int njobs, int r, int64_t k) {
   if (njobs == 0) return;
-  const size_t smem = sizeof(S) * 4 * r * r + sizeof(double) * r;
+  const size_t smem = sizeof(S) * (4 * r * r + 4) + sizeof(double) * r;
   if (smem > 227 * 1024)  // real: r <= 85, complex: r <= 60
     throw LrsError(LRS_ERR_PARAMETER, "n_svd too large for the shared-memory interface setup");
   static size_t attr = 0;
