@@ -650,14 +650,17 @@ def _apply_roofline(kt, reps, info, hbm_peak, peak_src, steps, cfg_key):
     ms, n = kt["band_solve"]
     if not applies or not n:
         return None
-    # the Krylov-phase solves are the single-column launches: 2 per apply
+    # the Krylov-phase sweeps: one fused L + U launch per apply (band_solve_lu1_kernel), or
+    # two launches with LRS_SOLVE_FUSED=0
+    per_apply_launches = 1 if n <= applies else 2
     ms_iface = kt["iface_apply"][0] + kt["recovery"][0]
-    per_apply_ms = (ms * (2 * applies / n) + ms_iface) / applies
+    sweeps_ms = ms * (per_apply_launches * applies / n)
+    per_apply_ms = (sweeps_ms + ms_iface) / applies
     gbs = info["apply_bytes"] / (per_apply_ms / 1e3) / 1e9
     traffic = _ncu_traffic(cfg_key)
     return {"bound": "hbm",
-            "kernel": "band_solve_kernel<0, 1> + <1, 1> (one-RHS L and U dataflow sweeps of "
-                      "the apply) + iface + recovery",
+            "kernel": "band_solve_lu1_kernel (the one-RHS L and U dataflow sweeps of the "
+                      "apply, one launch) + iface + recovery",
             "achieved": gbs, "peak": hbm_peak, "unit": "GB/s", "frac": gbs / hbm_peak,
             "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_src})",
             # DRAM read + write of one apply's two sweeps from `ncu --set full`
@@ -665,7 +668,7 @@ def _apply_roofline(kt, reps, info, hbm_peak, peak_src, steps, cfg_key):
             "traffic": traffic.get("value"), "traffic_source": traffic.get("source"),
             "bytes_per_apply": info["apply_bytes"], "ms_per_apply": per_apply_ms,
             # the two sweeps alone (the iface / recovery kernels and launch gaps excluded)
-            "sweeps_gbs": info["apply_bytes"] / (ms * 2 / n / 1e3) / 1e9,
+            "sweeps_gbs": info["apply_bytes"] / (sweeps_ms / applies / 1e3) / 1e9,
             "ms_per_step": per_apply_ms * applies / steps,
             "frac_of_8TBs_nominal": gbs / 8000.0}
 
