@@ -226,50 +226,57 @@ __device__ __forceinline__ void digits7_bits(double x, int e, uint32_t* words, i
 }
 
 // ---------------------------------------------------------------------------------------
-// lu_i8_slice: grid (wl + wu, 4, P), 256 threads.  Blocks x < wl slice 32 rows (y) of the A
-// tile row I = K+2+x, the others 32 columns of the B tile column J = K+2+(x-wl); tiles
-// outside the band are zeros.  Thread (line = tid % 32, chunk = tid / 32): the line's
-// maximum over its 32 K values of the chunk (then over the 8 chunks in shared memory), then
-// the chunk's eight digit slices, two 16-byte K-core rows per slice stored straight into the
-// core-matrix layout (a warp writes 512 contiguous bytes per slice and K-core).
+// lu_i8_slice: grid (wl + wu, NB / LINES, P), 512 threads.  Blocks x < wl slice LINES rows
+// (y) of the A tile row I = K+STEPS+x, the others LINES columns of the B tile column
+// J = K+STEPS+(x-wl); tiles outside the band are zeros.  Thread (line = tid % LINES,
+// hc = tid / LINES): the 16 K values of K-core hc (chunk hc / 2, half hc % 2), the line's
+// maximum over them (then over every K-core in shared memory), then the K-core's seven
+// digit slices as one 16-byte core-matrix row each.  Two threads per 32-value chunk (16
+// values in registers each) keep ~50 registers per thread, so several CTAs share an SM:
+// the one-thread-per-chunk version (32 values in registers) ran two CTAs per SM and
+// streamed at 2.2 TB/s (ncu, c3).  LINES = 32 for pairs, 16 for quads (512 threads).
 // ---------------------------------------------------------------------------------------
-constexpr int I8_SLICE_SPLIT = 4;  // CTAs per tile (32 rows / columns each)
+constexpr int I8_SLICE_THREADS = 512;
 #ifndef LRS_I8_SLICE_L1
 #define LRS_I8_SLICE_L1 1
 #endif
+__host__ __device__ constexpr int i8_slice_lines(int steps) {
+  return I8_SLICE_THREADS / (2 * i8_nch(steps));
+}
 
 template <int STEPS>
-__global__ void __launch_bounds__(32 * STEPS * 4) lu_i8_slice_kernel(BandGeom g, const double* tiles,
-                                                                   int K, I8Panel pn) {
+__global__ void __launch_bounds__(I8_SLICE_THREADS) lu_i8_slice_kernel(BandGeom g,
+                                                                       const double* tiles, int K,
+                                                                       I8Panel pn) {
   constexpr int NCH = i8_nch(STEPS);
-  __shared__ double mx[NCH][32];
+  constexpr int LINES = i8_slice_lines(STEPS);
+  constexpr int NHC = 2 * NCH;  // K-cores of 16 values
+  __shared__ double mx[NHC][LINES];
   const int p = blockIdx.z, T = g.T[p];
   const int64_t base = g.tbase[p];
   auto tile = [&](int I, int J) -> const double* {
     return tiles + (base + (int64_t)I * g.W + (J - I + g.wl)) * TILE_ELEMS;
   };
-  const int tid = threadIdx.x, ln = tid & 31, kc = tid >> 5;
-  const int line = 32 * blockIdx.y + ln;  // A: row i, B: column j of the tile
+  const int tid = threadIdx.x, ln = tid % LINES, hc = tid / LINES;
+  const int line = LINES * blockIdx.y + ln;  // A: row i, B: column j of the tile
   const int x = blockIdx.x;
   const bool isA = x < g.wl;
   const int idx = isA ? x : x - g.wl;
   const int IJ = K + STEPS + idx;
   if (IJ >= T) return;
-  // this thread's chunk kc covers K values 32 (kc % 4) .. +31 of step K + kc / 4; tiles
-  // outside the band are zeros
-  const int d = kc >> 2;
+  const int kc = hc >> 1, hh = hc & 1;
+  const int d = kc >> 2;  // step K + d
   const double* src;
   if (isA) src = (IJ - (K + d) <= g.wl) ? tile(IJ, K + d) : nullptr;
   else src = (IJ - (K + d) <= g.wu) ? tile(K + d, IJ) : nullptr;
-  // the 32 K values k0 .. k0+31 of this line: A reads a column-major tile along its row
-  // (stride 128), B reads a column (contiguous)
-  const int k0 = (kc & 3) * I8_KC;
-  double v[32];
+  // the 16 K values k0 .. k0+15 of this line: A reads a column-major tile along its row
+  // (stride 128, lanes on consecutive rows: coalesced), B reads a column (contiguous per
+  // thread, lanes on different columns: through L1, a 32-byte sector serves 4 values)
+  const int k0 = (kc & 3) * I8_KC + 16 * hh;
+  double v[16];
 #pragma unroll
-  for (int kk = 0; kk < 32; ++kk) {
+  for (int kk = 0; kk < 16; ++kk) {
     const int k = k0 + kk;
-    // A: lanes read consecutive rows (coalesced); B: lanes read different columns, so the
-    // loads go through L1 (LRS_I8_SLICE_L1): the 32-byte sectors serve 4 consecutive k
 #if LRS_I8_SLICE_L1
     v[kk] = src ? (isA ? __ldcg(src + (int64_t)k * NB + line) : __ldca(src + (int64_t)line * NB + k))
                 : 0.0;
@@ -280,15 +287,15 @@ __global__ void __launch_bounds__(32 * STEPS * 4) lu_i8_slice_kernel(BandGeom g,
   }
   double m = 0.0;
 #pragma unroll
-  for (int kk = 0; kk < 32; ++kk) m = fmax(m, fabs(v[kk]));
-  mx[kc][ln] = m;
+  for (int kk = 0; kk < 16; ++kk) m = fmax(m, fabs(v[kk]));
+  mx[hc][ln] = m;
   __syncthreads();
   m = mx[0][ln];
 #pragma unroll
-  for (int c = 1; c < NCH; ++c) m = fmax(m, mx[c][ln]);
+  for (int c = 1; c < NHC; ++c) m = fmax(m, mx[c][ln]);
   int e = 0;
   if (m > 0.0) frexp(m, &e);
-  if (kc == 0) {
+  if (hc == 0) {
     int* ex = isA ? pn.ea + ((int64_t)p * g.wl + idx) * NB : pn.eb + ((int64_t)p * g.wu + idx) * NB;
     ex[line] = e;
   }
@@ -299,24 +306,20 @@ __global__ void __launch_bounds__(32 * STEPS * 4) lu_i8_slice_kernel(BandGeom g,
                      : pn.B + ((((int64_t)p * g.wu + idx) * I8_NH + line / I8_TN) * NCH + kc) *
                                   I8_BBLK;
   const int rows = isA ? NB : I8_TN;
+  uint32_t wd[I8_S][4];
 #pragma unroll
-  for (int h = 0; h < 2; ++h) {  // K-core: k0 + 16h .. k0 + 16h + 15
-    uint32_t wd[I8_S][4];
+  for (int q = 0; q < I8_S; ++q) wd[q][0] = wd[q][1] = wd[q][2] = wd[q][3] = 0u;
 #pragma unroll
-    for (int q = 0; q < I8_S; ++q) wd[q][0] = wd[q][1] = wd[q][2] = wd[q][3] = 0u;
+  for (int kk = 0; kk < 16; ++kk) {
+    uint32_t tmp[I8_S] = {0, 0, 0, 0, 0, 0, 0};
+    digits7_bits(v[kk], e, tmp, kk & 3);
 #pragma unroll
-    for (int kk = 0; kk < 16; ++kk) {
-      uint32_t tmp[I8_S] = {0, 0, 0, 0, 0, 0, 0};
-      digits7_bits(v[16 * h + kk], e, tmp, kk & 3);
-#pragma unroll
-      for (int q = 0; q < I8_S; ++q) wd[q][kk >> 2] |= tmp[q];
-    }
-    const int off = (h * (rows / 8) + (bl >> 3)) * 128 + (bl & 7) * 16;
-#pragma unroll
-    for (int q = 0; q < I8_S; ++q)
-      *reinterpret_cast<uint4*>(dst + q * sl + off) =
-          make_uint4(wd[q][0], wd[q][1], wd[q][2], wd[q][3]);
+    for (int q = 0; q < I8_S; ++q) wd[q][kk >> 2] |= tmp[q];
   }
+  const int off = (hh * (rows / 8) + (bl >> 3)) * 128 + (bl & 7) * 16;
+#pragma unroll
+  for (int q = 0; q < I8_S; ++q)
+    *reinterpret_cast<uint4*>(dst + q * sl + off) = make_uint4(wd[q][0], wd[q][1], wd[q][2], wd[q][3]);
 }
 
 // work item t of the kind-3 / kind-4 lists of a STEPS-step update (steps K .. K+D-1, D =
@@ -967,9 +970,11 @@ double run_i8_peak(Ctx* c) {
 void launch_lu_i8_slice(Ctx* c, cudaStream_t s, const BandGeom& g, const double* tiles, int K,
                         int steps, const I8Panel& pn) {
   if (steps == 4)
-    lu_i8_slice_kernel<4><<<dim3(g.wl + g.wu, I8_SLICE_SPLIT, g.P), 512, 0, s>>>(g, tiles, K, pn);
+    lu_i8_slice_kernel<4><<<dim3(g.wl + g.wu, NB / i8_slice_lines(4), g.P), I8_SLICE_THREADS, 0,
+                            s>>>(g, tiles, K, pn);
   else
-    lu_i8_slice_kernel<2><<<dim3(g.wl + g.wu, I8_SLICE_SPLIT, g.P), 256, 0, s>>>(g, tiles, K, pn);
+    lu_i8_slice_kernel<2><<<dim3(g.wl + g.wu, NB / i8_slice_lines(2), g.P), I8_SLICE_THREADS, 0,
+                            s>>>(g, tiles, K, pn);
   LRS_LAUNCHED(c);
 }
 
