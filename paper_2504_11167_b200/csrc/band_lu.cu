@@ -876,7 +876,8 @@ int launch_band_lu(Ctx* c, const BandGeom& g, double* tiles, int Tmax, int* stat
   lu_attrs();
   LuKernels L{real_diag, real_gemm, LRS_LU_PAIRS != 0};
   DevBuf<uint8_t> buf;
-  I8Panel pn[2];
+  I8Panel pn[3];  // [0], [1]: the bulk update's buffers (alternating); [2]: the quad
+                  // look-ahead's pair update (steps = 4 only)
   int steps = lu_i8_steps(g, c->num_sms);
   if (steps == 4 && !lu_i8_fits(g, 4)) steps = 2;
   if (lu_i8_wanted(g, L) && lu_i8_fits(g, steps)) {
@@ -884,7 +885,11 @@ int launch_band_lu(Ctx* c, const BandGeom& g, double* tiles, int Tmax, int* stat
     const size_t a = al((size_t)g.P * g.wl * TILE_ELEMS * steps * 8),
                  b = al((size_t)g.P * g.wu * TILE_ELEMS * steps * 8),
                  ea = al(sizeof(int) * g.P * g.wl * NB), eb = al(sizeof(int) * g.P * g.wu * NB);
-    buf.alloc(2 * (a + b + ea + eb));
+    // the pair buffer of the quad look-ahead: half the A / B panel bytes of a quad buffer
+    const size_t a2 = al((size_t)g.P * g.wl * TILE_ELEMS * 2 * 8),
+                 b2 = al((size_t)g.P * g.wu * TILE_ELEMS * 2 * 8);
+    const size_t extra = steps == 4 ? a2 + b2 + ea + eb : 0;
+    buf.alloc(2 * (a + b + ea + eb) + extra);
     uint8_t* q = buf.get();
     for (int k = 0; k < 2; ++k) {
       pn[k].A = q;
@@ -892,6 +897,12 @@ int launch_band_lu(Ctx* c, const BandGeom& g, double* tiles, int Tmax, int* stat
       pn[k].ea = reinterpret_cast<int*>(q + a + b);
       pn[k].eb = reinterpret_cast<int*>(q + a + b + ea);
       q += a + b + ea + eb;
+    }
+    if (steps == 4) {
+      pn[2].A = q;
+      pn[2].B = q + a2;
+      pn[2].ea = reinterpret_cast<int*>(q + a2 + b2);
+      pn[2].eb = reinterpret_cast<int*>(q + a2 + b2 + ea);
     }
     L.i8 = pn;
     L.steps = steps;
@@ -946,8 +957,30 @@ void run_band_lu(Ctx* c, const BandGeom& g, void* tiles, int Tmax, int* status,
     //         diag/panel(s), step s on rows / columns s+1..K+7 (DMMA kind 60 + m)
     //         -> slice(K+4)
     // Every tile takes its updates in step order; main never waits on crit's latency chain.
-    auto mini = [&](int K0) {  // the serial LU of steps K0 .. K0+3 inside the look-ahead
+    // The serial LU of steps K0 .. K0+3 inside the look-ahead.  A full quad runs it as the
+    // pair schedule does: step K0 on row / column K0+1 (DMMA), diag / panel(K0+1), the
+    // INT8 pair update of rows / columns K0+2, K0+3 with steps K0, K0+1 (the look-ahead pair
+    // buffer L.i8[2]), step K0+2 on row / column K0+3 (DMMA), diag / panel(K0+3): a third of
+    // the DMMA tile-steps of applying each step to the rest of the quad window (kind 60+m,
+    // kept for a partial last quad).  LRS_QUAD_MINI_DMMA=1 selects the all-DMMA form.
+    static const bool mini_dmma = std::getenv("LRS_QUAD_MINI_DMMA") &&
+                                  std::getenv("LRS_QUAD_MINI_DMMA")[0] == '1';
+    auto mini = [&](int K0) {
       const int last = std::min(K0 + 3, Tmax - 1);
+      if (!mini_dmma && last == K0 + 3 && g.wl >= 4 && g.wu >= 4) {
+        if (K0 > 0) lu_diag_panel(c, sc, g, tiles, K0, status, L);  // step 0: done above
+        gemm(sc, K0, 2, K_LU_PANEL);
+        lu_diag_panel(c, sc, g, tiles, K0 + 1, status, L);
+        {
+          ProfScope ps_(c, K_LU_PANEL, sc);
+          launch_lu_i8_slice(c, sc, g, static_cast<const double*>(tiles), K0, 2, L.i8[2]);
+          launch_lu_i8_gemm(c, sc, g, static_cast<double*>(tiles), K0, 3, 2, L.i8[2]);
+        }
+        lu_diag_panel(c, sc, g, tiles, K0 + 2, status, L);
+        gemm(sc, K0 + 2, 2, K_LU_PANEL);
+        lu_diag_panel(c, sc, g, tiles, K0 + 3, status, L);
+        return;
+      }
       for (int st = K0; st <= last; ++st) {
         if (st > 0) lu_diag_panel(c, sc, g, tiles, st, status, L);  // step 0: done above
         if (last - st > 0 && g.wl > 0 && g.wu > 0) gemm(sc, st, 60 + (last - st), K_LU_PANEL);

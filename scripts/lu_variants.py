@@ -42,8 +42,11 @@ if __name__ == "__main__":
     if os.environ.get("LRS_VARIANT_CHILD"):
         print(json.dumps(one(name, scale, P, R)), flush=True)
         sys.exit(0)
-    variants = [("default", {}), ("quad", {"LRS_LU_QUAD": "1"}), ("2sm", {"LRS_I8_2SM": "1"}),
-                ("quad+2sm", {"LRS_LU_QUAD": "1", "LRS_I8_2SM": "1"})]
+    variants = [("default", {}), ("pairs", {"LRS_LU_QUAD": "0"}), ("quad", {"LRS_LU_QUAD": "1"}),
+                ("quad-mini-dmma", {"LRS_LU_QUAD": "1", "LRS_QUAD_MINI_DMMA": "1"})]
+    if os.environ.get("LRS_VARIANTS_2SM"):
+        variants += [("2sm", {"LRS_I8_2SM": "1"}),
+                     ("quad+2sm", {"LRS_LU_QUAD": "1", "LRS_I8_2SM": "1"})]
     for lib in sorted(glob.glob(os.path.join(ROOT, "build", "var_*", "liblrspike_cuda.so"))):
         variants.append((os.path.basename(os.path.dirname(lib)), {"LRS_LIB": lib}))
     for tag, env in variants:
