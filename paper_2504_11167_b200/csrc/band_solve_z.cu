@@ -14,15 +14,21 @@ constexpr int ZS_THREADS = 256;
 constexpr int ZCH_COLS = 16;
 constexpr int ZCH_SM = ZCH_COLS * NB;  // complex elements per chunk
 constexpr int ZNCH = NB / ZCH_COLS;    // 8 chunks per tile
-constexpr int ZSTAGES = 3;
+// Ring depth: the forward sweeps (the c5 apply: per SM a 32 KB chunk is ~0.75 us of HBM and
+// ~0.8 us of DMMA work) keep 5 chunks in flight; the adjoint sweeps also hold the transposed
+// accumulator and the K-quarter partials, which leave room for 3.
+template <int MODE>
+constexpr int zstages() { return MODE >= 2 ? 3 : 5; }
 
 template <int NR>
 constexpr int zpart_elems() { return 4 * ZCH_COLS * (NR + 1); }  // adjoint K-quarter partials
 
-template <int NR>
+template <int MODE, int NR>
 constexpr size_t zsolve_smem_bytes() {
-  return sizeof(zc) * ((size_t)ZSTAGES * ZCH_SM + 2 * (size_t)NB * (NR + 4) + zpart_elems<NR>()) +
-         16 * ZSTAGES + 64;
+  constexpr bool TRANS = MODE >= 2;
+  return sizeof(zc) * ((size_t)zstages<MODE>() * ZCH_SM + (TRANS ? 2 : 1) * (size_t)NB * (NR + 4) +
+                       (TRANS ? zpart_elems<NR>() : 0)) +
+         16 * zstages<MODE>() + 64;
 }
 
 #ifndef LRS_ZSOLVE_3M
@@ -43,11 +49,12 @@ __global__ void __launch_bounds__(ZS_THREADS, 1)
   constexpr bool TRANS = (MODE >= 2);
   constexpr int NJ = NR / 8;
   extern __shared__ __align__(128) unsigned char smraw[];
+  constexpr int ZSTAGES = zstages<MODE>();
   zc* ring = reinterpret_cast<zc*>(smraw);
   zc* xs = ring + (size_t)ZSTAGES * ZCH_SM;
-  zc* red = xs + NB * XLD;
-  zc* part = red + NB * XLD;  // [4][ZCH_COLS][NR + 1]: adjoint K-quarter partials
-  uint64_t* bars = reinterpret_cast<uint64_t*>(part + zpart_elems<NR>());
+  zc* red = xs + NB * XLD;    // adjoint only
+  zc* part = red + (TRANS ? NB * XLD : 0);  // [4][ZCH_COLS][NR + 1]: adjoint K-quarter partials
+  uint64_t* bars = reinterpret_cast<uint64_t*>(part + (TRANS ? zpart_elems<NR>() : 0));
   int* s_tk = reinterpret_cast<int*>(bars + ZSTAGES);
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   if (tid == 0) *s_tk = atomicAdd(ticket, 1);
@@ -366,7 +373,7 @@ static void zlaunch_mode(Ctx* c, const BandGeom& g, const zc* tiles, zc* x, int6
                          int64_t fs) {
   const int ngroups = (nrhs + NR - 1) / NR;
   static bool attr = false;
-  const size_t smem = zsolve_smem_bytes<NR>();
+  const size_t smem = zsolve_smem_bytes<MODE, NR>();
   if (!attr) {
     LRS_CUDA(cudaFuncSetAttribute(band_solve_z_kernel<MODE, NR>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
