@@ -841,11 +841,14 @@ bool lu_real_pairs(const BandGeom& g) {
 // unless LRS_LU_I8=0, the band is too narrow for the pair schedule, or the two panel
 // buffers do not fit the free device memory (driver free + the pool's cached blocks, which
 // an allocation releases on failure) with 2 GB to spare.
-static bool lu_i8_fits(const BandGeom& g, int steps) {
+bool lu_i8_bytes_fit(size_t bytes) {
   size_t fr = 0, tot = 0;
   if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) return false;
   const size_t avail = fr + pool_cached_bytes(), margin = size_t(2) << 30;
-  return avail > margin && 2 * lu_i8_panel_bytes(g, steps) < avail - margin;
+  return avail > margin && bytes < avail - margin;
+}
+static bool lu_i8_fits(const BandGeom& g, int steps) {
+  return lu_i8_bytes_fit(2 * lu_i8_panel_bytes(g, steps));
 }
 static bool lu_i8_wanted(const BandGeom& g, const LuKernels& L) {
   const char* e = std::getenv("LRS_LU_I8");
@@ -941,14 +944,20 @@ void run_band_lu(Ctx* c, const BandGeom& g, void* tiles, int Tmax, int* status,
   auto slice = [&](int K) {
     if (!L.i8) return;
     ProfScope ps_(c, K_LU_PANEL, sc);
-    launch_lu_i8_slice(c, sc, g, static_cast<const double*>(tiles), K, L.steps,
-                       L.i8[(K / L.steps) & 1]);
+    if (L.cplx)
+      launch_lu_i8_slice_z(c, sc, g, static_cast<const zc*>(tiles), K, L.i8[(K / L.steps) & 1]);
+    else
+      launch_lu_i8_slice(c, sc, g, static_cast<const double*>(tiles), K, L.steps,
+                         L.i8[(K / L.steps) & 1]);
   };
   auto upd2 = [&](cudaStream_t s, int K, int kind, int cls) {
     if (!L.i8) return gemm(s, K, kind, cls);
     ProfScope ps_(c, cls, s);
-    launch_lu_i8_gemm(c, s, g, static_cast<double*>(tiles), K, kind, L.steps,
-                      L.i8[(K / L.steps) & 1]);
+    if (L.cplx)
+      launch_lu_i8_gemm_z(c, s, g, static_cast<zc*>(tiles), K, kind, L.i8[(K / L.steps) & 1]);
+    else
+      launch_lu_i8_gemm(c, s, g, static_cast<double*>(tiles), K, kind, L.steps,
+                        L.i8[(K / L.steps) & 1]);
   };
   if (L.i8 && L.steps == 4) {
     // Steps in quads (K .. K+3) with a rank-512 INT8 bulk update and look-ahead depth 4:

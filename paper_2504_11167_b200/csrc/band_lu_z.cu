@@ -378,9 +378,39 @@ static void zgemm_attrs() {
   }
 }
 
-void launch_band_lu_z(Ctx* c, const BandGeom& g, zc* tiles, int Tmax, int* status) {
+// The complex LU: with a band of >= 3 tiles each side, steps in pairs whose two-step updates
+// run realified on the INT8 tensor cores (lu_i8_gemm_kernel<.., true>: C_re -= [Ar Ai][Br; -Bi],
+// C_im -= [Ar Ai][Bi; Br], exact integer slices as in the real LU); otherwise (or with
+// LRS_LU_I8=0, or when the panel buffers do not fit) single steps with the 3M DMMA update.
+// Returns the steps per INT8 update (2) or 0.
+int launch_band_lu_z(Ctx* c, const BandGeom& g, zc* tiles, int Tmax, int* status) {
   zgemm_attrs();
-  run_band_lu(c, g, tiles, Tmax, status, LuKernels{z_diag, z_gemm});
+  LuKernels L{z_diag, z_gemm};
+  DevBuf<uint8_t> buf;
+  I8Panel pn[2];
+  const char* e = std::getenv("LRS_LU_I8");
+  const bool want = !(e && e[0] == '0') && g.wl >= 3 && g.wu >= 3;
+  if (want && lu_i8_bytes_fit(2 * lu_i8_panel_bytes_z(g))) {
+    auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
+    const size_t a = al((size_t)g.P * g.wl * 2 * lu_i8_chunk_bytes(2)),
+                 b = al((size_t)g.P * g.wu * 4 * lu_i8_chunk_bytes(2)),
+                 ea = al(sizeof(int) * g.P * g.wl * NB), eb = al(sizeof(int) * g.P * g.wu * NB);
+    buf.alloc(2 * (a + b + ea + eb));
+    uint8_t* q = buf.get();
+    for (int k = 0; k < 2; ++k) {
+      pn[k].A = q;
+      pn[k].B = q + a;
+      pn[k].ea = reinterpret_cast<int*>(q + a + b);
+      pn[k].eb = reinterpret_cast<int*>(q + a + b + ea);
+      q += a + b + ea + eb;
+    }
+    L.pairs = true;
+    L.i8 = pn;
+    L.steps = 2;
+    L.cplx = true;
+  }
+  run_band_lu(c, g, tiles, Tmax, status, L);
+  return L.i8 ? 2 : 0;
 }
 
 // Partial-pivoting complex band LU (zgbtrf): the panel kernels of band_lu_piv.cu, then

@@ -14,11 +14,12 @@ constexpr int ZS_THREADS = 256;
 constexpr int ZCH_COLS = 16;
 constexpr int ZCH_SM = ZCH_COLS * NB;  // complex elements per chunk
 constexpr int ZNCH = NB / ZCH_COLS;    // 8 chunks per tile
-// Ring depth: the forward sweeps (the c5 apply: per SM a 32 KB chunk is ~0.75 us of HBM and
-// ~0.8 us of DMMA work) keep 5 chunks in flight; the adjoint sweeps also hold the transposed
-// accumulator and the K-quarter partials, which leave room for 3.
+// Ring depth 3 (per SM a 32 KB chunk is ~0.75 us of HBM and ~0.8 us of DMMA work in the c5
+// apply).  The forward sweeps do not hold the adjoint's transposed accumulator and partials,
+// so they could keep 5 chunks in flight: measured 1.8% slower on c5 (shift 0 solve 51.4 s vs
+// 50.5 s; ncu: DMMA pipe 57%, the sweeps are bound by the DMMA issue, not the stream).
 template <int MODE>
-constexpr int zstages() { return MODE >= 2 ? 3 : 5; }
+constexpr int zstages() { return 3; }
 
 template <int NR>
 constexpr int zpart_elems() { return 4 * ZCH_COLS * (NR + 1); }  // adjoint K-quarter partials

@@ -47,7 +47,11 @@ void launch_extract_tiles(Ctx* c, const Mat* m, const BandGeom& g, double* tiles
 // status[2p] = min column needing a row interchange, status[2p+1] = min zero-pivot column.
 // returns the steps per INT8-sliced tensor-core update (2 or 4; lu_i8.cu), 0 on DMMA
 int launch_band_lu(Ctx* c, const BandGeom& g, double* tiles, int Tmax, int* status);
-void launch_band_lu_z(Ctx* c, const BandGeom& g, zc* tiles, int Tmax, int* status);
+int launch_band_lu_z(Ctx* c, const BandGeom& g, zc* tiles, int Tmax, int* status);
+// the INT8 panel buffers fit the free device memory (+ pool cache) with 2 GB to spare
+bool lu_i8_bytes_fit(size_t bytes);
+// bytes of the digit slices of one 128 x 128 tile's K chunks for a D-step update
+size_t lu_i8_chunk_bytes(int steps);
 // integer-sliced (INT8 tensor core) two-step trailing update, lu_i8.cu: digit slices of one
 // step pair's A panel (rows K+2..K+1+wl) and B panel (columns K+2..K+1+wu)
 struct I8Panel {
@@ -60,6 +64,12 @@ struct I8Panel {
 size_t lu_i8_panel_bytes(const BandGeom& g, int steps);
 void launch_lu_i8_slice(Ctx* c, cudaStream_t s, const BandGeom& g, const double* tiles, int K,
                         int steps, const I8Panel& pn);
+// complex128 pairs: realified INT8 update (A' = [Ar Ai], B'_re = [Br; -Bi], B'_im = [Bi; Br])
+void launch_lu_i8_slice_z(Ctx* c, cudaStream_t s, const BandGeom& g, const zc* tiles, int K,
+                          const I8Panel& pn);
+void launch_lu_i8_gemm_z(Ctx* c, cudaStream_t s, const BandGeom& g, zc* tiles, int K, int kind,
+                         const I8Panel& pn);
+size_t lu_i8_panel_bytes_z(const BandGeom& g);
 // kind 3: look-ahead rows / columns K+steps .. K+2 steps-1; kind 4: the bulk (I, J >= K+2 steps)
 void launch_lu_i8_gemm(Ctx* c, cudaStream_t s, const BandGeom& g, double* tiles, int K, int kind,
                        int steps, const I8Panel& pn);
@@ -72,6 +82,7 @@ struct LuKernels {
   bool pairs = false;
   const I8Panel* i8 = nullptr;  // [2] (update parity): kinds 3 / 4 on the INT8 tensor cores
   int steps = 2;                // steps per INT8 update: 2 (pairs) or 4 (quads, K = 512)
+  bool cplx = false;            // complex128 tiles: the realified INT8 kernels (pairs)
 };
 void run_band_lu(Ctx* c, const BandGeom& g, void* tiles, int Tmax, int* status,
                  const LuKernels& L);

@@ -123,6 +123,8 @@ constexpr int I8_TPC = LRS_I8_TPC;                    // tiles per CTA (bulk)
 constexpr size_t I8_SMEM = (size_t)I8_STAGES * I8_STAGE + 2048;
 static_assert(I8_TN == 128 || I8_SMEM * 2 <= 227 * 1024, "two CTAs per SM");
 
+size_t lu_i8_chunk_bytes(int steps) { return (size_t)i8_nch(steps) * I8_BLK; }
+
 size_t lu_i8_panel_bytes(const BandGeom& g, int steps) {
   return (size_t)g.P * (g.wl + g.wu) * (i8_nch(steps) * I8_BLK + sizeof(int) * NB);
 }
@@ -322,6 +324,98 @@ __global__ void __launch_bounds__(I8_SLICE_THREADS) lu_i8_slice_kernel(BandGeom 
     *reinterpret_cast<uint4*>(dst + q * sl + off) = make_uint4(wd[q][0], wd[q][1], wd[q][2], wd[q][3]);
 }
 
+// the seven digit slices of 16 K values (one K-core row of a core matrix) at dst + q sl + off
+__device__ __forceinline__ void i8_store_kcore(const double* v, bool neg, int e, uint8_t* dst,
+                                               int sl, int off) {
+  uint32_t wd[I8_S][4];
+#pragma unroll
+  for (int q = 0; q < I8_S; ++q) wd[q][0] = wd[q][1] = wd[q][2] = wd[q][3] = 0u;
+#pragma unroll
+  for (int kk = 0; kk < 16; ++kk) {
+    uint32_t tmp[I8_S] = {0, 0, 0, 0, 0, 0, 0};
+    digits7_bits(neg ? -v[kk] : v[kk], e, tmp, kk & 3);
+#pragma unroll
+    for (int q = 0; q < I8_S; ++q) wd[q][kk >> 2] |= tmp[q];
+  }
+#pragma unroll
+  for (int q = 0; q < I8_S; ++q)
+    *reinterpret_cast<uint4*>(dst + q * sl + off) = make_uint4(wd[q][0], wd[q][1], wd[q][2], wd[q][3]);
+}
+
+// Complex panels of the realified update (lu_i8_gemm_kernel<.., true>): A' = [Ar Ai] (K' = 2K:
+// the real parts' chunks, then the imaginary parts'), B'_re = [Br; -Bi] and B'_im = [Bi; Br]
+// (part 0 / 1 of each B tile column).  One exponent per row of A' (the maximum over both
+// parts) and per column of B'_re / B'_im (the same set of magnitudes).  Thread layout as
+// lu_i8_slice_kernel; each thread loads 16 complex values and writes both parts.
+template <int STEPS>
+__global__ void __launch_bounds__(I8_SLICE_THREADS) lu_i8_slice_z_kernel(BandGeom g,
+                                                                         const zc* tiles, int K,
+                                                                         I8Panel pn) {
+  constexpr int NCH = i8_nch(STEPS);
+  constexpr int LINES = i8_slice_lines(STEPS);
+  constexpr int NHC = 2 * NCH;
+  __shared__ double mx[NHC][LINES];
+  const int p = blockIdx.z, T = g.T[p];
+  const int64_t base = g.tbase[p];
+  auto tile = [&](int I, int J) -> const zc* {
+    return tiles + (base + (int64_t)I * g.W + (J - I + g.wl)) * TILE_ELEMS;
+  };
+  const int tid = threadIdx.x, ln = tid % LINES, hc = tid / LINES;
+  const int line = LINES * blockIdx.y + ln;
+  const int x = blockIdx.x;
+  const bool isA = x < g.wl;
+  const int idx = isA ? x : x - g.wl;
+  const int IJ = K + STEPS + idx;
+  if (IJ >= T) return;
+  const int kc = hc >> 1, hh = hc & 1, d = kc >> 2;
+  const zc* src;
+  if (isA) src = (IJ - (K + d) <= g.wl) ? tile(IJ, K + d) : nullptr;
+  else src = (IJ - (K + d) <= g.wu) ? tile(K + d, IJ) : nullptr;
+  const int k0 = (kc & 3) * I8_KC + 16 * hh;
+  double vr[16], vi[16];
+#pragma unroll
+  for (int kk = 0; kk < 16; ++kk) {
+    const int k = k0 + kk;
+    double2 z = make_double2(0.0, 0.0);
+    if (src)
+      z = isA ? __ldcg(reinterpret_cast<const double2*>(src + (int64_t)k * NB + line))
+              : __ldca(reinterpret_cast<const double2*>(src + (int64_t)line * NB + k));
+    vr[kk] = z.x;
+    vi[kk] = z.y;
+  }
+  double m = 0.0;
+#pragma unroll
+  for (int kk = 0; kk < 16; ++kk) m = fmax(m, fmax(fabs(vr[kk]), fabs(vi[kk])));
+  mx[hc][ln] = m;
+  __syncthreads();
+  m = mx[0][ln];
+#pragma unroll
+  for (int c = 1; c < NHC; ++c) m = fmax(m, mx[c][ln]);
+  int e = 0;
+  if (m > 0.0) frexp(m, &e);
+  if (hc == 0) {
+    int* ex = isA ? pn.ea + ((int64_t)p * g.wl + idx) * NB : pn.eb + ((int64_t)p * g.wu + idx) * NB;
+    ex[line] = e;
+  }
+  const int bl = isA ? line : (line & (I8_TN - 1));
+  const int rows = isA ? NB : I8_TN;
+  const int off = (hh * (rows / 8) + (bl >> 3)) * 128 + (bl & 7) * 16;
+  if (isA) {
+    uint8_t* a = pn.A + ((int64_t)p * g.wl + idx) * (2 * NCH) * I8_BLK;
+    i8_store_kcore(vr, false, e, a + (int64_t)kc * I8_BLK, I8_SL, off);
+    i8_store_kcore(vi, false, e, a + (int64_t)(kc + NCH) * I8_BLK, I8_SL, off);
+  } else {
+    auto bdst = [&](int part, int kcp) -> uint8_t* {
+      return pn.B + (((((int64_t)p * g.wu + idx) * 2 + part) * I8_NH + line / I8_TN) * (2 * NCH) +
+                     kcp) * I8_BBLK;
+    };
+    i8_store_kcore(vr, false, e, bdst(0, kc), I8_BSL, off);         // B'_re = [Br; -Bi]
+    i8_store_kcore(vi, true, e, bdst(0, kc + NCH), I8_BSL, off);
+    i8_store_kcore(vi, false, e, bdst(1, kc), I8_BSL, off);         // B'_im = [Bi; Br]
+    i8_store_kcore(vr, false, e, bdst(1, kc + NCH), I8_BSL, off);
+  }
+}
+
 // work item t of the kind-3 / kind-4 lists of a STEPS-step update (steps K .. K+D-1, D =
 // STEPS) -> (p, ia, jb, column block h); false when outside the blocks.
 //   KIND 3 (look-ahead): columns K+D .. K+2D-1 (rows K+D .. K+D-1+wl) and rows
@@ -400,10 +494,16 @@ __device__ __forceinline__ void i8_chunk_mmas(uint32_t tm, uint32_t a0, uint32_t
   }
 }
 
-template <int KIND, int STEPS>
+// CPLX: complex128 tiles, the 4M product realified -- C_re -= [Ar Ai] [Br; -Bi] and
+// C_im -= [Ar Ai] [Bi; Br] -- as two real updates with K doubled (work item = tile x part,
+// part the lowest index; the A' = [Ar Ai] slices are shared, B'_re / B'_im have their own;
+// C is written at stride 2 into the interleaved complex tile).  lu_i8_slice_z_kernel makes
+// the panels.
+template <int KIND, int STEPS, bool CPLX = false>
 __global__ void __launch_bounds__(I8_THREADS, I8_TN == 128 ? 1 : 2)
     lu_i8_gemm_kernel(BandGeom g, double* tiles, int K, I8Panel pn, int total, int tpc) {
-  constexpr int I8_NCH = i8_nch(STEPS);
+  constexpr int I8_NCH = i8_nch(STEPS) * (CPLX ? 2 : 1);
+  constexpr int CS = CPLX ? 2 : 1;  // doubles per tile element
   extern __shared__ __align__(1024) uint8_t smraw[];
   uint8_t* stage = smraw;
   uint64_t* full = reinterpret_cast<uint64_t*>(smraw + I8_STAGES * I8_STAGE);
@@ -418,8 +518,13 @@ __global__ void __launch_bounds__(I8_THREADS, I8_TN == 128 ? 1 : 2)
   const int t0 = blockIdx.x * tpc, t1 = min(total, t0 + tpc);
   auto ctile = [&](int p, int ia, int jb, int h) -> double* {
     const int I = K + STEPS + ia, J = K + STEPS + jb;
-    return tiles + (g.tbase[p] + (int64_t)I * g.W + (J - I + g.wl)) * TILE_ELEMS +
-           (int64_t)h * I8_TN * NB;
+    return tiles + ((g.tbase[p] + (int64_t)I * g.W + (J - I + g.wl)) * TILE_ELEMS +
+                    (int64_t)h * I8_TN * NB) * CS;
+  };
+  // work item t -> (p, ia, jb, h) and the complex part (0: re, 1: im)
+  auto decode = [&](int t, int& p, int& ia, int& jb, int& h, int& part) -> bool {
+    part = CPLX ? (t & 1) : 0;
+    return i8_decode<KIND, STEPS>(g, K, CPLX ? (t >> 1) : t, p, ia, jb, h);
   };
   if (threadIdx.x == 0) {
     for (int s = 0; s < I8_STAGES; ++s) {
@@ -447,11 +552,12 @@ __global__ void __launch_bounds__(I8_THREADS, I8_TN == 128 ? 1 : 2)
     if (lane == 0) {
       int it = 0;
       for (int t = t0; t < t1; ++t) {
-        int p, ia, jb, h;
-        if (!i8_decode<KIND, STEPS>(g, K, t, p, ia, jb, h)) continue;
-        bulk_prefetch_l2(ctile(p, ia, jb, h), sizeof(double) * NB * I8_TN);
+        int p, ia, jb, h, part;
+        if (!decode(t, p, ia, jb, h, part)) continue;
+        if (part == 0) bulk_prefetch_l2(ctile(p, ia, jb, h), sizeof(double) * NB * I8_TN * CS);
         const uint8_t* a = pn.A + ((int64_t)p * g.wl + ia) * I8_NCH * I8_BLK;
-        const uint8_t* b = pn.B + (((int64_t)p * g.wu + jb) * I8_NH + h) * I8_NCH * I8_BBLK;
+        const uint8_t* b =
+            pn.B + ((((int64_t)p * g.wu + jb) * CS + part) * I8_NH + h) * I8_NCH * I8_BBLK;
         for (int pass = 0; pass < I8_NP; ++pass) {
           const unsigned abytes = i8_pmax(pass) * I8_SL;
           const unsigned bbytes = i8_pmax(pass) * I8_BSL;
@@ -476,8 +582,8 @@ __global__ void __launch_bounds__(I8_THREADS, I8_TN == 128 ? 1 : 2)
       int uses[I8_GROUPS] = {0, 0, 0, 0};
       PRB(long long c_full = 0, c_chunk0 = 0; const long long c_start = clock64();)
       for (int t = t0; t < t1; ++t) {
-        int p, ia, jb, h;
-        if (!i8_decode<KIND, STEPS>(g, K, t, p, ia, jb, h)) continue;
+        int p, ia, jb, h, part;
+        if (!decode(t, p, ia, jb, h, part)) continue;
 #pragma unroll
         for (int pass = 0; pass < I8_NP; ++pass) {
           for (int kc = 0; kc < I8_NCH; ++kc, ++it) {
@@ -513,9 +619,9 @@ __global__ void __launch_bounds__(I8_THREADS, I8_TN == 128 ? 1 : 2)
     int u = 0, ptr = 0;
     PRB(long long c_tf = 0, c_drain = 0, c_red = 0; const long long c_start = clock64();)
     for (int t = t0; t < t1; ++t) {
-      int p, ia, jb, h;
-      if (!i8_decode<KIND, STEPS>(g, K, t, p, ia, jb, h)) continue;
-      double* C = ctile(p, ia, jb, h) + (int64_t)ch * I8_EPC * NB;
+      int p, ia, jb, h, part;
+      if (!decode(t, p, ia, jb, h, part)) continue;
+      double* C = ctile(p, ia, jb, h) + (int64_t)ch * I8_EPC * NB * CS + part;
       const double si = exp2i(pn.ea[((int64_t)p * g.wl + ia) * NB + i]);
       if (w == 2) {  // the previous tile's readers of sj passed the closing barrier
         const int* eb = pn.eb + ((int64_t)p * g.wu + jb) * NB + h * I8_TN;
@@ -574,7 +680,7 @@ __global__ void __launch_bounds__(I8_THREADS, I8_TN == 128 ? 1 : 2)
       if (!LRS_I8_EXP) {
 #pragma unroll
         for (int j = 0; j < I8_EPC; ++j)
-          red_add_f64(C + (int64_t)j * NB + i, -(acc[j] * si * sj[ch * I8_EPC + j]));
+          red_add_f64(C + ((int64_t)j * NB + i) * CS, -(acc[j] * si * sj[ch * I8_EPC + j]));
       }
       asm volatile("bar.sync 1, %0;" ::"n"(32 * I8_EPI) : "memory");  // sj free for the next tile
       PRB(c_red += clock64() - c1;)
@@ -978,26 +1084,47 @@ void launch_lu_i8_slice(Ctx* c, cudaStream_t s, const BandGeom& g, const double*
   LRS_LAUNCHED(c);
 }
 
-template <int KIND, int STEPS>
+template <int KIND, int STEPS, bool CPLX = false>
 static void i8_gemm_launch(Ctx* c, cudaStream_t s, const BandGeom& g, double* tiles, int K,
                            const I8Panel& pn) {
   static bool attr = false;
   if (!attr) {
-    LRS_CUDA(cudaFuncSetAttribute(lu_i8_gemm_kernel<KIND, STEPS>,
+    LRS_CUDA(cudaFuncSetAttribute(lu_i8_gemm_kernel<KIND, STEPS, CPLX>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)I8_SMEM));
     attr = true;
   }
   constexpr int D = STEPS;
   const int per = KIND == 4 ? (g.wl - D) * (g.wu - D) : D * g.wl + D * (g.wu - D);
-  const int total = per * g.P * I8_NH;
+  const int total = per * g.P * I8_NH * (CPLX ? 2 : 1);
   if (total <= 0) return;
   // the look-ahead launch (kind 3, on the critical stream) takes fewer tiles per CTA
   static const int tpc3 = std::getenv("LRS_I8_TPC3") ? std::atoi(std::getenv("LRS_I8_TPC3"))
                                                       : LRS_I8_TPC3;
   const int tpc = KIND == 4 ? I8_TPC : std::max(1, tpc3);
   const int grid = (total + tpc - 1) / tpc;
-  lu_i8_gemm_kernel<KIND, STEPS><<<grid, I8_THREADS, I8_SMEM, s>>>(g, tiles, K, pn, total, tpc);
+  lu_i8_gemm_kernel<KIND, STEPS, CPLX><<<grid, I8_THREADS, I8_SMEM, s>>>(g, tiles, K, pn, total,
+                                                                         tpc);
   LRS_LAUNCHED(c);
+}
+
+// complex128 tiles (pairs only): the realified update of lu_i8_gemm_kernel<.., true>
+void launch_lu_i8_slice_z(Ctx* c, cudaStream_t s, const BandGeom& g, const zc* tiles, int K,
+                          const I8Panel& pn) {
+  lu_i8_slice_z_kernel<2><<<dim3(g.wl + g.wu, NB / i8_slice_lines(2), g.P), I8_SLICE_THREADS, 0,
+                            s>>>(g, tiles, K, pn);
+  LRS_LAUNCHED(c);
+}
+void launch_lu_i8_gemm_z(Ctx* c, cudaStream_t s, const BandGeom& g, zc* tiles, int K, int kind,
+                         const I8Panel& pn) {
+  double* t = reinterpret_cast<double*>(tiles);
+  if (kind == 4) i8_gemm_launch<4, 2, true>(c, s, g, t, K, pn);
+  else i8_gemm_launch<3, 2, true>(c, s, g, t, K, pn);
+}
+// A' and B' panel bytes of the complex pair update (one buffer): A' twice the real A panel,
+// B' four times the real B panel (two parts, K doubled)
+size_t lu_i8_panel_bytes_z(const BandGeom& g) {
+  return (size_t)g.P * (2 * g.wl + 4 * g.wu) * (i8_nch(2) * I8_BLK) +
+         sizeof(int) * (size_t)g.P * (g.wl + g.wu) * NB;
 }
 
 template <int STEPS>

@@ -63,8 +63,11 @@ def test_i8_peak_positive(ctx):
     assert 500.0 < tops < 20000.0
 
 
-@pytest.mark.parametrize("name,scale", [("c2", 0.5), ("c3", 24 / 96), ("c4", 0.05)])
+@pytest.mark.parametrize("name,scale", [("c2", 0.5), ("c3", 24 / 96), ("c4", 0.05), ("c5", 0.5),
+                                        ("c5", 0.3)])
 def test_int8_update_matches_dmma(ctx, name, scale):
+    """c5: complex128 shifted systems z I - A, the realified update (A' = [Ar Ai], B'_re =
+    [Br; -Bi], B'_im = [Bi; Br]) against the 3M complex DMMA update."""
     cfg = configs.make_config(name, scale)
     assert -(-cfg.b // 128) >= 3  # the pair schedule (and so the INT8 update) is in play
     assert _compare(ctx, cfg.system(0), cfg) <= 1e-12
