@@ -347,13 +347,14 @@ __device__ __forceinline__ void i8_store_kcore(const double* v, bool neg, int e,
 // (part 0 / 1 of each B tile column).  One exponent per row of A' (the maximum over both
 // parts) and per column of B'_re / B'_im (the same set of magnitudes).  Thread layout as
 // lu_i8_slice_kernel; each thread loads 16 complex values and writes both parts.
+constexpr int I8_ZSLICE_THREADS = 256;  // 32 complex values in registers per thread
 template <int STEPS>
-__global__ void __launch_bounds__(I8_SLICE_THREADS) lu_i8_slice_z_kernel(BandGeom g,
-                                                                         const zc* tiles, int K,
-                                                                         I8Panel pn) {
+__global__ void __launch_bounds__(I8_ZSLICE_THREADS) lu_i8_slice_z_kernel(BandGeom g,
+                                                                          const zc* tiles, int K,
+                                                                          I8Panel pn) {
   constexpr int NCH = i8_nch(STEPS);
-  constexpr int LINES = i8_slice_lines(STEPS);
   constexpr int NHC = 2 * NCH;
+  constexpr int LINES = I8_ZSLICE_THREADS / NHC;
   __shared__ double mx[NHC][LINES];
   const int p = blockIdx.z, T = g.T[p];
   const int64_t base = g.tbase[p];
@@ -1110,8 +1111,8 @@ static void i8_gemm_launch(Ctx* c, cudaStream_t s, const BandGeom& g, double* ti
 // complex128 tiles (pairs only): the realified update of lu_i8_gemm_kernel<.., true>
 void launch_lu_i8_slice_z(Ctx* c, cudaStream_t s, const BandGeom& g, const zc* tiles, int K,
                           const I8Panel& pn) {
-  lu_i8_slice_z_kernel<2><<<dim3(g.wl + g.wu, NB / i8_slice_lines(2), g.P), I8_SLICE_THREADS, 0,
-                            s>>>(g, tiles, K, pn);
+  lu_i8_slice_z_kernel<2><<<dim3(g.wl + g.wu, NB / (I8_ZSLICE_THREADS / (2 * i8_nch(2))), g.P),
+                            I8_ZSLICE_THREADS, 0, s>>>(g, tiles, K, pn);
   LRS_LAUNCHED(c);
 }
 void launch_lu_i8_gemm_z(Ctx* c, cudaStream_t s, const BandGeom& g, zc* tiles, int K, int kind,
