@@ -40,8 +40,10 @@ __device__ __forceinline__ zc zacc(double br, double bi, double q1, double q2, d
   return {br + (q1 - q2), bi + (q3 - (q1 + q2))};
 }
 
-template <int MODE, int NR>
-__global__ void __launch_bounds__(ZS_THREADS, 1)
+// TH threads: the forward 16-column sweeps (the c5 apply) run 16 warps -- 8 row groups x 2
+// column groups of 8 -- for twice the warps to hide the DMMA latency; the rest 8 warps.
+template <int MODE, int NR, int TH = ZS_THREADS>
+__global__ void __launch_bounds__(TH, 1)
     band_solve_z_kernel(BandGeom g, const zc* __restrict__ tiles, zc* x, int64_t ld, int nrhs,
                         unsigned* flags, unsigned epoch, int* ticket, int p_only, int ngroups,
                         int64_t flag_stride) {
@@ -49,6 +51,10 @@ __global__ void __launch_bounds__(ZS_THREADS, 1)
   constexpr bool FWD = (MODE == 0 || MODE == 2);
   constexpr bool TRANS = (MODE >= 2);
   constexpr int NJ = NR / 8;
+  constexpr int CG = TRANS ? 1 : TH / 256;  // column groups of warps (forward only)
+  constexpr int NJW = NJ / CG;              // n8 tiles per warp
+  static_assert(!TRANS || TH == ZS_THREADS, "adjoint sweeps: 8 warps");
+  static_assert(NJ % CG == 0 && TH % 256 == 0, "warp split");
   extern __shared__ __align__(128) unsigned char smraw[];
   constexpr int ZSTAGES = zstages<MODE>();
   zc* ring = reinterpret_cast<zc*>(smraw);
@@ -58,6 +64,7 @@ __global__ void __launch_bounds__(ZS_THREADS, 1)
   uint64_t* bars = reinterpret_cast<uint64_t*>(part + (TRANS ? zpart_elems<NR>() : 0));
   int* s_tk = reinterpret_cast<int*>(bars + ZSTAGES);
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int wr = TRANS ? w : (w & 7), NJ0 = TRANS ? 0 : (w >> 3) * NJW;  // forward: rows, n8 base
   if (tid == 0) *s_tk = atomicAdd(ticket, 1);
   __syncthreads();
   const int tk0 = *s_tk;
@@ -105,33 +112,33 @@ __global__ void __launch_bounds__(ZS_THREADS, 1)
     for (int q = 0; q < ZSTAGES && q < Q; ++q) issue(q, q);
   const int64_t row0 = (int64_t)t * NB;
   const int gq = lane >> 2, tq = lane & 3;
-  double accr[2][NJ][2], acci[2][NJ][2];
+  double accr[2][NJW][2], acci[2][NJW][2];
   // forward products in the 3M form (LRS_ZSOLVE_3M): p1 = sum ar br, p2 = sum ai bi,
   // p3 = sum (ar + ai)(br + bi); re = p1 - p2, im = p3 - p1 - p2 (three DMMAs per complex
   // product instead of four); accr / acci carry the right-hand side
-  double p1[2][NJ][2], p2[2][NJ][2], p3[2][NJ][2];
+  double p1[2][NJW][2], p2[2][NJW][2], p3[2][NJW][2];
 #pragma unroll
   for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
-    for (int nj = 0; nj < NJ; ++nj)
+    for (int nj = 0; nj < NJW; ++nj)
 #pragma unroll
       for (int e = 0; e < 2; ++e) p1[mi][nj][e] = p2[mi][nj][e] = p3[mi][nj][e] = 0.0;
 #pragma unroll
   for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
-    for (int nj = 0; nj < NJ; ++nj)
+    for (int nj = 0; nj < NJW; ++nj)
 #pragma unroll
       for (int e = 0; e < 2; ++e) accr[mi][nj][e] = acci[mi][nj][e] = 0.0;
   if (!TRANS) {
 #pragma unroll
     for (int mi = 0; mi < 2; ++mi) {
-      const int m = 16 * w + 8 * mi + gq;
+      const int m = 16 * wr + 8 * mi + gq;
       if (row0 + m < size)
 #pragma unroll
-        for (int nj = 0; nj < NJ; ++nj)
+        for (int nj = 0; nj < NJW; ++nj)
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
-            const int n = 8 * nj + 2 * tq + e;
+            const int n = 8 * (NJ0 + nj) + 2 * tq + e;
             if (n < nrhs) {
               const zc v = x[off + row0 + m + n * ld];
               accr[mi][nj][e] = v.x;
@@ -140,20 +147,20 @@ __global__ void __launch_bounds__(ZS_THREADS, 1)
           }
     }
   } else {
-    for (int e = tid; e < NB * NR; e += ZS_THREADS) {
+    for (int e = tid; e < NB * NR; e += TH) {
       const int r = e % NB, j = e / NB;
       red[r * XLD + j] = (j < nrhs && row0 + r < size) ? x[off + row0 + r + j * ld] : zc{0.0, 0.0};
     }
   }
   // x_s of the next dependency is loaded into registers while the current one's chunks run
   // (when its flag is already up), as in band_solve_kernel
-  constexpr int XPT = NB * NR / ZS_THREADS;
-  static_assert((NB * NR) % ZS_THREADS == 0, "x prefetch split");
+  constexpr int XPT = NB * NR / TH;
+  static_assert((NB * NR) % TH == 0, "x prefetch split");
   zc xpre[XPT];
   bool have_pre = false;
   int* s_ready = s_tk;  // free once every thread has read its ticket
   auto load_x = [&](int sdep, int i) -> zc {
-    const int e = tid + i * ZS_THREADS;
+    const int e = tid + i * TH;
     const int r = e % NB, j = e / NB;
     const int64_t srow0 = (int64_t)sdep * NB;
     zc v = {0.0, 0.0};
@@ -172,7 +179,7 @@ __global__ void __launch_bounds__(ZS_THREADS, 1)
         if (have_pre) {
 #pragma unroll
           for (int i = 0; i < XPT; ++i) {
-            const int e = tid + i * ZS_THREADS;
+            const int e = tid + i * TH;
             xs[(e % NB) * XLD + e / NB] = xpre[i];
           }
         } else {
@@ -183,7 +190,7 @@ __global__ void __launch_bounds__(ZS_THREADS, 1)
           __syncthreads();
 #pragma unroll
           for (int i = 0; i < XPT; ++i) {
-            const int e = tid + i * ZS_THREADS;
+            const int e = tid + i * TH;
             xs[(e % NB) * XLD + e / NB] = load_x(s, i);
           }
         }
@@ -199,17 +206,17 @@ __global__ void __launch_bounds__(ZS_THREADS, 1)
 #pragma unroll
           for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
-            for (int nj = 0; nj < NJ; ++nj)
+            for (int nj = 0; nj < NJW; ++nj)
 #pragma unroll
               for (int e = 0; e < 2; ++e) {
-                xs[(16 * w + 8 * mi + gq) * XLD + 8 * nj + 2 * tq + e] = zacc(
+                xs[(16 * wr + 8 * mi + gq) * XLD + 8 * (NJ0 + nj) + 2 * tq + e] = zacc(
                     accr[mi][nj][e], acci[mi][nj][e], p1[mi][nj][e], p2[mi][nj][e], p3[mi][nj][e]);
                 accr[mi][nj][e] = acci[mi][nj][e] = 0.0;
                 p1[mi][nj][e] = p2[mi][nj][e] = p3[mi][nj][e] = 0.0;
               }
         } else {
           __syncthreads();
-          for (int e = tid; e < NB * NR; e += ZS_THREADS) {
+          for (int e = tid; e < NB * NR; e += TH) {
             const int r = e % NB, j = e / NB;
             xs[r * XLD + j] = red[r * XLD + j];
             red[r * XLD + j] = {0.0, 0.0};
@@ -225,10 +232,10 @@ __global__ void __launch_bounds__(ZS_THREADS, 1)
 #pragma unroll
       for (int k4 = 0; k4 < ZCH_COLS / 4; ++k4) {
         const int k = 4 * k4 + tq, kg = cbase + k;
-        double ar[2], ai[2], br[NJ], bi[NJ];
+        double ar[2], ai[2], br[NJW], bi[NJW];
 #pragma unroll
         for (int mi = 0; mi < 2; ++mi) {
-          const int m = 16 * w + 8 * mi + gq;
+          const int m = 16 * wr + 8 * mi + gq;
           zc v = ch[k * NB + m];
           if (diag) {
             if (!(MODE == 0 ? m > kg : m <= kg)) v = {0.0, 0.0};
@@ -239,21 +246,21 @@ __global__ void __launch_bounds__(ZS_THREADS, 1)
           ai[mi] = v.y;
         }
 #pragma unroll
-        for (int nj = 0; nj < NJ; ++nj) {
-          const zc v = xs[kg * XLD + 8 * nj + gq];
+        for (int nj = 0; nj < NJW; ++nj) {
+          const zc v = xs[kg * XLD + 8 * (NJ0 + nj) + gq];
           br[nj] = v.x;
           bi[nj] = v.y;
         }
         if (LRS_ZSOLVE_3M) {
-          double as[2], bs[NJ];
+          double as[2], bs[NJW];
 #pragma unroll
           for (int mi = 0; mi < 2; ++mi) as[mi] = ar[mi] + ai[mi];
 #pragma unroll
-          for (int nj = 0; nj < NJ; ++nj) bs[nj] = br[nj] + bi[nj];
+          for (int nj = 0; nj < NJW; ++nj) bs[nj] = br[nj] + bi[nj];
 #pragma unroll
           for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
-            for (int nj = 0; nj < NJ; ++nj) {
+            for (int nj = 0; nj < NJW; ++nj) {
               dmma_8x8x4(p1[mi][nj][0], p1[mi][nj][1], ar[mi], br[nj]);
               dmma_8x8x4(p2[mi][nj][0], p2[mi][nj][1], ai[mi], bi[nj]);
               dmma_8x8x4(p3[mi][nj][0], p3[mi][nj][1], as[mi], bs[nj]);
@@ -262,7 +269,7 @@ __global__ void __launch_bounds__(ZS_THREADS, 1)
 #pragma unroll
           for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
-            for (int nj = 0; nj < NJ; ++nj) {
+            for (int nj = 0; nj < NJW; ++nj) {
               dmma_8x8x4(accr[mi][nj][0], accr[mi][nj][1], ar[mi], br[nj]);
               dmma_8x8x4(accr[mi][nj][0], accr[mi][nj][1], -ai[mi], bi[nj]);
               dmma_8x8x4(acci[mi][nj][0], acci[mi][nj][1], ar[mi], bi[nj]);
@@ -325,7 +332,7 @@ __global__ void __launch_bounds__(ZS_THREADS, 1)
         }
       }
       __syncthreads();
-      for (int e = tid; e < ZCH_COLS * NR; e += ZS_THREADS) {
+      for (int e = tid; e < ZCH_COLS * NR; e += TH) {
         const int mm = e / NR, nn = e % NR;
         const zc v = s_add(s_add(s_add(part[mm * PLD + nn], part[(ZCH_COLS + mm) * PLD + nn]),
                                  part[(2 * ZCH_COLS + mm) * PLD + nn]),
@@ -340,13 +347,13 @@ __global__ void __launch_bounds__(ZS_THREADS, 1)
   if (!TRANS) {
 #pragma unroll
     for (int mi = 0; mi < 2; ++mi) {
-      const int m = 16 * w + 8 * mi + gq;
+      const int m = 16 * wr + 8 * mi + gq;
       if (row0 + m >= size) continue;
 #pragma unroll
-      for (int nj = 0; nj < NJ; ++nj)
+      for (int nj = 0; nj < NJW; ++nj)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-          const int n = 8 * nj + 2 * tq + e;
+          const int n = 8 * (NJ0 + nj) + 2 * tq + e;
           if (n >= nrhs) continue;
           zc v = zacc(accr[mi][nj][e], acci[mi][nj][e], p1[mi][nj][e], p2[mi][nj][e], p3[mi][nj][e]);
           if (MODE == 0) v = s_add(v, xs[m * XLD + n]);
@@ -354,7 +361,7 @@ __global__ void __launch_bounds__(ZS_THREADS, 1)
         }
     }
   } else {
-    for (int e = tid; e < NB * NR; e += ZS_THREADS) {
+    for (int e = tid; e < NB * NR; e += TH) {
       const int r = e % NB, j = e / NB;
       if (j < nrhs && row0 + r < size) {
         zc v = red[r * XLD + j];
@@ -368,20 +375,24 @@ __global__ void __launch_bounds__(ZS_THREADS, 1)
   if (tid == 0) st_release_u32(flags + g.fbase[p] + t, epoch);
 }
 
+#ifndef LRS_ZSOLVE_TH16
+#define LRS_ZSOLVE_TH16 512
+#endif
 template <int MODE, int NR>
 static void zlaunch_mode(Ctx* c, const BandGeom& g, const zc* tiles, zc* x, int64_t ld, int nrhs,
                          unsigned* flags, unsigned epoch, int* ticket, int p_only, int ntiles,
                          int64_t fs) {
+  constexpr int TH = (MODE < 2 && NR == 16) ? LRS_ZSOLVE_TH16 : ZS_THREADS;
   const int ngroups = (nrhs + NR - 1) / NR;
   static bool attr = false;
   const size_t smem = zsolve_smem_bytes<MODE, NR>();
   if (!attr) {
-    LRS_CUDA(cudaFuncSetAttribute(band_solve_z_kernel<MODE, NR>,
+    LRS_CUDA(cudaFuncSetAttribute(band_solve_z_kernel<MODE, NR, TH>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = true;
   }
   ProfScope ps_(c, c->in_setup ? K_SPIKE_SOLVE : (MODE >= 2 ? K_SOLVE_ADJ : K_SOLVE));
-  band_solve_z_kernel<MODE, NR><<<ntiles * ngroups, ZS_THREADS, smem, c->stream>>>(
+  band_solve_z_kernel<MODE, NR, TH><<<ntiles * ngroups, TH, smem, c->stream>>>(
       g, tiles, x, ld, nrhs, flags, epoch, ticket, p_only, ngroups, fs);
   LRS_LAUNCHED(c);
 }
