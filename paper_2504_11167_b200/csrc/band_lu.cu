@@ -848,7 +848,9 @@ bool lu_i8_bytes_fit(size_t bytes) {
   return avail > margin && bytes < avail - margin;
 }
 static bool lu_i8_fits(const BandGeom& g, int steps) {
-  return lu_i8_bytes_fit(2 * lu_i8_panel_bytes(g, steps));
+  // quads also hold the pair buffer of their look-ahead
+  return lu_i8_bytes_fit(2 * lu_i8_panel_bytes(g, steps) +
+                         (steps == 4 ? lu_i8_panel_bytes(g, 2) : 0));
 }
 static bool lu_i8_wanted(const BandGeom& g, const LuKernels& L) {
   const char* e = std::getenv("LRS_LU_I8");
