@@ -376,7 +376,7 @@ __global__ void __launch_bounds__(TH, 1)
 }
 
 #ifndef LRS_ZSOLVE_TH16
-#define LRS_ZSOLVE_TH16 512
+#define LRS_ZSOLVE_TH16 256  // 512 (16 warps, 2 column groups): c5 shift 0 solve 63.4 s vs 50.5 s
 #endif
 template <int MODE, int NR>
 static void zlaunch_mode(Ctx* c, const BandGeom& g, const zc* tiles, zc* x, int64_t ld, int nrhs,
