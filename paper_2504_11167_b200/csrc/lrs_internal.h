@@ -111,7 +111,7 @@ struct Ctx {
   void stage_h2d(void* dst, const void* src, size_t bytes);  // pool.cu
   // pinned landing buffer of the Krylov dot products (allocated once: cudaMallocHost /
   // cudaFreeHost per solve cost milliseconds and synchronize the device)
-  static constexpr size_t DOTS_HOST_BYTES = sizeof(double) * 64 * MAX_RHS * 2;
+  static constexpr size_t DOTS_HOST_BYTES = sizeof(double) * 64 * MAX_RHS * 2 * 3;  // 3 slots
   double* dots_host = nullptr;
   // profiling: (class, start, end) event triples, summed on demand
   bool prof = false;

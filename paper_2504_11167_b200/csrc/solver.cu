@@ -1248,8 +1248,23 @@ struct Work {
     launch_multidot_persum(c(), ch, 2 * nr * SW<S>, f->partial.get(), f->persum.get());
     dots_finish(2, res);
   }
-  // per-partition sums (persum) -> global partition-ordered totals -> host
-  void dots_finish(int nvec, H* out) {
+  // dots without the host round trip: the totals land in pinned slot `slot` when the stream
+  // gets there (GMRES reads the three CGS2 results after ONE synchronization per step)
+  static constexpr size_t SLOT = 64 * MAX_RHS * 2;  // doubles per slot
+  void dots_enqueue(const S* X, int64_t strideX, int nvec, const S* Y, int slot) {
+    launch_multidot_partition_t<S>(c(), ch, X, n, strideX, nvec, Y, n, nr, sp<S>(f->partial),
+                                   sp<S>(f->persum));
+    dots_total(nvec, hbuf + slot * SLOT);
+  }
+  void dots_wait() {
+    LRS_CUDA(cudaStreamSynchronize(c()->stream));
+    ++f->scalar_syncs;
+  }
+  void dots_read(int nvec, int slot, H* out) const {
+    std::memcpy(static_cast<void*>(out), hbuf + slot * SLOT, sizeof(double) * nvec * nr * SW<S>);
+  }
+  // per-partition sums -> global totals (dotout) -> async copy to `host`
+  void dots_total(int nvec, double* host) {
     const int nout = nvec * nr * SW<S>;  // doubles
     if (f->dist) {
       if (!f->comm.stream_ordered) {
@@ -1266,11 +1281,14 @@ struct Work {
       launch_partition_total(c(), f->persum.get(), f->d_rank_pl.get(), 1, f->P, nout,
                              f->dotout.get());
     }
-    LRS_CUDA(cudaMemcpyAsync(hbuf, f->dotout.get(), sizeof(double) * nout, cudaMemcpyDeviceToHost,
+    LRS_CUDA(cudaMemcpyAsync(host, f->dotout.get(), sizeof(double) * nout, cudaMemcpyDeviceToHost,
                              c()->stream));
-    LRS_CUDA(cudaStreamSynchronize(c()->stream));
-    ++f->scalar_syncs;
-    std::memcpy(static_cast<void*>(out), hbuf, sizeof(double) * nout);
+  }
+  // per-partition sums (persum) -> global partition-ordered totals -> host
+  void dots_finish(int nvec, H* out) {
+    dots_total(nvec, hbuf);
+    dots_wait();
+    dots_read(nvec, 0, out);
   }
   void norms(const S* X, double* out) {
     std::vector<H> d(nr);
@@ -1645,14 +1663,23 @@ void run_gmres(Work<S>& w, const S* b, S* x, const lrs_iter_cfg& cfg, bool has_x
       S* Zj = Z + blk * jj;
       w.M(Vj, Zj);
       w.Aop(Zj, wv);
-      // CGS2 (the projections stay on the device in dotout and feed the update directly)
-      w.dots(V, (int64_t)blk, jj + 1, wv, h.data());
+      // CGS2 (the projections stay on the device in dotout and feed the update directly;
+      // the host reads h, h2 and the norm after one synchronization)
+      w.dots_enqueue(V, (int64_t)blk, jj + 1, wv, 0);
       launch_multi_axpy_t<S>(c, w.nl, nr, V + w.lo, n, (int64_t)blk, jj + 1, w.dotout(), -1.0,
                              wv + w.lo, n);
-      w.dots(V, (int64_t)blk, jj + 1, wv, h2.data());
+      w.dots_enqueue(V, (int64_t)blk, jj + 1, wv, 1);
       launch_multi_axpy_t<S>(c, w.nl, nr, V + w.lo, n, (int64_t)blk, jj + 1, w.dotout(), -1.0,
                              wv + w.lo, n);
-      w.norms(wv, hn.data());
+      w.dots_enqueue(wv, 0, 1, wv, 2);
+      w.dots_wait();
+      w.dots_read(jj + 1, 0, h.data());
+      w.dots_read(jj + 1, 1, h2.data());
+      {
+        std::vector<H> nn(nr);
+        w.dots_read(1, 2, nn.data());
+        for (int j = 0; j < nr; ++j) hn[j] = std::sqrt(hreal(nn[j]));
+      }
       for (int q = 0; q < (jj + 1) * nr; ++q) h[q] += h2[q];
       std::vector<H> invn(nr);
       for (int j = 0; j < nr; ++j) invn[j] = H(1.0 / (hn[j] > 0 ? hn[j] : 1.0));
