@@ -115,6 +115,9 @@ constexpr int I8_TPC = LRS_I8_TPC;                    // tiles per CTA (bulk)
 #ifndef LRS_I8_PROBE
 #define LRS_I8_PROBE 0
 #endif
+#ifndef LRS_I8_PROBE_K
+#define LRS_I8_PROBE_K 100  // the bulk launch whose CTAs report
+#endif
 #if LRS_I8_PROBE
 #define PRB(...) __VA_ARGS__
 #else
@@ -607,7 +610,7 @@ __global__ void __launch_bounds__(I8_THREADS, I8_TN == 128 ? 1 : 2)
           ptr = (ptr + i8_ng(pass)) & (I8_GROUPS - 1);
         }
       }
-      PRB(if (KIND == 4 && K == 100 && (blockIdx.x % 300) == 0) printf(
+      PRB(if (KIND == 4 && K == LRS_I8_PROBE_K && (blockIdx.x % 997) == 0) printf(
               "PROBE mma cta %d tiles %d total %lld full_wait %lld chunk0(tempty) %lld\n",
               blockIdx.x, t1 - t0, clock64() - c_start, c_full, c_chunk0);)
     }
@@ -686,7 +689,7 @@ __global__ void __launch_bounds__(I8_THREADS, I8_TN == 128 ? 1 : 2)
       asm volatile("bar.sync 1, %0;" ::"n"(32 * I8_EPI) : "memory");  // sj free for the next tile
       PRB(c_red += clock64() - c1;)
     }
-    PRB(if (KIND == 4 && K == 100 && (blockIdx.x % 300) == 0 && lane == 0 && (w == 2 || w == 9))
+    PRB(if (KIND == 4 && K == LRS_I8_PROBE_K && (blockIdx.x % 997) == 0 && lane == 0 && (w == 2 || w == 9))
             printf("PROBE epi cta %d warp %d total %lld tfull_wait %lld drain %lld red %lld\n",
                    blockIdx.x, w, clock64() - c_start, c_tf, c_drain, c_red);)
   }
