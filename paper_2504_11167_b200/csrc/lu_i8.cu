@@ -907,6 +907,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8_THREADS, 1)
       // ---- MMA issuer (leader) ---------------------------------------------------------
       int it = 0, ptr = 0, u = 0;
       int uses[I8_GROUPS] = {0, 0, 0, 0};
+      PRB(long long c_full = 0, c_fullp = 0, c_chunk0 = 0; const long long c_start = clock64();)
       for (int t = t0; t < t1; ++t) {
         int p, ia, jb;
         bool own;
@@ -915,12 +916,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8_THREADS, 1)
         for (int pass = 0; pass < I8_NP; ++pass) {
           for (int kc = 0; kc < NCH; ++kc, ++it) {
             const int s = it % ST;
+            PRB(long long c0 = clock64();)
             mbar_wait_trap(&full[s], (it / ST) & 1);
+            PRB(c_full += clock64() - c0; c0 = clock64();)
             mbar_wait_trap(&fullp[s], (it / ST) & 1);
+            PRB(c_fullp += clock64() - c0; c0 = clock64();)
             tc_fence_after();
             const uint32_t a0 = smem_u32(stage + s * I8P_STAGE), b0 = a0 + I8_BLK;
             if (pass == 0) i8p_chunk_mmas<0>(tm, a0, b0, kc == 0, tempty, ptr, uses);
             else i8p_chunk_mmas<1>(tm, a0, b0, kc == 0, tempty, ptr, uses);
+            PRB(if (kc == 0) c_chunk0 += clock64() - c0;)
             umma_commit_pair(&empty[s]);
           }
           umma_commit_pair(&tfull[u & 1]);
@@ -930,6 +935,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8_THREADS, 1)
           ptr = (ptr + i8_ng(pass)) & (I8_GROUPS - 1);
         }
       }
+      PRB(if (K == LRS_I8_PROBE_K && ((blockIdx.x >> 1) % 499) == 0) printf(
+              "PROBE2 mma cl %d items %d total %lld full_wait %lld fullp_wait %lld "
+              "chunk0(tempty) %lld\n",
+              blockIdx.x >> 1, t1 - t0, clock64() - c_start, c_full, c_fullp, c_chunk0);)
     }
   } else {
     // ---- epilogue (both CTAs): drain own TMEM rows, release to the leader, C update ----
