@@ -115,6 +115,9 @@ constexpr int I8_TPC = LRS_I8_TPC;                    // tiles per CTA (bulk)
 #ifndef LRS_I8_PROBE
 #define LRS_I8_PROBE 0
 #endif
+#ifndef LRS_I8_WARP_ISSUE
+#define LRS_I8_WARP_ISSUE 1
+#endif
 #ifndef LRS_I8_PROBE_K
 #define LRS_I8_PROBE_K 100  // the bulk launch whose CTAs report
 #endif
@@ -153,6 +156,29 @@ __device__ __forceinline__ void umma_i8(uint32_t d, uint64_t a, uint64_t b, uint
   else if (COLL == 2) LRS_UMMA_I8(".collector::a::use");
   else LRS_UMMA_I8(".collector::a::lastuse");
 #undef LRS_UMMA_I8
+}
+// the same, issued by ONE elected lane while the whole MMA warp runs the (warp-uniform)
+// issue loop: descriptor arithmetic then stays on the uniform datapath instead of a
+// per-MMA ELECT / R2UR.BROADCAST waterfall of a single-thread loop
+template <int COLL>
+__device__ __forceinline__ void umma_i8_warp(uint32_t d, uint64_t a, uint64_t b, uint32_t acc) {
+#define LRS_UMMA_I8W(Q)                                                                    \
+  asm volatile("{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %4, 0;\n\t"                      \
+               "elect.sync _|e, 0xffffffff;\n\t"                                            \
+               "@e tcgen05.mma.cta_group::1.kind::i8" Q " [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d), \
+               "l"(a), "l"(b), "r"(I8_IDESC), "r"(acc))
+  if (COLL == 0) LRS_UMMA_I8W("");
+  else if (COLL == 1) LRS_UMMA_I8W(".collector::a::fill");
+  else if (COLL == 2) LRS_UMMA_I8W(".collector::a::use");
+  else LRS_UMMA_I8W(".collector::a::lastuse");
+#undef LRS_UMMA_I8W
+}
+__device__ __forceinline__ void umma_commit_warp(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}\n" ::"r"(
+          smem_u32(bar))
+      : "memory");
 }
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   asm volatile(
@@ -471,7 +497,7 @@ __device__ __forceinline__ bool i8_decode(const BandGeom& g, int K, int t, int& 
 // first writes of the groups (p = 1) go to the pass's slots in ring order -- the order the
 // epilogue releases them.  Before its first write a slot waits for the drain of its
 // previous use (uses[slot] counts them).
-template <int PASS>
+template <int PASS, bool WARP = false>
 __device__ __forceinline__ void i8_chunk_mmas(uint32_t tm, uint32_t a0, uint32_t b0, bool first,
                                               uint64_t* tempty, int ptr, const int* uses) {
   constexpr int top = i8_top(PASS), ng = i8_ng(PASS), pmax = i8_pmax(PASS);
@@ -490,10 +516,17 @@ __device__ __forceinline__ void i8_chunk_mmas(uint32_t tm, uint32_t a0, uint32_t
       const uint64_t ad = umma_sdesc(a0 + (pp - 1) * I8_SL, NB * 16, 128);
       const uint64_t bd = umma_sdesc(b0 + (q - 1) * I8_BSL, I8_TN * 16, 128);
       const uint32_t ac = (first && pp == 1) ? 0u : 1u;
-      if (qhi == qlo) umma_i8<0>(dd, ad, bd, ac);
-      else if (q == qhi) umma_i8<1>(dd, ad, bd, ac);
-      else if (q == qlo) umma_i8<3>(dd, ad, bd, ac);
-      else umma_i8<2>(dd, ad, bd, ac);
+      if (WARP) {
+        if (qhi == qlo) umma_i8_warp<0>(dd, ad, bd, ac);
+        else if (q == qhi) umma_i8_warp<1>(dd, ad, bd, ac);
+        else if (q == qlo) umma_i8_warp<3>(dd, ad, bd, ac);
+        else umma_i8_warp<2>(dd, ad, bd, ac);
+      } else {
+        if (qhi == qlo) umma_i8<0>(dd, ad, bd, ac);
+        else if (q == qhi) umma_i8<1>(dd, ad, bd, ac);
+        else if (q == qlo) umma_i8<3>(dd, ad, bd, ac);
+        else umma_i8<2>(dd, ad, bd, ac);
+      }
     }
   }
 }
@@ -580,8 +613,8 @@ __global__ void __launch_bounds__(I8_THREADS, I8_TN == 128 ? 1 : 2)
       }
     }
   } else if (w == 1) {
-    // ---- MMA issuer ------------------------------------------------------------------
-    if (lane == 0) {
+    // ---- MMA issuer: the whole warp runs the loop, one elected lane issues ------------
+    if (LRS_I8_WARP_ISSUE || lane == 0) {
       int it = 0, ptr = 0, u = 0;
       int uses[I8_GROUPS] = {0, 0, 0, 0};
       PRB(long long c_full = 0, c_chunk0 = 0; const long long c_start = clock64();)
@@ -597,20 +630,23 @@ __global__ void __launch_bounds__(I8_THREADS, I8_TN == 128 ? 1 : 2)
             PRB(c_full += clock64() - c0; c0 = clock64();)
             tc_fence_after();
             const uint32_t a0 = smem_u32(stage + s * I8_STAGE), b0 = a0 + I8_BLK;
-            if (pass == 0) i8_chunk_mmas<0>(tm, a0, b0, kc == 0, tempty, ptr, uses);
-            else if (pass == 1) i8_chunk_mmas<1>(tm, a0, b0, kc == 0, tempty, ptr, uses);
-            else i8_chunk_mmas<2 % I8_NP>(tm, a0, b0, kc == 0, tempty, ptr, uses);
+            constexpr bool WI = LRS_I8_WARP_ISSUE != 0;
+            if (pass == 0) i8_chunk_mmas<0, WI>(tm, a0, b0, kc == 0, tempty, ptr, uses);
+            else if (pass == 1) i8_chunk_mmas<1, WI>(tm, a0, b0, kc == 0, tempty, ptr, uses);
+            else i8_chunk_mmas<2 % I8_NP, WI>(tm, a0, b0, kc == 0, tempty, ptr, uses);
             PRB(if (kc == 0) c_chunk0 += clock64() - c0;)
-            umma_commit(&empty[s]);
+            if (WI) umma_commit_warp(&empty[s]);
+            else umma_commit(&empty[s]);
           }
-          umma_commit(&tfull[u & 1]);
+          if (LRS_I8_WARP_ISSUE) umma_commit_warp(&tfull[u & 1]);
+          else umma_commit(&tfull[u & 1]);
           ++u;
 #pragma unroll
           for (int gi = 0; gi < i8_ng(pass); ++gi) ++uses[(ptr + gi) & (I8_GROUPS - 1)];
           ptr = (ptr + i8_ng(pass)) & (I8_GROUPS - 1);
         }
       }
-      PRB(if (KIND == 4 && K == LRS_I8_PROBE_K && (blockIdx.x % 997) == 0) printf(
+      PRB(if (KIND == 4 && K == LRS_I8_PROBE_K && (blockIdx.x % 997) == 0 && lane == 0) printf(
               "PROBE mma cta %d tiles %d total %lld full_wait %lld chunk0(tempty) %lld\n",
               blockIdx.x, t1 - t0, clock64() - c_start, c_full, c_chunk0);)
     }
