@@ -57,6 +57,24 @@ constexpr int I8_SL = NB * I8_KC;                     // 4096 B: one A slice of 
 constexpr int I8_BLK = I8_S * I8_SL;                  // 28 KB: all A slices of one chunk
 // output columns per CTA: 128 (one CTA per SM, all 512 TMEM columns) or 64 (two CTAs per SM
 // with 256 columns each, so one CTA's MMAs run while the other drains)
+// LRS_I8_ONEPASS=1: 128 x 64 work items with all seven group accumulators resident (7 x 64
+// of the 512 TMEM columns, an eighth 64-column slot spare), ONE pass over K -- no slices
+// streamed twice, no pass hand-off inside a tile; the slots form a ring of 8, so the next
+// item starts in the spare slot and follows the drain of the previous one slot by slot
+#ifndef LRS_I8_ONEPASS
+#define LRS_I8_ONEPASS 0
+#endif
+#if LRS_I8_ONEPASS
+#undef LRS_I8_TN
+#define LRS_I8_TN 64
+#undef LRS_I8_NPASS
+#define LRS_I8_NPASS 1
+#undef LRS_I8_EPC
+#define LRS_I8_EPC 32
+#ifndef LRS_I8_STAGES
+#define LRS_I8_STAGES 5  // 5 x 42 KB
+#endif
+#endif
 #ifndef LRS_I8_TN
 #define LRS_I8_TN 128
 #endif
@@ -68,8 +86,8 @@ constexpr int I8_STAGE = I8_BLK + I8_BBLK;            // A + B
 #ifndef LRS_I8_STAGES
 #define LRS_I8_STAGES 4  // 4 x 56 KB + 2 KB barriers fit the 227 KB opt-in limit
 #endif
-constexpr int I8_STAGES = I8_TN == 128 ? LRS_I8_STAGES : 2;
-constexpr int I8_GROUPS = 4;                          // accumulators per pass (4 x TN cols)
+constexpr int I8_STAGES = (I8_TN == 128 || LRS_I8_ONEPASS) ? LRS_I8_STAGES : 2;
+constexpr int I8_GROUPS = LRS_I8_ONEPASS ? 8 : 4;     // TMEM accumulator slots (x TN columns)
 // Passes over K per tile.  Pass k forms the groups s = top(k), top(k) - 1, .. (ng(k) of them)
 // from slices 1..pmax(k).  The group accumulators take the TMEM slots as a ring: a pass
 // takes the next ng slots after the previous pass's, so while the epilogue drains one pass
@@ -83,12 +101,12 @@ constexpr int I8_GROUPS = 4;                          // accumulators per pass (
 #define LRS_I8_NPASS 2  // measured: 3 passes 0.84 ms vs 2 passes 0.75 ms per c2 launch
 #endif
 constexpr int I8_NP = LRS_I8_NPASS;
-static_assert(I8_NP == 2 || I8_NP == 3, "pass split");
+static_assert(I8_NP >= 1 && I8_NP <= 3, "pass split");
 __host__ __device__ constexpr int i8_top(int k) {
-  return I8_NP == 3 ? (k == 0 ? 8 : k == 1 ? 6 : 4) : (k == 0 ? 8 : 4);
+  return I8_NP == 1 ? 8 : I8_NP == 3 ? (k == 0 ? 8 : k == 1 ? 6 : 4) : (k == 0 ? 8 : 4);
 }
 __host__ __device__ constexpr int i8_ng(int k) {
-  return I8_NP == 3 ? (k == 2 ? 3 : 2) : (k == 0 ? 4 : 3);
+  return I8_NP == 1 ? 7 : I8_NP == 3 ? (k == 2 ? 3 : 2) : (k == 0 ? 4 : 3);
 }
 __host__ __device__ constexpr int i8_pmax(int k) { return i8_top(k) - 1 < I8_S ? i8_top(k) - 1 : I8_S; }
 constexpr int I8_PRODUCTS = 28;                       // digit-slice products per K chunk
@@ -118,6 +136,23 @@ constexpr int I8_TPC = LRS_I8_TPC;                    // tiles per CTA (bulk)
 #ifndef LRS_I8_WARP_ISSUE
 #define LRS_I8_WARP_ISSUE 1
 #endif
+// LRS_I8_EPI64=1: the epilogue sums the group accumulators of a tile as two exact 64-bit
+// integers (H_A = sum_{s=5..8} G_s 2^(8(8-s)) < 2^51, H_B = sum_{s=2..4} G_s 2^(8(4-s)) < 2^43:
+// one IMAD.WIDE per value while the TMEM slot is held, instead of an FP64 add and FMA) and
+// rounds once: 2^-28 (H_A 2^-32 + H_B)
+#ifndef LRS_I8_EPI64
+#define LRS_I8_EPI64 0
+#endif
+// LRS_I8_CRMW=1: C is updated by plain loads and stores in batches of LRS_I8_CBATCH columns
+// (every C element of a launch belongs to exactly one thread, so no atomic is needed; REDG
+// retires ~1.3 cycles per LANE and SM -- ~20k cycles for the 16,384 elements of a tile, as
+// long as the tile's MMAs).  0: fire-and-forget L2 reductions.  Same rounding either way.
+#ifndef LRS_I8_CRMW
+#define LRS_I8_CRMW 1
+#endif
+#ifndef LRS_I8_CBATCH
+#define LRS_I8_CBATCH 16
+#endif
 #ifndef LRS_I8_PROBE_K
 #define LRS_I8_PROBE_K 100  // the bulk launch whose CTAs report
 #endif
@@ -127,7 +162,8 @@ constexpr int I8_TPC = LRS_I8_TPC;                    // tiles per CTA (bulk)
 #define PRB(...)
 #endif
 constexpr size_t I8_SMEM = (size_t)I8_STAGES * I8_STAGE + 2048;
-static_assert(I8_TN == 128 || I8_SMEM * 2 <= 227 * 1024, "two CTAs per SM");
+constexpr int I8_CTAS_PER_SM = (I8_TN == 128 || LRS_I8_ONEPASS) ? 1 : 2;
+static_assert(I8_SMEM * I8_CTAS_PER_SM <= 227 * 1024, "shared memory per SM");
 
 size_t lu_i8_chunk_bytes(int steps) { return (size_t)i8_nch(steps) * I8_BLK; }
 
@@ -222,6 +258,23 @@ __device__ __forceinline__ void mbar_wait_trap(uint64_t* bar, unsigned parity) {
         : "memory");
     if (ok) return;
     if (i > (SLEEP ? (1l << 24) : (1l << 28))) __trap();
+  }
+}
+// the same for a whole (converged) warp: the loop exits on a warp vote, so control flow and
+// everything computed after it stay warp-uniform for the compiler (uniform registers feed
+// the tcgen05 descriptors without per-MMA R2UR moves)
+__device__ __forceinline__ void mbar_wait_warp(uint64_t* bar, unsigned parity) {
+  for (long i = 0;; ++i) {
+    uint32_t ok = 0;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (__all_sync(0xffffffffu, ok != 0)) return;
+    if (i > (1l << 28)) __trap();
   }
 }
 __device__ __forceinline__ void red_add_f64(double* p, double v) {
@@ -497,9 +550,12 @@ __device__ __forceinline__ bool i8_decode(const BandGeom& g, int K, int t, int& 
 // first writes of the groups (p = 1) go to the pass's slots in ring order -- the order the
 // epilogue releases them.  Before its first write a slot waits for the drain of its
 // previous use (uses[slot] counts them).
+// used / par: bit masks over the slots -- the slot has been used before / parity of its
+// number of uses (its tempty barrier has completed that many phases once drained)
 template <int PASS, bool WARP = false>
 __device__ __forceinline__ void i8_chunk_mmas(uint32_t tm, uint32_t a0, uint32_t b0, bool first,
-                                              uint64_t* tempty, int ptr, const int* uses) {
+                                              uint64_t* tempty, int ptr, uint32_t used,
+                                              uint32_t par) {
   constexpr int top = i8_top(PASS), ng = i8_ng(PASS), pmax = i8_pmax(PASS);
 #pragma unroll
   for (int pp = 1; pp <= pmax; ++pp) {
@@ -508,8 +564,9 @@ __device__ __forceinline__ void i8_chunk_mmas(uint32_t tm, uint32_t a0, uint32_t
     for (int q = I8_S; q >= 1; --q) {
       if (q > qhi || q < qlo) continue;
       const int slot = (ptr + top - pp - q) & (I8_GROUPS - 1);
-      if (first && pp == 1 && uses[slot] > 0) {
-        mbar_wait_trap(&tempty[slot], (uses[slot] - 1) & 1);
+      if (first && pp == 1 && ((used >> slot) & 1u)) {
+        if (WARP) mbar_wait_warp(&tempty[slot], ((par >> slot) & 1u) ^ 1u);
+        else mbar_wait_trap(&tempty[slot], ((par >> slot) & 1u) ^ 1u);
         tc_fence_after();
       }
       const uint32_t dd = tm + slot * I8_TN;
@@ -537,7 +594,7 @@ __device__ __forceinline__ void i8_chunk_mmas(uint32_t tm, uint32_t a0, uint32_t
 // C is written at stride 2 into the interleaved complex tile).  lu_i8_slice_z_kernel makes
 // the panels.
 template <int KIND, int STEPS, bool CPLX = false>
-__global__ void __launch_bounds__(I8_THREADS, I8_TN == 128 ? 1 : 2)
+__global__ void __launch_bounds__(I8_THREADS, I8_CTAS_PER_SM)
     lu_i8_gemm_kernel(BandGeom g, double* tiles, int K, I8Panel pn, int total, int tpc) {
   constexpr int I8_NCH = i8_nch(STEPS) * (CPLX ? 2 : 1);
   constexpr int CS = CPLX ? 2 : 1;  // doubles per tile element
@@ -616,7 +673,7 @@ __global__ void __launch_bounds__(I8_THREADS, I8_TN == 128 ? 1 : 2)
     // ---- MMA issuer: the whole warp runs the loop, one elected lane issues ------------
     if (LRS_I8_WARP_ISSUE || lane == 0) {
       int it = 0, ptr = 0, u = 0;
-      int uses[I8_GROUPS] = {0, 0, 0, 0};
+      uint32_t used = 0u, par = 0u;
       PRB(long long c_full = 0, c_chunk0 = 0; const long long c_start = clock64();)
       for (int t = t0; t < t1; ++t) {
         int p, ia, jb, h, part;
@@ -626,14 +683,15 @@ __global__ void __launch_bounds__(I8_THREADS, I8_TN == 128 ? 1 : 2)
           for (int kc = 0; kc < I8_NCH; ++kc, ++it) {
             const int s = it % I8_STAGES;
             PRB(long long c0 = clock64();)
-            mbar_wait_trap(&full[s], (it / I8_STAGES) & 1);
+            constexpr bool WI = LRS_I8_WARP_ISSUE != 0;
+            if (WI) mbar_wait_warp(&full[s], (it / I8_STAGES) & 1);
+            else mbar_wait_trap(&full[s], (it / I8_STAGES) & 1);
             PRB(c_full += clock64() - c0; c0 = clock64();)
             tc_fence_after();
             const uint32_t a0 = smem_u32(stage + s * I8_STAGE), b0 = a0 + I8_BLK;
-            constexpr bool WI = LRS_I8_WARP_ISSUE != 0;
-            if (pass == 0) i8_chunk_mmas<0, WI>(tm, a0, b0, kc == 0, tempty, ptr, uses);
-            else if (pass == 1) i8_chunk_mmas<1, WI>(tm, a0, b0, kc == 0, tempty, ptr, uses);
-            else i8_chunk_mmas<2 % I8_NP, WI>(tm, a0, b0, kc == 0, tempty, ptr, uses);
+            if (pass == 0) i8_chunk_mmas<0, WI>(tm, a0, b0, kc == 0, tempty, ptr, used, par);
+            else if (pass == 1) i8_chunk_mmas<1 % I8_NP, WI>(tm, a0, b0, kc == 0, tempty, ptr, used, par);
+            else i8_chunk_mmas<2 % I8_NP, WI>(tm, a0, b0, kc == 0, tempty, ptr, used, par);
             PRB(if (kc == 0) c_chunk0 += clock64() - c0;)
             if (WI) umma_commit_warp(&empty[s]);
             else umma_commit(&empty[s]);
@@ -642,7 +700,11 @@ __global__ void __launch_bounds__(I8_THREADS, I8_TN == 128 ? 1 : 2)
           else umma_commit(&tfull[u & 1]);
           ++u;
 #pragma unroll
-          for (int gi = 0; gi < i8_ng(pass); ++gi) ++uses[(ptr + gi) & (I8_GROUPS - 1)];
+          for (int gi = 0; gi < i8_ng(pass); ++gi) {
+            const uint32_t bit = 1u << ((ptr + gi) & (I8_GROUPS - 1));
+            used |= bit;
+            par ^= bit;
+          }
           ptr = (ptr + i8_ng(pass)) & (I8_GROUPS - 1);
         }
       }
@@ -669,9 +731,19 @@ __global__ void __launch_bounds__(I8_THREADS, I8_TN == 128 ? 1 : 2)
         for (int r = 0; r < I8_TN / 32; ++r) sj[lane + 32 * r] = exp2i(eb[lane + 32 * r]);
       }
       const uint32_t trow = tm + ((uint32_t)(32 * qd) << 16) + ch * I8_EPC;
+#if LRS_I8_EPI64
+      // hA: groups 8..5 as one exact integer; groups 4..2 likewise in hB when the registers
+      // allow (32 columns per warp), else in FP64 on top of the converted hA
+      constexpr bool B64 = I8_EPC <= 32;
+      constexpr long long MAGIC = 0x4338000000000000ll;  // bits of 2^52 + 2^51
+      constexpr double MAGICD = 6755399441055744.0;
+      long long hA[I8_EPC], hB[B64 ? I8_EPC : 1];
+      double acc[B64 ? 1 : I8_EPC];
+#else
       double acc[I8_EPC];
 #pragma unroll
       for (int j = 0; j < I8_EPC; ++j) acc[j] = 0.0;
+#endif
 #pragma unroll
       for (int pass = 0; pass < I8_NP; ++pass, ++u) {
         PRB(long long c0 = clock64();)
@@ -703,11 +775,34 @@ __global__ void __launch_bounds__(I8_THREADS, I8_TN == 128 ? 1 : 2)
               __syncwarp();
               if (lane == 0) mbar_arrive1(&tempty[slot]);
             }
+#if LRS_I8_EPI64
+            {
+              const int sg = i8_top(pass) - gi;  // group s (the loops are fully unrolled)
+              const long long wt = 1ll << (8 * ((sg >= 5 ? 8 : 4) - sg));
+#pragma unroll
+              for (int j = 0; j < 32; ++j) {
+                const int c = h2 * 32 + j;
+                const long long gv = (long long)(int)v[j];
+                if (sg == 8) hA[c] = gv;
+                else if (sg >= 5) hA[c] += gv * wt;
+                else if (B64) {
+                  if (sg == 4) hB[c] = gv;
+                  else hB[c] += gv * wt;
+                } else {
+                  if (sg == 4)  // |hA| < 2^51: 2^52 + 2^51 + hA is exact
+                    acc[c] = (__longlong_as_double(hA[c] + MAGIC) - MAGICD) * exp2i(4 - 64);
+                  acc[c] = fma(__hiloint2double(0x43300000, (int)(v[j] ^ 0x80000000u)) - BIAS, sc,
+                               acc[c]);
+                }
+              }
+            }
+#else
 #pragma unroll
             for (int j = 0; j < 32; ++j)
               acc[h2 * 32 + j] = fma(
                   __hiloint2double(0x43300000, (int)(v[j] ^ 0x80000000u)) - BIAS, sc,
                   acc[h2 * 32 + j]);
+#endif
           }
         }
         ptr = (ptr + i8_ng(pass)) & (I8_GROUPS - 1);
@@ -718,9 +813,39 @@ __global__ void __launch_bounds__(I8_THREADS, I8_TN == 128 ? 1 : 2)
       // C -= 2^(ea+eb) acc as fire-and-forget L2 reductions: no load round trip in the
       // epilogue, and with one contribution per element fl(c + (-r)) == fl(c - r) exactly
       if (!LRS_I8_EXP) {
+        // r(j) = the update of C(i, j); C -= r either by load / store batches or by L2 reductions
+#if LRS_I8_EPI64
+        const double si28 = si * exp2i(-28);
+#endif
+        auto upd = [&](int j) -> double {
+#if LRS_I8_EPI64
+          if (B64) {
+            const double dA = __longlong_as_double(hA[j] + MAGIC) - MAGICD;
+            const double dB = __longlong_as_double(hB[B64 ? j : 0] + MAGIC) - MAGICD;
+            const double u = fma(dA, 2.3283064365386963e-10 /* 2^-32 */, dB);  // one rounding
+            return u * si28 * sj[ch * I8_EPC + j];
+          }
+          return acc[B64 ? 0 : j] * si * sj[ch * I8_EPC + j];
+#else
+          return acc[j] * si * sj[ch * I8_EPC + j];
+#endif
+        };
+#if LRS_I8_CRMW
+        constexpr int CB = LRS_I8_CBATCH;
+        static_assert(I8_EPC % CB == 0, "C batch");
 #pragma unroll
-        for (int j = 0; j < I8_EPC; ++j)
-          red_add_f64(C + ((int64_t)j * NB + i) * CS, -(acc[j] * si * sj[ch * I8_EPC + j]));
+        for (int j0 = 0; j0 < I8_EPC; j0 += CB) {
+          double cv[CB];
+#pragma unroll
+          for (int jj = 0; jj < CB; ++jj) cv[jj] = __ldcg(C + ((int64_t)(j0 + jj) * NB + i) * CS);
+#pragma unroll
+          for (int jj = 0; jj < CB; ++jj)
+            __stcg(C + ((int64_t)(j0 + jj) * NB + i) * CS, cv[jj] - upd(j0 + jj));
+        }
+#else
+#pragma unroll
+        for (int j = 0; j < I8_EPC; ++j) red_add_f64(C + ((int64_t)j * NB + i) * CS, -upd(j));
+#endif
       }
       asm volatile("bar.sync 1, %0;" ::"n"(32 * I8_EPI) : "memory");  // sj free for the next tile
       PRB(c_red += clock64() - c1;)
@@ -821,6 +946,7 @@ __device__ __forceinline__ bool i8p_decode(const BandGeom& g, int K, int t, int 
   return true;
 }
 
+#if !LRS_I8_ONEPASS
 template <int PASS>
 __device__ __forceinline__ void i8p_chunk_mmas(uint32_t tm, uint32_t a0, uint32_t b0, bool first,
                                                uint64_t* tempty, int ptr, const int* uses) {
@@ -1046,6 +1172,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8_THREADS, 1)
   }
 }
 
+#endif  // !LRS_I8_ONEPASS
+
 // ---- INT8 peak (roofline denominator): every SM issues M=128, N=256, K=32 MMAs from
 // resident operands into 2 accumulators (the best-rate shape), 8 K-steps each
 __global__ void __launch_bounds__(128, 1) i8_peak_kernel(int iters, int* out) {
@@ -1176,6 +1304,7 @@ size_t lu_i8_panel_bytes_z(const BandGeom& g) {
          sizeof(int) * (size_t)g.P * (g.wl + g.wu) * NB;
 }
 
+#if !LRS_I8_ONEPASS
 template <int STEPS>
 static void i8_gemm2_launch(Ctx* c, cudaStream_t s, const BandGeom& g, double* tiles, int K,
                             const I8Panel& pn) {
@@ -1197,18 +1326,26 @@ static void i8_gemm2_launch(Ctx* c, cudaStream_t s, const BandGeom& g, double* t
   LRS_LAUNCHED(c);
 }
 
+#endif
+
 bool lu_i8_2sm() {
+#if LRS_I8_ONEPASS
+  return false;
+#else
   const char* e = std::getenv("LRS_I8_2SM");
   return e && e[0] == '1';
+#endif
 }
 
 void launch_lu_i8_gemm(Ctx* c, cudaStream_t s, const BandGeom& g, double* tiles, int K, int kind,
                        int steps, const I8Panel& pn) {
+#if !LRS_I8_ONEPASS
   if (kind == 4 && lu_i8_2sm()) {
     if (steps == 4) i8_gemm2_launch<4>(c, s, g, tiles, K, pn);
     else i8_gemm2_launch<2>(c, s, g, tiles, K, pn);
     return;
   }
+#endif
   if (steps == 4) {
     if (kind == 4) i8_gemm_launch<4, 4>(c, s, g, tiles, K, pn);
     else i8_gemm_launch<3, 4>(c, s, g, tiles, K, pn);
