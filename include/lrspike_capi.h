@@ -167,6 +167,9 @@ typedef struct lrs_fact_info {
   int32_t lu_pairs;             /* steps per bulk LU update launch: 4 (INT8, K = 512), 2, or 0 */
   int32_t pivoted;              /* some block needed row interchanges: partial-pivoting LU */
   int32_t lu_int8;              /* bulk updates ran INT8-sliced on tcgen05 (LRS_LU_I8) */
+  int32_t lu_sym;               /* symmetric blocks (A == A^T bitwise, no interchanges): the LU
+                                   formed the lower trailing tiles only and took each U panel
+                                   from its L panel, U_KJ = diag(U_KK) L_JK^T (LRS_LU_SYM=0: off) */
 } lrs_fact_info;
 
 typedef struct lrs_error_info {

@@ -71,7 +71,7 @@ class FactInfoC(ctypes.Structure):
                 ("lu_flops", i64), ("apply_bytes", i64), ("rank_collapsed", i32),
                 ("variant", i32), ("t_factorize", f64), ("t_lu", f64), ("t_spikes", f64),
                 ("t_precond", f64), ("max_interface_cond", f64), ("lu_pairs", i32),
-                ("pivoted", i32), ("lu_int8", i32)]
+                ("pivoted", i32), ("lu_int8", i32), ("lu_sym", i32)]
 
 
 _OPFN = ctypes.CFUNCTYPE(i32, vp, vp, vp, i64, i64)

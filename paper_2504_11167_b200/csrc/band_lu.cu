@@ -748,12 +748,13 @@ static void real_gemm(Ctx* c, cudaStream_t s, const BandGeom& g, void* tiles, in
   if ((LRS_LU_SKIP == 4 && kind == 4) || (LRS_LU_SKIP == 1 && kind != 4)) return;
   if (kind > 60) {  // kind 60 + m: rows / columns K+1 .. K+m with step K (quad look-ahead)
     const int m = kind - 60;
-    lu_gemm_kernel<6><<<dim3(S * m * (g.wl + g.wu - m), g.P), GEMM_THREADS, GEMM_SMEM, s>>>(
-        g, t, K, status, m);
+    // (symmetric blocks: the column part only, x < m wl)
+    lu_gemm_kernel<6><<<dim3(S * m * (g.sym ? g.wl : g.wl + g.wu - m), g.P), GEMM_THREADS,
+                        GEMM_SMEM, s>>>(g, t, K, status, m);
   } else if (kind == 0) {
     // the two half-tile CTAs of a tile form a cluster (tile_gemm's in-place L panel)
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(S * (g.wl + g.wu), g.P);
+    cfg.gridDim = dim3(S * (g.sym ? g.wl : g.wl + g.wu), g.P);  // sym: the L panel only
     cfg.blockDim = dim3(GEMM_THREADS);
     cfg.dynamicSmemBytes = GEMM_SMEM;
     cfg.stream = s;
@@ -765,6 +766,7 @@ static void real_gemm(Ctx* c, cudaStream_t s, const BandGeom& g, void* tiles, in
     cfg.attrs = at;
     cfg.numAttrs = 1;
     LRS_CUDA(cudaLaunchKernelEx(&cfg, lu_gemm_kernel<0>, g, t, K, status, 0));
+    if (g.sym && g.wu > 0) lu_mirror_kernel<double><<<dim3(g.wu, g.P), 256, 0, s>>>(g, t, K);
   }
   else if (kind == 1 && LRS_LU_PERSISTENT) {
     // each CTA takes at most LRS_REST_TPC half-tiles and retires, so the high-priority
@@ -778,8 +780,8 @@ static void real_gemm(Ctx* c, cudaStream_t s, const BandGeom& g, void* tiles, in
     lu_gemm_kernel<1><<<dim3(S * (g.wl - 1) * (g.wu - 1), g.P), GEMM_THREADS, GEMM_SMEM, s>>>(
         g, t, K, status);
   else if (kind == 2)
-    lu_gemm_kernel<2><<<dim3(S * (g.wl + g.wu - 1), g.P), GEMM_THREADS, GEMM_SMEM, s>>>(g, t, K,
-                                                                                       status);
+    lu_gemm_kernel<2><<<dim3(S * (g.sym ? g.wl : g.wl + g.wu - 1), g.P), GEMM_THREADS, GEMM_SMEM,
+                        s>>>(g, t, K, status);
   else if (kind == 5)
     lu_gemm_kernel<5><<<dim3(S * g.wu, g.P), GEMM_THREADS, GEMM_SMEM, s>>>(g, t, K, status);
   else if (kind == 3)
@@ -877,8 +879,20 @@ static int lu_i8_steps(const BandGeom& g, int num_sms) {
   return tiles >= per_sm * num_sms ? 4 : 2;
 }
 
-int launch_band_lu(Ctx* c, const BandGeom& g, double* tiles, int Tmax, int* status) {
+// The symmetric schedule rides on the INT8 pair / quad schedule (its DMMA kinds 0, 2, 60+m
+// and the INT8 kinds 3, 4 know g.sym); LRS_LU_SYM=0 switches it off.
+bool lu_sym_wanted(const BandGeom& g) {
+  const char* e = std::getenv("LRS_LU_SYM");
+  if (e && e[0] == '0') return false;
+  return g.wl == g.wu && !lu_i8_2sm();
+}
+
+int launch_band_lu(Ctx* c, const BandGeom& g0, double* tiles, int Tmax, int* status, bool sym,
+                   bool* sym_used) {
   lu_attrs();
+  BandGeom g = g0;
+  g.sym = 0;
+  if (sym_used) *sym_used = false;
   LuKernels L{real_diag, real_gemm, LRS_LU_PAIRS != 0};
   DevBuf<uint8_t> buf;
   I8Panel pn[3];  // [0], [1]: the bulk update's buffers (alternating); [2]: the quad
@@ -911,6 +925,10 @@ int launch_band_lu(Ctx* c, const BandGeom& g, double* tiles, int Tmax, int* stat
     }
     L.i8 = pn;
     L.steps = steps;
+    if (sym && lu_sym_wanted(g)) {
+      g.sym = 1;
+      if (sym_used) *sym_used = true;
+    }
   }
   run_band_lu(c, g, tiles, Tmax, status, L);
   return L.i8 != nullptr ? L.steps : 0;

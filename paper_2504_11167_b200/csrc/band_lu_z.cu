@@ -340,7 +340,7 @@ static void z_gemm(Ctx* c, cudaStream_t s, const BandGeom& g, void* tiles, int K
   zc* t = static_cast<zc*>(tiles);
   if (kind == 0) {
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(2 * (g.wl + g.wu), g.P);
+    cfg.gridDim = dim3(2 * (g.sym ? g.wl : g.wl + g.wu), g.P);  // sym: the L panel only
     cfg.blockDim = dim3(ZG_THREADS);
     cfg.dynamicSmemBytes = ZGEMM_SMEM;
     cfg.stream = s;
@@ -352,6 +352,7 @@ static void z_gemm(Ctx* c, cudaStream_t s, const BandGeom& g, void* tiles, int K
     cfg.attrs = at;
     cfg.numAttrs = 1;
     LRS_CUDA(cudaLaunchKernelEx(&cfg, lu_zgemm_kernel<0>, g, t, K, status));
+    if (g.sym && g.wu > 0) lu_mirror_kernel<zc><<<dim3(g.wu, g.P), 256, 0, s>>>(g, t, K);
   }
   else if (kind == 5)
     lu_zgemm_kernel<5><<<dim3(2 * g.wu, g.P), ZG_THREADS, ZGEMM_SMEM, s>>>(g, t, K, status);
@@ -359,8 +360,8 @@ static void z_gemm(Ctx* c, cudaStream_t s, const BandGeom& g, void* tiles, int K
     lu_zgemm_kernel<1><<<dim3(2 * (g.wl - 1) * (g.wu - 1), g.P), ZG_THREADS, ZGEMM_SMEM, s>>>(
         g, t, K, status);
   else
-    lu_zgemm_kernel<2><<<dim3(2 * (g.wl + g.wu - 1), g.P), ZG_THREADS, ZGEMM_SMEM, s>>>(g, t, K,
-                                                                                       status);
+    lu_zgemm_kernel<2><<<dim3(2 * (g.sym ? g.wl : g.wl + g.wu - 1), g.P), ZG_THREADS, ZGEMM_SMEM,
+                         s>>>(g, t, K, status);
 }
 
 static void zgemm_attrs() {
@@ -383,8 +384,12 @@ static void zgemm_attrs() {
 // C_im -= [Ar Ai][Bi; Br], exact integer slices as in the real LU); otherwise (or with
 // LRS_LU_I8=0, or when the panel buffers do not fit) single steps with the 3M DMMA update.
 // Returns the steps per INT8 update (2) or 0.
-int launch_band_lu_z(Ctx* c, const BandGeom& g, zc* tiles, int Tmax, int* status) {
+int launch_band_lu_z(Ctx* c, const BandGeom& g0, zc* tiles, int Tmax, int* status, bool sym,
+                     bool* sym_used) {
   zgemm_attrs();
+  BandGeom g = g0;
+  g.sym = 0;
+  if (sym_used) *sym_used = false;
   LuKernels L{z_diag, z_gemm};
   DevBuf<uint8_t> buf;
   I8Panel pn[2];
@@ -408,6 +413,11 @@ int launch_band_lu_z(Ctx* c, const BandGeom& g, zc* tiles, int Tmax, int* status
     L.i8 = pn;
     L.steps = 2;
     L.cplx = true;
+    // complex symmetric blocks (A == A^T, not Hermitian): the symmetric schedule of band_lu.cu
+    if (sym && lu_sym_wanted(g)) {
+      g.sym = 1;
+      if (sym_used) *sym_used = true;
+    }
   }
   run_band_lu(c, g, tiles, Tmax, status, L);
   return L.i8 ? 2 : 0;

@@ -133,4 +133,45 @@ void launch_csr_transpose(Ctx* c, Mat* m) {
   LRS_LAUNCHED(c);
 }
 
+// A == A^T bitwise (plain transpose; w doubles per value): the transposed CSR (rows sorted by
+// column) equals the CSR itself
+__global__ void csr_equal_kernel(const int* __restrict__ rp, const int* __restrict__ trp,
+                                 int64_t n1, const int* __restrict__ ci,
+                                 const int* __restrict__ tci, const long long* __restrict__ va,
+                                 const long long* __restrict__ tva, int64_t nnz, int w,
+                                 int* differ) {
+  bool bad = false;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nnz;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    bad |= ci[e] != tci[e];
+    for (int q = 0; q < w; ++q) bad |= va[e * w + q] != tva[e * w + q];
+  }
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n1;
+       i += (int64_t)gridDim.x * blockDim.x)
+    bad |= rp[i] != trp[i];
+  if (bad) *differ = 1;
+}
+
+bool mat_is_symmetric(Ctx* c, Mat* m) {
+  if (m->symmetric >= 0) return m->symmetric == 1;
+  if (m->nnz == 0 || m->n == 0) return (m->symmetric = 0) == 1;
+  DevBuf<int> differ;
+  differ.alloc(1);
+  LRS_CUDA(cudaMemsetAsync(differ.get(), 0, sizeof(int), c->stream));
+  {
+    ProfScope ps_(c, K_SETUP);
+    csr_equal_kernel<<<c->num_sms * 4, 256, 0, c->stream>>>(
+        m->row_ptr.get(), m->trow_ptr.get(), m->n + 1, m->col_idx.get(), m->tcol_idx.get(),
+        reinterpret_cast<const long long*>(m->vals.get()),
+        reinterpret_cast<const long long*>(m->tvals.get()), m->nnz,
+        m->scalar == LRS_C128 ? 2 : 1, differ.get());
+    LRS_LAUNCHED(c);
+  }
+  int h = 1;
+  LRS_CUDA(cudaMemcpyAsync(&h, differ.get(), sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  LRS_CUDA(cudaStreamSynchronize(c->stream));
+  m->symmetric = h ? 0 : 1;
+  return m->symmetric == 1;
+}
+
 }  // namespace lrs

@@ -17,6 +17,9 @@ struct BandGeom {
   int wl, wu, W;         // tiles below / above the diagonal, W = wl + wu + 1
   const int64_t* goff;   // global partition row offsets [Pg + 1]
   int p0, Pg;            // global index of local partition 0, global partition count
+  int sym = 0;           // band LU only: the blocks are symmetric, so the LU forms the lower
+                         // trailing tiles (I >= J) and takes each U panel from its L panel,
+                         // U_KJ = diag(U_KK) L_JK^T (band_lu.cu, lu_i8.cu)
 };
 
 // ---- spmv.cu -------------------------------------------------------------------------
@@ -46,8 +49,16 @@ void launch_extract_tiles(Ctx* c, const Mat* m, const BandGeom& g, double* tiles
 // Tiled no-pivot band LU of all partitions (Tmax steps, look-ahead over two streams).
 // status[2p] = min column needing a row interchange, status[2p+1] = min zero-pivot column.
 // returns the steps per INT8-sliced tensor-core update (2 or 4; lu_i8.cu), 0 on DMMA
-int launch_band_lu(Ctx* c, const BandGeom& g, double* tiles, int Tmax, int* status);
-int launch_band_lu_z(Ctx* c, const BandGeom& g, zc* tiles, int Tmax, int* status);
+// sym: the blocks are symmetric (mat_is_symmetric): eligible for the symmetric schedule.
+// Returns the steps per INT8 update (0: DMMA); *sym_used says whether that schedule ran.
+int launch_band_lu(Ctx* c, const BandGeom& g, double* tiles, int Tmax, int* status,
+                   bool sym = false, bool* sym_used = nullptr);
+// A == A^T bitwise (pattern and values; real matrices), cached on the matrix
+bool mat_is_symmetric(Ctx* c, Mat* m);
+int launch_band_lu_z(Ctx* c, const BandGeom& g, zc* tiles, int Tmax, int* status,
+                     bool sym = false, bool* sym_used = nullptr);
+// the symmetric schedule is allowed on this geometry (wl == wu, LRS_LU_SYM != 0, no 2-SM update)
+bool lu_sym_wanted(const BandGeom& g);
 // the INT8 panel buffers fit the free device memory (+ pool cache) with 2 GB to spare
 bool lu_i8_bytes_fit(size_t bytes);
 // bytes of the digit slices of one 128 x 128 tile's K chunks for a D-step update
@@ -73,6 +84,7 @@ size_t lu_i8_panel_bytes_z(const BandGeom& g);
 // kind 3: look-ahead rows / columns K+steps .. K+2 steps-1; kind 4: the bulk (I, J >= K+2 steps)
 void launch_lu_i8_gemm(Ctx* c, cudaStream_t s, const BandGeom& g, double* tiles, int K, int kind,
                        int steps, const I8Panel& pn);
+bool lu_i8_2sm();  // LRS_I8_2SM=1: the bulk update on SM pairs (lu_i8_gemm2_kernel)
 // the look-ahead driver, shared by the real and complex kernels
 struct LuKernels {
   void (*diag)(Ctx*, cudaStream_t, const BandGeom&, void* tiles, int K, int* status);

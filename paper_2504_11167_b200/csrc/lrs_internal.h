@@ -181,6 +181,7 @@ struct Mat {
   DevBuf<double> vals;
   DevBuf<int> trow_ptr, tcol_idx;    // CSR of A^T (spike adjoint couplings)
   DevBuf<double> tvals;
+  int symmetric = -1;                // A == A^T bitwise: -1 not checked yet, 0, 1
 };
 
 struct Fact;  // defined in fact.h

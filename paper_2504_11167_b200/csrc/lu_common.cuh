@@ -88,4 +88,36 @@ __device__ __forceinline__ void diag_inverses_z(zc* A, zc* part, int tid) {
   }
 }
 
+// Symmetric blocks (g.sym): with A_i = A_i^T (plain transpose, also for complex blocks) and
+// no interchanges the trailing matrix stays symmetric, so U_KJ = inv(L_KK) A_KJ =
+// diag(U_KK) L_JK^T: the U panel of step K is the transposed L panel with row a scaled by
+// u_aa (the diagonal tile holds 1 / u_aa on the diagonal of inv(U_KK)).  The upper trailing
+// tiles are then never read, and every trailing update forms the lower tiles only (half the
+// GEMM work of the LU).  One CTA per panel tile, 32 x 32 blocks transposed through shared
+// memory.
+template <class S>
+__global__ void __launch_bounds__(256) lu_mirror_kernel(BandGeom g, S* tiles, int K) {
+  __shared__ S blk[32][33];
+  __shared__ S d[NB];
+  const int p = blockIdx.y, T = g.T[p], J = K + 1 + blockIdx.x;
+  if (J >= T) return;
+  const int64_t base = g.tbase[p];
+  const S* dg = tiles + (base + (int64_t)K * g.W + g.wl) * TILE_ELEMS;
+  const S* src = tiles + (base + (int64_t)J * g.W + (K - J + g.wl)) * TILE_ELEMS;  // L_JK
+  S* dst = tiles + (base + (int64_t)K * g.W + (J - K + g.wl)) * TILE_ELEMS;        // U_KJ
+  if (threadIdx.x < NB) d[threadIdx.x] = s_inv(dg[threadIdx.x * NB + threadIdx.x]);
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  for (int bb = 0; bb < 16; ++bb) {
+    const int a0 = (bb >> 2) * 32, b0 = (bb & 3) * 32;  // block of U: rows a0.., columns b0..
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 4; ++q)  // L_JK[b0 + tx][a0 + ty + 8 q]
+      blk[ty + 8 * q][tx] = src[(int64_t)(a0 + ty + 8 * q) * NB + b0 + tx];
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 4; ++q)  // U_KJ[a0 + tx][b0 + ty + 8 q] = u_aa L_JK[b][a]
+      dst[(int64_t)(b0 + ty + 8 * q) * NB + a0 + tx] = s_mul(d[a0 + tx], blk[tx][ty + 8 * q]);
+  }
+}
+
 }  // namespace lrs

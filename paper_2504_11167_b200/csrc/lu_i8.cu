@@ -504,17 +504,35 @@ __global__ void __launch_bounds__(I8_ZSLICE_THREADS) lu_i8_slice_z_kernel(BandGe
 //   KIND 3 (look-ahead): columns K+D .. K+2D-1 (rows K+D .. K+D-1+wl) and rows
 //                        K+D .. K+2D-1 (columns K+2D .. K+D-1+wu)
 //   KIND 4 (bulk):       I = K+2D .. K+D-1+wl, J = K+2D .. K+D-1+wu
+// Work items per partition.  g.sym (symmetric blocks, wl == wu): only the lower trailing
+// tiles are formed -- kind 4 the triangle I >= J of the bulk window, kind 3 the columns
+// K+D .. K+2D-1 (the rows of the look-ahead come from the mirrored L panels, band_lu.cu).
+template <int KIND, int STEPS>
+__host__ __device__ __forceinline__ int i8_per(const BandGeom& g) {
+  constexpr int D = STEPS;
+  if (KIND == 4) return g.sym ? (g.wl - D) * (g.wl - D + 1) / 2 : (g.wl - D) * (g.wu - D);
+  if (g.sym) return D == 2 ? 2 * g.wl - 1 : D * g.wl;
+  return D * g.wl + D * (g.wu - D);
+}
+
 template <int KIND, int STEPS>
 __device__ __forceinline__ bool i8_decode(const BandGeom& g, int K, int t, int& p, int& ia,
                                           int& jb, int& h) {
   constexpr int D = STEPS;
-  const int per = KIND == 4 ? (g.wl - D) * (g.wu - D) : D * g.wl + D * (g.wu - D);
+  const int per = i8_per<KIND, STEPS>(g);
   h = t % I8_NH;
   t /= I8_NH;
   p = t / per;
   int r = t % per;
   int I, J;
-  if (KIND == 4) {
+  if (KIND == 4 && g.sym) {
+    // row-major over the lower triangle: r = a (a + 1) / 2 + b, b <= a
+    int a = (int)((sqrtf(8.0f * (float)r + 1.0f) - 1.0f) * 0.5f);
+    while ((a + 1) * (a + 2) / 2 <= r) ++a;
+    while (a * (a + 1) / 2 > r) --a;
+    I = K + 2 * D + a;
+    J = K + 2 * D + (r - a * (a + 1) / 2);
+  } else if (KIND == 4) {
     I = K + 2 * D + r / (g.wu - D);
     J = K + 2 * D + r % (g.wu - D);
   } else if (D == 2) {  // pairs: column K+2, column K+3, row K+2, row K+3
@@ -1270,8 +1288,7 @@ static void i8_gemm_launch(Ctx* c, cudaStream_t s, const BandGeom& g, double* ti
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)I8_SMEM));
     attr = true;
   }
-  constexpr int D = STEPS;
-  const int per = KIND == 4 ? (g.wl - D) * (g.wu - D) : D * g.wl + D * (g.wu - D);
+  const int per = i8_per<KIND, STEPS>(g);
   const int total = per * g.P * I8_NH * (CPLX ? 2 : 1);
   if (total <= 0) return;
   // the look-ahead launch (kind 3, on the critical stream) takes fewer tiles per CTA

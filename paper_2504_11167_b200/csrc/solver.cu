@@ -1059,8 +1059,12 @@ Fact* factorize(Ctx* c, Mat* m, const lrs_solver_cfg& cfg, const lrs_comm* comm)
       omega_future = std::async(std::launch::async, make_omega, f->seed, f->Pg, f->p0,
                                 f->p0 + P, f->k, l0);
   }
-  if (cplx) f->lu_int8 = launch_band_lu_z(c, g, sp<zc>(f->tiles), f->Tmax, f->status.get());
-  else f->lu_int8 = launch_band_lu(c, g, f->tiles.get(), f->Tmax, f->status.get());
+  if (cplx)
+    f->lu_int8 = launch_band_lu_z(c, g, sp<zc>(f->tiles), f->Tmax, f->status.get(),
+                                  mat_is_symmetric(c, m), &f->lu_sym);
+  else
+    f->lu_int8 = launch_band_lu(c, g, f->tiles.get(), f->Tmax, f->status.get(),
+                                mat_is_symmetric(c, m), &f->lu_sym);
   // first (global block, column) needing a row interchange / holding an exact zero pivot,
   // agreed over all ranks
   auto first_problem = [&](int which) {
@@ -1174,6 +1178,7 @@ Fact* factorize(Ctx* c, Mat* m, const lrs_solver_cfg& cfg, const lrs_comm* comm)
   in.lu_pairs = f->pivoted ? 0 : (f->lu_int8 ? f->lu_int8 : (!cplx && lu_real_pairs(g) ? 2 : 0));
   in.pivoted = f->pivoted ? 1 : 0;
   in.lu_int8 = f->lu_int8 ? 1 : 0;
+  in.lu_sym = (f->lu_sym && !f->pivoted) ? 1 : 0;
   in.t_lu = elapsed_ms(e0, e1) * 1e-3;
   in.t_spikes = elapsed_ms(e1, e2) * 1e-3;
   in.t_precond = 0.0;

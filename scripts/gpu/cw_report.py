@@ -5,5 +5,5 @@ from tests import test_gpu_lu_int8 as T
 from paper_2504_11167_b200 import api
 
 ctx = api.Context(0)
-for name, scale in (("c3", 24 / 96), ("c4", 0.05)):
-    print(json.dumps(T.componentwise_report(ctx, name, scale)), flush=True)
+for name, scale, sym in (("c3", 24 / 96, False), ("c4", 0.05, False), ("c3", 24 / 96, True)):
+    print(json.dumps(T.componentwise_report(ctx, name, scale, sym=sym)), flush=True)

@@ -14,12 +14,14 @@ from paper_2504_11167_b200.configs import Csr
 pytestmark = pytest.mark.gpu
 
 
-def _factor(ctx, csr, cfg, i8, quad=False, two_sm=None):
-    old = {k: os.environ.get(k) for k in ("LRS_LU_I8", "LRS_LU_QUAD", "LRS_I8_2SM")}
+def _factor(ctx, csr, cfg, i8, quad=False, two_sm=None, sym=None):
+    old = {k: os.environ.get(k) for k in ("LRS_LU_I8", "LRS_LU_QUAD", "LRS_I8_2SM", "LRS_LU_SYM")}
     os.environ["LRS_LU_I8"] = "1" if i8 else "0"
     os.environ["LRS_LU_QUAD"] = "1" if quad else "0"
     if two_sm is not None:
         os.environ["LRS_I8_2SM"] = "1" if two_sm else "0"
+    if sym is not None:
+        os.environ["LRS_LU_SYM"] = "1" if sym else "0"
     try:
         A = api.CsrMatrix.from_csr(ctx, csr)
         return api.factorize(ctx, A, api.SolverConfig(variant="BJ", p=cfg.P, k=cfg.b, n_svd=0))
@@ -51,8 +53,8 @@ def test_int8_2sm_update_bitwise(ctx, name, scale, quad):
     the same integer products and the same FP64 epilogue as the 1-SM kernel: the factors
     are bitwise identical, including an odd last row pair (c3 at 24^3: 3 bulk rows)."""
     cfg = configs.make_config(name, scale)
-    F2 = _factor(ctx, cfg.system(0), cfg, True, quad, two_sm=True)
-    F1 = _factor(ctx, cfg.system(0), cfg, True, quad, two_sm=False)
+    F2 = _factor(ctx, cfg.system(0), cfg, True, quad, two_sm=True, sym=False)
+    F1 = _factor(ctx, cfg.system(0), cfg, True, quad, two_sm=False, sym=False)
     assert F2.info["lu_int8"] == 1
     for i in range(cfg.P):
         assert np.array_equal(F2.tiles(i), F1.tiles(i)), i
@@ -79,6 +81,43 @@ def test_int8_quad_update_matches_dmma(ctx, name, scale):
     cfg = configs.make_config(name, scale)
     assert -(-cfg.b // 128) >= 8
     assert _compare(ctx, cfg.system(0), cfg, quad=True) <= 1e-12
+
+
+@pytest.mark.parametrize("name,scale,quad", [("c3", 24 / 96, False), ("c3", 32 / 96, False),
+                                             ("c3", 32 / 96, True), ("c3", 40 / 96, True),
+                                             ("c5", 0.5, False), ("c5", 0.3, False)])
+def test_symmetric_schedule_matches_full_lu(ctx, name, scale, quad):
+    """Symmetric blocks (c3: A == A^T bitwise): the LU forms the lower trailing tiles only
+    and takes each U panel from its L panel, U_KJ = diag(U_KK) L_JK^T.  Every band tile
+    (L, U and the diagonal inverses) within 1e-12 of the full-schedule INT8 LU and of the
+    DMMA LU, relative to the partition's largest entry; pairs and quads.  c5: the complex
+    symmetric (not Hermitian) shifted systems z I - A, realified INT8 update."""
+    cfg = configs.make_config(name, scale)
+    assert -(-cfg.b // 128) >= (8 if quad else 3)
+    Fs = _factor(ctx, cfg.system(0), cfg, True, quad, sym=True)
+    Ff = _factor(ctx, cfg.system(0), cfg, True, quad, sym=False)
+    Fd = _factor(ctx, cfg.system(0), cfg, False, sym=False)
+    assert Fs.info["lu_sym"] == 1 and Ff.info["lu_sym"] == 0 and Fd.info["lu_sym"] == 0
+    assert Fs.info["lu_int8"] == 1 and not Fs.info["pivoted"]
+    assert Fs.info["lu_pairs"] == (4 if quad else 2)
+    for i in range(cfg.P):
+        a, b, d = Fs.tiles(i), Ff.tiles(i), Fd.tiles(i)
+        sc = np.max(np.abs(d))
+        assert np.max(np.abs(a - b)) / sc <= 1e-12, i
+        assert np.max(np.abs(a - d)) / sc <= 1e-12, i
+
+
+def test_symmetric_schedule_only_for_symmetric_blocks(ctx):
+    """c2 (convection: A != A^T) and a c3 matrix with one perturbed entry keep the full LU."""
+    cfg = configs.make_config("c2", 0.5)
+    assert _factor(ctx, cfg.system(0), cfg, True).info["lu_sym"] == 0
+    cfg = configs.make_config("c3", 24 / 96)
+    m = cfg.matrix
+    vals = m.values.copy()
+    j = int(np.flatnonzero(m.col_idx[: m.row_ptr[1]] != 0)[0])  # an off-diagonal of row 0
+    vals[j] *= 1.0 + 2.0 ** -40
+    F = _factor(ctx, Csr(m.n, m.row_ptr, m.col_idx, vals), cfg, True)
+    assert F.info["lu_sym"] == 0 and F.info["lu_int8"] == 1
 
 
 @pytest.mark.parametrize("e", [-300, 300])
@@ -178,7 +217,7 @@ def _lapack_lu(Ai):
     return L, U
 
 
-def componentwise_error(Ad, L, U, rows):
+def componentwise_error(Ad, L, U, rows, sym=False):
     """Backward error of A = L U over the sampled rows, in long double (64-bit mantissa: the
     residual's own rounding is ~u/2000 of the bounds below).  Returns
       scaled  max |A - LU|_ij / (max_k |L_ik| max_k |U_kj|)   -- the row / column-scaled
@@ -189,11 +228,18 @@ def componentwise_error(Ad, L, U, rows):
               gamma |L||U|); the floor drops structural zeros, where the diagonal tiles'
               stored inverses re-invert to ~1e-20 instead of 0
       buckets the componentwise maximum per band of (|L||U|)_ij / scale: [2^-10, 1],
-              [2^-20, 2^-10), [2^-30, 2^-20), [2^-40, 2^-30)"""
+              [2^-20, 2^-10), [2^-30, 2^-20), [2^-40, 2^-30)
+    sym: factors of the symmetric schedule (U = diag(U) L^T mirrored from L, the lower
+    trailing tiles formed only).  An upper entry (i, j) then carries the integer-split error
+    of its mirror (j, i), whose scale is max|L_j.| max|U_.i|, so the scale of an entry is the
+    larger of its own and its mirror's row x column scale."""
     Lr = L[rows]
     R = np.abs(Ad[rows].astype(np.longdouble) - Lr @ U)
     B = np.abs(Lr) @ np.abs(U)
-    scale = np.abs(Lr).max(axis=1)[:, None] * np.abs(U).max(axis=0)[None, :]
+    rowL, colU = np.abs(L).max(axis=1), np.abs(U).max(axis=0)
+    scale = rowL[rows][:, None] * colU[None, :]
+    if sym:
+        scale = np.maximum(scale, colU[rows][:, None] * rowL[None, :])
     rel = np.where(scale > 0, B / np.where(scale > 0, scale, 1), 0)
     out = {"scaled": float(np.max(R / np.where(scale > 0, scale, 1)))}
     cw = np.where(B > 0, R / np.where(B > 0, B, 1), 0)
@@ -205,15 +251,17 @@ def componentwise_error(Ad, L, U, rows):
     return out
 
 
-def componentwise_report(ctx, name, scale, n_rows=48, seed=0):
+def componentwise_report(ctx, name, scale, n_rows=48, seed=0, sym=False):
     cfg = configs.make_config(name, scale)
     S = cfg.matrix.to_scipy()
     lay = O.make_layout(S.shape[0], cfg.P, cfg.b)
     blocks = O.extract_blocks(S, lay)
-    F8 = _factor(ctx, cfg.matrix, cfg, True)
+    F8 = _factor(ctx, cfg.matrix, cfg, True, sym=sym)
     F64 = _factor(ctx, cfg.matrix, cfg, False)
     assert F8.info["lu_int8"] == 1 and F8.info["lu_pairs"] == 2
-    out = {"config": name, "scale": scale, "u": float(np.finfo(np.float64).eps / 2)}
+    assert F8.info["lu_sym"] == (1 if sym else 0)
+    out = {"config": name, "scale": scale, "u": float(np.finfo(np.float64).eps / 2),
+           "lu_sym": int(sym)}
     rng = np.random.default_rng(seed)
     for i in (0, cfg.P // 2):
         n_i = lay.sizes[i]
@@ -224,13 +272,14 @@ def componentwise_report(ctx, name, scale, n_rows=48, seed=0):
         e = {}
         for tag, LU in (("int8", _effective_lu(F8, i, n_i)), ("dmma", _effective_lu(F64, i, n_i)),
                         ("lapack", _lapack_lu(blocks.A[i]))):
-            e[tag] = componentwise_error(Ad, LU[0], LU[1], rows)
+            e[tag] = componentwise_error(Ad, LU[0], LU[1], rows, sym=sym and tag == "int8")
         out[f"partition{i}"] = e
     return out
 
 
-@pytest.mark.parametrize("name,scale", [("c3", 24 / 96), ("c4", 0.05)])
-def test_int8_componentwise_backward_error(ctx, name, scale):
+@pytest.mark.parametrize("name,scale,sym", [("c3", 24 / 96, False), ("c4", 0.05, False),
+                                            ("c3", 24 / 96, True)])
+def test_int8_componentwise_backward_error(ctx, name, scale, sym):
     """|A_i - L U| for the INT8-sliced factors on the c3 (10^4 coefficient contrast) and c4
     (random band) structures, beside the FP64 DMMA factors and LAPACK dgbtrf.
 
@@ -244,8 +293,10 @@ def test_int8_componentwise_backward_error(ctx, name, scale):
         [2^-30, 2^-20), 1.7e-5 in [2^-40, 2^-30) -- an entry 2^-e below its row x column
         scale keeps ~54 - e bits: normwise FP64, not componentwise.
     Bars: scaled <= 32 u for all three; LAPACK componentwise <= 32 u; DMMA <= 1e-11; INT8 per
-    band <= 64 2^-54 / (band floor), the digit-split bound."""
-    rep = componentwise_report(ctx, name, scale)
+    band <= 64 2^-54 / (band floor), the digit-split bound.
+    sym = True: the symmetric schedule's factors (c3 is symmetric), measured against the
+    symmetrized scale (componentwise_error); sym = False forces the full schedule."""
+    rep = componentwise_report(ctx, name, scale, sym=sym)
     print(rep)
     u = rep["u"]
     for key, e in rep.items():
