@@ -44,6 +44,7 @@ struct Fact {
   // partial pivoting (band_lu_piv.cu): the blocks were factored with row interchanges
   bool pivoted = false;
   int lu_int8 = 0;  // steps per INT8-sliced LU update (2 or 4; lu_i8.cu), 0: DMMA
+  bool blocks_sym = false;  // A == A^T bitwise (and LRS_LU_SYM != 0): the diagonal blocks are symmetric
   bool lu_sym = false;  // symmetric blocks: the LU formed the lower trailing tiles only
   DevBuf<int> ipiv, perm;
   // mixed precision: FP32 copy of the tiles, read for the off-diagonal tiles of the applies

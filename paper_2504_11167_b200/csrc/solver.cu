@@ -697,7 +697,9 @@ bool build_lowrank(Fact* f, int r, int* bad_iface, double* bad_cond, std::vector
     // Tt_apply: Zt[slot] = coupling^H (A_i^-H Q)|tip, Q = columns of Y  (= T^H Q)
     auto Tt_apply = [&]() {
       copy_block(c, Sx, n, Y, n, n, L2);
-      dstage_t(f, Sx, n, L2, true, -1);
+      // real symmetric blocks: A_i^-T = A_i^-1, so the adjoint solve runs the (faster)
+      // forward sweeps L, U instead of U^T, L^T
+      dstage_t(f, Sx, n, L2, !(f->blocks_sym && !IsC<S>::value && !f->pivoted), -1);
       std::vector<CoupleJobT<S>> jobs;
       for (auto [i, side] : spk) {
         CoupleJobT<S> j{};
@@ -1065,6 +1067,10 @@ Fact* factorize(Ctx* c, Mat* m, const lrs_solver_cfg& cfg, const lrs_comm* comm)
   else
     f->lu_int8 = launch_band_lu(c, g, f->tiles.get(), f->Tmax, f->status.get(),
                                 mat_is_symmetric(c, m), &f->lu_sym);
+  {
+    const char* e = std::getenv("LRS_LU_SYM");
+    f->blocks_sym = mat_is_symmetric(c, m) && !(e && e[0] == '0');
+  }
   // first (global block, column) needing a row interchange / holding an exact zero pivot,
   // agreed over all ranks
   auto first_problem = [&](int which) {

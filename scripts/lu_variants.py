@@ -43,7 +43,10 @@ if __name__ == "__main__":
         print(json.dumps(one(name, scale, P, R)), flush=True)
         sys.exit(0)
     variants = [("default", {}), ("pairs", {"LRS_LU_QUAD": "0"}), ("quad", {"LRS_LU_QUAD": "1"}),
-                ("quad-mini-dmma", {"LRS_LU_QUAD": "1", "LRS_QUAD_MINI_DMMA": "1"})]
+                ("quad-mini-dmma", {"LRS_LU_QUAD": "1", "LRS_QUAD_MINI_DMMA": "1"}),
+                # the full schedule on symmetric blocks (no effect on c2 / c4)
+                ("sym-off", {"LRS_LU_SYM": "0"}),
+                ("pairs sym-off", {"LRS_LU_QUAD": "0", "LRS_LU_SYM": "0"})]
     if os.environ.get("LRS_VARIANTS_2SM"):
         variants += [("2sm", {"LRS_I8_2SM": "1"}),
                      ("quad+2sm", {"LRS_LU_QUAD": "1", "LRS_I8_2SM": "1"})]
