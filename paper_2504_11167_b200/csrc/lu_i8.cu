@@ -124,6 +124,11 @@ constexpr int I8_TPC = LRS_I8_TPC;                    // tiles per CTA (bulk)
 #ifndef LRS_I8_TPC3
 #define LRS_I8_TPC3 8  // c2 LU medians: 1 tile 0.156 s, 2: 0.155, 4: 0.155, 8: 0.154 (noise level)
 #endif
+// LRS_I8_LDPIPE=1: the epilogue's TMEM loads are software pipelined against the INT32 -> FP64
+// conversion (two 32-column register buffers); 0: load, wait, convert per batch
+#ifndef LRS_I8_LDPIPE
+#define LRS_I8_LDPIPE 1
+#endif
 // LRS_I8_EXP (timing experiments only, wrong results): 1 skips the epilogue arithmetic,
 // 2 also skips the operand copies
 #ifndef LRS_I8_EXP
@@ -237,6 +242,15 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t* v) {
 }
 __device__ __forceinline__ void tmem_ld_wait() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+// Ties 32 registers filled by an earlier tcgen05.ld to this point of the volatile-asm order
+// (right after tcgen05.wait::ld): their readers depend on these outputs, so the compiler
+// cannot schedule them above the wait when other work sits between the load and the wait.
+__device__ __forceinline__ void reg_fence32(uint32_t* v) {
+#pragma unroll
+  for (int q = 0; q < 32; q += 8)
+    asm volatile("" : "+r"(v[q]), "+r"(v[q + 1]), "+r"(v[q + 2]), "+r"(v[q + 3]), "+r"(v[q + 4]),
+                      "+r"(v[q + 5]), "+r"(v[q + 6]), "+r"(v[q + 7]));
 }
 __device__ __forceinline__ void mbar_arrive1(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
@@ -778,16 +792,41 @@ __global__ void __launch_bounds__(I8_THREADS, I8_CTAS_PER_SM)
         }
         // drain in ring order (the next pass reuses the first slots first), smallest
         // group weight first for the FP64 accumulation
+#if LRS_I8_LDPIPE
+        // two 32-column register buffers: the TMEM load of batch b + 1 is in flight while
+        // batch b converts, and a slot is released as soon as its last load has landed
+        // (not after the conversion of the batch before it)
+        uint32_t vb[2][32];
+        {
+          const int slot0 = ptr & (I8_GROUPS - 1);
+#pragma unroll
+          for (int c8 = 0; c8 < 32; c8 += 8) tmem_ld8(trow + slot0 * I8_TN + c8, vb[0] + c8);
+        }
+#endif
 #pragma unroll
         for (int gi = 0; gi < i8_ng(pass); ++gi) {
           const int slot = (ptr + gi) & (I8_GROUPS - 1);
           const double sc = exp2i(4 - 8 * (i8_top(pass) - gi));
 #pragma unroll
           for (int h2 = 0; h2 < I8_EPC / 32; ++h2) {
+#if LRS_I8_LDPIPE
+            constexpr int NB2 = I8_EPC / 32;
+            const int b = gi * NB2 + h2;
+            uint32_t* v = vb[b & 1];
+            tmem_ld_wait();
+            reg_fence32(v);
+            if (b + 1 < i8_ng(pass) * NB2) {
+              const int slot1 = (ptr + (b + 1) / NB2) & (I8_GROUPS - 1);
+#pragma unroll
+              for (int c8 = 0; c8 < 32; c8 += 8)
+                tmem_ld8(trow + slot1 * I8_TN + ((b + 1) % NB2) * 32 + c8, vb[(b + 1) & 1] + c8);
+            }
+#else
             uint32_t v[32];
 #pragma unroll
             for (int c8 = 0; c8 < 32; c8 += 8) tmem_ld8(trow + slot * I8_TN + h2 * 32 + c8, v + c8);
             tmem_ld_wait();
+#endif
             if (h2 == I8_EPC / 32 - 1) {  // the warp's part of the slot is in registers: release it
               tc_fence_before();
               __syncwarp();
