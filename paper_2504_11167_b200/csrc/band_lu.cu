@@ -865,16 +865,18 @@ static bool lu_i8_wanted(const BandGeom& g, const LuKernels& L) {
 // pair) and four serial diagonal factorizations per quad lengthen the critical stream.
 // They pay when the bulk launch is large against that chain: measured (profiles/
 // r02_lu_variants_*.jsonl) c3 at P = 64 (305k tiles per quad launch, 2060 per SM) LU
-// 1.167 s vs 1.237 s with pairs; c2 (6.3k tiles, 42 per SM) 0.162 s vs 0.152 s.  So quads
-// when the first bulk launch holds >= LRS_QUAD_TILES_PER_SM (200) tiles per SM;
-// LRS_LU_QUAD=0 / 1 forces pairs / quads.
+// 1.167 s vs 1.237 s with pairs; c2 (6.3k tiles, 42 per SM) 0.162 s vs 0.152 s with the
+// all-DMMA look-ahead inside the quad.  With the pair-form look-ahead (run_band_lu) quads
+// are level with pairs on c2 or ahead (session 4: 0.148 vs 0.146 s; session 5's boxes:
+// 0.166 vs 0.181 s), so quads when the first bulk launch holds >= LRS_QUAD_TILES_PER_SM
+// (40) tiles per SM; LRS_LU_QUAD=0 / 1 forces pairs / quads.
 static int lu_i8_steps(const BandGeom& g, int num_sms) {
   if (!(g.wl >= 8 && g.wu >= 8)) return 2;
   const char* e = std::getenv("LRS_LU_QUAD");
   if (e && e[0] == '1') return 4;
   if (e && e[0] == '0') return 2;
   const char* t = std::getenv("LRS_QUAD_TILES_PER_SM");
-  const double per_sm = t ? std::atof(t) : 200.0;
+  const double per_sm = t ? std::atof(t) : 40.0;
   const double tiles = (double)g.P * (g.wl - 4) * (g.wu - 4);
   return tiles >= per_sm * num_sms ? 4 : 2;
 }
