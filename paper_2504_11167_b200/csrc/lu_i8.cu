@@ -129,6 +129,11 @@ constexpr int I8_TPC = LRS_I8_TPC;                    // tiles per CTA (bulk)
 #ifndef LRS_I8_LDPIPE
 #define LRS_I8_LDPIPE 1
 #endif
+// LRS_I8_CPREFETCH=1: the producer prefetches the tile's C block into L2 when it starts the
+// tile's operand loads, ~1.5 tiles before the epilogue's reductions reach it
+#ifndef LRS_I8_CPREFETCH
+#define LRS_I8_CPREFETCH 1
+#endif
 // LRS_I8_EXP (timing experiments only, wrong results): 1 skips the epilogue arithmetic,
 // 2 also skips the operand copies
 #ifndef LRS_I8_EXP
@@ -680,7 +685,8 @@ __global__ void __launch_bounds__(I8_THREADS, I8_CTAS_PER_SM)
       for (int t = t0; t < t1; ++t) {
         int p, ia, jb, h, part;
         if (!decode(t, p, ia, jb, h, part)) continue;
-        if (part == 0) bulk_prefetch_l2(ctile(p, ia, jb, h), sizeof(double) * NB * I8_TN * CS);
+        if (LRS_I8_CPREFETCH && part == 0)
+          bulk_prefetch_l2(ctile(p, ia, jb, h), sizeof(double) * NB * I8_TN * CS);
         const uint8_t* a = pn.A + ((int64_t)p * g.wl + ia) * I8_NCH * I8_BLK;
         const uint8_t* b =
             pn.B + ((((int64_t)p * g.wu + jb) * CS + part) * I8_NH + h) * I8_NCH * I8_BBLK;
