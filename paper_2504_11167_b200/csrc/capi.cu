@@ -3,6 +3,7 @@
 // exception classes carry (proj/core/include/lrspike/errors.hpp:11-94).
 #include <algorithm>
 #include <cmath>
+#include <chrono>
 #include <cstring>
 #include <memory>
 #include <new>
@@ -266,6 +267,37 @@ lrs_status lrs_mat_upload_csr(lrs_ctx* c, int64_t n, int64_t nnz, const int64_t*
       ci = ci_h.data();
       va = va_h.data();
     }
+    const bool trace = std::getenv("LRS_UPLOAD_TRACE") != nullptr;
+    auto now = [] { return std::chrono::steady_clock::now(); };
+    auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+    const auto t_begin = now();
+    // The device arrays first: the values and the column indices (int64 -> a device
+    // temporary, narrowed to int32 by a kernel) travel while the host threads validate.
+    // A failed validation synchronizes the stream before the buffers unwind.
+    m->row_ptr.alloc(n + 1);
+    m->col_idx.alloc(std::max<int64_t>(nnz, 1));
+    m->vals.alloc(std::max<int64_t>(nnz, 1) * w);
+    DevBuf<int64_t> ci64;
+    struct SyncOnError {
+      cudaStream_t s;
+      bool armed = true;
+      ~SyncOnError() { if (armed) cudaStreamSynchronize(s); }
+    } sync_guard{c->stream};
+    if (nnz) {
+      if (mem == LRS_MEM_DEVICE) {
+        LRS_CUDA(cudaMemcpyAsync(m->vals.get(), values, sizeof(double) * nnz * w,
+                                 cudaMemcpyDeviceToDevice, c->stream));
+        launch_narrow_i64(c, col_idx, m->col_idx.get(), nnz);
+      } else {
+        ci64.alloc(nnz);
+        LRS_CUDA(cudaMemcpyAsync(ci64.get(), ci, sizeof(int64_t) * nnz, cudaMemcpyHostToDevice,
+                                 c->stream));
+        launch_narrow_i64(c, ci64.get(), m->col_idx.get(), nnz);
+        LRS_CUDA(cudaMemcpyAsync(m->vals.get(), va, sizeof(double) * nnz * w,
+                                 cudaMemcpyHostToDevice, c->stream));
+      }
+    }
+    const auto t_issued = now();
     auto absv = [&](int64_t p) {
       return w == 1 ? std::fabs(va[p]) : std::hypot(va[2 * p], va[2 * p + 1]);
     };
@@ -280,7 +312,7 @@ lrs_status lrs_mat_upload_csr(lrs_ctx* c, int64_t n, int64_t nnz, const int64_t*
       double dsum = 0.0, tsum = 0.0;
     };
     std::vector<Part> parts((size_t)nch);
-    std::vector<int> rp32(n + 1), ci32(nnz);
+    std::vector<int> rp32(n + 1);
     auto work = [&](int64_t c0, int64_t c1) {
       for (int64_t ch = c0; ch < c1; ++ch) {
         Part& pt = parts[ch];
@@ -291,7 +323,6 @@ lrs_status lrs_mat_upload_csr(lrs_ctx* c, int64_t n, int64_t nnz, const int64_t*
             const int64_t j = ci[p];
             if (j < 0 || j >= n) { pt.bad = 2; pt.bad_row = i; break; }
             if (p > rp[i] && j <= ci[p - 1]) { pt.bad = 3; pt.bad_row = i; break; }
-            ci32[p] = (int)j;
             if (j > i) pt.ku = std::max(pt.ku, j - i);
             if (j < i) pt.kl = std::max(pt.kl, i - j);
             const double a = absv(p);
@@ -310,6 +341,7 @@ lrs_status lrs_mat_upload_csr(lrs_ctx* c, int64_t n, int64_t nnz, const int64_t*
       for (auto& t : th) t.join();
     }
     rp32[n] = (int)rp[n];
+    const auto t_valid = now();
     int64_t ku = 0, kl = 0;
     double dsum = 0.0, tsum = 0.0;
     for (const Part& pt : parts) {
@@ -332,17 +364,18 @@ lrs_status lrs_mat_upload_csr(lrs_ctx* c, int64_t n, int64_t nnz, const int64_t*
     m->diag_weight = tsum > 0 ? dsum / tsum : 0.0;
     const double cells = (double)(ku + kl + 1) * (double)n;
     m->band_density = cells > 0 ? (double)nnz / cells : 0.0;
-    // device CSR with int32 indices; the transpose is built on the device (csr.cu)
-    m->row_ptr.alloc(n + 1);
-    m->col_idx.alloc(std::max<int64_t>(nnz, 1));
-    m->vals.alloc(std::max<int64_t>(nnz, 1) * w);
-    LRS_CUDA(cudaMemcpy(m->row_ptr.get(), rp32.data(), sizeof(int) * (n + 1), cudaMemcpyHostToDevice));
-    if (nnz) {
-      LRS_CUDA(cudaMemcpy(m->col_idx.get(), ci32.data(), sizeof(int) * nnz, cudaMemcpyHostToDevice));
-      LRS_CUDA(cudaMemcpy(m->vals.get(), va, sizeof(double) * nnz * w, cudaMemcpyHostToDevice));
-    }
+    // device CSR with int32 indices (col_idx / values are already on their way); the
+    // transpose is built on the device (csr.cu)
+    LRS_CUDA(cudaMemcpyAsync(m->row_ptr.get(), rp32.data(), sizeof(int) * (n + 1),
+                             cudaMemcpyHostToDevice, c->stream));
     launch_csr_transpose(c, m.get());
+    const auto t_launched = now();
     LRS_CUDA(cudaStreamSynchronize(c->stream));
+    sync_guard.armed = false;
+    if (trace)
+      std::fprintf(stderr, "lrs upload: alloc + copy issue %.1f ms, validate %.1f ms, transpose "
+                   "issue %.1f ms, wait %.1f ms\n", ms(t_begin, t_issued), ms(t_issued, t_valid),
+                   ms(t_valid, t_launched), ms(t_launched, now()));
   });
   if (s == LRS_OK) {
     *out = m.release();

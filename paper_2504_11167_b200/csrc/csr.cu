@@ -133,6 +133,20 @@ void launch_csr_transpose(Ctx* c, Mat* m) {
   LRS_LAUNCHED(c);
 }
 
+// int64 column indices (the reference's index_t, matrix.hpp:11) -> the device's int32
+__global__ void narrow_i64_kernel(const long long* __restrict__ src, int* __restrict__ dst,
+                                  int64_t cnt) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < cnt;
+       e += (int64_t)gridDim.x * blockDim.x)
+    dst[e] = (int)src[e];
+}
+void launch_narrow_i64(Ctx* c, const int64_t* src, int* dst, int64_t cnt) {
+  if (cnt <= 0) return;
+  narrow_i64_kernel<<<c->num_sms * 8, 256, 0, c->stream>>>(
+      reinterpret_cast<const long long*>(src), dst, cnt);
+  LRS_LAUNCHED(c);
+}
+
 // A == A^T bitwise (plain transpose; w doubles per value): the transposed CSR (rows sorted by
 // column) equals the CSR itself
 __global__ void csr_equal_kernel(const int* __restrict__ rp, const int* __restrict__ trp,

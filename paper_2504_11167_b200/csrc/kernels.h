@@ -53,6 +53,8 @@ void launch_extract_tiles(Ctx* c, const Mat* m, const BandGeom& g, double* tiles
 // Returns the steps per INT8 update (0: DMMA); *sym_used says whether that schedule ran.
 int launch_band_lu(Ctx* c, const BandGeom& g, double* tiles, int Tmax, int* status,
                    bool sym = false, bool* sym_used = nullptr);
+// dst[e] = (int)src[e] on the context stream (device arrays)
+void launch_narrow_i64(Ctx* c, const int64_t* src, int* dst, int64_t cnt);
 // A == A^T bitwise (pattern and values; real matrices), cached on the matrix
 bool mat_is_symmetric(Ctx* c, Mat* m);
 int launch_band_lu_z(Ctx* c, const BandGeom& g, zc* tiles, int Tmax, int* status,
