@@ -76,3 +76,61 @@ def test_solve_matches_oracle_fixture(ctx, case):
     assert rep.residual_final <= cfg.tol
     assert abs(rep.iterations - meta["iterations"]) <= 2
     assert rel <= 1e-8
+
+
+@pytest.mark.parametrize("name,P,shift", [("c3", 64, None), ("c5", 16, 2)],
+                         ids=["c3_full_P64", "c5_full_P16_shift2"])
+def test_full_size_properties(ctx, name, P, shift):
+    """Size-independent properties at BASELINE's full sizes, where the oracle cannot run
+    inside a test (c3: the bench workload, symmetric INT8 quad schedule; c5: one complex
+    contour system, complex symmetric INT8 pair schedule, 16 right-hand sides):
+
+    * block-solve round trips on two partitions: A_i solve_block(R) = R and
+      A_i^H solve_block_adjoint(R) = R with A_i taken from the host CSR (scipy), to 1e-12 (measured 1e-15 / 1e-14);
+    * the apply is linear (1e-12) and repeatable bit for bit;
+    * the library's SpMV equals scipy's (1e-14), and the solve's reported residual equals
+      the residual recomputed on the host from x."""
+    cfg = configs.make_config(name, 1.0, P)
+    csr = cfg.matrix if shift is None else cfg.system(shift)
+    S = csr.to_scipy().tocsr()
+    n = S.shape[0]
+    cplx = shift is not None
+    A = api.CsrMatrix.from_csr(ctx, csr)
+    F = api.factorize(ctx, A, api.SolverConfig(variant="T", p=cfg.P, k=cfg.b, n_svd=cfg.r,
+                                               seed=cfg.seed))
+    assert F.info["lu_int8"] == 1 and F.info["lu_sym"] == 1 and not F.info["pivoted"]
+    rng = np.random.default_rng(11)
+
+    def rand(rows, cols):
+        v = rng.uniform(-1, 1, (rows, cols))
+        if cplx:
+            v = v + 1j * rng.uniform(-1, 1, (rows, cols))
+        return np.asfortranarray(v)
+
+    rel = lambda a, b: float(np.linalg.norm(a - b) / np.linalg.norm(b))
+    for i in (0, cfg.P // 2):
+        o, ni = F.offsets[i], F.sizes[i]
+        Ai = S[o:o + ni, o:o + ni]
+        R = rand(ni, 3)
+        e1 = rel(Ai @ F.solve_block(i, R), R)
+        e2 = rel(Ai.conj().T @ F.solve_block_adjoint(i, R), R)
+        print(f"{name} partition {i}: round trip {e1:.2e}, adjoint {e2:.2e}")
+        assert e1 <= 1e-12 and e2 <= 1e-12, i
+    nc = 2
+    f, g = rand(n, nc), rand(n, nc)
+    Mf, Mg = F.apply_precond_T(f), F.apply_precond_T(g)
+    assert np.array_equal(Mf, F.apply_precond_T(f))
+    e3 = rel(F.apply_precond_T(np.asfortranarray(2.0 * f - 3.0 * g)), 2.0 * Mf - 3.0 * Mg)
+    e4 = rel(A.spmv(f), S @ f)
+    print(f"{name}: apply linearity {e3:.2e}, spmv vs scipy {e4:.2e}")
+    assert e3 <= 1e-12 and e4 <= 1e-14
+    rhs = cfg.rhs if not cplx else np.asfortranarray(cfg.rhs[:, :2].astype(np.complex128))
+    if name == "c3":
+        return  # the solve of the bench workload is test_solve_matches_oracle_fixture[c3_s1_P64]
+    it = api.IterConfig(tol=cfg.tol, method=cfg.method, restart=cfg.m or 30, max_iters=2000)
+    x, rep, _F = api.solve(A, rhs, it=it, F=F)
+    assert rep.converged and rep.residual_final <= cfg.tol
+    res = max(np.linalg.norm(rhs[:, j] - S @ x[:, j]) / np.linalg.norm(rhs[:, j])
+              for j in range(rhs.shape[1]))
+    assert res <= cfg.tol * (1 + 1e-6)
+    assert abs(res - rep.residual_final) <= 1e-3 * cfg.tol
