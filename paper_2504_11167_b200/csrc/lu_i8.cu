@@ -134,6 +134,9 @@ constexpr int I8_TPC = LRS_I8_TPC;                    // tiles per CTA (bulk)
 #ifndef LRS_I8_CPREFETCH
 #define LRS_I8_CPREFETCH 1
 #endif
+#ifndef LRS_I8_SYM_ORDER
+#define LRS_I8_SYM_ORDER 0
+#endif
 // LRS_I8_EXP (timing experiments only, wrong results): 1 skips the epilogue arithmetic,
 // 2 also skips the operand copies
 #ifndef LRS_I8_EXP
@@ -546,11 +549,19 @@ __device__ __forceinline__ bool i8_decode(const BandGeom& g, int K, int t, int& 
   int I, J;
   if (KIND == 4 && g.sym) {
     // row-major over the lower triangle: r = a (a + 1) / 2 + b, b <= a
+    // (LRS_I8_SYM_ORDER=1: column-major -- the mirrored walk, consecutive items share B_J)
+    if (LRS_I8_SYM_ORDER == 1) r = per - 1 - r;
     int a = (int)((sqrtf(8.0f * (float)r + 1.0f) - 1.0f) * 0.5f);
     while ((a + 1) * (a + 2) / 2 <= r) ++a;
     while (a * (a + 1) / 2 > r) --a;
+    int b = r - a * (a + 1) / 2;
+    if (LRS_I8_SYM_ORDER == 1) {
+      const int m = g.wl - D, a2 = m - 1 - b;
+      b = m - 1 - a;
+      a = a2;
+    }
     I = K + 2 * D + a;
-    J = K + 2 * D + (r - a * (a + 1) / 2);
+    J = K + 2 * D + b;
   } else if (KIND == 4) {
     I = K + 2 * D + r / (g.wu - D);
     J = K + 2 * D + r % (g.wu - D);
