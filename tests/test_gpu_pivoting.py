@@ -136,3 +136,33 @@ def test_pivoted_complex_lowrank_solve_parity(ctx):
     assert rep.converged and repo.converged
     assert abs(rep.iterations - repo.iterations) <= 2
     assert _rel(x, xo) <= 1e-8
+
+
+def test_symmetric_block_that_interchanges_leaves_the_symmetric_schedule(ctx):
+    """A symmetric band whose blocks need row interchanges (a dominant symmetric band with a
+    few diagonal entries shrunk to 1e-6): the symmetric no-interchange schedule starts
+    (A == A^T, band of >= 3 tiles), its pivot test fires on the L panel, and the blocks are
+    redone on the partial-pivoting path -- fact_info reports pivoted, not lu_sym; block solves
+    equal LAPACK's."""
+    n, k, P = 6000, 520, 2
+    rng = np.random.default_rng(21)
+    offs = list(range(1, k + 1))
+    up = sp.diags([rng.standard_normal(n - d) for d in offs], offs, shape=(n, n)).tocsr()
+    A = (up + up.T).tocsr()
+    d = np.asarray(abs(A).sum(axis=1)).ravel() * 1.2 + 1e-3
+    weak = rng.choice(n, size=12, replace=False)
+    d[weak] = 1e-6
+    S = (A + sp.diags(d)).tocsr()
+    S.sort_indices()
+    assert abs(S - S.T).max() == 0.0
+    lay = O.make_layout(n, P, k)
+    blocks = O.extract_blocks(S, lay)
+    fos = [O.factorize_block(Ai) for Ai in blocks.A]
+    assert any(fo.swaps > 0 for fo in fos)
+    F = api.factorize(ctx, _gpu(ctx, S), api.SolverConfig(variant="BJ", p=P, k=k, n_svd=0))
+    assert F.info["pivoted"] == 1 and F.info["lu_sym"] == 0
+    R = np.asfortranarray(rng.standard_normal((lay.sizes[0], 2)))
+    for i in range(P):
+        R = np.asfortranarray(rng.standard_normal((lay.sizes[i], 2)))
+        assert _rel(F.solve_block(i, R), O.solve_block(fos[i], R)) < 1e-8
+        assert _rel(blocks.A[i].toarray() @ F.solve_block(i, R), R) < 1e-8
