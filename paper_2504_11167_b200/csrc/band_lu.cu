@@ -766,7 +766,10 @@ static void real_gemm(Ctx* c, cudaStream_t s, const BandGeom& g, void* tiles, in
     cfg.attrs = at;
     cfg.numAttrs = 1;
     LRS_CUDA(cudaLaunchKernelEx(&cfg, lu_gemm_kernel<0>, g, t, K, status, 0));
-    if (g.sym && g.wu > 0) lu_mirror_kernel<double><<<dim3(g.wu, g.P), 256, 0, s>>>(g, t, K);
+    if (g.sym && g.wu > 0) {
+      lu_mirror_kernel<double><<<dim3(g.wu, g.P), 256, 0, s>>>(g, t, K);
+      LRS_LAUNCHED(c);
+    }
   }
   else if (kind == 1 && LRS_LU_PERSISTENT) {
     // each CTA takes at most LRS_REST_TPC half-tiles and retires, so the high-priority

@@ -352,7 +352,10 @@ static void z_gemm(Ctx* c, cudaStream_t s, const BandGeom& g, void* tiles, int K
     cfg.attrs = at;
     cfg.numAttrs = 1;
     LRS_CUDA(cudaLaunchKernelEx(&cfg, lu_zgemm_kernel<0>, g, t, K, status));
-    if (g.sym && g.wu > 0) lu_mirror_kernel<zc><<<dim3(g.wu, g.P), 256, 0, s>>>(g, t, K);
+    if (g.sym && g.wu > 0) {
+      lu_mirror_kernel<zc><<<dim3(g.wu, g.P), 256, 0, s>>>(g, t, K);
+      LRS_LAUNCHED(c);
+    }
   }
   else if (kind == 5)
     lu_zgemm_kernel<5><<<dim3(2 * g.wu, g.P), ZG_THREADS, ZGEMM_SMEM, s>>>(g, t, K, status);
