@@ -538,6 +538,9 @@ def run_ours(args):
                     "traffic_source": _ncu_traffic(f"{args.config}_P{cfg.P}_lu_i8").get("source"),
                     "launches": int(upd_n), "avg_launch_ms": avg_launch_s * 1e3,
                     "int8_ops_per_launch": ops_launch,
+                    # 1.0: every trailing tile; ~0.51: the symmetric schedule's lower tiles
+                    # (the ops counted above are the ones issued, not the full schedule's)
+                    "tiles_share_of_full_schedule": sym_scale,
                     "fp64_equiv": {"achieved": achieved_tf, "unit": "TFLOP/s",
                                    "dmma_peak": dmma_peak,
                                    "ratio_to_dmma_peak": achieved_tf / dmma_peak if dmma_peak else None,
