@@ -155,6 +155,8 @@ lrs_status lrs_ctx_create(int device, void* stream, lrs_ctx** out) {
     int lo_prio = 0, hi_prio = 0;
     LRS_CUDA(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
     LRS_CUDA(cudaStreamCreateWithPriority(&c->stream_hi, cudaStreamNonBlocking, hi_prio));
+    LRS_CUDA(cudaStreamCreateWithFlags(&c->stream_copy, cudaStreamNonBlocking));
+    LRS_CUDA(cudaEventCreateWithFlags(&c->ev_omega, cudaEventDisableTiming));
     pool_stream_open(c->stream);
     c->stage_cap = size_t(8) << 20;
     LRS_CUDA(cudaMallocHost(reinterpret_cast<void**>(&c->stage), c->stage_cap));
@@ -171,6 +173,12 @@ static void ctx_teardown(Ctx* c) {
   pool_stream_retire(c->stream);
   if (c->stage) cudaFreeHost(c->stage);
   if (c->dots_host) cudaFreeHost(c->dots_host);
+  if (c->stream_copy) {
+    cudaStreamSynchronize(c->stream_copy);
+    cudaStreamDestroy(c->stream_copy);
+  }
+  if (c->omega_host) cudaFreeHost(c->omega_host);
+  if (c->ev_omega) cudaEventDestroy(c->ev_omega);
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
   if (c->own_stream) cudaStreamDestroy(c->stream);

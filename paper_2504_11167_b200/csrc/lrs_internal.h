@@ -113,6 +113,12 @@ struct Ctx {
   // cudaFreeHost per solve cost milliseconds and synchronize the device)
   static constexpr size_t DOTS_HOST_BYTES = sizeof(double) * 64 * MAX_RHS * 2 * 3;  // 3 slots
   double* dots_host = nullptr;
+  // spike test matrices Omega: page-locked staging (grown on demand, reused across
+  // factorizations) and the copy stream a host thread uploads them on while the band LU runs
+  double* omega_host = nullptr;
+  size_t omega_host_cap = 0;
+  cudaStream_t stream_copy = nullptr;
+  cudaEvent_t ev_omega = nullptr;
   // profiling: (class, start, end) event triples, summed on demand
   bool prof = false;
   uint32_t prof_mask = ~0u;  // classes timed while profiling (bit k: class k)

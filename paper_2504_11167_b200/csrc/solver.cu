@@ -286,15 +286,15 @@ void apply_precond_t(Fact* f, const S* in, int64_t ldi, S* out, int64_t ldo, int
 // Drawn on the host with the shared counter-based generator (bit-identical to the
 // checker's Omega), split over host threads: every draw is a pure function of (seed,
 // stream, index), so the result does not depend on the thread count.
-std::vector<double> make_omega(uint64_t seed, int Pg, int plo, int phi, int64_t k, int l) {
-  std::vector<double> h((size_t)Pg * 2 * k * l, 0.0);
+void fill_omega(double* h, uint64_t seed, int Pg, int plo, int phi, int64_t k, int l) {
+  std::memset(h, 0, sizeof(double) * (size_t)Pg * 2 * k * l);
   std::vector<std::pair<int, int>> slots;
   for (int i = plo; i < phi; ++i)
     for (int side = 0; side < 2; ++side)
       if (!((side == LRS_SIDE_T && i == Pg - 1) || (side == LRS_SIDE_W && i == 0)))
         slots.push_back({i, side});
   const int64_t per = k * l, total = per * (int64_t)slots.size();
-  if (total == 0) return h;
+  if (total == 0) return;
   unsigned nt = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
   nt = (unsigned)std::min<int64_t>(nt, std::max<int64_t>(1, total / 65536));
   auto work = [&](int64_t e0, int64_t e1) {
@@ -308,7 +308,47 @@ std::vector<double> make_omega(uint64_t seed, int Pg, int plo, int phi, int64_t 
   for (unsigned t = 1; t < nt; ++t) th.emplace_back(work, total * t / nt, total * (t + 1) / nt);
   work(0, total / nt);
   for (auto& t : th) t.join();
+}
+std::vector<double> make_omega(uint64_t seed, int Pg, int plo, int phi, int64_t k, int l) {
+  std::vector<double> h((size_t)Pg * 2 * k * l);
+  fill_omega(h.data(), seed, Pg, plo, phi, k, l);
   return h;
+}
+
+// Omega drawn into the context's page-locked staging buffer and uploaded on the copy stream
+// by a host thread, both while the band LU runs: dev (real, Pg * 2 * k * l doubles) is valid
+// for the main stream once it has waited for c->ev_omega.  ev_alloc orders the copy after
+// whatever used dev's pool block before.  Returns false (and leaves dev alone) on any error:
+// the caller then draws and copies Omega synchronously.
+bool omega_upload_task(Ctx* c, double* dev, cudaEvent_t ev_alloc, uint64_t seed, int Pg, int plo,
+                       int phi, int64_t k, int l) {
+  const size_t cnt = (size_t)Pg * 2 * k * l;
+  if (cudaSetDevice(c->device) != cudaSuccess) return false;
+  if (c->omega_host_cap < cnt) {
+    if (c->omega_host) cudaFreeHost(c->omega_host);
+    c->omega_host = nullptr;
+    c->omega_host_cap = 0;
+    if (cudaMallocHost(reinterpret_cast<void**>(&c->omega_host), sizeof(double) * cnt) !=
+        cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    c->omega_host_cap = cnt;
+  }
+  fill_omega(c->omega_host, seed, Pg, plo, phi, k, l);
+  if (cudaStreamWaitEvent(c->stream_copy, ev_alloc, 0) != cudaSuccess) return false;
+  if (cudaMemcpyAsync(dev, c->omega_host, sizeof(double) * cnt, cudaMemcpyHostToDevice,
+                      c->stream_copy) != cudaSuccess)
+    return false;
+  return cudaEventRecord(c->ev_omega, c->stream_copy) == cudaSuccess;
+}
+
+template <class S>
+__global__ void omega_expand_kernel(const double* __restrict__ src, S* __restrict__ dst,
+                                    int64_t cnt) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < cnt;
+       e += (int64_t)gridDim.x * blockDim.x)
+    dst[e] = s_real<S>(src[e]);
 }
 
 // spike_mode = coupling (BASELINE.json north_star setup (1)):
@@ -598,7 +638,7 @@ bool finish_interfaces(Fact* f, int r, int* bad_iface, double* bad_cond) {
 }
 
 template <class S>
-bool build_lowrank(Fact* f, int r, int* bad_iface, double* bad_cond, std::vector<double>* pre) {
+bool build_lowrank(Fact* f, int r, int* bad_iface, double* bad_cond, const double* omega_dev) {
   Ctx* c = f->ctx;
   Mat* m = f->mat;
   const int Pg = f->Pg, p0 = f->p0, P = f->P;
@@ -640,10 +680,13 @@ bool build_lowrank(Fact* f, int r, int* bad_iface, double* bad_cond, std::vector
   auto gsize = [&](int i) { return f->goff[i + 1] - f->goff[i]; };
   // Omega from the shared counter-based generator, normally drawn by a
   // host thread while the band LU ran
-  {
-    std::vector<double> h = (pre && pre->size() == (size_t)Pg * 2 * k * l)
-                                ? std::move(*pre)
-                                : make_omega(f->seed, Pg, p0, p0 + P, k, l);
+  if (omega_dev) {
+    // uploaded by omega_upload_task while the LU ran (the main stream already waits on it)
+    const int64_t cnt = (int64_t)Pg * 2 * k * l;
+    omega_expand_kernel<S><<<c->num_sms * 8, 256, 0, c->stream>>>(omega_dev, Om, cnt);
+    LRS_LAUNCHED(c);
+  } else {
+    std::vector<double> h = make_omega(f->seed, Pg, p0, p0 + P, k, l);
     if constexpr (IsC<S>::value) {
       std::vector<double> hz(h.size() * 2, 0.0);
       for (size_t e = 0; e < h.size(); ++e) hz[2 * e] = h[e];
@@ -1052,14 +1095,31 @@ Fact* factorize(Ctx* c, Mat* m, const lrs_solver_cfg& cfg, const lrs_comm* comm)
     f->coupled = any_c > 0 && f->Pg > 1;
   }
   // the host draws Omega for the spike SVDs while the GPU runs the band LU
-  std::future<std::vector<double>> omega_future;
+  // a host thread draws Omega for the spike SVDs into page-locked memory and uploads it on
+  // the copy stream while the GPU runs the band LU
+  // (destruction order on an early exit: the future joins the host thread, the guard drains
+  // the copy stream, and only then omega_dev goes back to the pool)
+  DevBuf<double> omega_dev;
+  struct CopyGuard {
+    Ctx* c;
+    cudaEvent_t ev = nullptr;  // recorded on the main stream when omega_dev was allocated
+    ~CopyGuard() {
+      cudaStreamSynchronize(c->stream_copy);
+      if (ev) c->ev_pool.push_back(ev);
+    }
+  } omega_guard{c};
+  std::future<bool> omega_future;
   {
     const int r0 = (int)cfg.n_svd;
     const int l0 = r0 + (cfg.oversample >= 0 ? (int)cfg.oversample : (r0 + 1) / 2);
     if ((f->variant == LRS_VARIANT_T || f->variant == LRS_VARIANT_I ||
-         f->variant == LRS_VARIANT_OTF) && f->Pg > 1 && r0 >= 1 && l0 <= f->k)
-      omega_future = std::async(std::launch::async, make_omega, f->seed, f->Pg, f->p0,
-                                f->p0 + P, f->k, l0);
+         f->variant == LRS_VARIANT_OTF) && f->Pg > 1 && r0 >= 1 && l0 <= f->k) {
+      omega_dev.alloc((size_t)f->Pg * 2 * f->k * l0);
+      omega_guard.ev = c->take_event();
+      LRS_CUDA(cudaEventRecord(omega_guard.ev, c->stream));
+      omega_future = std::async(std::launch::async, omega_upload_task, c, omega_dev.get(),
+                                omega_guard.ev, f->seed, f->Pg, f->p0, f->p0 + P, f->k, l0);
+    }
   }
   if (cplx)
     f->lu_int8 = launch_band_lu_z(c, g, sp<zc>(f->tiles), f->Tmax, f->status.get(),
@@ -1141,10 +1201,13 @@ Fact* factorize(Ctx* c, Mat* m, const lrs_solver_cfg& cfg, const lrs_comm* comm)
       c->in_setup = true;
       bool ok;
       try {
-        std::vector<double> pre;
-        if (attempt == 0 && omega_future.valid()) pre = omega_future.get();
-        ok = cplx ? build_lowrank<zc>(f.get(), r, &bi, &bc, &pre)
-                  : build_lowrank<double>(f.get(), r, &bi, &bc, &pre);
+        const double* pre = nullptr;
+        if (attempt == 0 && omega_future.valid() && omega_future.get()) {
+          LRS_CUDA(cudaStreamWaitEvent(c->stream, c->ev_omega, 0));
+          pre = omega_dev.get();
+        }
+        ok = cplx ? build_lowrank<zc>(f.get(), r, &bi, &bc, pre)
+                  : build_lowrank<double>(f.get(), r, &bi, &bc, pre);
       } catch (...) {
         c->in_setup = false;
         throw;
