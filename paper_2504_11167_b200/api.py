@@ -584,7 +584,14 @@ class SpikeFactorization:
 
     def solve_block(self, i: int, R, adjoint: bool = False):
         """SPEC.md:226-241 on partition i (host arrays)."""
-        R = np.asfortranarray(np.asarray(R, dtype=self.A.dtype).reshape(self.sizes[i], -1))
+        if not 0 <= i < len(self.sizes):
+            raise ParameterError(f"partition index {i} outside [0, {len(self.sizes)})")
+        R = np.asarray(R, dtype=self.A.dtype)
+        if R.ndim == 1:
+            R = R.reshape(-1, 1)
+        if R.ndim != 2 or R.shape[0] != self.sizes[i]:
+            raise DimensionError(f"right-hand side must have {self.sizes[i]} rows (partition {i})")
+        R = np.asfortranarray(R)
         X = np.empty_like(R, order="F")
         _check(lib().lrs_solve_block(self.h, i, R.ctypes.data, R.shape[0], X.ctypes.data,
                                      X.shape[0], R.shape[1], 1 if adjoint else 0, MEM_HOST),

@@ -122,3 +122,35 @@ def test_full_rank_two_partitions_is_exact(ctx):
     assert F.n_svd == cfg.b == Fo.n_svd
     assert repo.iterations == 1 and rep.iterations == 1
     assert rep.residual_final <= 1e-10 and _rel(x, xo) <= 1e-10
+
+
+def test_zero_columns_and_shape_misuse(ctx):
+    """Zero-column blocks pass through as empty results; wrong shapes, dtypes and partition
+    indices raise the typed errors (DimensionError / ParameterError), never a crash."""
+    cfg = configs.make_config("c1", 48 / 256)
+    n = cfg.matrix.n
+    A = api.CsrMatrix.from_csr(ctx, cfg.matrix)
+    F = api.factorize(ctx, A, api.SolverConfig(p=cfg.P, k=cfg.b, n_svd=8, seed=0))
+    assert F.apply_precond_T(np.zeros((n, 0), order="F")).shape == (n, 0)
+    assert A.spmv(np.zeros((n, 0), order="F")).shape == (n, 0)
+    assert F.solve_block(0, np.zeros((F.sizes[0], 0), order="F")).shape == (F.sizes[0], 0)
+    assert api.solve(A, np.zeros((n, 0), order="F"), F=F)[0].shape == (n, 0)
+    with pytest.raises(api.DimensionError):
+        F.apply_precond_T(np.zeros((n - 1, 1), order="F"))
+    with pytest.raises(api.DimensionError):
+        F.apply_precond_T(np.zeros((n, 1), dtype=np.float32, order="F"))
+    with pytest.raises(api.DimensionError):
+        F.apply_precond_T(np.zeros((n, 2), order="C"))
+    with pytest.raises(api.ParameterError):
+        F.solve_block(len(F.sizes), np.zeros((F.sizes[0], 1), order="F"))
+    with pytest.raises(api.DimensionError):
+        F.solve_block(0, np.zeros((F.sizes[0] + 1, 1), order="F"))
+    with pytest.raises(api.ParameterError):
+        api.factorize(ctx, A, api.SolverConfig(p=0, k=cfg.b, n_svd=8))
+    # more right-hand sides than one batch of the multi-RHS kernels: solved in batches
+    B = np.asfortranarray(np.random.default_rng(2).uniform(-1, 1, (n, 70)))
+    X, rep, _ = api.solve(A, B, F=F, it=api.IterConfig(tol=1e-8, method="gmres", restart=30))
+    assert rep.converged
+    S = cfg.matrix.to_scipy()
+    assert max(np.linalg.norm(B[:, j] - S @ X[:, j]) / np.linalg.norm(B[:, j])
+               for j in range(70)) <= 1e-8 * (1 + 1e-6)
