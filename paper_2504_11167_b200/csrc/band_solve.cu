@@ -184,7 +184,9 @@ __device__ __forceinline__ void band_solve_body(BandGeom g, const double* __rest
   auto issue = [&](int q, int st) {
     const int d = q / NCH;
     if (t32 && d != ndeps) {
-      const float* src = t32 + (tile_ptr(d) - tiles) + (size_t)(q % NCH) * CH_COLS * NB;
+      // the FP32 copy is compact: slot -> its index among the in-block tiles
+      const int64_t slot = (tile_ptr(d) - tiles) / TILE_ELEMS;
+      const float* src = t32 + (size_t)g.t32_idx[slot] * TILE_ELEMS + (size_t)(q % NCH) * CH_COLS * NB;
       mbar_expect_tx(&bars[st], CH_COLS * NB * sizeof(float));
       bulk_g2s(ring + (size_t)st * CH_SM, src, CH_COLS * NB * sizeof(float), &bars[st]);
       return;
@@ -689,17 +691,27 @@ void launch_band_solve(Ctx* c, const BandGeom& g, const double* tiles, int mode,
   }
 }
 
-__global__ void tiles_to_fp32_kernel(const double* __restrict__ t, float* __restrict__ t32,
-                                     int64_t n) {
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n;
-       e += (int64_t)gridDim.x * blockDim.x)
-    t32[e] = (float)t[e];
+__global__ void __launch_bounds__(256) tiles_to_fp32_kernel(const double* __restrict__ t,
+                                                            float* __restrict__ t32,
+                                                            const int* __restrict__ idx,
+                                                            int64_t nslots) {
+  for (int64_t s = blockIdx.x; s < nslots; s += gridDim.x) {
+    const int ci = idx[s];
+    if (ci < 0) continue;
+    const double2* src = reinterpret_cast<const double2*>(t + s * TILE_ELEMS);
+    float2* dst = reinterpret_cast<float2*>(t32 + (int64_t)ci * TILE_ELEMS);
+    for (int e = threadIdx.x; e < TILE_ELEMS / 2; e += 256) {
+      const double2 v = src[e];
+      dst[e] = make_float2((float)v.x, (float)v.y);
+    }
+  }
 }
 
-void launch_tiles_to_fp32(Ctx* c, const double* tiles, float* t32, int64_t count) {
-  if (count == 0) return;
+void launch_tiles_to_fp32(Ctx* c, const double* tiles, float* t32, const int* idx,
+                          int64_t nslots) {
+  if (nslots == 0) return;
   ProfScope ps_(c, K_SETUP);
-  tiles_to_fp32_kernel<<<c->num_sms * 8, 256, 0, c->stream>>>(tiles, t32, count);
+  tiles_to_fp32_kernel<<<c->num_sms * 16, 256, 0, c->stream>>>(tiles, t32, idx, nslots);
   LRS_LAUNCHED(c);
 }
 

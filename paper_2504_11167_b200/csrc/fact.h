@@ -49,7 +49,9 @@ struct Fact {
   DevBuf<int> ipiv, perm;
   // mixed precision: FP32 copy of the tiles, read for the off-diagonal tiles of the applies
   bool fp32 = false;
-  DevBuf<float> tiles32;
+  DevBuf<float> tiles32;   // compact: only the tile slots inside their block (t32_idx)
+  DevBuf<int> t32_idx;     // [total_tiles]: slot -> index in tiles32, or -1
+  int64_t tiles32_count = 0;
   // low-rank spikes: u as n x r (global rows, ld n); v^T, sigma in GLOBAL partition slots
   DevBuf<double> uT, uW, vtT, vtW, sT, sW;
   // interfaces with at least one local side (jobs in global interface order)
@@ -109,6 +111,7 @@ struct Fact {
     g.goff = d_goff.get();
     g.p0 = p0;
     g.Pg = Pg;
+    g.t32_idx = fp32 ? t32_idx.get() : nullptr;
     return g;
   }
   Chunks chunks() const {

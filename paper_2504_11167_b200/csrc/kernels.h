@@ -17,6 +17,8 @@ struct BandGeom {
   int wl, wu, W;         // tiles below / above the diagonal, W = wl + wu + 1
   const int64_t* goff;   // global partition row offsets [Pg + 1]
   int p0, Pg;            // global index of local partition 0, global partition count
+  const int* t32_idx = nullptr;  // mixed precision: compact index of every tile slot in the
+                                 // FP32 copy (-1: the slot lies outside its block)
   int sym = 0;           // band LU only: the blocks are symmetric, so the LU forms the lower
                          // trailing tiles (I >= J) and takes each U panel from its L panel,
                          // U_KJ = diag(U_KK) L_JK^T (band_lu.cu, lu_i8.cu)
@@ -139,8 +141,11 @@ void launch_band_solve(Ctx* c, const BandGeom& g, const double* tiles, int mode,
                        int64_t ld, int nrhs, unsigned* flags, unsigned epoch, int* ticket,
                        int p_only, int ntiles, int64_t flag_stride, const float* t32,
                        unsigned long long* mbox);
-// tiles32[e] = (float)tiles[e] for the off-diagonal tiles (mixed-precision apply)
-void launch_tiles_to_fp32(Ctx* c, const double* tiles, float* t32, int64_t count);
+// The FP32 copy of the band factors (mixed-precision apply) holds only the tile slots inside
+// their block, densely: t32[idx[s] * TILE_ELEMS + e] = (float)tiles[s * TILE_ELEMS + e] for
+// the nslots slots s with idx[s] >= 0.
+void launch_tiles_to_fp32(Ctx* c, const double* tiles, float* t32, const int* idx,
+                          int64_t nslots);
 constexpr int ZSOLVE_MAX_RHS = 16 * SOLVE_GROUPS;  // 96
 // complex: modes 2 / 3 are the conjugate transposes U^H, L^H
 void launch_band_solve_z(Ctx* c, const BandGeom& g, const zc* tiles, int mode, zc* x, int64_t ld,
