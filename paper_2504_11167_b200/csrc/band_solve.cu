@@ -383,9 +383,19 @@ __device__ __forceinline__ void band_solve_body(BandGeom g, const double* __rest
     const bool f32 = t32 != nullptr && !diag;
     const int cbase = sub * CH_COLS;
     if (!TRANS && !MMA && f32) {
-#pragma unroll 4
-      for (int cc = hh * 16; cc < hh * 16 + 16; ++cc)
-        acc1 = fma(-(double)chf[cc * NB + row], xs[cbase + cc], acc1);
+      // four independent partial sums per chunk: the FP32 chunk carries half the bytes of
+      // an FP64 one, and a single 16-step dependent FMA chain per chunk (as the FP64 branch
+      // below keeps, for its bitwise guarantees) would bound the sweep below the HBM rate
+      double b0 = 0.0, b1 = 0.0, b2 = 0.0, b3 = 0.0;
+#pragma unroll
+      for (int c4 = 0; c4 < 16; c4 += 4) {
+        const int cc = hh * 16 + c4;
+        b0 = fma(-(double)chf[cc * NB + row], xs[cbase + cc], b0);
+        b1 = fma(-(double)chf[(cc + 1) * NB + row], xs[cbase + cc + 1], b1);
+        b2 = fma(-(double)chf[(cc + 2) * NB + row], xs[cbase + cc + 2], b2);
+        b3 = fma(-(double)chf[(cc + 3) * NB + row], xs[cbase + cc + 3], b3);
+      }
+      acc1 += (b0 + b1) + (b2 + b3);
     } else if (!TRANS && !MMA) {
       // out[row] (+|-)= sum_c Tile[row][c] xs[c], half the chunk columns per thread
 #pragma unroll 4
