@@ -34,6 +34,11 @@ def test_fp32_factors_parity(ctx, name, scale, method):
     assert _rel(y, O.apply_precond_T(Fo, f)) < 1e-10
     assert _rel(F.apply_block_jacobi(f), O.apply_block_jacobi(Fo, f)) < 1e-10
     assert 1e-12 < _rel(y, F64.apply_precond_T(f)) < 1e-5  # FP32 rounding, not FP64
+    # the one-column apply runs the FMA sweeps (four partial sums per FP32 chunk)
+    f1 = np.asfortranarray(f[:, :1])
+    assert _rel(F.apply_precond_T(f1), O.apply_precond_T(Fo, f1)) < 1e-10
+    # the FP32 copy holds only the tile slots inside their block: at most half the FP64 bytes
+    assert F.info["factor_bytes"] - F64.info["factor_bytes"] <= F64.info["factor_bytes"] // 2
     it = api.IterConfig(tol=cfg.tol, method=method, restart=cfg.m or 30, max_iters=500)
     x, rep, _ = api.solve(A, cfg.rhs, it=it, F=F)
     xo, repo, _ = O.solve(S, cfg.rhs, oc, O.IterConfig(tol=cfg.tol, restart=cfg.m or 30,
