@@ -495,7 +495,7 @@ def run_ours(args):
     # the symmetric schedule (info.lu_sym) forms the lower trailing tiles only: its FP64-
     # equivalent work is the full update's scaled by the share of tiles it computes
     sym_scale = 1.0
-    if info.get("lu_sym") and info.get("lu_int8"):
+    if info.get("lu_sym") and lu_steps:
         sizes = _partition_sizes(cfg.matrix.n, cfg.P)
         full = sum(_i8_bulk_tiles(s, info["wl"], info["wu"], info["nb"], lu_steps) for s in sizes)
         half = sum(_i8_bulk_tiles(s, info["wl"], info["wu"], info["nb"], lu_steps, True)

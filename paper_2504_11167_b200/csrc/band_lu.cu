@@ -601,6 +601,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, GEMM_SPLIT) lu_gemm_kernel(BandG
         I = K + 3;
         J = K + 4 + y;
       }
+    } else if (g.sym) {
+      // symmetric blocks: the lower triangle of the bulk window, row-major (x = a (a+1)/2 + b)
+      int a = (int)((sqrtf(8.0f * (float)x + 1.0f) - 1.0f) * 0.5f);
+      while ((a + 1) * (a + 2) / 2 <= x) ++a;
+      while (a * (a + 1) / 2 > x) --a;
+      I = K + 4 + a;
+      J = K + 4 + (x - a * (a + 1) / 2);
     } else {
       I = K + 4 + x / (g.wu - 2);
       J = K + 4 + x % (g.wu - 2);
@@ -787,12 +794,12 @@ static void real_gemm(Ctx* c, cudaStream_t s, const BandGeom& g, void* tiles, in
                         s>>>(g, t, K, status);
   else if (kind == 5)
     lu_gemm_kernel<5><<<dim3(S * g.wu, g.P), GEMM_THREADS, GEMM_SMEM, s>>>(g, t, K, status);
-  else if (kind == 3)
-    lu_gemm_kernel<3><<<dim3(S * (2 * g.wl + 2 * g.wu - 4), g.P), GEMM_THREADS, GEMM_SMEM, s>>>(
-        g, t, K, status);
-  else
-    lu_gemm_kernel<4><<<dim3(S * (g.wl - 2) * (g.wu - 2), g.P), GEMM_THREADS, GEMM_SMEM, s>>>(
-        g, t, K, status);
+  else if (kind == 3)  // (symmetric blocks: columns K+2, K+3 only, the first 2 wl - 1 items)
+    lu_gemm_kernel<3><<<dim3(S * (g.sym ? 2 * g.wl - 1 : 2 * g.wl + 2 * g.wu - 4), g.P),
+                        GEMM_THREADS, GEMM_SMEM, s>>>(g, t, K, status);
+  else  // (symmetric blocks: the lower triangle of the bulk window)
+    lu_gemm_kernel<4><<<dim3(S * (g.sym ? (g.wl - 2) * (g.wl - 1) / 2 : (g.wl - 2) * (g.wu - 2)),
+                             g.P), GEMM_THREADS, GEMM_SMEM, s>>>(g, t, K, status);
 }
 
 static void lu_diag_panel(Ctx* c, cudaStream_t s, const BandGeom& g, void* tiles, int K,
@@ -884,7 +891,7 @@ static int lu_i8_steps(const BandGeom& g, int num_sms) {
   return tiles >= per_sm * num_sms ? 4 : 2;
 }
 
-// The symmetric schedule rides on the INT8 pair / quad schedule (its DMMA kinds 0, 2, 60+m
+// The symmetric schedule rides on the pair / quad schedules (the DMMA kinds 0, 2, 3, 4, 60+m
 // and the INT8 kinds 3, 4 know g.sym); LRS_LU_SYM=0 switches it off.
 bool lu_sym_wanted(const BandGeom& g) {
   const char* e = std::getenv("LRS_LU_SYM");
@@ -930,10 +937,11 @@ int launch_band_lu(Ctx* c, const BandGeom& g0, double* tiles, int Tmax, int* sta
     }
     L.i8 = pn;
     L.steps = steps;
-    if (sym && lu_sym_wanted(g)) {
-      g.sym = 1;
-      if (sym_used) *sym_used = true;
-    }
+  }
+  // the symmetric schedule needs the pair / quad form (INT8, or the DMMA two-step kinds 3 / 4)
+  if (sym && lu_sym_wanted(g) && (L.i8 || lu_uses_pairs(g, L))) {
+    g.sym = 1;
+    if (sym_used) *sym_used = true;
   }
   run_band_lu(c, g, tiles, Tmax, status, L);
   return L.i8 != nullptr ? L.steps : 0;

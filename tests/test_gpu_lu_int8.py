@@ -100,11 +100,17 @@ def test_symmetric_schedule_matches_full_lu(ctx, name, scale, quad):
     assert Fs.info["lu_sym"] == 1 and Ff.info["lu_sym"] == 0 and Fd.info["lu_sym"] == 0
     assert Fs.info["lu_int8"] == 1 and not Fs.info["pivoted"]
     assert Fs.info["lu_pairs"] == (4 if quad else 2)
+    # the DMMA two-step kinds take the symmetric schedule too (real blocks; LRS_LU_I8=0)
+    Fds = _factor(ctx, cfg.system(0), cfg, False, sym=True) if name == "c3" else None
+    if Fds is not None:
+        assert Fds.info["lu_sym"] == 1 and Fds.info["lu_int8"] == 0
     for i in range(cfg.P):
         a, b, d = Fs.tiles(i), Ff.tiles(i), Fd.tiles(i)
         sc = np.max(np.abs(d))
         assert np.max(np.abs(a - b)) / sc <= 1e-12, i
         assert np.max(np.abs(a - d)) / sc <= 1e-12, i
+        if Fds is not None:
+            assert np.max(np.abs(Fds.tiles(i) - d)) / sc <= 1e-12, i
 
 
 def test_symmetric_schedule_only_for_symmetric_blocks(ctx):
