@@ -118,7 +118,11 @@ constexpr int I8_EPC = LRS_I8_EPC;                    // columns per epilogue wa
 constexpr int I8_EPI = 4 * I8_TN / I8_EPC;            // epilogue warps
 constexpr int I8_THREADS = 32 * (2 + I8_EPI);         // producer, MMA, epilogue warps
 #ifndef LRS_I8_TPC
-#define LRS_I8_TPC 8  // c2 LU median 0.1535 s vs 0.1596 s (4 tiles), 0.161 s (16)
+// Round 1 (pairs): 8 tiles, c2 LU median 0.1535 s vs 0.1596 s (4 tiles), 0.161 s (16).  With
+// quads a tile takes twice as long, and c2's critical stream waits on the bulk CTAs to retire:
+// session 5 (profiles/r02_lu_tpc_sweep.txt) c2 0.166 s and unsteady (8), 0.159 (4), 0.152-0.159
+// (2), 0.158 (1), 0.170 (16); c3 0.6835 (8), 0.6826 (4), 0.694 (2); c4 at 0.25 0.259 (any)
+#define LRS_I8_TPC 8  // launches of >= 200 tiles per SM; smaller ones take 4 (i8_gemm_launch)
 #endif
 constexpr int I8_TPC = LRS_I8_TPC;                    // tiles per CTA (bulk)
 #ifndef LRS_I8_TPC3
@@ -1350,7 +1354,13 @@ static void i8_gemm_launch(Ctx* c, cudaStream_t s, const BandGeom& g, double* ti
   // the look-ahead launch (kind 3, on the critical stream) takes fewer tiles per CTA
   static const int tpc3 = std::getenv("LRS_I8_TPC3") ? std::atoi(std::getenv("LRS_I8_TPC3"))
                                                       : LRS_I8_TPC3;
-  const int tpc = KIND == 4 ? I8_TPC : std::max(1, tpc3);
+  // bulk: LRS_I8_TPC tiles per CTA (environment LRS_I8_TPC_RT overrides it at run time)
+  // Small bulk launches (c2: 42 tiles per SM) run under a critical stream that waits for bulk
+  // CTAs to retire: they take 4 tiles per CTA, large ones (c3: ~1000 per SM) LRS_I8_TPC = 8.
+  static const int tpc_env = std::getenv("LRS_I8_TPC_RT") ? std::atoi(std::getenv("LRS_I8_TPC_RT"))
+                                                           : 0;
+  const int tpc4 = tpc_env > 0 ? tpc_env : (total < 200 * c->num_sms ? std::min(4, I8_TPC) : I8_TPC);
+  const int tpc = KIND == 4 ? std::max(1, tpc4) : std::max(1, tpc3);
   const int grid = (total + tpc - 1) / tpc;
   lu_i8_gemm_kernel<KIND, STEPS, CPLX><<<grid, I8_THREADS, I8_SMEM, s>>>(g, tiles, K, pn, total,
                                                                          tpc);
