@@ -126,7 +126,10 @@ constexpr int I8_THREADS = 32 * (2 + I8_EPI);         // producer, MMA, epilogue
 #endif
 constexpr int I8_TPC = LRS_I8_TPC;                    // tiles per CTA (bulk)
 #ifndef LRS_I8_TPC3
-#define LRS_I8_TPC3 8  // c2 LU medians: 1 tile 0.156 s, 2: 0.155, 4: 0.155, 8: 0.154 (noise level)
+// round 1 (pairs), c2 LU medians: 1 tile 0.156 s, 2: 0.155, 4: 0.155, 8: 0.154 (noise level);
+// session 5 (quads), c2: 8 tiles 0.159-0.174 s from run to run, 4: 0.158-0.171, 2: 0.159
+// steady, 1: 0.160; c3: 0.6836 (8) / 0.6847 (2)
+#define LRS_I8_TPC3 2
 #endif
 // LRS_I8_LDPIPE=1: the epilogue's TMEM loads are software pipelined against the INT32 -> FP64
 // conversion (two 32-column register buffers); 0: load, wait, convert per batch
