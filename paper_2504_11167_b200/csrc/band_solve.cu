@@ -44,6 +44,9 @@
 
 namespace lrs {
 
+#ifndef LRS_SOLVE_FMA_ACC
+#define LRS_SOLVE_FMA_ACC 4  // partial sums per chunk of the one-RHS FMA sweeps (1: a single chain)
+#endif
 constexpr int SOLVE_THREADS = 256;
 constexpr int CH_COLS = 32;
 constexpr int CLD = NB;                  // column stride of a chunk in shared memory
@@ -398,6 +401,32 @@ __device__ __forceinline__ void band_solve_body(BandGeom g, const double* __rest
       acc1 += (b0 + b1) + (b2 + b3);
     } else if (!TRANS && !MMA) {
       // out[row] (+|-)= sum_c Tile[row][c] xs[c], half the chunk columns per thread
+#if LRS_SOLVE_FMA_ACC > 1
+      // NA partial sums per chunk: a single 16-step dependent FMA chain per chunk held the
+      // sweep ~5% under the HBM rate (and more under a power cap: the chain scales with the
+      // SM clock).  Fixed order: column cc goes to partial cc mod NA, the partials are summed
+      // as a balanced tree and added to the running sum once per chunk.
+      constexpr int NA = LRS_SOLVE_FMA_ACC;
+      static_assert(NA == 2 || NA == 4 || NA == 8 || NA == 16, "partial sums per chunk");
+      double b[NA];
+#pragma unroll
+      for (int e = 0; e < NA; ++e) b[e] = 0.0;
+#pragma unroll
+      for (int c4 = 0; c4 < 16; c4 += NA)
+#pragma unroll
+        for (int e = 0; e < NA; ++e) {
+          const int cc = hh * 16 + c4 + e, c = cbase + cc;
+          double v = ch[cc * CLD + row];
+          if (diag) v = (MODE == 0) ? (row > c ? v : 0.0) : (row <= c ? v : 0.0);
+          else v = -v;
+          b[e] = fma(v, xs[c], b[e]);
+        }
+#pragma unroll
+      for (int w2 = NA / 2; w2 >= 1; w2 >>= 1)
+#pragma unroll
+        for (int e = 0; e < w2; ++e) b[e] += b[e + w2];
+      acc1 += b[0];
+#else
 #pragma unroll 4
       for (int cc = hh * 16; cc < hh * 16 + 16; ++cc) {
         const int c = cbase + cc;
@@ -406,6 +435,7 @@ __device__ __forceinline__ void band_solve_body(BandGeom g, const double* __rest
         else v = -v;
         acc1 = fma(v, xs[c], acc1);
       }
+#endif
     } else if (!TRANS) {
       // (128 x 32) x (32 x NR) on DMMA: A = chunk (row-major view ch[k*CLD + m]), B = xs rows
 #pragma unroll
